@@ -1,0 +1,371 @@
+#!/usr/bin/env python
+"""Benchmark of the RTG-SLAM mapping hot path on B200 (contract: DESIGN.md §7).
+
+One STEP = one pass of every §8(a) row over one synthetic C3 (Replica-shaped, 1200x680, 1M Gaussians,
+10 % unstable) frame:
+    ingest     A1 project -> A2 bin (all tiles) -> A3/A4 FULL render -> A7 classify + sample
+    iteration  A1 project -> A0 coverage + tile keep -> A2 bin (kept tiles) -> A3/A4 MASKED render
+               -> A5 masked backward -> [N>1: NCCL all-reduce of the slot gradients] -> A6 Adam
+`value` counts one mapping iteration per step (each step also carries a full frame ingest, so it is
+conservative w.r.t. the paper's 'mapping / iteration').
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "mapping iters/sec (fwd+masked bwd) and Gaussian-pixel blends/s vs roofline"
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), float(d.get("sm_max_mhz", 1965.0)), "measured"
+    return 6650.0, 1965.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 100 ms during the timed region."""
+
+    def __init__(self, idx: int):
+        self.idx = idx
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+                self.lines = [l for l in out.splitlines() if l.strip()]
+            except Exception:
+                pass
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            parts = [p.strip() for p in l.split(",")]
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except (ValueError, IndexError):
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons), "samples": len(sm)}
+
+
+_SCENES = {}
+
+
+def _scene(cfg_name):
+    from synth import CONFIGS, make_frame, make_pose, make_scene
+    if cfg_name not in _SCENES:
+        cfg = CONFIGS[cfg_name]
+        scene = make_scene(cfg)
+        R, t = make_pose(cfg)
+        _SCENES[cfg_name] = (cfg, scene, R, t, make_frame(cfg))
+    return _SCENES[cfg_name]
+
+
+def cpu_baseline(cfg_name: str, n_pixels: int = 48, seed: int = 0):
+    """The oracle (float64 CPU, as it stands) on a bounded sample of the same workload: projection of
+    ALL Gaussians + render and autograd backward of `n_pixels` active pixels; extrapolated linearly in
+    the active-pixel count to one full mapping iteration."""
+    import torch
+    from oracle import projection as OP, raster as OR
+    cfg, scene, R, t, (col, dep) = _scene(cfg_name)
+    cam = OP.camera(cfg)
+    threads = torch.get_num_threads()
+    t0 = time.perf_counter()
+    prm = OP.params_from_scene(scene, requires_grad=True)
+    proj = OP.project(prm, R, t, cam, scene["sh_degree"])
+    t_proj = time.perf_counter() - t0
+    # active pixels of the slab: sample among pixels covered by unstable Gaussians (right border)
+    rng = np.random.default_rng(seed)
+    u = scene["u_img"][(scene["flags"] & 2) == 0]
+    x_lo = int(np.percentile(u, 5))
+    px = rng.integers(max(x_lo, 0), cfg.width, n_pixels)
+    py = rng.integers(0, cfg.height, n_pixels)
+    pix = np.stack([px, py], 1)
+    t1 = time.perf_counter()
+    out = OR.render_pixels(proj, pix, cam, R, chunk=4, want_margin=False)
+    Ct = torch.as_tensor(col[:, py, px].T.astype(np.float64))
+    L = (out["color"] - Ct).abs().sum() / (3.0 * n_pixels)
+    L.backward()
+    t_pix = time.perf_counter() - t1
+    # |P| of the C3 iteration ~ the slab share of the image (measured by the GPU arm and passed in)
+    return dict(t_proj=t_proj, t_pix=t_pix, n_pixels=n_pixels, threads=threads)
+
+
+def reference_arm(args, rank, world):
+    """--impl reference: the oracle timed on the host cores (rank 0 only), bounded sample per step."""
+    if rank != 0:
+        return
+    from synth import CONFIGS
+    cfg = CONFIGS[args.config]
+    n_active = args.active_pixels or int(0.12 * cfg.width * cfg.height)
+    times = []
+    for s in range(args.warmup + args.steps):
+        r = cpu_baseline(args.config, n_pixels=args.ref_pixels, seed=s)
+        t_iter = r["t_proj"] + r["t_pix"] * n_active / r["n_pixels"]
+        if s >= args.warmup:
+            times.append(t_iter)
+    t = statistics.mean(times)
+    v = 1.0 / t
+    line = {"metric": METRIC, "value": v, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * t, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config} Replica-shaped 1200x680, 1M Gaussians, 10% unstable, full mapping "
+                                   "iteration (oracle sample extrapolated)", "l2": "n/a (CPU)"},
+            "impl": "reference",
+            "cpu_baseline": {"value": v, "unit": "iters/s", "cores": r["threads"], "kind": "oracle",
+                             "sample": f"projection of all {cfg.n} Gaussians + render/backward of {args.ref_pixels} "
+                                       f"active pixels, extrapolated to {n_active} active pixels"},
+            "e2e": {"value": v, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-pixels", type=int, default=24)
+    ap.add_argument("--active-pixels", type=int, default=0)
+    ap.add_argument("--phases", action="store_true", help="print per-call timings to stderr")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        reference_arm(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_2404_19706_b200 as P
+    from paper_2404_19706_b200 import build as B
+    from paper_2404_19706_b200.dist import allreduce_grads
+    from synth import CONFIGS, make_frame, make_pose, make_scene
+    if rank == 0:
+        B.build()
+    if world > 1:
+        dist.barrier()
+    cfg = CONFIGS[args.config]
+    scene = make_scene(cfg)
+    # each rank optimises the shared map from its own keyframe view (rank 0 = the primary view)
+    R, t = make_pose(cfg) if rank == 0 else make_pose(cfg, view=rank)
+    col_h, dep_h = make_frame(cfg, (R, t))
+    gm = P.GaussianMap.from_arrays(scene)
+    cam = P.camera_of(cfg)
+    pose = P.make_pose(R, t)
+    eng = P.MappingEngine(gm, cam, capacity=4 * cfg.n)
+    col = torch.as_tensor(col_h, device="cuda")
+    dep = torch.as_tensor(dep_h, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def step(c, d, frame_idx):
+        eng.ingest(c, d, pose, seed=1234, frame_idx=frame_idx)
+        eng.forward_masked(pose)
+        eng.backward(c, d, pose)
+        if world > 1:
+            allreduce_grads(eng.grad)
+        eng.optimizer_step()
+
+    for i in range(args.warmup):
+        step(col, dep, i)
+    torch.cuda.synchronize()
+    n_inst = int(eng.bins.n_instances.item())
+    if n_inst > eng.capacity:
+        raise RuntimeError(f"instance capacity {eng.capacity} < {n_inst}")
+
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+
+    # ---- device-timed region: K steps, L2 flushed between steps (outside the events) -------------
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    l0 = P.launch_count()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()
+            starts[i].record(stream)
+            step(col, dep, args.warmup + i)
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+    launches = (P.launch_count() - l0)
+    ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    t_step = sum(ms) / len(ms)
+    if world > 1:
+        tt = torch.tensor([t_step], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_step = float(tt.item())
+        dist.barrier()
+
+    # ---- per-call phase timing (one instrumented step, same stream) ------------------------------
+    phases = {}
+    if rank == 0:
+        ev = {}
+
+        def mark(name):
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(stream)
+            ev.setdefault(name, []).append(e)
+
+        flush.zero_()
+        mark("start")
+        P.project_gaussians(gm, pose, cam, eng.proj); mark("ingest.project")
+        P.bin_and_sort(eng.proj, gm.n, cam, None, eng.bins, eng.ws_bin); mark("ingest.bin_and_sort")
+        P.render_color_depth(gm, eng.proj, eng.bins, pose, cam, P.RTGS_RENDER_FULL, eng.full); mark("ingest.render_full")
+        P.classify_and_add_pixels(eng.full, col, dep, gm.flags, cam, P.add_params(seed=1234), eng.pixel_class,
+                                  eng.samples, eng.add_counts, eng.ws_cls); mark("ingest.classify")
+        P.project_gaussians(gm, pose, cam, eng.proj); mark("iter.project")
+        P.render_color_depth(gm, eng.proj, None, pose, cam, P.RTGS_RENDER_COVERAGE, eng.out); mark("iter.coverage")
+        P.bin_and_sort(eng.proj, gm.n, cam, eng.out.tile_keep, eng.bins, eng.ws_bin); mark("iter.bin_and_sort")
+        P.render_color_depth(gm, eng.proj, eng.bins, pose, cam, P.RTGS_RENDER_MASKED, eng.out); mark("iter.render_masked")
+        eng.backward(col, dep, pose); mark("iter.backward")
+        eng.optimizer_step(); mark("iter.adam")
+        torch.cuda.synchronize()
+        names = list(ev)
+        for a, b in zip(names[:-1], names[1:]):
+            phases[b] = ev[a][0].elapsed_time(ev[b][0])
+        # project kernel alone, averaged over several launches (HBM roofline of A1)
+        reps = 10
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        pt = []
+        for _ in range(reps):
+            flush.zero_()
+            e0.record(stream)
+            P.project_gaussians(gm, pose, cam, eng.proj)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            pt.append(e0.elapsed_time(e1))
+        phases["project_alone_ms"] = statistics.mean(pt)
+        counts_full = None
+        counts = eng.out.counts.cpu().numpy().tolist()
+        ninst_iter = int(eng.bins.n_instances.item())
+        if args.phases:
+            print(json.dumps({"phases_ms": phases, "counts": counts, "n_inst_iter": ninst_iter,
+                              "n_inst_full": n_inst}), file=sys.stderr)
+        _ = counts_full
+
+    # ---- e2e: host frame in pinned memory -> device, step, loss + counts back ----------------------
+    col_pin = torch.as_tensor(col_h).pin_memory()
+    dep_pin = torch.as_tensor(dep_h).pin_memory()
+    loss_h = torch.empty(4, dtype=torch.float32).pin_memory()
+    cnt_h = torch.empty(5, dtype=torch.int32).pin_memory()
+    col_d = torch.empty_like(col)
+    dep_d = torch.empty_like(dep)
+    e2e = []
+    for i in range(max(3, args.steps // 2)):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        col_d.copy_(col_pin, non_blocking=True)
+        dep_d.copy_(dep_pin, non_blocking=True)
+        step(col_d, dep_d, 1000 + i)
+        loss_h.copy_(eng.loss, non_blocking=True)
+        cnt_h.copy_(eng.add_counts, non_blocking=True)
+        b.record(stream)
+        torch.cuda.synchronize()
+        e2e.append(a.elapsed_time(b))
+    t_e2e = statistics.mean(e2e)
+    if world > 1:
+        tt = torch.tensor([t_e2e], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_e2e = float(tt.item())
+
+    if rank == 0:
+        hbm, sm_max, peak_kind = _peaks()
+        K = (cfg.sh_degree + 1) ** 2
+        # A1 algorithmic bytes per visible Gaussian: read pos 12, log_scale 12, rot 16, opacity 4, SH 12K,
+        # write rec 64, zkey 4, rect 8, tiles_touched 4
+        bytes_per_g = 12 + 12 + 16 + 4 + 12 * K + 64 + 4 + 8 + 4
+        t_proj_s = phases["project_alone_ms"] * 1e-3
+        achieved = bytes_per_g * cfg.n / t_proj_s / 1e9
+        clocks = clk.summary()
+        value = world * 1e3 / t_step
+        line = {
+            "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{cfg.name} Replica-shaped {cfg.width}x{cfg.height}, {cfg.n} Gaussians "
+                                   f"(10% transparent), {int(cfg.frac_unstable * 100)}% unstable slab, SH deg "
+                                   f"{cfg.sh_degree}; step = frame ingest (A1,A2,A3/A4 FULL,A7) + one masked "
+                                   "mapping iteration (A1,A0,A2,A3/A4,A5,A6)",
+                       "l2": "flushed between timed steps (256 MB write); Gaussian SoA 237 MB > L2",
+                       "parallelism": f"dp{world} over keyframe views" if world > 1 else "single GPU"},
+            "roofline": {"kernel": "k_project (A1)", "bound": "hbm", "achieved": achieved, "peak": hbm,
+                         "unit": "GB/s", "frac": achieved / hbm, "traffic": None, "peak_kind": peak_kind,
+                         "bytes_per_gaussian": bytes_per_g},
+            "clocks": clocks,
+            "gpu_launches": int(launches),
+            "e2e": {"value": world * 1e3 / t_e2e, "unit": "iters/s",
+                    "h2d_bytes_per_step": int(col_h.nbytes + dep_h.nbytes), "d2h_bytes_per_step": 4 * 4 + 5 * 4},
+            "phases_ms": {k: round(v, 4) for k, v in phases.items()},
+            "iter_ms": round(sum(v for k, v in phases.items() if k.startswith("iter.")), 4),
+            "ingest_ms": round(sum(v for k, v in phases.items() if k.startswith("ingest.")), 4),
+            "active": {"kept_tiles": counts[0], "active_px": counts[1], "instances_full": n_inst,
+                       "instances_iter": ninst_iter},
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                r = cpu_baseline(args.config, n_pixels=args.ref_pixels)
+                t_cpu = r["t_proj"] + r["t_pix"] * max(counts[1], 1) / r["n_pixels"]
+                line["cpu_baseline"] = {"value": 1.0 / t_cpu, "unit": "iters/s", "cores": r["threads"], "kind": "oracle",
+                                        "sample": f"projection of all {cfg.n} Gaussians + render/backward of "
+                                                  f"{r['n_pixels']} active pixels (float64 torch CPU), extrapolated to "
+                                                  f"|P| = {counts[1]} active pixels"}
+            except Exception as e:  # report, never fake
+                line["cpu_baseline"] = {"value": None, "error": repr(e)[:200]}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

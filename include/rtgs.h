@@ -1,0 +1,250 @@
+/*
+ * rtgs.h — C ABI of librtgs.so, the B200 (sm_100a) mapping hot path of RTG-SLAM
+ * (Peng et al., arXiv 2404.19706).  "P:n" = line n of the paper text; "Rn" = reading n of
+ * DESIGN.md §3 (where the paper is silent or garbled); "Eq.k" numbered in order of appearance.
+ *
+ * Conventions shared by every call
+ *  - All buffer pointers are DEVICE pointers owned by the caller unless stated otherwise; the
+ *    library never allocates device memory and never frees caller memory.  Scratch space is passed
+ *    as (workspace, workspace_bytes); query the size with the matching *_workspace_size call.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).  Every call only
+ *    ENQUEUES work on `stream` and returns; nothing synchronises, nothing reads results back, so an
+ *    iteration can be captured into a CUDA graph.
+ *  - Arguments are validated on the host before any launch.  Errors are returned as rtgs_status;
+ *    nothing aborts or throws across the ABI.  On error no work has been enqueued (INVALID_ARG,
+ *    WORKSPACE) or the CUDA launch failed (ERR_CUDA; see rtgs_last_cuda_error()).
+ *  - Images are planar float32, row-major: color [3][H][W], single channel [H][W].  Pixel (px, py)
+ *    has its centre at (px, py) (R1).  Tiles are 16 x 16 pixels, tile id = ty * TX + tx with
+ *    TX = ceil(W/16), TY = ceil(H/16).  Pixel bit masks hold bit (py*W+px) in word (py*W+px)/32.
+ *  - Pointers to float/int arrays must be 4-byte aligned, and `rec`, `pos`, `sh` 16-byte aligned.
+ *  - Gaussian ids (gid) are indices into the flat Gaussian arrays, 0 <= gid < n < 2^31.
+ */
+#ifndef RTGS_H
+#define RTGS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  RTGS_OK = 0,
+  RTGS_ERR_INVALID_ARG = 1, /* null / mis-sized / misaligned argument, bad mode, non-finite pose  */
+  RTGS_ERR_CAPACITY = 2,    /* reserved: instance overflow is reported through n_instances        */
+  RTGS_ERR_CUDA = 3,        /* a kernel launch failed; see rtgs_last_cuda_error()                 */
+  RTGS_ERR_WORKSPACE = 4    /* workspace pointer null or smaller than the *_workspace_size query  */
+} rtgs_status;
+
+/* Intrinsics K.  fx, fy > 0; 1 <= width, height <= 16384. */
+typedef struct {
+  float fx, fy, cx, cy;
+  int32_t width, height;
+} rtgs_camera;
+
+/* Camera->world pose T_g = [R t; 0 1] in SE(3), row-major R, HOST memory, float64 so the
+ * camera-frame position p_c = R^T (p - t) is formed without float32 cancellation. */
+typedef struct {
+  double R[9];
+  double t[3];
+} rtgs_pose;
+
+/* The Gaussian map, structure of arrays, float32, read-only for rendering.
+ *   pos       [n][3]  position p
+ *   log_scale [n][3]  s = exp(log_scale) (R3)
+ *   rot       [n][4]  quaternion (w, x, y, z), normalised inside the forward pass (R3)
+ *   opacity   [n]     alpha: 0.99 opaque / 0.1 transparent; never optimised (lr_alpha = 0)
+ *   sh        [n][K][3], K = (sh_degree+1)^2, coefficient-major, channel-minor (R2)
+ *   flags     [n]     bit0 = transparent, bit1 = stable (eta > delta_eta) */
+typedef struct {
+  const float *pos, *log_scale, *rot, *opacity, *sh;
+  const uint8_t *flags;
+  int32_t n;
+  int32_t sh_degree; /* 0..3 */
+} rtgs_gaussians;
+
+/* Mutable view of the optimised parameters (adam_step_unstable). Same layouts as rtgs_gaussians. */
+typedef struct {
+  float *pos, *log_scale, *rot, *sh;
+  int32_t n;
+  int32_t sh_degree;
+} rtgs_params;
+
+/* Per-Gaussian projection (O1, Eq.2).  Written by rtgs_project_gaussians.
+ *   rec [n][16] float32, 64 B per Gaussian:
+ *     [0] mu_x hi  [1] mu_y hi  [2] mu_x lo  [3] mu_y lo      mu = hi + lo (double-float)
+ *     [4] conic A  [5] conic B  [6] conic C  [7] alpha        Sigma2D^-1 = [[A,B],[B,C]]
+ *     [8] r  [9] g  [10] b                                    colour from SH at the view direction (R2)
+ *     [11] support half-extents (ex, ey) in pixels as two IEEE halves (low half = ex), rounded up
+ *     [12..14] n_c (unit disc normal, camera frame)  [15] n_c . p_c   (disc plane, Eq.4, R10, R12)
+ *   zkey [n]  float32 bits of the camera-frame centre depth z (R8); 0xFFFFFFFF when culled
+ *   rect [n][4] int16 pixel rect x0, y0, x1, y1 (inclusive, clipped to the image) of the support (R7);
+ *               empty (x0 > x1) when culled (z <= 0.2 m (R6), alpha <= 1/255, or off-image)
+ *   tiles_touched [n]  number of 16x16 tiles the rect covers (0 when culled) */
+typedef struct {
+  float* rec;
+  uint32_t* zkey;
+  int16_t* rect;
+  uint32_t* tiles_touched;
+} rtgs_projected;
+
+/* Tile bins (O8).  sorted_gid[capacity]: gids ordered by (tile, zkey bits, gid) (R8);
+ * tile_range [TX*TY][2]: [start, end) of every tile in sorted_gid (0,0 when empty);
+ * n_instances [1]: total instance count I (may exceed capacity: then the output is truncated,
+ * memory-safe but invalid, and the caller must re-run with capacity >= I). */
+typedef struct {
+  uint32_t* sorted_gid;
+  uint32_t* tile_range;
+  uint32_t* n_instances;
+  uint32_t capacity;
+} rtgs_bins;
+
+enum { RTGS_RENDER_FULL = 0, RTGS_RENDER_MASKED = 1, RTGS_RENDER_COVERAGE = 2 };
+
+/* Render buffers (O2-O4).  Which fields are read / written depends on the mode, see the call. */
+typedef struct {
+  float* color;          /* [3][H][W]  C^ (Eq.1), black background (R23)                         */
+  float* trans;          /* [H][W]     T^ (Eq.3)                                                  */
+  float* depth;          /* [H][W]     D^ (Eq.5); -1 where no opaque disc is hit                  */
+  float* normal;         /* [3][H][W]  N^ world frame, zero without hit; NULLABLE         */
+  int32_t* index;        /* [H][W]     I^: gid of the hit Gaussian or -1                  */
+  uint32_t* n_contrib;   /* [H][W]     sorted-list position just past the last blended entry      */
+  uint32_t* active_bits; /* [ceil(H*W/32)]  M_unstable (Eq.12) — COVERAGE output, MASKED input     */
+  uint8_t* tile_keep;    /* [TX*TY]    1 iff >= 50 % of the tile's pixels are active (R15) */
+  uint32_t* tile_list;   /* [TX*TY]    ids of kept tiles (order unspecified)                      */
+  uint32_t* counts;      /* [4] device: [0] #kept tiles, [1] |P| (active pixels in kept tiles),
+                                        [2] |M_unstable|, [3] reserved                             */
+} rtgs_render_out;
+
+/* Target RGBD frame C_k, D_k: color [3][H][W] in [0,1]; depth [H][W] metres, <= 0 or
+ * non-finite = invalid (R24). */
+typedef struct {
+  const float* color;
+  const float* depth;
+} rtgs_frame;
+
+/* Loss weights of Eq.8: w_c = 1, w_d = 1, w_reg = 1000. */
+typedef struct {
+  float w_c, w_d, w_reg;
+} rtgs_loss_weights;
+
+/* Per-group learning rates and Adam constants (R19: beta 0.9/0.999, eps 1e-15). */
+typedef struct {
+  float lr_pos, lr_sh0, lr_shrest, lr_scale, lr_rot;
+  float beta1, beta2, eps;
+} rtgs_hparams;
+
+/* Gaussian-adding thresholds: delta_T 0.5, delta_d 0.1, delta_c 0.1, ratio 0.05. */
+typedef struct {
+  float delta_T, delta_d, delta_c;
+  double sample_ratio; /* threshold round(ratio * 2^32) is formed in float64 */
+  uint64_t seed;
+  uint32_t frame_idx;
+} rtgs_add_params;
+
+/* ---------------------------------------------------------------------------------------------
+ * A1 — rtgs_project_gaussians (O1; Eq.2, R2-R8, R12)
+ * For every Gaussian: cull (z <= 0.2 m), EWA Sigma2D = (J V) Sigma (J V)^T + 0.3 I with the 1.3x-FOV
+ * Jacobian clamp, conic, mu, SH colour max(0, SH(d) + 0.5), disc normal (smallest axis) and its
+ * camera-frame plane, float32 depth key, support rect and tile count.  Writes every field of `out`
+ * for all n Gaussians.  1 thread per Gaussian, SH staged through shared memory by bulk copies.
+ * ------------------------------------------------------------------------------------------- */
+rtgs_status rtgs_project_gaussians(const rtgs_gaussians* g, const rtgs_pose* pose, const rtgs_camera* cam,
+                                   rtgs_projected* out, void* stream);
+
+/* ---------------------------------------------------------------------------------------------
+ * A2 — rtgs_bin_and_sort (O8, R7, R8, R15)
+ * Instances (tile, gid) for every tile of every Gaussian's tile rect — restricted to tiles with
+ * tile_keep[t] != 0 when tile_keep is non-NULL — ordered by (tile, zkey bits, gid).  Implementation:
+ * stable compaction of the Gaussians with >= 1 instance, LSD radix sort of their depth keys, emission
+ * in depth order, stable LSD radix sort of the instances by tile id.  Reads proj->zkey, proj->rect.
+ * `n_instances` receives I; if I > capacity the output is truncated (see rtgs_bins).
+ * ------------------------------------------------------------------------------------------- */
+size_t rtgs_bin_workspace_size(int32_t n, const rtgs_camera* cam, uint32_t capacity);
+rtgs_status rtgs_bin_and_sort(const rtgs_projected* proj, int32_t n, const rtgs_camera* cam,
+                              const uint8_t* tile_keep, rtgs_bins* out, void* workspace, size_t workspace_bytes,
+                              void* stream);
+
+/* ---------------------------------------------------------------------------------------------
+ * A0/A3/A4 — rtgs_render_color_depth (O2-O4; Eq.1-5, Eq.12, R7-R12, R15, R16)
+ *  mode FULL:     every pixel, every tile.  Writes color, trans, depth, index, n_contrib, normal (if
+ *                 non-NULL).  Needs proj, bins.
+ *  mode MASKED:   only the active pixels P = M_unstable ∩ kept tiles (out->active_bits, out->tile_keep,
+ *                 out->tile_list, out->counts[0] from a previous COVERAGE call); same outputs, other
+ *                 pixels untouched.  Needs proj, bins (binned with the same tile_keep or with all tiles).
+ *  mode COVERAGE: M_unstable(u) = [some unstable (flags bit1 clear), non-culled Gaussian has
+ *                 power >= -4.5 and f >= 1/255 at u] (exactly T^_unstable(u) < 1, R16), tile keep
+ *                 (>= 50 % of in-image pixels), kept-tile list, counts.  Writes active_bits, tile_keep,
+ *                 tile_list, counts; needs proj and g->flags only (bins may be NULL).
+ * Blending per pixel in (zkey, gid) order: skip if power < -4.5 or f = min(0.99, alpha e^power) < 1/255;
+ * the first f > e^-0.5 is the depth hit (tested before termination, R9); stop when T (1-f) < 1e-4.
+ * ------------------------------------------------------------------------------------------- */
+rtgs_status rtgs_render_color_depth(const rtgs_gaussians* g, const rtgs_projected* proj, const rtgs_bins* bins,
+                                    const rtgs_pose* pose, const rtgs_camera* cam, int32_t mode,
+                                    rtgs_render_out* out, void* stream);
+
+/* ---------------------------------------------------------------------------------------------
+ * A5 — rtgs_render_backward_masked (O5; Eq.7-8, R13, R14, R17)
+ * Masked L1 loss on P (colour: mean over 3|P| values; depth: mean over P_d = P ∩ {D^ != -1} ∩ {D > 0})
+ * and its gradient with respect to the parameters of the UNSTABLE Gaussians only (slot_of_gid[gid] >= 0).
+ * `fwd` must hold a MASKED (or FULL) render of the same proj/bins plus the COVERAGE fields.
+ *   slot_of_gid [n]       slot of each Gaussian, -1 for stable / not optimised
+ *   gid_of_slot [n_slots] inverse map
+ *   grad [n_slots][10+3K] ACCUMULATED (+=): pos 3, log_scale 3, rot 4, sh K*3 (DC first)
+ *   loss_out [4] device float, OVERWRITTEN: L_color, L_depth, w_c L_color + w_d L_depth, |P_d|
+ * No gradient flows through discrete choices (hit, 60 deg branch, termination, cut-offs, clamps; R17)
+ * nor to opacity (lr_alpha = 0).
+ * ------------------------------------------------------------------------------------------- */
+size_t rtgs_backward_workspace_size(int32_t n_slots);
+rtgs_status rtgs_render_backward_masked(const rtgs_gaussians* g, const rtgs_projected* proj, const rtgs_bins* bins,
+                                        const rtgs_pose* pose, const rtgs_camera* cam, const rtgs_render_out* fwd,
+                                        const rtgs_frame* target, const rtgs_loss_weights* w,
+                                        const int32_t* slot_of_gid, const int32_t* gid_of_slot, int32_t n_slots,
+                                        float* grad, float* loss_out, void* workspace, size_t workspace_bytes,
+                                        void* stream);
+
+/* ---------------------------------------------------------------------------------------------
+ * A6 — rtgs_adam_step_unstable (O6; Eq.8, R18-R20)
+ * For each slot s (gid = gid_of_slot[s]): for transparent slots add grad of w_reg L_reg,
+ * L_reg = mean over the 10 n_transparent geometry scalars of (theta - init_geom)^2; one Adam step
+ * (bias correction with `step` >= 1) with the group learning rates; eta[gid] += 1 iff any SH gradient
+ * component of the slot is non-zero; grad is consumed and ZEROED.
+ *   m, v [n_slots][10+3K] Adam moments; init_geom [n_slots][10] (pos 3, log_scale 3, rot 4) (D12)
+ * ------------------------------------------------------------------------------------------- */
+rtgs_status rtgs_adam_step_unstable(rtgs_params* params, const int32_t* gid_of_slot, int32_t n_slots,
+                                    const uint8_t* flags, float* grad, float* m, float* v, const float* init_geom,
+                                    int32_t n_transparent, float w_reg, const rtgs_hparams* hp, int32_t step,
+                                    uint32_t* eta, void* stream);
+
+/* ---------------------------------------------------------------------------------------------
+ * A7 — rtgs_classify_and_add_pixels (O7; Eq.6, R21, R22, R24)
+ * On a FULL render at the new frame's pose, in float32 with this exact operation order:
+ *   valid = isfinite(D) && D > 0
+ *   M_s   = valid && (T^ > delta_T || |D^ - D| > delta_d)
+ *   err   = ((|dR| + |dG|) + |dB|) / 3,  dX = C^_X - C_X
+ *   M_c   = valid && !M_s && err > delta_c
+ *   sampled(u) = (splitmix64(seed ^ (frame_idx << 32) ^ (py*W+px)) >> 32) < round(ratio * 2^32)
+ * pixel_class [H][W] = mask (0 none, 1 M_s, 2 M_c) | sampled << 2 | action << 3 with action
+ *   1 OPAQUE_NEW (sampled M_s), 2 TRANSPARENT_NEW (sampled M_c whose I^ Gaussian is stable),
+ *   3 SKIP (sampled M_c whose I^ Gaussian is unstable).
+ * samples [cap]: (py*W+px) | action << 30 for actions 1 and 2, in row-major order.
+ * counts [5] device: |M_s|, |M_c|, #OPAQUE_NEW, #TRANSPARENT_NEW, #SKIP (samples beyond cap dropped).
+ * ------------------------------------------------------------------------------------------- */
+size_t rtgs_classify_workspace_size(const rtgs_camera* cam);
+rtgs_status rtgs_classify_and_add_pixels(const rtgs_render_out* full, const rtgs_frame* frame, const uint8_t* flags,
+                                         const rtgs_camera* cam, const rtgs_add_params* ap, uint8_t* pixel_class,
+                                         uint32_t* samples, uint32_t cap, uint32_t* counts, void* workspace,
+                                         size_t workspace_bytes, void* stream);
+
+/* Utilities */
+const char* rtgs_status_string(rtgs_status s);
+const char* rtgs_last_cuda_error(void);
+int32_t rtgs_version(void);
+/* Number of kernel launches the library has enqueued since load (for bench accounting). */
+uint64_t rtgs_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RTGS_H */

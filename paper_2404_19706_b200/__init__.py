@@ -1,0 +1,12 @@
+"""B200-native (sm_100a) mapping hot path of RTG-SLAM (arXiv 2404.19706).
+
+The compute path is librtgs.so (CUDA kernels behind the C ABI in include/rtgs.h); this package is
+its thin Python binding (argument marshalling and torch-allocated device buffers).  There is no CPU
+fallback: importing the binding and calling it without the built library raises.
+"""
+from ._abi import LIB_PATH, RTGSError, lib  # noqa: F401
+from .mapping import (GaussianMap, MappingEngine, ProjectedBuffers, BinBuffers, RenderBuffers,  # noqa: F401
+                      project_gaussians, bin_and_sort, render_color_depth, render_backward_masked,
+                      adam_step_unstable, classify_and_add_pixels, make_camera, make_pose, camera_of,
+                      hparams, add_params, launch_count, RTGS_RENDER_FULL, RTGS_RENDER_MASKED,
+                      RTGS_RENDER_COVERAGE)

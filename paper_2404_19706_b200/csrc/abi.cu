@@ -1,0 +1,164 @@
+// abi.cu — the extern "C" boundary of librtgs.so (include/rtgs.h): host-side argument validation,
+// then the launchers of internal.h.  No CPU fallback exists: every call either enqueues the CUDA
+// kernels or returns an error status.
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace rtgs {
+static std::atomic<uint64_t> g_launches{0};
+void note_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+}  // namespace rtgs
+
+using namespace rtgs;
+
+namespace {
+thread_local char g_cuda_err[256] = "";
+
+inline bool a16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+inline bool a4(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 3u) == 0; }
+
+bool cam_ok(const rtgs_camera* c) {
+  return c && std::isfinite(c->fx) && std::isfinite(c->fy) && std::isfinite(c->cx) && std::isfinite(c->cy) &&
+         c->fx > 0.f && c->fy > 0.f && c->width >= 1 && c->height >= 1 && c->width <= 16384 && c->height <= 16384;
+}
+bool pose_ok(const rtgs_pose* p) {
+  if (!p) return false;
+  for (double v : p->R)
+    if (!std::isfinite(v)) return false;
+  for (double v : p->t)
+    if (!std::isfinite(v)) return false;
+  return true;
+}
+bool gauss_ok(const rtgs_gaussians* g, bool need_flags) {
+  if (!g || g->n < 0 || g->sh_degree < 0 || g->sh_degree > 3) return false;
+  if (g->n == 0) return true;
+  if (!g->pos || !g->log_scale || !g->rot || !g->opacity || !g->sh) return false;
+  if (need_flags && !g->flags) return false;
+  return a16(g->pos) && a4(g->log_scale) && a16(g->rot) && a4(g->opacity) && a16(g->sh);
+}
+bool proj_ok(const rtgs_projected* p, int n) {
+  if (!p) return false;
+  if (n == 0) return true;
+  return p->rec && p->zkey && p->rect && p->tiles_touched && a16(p->rec) && a4(p->zkey) &&
+         (reinterpret_cast<uintptr_t>(p->rect) & 7u) == 0 && a4(p->tiles_touched);
+}
+bool bins_ok(const rtgs_bins* b) {
+  return b && b->sorted_gid && b->tile_range && b->n_instances && (reinterpret_cast<uintptr_t>(b->tile_range) & 7u) == 0;
+}
+rtgs_status finish(cudaError_t e) {
+  if (e == cudaSuccess) return RTGS_OK;
+  std::snprintf(g_cuda_err, sizeof(g_cuda_err), "%s: %s", cudaGetErrorName(e), cudaGetErrorString(e));
+  return RTGS_ERR_CUDA;
+}
+inline cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+}  // namespace
+
+extern "C" {
+
+rtgs_status rtgs_project_gaussians(const rtgs_gaussians* g, const rtgs_pose* pose, const rtgs_camera* cam,
+                                   rtgs_projected* out, void* stream) {
+  if (!gauss_ok(g, false) || !pose_ok(pose) || !cam_ok(cam) || !proj_ok(out, g ? g->n : 0))
+    return RTGS_ERR_INVALID_ARG;
+  return finish(launch_project(*g, make_pose(*pose), *cam, *out, S(stream)));
+}
+
+size_t rtgs_bin_workspace_size(int32_t n, const rtgs_camera* cam, uint32_t capacity) {
+  if (n < 0 || !cam_ok(cam)) return 0;
+  return bin_workspace_size(n, *cam, capacity);
+}
+
+rtgs_status rtgs_bin_and_sort(const rtgs_projected* proj, int32_t n, const rtgs_camera* cam, const uint8_t* tile_keep,
+                              rtgs_bins* out, void* workspace, size_t workspace_bytes, void* stream) {
+  if (n < 0 || !cam_ok(cam) || !proj_ok(proj, n) || !bins_ok(out)) return RTGS_ERR_INVALID_ARG;
+  if (!workspace || workspace_bytes < bin_workspace_size(n, *cam, out->capacity)) return RTGS_ERR_WORKSPACE;
+  return finish(launch_bin(*proj, n, *cam, tile_keep, *out, workspace, S(stream)));
+}
+
+rtgs_status rtgs_render_color_depth(const rtgs_gaussians* g, const rtgs_projected* proj, const rtgs_bins* bins,
+                                    const rtgs_pose* pose, const rtgs_camera* cam, int32_t mode,
+                                    rtgs_render_out* out, void* stream) {
+  if (!cam_ok(cam) || !out || !pose_ok(pose)) return RTGS_ERR_INVALID_ARG;
+  if (mode == RTGS_RENDER_COVERAGE) {
+    if (!g || g->n < 0 || (g->n > 0 && !g->flags) || !proj_ok(proj, g->n)) return RTGS_ERR_INVALID_ARG;
+    if (!out->active_bits || !out->tile_keep || !out->tile_list || !out->counts) return RTGS_ERR_INVALID_ARG;
+    return finish(launch_coverage(*g, *proj, *cam, *out, S(stream)));
+  }
+  if (mode != RTGS_RENDER_FULL && mode != RTGS_RENDER_MASKED) return RTGS_ERR_INVALID_ARG;
+  if (!proj || !proj->rec || !proj->zkey || !a16(proj->rec) || !bins_ok(bins)) return RTGS_ERR_INVALID_ARG;
+  if (!out->color || !out->trans || !out->depth || !out->index || !out->n_contrib) return RTGS_ERR_INVALID_ARG;
+  if (mode == RTGS_RENDER_MASKED && (!out->active_bits || !out->tile_list || !out->counts))
+    return RTGS_ERR_INVALID_ARG;
+  return finish(launch_render(*proj, *bins, make_pose(*pose), *cam, mode == RTGS_RENDER_MASKED, *out, S(stream)));
+}
+
+size_t rtgs_backward_workspace_size(int32_t n_slots) { return n_slots < 0 ? 0 : backward_workspace_size(n_slots); }
+
+rtgs_status rtgs_render_backward_masked(const rtgs_gaussians* g, const rtgs_projected* proj, const rtgs_bins* bins,
+                                        const rtgs_pose* pose, const rtgs_camera* cam, const rtgs_render_out* fwd,
+                                        const rtgs_frame* target, const rtgs_loss_weights* w,
+                                        const int32_t* slot_of_gid, const int32_t* gid_of_slot, int32_t n_slots,
+                                        float* grad, float* loss_out, void* workspace, size_t workspace_bytes,
+                                        void* stream) {
+  if (!gauss_ok(g, false) || !proj_ok(proj, g ? g->n : 0) || !bins_ok(bins) || !pose_ok(pose) || !cam_ok(cam))
+    return RTGS_ERR_INVALID_ARG;
+  if (!fwd || !fwd->color || !fwd->depth || !fwd->index || !fwd->n_contrib || !fwd->active_bits ||
+      !fwd->tile_list || !fwd->counts)
+    return RTGS_ERR_INVALID_ARG;
+  if (!target || !target->color || !target->depth || !w || n_slots < 0 || !loss_out) return RTGS_ERR_INVALID_ARG;
+  if (g->n > 0 && !slot_of_gid) return RTGS_ERR_INVALID_ARG;
+  if (n_slots > 0 && (!gid_of_slot || !grad)) return RTGS_ERR_INVALID_ARG;
+  if (!workspace || workspace_bytes < backward_workspace_size(n_slots) || !a16(workspace)) return RTGS_ERR_WORKSPACE;
+  return finish(launch_backward(*g, *proj, *bins, make_pose(*pose), *cam, *fwd, *target, *w, slot_of_gid, gid_of_slot,
+                                n_slots, grad, loss_out, workspace, S(stream)));
+}
+
+rtgs_status rtgs_adam_step_unstable(rtgs_params* params, const int32_t* gid_of_slot, int32_t n_slots,
+                                    const uint8_t* flags, float* grad, float* m, float* v, const float* init_geom,
+                                    int32_t n_transparent, float w_reg, const rtgs_hparams* hp, int32_t step,
+                                    uint32_t* eta, void* stream) {
+  if (!params || !hp || n_slots < 0 || step < 1 || n_transparent < 0 || params->sh_degree < 0 ||
+      params->sh_degree > 3 || !std::isfinite(w_reg))
+    return RTGS_ERR_INVALID_ARG;
+  if (n_slots > 0 && (!params->pos || !params->log_scale || !params->rot || !params->sh || !gid_of_slot || !flags ||
+                      !grad || !m || !v || !eta || (n_transparent > 0 && !init_geom)))
+    return RTGS_ERR_INVALID_ARG;
+  return finish(launch_adam(*params, gid_of_slot, n_slots, flags, grad, m, v, init_geom, n_transparent, w_reg, *hp, step,
+                            eta, S(stream)));
+}
+
+size_t rtgs_classify_workspace_size(const rtgs_camera* cam) { return cam_ok(cam) ? classify_workspace_size(*cam) : 0; }
+
+rtgs_status rtgs_classify_and_add_pixels(const rtgs_render_out* full, const rtgs_frame* frame, const uint8_t* flags,
+                                         const rtgs_camera* cam, const rtgs_add_params* ap, uint8_t* pixel_class,
+                                         uint32_t* samples, uint32_t cap, uint32_t* counts, void* workspace,
+                                         size_t workspace_bytes, void* stream) {
+  if (!full || !full->color || !full->trans || !full->depth || !full->index || !frame || !frame->color ||
+      !frame->depth || !flags || !cam_ok(cam) || !ap || !pixel_class || !counts || (cap > 0 && !samples))
+    return RTGS_ERR_INVALID_ARG;
+  if (!(ap->sample_ratio >= 0.0) || !std::isfinite(ap->sample_ratio)) return RTGS_ERR_INVALID_ARG;
+  if (!workspace || workspace_bytes < classify_workspace_size(*cam)) return RTGS_ERR_WORKSPACE;
+  return finish(launch_classify(*full, *frame, flags, *cam, *ap, pixel_class, samples, cap, counts, workspace,
+                                S(stream)));
+}
+
+const char* rtgs_status_string(rtgs_status s) {
+  switch (s) {
+    case RTGS_OK: return "RTGS_OK";
+    case RTGS_ERR_INVALID_ARG: return "RTGS_ERR_INVALID_ARG";
+    case RTGS_ERR_CAPACITY: return "RTGS_ERR_CAPACITY";
+    case RTGS_ERR_CUDA: return "RTGS_ERR_CUDA";
+    case RTGS_ERR_WORKSPACE: return "RTGS_ERR_WORKSPACE";
+  }
+  return "RTGS_UNKNOWN";
+}
+
+const char* rtgs_last_cuda_error(void) { return g_cuda_err; }
+int32_t rtgs_version(void) { return 1; }
+uint64_t rtgs_launch_count(void) { return g_launches.load(); }
+
+}  // extern "C"

@@ -1,0 +1,516 @@
+// backward.cu — A5: masked L1 loss and its gradient for the unstable Gaussians
+// (O5; Eq.7-8, readings R13, R14, R17).
+//
+// K5 k_render_bwd: one CTA per kept tile (same geometry and batching as the forward).  Each active
+//   pixel REPLAYS the forward front to back with the identical arithmetic (eval_pair), so T_i and
+//   every decision are bit-identical to the forward; the colour suffix S_i = C^ - prefix_i comes from
+//   the stored C^.  For every UNSTABLE record a warp touches, the 8 screen-space gradients
+//   (mu 2, conic 3, rgb 3) are reduced over the warp with shuffles and added with one red.global
+//   per value.  Depth gradients go to the single hit Gaussian of each pixel (Eq.4-5).
+// K5b k_project_bwd: one thread per slot: chain rule from the screen-space gradients through
+//   EWA / SH / disc plane to (pos, log_scale, rot, sh) (hand-derived; checked against the
+//   oracle's autograd in tests/test_gpu_backward.py).
+#include "common.cuh"
+#include "internal.h"
+
+namespace rtgs {
+
+constexpr int kBatchB = 256;
+constexpr int kSG = 16;  // screen-space gradient floats per slot
+
+// workspace: sgrad [n_slots][16] | acc [4] floats: sum|dC|, sum|dD| over P_d, |P_d|, spare
+size_t backward_workspace_size(int n_slots) { return ((size_t)n_slots * kSG + 8) * sizeof(float) + 256; }
+
+struct BwdArgs {
+  const float4* rec;
+  const uint32_t* zkey;
+  const uint32_t* sorted_gid;
+  const uint2* range;
+  const uint32_t* tile_list;
+  const uint32_t* counts;
+  const uint32_t* active;
+  const float* color;
+  const float* depth;
+  const int32_t* index;
+  const uint32_t* n_contrib;
+  const float* tcolor;
+  const float* tdepth;
+  const int32_t* slot_of_gid;
+  CamK cam;
+  float w_c;
+  float* sgrad;
+  float* acc;
+};
+
+__global__ void __launch_bounds__(256) k_render_bwd(const BwdArgs a) {
+  __shared__ __align__(16) float4 s_rec[2][kBatchB][3];
+  __shared__ int32_t s_slot[2][kBatchB];
+  __shared__ float s_red[3][8];
+  if (blockIdx.x >= a.counts[0]) return;
+  const int tile = (int)a.tile_list[blockIdx.x];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int tx = tile % a.cam.TX, ty = tile / a.cam.TX;
+  const int wx0 = tx * kTile + (w & 1) * 8, wy0 = ty * kTile + (w >> 1) * 4;
+  const int px = wx0 + (lane & 7), py = wy0 + (lane >> 3);
+  const bool inside = px < a.cam.W && py < a.cam.H;
+  const uint32_t lin = (uint32_t)py * (uint32_t)a.cam.W + (uint32_t)px;
+  const bool want = inside && ((a.active[lin >> 5] >> (lin & 31u)) & 1u);
+  const size_t HW = (size_t)a.cam.W * a.cam.H;
+  const float fpx = (float)px, fpy = (float)py;
+
+  // per-pixel loss terms (R13, R14, R24)
+  float gCr = 0.f, gCg = 0.f, gCb = 0.f, Cr = 0.f, Cg = 0.f, Cb = 0.f;
+  uint32_t last = 0;
+  float l1c = 0.f, l1d = 0.f, nd = 0.f;
+  const float invP = a.w_c / (3.f * (float)max(1u, a.counts[1]));
+  if (want) {
+    Cr = a.color[lin]; Cg = a.color[HW + lin]; Cb = a.color[2 * HW + lin];
+    const float dr = Cr - a.tcolor[lin], dg = Cg - a.tcolor[HW + lin], db = Cb - a.tcolor[2 * HW + lin];
+    l1c = fabsf(dr) + fabsf(dg) + fabsf(db);
+    gCr = dr > 0.f ? invP : (dr < 0.f ? -invP : 0.f);
+    gCg = dg > 0.f ? invP : (dg < 0.f ? -invP : 0.f);
+    gCb = db > 0.f ? invP : (db < 0.f ? -invP : 0.f);
+    last = a.n_contrib[lin];
+    const int hit = a.index[lin];
+    const float Dt = a.tdepth[lin];
+    if (hit >= 0 && isfinite(Dt) && Dt > 0.f) {
+      const float Dh = a.depth[lin];
+      const float dd = Dh - Dt;
+      l1d = fabsf(dd);
+      nd = 1.f;
+      const float gD = dd > 0.f ? 1.f : (dd < 0.f ? -1.f : 0.f);  // scaled by w_d / |P_d| in K5b
+      const int slot = a.slot_of_gid[hit];
+      if (slot >= 0 && gD != 0.f) {
+        const float4 pl = a.rec[(size_t)4 * hit + 3];
+        const float rx = (fpx - a.cam.cx) / a.cam.fx, ry = (fpy - a.cam.cy) / a.cam.fy;
+        const float ndr = pl.x * rx + pl.y * ry + pl.z;
+        const float nn = sqrtf(pl.x * pl.x + pl.y * pl.y + pl.z * pl.z);
+        const float cosang = fabsf(ndr) / (sqrtf(rx * rx + ry * ry + 1.f) * nn);
+        float* sg = a.sgrad + (size_t)slot * kSG;
+        if (cosang > kCos60) {
+          // D = (n.p)/(n.r): dD/dp_c = n/(n.r), dD/dn_c = (p_c - D r)/(n.r)
+          const float q = gD / ndr;
+          atomicAdd(sg + 8, q);
+          atomicAdd(sg + 9, q * Dh * rx);
+          atomicAdd(sg + 10, q * Dh * ry);
+          atomicAdd(sg + 11, q * Dh);
+        } else {
+          atomicAdd(sg + 12, gD);  // D = z: dD/dp_c = e_z
+        }
+      }
+    }
+  }
+  // loss accumulation (block reduce, 3 atomics per CTA)
+  {
+    const float s0 = warp_sum(l1c), s1 = warp_sum(l1d), s2 = warp_sum(nd);
+    if (lane == 0) { s_red[0][w] = s0; s_red[1][w] = s1; s_red[2][w] = s2; }
+    __syncthreads();
+    if (tid < 3) {
+      float t = 0.f;
+      for (int k = 0; k < 8; ++k) t += s_red[tid][k];
+      atomicAdd(a.acc + tid, t);
+    }
+  }
+
+  bool done = !want;
+  const float bx0 = (float)wx0, bx1 = (float)(wx0 + 7), by0 = (float)wy0, by1 = (float)(wy0 + 3);
+  const uint2 rg = a.range[tile];
+  const int start = (int)rg.x;
+  int end = (int)rg.y;
+  // nothing past the largest last-blended position of the CTA can contribute
+  {
+    __shared__ uint32_t s_last;
+    if (tid == 0) s_last = 0;
+    __syncthreads();
+    if (want) atomicMax(&s_last, last);
+    __syncthreads();
+    end = min(end, (int)s_last);
+  }
+  const int nb = end > start ? (end - start + kBatchB - 1) / kBatchB : 0;
+  float T = 1.f, ar = 0.f, ag = 0.f, ab = 0.f;
+
+  auto load = [&](int b, int buf) {
+    const int i = start + b * kBatchB + tid;
+    if (i < end) {
+      const uint32_t g = a.sorted_gid[i];
+      s_slot[buf][tid] = a.slot_of_gid[g];
+      const float4* src = a.rec + (size_t)4 * g;
+      cp_async16(&s_rec[buf][tid][0], src);
+      cp_async16(&s_rec[buf][tid][1], src + 1);
+      cp_async16(&s_rec[buf][tid][2], src + 2);
+    }
+    cp_async_commit();
+  };
+
+  if (nb > 0) load(0, 0);
+  for (int b = 0; b < nb; ++b) {
+    const int buf = b & 1;
+    if (b + 1 < nb) load(b + 1, buf ^ 1); else cp_async_commit();
+    cp_async_wait<1>();
+    if (__syncthreads_count(!done) == 0) break;
+    const int cnt = min(kBatchB, end - (start + b * kBatchB));
+    bool wdone = __all_sync(0xffffffffu, done);
+    for (int g0 = 0; g0 < cnt && !wdone; g0 += 32) {
+      const int j = g0 + lane;
+      bool ov = false;
+      if (j < cnt) {
+        const float4 r0 = s_rec[buf][j][0];
+        const float2 ext = unpack_ext(s_rec[buf][j][2].w);
+        ov = (r0.x + ext.x >= bx0) && (r0.x - ext.x <= bx1) && (r0.y + ext.y >= by0) && (r0.y - ext.y <= by1);
+      }
+      uint32_t m = __ballot_sync(0xffffffffu, ov);
+      while (m) {
+        const int k = __ffs(m) - 1;
+        m &= m - 1;
+        const int idx = g0 + k;
+        const int slot = s_slot[buf][idx];  // warp-uniform
+        const uint32_t pos = (uint32_t)(start + b * kBatchB + idx);
+        float g_mx = 0.f, g_my = 0.f, g_A = 0.f, g_B = 0.f, g_C = 0.f, g_r = 0.f, g_g = 0.f, g_b = 0.f;
+        bool contrib = false;
+        if (!done) {
+          if (pos >= last) {
+            done = true;
+          } else {
+            const float4 r0 = s_rec[buf][idx][0], r1 = s_rec[buf][idx][1];
+            PairEval e;
+            if (eval_pair(r0, r1, fpx, fpy, e)) {
+              const float test = __fmul_rn(T, __fsub_rn(1.f, e.f));
+              if (test < kTMin) {
+                done = true;
+              } else {
+                const float4 r2 = s_rec[buf][idx][2];
+                const float wgt = __fmul_rn(e.f, T);
+                ar = __fmaf_rn(r2.x, wgt, ar);
+                ag = __fmaf_rn(r2.y, wgt, ag);
+                ab = __fmaf_rn(r2.z, wgt, ab);
+                if (slot >= 0) {
+                  contrib = true;
+                  // S_i = sum_{j>i} c_j f_j T_j = C^ - prefix_i
+                  const float Sr = Cr - ar, Sg = Cg - ag, Sb = Cb - ab;
+                  const float inv1mf = 1.f / (1.f - e.f);
+                  g_r = gCr * wgt; g_g = gCg * wgt; g_b = gCb * wgt;
+                  const float dLdf = gCr * (r2.x * T - Sr * inv1mf) + gCg * (r2.y * T - Sg * inv1mf) +
+                                     gCb * (r2.z * T - Sb * inv1mf);
+                  // f = alpha e^power (the 0.99 cap passes no gradient when active, R17)
+                  const float dLdp = (e.fraw < kFMax) ? dLdf * e.f : 0.f;
+                  g_mx = -dLdp * (r1.x * e.dx + r1.y * e.dy);
+                  g_my = -dLdp * (r1.y * e.dx + r1.z * e.dy);
+                  g_A = -0.5f * dLdp * e.dx * e.dx;
+                  g_B = -dLdp * e.dx * e.dy;
+                  g_C = -0.5f * dLdp * e.dy * e.dy;
+                }
+                T = test;
+              }
+            }
+          }
+        }
+        if (slot >= 0 && __any_sync(0xffffffffu, contrib)) {
+          g_mx = warp_sum(g_mx); g_my = warp_sum(g_my);
+          g_A = warp_sum(g_A); g_B = warp_sum(g_B); g_C = warp_sum(g_C);
+          g_r = warp_sum(g_r); g_g = warp_sum(g_g); g_b = warp_sum(g_b);
+          if (lane == 0) {
+            float* sg = a.sgrad + (size_t)slot * kSG;
+            atomicAdd(sg + 0, g_mx); atomicAdd(sg + 1, g_my);
+            atomicAdd(sg + 2, g_A); atomicAdd(sg + 3, g_B); atomicAdd(sg + 4, g_C);
+            atomicAdd(sg + 5, g_r); atomicAdd(sg + 6, g_g); atomicAdd(sg + 7, g_b);
+          }
+        }
+      }
+      wdone = __all_sync(0xffffffffu, done);
+    }
+    __syncthreads();
+  }
+  cp_async_wait<0>();
+}
+
+// ------------------------------------------------------------------------------------------------
+// K5b: chain rule through the projection (float32, recomputing the forward quantities)
+// ------------------------------------------------------------------------------------------------
+struct PBArgs {
+  const float* pos;
+  const float* log_scale;
+  const float* rot;
+  const float* sh;
+  int K, D;  // D = 10 + 3K
+  const int32_t* gid_of_slot;
+  int n_slots;
+  const float* sgrad;
+  const float* acc;  // acc[2] = |P_d|
+  float w_d;
+  double V[9], tp[3], campos[3];
+  float Vf[9];
+  CamK cam;
+  float limx0, limx1, limy0, limy1;
+  float* grad;
+  float* loss_out;
+  float w_c;
+  const uint32_t* counts;
+};
+
+__device__ __forceinline__ void sh_basis_grad(int K, float x, float y, float z, float* Y, float* dx, float* dy, float* dz) {
+  const float C0 = 0.28209479177387814f, C1 = 0.4886025119029199f;
+  const float C20 = 1.0925484305920792f, C21 = -1.0925484305920792f, C22 = 0.31539156525252005f,
+              C23 = -1.0925484305920792f, C24 = 0.5462742152960396f;
+  const float C30 = -0.5900435899266435f, C31 = 2.890611442640554f, C32 = -0.4570457994644658f,
+              C33 = 0.3731763325901154f, C34 = -0.4570457994644658f, C35 = 1.445305721320277f,
+              C36 = -0.5900435899266435f;
+  for (int k = 0; k < 16; ++k) { Y[k] = 0.f; dx[k] = 0.f; dy[k] = 0.f; dz[k] = 0.f; }
+  Y[0] = C0;
+  if (K > 1) {
+    Y[1] = -C1 * y; dy[1] = -C1;
+    Y[2] = C1 * z;  dz[2] = C1;
+    Y[3] = -C1 * x; dx[3] = -C1;
+  }
+  if (K > 4) {
+    const float xx = x * x, yy = y * y, zz = z * z;
+    Y[4] = C20 * x * y;               dx[4] = C20 * y; dy[4] = C20 * x;
+    Y[5] = C21 * y * z;               dy[5] = C21 * z; dz[5] = C21 * y;
+    Y[6] = C22 * (2.f * zz - xx - yy); dx[6] = -2.f * C22 * x; dy[6] = -2.f * C22 * y; dz[6] = 4.f * C22 * z;
+    Y[7] = C23 * x * z;               dx[7] = C23 * z; dz[7] = C23 * x;
+    Y[8] = C24 * (xx - yy);           dx[8] = 2.f * C24 * x; dy[8] = -2.f * C24 * y;
+    if (K > 9) {
+      Y[9] = C30 * y * (3.f * xx - yy);  dx[9] = 6.f * C30 * x * y; dy[9] = C30 * (3.f * xx - 3.f * yy);
+      Y[10] = C31 * x * y * z;           dx[10] = C31 * y * z; dy[10] = C31 * x * z; dz[10] = C31 * x * y;
+      Y[11] = C32 * y * (4.f * zz - xx - yy);
+      dx[11] = -2.f * C32 * x * y; dy[11] = C32 * (4.f * zz - xx - 3.f * yy); dz[11] = 8.f * C32 * y * z;
+      Y[12] = C33 * z * (2.f * zz - 3.f * xx - 3.f * yy);
+      dx[12] = -6.f * C33 * x * z; dy[12] = -6.f * C33 * y * z; dz[12] = C33 * (6.f * zz - 3.f * xx - 3.f * yy);
+      Y[13] = C34 * x * (4.f * zz - xx - yy);
+      dx[13] = C34 * (4.f * zz - 3.f * xx - yy); dy[13] = -2.f * C34 * x * y; dz[13] = 8.f * C34 * x * z;
+      Y[14] = C35 * z * (xx - yy);       dx[14] = 2.f * C35 * x * z; dy[14] = -2.f * C35 * y * z; dz[14] = C35 * (xx - yy);
+      Y[15] = C36 * x * (xx - 3.f * yy); dx[15] = C36 * (3.f * xx - 3.f * yy); dy[15] = -6.f * C36 * x * y;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(128) k_project_bwd(const PBArgs a) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s == 0) {  // loss values (device-side, no host sync)
+    const float nP = (float)max(1u, a.counts[1]);
+    const float Lc = a.acc[0] / (3.f * nP);
+    const float Ld = a.acc[1] / fmaxf(1.f, a.acc[2]);
+    a.loss_out[0] = Lc;
+    a.loss_out[1] = Ld;
+    a.loss_out[2] = a.w_c * Lc + a.w_d * Ld;
+    a.loss_out[3] = a.acc[2];
+  }
+  if (s >= a.n_slots) return;
+  const float* sg = a.sgrad + (size_t)s * kSG;
+  const float4 g0 = *reinterpret_cast<const float4*>(sg);
+  const float4 g1 = *reinterpret_cast<const float4*>(sg + 4);
+  const float4 g2 = *reinterpret_cast<const float4*>(sg + 8);
+  const float gz2 = sg[12];
+  const float dscale = a.w_d / fmaxf(1.f, a.acc[2]);
+  const float dMx = g0.x, dMy = g0.y, dA = g0.z, dB = g0.w, dCc = g1.x;
+  const float drgb[3] = {g1.y, g1.z, g1.w};
+  const float dDa = g2.x * dscale, dDb0 = g2.y * dscale, dDb1 = g2.z * dscale, dDb2 = g2.w * dscale;
+  const float dDz = gz2 * dscale;
+  if (dMx == 0.f && dMy == 0.f && dA == 0.f && dB == 0.f && dCc == 0.f && drgb[0] == 0.f && drgb[1] == 0.f &&
+      drgb[2] == 0.f && dDa == 0.f && dDb0 == 0.f && dDb1 == 0.f && dDb2 == 0.f && dDz == 0.f)
+    return;
+  const int i = a.gid_of_slot[s];
+  const float px = a.pos[3 * i], py = a.pos[3 * i + 1], pz = a.pos[3 * i + 2];
+  const double X = fma(a.V[0], (double)px, fma(a.V[1], (double)py, fma(a.V[2], (double)pz, a.tp[0])));
+  const double Y = fma(a.V[3], (double)px, fma(a.V[4], (double)py, fma(a.V[5], (double)pz, a.tp[1])));
+  const double Z = fma(a.V[6], (double)px, fma(a.V[7], (double)py, fma(a.V[8], (double)pz, a.tp[2])));
+  const float x = (float)X, y = (float)Y, z = (float)Z;
+  const float* V = a.Vf;
+  const float q0 = a.rot[4 * i], q1 = a.rot[4 * i + 1], q2 = a.rot[4 * i + 2], q3 = a.rot[4 * i + 3];
+  const float qn2 = q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3;
+  const float qinv = rsqrtf(qn2);
+  const float qw = q0 * qinv, qx = q1 * qinv, qy = q2 * qinv, qz = q3 * qinv;
+  float R[3][3] = {{1.f - 2.f * (qy * qy + qz * qz), 2.f * (qx * qy - qw * qz), 2.f * (qx * qz + qw * qy)},
+                   {2.f * (qx * qy + qw * qz), 1.f - 2.f * (qx * qx + qz * qz), 2.f * (qy * qz - qw * qx)},
+                   {2.f * (qx * qz - qw * qy), 2.f * (qy * qz + qw * qx), 1.f - 2.f * (qx * qx + qy * qy)}};
+  const float l[3] = {a.log_scale[3 * i], a.log_scale[3 * i + 1], a.log_scale[3 * i + 2]};
+  const float sc[3] = {expf(l[0]), expf(l[1]), expf(l[2])};
+  float M[3][3], Sg[3][3];
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) M[r][c] = R[r][c] * sc[c];
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) Sg[r][c] = M[r][0] * M[c][0] + M[r][1] * M[c][1] + M[r][2] * M[c][2];
+  const float iz = 1.f / z;
+  const float ux = x * iz, uy = y * iz;
+  const bool clx = ux < a.limx0 || ux > a.limx1, cly = uy < a.limy0 || uy > a.limy1;
+  const float limx = fminf(fmaxf(ux, a.limx0), a.limx1), limy = fminf(fmaxf(uy, a.limy0), a.limy1);
+  const float xc = z * limx, yc = z * limy;
+  const float fx = a.cam.fx, fy = a.cam.fy;
+  float J[2][3] = {{fx * iz, 0.f, -fx * xc * iz * iz}, {0.f, fy * iz, -fy * yc * iz * iz}};
+  float Tm[2][3];
+  for (int r = 0; r < 2; ++r)
+    for (int c = 0; c < 3; ++c) Tm[r][c] = J[r][0] * V[c] + J[r][1] * V[3 + c] + J[r][2] * V[6 + c];
+  float TS[2][3];
+  for (int r = 0; r < 2; ++r)
+    for (int c = 0; c < 3; ++c) TS[r][c] = Tm[r][0] * Sg[0][c] + Tm[r][1] * Sg[1][c] + Tm[r][2] * Sg[2][c];
+  const float ca = TS[0][0] * Tm[0][0] + TS[0][1] * Tm[0][1] + TS[0][2] * Tm[0][2] + kDilation;
+  const float cb = TS[0][0] * Tm[1][0] + TS[0][1] * Tm[1][1] + TS[0][2] * Tm[1][2];
+  const float cc = TS[1][0] * Tm[1][0] + TS[1][1] * Tm[1][1] + TS[1][2] * Tm[1][2] + kDilation;
+  const double det = (double)ca * cc - (double)cb * cb;
+  const float Qa = (float)(cc / det), Qb = (float)(-cb / det), Qc = (float)(ca / det);
+
+  // conic -> Sigma2D: dL/dSigma' = -Q G Q, G = [[dA, dB/2], [dB/2, dC]]
+  const float G01 = 0.5f * dB;
+  const float QG00 = Qa * dA + Qb * G01, QG01 = Qa * G01 + Qb * dCc;
+  const float QG10 = Qb * dA + Qc * G01, QG11 = Qb * G01 + Qc * dCc;
+  const float dS00 = -(QG00 * Qa + QG01 * Qb), dS01 = -(QG00 * Qb + QG01 * Qc);
+  const float dS11 = -(QG10 * Qb + QG11 * Qc);
+  const float dSp[2][2] = {{dS00, dS01}, {dS01, dS11}};
+  // Sigma' = T Sigma T^T: dL/dSigma = T^T dS' T ; dL/dT = 2 dS' T Sigma
+  float dSig[3][3];
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) {
+      float v = 0.f;
+      for (int p = 0; p < 2; ++p)
+        for (int q = 0; q < 2; ++q) v += Tm[p][r] * dSp[p][q] * Tm[q][c];
+      dSig[r][c] = v;
+    }
+  float dT[2][3];
+  for (int r = 0; r < 2; ++r)
+    for (int c = 0; c < 3; ++c) dT[r][c] = 2.f * (dSp[r][0] * TS[0][c] + dSp[r][1] * TS[1][c]);
+  // T = J V: dL/dJ = dT V^T
+  float dJ[2][3];
+  for (int r = 0; r < 2; ++r)
+    for (int c = 0; c < 3; ++c) dJ[r][c] = dT[r][0] * V[3 * c] + dT[r][1] * V[3 * c + 1] + dT[r][2] * V[3 * c + 2];
+  // J(x', y', z), x' = z clamp(x/z) (R5)
+  float dx = 0.f, dy = 0.f, dz = 0.f;
+  dz += dJ[0][0] * (-fx * iz * iz) + dJ[0][2] * (2.f * fx * xc * iz * iz * iz);
+  dz += dJ[1][1] * (-fy * iz * iz) + dJ[1][2] * (2.f * fy * yc * iz * iz * iz);
+  const float dxc = dJ[0][2] * (-fx * iz * iz), dyc = dJ[1][2] * (-fy * iz * iz);
+  if (clx) dz += dxc * limx; else dx += dxc;
+  if (cly) dz += dyc * limy; else dy += dyc;
+  // mu = (fx x/z + cx, fy y/z + cy)
+  dx += dMx * fx * iz;
+  dy += dMy * fy * iz;
+  dz += -dMx * fx * x * iz * iz - dMy * fy * y * iz * iz;
+  // depth (Eq.4-5): dL/dp_c += dDa n_c + dDz e_z ; dL/dn_c = dDa p_c - dDb
+  int k = 2;
+  if (l[1] < l[k]) k = 1;
+  if (l[0] < l[k]) k = 0;
+  const float nwx = R[0][k], nwy = R[1][k], nwz = R[2][k];
+  const float ncx = V[0] * nwx + V[1] * nwy + V[2] * nwz;
+  const float ncy = V[3] * nwx + V[4] * nwy + V[5] * nwz;
+  const float ncz = V[6] * nwx + V[7] * nwy + V[8] * nwz;
+  dx += dDa * ncx;
+  dy += dDa * ncy;
+  dz += dDa * ncz + dDz;
+  const float dncx = dDa * x - dDb0, dncy = dDa * y - dDb1, dncz = dDa * z - dDb2;
+  // world position: p_c = V (p - t)  ->  dL/dp = V^T dL/dp_c
+  float gp0 = V[0] * dx + V[3] * dy + V[6] * dz;
+  float gp1 = V[1] * dx + V[4] * dy + V[7] * dz;
+  float gp2 = V[2] * dx + V[5] * dy + V[8] * dz;
+  // dL/dn_world = V^T dL/dn_c
+  const float dnw0 = V[0] * dncx + V[3] * dncy + V[6] * dncz;
+  const float dnw1 = V[1] * dncx + V[4] * dncy + V[7] * dncz;
+  const float dnw2 = V[2] * dncx + V[5] * dncy + V[8] * dncz;
+  // SH colour: rgb = max(0, sum_k Y_k(d) sh_k + 0.5), d = (p - campos)/|p - campos|
+  const double vx = (double)px - a.campos[0], vy = (double)py - a.campos[1], vz = (double)pz - a.campos[2];
+  const double vnorm = sqrt(vx * vx + vy * vy + vz * vz);
+  const float dirx = (float)(vx / vnorm), diry = (float)(vy / vnorm), dirz = (float)(vz / vnorm);
+  float Yb[16], Yx[16], Yy[16], Yz[16];
+  sh_basis_grad(a.K, dirx, diry, dirz, Yb, Yx, Yy, Yz);
+  const float* shc = a.sh + (size_t)i * 3 * a.K;
+  float* gout = a.grad + (size_t)s * a.D;
+  float gd0 = 0.f, gd1 = 0.f, gd2 = 0.f;
+  for (int ch = 0; ch < 3; ++ch) {
+    float raw = 0.5f;
+    for (int kk = 0; kk < a.K; ++kk) raw += Yb[kk] * shc[3 * kk + ch];
+    const float gch = raw >= 0.f ? drgb[ch] : 0.f;  // clamp at 0 (R17)
+    if (gch == 0.f) continue;
+    for (int kk = 0; kk < a.K; ++kk) {
+      gout[10 + 3 * kk + ch] += Yb[kk] * gch;
+      const float c = shc[3 * kk + ch] * gch;
+      gd0 += Yx[kk] * c;
+      gd1 += Yy[kk] * c;
+      gd2 += Yz[kk] * c;
+    }
+  }
+  {
+    const float dd = gd0 * dirx + gd1 * diry + gd2 * dirz;
+    const float inv = (float)(1.0 / vnorm);
+    gp0 += (gd0 - dd * dirx) * inv;
+    gp1 += (gd1 - dd * diry) * inv;
+    gp2 += (gd2 - dd * dirz) * inv;
+  }
+  gout[0] += gp0; gout[1] += gp1; gout[2] += gp2;
+  // Sigma = M M^T, M = R diag(s): dL/dM = 2 dSig M
+  float dM[3][3];
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) dM[r][c] = 2.f * (dSig[r][0] * M[0][c] + dSig[r][1] * M[1][c] + dSig[r][2] * M[2][c]);
+  for (int c = 0; c < 3; ++c) {
+    const float dsc = dM[0][c] * R[0][c] + dM[1][c] * R[1][c] + dM[2][c] * R[2][c];
+    gout[3 + c] += dsc * sc[c];  // s = exp(log_scale)
+  }
+  float GR[3][3];
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) GR[r][c] = dM[r][c] * sc[c];
+  GR[0][k] += dnw0; GR[1][k] += dnw1; GR[2][k] += dnw2;
+  // rotation matrix of the unit quaternion
+  const float gw = 2.f * (-qz * GR[0][1] + qy * GR[0][2] + qz * GR[1][0] - qx * GR[1][2] - qy * GR[2][0] + qx * GR[2][1]);
+  const float gx = 2.f * (qy * GR[0][1] + qz * GR[0][2] + qy * GR[1][0] - 2.f * qx * GR[1][1] - qw * GR[1][2] +
+                          qz * GR[2][0] + qw * GR[2][1] - 2.f * qx * GR[2][2]);
+  const float gy = 2.f * (-2.f * qy * GR[0][0] + qx * GR[0][1] + qw * GR[0][2] + qx * GR[1][0] + qz * GR[1][2] -
+                          qw * GR[2][0] + qz * GR[2][1] - 2.f * qy * GR[2][2]);
+  const float gz = 2.f * (-2.f * qz * GR[0][0] - qw * GR[0][1] + qx * GR[0][2] + qw * GR[1][0] - 2.f * qz * GR[1][1] +
+                          qy * GR[1][2] + qx * GR[2][0] + qy * GR[2][1]);
+  // through q = q~/|q~|
+  const float dot = gw * qw + gx * qx + gy * qy + gz * qz;
+  gout[6] += (gw - dot * qw) * qinv;
+  gout[7] += (gx - dot * qx) * qinv;
+  gout[8] += (gy - dot * qy) * qinv;
+  gout[9] += (gz - dot * qz) * qinv;
+}
+
+cudaError_t launch_backward(const rtgs_gaussians& g, const rtgs_projected& proj, const rtgs_bins& bins,
+                            const PoseF& pose, const rtgs_camera& cam, const rtgs_render_out& fwd,
+                            const rtgs_frame& target, const rtgs_loss_weights& w, const int32_t* slot_of_gid,
+                            const int32_t* gid_of_slot, int n_slots, float* grad, float* loss_out, void* ws,
+                            cudaStream_t s) {
+  float* sgrad = static_cast<float*>(ws);
+  float* acc = sgrad + (size_t)n_slots * kSG;
+  cudaMemsetAsync(ws, 0, ((size_t)n_slots * kSG + 8) * sizeof(float), s);
+  BwdArgs a;
+  a.rec = reinterpret_cast<const float4*>(proj.rec);
+  a.zkey = proj.zkey;
+  a.sorted_gid = bins.sorted_gid;
+  a.range = reinterpret_cast<const uint2*>(bins.tile_range);
+  a.tile_list = fwd.tile_list;
+  a.counts = fwd.counts;
+  a.active = fwd.active_bits;
+  a.color = fwd.color; a.depth = fwd.depth; a.index = fwd.index; a.n_contrib = fwd.n_contrib;
+  a.tcolor = target.color; a.tdepth = target.depth;
+  a.slot_of_gid = slot_of_gid;
+  a.cam = make_cam(cam);
+  a.w_c = w.w_c;
+  a.sgrad = sgrad;
+  a.acc = acc;
+  const int T = a.cam.TX * a.cam.TY;
+  k_render_bwd<<<T, 256, 0, s>>>(a);
+  note_launch();
+  PBArgs b;
+  b.pos = g.pos; b.log_scale = g.log_scale; b.rot = g.rot; b.sh = g.sh;
+  b.K = (g.sh_degree + 1) * (g.sh_degree + 1);
+  b.D = 10 + 3 * b.K;
+  b.gid_of_slot = gid_of_slot;
+  b.n_slots = n_slots;
+  b.sgrad = sgrad;
+  b.acc = acc;
+  b.w_d = w.w_d;
+  b.w_c = w.w_c;
+  for (int k = 0; k < 9; ++k) { b.V[k] = pose.V[k]; b.Vf[k] = pose.Vf[k]; }
+  for (int k = 0; k < 3; ++k) { b.tp[k] = pose.tp[k]; b.campos[k] = pose.campos[k]; }
+  b.cam = a.cam;
+  const double W = cam.width, H = cam.height;
+  b.limx0 = (float)((-0.15 * W - cam.cx) / cam.fx);
+  b.limx1 = (float)((1.15 * W - cam.cx) / cam.fx);
+  b.limy0 = (float)((-0.15 * H - cam.cy) / cam.fy);
+  b.limy1 = (float)((1.15 * H - cam.cy) / cam.fy);
+  b.grad = grad;
+  b.loss_out = loss_out;
+  b.counts = fwd.counts;
+  const int nb = n_slots > 0 ? (n_slots + 127) / 128 : 1;
+  k_project_bwd<<<nb, 128, 0, s>>>(b);
+  note_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace rtgs

@@ -1,0 +1,144 @@
+// common.cuh — device helpers shared by the librtgs kernels (sm_100a).
+// Nothing here is shared with oracle/ (DESIGN.md §4): constants are restated from the paper.
+#pragma once
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "rtgs.h"
+
+namespace rtgs {
+
+// ---- constants of the method (PAPER.md; readings in DESIGN.md §3) -----------------------------
+constexpr float kDeltaAlpha = 0.60653065971263342f;  // e^-0.5
+constexpr float kTMin = 1e-4f;                       // early termination (R7)
+constexpr float kFMin = 1.0f / 255.0f;               // R7
+constexpr float kFMax = 0.99f;                       // R7
+constexpr float kPowerMin = -4.5f;                   // 3 sigma (R7)
+constexpr float kCos60 = 0.5f;                       // Eq.5 60 deg switch (R11)
+constexpr float kNear = 0.2f;                        // R6
+constexpr float kDilation = 0.3f;                    // R4
+constexpr float kRectPad = 0.015625f;                // 2^-6 px (R7)
+constexpr int kTile = 16;
+constexpr int kRecFloats = 16;                       // projected record, 64 B
+
+struct CamK {
+  float fx, fy, cx, cy;
+  int W, H, TX, TY;
+};
+
+static inline CamK make_cam(const rtgs_camera& c) {
+  CamK k;
+  k.fx = c.fx; k.fy = c.fy; k.cx = c.cx; k.cy = c.cy;
+  k.W = c.width; k.H = c.height;
+  k.TX = (c.width + kTile - 1) / kTile;
+  k.TY = (c.height + kTile - 1) / kTile;
+  return k;
+}
+
+// Launch accounting (rtgs_launch_count)
+void note_launch(int n = 1);
+
+// ---- small PTX wrappers --------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem)), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// mbarrier + 1D bulk copy (TMA engine, cp.async.bulk) global -> shared
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(smem)),
+      "l"(gmem), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// inclusive warp scan of uint32
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t t = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += t;
+  }
+  return v;
+}
+
+// Block-wide exclusive scan (blockDim.x multiple of 32, <= 1024). Returns the exclusive prefix of v
+// and writes the block total to *total. `sh` needs 33 uint32 of shared memory.
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* sh, uint32_t* total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  uint32_t inc = warp_incl_scan(v);
+  if (lane == 31) sh[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    uint32_t s = lane < nw ? sh[lane] : 0u;
+    uint32_t si = warp_incl_scan(s);
+    if (lane < nw) sh[lane] = si - s;
+    if (lane == 31) sh[32] = si;
+  }
+  __syncthreads();
+  uint32_t r = inc - v + sh[wid];
+  *total = sh[32];
+  __syncthreads();
+  return r;
+}
+
+// ---- the per-pair evaluation shared by the forward and the backward replay --------------------
+// Every operation is an explicitly rounded intrinsic, so both kernels take bit-identical decisions
+// (same T sequence, same termination, same hit) whatever the compiler does elsewhere.
+//   a = (mu_x hi, mu_y hi, mu_x lo, mu_y lo), b = (A, B, C, alpha)
+//   d = mu - u (double-float mu: the hi part minus the integer pixel centre is exact)
+struct PairEval {
+  float dx, dy, power, fraw, f;
+};
+__device__ __forceinline__ bool eval_pair(const float4 a, const float4 b, float px, float py, PairEval& e) {
+  e.dx = __fadd_rn(__fsub_rn(a.x, px), a.z);
+  e.dy = __fadd_rn(__fsub_rn(a.y, py), a.w);
+  const float q = __fmaf_rn(__fmul_rn(b.x, e.dx), e.dx, __fmul_rn(__fmul_rn(b.z, e.dy), e.dy));  // A dx^2 + C dy^2
+  e.power = __fmaf_rn(-0.5f, q, -__fmul_rn(__fmul_rn(b.y, e.dx), e.dy));
+  e.fraw = __fmul_rn(b.w, __expf(e.power));
+  e.f = fminf(kFMax, e.fraw);
+  return (e.power >= kPowerMin) && (e.f >= kFMin);
+}
+
+__device__ __forceinline__ float2 unpack_ext(float w) {
+  const uint32_t u = __float_as_uint(w);
+  return make_float2(__half2float(__ushort_as_half((unsigned short)(u & 0xFFFFu))),
+                     __half2float(__ushort_as_half((unsigned short)(u >> 16))));
+}
+
+}  // namespace rtgs

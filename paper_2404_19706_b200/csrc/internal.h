@@ -1,0 +1,50 @@
+// internal.h — host-side launchers behind the C ABI (abi.cu validates, these enqueue kernels).
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include "rtgs.h"
+
+namespace rtgs {
+
+struct PoseF {  // world->camera V = R^T, t' = -R^T t (double and float32 copies), camera centre
+  double V[9], tp[3], campos[3];
+  float Vf[9], tpf[3];
+  float Rf[9];  // camera->world rotation (normal map)
+};
+PoseF make_pose(const rtgs_pose& p);
+
+cudaError_t launch_project(const rtgs_gaussians& g, const PoseF& pose, const rtgs_camera& cam,
+                           const rtgs_projected& out, cudaStream_t s);
+
+size_t bin_workspace_size(int n, const rtgs_camera& cam, uint32_t capacity);
+cudaError_t launch_bin(const rtgs_projected& proj, int n, const rtgs_camera& cam, const uint8_t* keep,
+                       const rtgs_bins& out, void* ws, cudaStream_t s);
+
+cudaError_t launch_coverage(const rtgs_gaussians& g, const rtgs_projected& proj, const rtgs_camera& cam,
+                            const rtgs_render_out& out, cudaStream_t s);
+cudaError_t launch_render(const rtgs_projected& proj, const rtgs_bins& bins, const PoseF& pose,
+                          const rtgs_camera& cam, int masked, const rtgs_render_out& out, cudaStream_t s);
+
+size_t backward_workspace_size(int n_slots);
+cudaError_t launch_backward(const rtgs_gaussians& g, const rtgs_projected& proj, const rtgs_bins& bins,
+                            const PoseF& pose, const rtgs_camera& cam, const rtgs_render_out& fwd,
+                            const rtgs_frame& target, const rtgs_loss_weights& w, const int32_t* slot_of_gid,
+                            const int32_t* gid_of_slot, int n_slots, float* grad, float* loss_out, void* ws,
+                            cudaStream_t s);
+
+cudaError_t launch_adam(const rtgs_params& p, const int32_t* gid_of_slot, int n_slots, const uint8_t* flags,
+                        float* grad, float* m, float* v, const float* init_geom, int n_transparent, float w_reg,
+                        const rtgs_hparams& hp, int step, uint32_t* eta, cudaStream_t s);
+
+size_t classify_workspace_size(const rtgs_camera& cam);
+cudaError_t launch_classify(const rtgs_render_out& full, const rtgs_frame& frame, const uint8_t* flags,
+                            const rtgs_camera& cam, const rtgs_add_params& ap, uint8_t* cls, uint32_t* samples,
+                            uint32_t cap, uint32_t* counts, void* ws, cudaStream_t s);
+
+// generic device-wide exclusive scan of uint32 (length known on the host; zeros past the live part)
+size_t scan_workspace_size(size_t len);
+cudaError_t launch_scan(const uint32_t* in, uint32_t* out, size_t len, uint32_t* total, void* ws, cudaStream_t s);
+
+}  // namespace rtgs

@@ -1,0 +1,304 @@
+"""Python binding of librtgs.so: argument marshalling only.
+
+Every step of the mapping path runs in the CUDA kernels behind include/rtgs.h; this module only
+allocates device buffers with torch (plumbing), builds the C structs and calls the six entry points
+under the same names:
+
+    project_gaussians, bin_and_sort, render_color_depth, render_backward_masked,
+    adam_step_unstable, classify_and_add_pixels
+
+`MappingEngine` strings them together into the paper's per-frame flow:
+    ingest(frame)     A1 project -> A2 bin (all tiles) -> A3/A4 FULL render -> A7 classify
+    iteration(frame)  A1 project -> A0 coverage/tile keep -> A2 bin (kept tiles) -> A3/A4 MASKED
+                      -> A5 masked backward -> A6 Adam over the unstable Gaussians
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+
+import numpy as np
+import torch
+
+from . import _abi
+from ._abi import RTGS_RENDER_COVERAGE, RTGS_RENDER_FULL, RTGS_RENDER_MASKED, check, lib
+
+FLAG_TRANSPARENT = 1
+FLAG_STABLE = 2
+
+
+def _p(t: torch.Tensor | None):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return C.c_void_p(s.cuda_stream)
+
+
+def make_camera(fx, fy, cx, cy, width, height) -> _abi.Camera:
+    return _abi.Camera(float(fx), float(fy), float(cx), float(cy), int(width), int(height))
+
+
+def camera_of(cfg) -> _abi.Camera:
+    return make_camera(cfg.fx, cfg.fy, cfg.cx, cfg.cy, cfg.width, cfg.height)
+
+
+def make_pose(R, t) -> _abi.Pose:
+    R = np.asarray(R, dtype=np.float64).reshape(9)
+    t = np.asarray(t, dtype=np.float64).reshape(3)
+    return _abi.Pose((C.c_double * 9)(*R), (C.c_double * 3)(*t))
+
+
+@dataclasses.dataclass
+class GaussianMap:
+    """Device SoA of the Gaussian map, float32."""
+    pos: torch.Tensor
+    log_scale: torch.Tensor
+    rot: torch.Tensor
+    opacity: torch.Tensor
+    sh: torch.Tensor
+    flags: torch.Tensor  # uint8
+    sh_degree: int
+
+    @property
+    def n(self) -> int:
+        return int(self.pos.shape[0])
+
+    @classmethod
+    def from_arrays(cls, scene: dict, device="cuda") -> "GaussianMap":
+        f = lambda k: torch.as_tensor(np.ascontiguousarray(scene[k]), device=device).contiguous()
+        return cls(f("pos"), f("log_scale"), f("rot"), f("opacity"), f("sh"), f("flags"), int(scene["sh_degree"]))
+
+    def c_struct(self) -> _abi.Gaussians:
+        return _abi.Gaussians(_p(self.pos), _p(self.log_scale), _p(self.rot), _p(self.opacity), _p(self.sh),
+                              _p(self.flags), self.n, self.sh_degree)
+
+    def c_params(self) -> _abi.Params:
+        return _abi.Params(_p(self.pos), _p(self.log_scale), _p(self.rot), _p(self.sh), self.n, self.sh_degree)
+
+
+class ProjectedBuffers:
+    def __init__(self, n: int, device="cuda"):
+        nn = max(n, 1)
+        self.rec = torch.empty((nn, 16), dtype=torch.float32, device=device)
+        self.zkey = torch.empty(nn, dtype=torch.int32, device=device)
+        self.rect = torch.empty((nn, 4), dtype=torch.int16, device=device)
+        self.tiles_touched = torch.empty(nn, dtype=torch.int32, device=device)
+
+    def c_struct(self):
+        return _abi.Projected(_p(self.rec), _p(self.zkey), _p(self.rect), _p(self.tiles_touched))
+
+
+class BinBuffers:
+    def __init__(self, cam: _abi.Camera, capacity: int, device="cuda"):
+        T = ((cam.width + 15) // 16) * ((cam.height + 15) // 16)
+        self.capacity = int(capacity)
+        self.sorted_gid = torch.empty(max(capacity, 1), dtype=torch.int32, device=device)
+        self.tile_range = torch.zeros((T, 2), dtype=torch.int32, device=device)
+        self.n_instances = torch.zeros(1, dtype=torch.int32, device=device)
+
+    def c_struct(self):
+        return _abi.Bins(_p(self.sorted_gid), _p(self.tile_range), _p(self.n_instances), self.capacity)
+
+
+class RenderBuffers:
+    def __init__(self, cam: _abi.Camera, device="cuda", normal=True):
+        H, W = cam.height, cam.width
+        T = ((W + 15) // 16) * ((H + 15) // 16)
+        self.color = torch.zeros((3, H, W), dtype=torch.float32, device=device)
+        self.trans = torch.zeros((H, W), dtype=torch.float32, device=device)
+        self.depth = torch.zeros((H, W), dtype=torch.float32, device=device)
+        self.normal = torch.zeros((3, H, W), dtype=torch.float32, device=device) if normal else None
+        self.index = torch.zeros((H, W), dtype=torch.int32, device=device)
+        self.n_contrib = torch.zeros((H, W), dtype=torch.int32, device=device)
+        self.active_bits = torch.zeros((H * W + 31) // 32, dtype=torch.int32, device=device)
+        self.tile_keep = torch.zeros(T, dtype=torch.uint8, device=device)
+        self.tile_list = torch.zeros(T, dtype=torch.int32, device=device)
+        self.counts = torch.zeros(4, dtype=torch.int32, device=device)
+
+    def c_struct(self):
+        return _abi.RenderOut(_p(self.color), _p(self.trans), _p(self.depth), _p(self.normal), _p(self.index),
+                              _p(self.n_contrib), _p(self.active_bits), _p(self.tile_keep), _p(self.tile_list),
+                              _p(self.counts))
+
+    def active_mask(self) -> torch.Tensor:
+        """Unpack active_bits into a bool [H, W] image (test / inspection helper)."""
+        H, W = self.trans.shape
+        words = self.active_bits.to(torch.int64) & 0xFFFFFFFF
+        bits = (words[:, None] >> torch.arange(32, device=words.device)) & 1
+        return bits.reshape(-1)[: H * W].reshape(H, W).bool()
+
+
+# ---------------------------------------------------------------------------------------------
+# the six entry points (same names as the C ABI)
+# ---------------------------------------------------------------------------------------------
+def project_gaussians(gm: GaussianMap, pose: _abi.Pose, cam: _abi.Camera, proj: ProjectedBuffers, stream=None):
+    g = gm.c_struct()
+    pr = proj.c_struct()
+    check(lib().rtgs_project_gaussians(C.byref(g), C.byref(pose), C.byref(cam), C.byref(pr), _stream(stream)),
+          "rtgs_project_gaussians")
+
+
+def bin_workspace_size(n: int, cam: _abi.Camera, capacity: int) -> int:
+    return int(lib().rtgs_bin_workspace_size(n, C.byref(cam), capacity))
+
+
+def bin_and_sort(proj: ProjectedBuffers, n: int, cam: _abi.Camera, tile_keep: torch.Tensor | None, bins: BinBuffers,
+                 workspace: torch.Tensor, stream=None):
+    pr = proj.c_struct()
+    b = bins.c_struct()
+    check(lib().rtgs_bin_and_sort(C.byref(pr), n, C.byref(cam), _p(tile_keep), C.byref(b), _p(workspace),
+                                  workspace.numel() * workspace.element_size(), _stream(stream)), "rtgs_bin_and_sort")
+
+
+def render_color_depth(gm: GaussianMap, proj: ProjectedBuffers, bins: BinBuffers | None, pose: _abi.Pose,
+                       cam: _abi.Camera, mode: int, out: RenderBuffers, stream=None):
+    g = gm.c_struct()
+    pr = proj.c_struct()
+    o = out.c_struct()
+    b = bins.c_struct() if bins is not None else None
+    check(lib().rtgs_render_color_depth(C.byref(g), C.byref(pr), C.byref(b) if b is not None else None, C.byref(pose),
+                                        C.byref(cam), mode, C.byref(o), _stream(stream)), "rtgs_render_color_depth")
+
+
+def backward_workspace_size(n_slots: int) -> int:
+    return int(lib().rtgs_backward_workspace_size(n_slots))
+
+
+def render_backward_masked(gm: GaussianMap, proj: ProjectedBuffers, bins: BinBuffers, pose: _abi.Pose, cam: _abi.Camera,
+                           fwd: RenderBuffers, target_color: torch.Tensor, target_depth: torch.Tensor,
+                           weights: tuple, slot_of_gid: torch.Tensor, gid_of_slot: torch.Tensor, grad: torch.Tensor,
+                           loss_out: torch.Tensor, workspace: torch.Tensor, stream=None):
+    g = gm.c_struct()
+    pr = proj.c_struct()
+    b = bins.c_struct()
+    o = fwd.c_struct()
+    fr = _abi.Frame(_p(target_color), _p(target_depth))
+    w = _abi.LossWeights(*[float(x) for x in weights])
+    check(lib().rtgs_render_backward_masked(C.byref(g), C.byref(pr), C.byref(b), C.byref(pose), C.byref(cam), C.byref(o),
+                                            C.byref(fr), C.byref(w), _p(slot_of_gid), _p(gid_of_slot),
+                                            int(gid_of_slot.numel()), _p(grad), _p(loss_out), _p(workspace),
+                                            workspace.numel() * workspace.element_size(), _stream(stream)),
+          "rtgs_render_backward_masked")
+
+
+def adam_step_unstable(gm: GaussianMap, gid_of_slot: torch.Tensor, grad: torch.Tensor, m: torch.Tensor,
+                       v: torch.Tensor, init_geom: torch.Tensor | None, n_transparent: int, w_reg: float,
+                       hparams: _abi.HParams, step: int, eta: torch.Tensor, stream=None):
+    prm = gm.c_params()
+    check(lib().rtgs_adam_step_unstable(C.byref(prm), _p(gid_of_slot), int(gid_of_slot.numel()), _p(gm.flags), _p(grad),
+                                        _p(m), _p(v), _p(init_geom), int(n_transparent), float(w_reg), C.byref(hparams),
+                                        int(step), _p(eta), _stream(stream)), "rtgs_adam_step_unstable")
+
+
+def classify_workspace_size(cam: _abi.Camera) -> int:
+    return int(lib().rtgs_classify_workspace_size(C.byref(cam)))
+
+
+def classify_and_add_pixels(full: RenderBuffers, frame_color: torch.Tensor, frame_depth: torch.Tensor,
+                            flags: torch.Tensor, cam: _abi.Camera, add: _abi.AddParams, pixel_class: torch.Tensor,
+                            samples: torch.Tensor, counts: torch.Tensor, workspace: torch.Tensor, stream=None):
+    o = full.c_struct()
+    fr = _abi.Frame(_p(frame_color), _p(frame_depth))
+    check(lib().rtgs_classify_and_add_pixels(C.byref(o), C.byref(fr), _p(flags), C.byref(cam), C.byref(add),
+                                             _p(pixel_class), _p(samples), int(samples.numel()), _p(counts),
+                                             _p(workspace), workspace.numel() * workspace.element_size(),
+                                             _stream(stream)), "rtgs_classify_and_add_pixels")
+
+
+def hparams(preset: str = "replica") -> _abi.HParams:
+    """Learning rates of P:501: Replica / ScanNet++ vs Azure / TUM."""
+    if preset in ("replica", "scannetpp"):
+        lr_pos, lr_sh0, lr_scale, lr_rot = 1e-3, 5e-4, 4e-3, 1e-3
+    else:
+        lr_pos, lr_sh0, lr_scale, lr_rot = 1e-3, 1e-3, 2e-3, 1e-3
+    return _abi.HParams(lr_pos, lr_sh0, 0.05 * lr_sh0, lr_scale, lr_rot, 0.9, 0.999, 1e-15)
+
+
+def add_params(seed=0, frame_idx=0, delta_T=0.5, delta_d=0.1, delta_c=0.1, ratio=0.05) -> _abi.AddParams:
+    return _abi.AddParams(delta_T, delta_d, delta_c, ratio, seed, frame_idx)
+
+
+# ---------------------------------------------------------------------------------------------
+class MappingEngine:
+    """Device buffers + the per-frame call sequence for one camera and one Gaussian map."""
+
+    def __init__(self, gm: GaussianMap, cam: _abi.Camera, capacity: int | None = None, preset="replica",
+                 weights=(1.0, 1.0, 1000.0), sample_cap: int | None = None, device="cuda"):
+        self.gm, self.cam, self.device = gm, cam, device
+        n = gm.n
+        self.capacity = int(capacity if capacity is not None else max(4 * n, 1 << 16))
+        self.proj = ProjectedBuffers(n, device)
+        self.bins = BinBuffers(cam, self.capacity, device)
+        self.out = RenderBuffers(cam, device)
+        self.full = RenderBuffers(cam, device)
+        self.ws_bin = torch.empty(bin_workspace_size(n, cam, self.capacity), dtype=torch.uint8, device=device)
+        self.ws_cls = torch.empty(classify_workspace_size(cam), dtype=torch.uint8, device=device)
+        self.weights = weights
+        self.hp = hparams(preset)
+        self.loss = torch.zeros(4, dtype=torch.float32, device=device)
+        HW = cam.width * cam.height
+        self.pixel_class = torch.zeros((cam.height, cam.width), dtype=torch.uint8, device=device)
+        self.samples = torch.zeros(sample_cap if sample_cap is not None else max(HW // 8, 1), dtype=torch.int32,
+                                   device=device)
+        self.add_counts = torch.zeros(5, dtype=torch.int32, device=device)
+        self.eta = torch.zeros(n, dtype=torch.int32, device=device)
+        self.reset_window()
+
+    def reset_window(self):
+        """(Re)build the unstable slot set from flags and reset the Adam state (R19: per window)."""
+        flags = self.gm.flags.cpu().numpy()
+        gid = np.nonzero((flags & FLAG_STABLE) == 0)[0].astype(np.int32)
+        slot = np.full(self.gm.n, -1, dtype=np.int32)
+        slot[gid] = np.arange(len(gid), dtype=np.int32)
+        self.gid_of_slot = torch.as_tensor(gid, device=self.device)
+        self.slot_of_gid = torch.as_tensor(slot, device=self.device)
+        n_slots = len(gid)
+        D = 10 + 3 * (self.gm.sh_degree + 1) ** 2
+        self.grad = torch.zeros((max(n_slots, 1), D), dtype=torch.float32, device=self.device)
+        self.m = torch.zeros_like(self.grad)
+        self.v = torch.zeros_like(self.grad)
+        self.n_transparent = int(((flags[gid] & FLAG_TRANSPARENT) != 0).sum())
+        gid_t = self.gid_of_slot.long()
+        self.init_geom = torch.cat([self.gm.pos[gid_t], self.gm.log_scale[gid_t], self.gm.rot[gid_t]], 1).contiguous() \
+            if n_slots else torch.zeros((1, 10), device=self.device)
+        self.ws_bwd = torch.empty(backward_workspace_size(n_slots), dtype=torch.uint8, device=self.device)
+        self.step_count = 0
+
+    # --- the two flows ---------------------------------------------------------------------------
+    def ingest(self, frame_color, frame_depth, pose: _abi.Pose, seed=0, frame_idx=0, stream=None):
+        """A1 -> A2 (all tiles) -> A3/A4 FULL -> A7."""
+        project_gaussians(self.gm, pose, self.cam, self.proj, stream)
+        bin_and_sort(self.proj, self.gm.n, self.cam, None, self.bins, self.ws_bin, stream)
+        render_color_depth(self.gm, self.proj, self.bins, pose, self.cam, RTGS_RENDER_FULL, self.full, stream)
+        classify_and_add_pixels(self.full, frame_color, frame_depth, self.gm.flags, self.cam,
+                                add_params(seed=seed, frame_idx=frame_idx), self.pixel_class, self.samples,
+                                self.add_counts, self.ws_cls, stream)
+
+    def forward_masked(self, pose: _abi.Pose, stream=None):
+        """A1 -> A0 -> A2 (kept tiles) -> A3/A4 MASKED (Eq.12)."""
+        project_gaussians(self.gm, pose, self.cam, self.proj, stream)
+        render_color_depth(self.gm, self.proj, None, pose, self.cam, RTGS_RENDER_COVERAGE, self.out, stream)
+        bin_and_sort(self.proj, self.gm.n, self.cam, self.out.tile_keep, self.bins, self.ws_bin, stream)
+        render_color_depth(self.gm, self.proj, self.bins, pose, self.cam, RTGS_RENDER_MASKED, self.out, stream)
+
+    def backward(self, frame_color, frame_depth, pose: _abi.Pose, stream=None):
+        render_backward_masked(self.gm, self.proj, self.bins, pose, self.cam, self.out, frame_color, frame_depth,
+                               self.weights, self.slot_of_gid, self.gid_of_slot, self.grad, self.loss, self.ws_bwd,
+                               stream)
+
+    def optimizer_step(self, stream=None):
+        self.step_count += 1
+        adam_step_unstable(self.gm, self.gid_of_slot, self.grad, self.m, self.v, self.init_geom, self.n_transparent,
+                           self.weights[2], self.hp, self.step_count, self.eta, stream)
+
+    def iteration(self, frame_color, frame_depth, pose: _abi.Pose, stream=None):
+        """One mapping optimisation iteration A0-A6 (the paper's 'mapping / iteration')."""
+        self.forward_masked(pose, stream)
+        self.backward(frame_color, frame_depth, pose, stream)
+        self.optimizer_step(stream)
+
+
+def launch_count() -> int:
+    return int(lib().rtgs_launch_count())

@@ -74,6 +74,7 @@ CONFIGS: dict[str, SceneConfig] = {
     "T1": SceneConfig("T1", 200, 136, 120.0, 120.0, 99.5, 67.5, 12_000, 0.1, 0.2, "slab", 4.0, 107),
     "T2": SceneConfig("T2", 333, 250, 260.0, 262.0, 166.0, 124.5, 30_000, 0.1, 0.3, "scattered", 3.5, 108,
                       depth_noise=0.0015, hole_frac=0.02, color_noise=0.02),
+    "T3": SceneConfig("T3", 96, 64, 80.0, 80.0, 47.5, 31.5, 3000, 0.1, 0.3, "slab", 3.0, 109),
 }
 
 

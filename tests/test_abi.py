@@ -1,0 +1,73 @@
+"""CPU-side checks of the C ABI: the library builds, loads, exports every symbol include/rtgs.h
+declares, and rejects invalid arguments before touching the GPU."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+from paper_2404_19706_b200 import build as B
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def L():
+    B.build()
+    from paper_2404_19706_b200 import _abi
+    return _abi.lib()
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "rtgs.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(rtgs_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_every_declared_symbol_is_exported(L):
+    names = _declared()
+    assert len(names) == 13
+    for n in names:
+        assert hasattr(L, n), n
+    from paper_2404_19706_b200 import _abi
+    assert set(_abi.EXPORTS) == set(names)
+
+
+def test_status_strings_and_version(L):
+    assert L.rtgs_status_string(0) == b"RTGS_OK"
+    assert L.rtgs_status_string(1) == b"RTGS_ERR_INVALID_ARG"
+    assert L.rtgs_version() == 1
+
+
+def test_invalid_arguments_rejected_on_host(L):
+    from paper_2404_19706_b200 import _abi, mapping
+    cam = mapping.make_camera(500, 500, 320, 240, 640, 480)
+    pose = mapping.make_pose([[1, 0, 0], [0, 1, 0], [0, 0, 1]], [0, 0, 0])
+    g = _abi.Gaussians(None, None, None, None, None, None, 10, 3)
+    pr = _abi.Projected(None, None, None, None)
+    assert L.rtgs_project_gaussians(C.byref(g), C.byref(pose), C.byref(cam), C.byref(pr), None) == 1
+    g0 = _abi.Gaussians(None, None, None, None, None, None, 0, 4)      # bad SH degree
+    assert L.rtgs_project_gaussians(C.byref(g0), C.byref(pose), C.byref(cam), C.byref(pr), None) == 1
+    bad_cam = mapping.make_camera(-1, 500, 320, 240, 640, 480)
+    g1 = _abi.Gaussians(None, None, None, None, None, None, 0, 3)
+    assert L.rtgs_project_gaussians(C.byref(g1), C.byref(pose), C.byref(bad_cam), C.byref(pr), None) == 1
+    nan_pose = mapping.make_pose([[float("nan"), 0, 0], [0, 1, 0], [0, 0, 1]], [0, 0, 0])
+    assert L.rtgs_project_gaussians(C.byref(g1), C.byref(nan_pose), C.byref(cam), C.byref(pr), None) == 1
+    out = _abi.RenderOut()
+    assert L.rtgs_render_color_depth(C.byref(g1), C.byref(pr), None, C.byref(pose), C.byref(cam), 7, C.byref(out), None) == 1
+    b = _abi.Bins(None, None, None, 0)
+    assert L.rtgs_bin_and_sort(C.byref(pr), 0, C.byref(cam), None, C.byref(b), None, 0, None) == 1
+    hp = mapping.hparams()
+    prm = _abi.Params(None, None, None, None, 0, 3)
+    assert L.rtgs_adam_step_unstable(C.byref(prm), None, 0, None, None, None, None, None, 0, 1000.0, C.byref(hp), 0,
+                                     None, None) == 1                  # step must be >= 1
+
+
+def test_workspace_sizes(L):
+    from paper_2404_19706_b200 import mapping
+    cam = mapping.make_camera(600, 600, 599.5, 339.5, 1200, 680)
+    a = mapping.bin_workspace_size(1000, cam, 1 << 16)
+    b = mapping.bin_workspace_size(1_000_000, cam, 4 << 20)
+    assert 0 < a < b
+    assert mapping.backward_workspace_size(100_000) >= 100_000 * 16 * 4
+    assert mapping.classify_workspace_size(cam) > 0
