@@ -216,9 +216,12 @@ def main():
     for i in range(args.warmup):
         step(col, dep, i)
     torch.cuda.synchronize()
-    n_inst = int(eng.bins.n_instances.item())
-    if n_inst > eng.capacity:
-        raise RuntimeError(f"instance capacity {eng.capacity} < {n_inst}")
+    n_inst_iter0 = int(eng.bins.n_instances.item())
+    eng.ingest(col, dep, pose, seed=1234, frame_idx=0)
+    torch.cuda.synchronize()
+    n_inst = int(eng.bins.n_instances.item())          # full-frame instance count (ingest binning)
+    if max(n_inst, n_inst_iter0) > eng.capacity:
+        raise RuntimeError(f"instance capacity {eng.capacity} < {max(n_inst, n_inst_iter0)}")
 
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")  # > 126 MB L2
 

@@ -129,10 +129,11 @@ typedef struct {
   float w_c, w_d, w_reg;
 } rtgs_loss_weights;
 
-/* Per-group learning rates and Adam constants (R19: beta 0.9/0.999, eps 1e-15). */
+/* Per-group learning rates and Adam constants (R19: beta 0.9/0.999, eps 1e-15).  The betas
+ * are float64 so that 1 - beta2 = 1e-3 is formed exactly before rounding to the kernel's float32. */
 typedef struct {
   float lr_pos, lr_sh0, lr_shrest, lr_scale, lr_rot;
-  float beta1, beta2, eps;
+  double beta1, beta2, eps;
 } rtgs_hparams;
 
 /* Gaussian-adding thresholds: delta_T 0.5, delta_d 0.1, delta_c 0.1, ratio 0.05. */

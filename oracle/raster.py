@@ -121,12 +121,17 @@ def render_pixels(proj: dict, pixels: np.ndarray, cam: dict, R: np.ndarray, orde
                    index=hit_gid.numpy().copy(), n_blend=blended.sum(1).numpy(),
                    use_plane=(use_plane & has_hit).numpy())
         if want_margin:
+            # only Gaussians up to the terminating one take part in the pixel's decisions
+            M = power.shape[1]
+            ft = first_term.numpy()
+            term_col = np.where(ft < K, idx.numpy()[np.arange(p), np.minimum(ft, K - 1)], M - 1)
+            seen = np.arange(M)[None, :] <= term_col[:, None]
             pw = power.detach().numpy()
             fr = fraw.detach().numpy()
             fd = f.detach().numpy()
-            m = np.minimum(_rel(pw, POWER_MIN).min(1, initial=np.inf),
-                           (np.abs(fd - F_MIN) / F_MIN).min(1, initial=np.inf))
-            m = np.minimum(m, _rel(fr, F_MAX).min(1, initial=np.inf))
+            m = np.minimum(np.where(seen, _rel(pw, POWER_MIN), np.inf).min(1, initial=np.inf),
+                           np.where(seen, np.abs(fd - F_MIN) / F_MIN, np.inf).min(1, initial=np.inf))
+            m = np.minimum(m, np.where(seen, _rel(fr, F_MAX), np.inf).min(1, initial=np.inf))
             upto = (valid & (kk <= first_term[:, None])).numpy()
             fpn = f_pad.detach().numpy()
             tn = (T * om).detach().numpy()

@@ -54,7 +54,7 @@ class LossWeights(C.Structure):
 
 class HParams(C.Structure):
     _fields_ = [("lr_pos", C.c_float), ("lr_sh0", C.c_float), ("lr_shrest", C.c_float), ("lr_scale", C.c_float),
-                ("lr_rot", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float), ("eps", C.c_float)]
+                ("lr_rot", C.c_float), ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double)]
 
 
 class AddParams(C.Structure):

@@ -16,6 +16,31 @@
 namespace rtgs {
 
 constexpr int kBatchB = 256;
+
+// Transpose-reduce of 8 values over a warp in 9 shuffles (instead of 8 x 5): after the call, lane l
+// holds the warp sum of value j = 4*bit4(l) + 2*bit3(l) + bit2(l), identical on the 4 lanes l^{0..3}.
+__device__ __forceinline__ float warp_reduce8(const float v[8], int lane, int& j) {
+  const bool b16 = lane & 16, b8 = lane & 8, b4 = lane & 4;
+  float u[4], w2[2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float send = b16 ? v[i] : v[i + 4];
+    const float keep = b16 ? v[i + 4] : v[i];
+    u[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const float send = b8 ? u[i] : u[i + 2];
+    const float keep = b8 ? u[i + 2] : u[i];
+    w2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  const float send = b4 ? w2[0] : w2[1];
+  float x = (b4 ? w2[1] : w2[0]) + __shfl_xor_sync(0xffffffffu, send, 4);
+  x += __shfl_xor_sync(0xffffffffu, x, 2);
+  x += __shfl_xor_sync(0xffffffffu, x, 1);
+  j = (b16 ? 4 : 0) + (b8 ? 2 : 0) + (b4 ? 1 : 0);
+  return x;
+}
 constexpr int kSG = 16;  // screen-space gradient floats per slot
 
 // workspace: sgrad [n_slots][16] | acc [4] floats: sum|dC|, sum|dD| over P_d, |P_d|, spare
@@ -205,15 +230,10 @@ __global__ void __launch_bounds__(256) k_render_bwd(const BwdArgs a) {
           }
         }
         if (slot >= 0 && __any_sync(0xffffffffu, contrib)) {
-          g_mx = warp_sum(g_mx); g_my = warp_sum(g_my);
-          g_A = warp_sum(g_A); g_B = warp_sum(g_B); g_C = warp_sum(g_C);
-          g_r = warp_sum(g_r); g_g = warp_sum(g_g); g_b = warp_sum(g_b);
-          if (lane == 0) {
-            float* sg = a.sgrad + (size_t)slot * kSG;
-            atomicAdd(sg + 0, g_mx); atomicAdd(sg + 1, g_my);
-            atomicAdd(sg + 2, g_A); atomicAdd(sg + 3, g_B); atomicAdd(sg + 4, g_C);
-            atomicAdd(sg + 5, g_r); atomicAdd(sg + 6, g_g); atomicAdd(sg + 7, g_b);
-          }
+          float v[8] = {g_mx, g_my, g_A, g_B, g_C, g_r, g_g, g_b};
+          int j;
+          const float x = warp_reduce8(v, lane, j);
+          if ((lane & 3) == 0) atomicAdd(a.sgrad + (size_t)slot * kSG + j, x);  // 8 lanes, 8 values
         }
       }
       wdone = __all_sync(0xffffffffu, done);
@@ -247,14 +267,16 @@ struct PBArgs {
   const uint32_t* counts;
 };
 
-__device__ __forceinline__ void sh_basis_grad(int K, float x, float y, float z, float* Y, float* dx, float* dy, float* dz) {
+template <int K>
+__device__ __forceinline__ void sh_basis_grad(float x, float y, float z, float* Y, float* dx, float* dy, float* dz) {
   const float C0 = 0.28209479177387814f, C1 = 0.4886025119029199f;
   const float C20 = 1.0925484305920792f, C21 = -1.0925484305920792f, C22 = 0.31539156525252005f,
               C23 = -1.0925484305920792f, C24 = 0.5462742152960396f;
   const float C30 = -0.5900435899266435f, C31 = 2.890611442640554f, C32 = -0.4570457994644658f,
               C33 = 0.3731763325901154f, C34 = -0.4570457994644658f, C35 = 1.445305721320277f,
               C36 = -0.5900435899266435f;
-  for (int k = 0; k < 16; ++k) { Y[k] = 0.f; dx[k] = 0.f; dy[k] = 0.f; dz[k] = 0.f; }
+#pragma unroll
+  for (int k = 0; k < K; ++k) { Y[k] = 0.f; dx[k] = 0.f; dy[k] = 0.f; dz[k] = 0.f; }
   Y[0] = C0;
   if (K > 1) {
     Y[1] = -C1 * y; dy[1] = -C1;
@@ -283,18 +305,9 @@ __device__ __forceinline__ void sh_basis_grad(int K, float x, float y, float z, 
   }
 }
 
-__global__ void __launch_bounds__(128) k_project_bwd(const PBArgs a) {
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s == 0) {  // loss values (device-side, no host sync)
-    const float nP = (float)max(1u, a.counts[1]);
-    const float Lc = a.acc[0] / (3.f * nP);
-    const float Ld = a.acc[1] / fmaxf(1.f, a.acc[2]);
-    a.loss_out[0] = Lc;
-    a.loss_out[1] = Ld;
-    a.loss_out[2] = a.w_c * Lc + a.w_d * Ld;
-    a.loss_out[3] = a.acc[2];
-  }
-  if (s >= a.n_slots) return;
+// chain rule for slot s; accumulates the D = 10 + 3K parameter gradients into gout (zeroed)
+template <int K>
+__device__ __forceinline__ void project_bwd_slot(const PBArgs& a, int s, float* gout) {
   const float* sg = a.sgrad + (size_t)s * kSG;
   const float4 g0 = *reinterpret_cast<const float4*>(sg);
   const float4 g1 = *reinterpret_cast<const float4*>(sg + 4);
@@ -307,7 +320,7 @@ __global__ void __launch_bounds__(128) k_project_bwd(const PBArgs a) {
   const float dDz = gz2 * dscale;
   if (dMx == 0.f && dMy == 0.f && dA == 0.f && dB == 0.f && dCc == 0.f && drgb[0] == 0.f && drgb[1] == 0.f &&
       drgb[2] == 0.f && dDa == 0.f && dDb0 == 0.f && dDb1 == 0.f && dDb2 == 0.f && dDz == 0.f)
-    return;
+    return;  // nothing reached this slot
   const int i = a.gid_of_slot[s];
   const float px = a.pos[3 * i], py = a.pos[3 * i + 1], pz = a.pos[3 * i + 2];
   const double X = fma(a.V[0], (double)px, fma(a.V[1], (double)py, fma(a.V[2], (double)pz, a.tp[0])));
@@ -386,7 +399,10 @@ __global__ void __launch_bounds__(128) k_project_bwd(const PBArgs a) {
   int k = 2;
   if (l[1] < l[k]) k = 1;
   if (l[0] < l[k]) k = 0;
-  const float nwx = R[0][k], nwy = R[1][k], nwz = R[2][k];
+  // (selects, not dynamic indexing: keeps R / GR in registers)
+  const float nwx = k == 0 ? R[0][0] : (k == 1 ? R[0][1] : R[0][2]);
+  const float nwy = k == 0 ? R[1][0] : (k == 1 ? R[1][1] : R[1][2]);
+  const float nwz = k == 0 ? R[2][0] : (k == 1 ? R[2][1] : R[2][2]);
   const float ncx = V[0] * nwx + V[1] * nwy + V[2] * nwz;
   const float ncy = V[3] * nwx + V[4] * nwy + V[5] * nwz;
   const float ncz = V[6] * nwx + V[7] * nwy + V[8] * nwz;
@@ -406,17 +422,18 @@ __global__ void __launch_bounds__(128) k_project_bwd(const PBArgs a) {
   const double vx = (double)px - a.campos[0], vy = (double)py - a.campos[1], vz = (double)pz - a.campos[2];
   const double vnorm = sqrt(vx * vx + vy * vy + vz * vz);
   const float dirx = (float)(vx / vnorm), diry = (float)(vy / vnorm), dirz = (float)(vz / vnorm);
-  float Yb[16], Yx[16], Yy[16], Yz[16];
-  sh_basis_grad(a.K, dirx, diry, dirz, Yb, Yx, Yy, Yz);
-  const float* shc = a.sh + (size_t)i * 3 * a.K;
-  float* gout = a.grad + (size_t)s * a.D;
+  float Yb[K], Yx[K], Yy[K], Yz[K];
+  sh_basis_grad<K>(dirx, diry, dirz, Yb, Yx, Yy, Yz);
+  const float* shc = a.sh + (size_t)i * 3 * K;
   float gd0 = 0.f, gd1 = 0.f, gd2 = 0.f;
   for (int ch = 0; ch < 3; ++ch) {
     float raw = 0.5f;
-    for (int kk = 0; kk < a.K; ++kk) raw += Yb[kk] * shc[3 * kk + ch];
+#pragma unroll
+    for (int kk = 0; kk < K; ++kk) raw += Yb[kk] * shc[3 * kk + ch];
     const float gch = raw >= 0.f ? drgb[ch] : 0.f;  // clamp at 0 (R17)
     if (gch == 0.f) continue;
-    for (int kk = 0; kk < a.K; ++kk) {
+#pragma unroll
+    for (int kk = 0; kk < K; ++kk) {
       gout[10 + 3 * kk + ch] += Yb[kk] * gch;
       const float c = shc[3 * kk + ch] * gch;
       gd0 += Yx[kk] * c;
@@ -443,7 +460,10 @@ __global__ void __launch_bounds__(128) k_project_bwd(const PBArgs a) {
   float GR[3][3];
   for (int r = 0; r < 3; ++r)
     for (int c = 0; c < 3; ++c) GR[r][c] = dM[r][c] * sc[c];
-  GR[0][k] += dnw0; GR[1][k] += dnw1; GR[2][k] += dnw2;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    if (c == k) { GR[0][c] += dnw0; GR[1][c] += dnw1; GR[2][c] += dnw2; }
+  }
   // rotation matrix of the unit quaternion
   const float gw = 2.f * (-qz * GR[0][1] + qy * GR[0][2] + qz * GR[1][0] - qx * GR[1][2] - qy * GR[2][0] + qx * GR[2][1]);
   const float gx = 2.f * (qy * GR[0][1] + qz * GR[0][2] + qy * GR[1][0] - 2.f * qx * GR[1][1] - qw * GR[1][2] +
@@ -458,6 +478,37 @@ __global__ void __launch_bounds__(128) k_project_bwd(const PBArgs a) {
   gout[7] += (gx - dot * qx) * qinv;
   gout[8] += (gy - dot * qy) * qinv;
   gout[9] += (gz - dot * qz) * qinv;
+}
+
+// One thread per slot; the 128 slot rows of the CTA are staged in shared memory (pitch D+1,
+// conflict-free) and added to the contiguous grad block with coalesced read-modify-writes.
+template <int K>
+__global__ void __launch_bounds__(128) k_project_bwd(const PBArgs a) {
+  constexpr int D = 10 + 3 * K, LD = D + 1;
+  __shared__ float s_out[128 * LD];
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s == 0) {  // loss values (device-side, no host sync)
+    const float nP = (float)max(1u, a.counts[1]);
+    const float Lc = a.acc[0] / (3.f * nP);
+    const float Ld = a.acc[1] / fmaxf(1.f, a.acc[2]);
+    a.loss_out[0] = Lc;
+    a.loss_out[1] = Ld;
+    a.loss_out[2] = a.w_c * Lc + a.w_d * Ld;
+    a.loss_out[3] = a.acc[2];
+  }
+  float* gout = s_out + threadIdx.x * LD;
+#pragma unroll
+  for (int j = 0; j < D; ++j) gout[j] = 0.f;
+  if (s < a.n_slots) project_bwd_slot<K>(a, s, gout);
+  __syncthreads();
+  const int s0 = blockIdx.x * blockDim.x;
+  const int ns = min((int)blockDim.x, a.n_slots - s0);
+  float* G = a.grad + (size_t)s0 * D;
+  for (int e = threadIdx.x; e < ns * D; e += blockDim.x) {
+    const int ls = e / D, j = e - ls * D;
+    const float v = s_out[ls * LD + j];
+    if (v != 0.f) G[e] += v;
+  }
 }
 
 cudaError_t launch_backward(const rtgs_gaussians& g, const rtgs_projected& proj, const rtgs_bins& bins,
@@ -508,7 +559,12 @@ cudaError_t launch_backward(const rtgs_gaussians& g, const rtgs_projected& proj,
   b.loss_out = loss_out;
   b.counts = fwd.counts;
   const int nb = n_slots > 0 ? (n_slots + 127) / 128 : 1;
-  k_project_bwd<<<nb, 128, 0, s>>>(b);
+  switch (b.K) {
+    case 1: k_project_bwd<1><<<nb, 128, 0, s>>>(b); break;
+    case 4: k_project_bwd<4><<<nb, 128, 0, s>>>(b); break;
+    case 9: k_project_bwd<9><<<nb, 128, 0, s>>>(b); break;
+    default: k_project_bwd<16><<<nb, 128, 0, s>>>(b); break;
+  }
   note_launch();
   return cudaGetLastError();
 }

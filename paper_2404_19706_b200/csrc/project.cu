@@ -29,34 +29,42 @@ struct ProjArgs {
   uint32_t* touched;
 };
 
-__device__ __forceinline__ float sh_eval(const float* c, int K, int ch, float x, float y, float z) {
+// coefficient (k, channel ch) of this thread's Gaussian in the transposed shared tile: c[(3k+ch)*kLd]
+constexpr int kLd = 129;  // kProjThreads + 1: conflict-free rows
+template <int K>
+__device__ __forceinline__ float sh_eval(const float* c, int ch, float x, float y, float z) {
   // 3DGS real basis (R2), constants restated from their closed forms sqrt((2l+1)/4pi ...)
+#define SHC(k) c[(3 * (k) + ch) * kLd]
   const float C0 = 0.28209479177387814f, C1 = 0.4886025119029199f;
-  float r = C0 * c[ch];
-  if (K > 1) r += -C1 * y * c[3 + ch] + C1 * z * c[6 + ch] - C1 * x * c[9 + ch];
+  float r = C0 * SHC(0);
+  if (K > 1) r += -C1 * y * SHC(1) + C1 * z * SHC(2) - C1 * x * SHC(3);
   if (K > 4) {
     const float xx = x * x, yy = y * y, zz = z * z;
-    r += 1.0925484305920792f * x * y * c[12 + ch] - 1.0925484305920792f * y * z * c[15 + ch] +
-         0.31539156525252005f * (2.f * zz - xx - yy) * c[18 + ch] - 1.0925484305920792f * x * z * c[21 + ch] +
-         0.5462742152960396f * (xx - yy) * c[24 + ch];
+    r += 1.0925484305920792f * x * y * SHC(4) - 1.0925484305920792f * y * z * SHC(5) +
+         0.31539156525252005f * (2.f * zz - xx - yy) * SHC(6) - 1.0925484305920792f * x * z * SHC(7) +
+         0.5462742152960396f * (xx - yy) * SHC(8);
     if (K > 9) {
-      r += -0.5900435899266435f * y * (3.f * xx - yy) * c[27 + ch] + 2.890611442640554f * x * y * z * c[30 + ch] -
-           0.4570457994644658f * y * (4.f * zz - xx - yy) * c[33 + ch] +
-           0.3731763325901154f * z * (2.f * zz - 3.f * xx - 3.f * yy) * c[36 + ch] -
-           0.4570457994644658f * x * (4.f * zz - xx - yy) * c[39 + ch] +
-           1.445305721320277f * z * (xx - yy) * c[42 + ch] - 0.5900435899266435f * x * (xx - 3.f * yy) * c[45 + ch];
+      r += -0.5900435899266435f * y * (3.f * xx - yy) * SHC(9) + 2.890611442640554f * x * y * z * SHC(10) -
+           0.4570457994644658f * y * (4.f * zz - xx - yy) * SHC(11) +
+           0.3731763325901154f * z * (2.f * zz - 3.f * xx - 3.f * yy) * SHC(12) -
+           0.4570457994644658f * x * (4.f * zz - xx - yy) * SHC(13) +
+           1.445305721320277f * z * (xx - yy) * SHC(14) - 0.5900435899266435f * x * (xx - 3.f * yy) * SHC(15);
     }
   }
+#undef SHC
   return r;
 }
 
+template <int K>
 __global__ void __launch_bounds__(kProjThreads) k_project(const ProjArgs a) {
-  extern __shared__ __align__(16) float s_sh[];  // [kProjThreads][3K]
+  // s_sh: [kProjThreads][3K] as copied (AoS), then s_t: [3K][kLd] transposed for conflict-free reads
+  extern __shared__ __align__(16) float s_sh[];
+  float* s_t = s_sh + kProjThreads * 3 * K;
   __shared__ uint64_t bar;
   const int tid = threadIdx.x;
   const int base = blockIdx.x * kProjThreads;
   const int cnt = min(kProjThreads, a.n - base);
-  const int shf = 3 * a.K;  // floats per Gaussian
+  constexpr int shf = 3 * K;  // floats per Gaussian
   const uint32_t bytes = (uint32_t)cnt * shf * 4u;
   const uint32_t bulk = bytes & ~15u;
   if (tid == 0) {
@@ -167,12 +175,18 @@ __global__ void __launch_bounds__(kProjThreads) k_project(const ProjArgs a) {
   }
   mbar_wait(&bar, 0);
   __syncthreads();  // trailing scalar loads of the tail block
+  // transpose AoS [g][j] -> [j][g] (row pitch kLd): reads consecutive, writes to distinct banks
+  for (int i = tid; i < cnt * shf; i += kProjThreads) {
+    const int g = i / shf, j = i - g * shf;
+    s_t[j * kLd + g] = s_sh[i];
+  }
+  __syncthreads();
   if (live) {
     if (vis) {
-      const float* c = s_sh + tid * shf;
-      r2.x = fmaxf(0.f, sh_eval(c, a.K, 0, dirx, diry, dirz) + 0.5f);
-      r2.y = fmaxf(0.f, sh_eval(c, a.K, 1, dirx, diry, dirz) + 0.5f);
-      r2.z = fmaxf(0.f, sh_eval(c, a.K, 2, dirx, diry, dirz) + 0.5f);
+      const float* c = s_t + tid;
+      r2.x = fmaxf(0.f, sh_eval<K>(c, 0, dirx, diry, dirz) + 0.5f);
+      r2.y = fmaxf(0.f, sh_eval<K>(c, 1, dirx, diry, dirz) + 0.5f);
+      r2.z = fmaxf(0.f, sh_eval<K>(c, 2, dirx, diry, dirz) + 0.5f);
     }
     float4* o = a.rec + (size_t)4 * i;
     o[0] = r0; o[1] = r1; o[2] = r2; o[3] = r3;
@@ -215,9 +229,20 @@ cudaError_t launch_project(const rtgs_gaussians& g, const PoseF& pose, const rtg
   a.zkey = out.zkey;
   a.rect = reinterpret_cast<uint2*>(out.rect);
   a.touched = out.tiles_touched;
-  const size_t smem = (size_t)kProjThreads * 3 * a.K * sizeof(float);
+  const size_t smem = (size_t)(kProjThreads + kLd) * 3 * a.K * sizeof(float);
   const int blocks = (g.n + kProjThreads - 1) / kProjThreads;
-  k_project<<<blocks, kProjThreads, smem, s>>>(a);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_project<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    cudaFuncSetAttribute(k_project<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    attr = true;
+  }
+  switch (a.K) {
+    case 1: k_project<1><<<blocks, kProjThreads, smem, s>>>(a); break;
+    case 4: k_project<4><<<blocks, kProjThreads, smem, s>>>(a); break;
+    case 9: k_project<9><<<blocks, kProjThreads, smem, s>>>(a); break;
+    default: k_project<16><<<blocks, kProjThreads, smem, s>>>(a); break;
+  }
   note_launch();
   return cudaGetLastError();
 }

@@ -1,12 +1,18 @@
-// sort.cu — A2: tile binning and the hand-written radix sort (O8, readings R7, R8, R15).
+// sort.cu — A2: tile binning with a hand-written per-tile LSD radix sort (O8, readings R7,
+// R8, R15).
 //
-//  1. k_bin_count    per Gaussian: #kept tiles its rect covers; block counts of Gaussians with >= 1
-//  2. scan           block offsets;            3. k_compact  stable compaction (key = z bits, val = gid)
-//  4. 4 x LSD radix passes on (z bits, gid), 8-bit digits  -> depth order, ties by gid (stability)
-//  5. k_gather_cnt + scan -> instance offsets in depth order; total I
-//  6. k_emit         (tile, gid) instances in depth order
-//  7. 2+ x LSD radix passes on the tile id (stable) -> (tile, z, gid) order;  8. k_tile_range
-// Device-side counts (m Gaussians, I instances) are read by the kernels, so nothing syncs.
+// B200 design: the C3 frame has ~1.5M instances over 3,225 tiles (~480 per tile), so instead of a
+// device-wide sort of 64-bit tile|depth keys (3DGS) every tile's list is sorted inside ONE CTA in
+// shared memory:
+//   1. k_tile_count   per Gaussian, per kept tile of its rect: atomicAdd(tile_count[t])
+//   2. k_tile_offsets one CTA: exclusive scan of the counts -> tile_range, n_instances
+//   3. k_emit         per Gaussian, per kept tile: slot = start[t] + atomicAdd(cursor[t]) and store
+//                     the 64-bit pair (zkey << 32 | gid)   (order inside a tile still arbitrary)
+//   4. k_tile_sort    one CTA per tile: key' = ((zkey - zmin) << gid_bits) | gid, stable LSD radix
+//                     sort with 8-bit digits (warp match_any ranking) on the bits that vary, in
+//                     shared memory (global-memory ping-pong for tiles above kSortCap), write gids.
+// The output is the unique (tile, zkey bits, gid) order, so it is deterministic and bit-exact with
+// the oracle although the emission order is not.
 #include "common.cuh"
 #include "internal.h"
 
@@ -15,15 +21,15 @@ namespace rtgs {
 constexpr int kScanThreads = 256;
 constexpr int kScanItems = 8;
 constexpr int kScanChunk = kScanThreads * kScanItems;  // 2048
-constexpr int kRadixThreads = 256;
-constexpr int kRadixItems = 16;
-constexpr int kRadixTile = kRadixThreads * kRadixItems;  // 4096 keys per CTA
-constexpr int kRadixWarps = kRadixThreads / 32;
+constexpr int kSortThreads = 256;
+constexpr int kSortWarps = kSortThreads / 32;
+constexpr int kSortCap = 2048;  // tile lists up to this length are sorted in shared memory
+constexpr int kRep = 8;         // replicated tile counters: spreads same-address atomics 8 ways
 
 static inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
 // ------------------------------------------------------------------------------------------------
-// generic exclusive scan (3 kernels: chunk sums, scan of sums in one CTA, down-sweep)
+// generic exclusive scan (3 kernels: chunk sums, scan of sums in one CTA, down-sweep); used by A7
 // ------------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(kScanThreads) k_scan_reduce(const uint32_t* __restrict__ in, size_t len,
                                                               uint32_t* __restrict__ sums) {
@@ -62,7 +68,6 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_down(const uint32_t* __re
                                                             const uint32_t* __restrict__ sums,
                                                             uint32_t* __restrict__ out) {
   __shared__ uint32_t sh[33];
-  // blocked arrangement: thread t owns items [t*8, t*8+8) of the chunk
   const size_t base = (size_t)blockIdx.x * kScanChunk + (size_t)threadIdx.x * kScanItems;
   uint32_t v[kScanItems];
   uint32_t s = 0;
@@ -97,128 +102,7 @@ cudaError_t launch_scan(const uint32_t* in, uint32_t* out, size_t len, uint32_t*
 }
 
 // ------------------------------------------------------------------------------------------------
-// LSD radix sort pass on (key, value) u32 pairs, count read from the device.
-// Stability: CTA b owns keys [b*4096, (b+1)*4096); warp w owns a contiguous 512-key run of it,
-// processed in 16 rounds of 32 lanes, so (warp, round, lane) order == input order.
-// ------------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(kRadixThreads) k_radix_hist(const uint32_t* __restrict__ keys,
-                                                              const uint32_t* __restrict__ count, int shift,
-                                                              int bits, uint32_t* __restrict__ hist, int nblocks) {
-  __shared__ uint32_t h[256];
-  const uint32_t n = *count;
-  const int ndig = 1 << bits;
-  for (int d = threadIdx.x; d < 256; d += blockDim.x) h[d] = 0;
-  __syncthreads();
-  const size_t base = (size_t)blockIdx.x * kRadixTile;
-  if (base < n) {
-    const uint32_t mask = (uint32_t)ndig - 1u;
-#pragma unroll 4
-    for (int k = 0; k < kRadixItems; ++k) {
-      const size_t i = base + (size_t)k * kRadixThreads + threadIdx.x;
-      if (i < n) atomicAdd(&h[(keys[i] >> shift) & mask], 1u);
-    }
-  }
-  __syncthreads();
-  for (int d = threadIdx.x; d < ndig; d += blockDim.x) hist[(size_t)d * nblocks + blockIdx.x] = h[d];
-}
-
-__global__ void __launch_bounds__(kRadixThreads) k_radix_scatter(const uint32_t* __restrict__ kin,
-                                                                 const uint32_t* __restrict__ vin,
-                                                                 uint32_t* __restrict__ kout,
-                                                                 uint32_t* __restrict__ vout,
-                                                                 const uint32_t* __restrict__ count, int shift,
-                                                                 int bits, const uint32_t* __restrict__ offs,
-                                                                 int nblocks) {
-  __shared__ uint32_t wcnt[kRadixWarps][256];
-  __shared__ uint32_t gbase[256];
-  const uint32_t n = *count;
-  const size_t base = (size_t)blockIdx.x * kRadixTile;
-  if (base >= n) return;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int ndig = 1 << bits;
-  const uint32_t mask = (uint32_t)ndig - 1u;
-  for (int d = threadIdx.x; d < kRadixWarps * 256; d += blockDim.x) (&wcnt[0][0])[d] = 0;
-  for (int d = threadIdx.x; d < ndig; d += blockDim.x) gbase[d] = offs[(size_t)d * nblocks + blockIdx.x];
-  __syncthreads();
-  const uint32_t lt = (1u << lane) - 1u;
-  uint32_t key[kRadixItems], val[kRadixItems], rank[kRadixItems];
-  const size_t wbase = base + (size_t)w * 32 * kRadixItems;
-#pragma unroll
-  for (int r = 0; r < kRadixItems; ++r) {
-    const size_t i = wbase + (size_t)r * 32 + lane;
-    const bool ok = i < n;
-    key[r] = ok ? kin[i] : 0u;
-    val[r] = ok ? vin[i] : 0u;
-    const uint32_t d = ok ? ((key[r] >> shift) & mask) : 0x1000u;
-    const uint32_t peers = __match_any_sync(0xffffffffu, d);
-    const uint32_t before = ok ? wcnt[w][d] : 0u;
-    rank[r] = ok ? (before + __popc(peers & lt)) : 0xFFFFFFFFu;
-    __syncwarp();
-    if (ok && (31 - __clz(peers)) == lane) wcnt[w][d] = before + __popc(peers);
-    __syncwarp();
-  }
-  __syncthreads();
-  // exclusive prefix over warps for each digit
-  for (int d = threadIdx.x; d < ndig; d += blockDim.x) {
-    uint32_t run = 0;
-#pragma unroll
-    for (int ww = 0; ww < kRadixWarps; ++ww) {
-      const uint32_t t = wcnt[ww][d];
-      wcnt[ww][d] = run;
-      run += t;
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int r = 0; r < kRadixItems; ++r) {
-    if (rank[r] != 0xFFFFFFFFu) {
-      const uint32_t d = (key[r] >> shift) & mask;
-      const uint32_t dst = gbase[d] + wcnt[w][d] + rank[r];
-      kout[dst] = key[r];
-      vout[dst] = val[r];
-    }
-  }
-}
-
-struct RadixWS {
-  uint32_t* hist;   // [256 * nblocks]
-  uint32_t* offs;   // [256 * nblocks]
-  void* scan_ws;
-};
-
-// sorts (k0, v0) in place on `bits` low-order key bits starting at bit 0 (`bits` <= 32), using
-// (k1, v1) as ping-pong; an even number of passes so the result lands back in (k0, v0).
-static cudaError_t radix_sort(uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1, const uint32_t* count,
-                              size_t max_n, int bits, const RadixWS& ws, cudaStream_t s) {
-  int passes = (bits + 7) / 8;
-  if (passes < 2) passes = 2;
-  if (passes & 1) passes += 1;
-  const int nblocks = (int)((max_n + kRadixTile - 1) / kRadixTile);
-  if (nblocks == 0) return cudaSuccess;
-  int shift = 0;
-  for (int p = 0; p < passes; ++p) {
-    const int remaining = passes - p;
-    const int bits_left = bits - shift;
-    int b = (bits_left + remaining - 1) / remaining;
-    if (b > 8) b = 8;
-    if (b < 0) b = 0;
-    const uint32_t* ki = (p & 1) ? k1 : k0;
-    const uint32_t* vi = (p & 1) ? v1 : v0;
-    uint32_t* ko = (p & 1) ? k0 : k1;
-    uint32_t* vo = (p & 1) ? v0 : v1;
-    k_radix_hist<<<nblocks, kRadixThreads, 0, s>>>(ki, count, shift, b, ws.hist, nblocks);
-    note_launch();
-    cudaError_t e = launch_scan(ws.hist, ws.offs, (size_t)(1 << b) * nblocks, nullptr, ws.scan_ws, s);
-    if (e != cudaSuccess) return e;
-    k_radix_scatter<<<nblocks, kRadixThreads, 0, s>>>(ki, vi, ko, vo, count, shift, b, ws.offs, nblocks);
-    note_launch();
-    shift += b;
-  }
-  return cudaGetLastError();
-}
-
-// ------------------------------------------------------------------------------------------------
-// binning kernels
+// binning
 // ------------------------------------------------------------------------------------------------
 __device__ __forceinline__ bool rect_tiles(uint2 r, int& tx0, int& ty0, int& tx1, int& ty1) {
   const int x0 = (int)(short)(r.x & 0xFFFF), y0 = (int)(short)(r.x >> 16);
@@ -228,131 +112,203 @@ __device__ __forceinline__ bool rect_tiles(uint2 r, int& tx0, int& ty0, int& tx1
   return true;
 }
 
-__global__ void __launch_bounds__(256) k_bin_count(const uint32_t* __restrict__ zkey, const uint2* __restrict__ rect,
-                                                   const uint8_t* __restrict__ keep, int n, int TX,
-                                                   uint32_t* __restrict__ cnt, uint32_t* __restrict__ blk) {
-  __shared__ uint32_t sh[33];
+__global__ void __launch_bounds__(256) k_tile_count(const uint32_t* __restrict__ zkey, const uint2* __restrict__ rect,
+                                                    const uint8_t* __restrict__ keep, int n, int TX, int T,
+                                                    uint32_t* __restrict__ cnt) {
   const int i = blockIdx.x * 256 + threadIdx.x;
-  uint32_t c = 0;
-  if (i < n && zkey[i] != 0xFFFFFFFFu) {
-    int tx0, ty0, tx1, ty1;
-    if (rect_tiles(rect[i], tx0, ty0, tx1, ty1)) {
-      if (!keep) {
-        c = (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
-      } else {
-        for (int ty = ty0; ty <= ty1; ++ty)
-          for (int tx = tx0; tx <= tx1; ++tx) c += keep[ty * TX + tx] ? 1u : 0u;
-      }
-    }
-  }
-  if (i < n) cnt[i] = c;
-  uint32_t tot;
-  block_excl_scan(c ? 1u : 0u, sh, &tot);
-  if (threadIdx.x == 0) blk[blockIdx.x] = tot;
-}
-
-__global__ void __launch_bounds__(256) k_compact(const uint32_t* __restrict__ zkey, const uint32_t* __restrict__ cnt,
-                                                 int n, const uint32_t* __restrict__ blk_off,
-                                                 uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
-  __shared__ uint32_t sh[33];
-  const int i = blockIdx.x * 256 + threadIdx.x;
-  const bool f = i < n && cnt[i] > 0;
-  uint32_t tot;
-  const uint32_t r = block_excl_scan(f ? 1u : 0u, sh, &tot);
-  if (f) {
-    const uint32_t p = blk_off[blockIdx.x] + r;
-    keys[p] = zkey[i];
-    vals[p] = (uint32_t)i;
-  }
-}
-
-__global__ void __launch_bounds__(256) k_gather_cnt(const uint32_t* __restrict__ vals, const uint32_t* __restrict__ cnt,
-                                                    const uint32_t* __restrict__ m_ptr, int n,
-                                                    uint32_t* __restrict__ cs) {
-  const int j = blockIdx.x * 256 + threadIdx.x;
-  if (j < n) cs[j] = (uint32_t)j < *m_ptr ? cnt[vals[j]] : 0u;
-}
-
-__global__ void __launch_bounds__(256) k_emit(const uint32_t* __restrict__ vals, const uint32_t* __restrict__ off,
-                                              const uint32_t* __restrict__ m_ptr, const uint2* __restrict__ rect,
-                                              const uint8_t* __restrict__ keep, int TX, uint32_t cap,
-                                              uint32_t* __restrict__ ikey, uint32_t* __restrict__ ival) {
-  const uint32_t j = blockIdx.x * 256 + threadIdx.x;
-  if (j >= *m_ptr) return;
-  const uint32_t g = vals[j];
-  uint32_t o = off[j];
+  cnt += (size_t)(blockIdx.x & (kRep - 1)) * T;
+  if (i >= n || zkey[i] == 0xFFFFFFFFu) return;
   int tx0, ty0, tx1, ty1;
-  if (!rect_tiles(rect[g], tx0, ty0, tx1, ty1)) return;
+  if (!rect_tiles(rect[i], tx0, ty0, tx1, ty1)) return;
+  for (int ty = ty0; ty <= ty1; ++ty)
+    for (int tx = tx0; tx <= tx1; ++tx) {
+      const int t = ty * TX + tx;
+      if (!keep || keep[t]) atomicAdd(&cnt[t], 1u);
+    }
+}
+
+// one CTA: tile_range[t] = [start, start + count) (clamped to the capacity), n_instances, and the
+// start of every counter replica inside its tile: start[r][t] = start(t) + sum_{r' < r} cnt[r'][t]
+__global__ void __launch_bounds__(1024) k_tile_offsets(const uint32_t* __restrict__ cnt, int T, uint32_t cap,
+                                                       uint32_t* __restrict__ start, uint2* __restrict__ range,
+                                                       uint32_t* __restrict__ n_inst) {
+  __shared__ uint32_t sh[33];
+  __shared__ uint32_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int b = 0; b < T; b += 1024) {
+    const int t = b + threadIdx.x;
+    uint32_t c = 0;
+    if (t < T)
+      for (int r = 0; r < kRep; ++r) c += cnt[(size_t)r * T + t];
+    uint32_t tot;
+    const uint32_t ex = block_excl_scan(c, sh, &tot) + carry;
+    if (t < T) {
+      uint32_t o = ex;
+      for (int r = 0; r < kRep; ++r) {
+        start[(size_t)r * T + t] = o;
+        o += cnt[(size_t)r * T + t];
+      }
+      const uint32_t s0 = ex < cap ? ex : cap;
+      const uint32_t e0 = ex + c < cap ? ex + c : cap;
+      range[t] = make_uint2(c ? s0 : 0u, c ? e0 : 0u);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *n_inst = carry;
+}
+
+__global__ void __launch_bounds__(256) k_emit(const uint32_t* __restrict__ zkey, const uint2* __restrict__ rect,
+                                              const uint8_t* __restrict__ keep, int n, int TX, int T,
+                                              const uint32_t* __restrict__ start, uint32_t* __restrict__ cursor,
+                                              uint32_t cap, unsigned long long* __restrict__ keys) {
+  const int i = blockIdx.x * 256 + threadIdx.x;
+  const size_t rep = (size_t)(blockIdx.x & (kRep - 1)) * T;  // same replica as k_tile_count
+  start += rep;
+  cursor += rep;
+  if (i >= n) return;
+  const uint32_t z = zkey[i];
+  if (z == 0xFFFFFFFFu) return;
+  int tx0, ty0, tx1, ty1;
+  if (!rect_tiles(rect[i], tx0, ty0, tx1, ty1)) return;
+  const unsigned long long k = ((unsigned long long)z << 32) | (uint32_t)i;
   for (int ty = ty0; ty <= ty1; ++ty)
     for (int tx = tx0; tx <= tx1; ++tx) {
       const int t = ty * TX + tx;
       if (keep && !keep[t]) continue;
-      if (o < cap) {
-        ikey[o] = (uint32_t)t;
-        ival[o] = g;
-      }
-      ++o;
+      const uint32_t pos = start[t] + atomicAdd(&cursor[t], 1u);
+      if (pos < cap) keys[pos] = k;
     }
 }
 
-__global__ void k_finalize_count(const uint32_t* __restrict__ total, uint32_t cap, uint32_t* __restrict__ n_inst,
-                                 uint32_t* __restrict__ n_live) {
-  const uint32_t I = *total;
-  *n_inst = I;
-  *n_live = I < cap ? I : cap;
+// Stable LSD radix sort of n 64-bit keys (8-bit digits over `nbits` low bits) by one CTA.
+// A/B/rank may live in shared or global memory; wcnt/dstart are shared.
+__device__ __forceinline__ void cta_radix_sort(unsigned long long* A, unsigned long long* B, uint32_t* rank, int n,
+                                               int nbits, uint32_t (*wcnt)[256], uint32_t* dstart,
+                                               uint32_t* scan_sh, unsigned long long** out) {
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const uint32_t lt = (1u << lane) - 1u;
+  const int run = ((n + kSortWarps * 32 - 1) / (kSortWarps * 32)) * 32;  // contiguous keys per warp
+  const int r0 = min(n, w * run), r1 = min(n, (w + 1) * run);
+  for (int shift = 0; shift < nbits; shift += 8) {
+    for (int d = tid; d < kSortWarps * 256; d += kSortThreads) (&wcnt[0][0])[d] = 0;
+    __syncthreads();
+    for (int base = r0; base < r1; base += 32) {
+      const int i = base + lane;
+      const bool ok = i < r1;
+      const uint32_t d = ok ? (uint32_t)((A[i] >> shift) & 0xFFu) : 0x1000u;
+      const uint32_t peers = __match_any_sync(0xffffffffu, d);
+      const uint32_t before = ok ? wcnt[w][d] : 0u;
+      if (ok) rank[i] = before + __popc(peers & lt);
+      __syncwarp();
+      if (ok && (31 - __clz(peers)) == lane) wcnt[w][d] = before + __popc(peers);
+      __syncwarp();
+    }
+    __syncthreads();
+    {  // per digit: prefix over warps, then exclusive scan over digits
+      const int d = tid;  // kSortThreads == 256 digits
+      uint32_t run_w = 0;
+#pragma unroll
+      for (int ww = 0; ww < kSortWarps; ++ww) {
+        const uint32_t c = wcnt[ww][d];
+        wcnt[ww][d] = run_w;
+        run_w += c;
+      }
+      uint32_t tot;
+      dstart[d] = block_excl_scan(run_w, scan_sh, &tot);
+    }
+    __syncthreads();
+    for (int i = tid; i < n; i += kSortThreads) {
+      const unsigned long long k = A[i];
+      const uint32_t d = (uint32_t)((k >> shift) & 0xFFu);
+      const int ww = i / run;
+      B[dstart[d] + wcnt[ww][d] + rank[i]] = k;
+    }
+    __syncthreads();
+    unsigned long long* t = A;
+    A = B;
+    B = t;
+  }
+  *out = A;
 }
 
-__global__ void __launch_bounds__(256) k_tile_range(const uint32_t* __restrict__ ikey, const uint32_t* __restrict__ n_live,
-                                                    uint2* __restrict__ range) {
-  const uint32_t i = blockIdx.x * 256 + threadIdx.x;
-  const uint32_t n = *n_live;
-  if (i >= n) return;
-  const uint32_t t = ikey[i];
-  if (i == 0 || ikey[i - 1] != t) range[t].x = i;
-  if (i == n - 1 || ikey[i + 1] != t) range[t].y = i + 1;
+__global__ void __launch_bounds__(kSortThreads) k_tile_sort(const uint2* __restrict__ range,
+                                                            unsigned long long* __restrict__ keys,
+                                                            unsigned long long* __restrict__ tmp,
+                                                            uint32_t* __restrict__ grank, int gid_bits,
+                                                            uint32_t* __restrict__ sorted_gid) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ uint32_t wcnt[kSortWarps][256];
+  __shared__ uint32_t dstart[256];
+  __shared__ uint32_t scan_sh[33];
+  __shared__ uint32_t s_zmin, s_zmax;
+  const uint2 rg = range[blockIdx.x];
+  const int n = (int)(rg.y - rg.x);
+  if (n <= 0) return;
+  const int tid = threadIdx.x;
+  unsigned long long* seg = keys + rg.x;
+  if (n == 1) {
+    if (tid == 0) sorted_gid[rg.x] = (uint32_t)(seg[0] & 0xFFFFFFFFull);
+    return;
+  }
+  const bool in_smem = n <= kSortCap;
+  unsigned long long* A = in_smem ? reinterpret_cast<unsigned long long*>(smem) : seg;
+  unsigned long long* B = in_smem ? A + kSortCap : tmp + rg.x;
+  uint32_t* rk = in_smem ? reinterpret_cast<uint32_t*>(A + 2 * kSortCap) : grank + rg.x;
+  if (tid == 0) { s_zmin = 0xFFFFFFFFu; s_zmax = 0u; }
+  __syncthreads();
+  uint32_t zmin = 0xFFFFFFFFu, zmax = 0u;
+  for (int i = tid; i < n; i += kSortThreads) {
+    const unsigned long long k = seg[i];
+    const uint32_t z = (uint32_t)(k >> 32);
+    zmin = min(zmin, z);
+    zmax = max(zmax, z);
+    if (in_smem) A[i] = k;
+  }
+  atomicMin(&s_zmin, zmin);
+  atomicMax(&s_zmax, zmax);
+  __syncthreads();
+  const uint32_t z0 = s_zmin;
+  const uint32_t zr = s_zmax - z0;
+  const int zbits = zr ? 32 - __clz(zr) : 0;
+  // compress: key' = ((z - zmin) << gid_bits) | gid  (order-preserving for (z, gid))
+  for (int i = tid; i < n; i += kSortThreads) {
+    const unsigned long long k = A[i];
+    const unsigned long long zz = (unsigned long long)((uint32_t)(k >> 32) - z0);
+    A[i] = (zz << gid_bits) | (k & 0xFFFFFFFFull);
+  }
+  __syncthreads();
+  unsigned long long* res;
+  cta_radix_sort(A, B, rk, n, zbits + gid_bits, wcnt, dstart, scan_sh, &res);
+  const unsigned long long gmask = (gid_bits >= 64) ? ~0ull : ((1ull << gid_bits) - 1ull);
+  for (int i = tid; i < n; i += kSortThreads) sorted_gid[rg.x + i] = (uint32_t)(res[i] & gmask);
 }
 
 // ------------------------------------------------------------------------------------------------
 struct BinWS {
-  uint32_t *cnt, *blk, *blk_off, *keys_a, *vals_a, *keys_b, *vals_b, *cs, *off, *ik_a, *ik_b, *iv_b;
-  uint32_t *m, *total, *n_live;
-  RadixWS rw;
-  void* scan_ws;
+  uint32_t *cnt, *start, *cursor, *grank;
+  unsigned long long *keys, *tmp;
 };
 
 static size_t carve(int n, const rtgs_camera& cam, uint32_t cap, BinWS* w, char* base) {
-  (void)cam;
+  (void)n;
   size_t o = 0;
   auto take = [&](size_t bytes) -> char* {
     char* p = base ? base + o : nullptr;
     o += align_up(bytes);
     return p;
   };
-  const size_t N = (size_t)(n > 0 ? n : 1);
-  const size_t nblk = (N + 255) / 256;
-  const size_t maxn = N > cap ? N : (size_t)cap;
-  const size_t rblocks = (maxn + kRadixTile - 1) / kRadixTile;
+  const CamK k = make_cam(cam);
+  const size_t T = (size_t)k.TX * k.TY;
   BinWS t;
-  t.cnt = (uint32_t*)take(N * 4);
-  t.blk = (uint32_t*)take(nblk * 4);
-  t.blk_off = (uint32_t*)take(nblk * 4);
-  t.keys_a = (uint32_t*)take(N * 4);
-  t.vals_a = (uint32_t*)take(N * 4);
-  t.keys_b = (uint32_t*)take(N * 4);
-  t.vals_b = (uint32_t*)take(N * 4);
-  t.cs = (uint32_t*)take(N * 4);
-  t.off = (uint32_t*)take(N * 4);
-  t.ik_a = (uint32_t*)take((size_t)cap * 4 + 4);
-  t.ik_b = (uint32_t*)take((size_t)cap * 4 + 4);
-  t.iv_b = (uint32_t*)take((size_t)cap * 4 + 4);
-  t.m = (uint32_t*)take(4);
-  t.total = (uint32_t*)take(4);
-  t.n_live = (uint32_t*)take(4);
-  t.rw.hist = (uint32_t*)take(256 * rblocks * 4);
-  t.rw.offs = (uint32_t*)take(256 * rblocks * 4);
-  const size_t scan_len = 256 * rblocks > maxn ? 256 * rblocks : maxn;
-  t.scan_ws = take(scan_workspace_size(scan_len));
-  t.rw.scan_ws = t.scan_ws;
+  t.cnt = (uint32_t*)take(kRep * T * 4);      // cnt and cursor adjacent: one memset clears both
+  t.cursor = (uint32_t*)take(kRep * T * 4);
+  t.start = (uint32_t*)take(kRep * T * 4);
+  t.keys = (unsigned long long*)take((size_t)cap * 8 + 8);
+  t.tmp = (unsigned long long*)take((size_t)cap * 8 + 8);
+  t.grank = (uint32_t*)take((size_t)cap * 4 + 4);
   if (w) *w = t;
   return o;
 }
@@ -367,35 +323,29 @@ cudaError_t launch_bin(const rtgs_projected& proj, int n, const rtgs_camera& cam
   const int T = k.TX * k.TY;
   BinWS w;
   carve(n, cam, out.capacity, &w, static_cast<char*>(ws));
-  cudaMemsetAsync(out.tile_range, 0, (size_t)T * 8, s);
-  if (n == 0) {
-    cudaMemsetAsync(out.n_instances, 0, 4, s);
-    return cudaGetLastError();
-  }
-  const int nblk = (n + 255) / 256;
+  cudaMemsetAsync(w.cnt, 0, (size_t)((char*)w.start - (char*)w.cnt), s);
   const uint2* rect = reinterpret_cast<const uint2*>(proj.rect);
-  k_bin_count<<<nblk, 256, 0, s>>>(proj.zkey, rect, keep, n, k.TX, w.cnt, w.blk);
+  const int nblk = (n + 255) / 256;
+  if (n > 0) {
+    k_tile_count<<<nblk, 256, 0, s>>>(proj.zkey, rect, keep, n, k.TX, T, w.cnt);
+    note_launch();
+  }
+  k_tile_offsets<<<1, 1024, 0, s>>>(w.cnt, T, out.capacity, w.start, reinterpret_cast<uint2*>(out.tile_range),
+                                    out.n_instances);
   note_launch();
-  cudaError_t e = launch_scan(w.blk, w.blk_off, nblk, w.m, w.scan_ws, s);
-  if (e) return e;
-  k_compact<<<nblk, 256, 0, s>>>(proj.zkey, w.cnt, n, w.blk_off, w.keys_a, w.vals_a);
-  note_launch();
-  e = radix_sort(w.keys_a, w.vals_a, w.keys_b, w.vals_b, w.m, (size_t)n, 32, w.rw, s);
-  if (e) return e;
-  k_gather_cnt<<<nblk, 256, 0, s>>>(w.vals_a, w.cnt, w.m, n, w.cs);
-  note_launch();
-  e = launch_scan(w.cs, w.off, (size_t)n, w.total, w.scan_ws, s);
-  if (e) return e;
-  k_finalize_count<<<1, 1, 0, s>>>(w.total, out.capacity, out.n_instances, w.n_live);
-  k_emit<<<nblk, 256, 0, s>>>(w.vals_a, w.off, w.m, rect, keep, k.TX, out.capacity, w.ik_a, out.sorted_gid);
-  note_launch(2);
-  int tbits = 0;
-  while ((1 << tbits) < T) ++tbits;
-  e = radix_sort(w.ik_a, out.sorted_gid, w.ik_b, w.iv_b, w.n_live, (size_t)out.capacity, tbits, w.rw, s);
-  if (e) return e;
-  const int iblk = (int)((out.capacity + 255) / 256);
-  if (iblk) {
-    k_tile_range<<<iblk, 256, 0, s>>>(w.ik_a, w.n_live, reinterpret_cast<uint2*>(out.tile_range));
+  if (n > 0) {
+    k_emit<<<nblk, 256, 0, s>>>(proj.zkey, rect, keep, n, k.TX, T, w.start, w.cursor, out.capacity, w.keys);
+    note_launch();
+    int gid_bits = 1;
+    while (gid_bits < 32 && (1u << gid_bits) < (uint32_t)n) ++gid_bits;
+    const size_t smem = (size_t)kSortCap * (8 + 8 + 4);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_tile_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = true;
+    }
+    k_tile_sort<<<T, kSortThreads, smem, s>>>(reinterpret_cast<const uint2*>(out.tile_range), w.keys, w.tmp, w.grank,
+                                              gid_bits, out.sorted_gid);
     note_launch();
   }
   return cudaGetLastError();

@@ -129,6 +129,15 @@ class RenderBuffers:
         bits = (words[:, None] >> torch.arange(32, device=words.device)) & 1
         return bits.reshape(-1)[: H * W].reshape(H, W).bool()
 
+    def active_set(self) -> torch.Tensor:
+        """P = M_unstable ∩ kept tiles as a bool [H, W] image (test / inspection helper)."""
+        H, W = self.trans.shape
+        TX = (W + 15) // 16
+        ys = torch.arange(H, device=self.tile_keep.device) // 16
+        xs = torch.arange(W, device=self.tile_keep.device) // 16
+        kept = self.tile_keep.bool()[(ys[:, None] * TX + xs[None, :])]
+        return self.active_mask() & kept
+
 
 # ---------------------------------------------------------------------------------------------
 # the six entry points (same names as the C ABI)
