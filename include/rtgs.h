@@ -74,7 +74,8 @@ typedef struct {
 /* Per-Gaussian projection (O1, Eq.2).  Written by rtgs_project_gaussians.
  *   rec [n][16] float32, 64 B per Gaussian:
  *     [0] mu_x hi  [1] mu_y hi  [2] mu_x lo  [3] mu_y lo      mu = hi + lo (double-float)
- *     [4] conic A  [5] conic B  [6] conic C  [7] alpha        Sigma2D^-1 = [[A,B],[B,C]]
+ *     [4] A'  [5] B'  [6] C'  [7] log2(alpha)   with Sigma2D^-1 = [[A,B],[B,C]] prescaled to base 2:
+ *         A' = -log2(e)/2 A, B' = -log2(e) B, C' = -log2(e)/2 C, so f = 2^(A'dx^2 + B'dx dy + C'dy^2 + log2 alpha)
  *     [8] r  [9] g  [10] b                                    colour from SH at the view direction (R2)
  *     [11] support half-extents (ex, ey) in pixels as two IEEE halves (low half = ex), rounded up
  *     [12..14] n_c (unit disc normal, camera frame)  [15] n_c . p_c   (disc plane, Eq.4, R10, R12)

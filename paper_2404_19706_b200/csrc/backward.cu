@@ -12,10 +12,11 @@
 //   oracle's autograd in tests/test_gpu_backward.py).
 #include "common.cuh"
 #include "internal.h"
+#include "tilepipe.cuh"
 
 namespace rtgs {
 
-constexpr int kBatchB = 256;
+constexpr int kSG = 16;  // screen-space gradient floats per slot
 
 // Transpose-reduce of 8 values over a warp in 9 shuffles (instead of 8 x 5): after the call, lane l
 // holds the warp sum of value j = 4*bit4(l) + 2*bit3(l) + bit2(l), identical on the 4 lanes l^{0..3}.
@@ -41,7 +42,6 @@ __device__ __forceinline__ float warp_reduce8(const float v[8], int lane, int& j
   j = (b16 ? 4 : 0) + (b8 ? 2 : 0) + (b4 ? 1 : 0);
   return x;
 }
-constexpr int kSG = 16;  // screen-space gradient floats per slot
 
 // workspace: sgrad [n_slots][16] | acc [4] floats: sum|dC|, sum|dD| over P_d, |P_d|, spare
 size_t backward_workspace_size(int n_slots) { return ((size_t)n_slots * kSG + 8) * sizeof(float) + 256; }
@@ -67,23 +67,33 @@ struct BwdArgs {
   float* acc;
 };
 
-__global__ void __launch_bounds__(256) k_render_bwd(const BwdArgs a) {
-  __shared__ __align__(16) float4 s_rec[2][kBatchB][3];
-  __shared__ int32_t s_slot[2][kBatchB];
-  __shared__ float s_red[3][8];
+struct BwdSmem {
+  PipeRing ring;
+  int32_t slot[kPipeStages][kPipeBatch];
+  float red[3][kConsumerWarps];
+  uint32_t last_max;
+};
+
+__global__ void __launch_bounds__(kPipeThreads) k_render_bwd(const BwdArgs a) {
+  __shared__ BwdSmem sm;  // static: stage addresses fold into immediates
+  PipeRing& r = sm.ring;
   if (blockIdx.x >= a.counts[0]) return;
   const int tile = (int)a.tile_list[blockIdx.x];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  pipe_init(r);
+  if (tid == 0) sm.last_max = 0;
+  const bool consumer = w < kConsumerWarps;
   const int tx = tile % a.cam.TX, ty = tile / a.cam.TX;
   const int wx0 = tx * kTile + (w & 1) * 8, wy0 = ty * kTile + (w >> 1) * 4;
   const int px = wx0 + (lane & 7), py = wy0 + (lane >> 3);
-  const bool inside = px < a.cam.W && py < a.cam.H;
+  const bool inside = consumer && px < a.cam.W && py < a.cam.H;
   const uint32_t lin = (uint32_t)py * (uint32_t)a.cam.W + (uint32_t)px;
   const bool want = inside && ((a.active[lin >> 5] >> (lin & 31u)) & 1u);
   const size_t HW = (size_t)a.cam.W * a.cam.H;
   const float fpx = (float)px, fpy = (float)py;
+  __syncthreads();
 
-  // per-pixel loss terms (R13, R14, R24)
+  // per-pixel loss terms (R13, R14, R24) and the depth gradient of the pixel's hit (Eq.4-5)
   float gCr = 0.f, gCg = 0.f, gCb = 0.f, Cr = 0.f, Cg = 0.f, Cb = 0.f;
   uint32_t last = 0;
   float l1c = 0.f, l1d = 0.f, nd = 0.f;
@@ -96,6 +106,7 @@ __global__ void __launch_bounds__(256) k_render_bwd(const BwdArgs a) {
     gCg = dg > 0.f ? invP : (dg < 0.f ? -invP : 0.f);
     gCb = db > 0.f ? invP : (db < 0.f ? -invP : 0.f);
     last = a.n_contrib[lin];
+    atomicMax(&sm.last_max, last);
     const int hit = a.index[lin];
     const float Dt = a.tdepth[lin];
     if (hit >= 0 && isfinite(Dt) && Dt > 0.f) {
@@ -125,122 +136,105 @@ __global__ void __launch_bounds__(256) k_render_bwd(const BwdArgs a) {
       }
     }
   }
-  // loss accumulation (block reduce, 3 atomics per CTA)
-  {
+  if (consumer) {  // loss sums: warp reduce, one atomic per value per CTA
     const float s0 = warp_sum(l1c), s1 = warp_sum(l1d), s2 = warp_sum(nd);
-    if (lane == 0) { s_red[0][w] = s0; s_red[1][w] = s1; s_red[2][w] = s2; }
-    __syncthreads();
-    if (tid < 3) {
-      float t = 0.f;
-      for (int k = 0; k < 8; ++k) t += s_red[tid][k];
-      atomicAdd(a.acc + tid, t);
-    }
+    if (lane == 0) { sm.red[0][w] = s0; sm.red[1][w] = s1; sm.red[2][w] = s2; }
+  }
+  __syncthreads();
+  if (tid < 3) {
+    float t = 0.f;
+    for (int k = 0; k < kConsumerWarps; ++k) t += sm.red[tid][k];
+    atomicAdd(a.acc + tid, t);
+  }
+  const uint2 rg = a.range[tile];
+  const int start = (int)rg.x;
+  const int end = min((int)rg.y, (int)sm.last_max);  // nothing past the last blended entry contributes
+  const int n = end - start;
+
+  if (!consumer) {
+    const int32_t* slot_of_gid = a.slot_of_gid;
+    auto extra = [&](int st, int j, uint32_t g) { cp_async4(&sm.slot[st][j], slot_of_gid + g); };
+    auto flush = [](int, int) {};
+    pipe_produce(r, a.rec, a.sorted_gid, start, end, extra, flush);
+    return;
   }
 
   bool done = !want;
   const float bx0 = (float)wx0, bx1 = (float)(wx0 + 7), by0 = (float)wy0, by1 = (float)(wy0 + 3);
-  const uint2 rg = a.range[tile];
-  const int start = (int)rg.x;
-  int end = (int)rg.y;
-  // nothing past the largest last-blended position of the CTA can contribute
-  {
-    __shared__ uint32_t s_last;
-    if (tid == 0) s_last = 0;
-    __syncthreads();
-    if (want) atomicMax(&s_last, last);
-    __syncthreads();
-    end = min(end, (int)s_last);
-  }
-  const int nb = end > start ? (end - start + kBatchB - 1) / kBatchB : 0;
+  const int nb = n > 0 ? (n + kPipeBatch - 1) / kPipeBatch : 0;
   float T = 1.f, ar = 0.f, ag = 0.f, ab = 0.f;
-
-  auto load = [&](int b, int buf) {
-    const int i = start + b * kBatchB + tid;
-    if (i < end) {
-      const uint32_t g = a.sorted_gid[i];
-      s_slot[buf][tid] = a.slot_of_gid[g];
-      const float4* src = a.rec + (size_t)4 * g;
-      cp_async16(&s_rec[buf][tid][0], src);
-      cp_async16(&s_rec[buf][tid][1], src + 1);
-      cp_async16(&s_rec[buf][tid][2], src + 2);
-    }
-    cp_async_commit();
-  };
-
-  if (nb > 0) load(0, 0);
+  bool wdone = __all_sync(0xffffffffu, done);
+  if (wdone && lane == 0) atomicSub(&r.alive, 1);
   for (int b = 0; b < nb; ++b) {
-    const int buf = b & 1;
-    if (b + 1 < nb) load(b + 1, buf ^ 1); else cp_async_commit();
-    cp_async_wait<1>();
-    if (__syncthreads_count(!done) == 0) break;
-    const int cnt = min(kBatchB, end - (start + b * kBatchB));
-    bool wdone = __all_sync(0xffffffffu, done);
-    for (int g0 = 0; g0 < cnt && !wdone; g0 += 32) {
-      const int j = g0 + lane;
-      bool ov = false;
-      if (j < cnt) {
-        const float4 r0 = s_rec[buf][j][0];
-        const float2 ext = unpack_ext(s_rec[buf][j][2].w);
-        ov = (r0.x + ext.x >= bx0) && (r0.x - ext.x <= bx1) && (r0.y + ext.y >= by0) && (r0.y - ext.y <= by1);
-      }
-      uint32_t m = __ballot_sync(0xffffffffu, ov);
-      while (m) {
-        const int k = __ffs(m) - 1;
-        m &= m - 1;
-        const int idx = g0 + k;
-        const int slot = s_slot[buf][idx];  // warp-uniform
-        const uint32_t pos = (uint32_t)(start + b * kBatchB + idx);
-        float g_mx = 0.f, g_my = 0.f, g_A = 0.f, g_B = 0.f, g_C = 0.f, g_r = 0.f, g_g = 0.f, g_b = 0.f;
-        bool contrib = false;
-        if (!done) {
-          if (pos >= last) {
-            done = true;
-          } else {
-            const float4 r0 = s_rec[buf][idx][0], r1 = s_rec[buf][idx][1];
-            PairEval e;
-            if (eval_pair(r0, r1, fpx, fpy, e)) {
-              const float test = __fmul_rn(T, __fsub_rn(1.f, e.f));
-              if (test < kTMin) {
-                done = true;
-              } else {
-                const float4 r2 = s_rec[buf][idx][2];
-                const float wgt = __fmul_rn(e.f, T);
-                ar = __fmaf_rn(r2.x, wgt, ar);
-                ag = __fmaf_rn(r2.y, wgt, ag);
-                ab = __fmaf_rn(r2.z, wgt, ab);
-                if (slot >= 0) {
-                  contrib = true;
-                  // S_i = sum_{j>i} c_j f_j T_j = C^ - prefix_i
-                  const float Sr = Cr - ar, Sg = Cg - ag, Sb = Cb - ab;
-                  const float inv1mf = 1.f / (1.f - e.f);
-                  g_r = gCr * wgt; g_g = gCg * wgt; g_b = gCb * wgt;
-                  const float dLdf = gCr * (r2.x * T - Sr * inv1mf) + gCg * (r2.y * T - Sg * inv1mf) +
-                                     gCb * (r2.z * T - Sb * inv1mf);
-                  // f = alpha e^power (the 0.99 cap passes no gradient when active, R17)
-                  const float dLdp = (e.fraw < kFMax) ? dLdf * e.f : 0.f;
-                  g_mx = -dLdp * (r1.x * e.dx + r1.y * e.dy);
-                  g_my = -dLdp * (r1.y * e.dx + r1.z * e.dy);
-                  g_A = -0.5f * dLdp * e.dx * e.dx;
-                  g_B = -dLdp * e.dx * e.dy;
-                  g_C = -0.5f * dLdp * e.dy * e.dy;
-                }
-                T = test;
-              }
+    const int st = b % kPipeStages;
+    mbar_wait(&r.full[st], (uint32_t)(b / kPipeStages) & 1u);
+    if (!wdone) {
+      const float4* srec = &r.rec[st][0][0];
+      const uint32_t pbase = (uint32_t)(start + b * kPipeBatch);
+      const int cnt = min(kPipeBatch, n - b * kPipeBatch);
+      for (int g0 = 0; g0 < cnt; g0 += 32) {
+        const int j = g0 + lane;
+        bool ov = false;
+        if (j < cnt) {
+          const float4 r0 = srec[3 * j];
+          const float2 ext = unpack_ext(srec[3 * j + 2].w);
+          ov = (r0.x + ext.x >= bx0) && (r0.x - ext.x <= bx1) && (r0.y + ext.y >= by0) && (r0.y - ext.y <= by1);
+        }
+        uint32_t m = __ballot_sync(0xffffffffu, ov);
+        while (m) {
+          const int idx = g0 + __ffs(m) - 1;
+          m &= m - 1;
+          const int slot = sm.slot[st][idx];  // warp-uniform
+          // branch-free replay of record idx (identical arithmetic and decisions to the forward)
+          const float4 r0 = srec[3 * idx], r1 = srec[3 * idx + 1], r2 = srec[3 * idx + 2];
+          const bool past = pbase + (uint32_t)idx >= last;  // beyond the last blended entry
+          done = done || past;
+          PairEval e;
+          bool ok = eval_pair(r0, r1, fpx, fpy, e) && !done;
+          const float test = __fmul_rn(T, __fsub_rn(1.f, e.f));
+          const bool term = ok && (test < kTMin);
+          done = done || term;
+          ok = ok && !term;
+          const float wgt = ok ? __fmul_rn(e.f, T) : 0.f;
+          ar = __fmaf_rn(r2.x, wgt, ar);
+          ag = __fmaf_rn(r2.y, wgt, ag);
+          ab = __fmaf_rn(r2.z, wgt, ab);
+          if (slot >= 0 && __any_sync(0xffffffffu, ok)) {
+            float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            if (ok) {
+              // S_i = sum_{j>i} c_j f_j T_j = C^ - prefix_i ;  dC/df_i = c_i T_i - S_i / (1 - f_i)
+              const float inv1mf = 1.f / (1.f - e.f);
+              const float dLdf = gCr * (r2.x * T - (Cr - ar) * inv1mf) + gCg * (r2.y * T - (Cg - ag) * inv1mf) +
+                                 gCb * (r2.z * T - (Cb - ab) * inv1mf);
+              // f = alpha e^power; the 0.99 cap passes no gradient when active (R17)
+              const float dLdp = (e.f < kFMax) ? dLdf * e.f : 0.f;
+              // power = p2 / log2(e): d power / d dx = (2 A' dx + B' dy) / log2(e) = -(A dx + B dy)
+              const float sc = dLdp * (1.f / kLog2e);
+              v[0] = sc * (2.f * r1.x * e.dx + r1.y * e.dy);  // d/d mu_x
+              v[1] = sc * (2.f * r1.z * e.dy + r1.y * e.dx);  // d/d mu_y
+              v[2] = -0.5f * dLdp * e.dx * e.dx;              // d/d A
+              v[3] = -dLdp * e.dx * e.dy;                     // d/d B
+              v[4] = -0.5f * dLdp * e.dy * e.dy;              // d/d C
+              v[5] = gCr * wgt;                               // d/d rgb
+              v[6] = gCg * wgt;
+              v[7] = gCb * wgt;
             }
+            int vj;
+            const float x = warp_reduce8(v, lane, vj);
+            if ((lane & 3) == 0) atomicAdd(a.sgrad + (size_t)slot * kSG + vj, x);  // 8 lanes, 8 values
           }
+          T = ok ? test : T;
         }
-        if (slot >= 0 && __any_sync(0xffffffffu, contrib)) {
-          float v[8] = {g_mx, g_my, g_A, g_B, g_C, g_r, g_g, g_b};
-          int j;
-          const float x = warp_reduce8(v, lane, j);
-          if ((lane & 3) == 0) atomicAdd(a.sgrad + (size_t)slot * kSG + j, x);  // 8 lanes, 8 values
+        if (__all_sync(0xffffffffu, done)) {
+          wdone = true;
+          if (lane == 0) atomicSub(&r.alive, 1);
+          break;
         }
       }
-      wdone = __all_sync(0xffffffffu, done);
     }
-    __syncthreads();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&r.empty[st]);
   }
-  cp_async_wait<0>();
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -424,7 +418,19 @@ __device__ __forceinline__ void project_bwd_slot(const PBArgs& a, int s, float* 
   const float dirx = (float)(vx / vnorm), diry = (float)(vy / vnorm), dirz = (float)(vz / vnorm);
   float Yb[K], Yx[K], Yy[K], Yz[K];
   sh_basis_grad<K>(dirx, diry, dirz, Yb, Yx, Yy, Yz);
-  const float* shc = a.sh + (size_t)i * 3 * K;
+  // the slot's SH row in registers, loaded with 16-byte vectors when the row is 16-byte aligned
+  float shc[3 * K];
+  if constexpr ((3 * K) % 4 == 0) {
+    const float4* s4 = reinterpret_cast<const float4*>(a.sh + (size_t)i * 3 * K);
+#pragma unroll
+    for (int q = 0; q < 3 * K / 4; ++q) {
+      const float4 t4 = s4[q];
+      shc[4 * q] = t4.x; shc[4 * q + 1] = t4.y; shc[4 * q + 2] = t4.z; shc[4 * q + 3] = t4.w;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < 3 * K; ++q) shc[q] = a.sh[(size_t)i * 3 * K + q];
+  }
   float gd0 = 0.f, gd1 = 0.f, gd2 = 0.f;
   for (int ch = 0; ch < 3; ++ch) {
     float raw = 0.5f;
@@ -535,7 +541,7 @@ cudaError_t launch_backward(const rtgs_gaussians& g, const rtgs_projected& proj,
   a.sgrad = sgrad;
   a.acc = acc;
   const int T = a.cam.TX * a.cam.TY;
-  k_render_bwd<<<T, 256, 0, s>>>(a);
+  k_render_bwd<<<T, kPipeThreads, 0, s>>>(a);
   note_launch();
   PBArgs b;
   b.pos = g.pos; b.log_scale = g.log_scale; b.rot = g.rot; b.sh = g.sh;

@@ -14,7 +14,7 @@ constexpr float kDeltaAlpha = 0.60653065971263342f;  // e^-0.5
 constexpr float kTMin = 1e-4f;                       // early termination (R7)
 constexpr float kFMin = 1.0f / 255.0f;               // R7
 constexpr float kFMax = 0.99f;                       // R7
-constexpr float kPowerMin = -4.5f;                   // 3 sigma (R7)
+constexpr float kPowerMin = -4.5f;                   // 3 sigma (R7), used as kP2Min below
 constexpr float kCos60 = 0.5f;                       // Eq.5 60 deg switch (R11)
 constexpr float kNear = 0.2f;                        // R6
 constexpr float kDilation = 0.3f;                    // R4
@@ -118,21 +118,43 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* sh, ui
 }
 
 // ---- the per-pair evaluation shared by the forward and the backward replay --------------------
-// Every operation is an explicitly rounded intrinsic, so both kernels take bit-identical decisions
-// (same T sequence, same termination, same hit) whatever the compiler does elsewhere.
-//   a = (mu_x hi, mu_y hi, mu_x lo, mu_y lo), b = (A, B, C, alpha)
-//   d = mu - u (double-float mu: the hi part minus the integer pixel centre is exact)
+// Record layout (include/rtgs.h): a = (mu_x hi, mu_y hi, mu_x lo, mu_y lo),
+// b = (A', B', C', log2 alpha) with the conic prescaled to base 2: A' = -log2(e)/2 A, B' = -log2(e) B,
+// C' = -log2(e)/2 C, so that p2 = A' dx^2 + B' dx dy + C' dy^2 = power * log2(e) and
+// f = min(0.99, 2^(p2 + log2 alpha)) = min(0.99, alpha e^power) (Eq.2).
+// Support test (R7): power >= -4.5  <=>  p2 >= -4.5 log2(e);  f >= 1/255  <=>  p2 + log2 alpha >= log2(1/255).
+// Every operation is an explicitly rounded intrinsic so the forward and the backward replay take
+// bit-identical decisions (same T sequence, termination and hit) whatever the compiler schedules.
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kP2Min = -4.5f * 1.4426950408889634f;   // -4.5 log2(e)
+constexpr float kLog2FMin = -7.9943534368588578f;       // log2(1/255)
 struct PairEval {
-  float dx, dy, power, fraw, f;
+  float dx, dy, p2, e, f;
 };
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ bool eval_pair(const float4 a, const float4 b, float px, float py, PairEval& e) {
-  e.dx = __fadd_rn(__fsub_rn(a.x, px), a.z);
+  e.dx = __fadd_rn(__fsub_rn(a.x, px), a.z);  // (mu_hi - u) is exact; + lo
   e.dy = __fadd_rn(__fsub_rn(a.y, py), a.w);
-  const float q = __fmaf_rn(__fmul_rn(b.x, e.dx), e.dx, __fmul_rn(__fmul_rn(b.z, e.dy), e.dy));  // A dx^2 + C dy^2
-  e.power = __fmaf_rn(-0.5f, q, -__fmul_rn(__fmul_rn(b.y, e.dx), e.dy));
-  e.fraw = __fmul_rn(b.w, __expf(e.power));
-  e.f = fminf(kFMax, e.fraw);
-  return (e.power >= kPowerMin) && (e.f >= kFMin);
+  const float u = __fmaf_rn(b.x, e.dx, __fmul_rn(b.y, e.dy));             // A' dx + B' dy
+  e.p2 = __fmaf_rn(e.dx, u, __fmul_rn(__fmul_rn(b.z, e.dy), e.dy));        // + C' dy^2
+  e.e = __fadd_rn(e.p2, b.w);
+  e.f = fminf(kFMax, ex2_approx(e.e));
+  return (e.p2 >= kP2Min) && (e.e >= kLog2FMin);
+}
+
+// mbarrier arrive / cp.async-tracked arrive (for the render pipelines)
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(smem)), "l"(gmem));
 }
 
 __device__ __forceinline__ float2 unpack_ext(float w) {

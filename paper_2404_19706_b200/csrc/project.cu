@@ -163,7 +163,8 @@ __global__ void __launch_bounds__(kProjThreads) k_project(const ProjArgs a) {
         const double ndp = (double)ncx * X + (double)ncy * Y + (double)ncz * Z;
         const unsigned short hx = __half_as_ushort(__float2half_ru(ex)), hy = __half_as_ushort(__float2half_ru(ey));
         r0 = make_float4(mxh, myh, mxl, myl);
-        r1 = make_float4(A, B, C, alpha);
+        // conic prescaled to base 2 and log2(alpha): f = 2^(A'dx^2 + B'dxdy + C'dy^2 + log2 alpha)
+        r1 = make_float4(-0.5f * kLog2e * A, -kLog2e * B, -0.5f * kLog2e * C, log2f(alpha));
         r2.w = __uint_as_float((uint32_t)hx | ((uint32_t)hy << 16));
         r3 = make_float4(ncx, ncy, ncz, (float)ndp);
         // viewing direction camera centre -> Gaussian (world frame)

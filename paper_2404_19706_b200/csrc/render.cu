@@ -2,17 +2,16 @@
 //             A3/A4 forward colour/transmission blending with the opaque-disc depth (O2/O3;
 //             Eq.1-5, R7-R12).
 //
-// Forward: one CTA per (kept) 16x16 tile, 8 warps, warp w owns an 8x4 pixel block, one pixel per
-// lane.  Gaussian records of the tile's depth-sorted list are staged in 256-entry batches into
-// double-buffered shared memory with cp.async; each warp culls a batch 32 records at a time against
+// Forward: one CTA per (kept) 16x16 tile = 8 consumer warps (warp w owns an 8x4 pixel block, one
+// pixel per lane) + 1 producer warp streaming the tile's depth-sorted records through a 4-stage
+// shared-memory ring (tilepipe.cuh).  Each consumer warp culls a batch 32 records at a time against
 // its 8x4 block (ballot over the records' support boxes) and only walks the survivors.  Pixels stop
-// at T (1 - f) < 1e-4; warps stop when all their lanes stopped; the CTA stops when all warps did.
+// at T (1 - f) < 1e-4; warps stop when all their lanes stopped; the producer stops when all did.
 #include "common.cuh"
 #include "internal.h"
+#include "tilepipe.cuh"
 
 namespace rtgs {
-
-constexpr int kBatch = 256;
 
 // ------------------------------------------------------------------------------------------------
 // A0: coverage by splatting the unstable Gaussians (existence test, no order needed, R16)
@@ -93,9 +92,8 @@ struct FwdArgs {
 };
 
 template <bool MASKED>
-__global__ void __launch_bounds__(256) k_render_fwd(const FwdArgs a) {
-  __shared__ __align__(16) float4 s_rec[2][kBatch][3];
-  __shared__ uint32_t s_gid[2][kBatch];
+__global__ void __launch_bounds__(kPipeThreads) k_render_fwd(const FwdArgs a) {
+  __shared__ PipeRing r;  // static: stage addresses fold into immediates
   int tile;
   if (MASKED) {
     if (blockIdx.x >= a.counts[0]) return;
@@ -103,7 +101,15 @@ __global__ void __launch_bounds__(256) k_render_fwd(const FwdArgs a) {
   } else {
     tile = blockIdx.x;
   }
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  pipe_init(r);
+  __syncthreads();
+  const uint2 rg = a.range[tile];
+  const int start = (int)rg.x, end = (int)rg.y;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (w == kProducerWarp) {
+    pipe_produce(r, a.rec, a.sorted_gid, start, end, [](int, int, uint32_t) {}, [](int, int) {});
+    return;
+  }
   const int tx = tile % a.cam.TX, ty = tile / a.cam.TX;
   const int wx0 = tx * kTile + (w & 1) * 8, wy0 = ty * kTile + (w >> 1) * 4;
   const int px = wx0 + (lane & 7), py = wy0 + (lane >> 3);
@@ -114,69 +120,60 @@ __global__ void __launch_bounds__(256) k_render_fwd(const FwdArgs a) {
   bool done = !want;
   const float fpx = (float)px, fpy = (float)py;
   const float bx0 = (float)wx0, bx1 = (float)(wx0 + 7), by0 = (float)wy0, by1 = (float)(wy0 + 3);
-
-  const uint2 rg = a.range[tile];
-  const int start = (int)rg.x, end = (int)rg.y;
-  const int nb = (end - start + kBatch - 1) / kBatch;
+  const int n = end - start;
+  const int nb = n > 0 ? (n + kPipeBatch - 1) / kPipeBatch : 0;
 
   float T = 1.f, cr = 0.f, cg = 0.f, cb = 0.f;
   int hit = -1;
   uint32_t last = (uint32_t)start;
-
-  auto load = [&](int b, int buf) {
-    const int i = start + b * kBatch + tid;
-    if (i < end) {
-      const uint32_t g = a.sorted_gid[i];
-      s_gid[buf][tid] = g;
-      const float4* src = a.rec + (size_t)4 * g;
-      cp_async16(&s_rec[buf][tid][0], src);
-      cp_async16(&s_rec[buf][tid][1], src + 1);
-      cp_async16(&s_rec[buf][tid][2], src + 2);
-    }
-    cp_async_commit();
-  };
-
-  if (nb > 0) load(0, 0);
+  bool wdone = __all_sync(0xffffffffu, done);
+  if (wdone && lane == 0) atomicSub(&r.alive, 1);
   for (int b = 0; b < nb; ++b) {
-    const int buf = b & 1;
-    if (b + 1 < nb) load(b + 1, buf ^ 1); else cp_async_commit();
-    cp_async_wait<1>();
-    if (__syncthreads_count(!done) == 0) break;
-    const int cnt = min(kBatch, end - (start + b * kBatch));
-    bool wdone = __all_sync(0xffffffffu, done);
-    for (int g0 = 0; g0 < cnt && !wdone; g0 += 32) {
-      const int j = g0 + lane;
-      bool ov = false;
-      if (j < cnt) {
-        const float4 r0 = s_rec[buf][j][0];
-        const float2 ext = unpack_ext(s_rec[buf][j][2].w);
-        ov = (r0.x + ext.x >= bx0) && (r0.x - ext.x <= bx1) && (r0.y + ext.y >= by0) && (r0.y - ext.y <= by1);
+    const int st = b % kPipeStages;
+    mbar_wait(&r.full[st], (uint32_t)(b / kPipeStages) & 1u);
+    if (!wdone) {
+      const float4* srec = &r.rec[st][0][0];
+      const uint32_t* sgid = r.gid[st];
+      const uint32_t pbase = (uint32_t)(start + b * kPipeBatch + 1);
+      const int cnt = min(kPipeBatch, n - b * kPipeBatch);
+      for (int g0 = 0; g0 < cnt; g0 += 32) {
+        const int j = g0 + lane;
+        bool ov = false;
+        if (j < cnt) {
+          const float4 r0 = srec[3 * j];
+          const float2 ext = unpack_ext(srec[3 * j + 2].w);
+          ov = (r0.x + ext.x >= bx0) && (r0.x - ext.x <= bx1) && (r0.y + ext.y >= by0) && (r0.y - ext.y <= by1);
+        }
+        uint32_t m = __ballot_sync(0xffffffffu, ov);
+        while (m) {
+          const int idx = g0 + __ffs(m) - 1;
+          m &= m - 1;
+          // branch-free body: every lane evaluates, the blend is predicated
+          const float4 r0 = srec[3 * idx], r1 = srec[3 * idx + 1], r2 = srec[3 * idx + 2];
+          PairEval e;
+          bool ok = eval_pair(r0, r1, fpx, fpy, e) && !done;
+          if (ok && hit < 0 && e.f > kDeltaAlpha) hit = (int)sgid[idx];  // R9: before termination
+          const float test = __fmul_rn(T, __fsub_rn(1.f, e.f));
+          const bool term = ok && (test < kTMin);
+          done = done || term;
+          ok = ok && !term;
+          const float wgt = ok ? __fmul_rn(e.f, T) : 0.f;
+          cr = __fmaf_rn(r2.x, wgt, cr);
+          cg = __fmaf_rn(r2.y, wgt, cg);
+          cb = __fmaf_rn(r2.z, wgt, cb);
+          T = ok ? test : T;
+          last = ok ? pbase + (uint32_t)idx : last;
+        }
+        if (__all_sync(0xffffffffu, done)) {
+          wdone = true;
+          if (lane == 0) atomicSub(&r.alive, 1);
+          break;
+        }
       }
-      uint32_t m = __ballot_sync(0xffffffffu, ov);
-      while (m) {
-        const int k = __ffs(m) - 1;
-        m &= m - 1;
-        if (done) continue;
-        const int idx = g0 + k;
-        const float4 r0 = s_rec[buf][idx][0], r1 = s_rec[buf][idx][1];
-        PairEval e;
-        if (!eval_pair(r0, r1, fpx, fpy, e)) continue;
-        if (hit < 0 && e.f > kDeltaAlpha) hit = (int)s_gid[buf][idx];  // R9: before termination
-        const float test = __fmul_rn(T, __fsub_rn(1.f, e.f));
-        if (test < kTMin) { done = true; continue; }
-        const float4 r2 = s_rec[buf][idx][2];
-        const float wgt = __fmul_rn(e.f, T);
-        cr = __fmaf_rn(r2.x, wgt, cr);
-        cg = __fmaf_rn(r2.y, wgt, cg);
-        cb = __fmaf_rn(r2.z, wgt, cb);
-        T = test;
-        last = (uint32_t)(start + b * kBatch + idx + 1);
-      }
-      wdone = __all_sync(0xffffffffu, done);
     }
-    __syncthreads();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&r.empty[st]);
   }
-  cp_async_wait<0>();
 
   if (!want) return;
   const size_t HW = (size_t)a.cam.W * a.cam.H;
@@ -240,8 +237,8 @@ cudaError_t launch_render(const rtgs_projected& proj, const rtgs_bins& bins, con
   a.color = out.color; a.trans = out.trans; a.depth = out.depth; a.normal = out.normal;
   a.index = out.index; a.n_contrib = out.n_contrib;
   const int T = a.cam.TX * a.cam.TY;
-  if (masked) k_render_fwd<true><<<T, 256, 0, s>>>(a);
-  else k_render_fwd<false><<<T, 256, 0, s>>>(a);
+  if (masked) k_render_fwd<true><<<T, kPipeThreads, 0, s>>>(a);
+  else k_render_fwd<false><<<T, kPipeThreads, 0, s>>>(a);
   note_launch();
   return cudaGetLastError();
 }

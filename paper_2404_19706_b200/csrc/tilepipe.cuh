@@ -1,0 +1,80 @@
+// tilepipe.cuh — warp-specialised producer/consumer pipeline over one tile's depth-sorted list,
+// shared by the forward render (A3/A4) and the backward replay (A5).
+//
+// CTA = 8 consumer warps (one 8x4 pixel block each, one pixel per lane) + 1 producer warp.
+// The producer streams the tile's records in batches of kPipeBatch through a kPipeStages-deep ring
+// in shared memory with cp.async (LDGSTS) and signals each stage on a `full` mbarrier
+// (cp.async.mbarrier.arrive.noinc: the arrival fires when the lane's copies have landed).  Every
+// consumer warp releases a stage on its `empty` mbarrier when it is done with it, so consumer
+// warps never wait for each other (no __syncthreads in the main loop): a warp can run up to
+// kPipeStages batches ahead of the slowest one.  When every consumer warp has terminated, the
+// producer stops copying and only signals, and the CTA drains.
+#pragma once
+#include "common.cuh"
+
+namespace rtgs {
+
+constexpr int kPipeStages = 4;
+constexpr int kPipeBatch = 128;
+constexpr int kConsumerWarps = 8;
+constexpr int kPipeThreads = 32 * (kConsumerWarps + 1);
+constexpr int kProducerWarp = kConsumerWarps;
+
+struct PipeRing {
+  float4 rec[kPipeStages][kPipeBatch][3];  // first 48 B of each record: mu hi/lo, conic', log2 alpha, rgb, ext
+  uint32_t gid[kPipeStages][kPipeBatch];
+  uint64_t full[kPipeStages];
+  uint64_t empty[kPipeStages];
+  int alive;                                // consumer warps not yet terminated
+};
+
+__device__ __forceinline__ void pipe_init(PipeRing& r) {
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kPipeStages; ++s) {
+      mbar_init(&r.full[s], 32);
+      mbar_init(&r.empty[s], kConsumerWarps);
+    }
+    r.alive = kConsumerWarps;
+    fence_mbar_init();
+  }
+}
+
+// producer: one lane per record slot; `extra(stage, j, gid, src_index)` may issue more cp.async.
+template <typename Extra, typename Flush>
+__device__ __forceinline__ void pipe_produce(PipeRing& r, const float4* __restrict__ rec,
+                                             const uint32_t* __restrict__ sorted_gid, int start, int end,
+                                             Extra extra, Flush flush) {
+  const int lane = threadIdx.x & 31;
+  const int n = end - start;
+  const int nb = n > 0 ? (n + kPipeBatch - 1) / kPipeBatch : 0;
+  for (int b = 0; b < nb; ++b) {
+    const int st = b % kPipeStages;
+    const uint32_t ph = (uint32_t)(b / kPipeStages) & 1u;
+    if (b >= kPipeStages) {
+      mbar_wait(&r.empty[st], ph ^ 1u);
+      flush(st, b - kPipeStages);
+    }
+    if (*((volatile int*)&r.alive) > 0) {
+      const int cnt = min(kPipeBatch, n - b * kPipeBatch);
+      for (int j = lane; j < cnt; j += 32) {
+        const int i = start + b * kPipeBatch + j;
+        const uint32_t g = sorted_gid[i];
+        cp_async4(&r.gid[st][j], sorted_gid + i);
+        const float4* src = rec + (size_t)4 * g;
+        cp_async16(&r.rec[st][j][0], src);
+        cp_async16(&r.rec[st][j][1], src + 1);
+        cp_async16(&r.rec[st][j][2], src + 2);
+        extra(st, j, g);
+      }
+    }
+    cp_async_mbar_arrive(&r.full[st]);
+  }
+  // the last stages are flushed once every consumer warp has released them
+  for (int b = max(0, nb - kPipeStages); b < nb; ++b) {
+    const int st = b % kPipeStages;
+    mbar_wait(&r.empty[st], (uint32_t)(b / kPipeStages) & 1u);
+    flush(st, b);
+  }
+}
+
+}  // namespace rtgs

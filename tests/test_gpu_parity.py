@@ -53,8 +53,10 @@ def test_project_parity(api, name):
     assert np.abs(mu - o["mu"].numpy()[v]).max() < 1e-5
     con = o["conic"].numpy()[v]
     scale = np.abs(con).max(1, keepdims=True)
-    assert (np.abs(rec[v, 4:7] - con) <= 1e-4 * np.maximum(np.abs(con), scale)).all()
-    assert np.array_equal(rec[v, 7], scene["opacity"][v].astype(np.float64))
+    # record stores the conic prescaled to base 2: (A', B', C') = -log2(e) (A/2, B, C/2)
+    gcon = rec[v, 4:7] / (-np.log2(np.e) * np.array([0.5, 1.0, 0.5]))
+    assert (np.abs(gcon - con) <= 1e-4 * np.maximum(np.abs(con), scale)).all()
+    np.testing.assert_allclose(2.0 ** rec[v, 7], scene["opacity"][v].astype(np.float64), rtol=1e-6)
     assert rel_close(rec[v, 8:11], o["rgb"].numpy()[v], 1e-4, 1e-2).all()
     assert np.abs(rec[v, 12:15] - o["n_c"].numpy()[v]).max() < 1e-5
     assert rel_close(rec[v, 15], o["plane_d"].numpy()[v], 1e-4, 1.0).all()
