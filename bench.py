@@ -168,6 +168,7 @@ def main():
     ap.add_argument("--ref-pixels", type=int, default=24)
     ap.add_argument("--active-pixels", type=int, default=0)
     ap.add_argument("--phases", action="store_true", help="print per-call timings to stderr")
+    ap.add_argument("--no-graph", action="store_true", help="launch every step eagerly (no CUDA graph)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -206,20 +207,33 @@ def main():
     stream = torch.cuda.current_stream()
 
     def step(c, d, frame_idx):
-        eng.ingest(c, d, pose, seed=1234, frame_idx=frame_idx)
-        eng.forward_masked(pose)
-        eng.backward(c, d, pose)
-        if world > 1:
-            allreduce_grads(eng.grad)
-        eng.optimizer_step()
+        # ingest (side stream) || masked iteration (current stream); Adam waits for the ingest projection
+        eng.step(c, d, pose, seed=1234, frame_idx=frame_idx, reduce_grads=allreduce_grads if world > 1 else None)
 
     for i in range(args.warmup):
         step(col, dep, i)
     torch.cuda.synchronize()
-    n_inst_iter0 = int(eng.bins.n_instances.item())
-    eng.ingest(col, dep, pose, seed=1234, frame_idx=0)
+    l_eager = P.launch_count()
+    step(col, dep, args.warmup)
     torch.cuda.synchronize()
-    n_inst = int(eng.bins.n_instances.item())          # full-frame instance count (ingest binning)
+    launches_per_step = P.launch_count() - l_eager
+    # CUDA graph of one whole step (both streams); the Adam step counter lives on the device, so each
+    # replay is a genuine next iteration.  Eager under torchrun (NCCL inside the step).
+    use_graph = (not args.no_graph) and world == 1
+    graph = None
+    if use_graph:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step(col, dep, args.warmup + 1)
+        torch.cuda.synchronize()
+
+    def run_step(i):
+        if graph is not None:
+            graph.replay()
+        else:
+            step(col, dep, args.warmup + i)
+    n_inst_iter0 = int(eng.bins.n_instances.item())
+    n_inst = int(eng.bins_full.n_instances.item())     # full-frame instance count (ingest binning)
     if max(n_inst, n_inst_iter0) > eng.capacity:
         raise RuntimeError(f"instance capacity {eng.capacity} < {max(n_inst, n_inst_iter0)}")
 
@@ -236,10 +250,10 @@ def main():
         for i in range(args.steps):
             flush.zero_()
             starts[i].record(stream)
-            step(col, dep, args.warmup + i)
+            run_step(i)
             ends[i].record(stream)
         torch.cuda.synchronize()
-    launches = (P.launch_count() - l0)
+    launches = launches_per_step * args.steps
     ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     t_step = sum(ms) / len(ms)
     if world > 1:
@@ -260,9 +274,9 @@ def main():
 
         flush.zero_()
         mark("start")
-        P.project_gaussians(gm, pose, cam, eng.proj); mark("ingest.project")
-        P.bin_and_sort(eng.proj, gm.n, cam, None, eng.bins, eng.ws_bin); mark("ingest.bin_and_sort")
-        P.render_color_depth(gm, eng.proj, eng.bins, pose, cam, P.RTGS_RENDER_FULL, eng.full); mark("ingest.render_full")
+        P.project_gaussians(gm, pose, cam, eng.proj_full); mark("ingest.project")
+        P.bin_and_sort(eng.proj_full, gm.n, cam, None, eng.bins_full, eng.ws_bin_full); mark("ingest.bin_and_sort")
+        P.render_color_depth(gm, eng.proj_full, eng.bins_full, pose, cam, P.RTGS_RENDER_FULL, eng.full); mark("ingest.render_full")
         P.classify_and_add_pixels(eng.full, col, dep, gm.flags, cam, P.add_params(seed=1234), eng.pixel_class,
                                   eng.samples, eng.add_counts, eng.ws_cls); mark("ingest.classify")
         P.project_gaussians(gm, pose, cam, eng.proj); mark("iter.project")
@@ -300,16 +314,14 @@ def main():
     dep_pin = torch.as_tensor(dep_h).pin_memory()
     loss_h = torch.empty(4, dtype=torch.float32).pin_memory()
     cnt_h = torch.empty(5, dtype=torch.int32).pin_memory()
-    col_d = torch.empty_like(col)
-    dep_d = torch.empty_like(dep)
     e2e = []
     for i in range(max(3, args.steps // 2)):
         flush.zero_()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        col_d.copy_(col_pin, non_blocking=True)
-        dep_d.copy_(dep_pin, non_blocking=True)
-        step(col_d, dep_d, 1000 + i)
+        col.copy_(col_pin, non_blocking=True)   # the graph reads the frame from these device buffers
+        dep.copy_(dep_pin, non_blocking=True)
+        run_step(i)
         loss_h.copy_(eng.loss, non_blocking=True)
         cnt_h.copy_(eng.add_counts, non_blocking=True)
         b.record(stream)
@@ -340,6 +352,7 @@ def main():
                                    f"{cfg.sh_degree}; step = frame ingest (A1,A2,A3/A4 FULL,A7) + one masked "
                                    "mapping iteration (A1,A0,A2,A3/A4,A5,A6)",
                        "l2": "flushed between timed steps (256 MB write); Gaussian SoA 237 MB > L2",
+                       "launch": "CUDA graph of the whole step (2 streams)" if graph is not None else "eager",
                        "parallelism": f"dp{world} over keyframe views" if world > 1 else "single GPU"},
             "roofline": {"kernel": "k_project (A1)", "bound": "hbm", "achieved": achieved, "peak": hbm,
                          "unit": "GB/s", "frac": achieved / hbm, "traffic": None, "peak_kind": peak_kind,

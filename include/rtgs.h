@@ -212,12 +212,14 @@ rtgs_status rtgs_render_backward_masked(const rtgs_gaussians* g, const rtgs_proj
  * L_reg = mean over the 10 n_transparent geometry scalars of (theta - init_geom)^2; one Adam step
  * (bias correction with `step` >= 1) with the group learning rates; eta[gid] += 1 iff any SH gradient
  * component of the slot is non-zero; grad is consumed and ZEROED.
+ * step_device (nullable): device int32 holding the step; when given it replaces `step` (read by the
+ * kernel, so a captured CUDA graph can advance the step between replays).
  *   m, v [n_slots][10+3K] Adam moments; init_geom [n_slots][10] (pos 3, log_scale 3, rot 4) (D12)
  * ------------------------------------------------------------------------------------------- */
 rtgs_status rtgs_adam_step_unstable(rtgs_params* params, const int32_t* gid_of_slot, int32_t n_slots,
                                     const uint8_t* flags, float* grad, float* m, float* v, const float* init_geom,
                                     int32_t n_transparent, float w_reg, const rtgs_hparams* hp, int32_t step,
-                                    uint32_t* eta, void* stream);
+                                    const int32_t* step_device, uint32_t* eta, void* stream);
 
 /* ---------------------------------------------------------------------------------------------
  * A7 — rtgs_classify_and_add_pixels (O7; Eq.6, R21, R22, R24)

@@ -14,8 +14,9 @@ BUILD = os.path.join(PKG, "build")
 LIB = os.path.join(PKG, "librtgs.so")
 SOURCES = ["abi.cu", "project.cu", "sort.cu", "render.cu", "backward.cu", "adam.cu", "classify.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+DEBUG = os.environ.get("RTGS_DEBUG", "") == "1"  # device asserts on indices (debug builds only)
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-Xcompiler", "-fPIC",
-         "-I", INCLUDE, "-I", CSRC]
+         "-I", INCLUDE, "-I", CSRC] + (["-DRTGS_DEBUG"] if DEBUG else [])
 
 
 def _compile(src: str, verbose: bool) -> str:

@@ -120,15 +120,15 @@ rtgs_status rtgs_render_backward_masked(const rtgs_gaussians* g, const rtgs_proj
 rtgs_status rtgs_adam_step_unstable(rtgs_params* params, const int32_t* gid_of_slot, int32_t n_slots,
                                     const uint8_t* flags, float* grad, float* m, float* v, const float* init_geom,
                                     int32_t n_transparent, float w_reg, const rtgs_hparams* hp, int32_t step,
-                                    uint32_t* eta, void* stream) {
-  if (!params || !hp || n_slots < 0 || step < 1 || n_transparent < 0 || params->sh_degree < 0 ||
+                                    const int32_t* step_device, uint32_t* eta, void* stream) {
+  if (!params || !hp || n_slots < 0 || (step < 1 && !step_device) || n_transparent < 0 || params->sh_degree < 0 ||
       params->sh_degree > 3 || !std::isfinite(w_reg))
     return RTGS_ERR_INVALID_ARG;
   if (n_slots > 0 && (!params->pos || !params->log_scale || !params->rot || !params->sh || !gid_of_slot || !flags ||
                       !grad || !m || !v || !eta || (n_transparent > 0 && !init_geom)))
     return RTGS_ERR_INVALID_ARG;
   return finish(launch_adam(*params, gid_of_slot, n_slots, flags, grad, m, v, init_geom, n_transparent, w_reg, *hp, step,
-                            eta, S(stream)));
+                            step_device, eta, S(stream)));
 }
 
 size_t rtgs_classify_workspace_size(const rtgs_camera* cam) { return cam_ok(cam) ? classify_workspace_size(*cam) : 0; }

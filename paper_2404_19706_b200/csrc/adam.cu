@@ -28,6 +28,8 @@ struct AdamArgs {
   float reg_coef;  // 2 w_reg / (10 N_t)
   float lr_pos, lr_sh0, lr_shrest, lr_scale, lr_rot;
   float b1, omb1, b2, omb2, eps, bc1, bc2;
+  double beta1, beta2;
+  const int32_t* step_device;  // when set, bias corrections are formed from the device step
   uint32_t* eta;
 };
 
@@ -46,6 +48,12 @@ __global__ void __launch_bounds__(kAdamThreads) k_adam(const AdamArgs a) {
     s_nz[threadIdx.x] = 0;
   }
   __syncthreads();
+  float bc1 = a.bc1, bc2 = a.bc2;
+  if (a.step_device) {
+    const double t = (double)*a.step_device;
+    bc1 = (float)(1.0 - pow(a.beta1, t));
+    bc2 = (float)(1.0 - pow(a.beta2, t));
+  }
   const size_t base = (size_t)s0 * D;
   for (int e = threadIdx.x; e < ns * D; e += kAdamThreads) {
     const int ls = e / D, j = e - ls * D;
@@ -63,7 +71,7 @@ __global__ void __launch_bounds__(kAdamThreads) k_adam(const AdamArgs a) {
     const float vv = a.b2 * a.v[o] + a.omb2 * g * g;
     a.m[o] = mm;
     a.v[o] = vv;
-    th -= lr * (mm / a.bc1) / (sqrtf(vv / a.bc2) + a.eps);
+    th -= lr * (mm / bc1) / (sqrtf(vv / bc2) + a.eps);
     *p = th;
     a.grad[o] = 0.f;  // consumed
   }
@@ -73,7 +81,8 @@ __global__ void __launch_bounds__(kAdamThreads) k_adam(const AdamArgs a) {
 
 cudaError_t launch_adam(const rtgs_params& p, const int32_t* gid_of_slot, int n_slots, const uint8_t* flags,
                         float* grad, float* m, float* v, const float* init_geom, int n_transparent, float w_reg,
-                        const rtgs_hparams& hp, int step, uint32_t* eta, cudaStream_t s) {
+                        const rtgs_hparams& hp, int step, const int32_t* step_device, uint32_t* eta,
+                        cudaStream_t s) {
   if (n_slots == 0) return cudaSuccess;
   AdamArgs a;
   a.pos = p.pos; a.log_scale = p.log_scale; a.rot = p.rot; a.sh = p.sh;
@@ -86,6 +95,9 @@ cudaError_t launch_adam(const rtgs_params& p, const int32_t* gid_of_slot, int n_
   a.eps = (float)hp.eps;
   a.bc1 = (float)(1.0 - pow(hp.beta1, step));
   a.bc2 = (float)(1.0 - pow(hp.beta2, step));
+  a.beta1 = hp.beta1;
+  a.beta2 = hp.beta2;
+  a.step_device = step_device;
   a.eta = eta;
   const int blocks = (n_slots + kAdamSlots - 1) / kAdamSlots;
   switch ((p.sh_degree + 1) * (p.sh_degree + 1)) {

@@ -241,6 +241,7 @@ __global__ void __launch_bounds__(kPipeThreads) k_render_bwd(const BwdArgs a) {
 // K5b: chain rule through the projection (float32, recomputing the forward quantities)
 // ------------------------------------------------------------------------------------------------
 struct PBArgs {
+  const float4* rec;
   const float* pos;
   const float* log_scale;
   const float* rot;
@@ -261,41 +262,44 @@ struct PBArgs {
   const uint32_t* counts;
 };
 
-template <int K>
-__device__ __forceinline__ void sh_basis_grad(float x, float y, float z, float* Y, float* dx, float* dy, float* dz) {
+// Y_k(d) and its gradient for ONE coefficient k (a compile-time constant after unrolling): the 3DGS
+// real basis (R2), constants restated from their closed forms.
+__device__ __forceinline__ void sh_basis_one(int k, float x, float y, float z, float& Y, float& dx, float& dy,
+                                             float& dz) {
   const float C0 = 0.28209479177387814f, C1 = 0.4886025119029199f;
   const float C20 = 1.0925484305920792f, C21 = -1.0925484305920792f, C22 = 0.31539156525252005f,
               C23 = -1.0925484305920792f, C24 = 0.5462742152960396f;
   const float C30 = -0.5900435899266435f, C31 = 2.890611442640554f, C32 = -0.4570457994644658f,
               C33 = 0.3731763325901154f, C34 = -0.4570457994644658f, C35 = 1.445305721320277f,
               C36 = -0.5900435899266435f;
-#pragma unroll
-  for (int k = 0; k < K; ++k) { Y[k] = 0.f; dx[k] = 0.f; dy[k] = 0.f; dz[k] = 0.f; }
-  Y[0] = C0;
-  if (K > 1) {
-    Y[1] = -C1 * y; dy[1] = -C1;
-    Y[2] = C1 * z;  dz[2] = C1;
-    Y[3] = -C1 * x; dx[3] = -C1;
-  }
-  if (K > 4) {
-    const float xx = x * x, yy = y * y, zz = z * z;
-    Y[4] = C20 * x * y;               dx[4] = C20 * y; dy[4] = C20 * x;
-    Y[5] = C21 * y * z;               dy[5] = C21 * z; dz[5] = C21 * y;
-    Y[6] = C22 * (2.f * zz - xx - yy); dx[6] = -2.f * C22 * x; dy[6] = -2.f * C22 * y; dz[6] = 4.f * C22 * z;
-    Y[7] = C23 * x * z;               dx[7] = C23 * z; dz[7] = C23 * x;
-    Y[8] = C24 * (xx - yy);           dx[8] = 2.f * C24 * x; dy[8] = -2.f * C24 * y;
-    if (K > 9) {
-      Y[9] = C30 * y * (3.f * xx - yy);  dx[9] = 6.f * C30 * x * y; dy[9] = C30 * (3.f * xx - 3.f * yy);
-      Y[10] = C31 * x * y * z;           dx[10] = C31 * y * z; dy[10] = C31 * x * z; dz[10] = C31 * x * y;
-      Y[11] = C32 * y * (4.f * zz - xx - yy);
-      dx[11] = -2.f * C32 * x * y; dy[11] = C32 * (4.f * zz - xx - 3.f * yy); dz[11] = 8.f * C32 * y * z;
-      Y[12] = C33 * z * (2.f * zz - 3.f * xx - 3.f * yy);
-      dx[12] = -6.f * C33 * x * z; dy[12] = -6.f * C33 * y * z; dz[12] = C33 * (6.f * zz - 3.f * xx - 3.f * yy);
-      Y[13] = C34 * x * (4.f * zz - xx - yy);
-      dx[13] = C34 * (4.f * zz - 3.f * xx - yy); dy[13] = -2.f * C34 * x * y; dz[13] = 8.f * C34 * x * z;
-      Y[14] = C35 * z * (xx - yy);       dx[14] = 2.f * C35 * x * z; dy[14] = -2.f * C35 * y * z; dz[14] = C35 * (xx - yy);
-      Y[15] = C36 * x * (xx - 3.f * yy); dx[15] = C36 * (3.f * xx - 3.f * yy); dy[15] = -6.f * C36 * x * y;
-    }
+  const float xx = x * x, yy = y * y, zz = z * z;
+  dx = dy = dz = 0.f;
+  switch (k) {
+    case 0: Y = C0; break;
+    case 1: Y = -C1 * y; dy = -C1; break;
+    case 2: Y = C1 * z; dz = C1; break;
+    case 3: Y = -C1 * x; dx = -C1; break;
+    case 4: Y = C20 * x * y; dx = C20 * y; dy = C20 * x; break;
+    case 5: Y = C21 * y * z; dy = C21 * z; dz = C21 * y; break;
+    case 6: Y = C22 * (2.f * zz - xx - yy); dx = -2.f * C22 * x; dy = -2.f * C22 * y; dz = 4.f * C22 * z; break;
+    case 7: Y = C23 * x * z; dx = C23 * z; dz = C23 * x; break;
+    case 8: Y = C24 * (xx - yy); dx = 2.f * C24 * x; dy = -2.f * C24 * y; break;
+    case 9: Y = C30 * y * (3.f * xx - yy); dx = 6.f * C30 * x * y; dy = C30 * (3.f * xx - 3.f * yy); break;
+    case 10: Y = C31 * x * y * z; dx = C31 * y * z; dy = C31 * x * z; dz = C31 * x * y; break;
+    case 11:
+      Y = C32 * y * (4.f * zz - xx - yy);
+      dx = -2.f * C32 * x * y; dy = C32 * (4.f * zz - xx - 3.f * yy); dz = 8.f * C32 * y * z;
+      break;
+    case 12:
+      Y = C33 * z * (2.f * zz - 3.f * xx - 3.f * yy);
+      dx = -6.f * C33 * x * z; dy = -6.f * C33 * y * z; dz = C33 * (6.f * zz - 3.f * xx - 3.f * yy);
+      break;
+    case 13:
+      Y = C34 * x * (4.f * zz - xx - yy);
+      dx = C34 * (4.f * zz - 3.f * xx - yy); dy = -2.f * C34 * x * y; dz = 8.f * C34 * x * z;
+      break;
+    case 14: Y = C35 * z * (xx - yy); dx = 2.f * C35 * x * z; dy = -2.f * C35 * y * z; dz = C35 * (xx - yy); break;
+    default: Y = C36 * x * (xx - 3.f * yy); dx = C36 * (3.f * xx - 3.f * yy); dy = -6.f * C36 * x * y; break;
   }
 }
 
@@ -416,8 +420,11 @@ __device__ __forceinline__ void project_bwd_slot(const PBArgs& a, int s, float* 
   const double vx = (double)px - a.campos[0], vy = (double)py - a.campos[1], vz = (double)pz - a.campos[2];
   const double vnorm = sqrt(vx * vx + vy * vy + vz * vz);
   const float dirx = (float)(vx / vnorm), diry = (float)(vy / vnorm), dirz = (float)(vz / vnorm);
-  float Yb[K], Yx[K], Yy[K], Yz[K];
-  sh_basis_grad<K>(dirx, diry, dirz, Yb, Yx, Yy, Yz);
+  // rgb = max(0, raw): the clamp decision (R17) comes from the projected colour (rgb == 0 <=> raw <= 0)
+  const float4 rgbq = a.rec[(size_t)4 * i + 2];
+  const float gc0 = rgbq.x > 0.f ? drgb[0] : 0.f;
+  const float gc1 = rgbq.y > 0.f ? drgb[1] : 0.f;
+  const float gc2 = rgbq.z > 0.f ? drgb[2] : 0.f;
   // the slot's SH row in registers, loaded with 16-byte vectors when the row is 16-byte aligned
   float shc[3 * K];
   if constexpr ((3 * K) % 4 == 0) {
@@ -432,20 +439,17 @@ __device__ __forceinline__ void project_bwd_slot(const PBArgs& a, int s, float* 
     for (int q = 0; q < 3 * K; ++q) shc[q] = a.sh[(size_t)i * 3 * K + q];
   }
   float gd0 = 0.f, gd1 = 0.f, gd2 = 0.f;
-  for (int ch = 0; ch < 3; ++ch) {
-    float raw = 0.5f;
 #pragma unroll
-    for (int kk = 0; kk < K; ++kk) raw += Yb[kk] * shc[3 * kk + ch];
-    const float gch = raw >= 0.f ? drgb[ch] : 0.f;  // clamp at 0 (R17)
-    if (gch == 0.f) continue;
-#pragma unroll
-    for (int kk = 0; kk < K; ++kk) {
-      gout[10 + 3 * kk + ch] += Yb[kk] * gch;
-      const float c = shc[3 * kk + ch] * gch;
-      gd0 += Yx[kk] * c;
-      gd1 += Yy[kk] * c;
-      gd2 += Yz[kk] * c;
-    }
+  for (int kk = 0; kk < K; ++kk) {
+    float Y, Yx, Yy, Yz;
+    sh_basis_one(kk, dirx, diry, dirz, Y, Yx, Yy, Yz);
+    gout[10 + 3 * kk] += Y * gc0;
+    gout[10 + 3 * kk + 1] += Y * gc1;
+    gout[10 + 3 * kk + 2] += Y * gc2;
+    const float c = shc[3 * kk] * gc0 + shc[3 * kk + 1] * gc1 + shc[3 * kk + 2] * gc2;
+    gd0 += Yx * c;
+    gd1 += Yy * c;
+    gd2 += Yz * c;
   }
   {
     const float dd = gd0 * dirx + gd1 * diry + gd2 * dirz;
@@ -544,6 +548,7 @@ cudaError_t launch_backward(const rtgs_gaussians& g, const rtgs_projected& proj,
   k_render_bwd<<<T, kPipeThreads, 0, s>>>(a);
   note_launch();
   PBArgs b;
+  b.rec = reinterpret_cast<const float4*>(proj.rec);
   b.pos = g.pos; b.log_scale = g.log_scale; b.rot = g.rot; b.sh = g.sh;
   b.K = (g.sh_degree + 1) * (g.sh_degree + 1);
   b.D = 10 + 3 * b.K;

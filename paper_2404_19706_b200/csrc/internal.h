@@ -36,7 +36,8 @@ cudaError_t launch_backward(const rtgs_gaussians& g, const rtgs_projected& proj,
 
 cudaError_t launch_adam(const rtgs_params& p, const int32_t* gid_of_slot, int n_slots, const uint8_t* flags,
                         float* grad, float* m, float* v, const float* init_geom, int n_transparent, float w_reg,
-                        const rtgs_hparams& hp, int step, uint32_t* eta, cudaStream_t s);
+                        const rtgs_hparams& hp, int step, const int32_t* step_device, uint32_t* eta,
+                        cudaStream_t s);
 
 size_t classify_workspace_size(const rtgs_camera& cam);
 cudaError_t launch_classify(const rtgs_render_out& full, const rtgs_frame& frame, const uint8_t* flags,

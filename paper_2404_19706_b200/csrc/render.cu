@@ -22,16 +22,29 @@ __global__ void __launch_bounds__(256) k_coverage(const float4* __restrict__ rec
   const int i = blockIdx.x * 256 + threadIdx.x;
   const int lane = threadIdx.x & 31;
   const bool mine = i < n && !(flags[i] & 2u) && zkey[i] != 0xFFFFFFFFu;
+  // every lane prefetches its own Gaussian; the warp then splats them one by one via shuffles
+  uint2 myr = make_uint2(1u | (1u << 16), 0u);
+  float4 mya = make_float4(0, 0, 0, 0), myb = mya;
+  if (mine) {
+    myr = rect[i];
+    mya = rec[4 * (size_t)i];
+    myb = rec[4 * (size_t)i + 1];
+  }
   uint32_t m = __ballot_sync(0xffffffffu, mine);
   while (m) {
     const int src = __ffs(m) - 1;
     m &= m - 1;
-    const int g = __shfl_sync(0xffffffffu, i, src);
-    const uint2 r = rect[g];
+    uint2 r;
+    r.x = __shfl_sync(0xffffffffu, myr.x, src);
+    r.y = __shfl_sync(0xffffffffu, myr.y, src);
     const int x0 = (int)(short)(r.x & 0xFFFF), y0 = (int)(short)(r.x >> 16);
     const int x1 = (int)(short)(r.y & 0xFFFF), y1 = (int)(short)(r.y >> 16);
     if (x0 > x1 || y0 > y1) continue;
-    const float4 a = rec[4 * g], b = rec[4 * g + 1];
+    float4 a, b;
+    a.x = __shfl_sync(0xffffffffu, mya.x, src); a.y = __shfl_sync(0xffffffffu, mya.y, src);
+    a.z = __shfl_sync(0xffffffffu, mya.z, src); a.w = __shfl_sync(0xffffffffu, mya.w, src);
+    b.x = __shfl_sync(0xffffffffu, myb.x, src); b.y = __shfl_sync(0xffffffffu, myb.y, src);
+    b.z = __shfl_sync(0xffffffffu, myb.z, src); b.w = __shfl_sync(0xffffffffu, myb.w, src);
     const int w = x1 - x0 + 1;
     const int tot = w * (y1 - y0 + 1);
     for (int p = lane; p < tot; p += 32) {

@@ -9,12 +9,19 @@
 //   3. k_emit         per Gaussian, per kept tile: slot = start[t] + atomicAdd(cursor[t]) and store
 //                     the 64-bit pair (zkey << 32 | gid)   (order inside a tile still arbitrary)
 //   4. k_tile_sort    one CTA per tile: key' = ((zkey - zmin) << gid_bits) | gid, stable LSD radix
-//                     sort with 8-bit digits (warp match_any ranking) on the bits that vary, in
-//                     shared memory (global-memory ping-pong for tiles above kSortCap), write gids.
+//                     sort with 8-bit digits (warp match_any ranking) on the depth bits that vary
+//                     (~3 passes), runs of equal depth then put in gid order; in shared memory
+//                     (global-memory ping-pong for tiles above kSortCap); write gids.
 // The output is the unique (tile, zkey bits, gid) order, so it is deterministic and bit-exact with
 // the oracle although the emission order is not.
 #include "common.cuh"
 #include "internal.h"
+#ifdef RTGS_DEBUG
+#include <cassert>
+#define RTGS_ASSERT(c) assert(c)
+#else
+#define RTGS_ASSERT(c)
+#endif
 
 namespace rtgs {
 
@@ -183,24 +190,27 @@ __global__ void __launch_bounds__(256) k_emit(const uint32_t* __restrict__ zkey,
     }
 }
 
-// Stable LSD radix sort of n 64-bit keys (8-bit digits over `nbits` low bits) by one CTA.
-// A/B/rank may live in shared or global memory; wcnt/dstart are shared.
+// Stable LSD radix sort of n 64-bit keys by one CTA on key bits [lo, lo + nbits) (8-bit digits).
+// Warp w owns the contiguous run [w*run, (w+1)*run) for ranking AND scattering, so the stable order
+// is (warp, round, lane).  Key / rank buffers are shared memory (KeyPtr = shared pointers, inlined
+// into LDS/STS) or global memory for oversized tiles.
 __device__ __forceinline__ void cta_radix_sort(unsigned long long* A, unsigned long long* B, uint32_t* rank, int n,
-                                               int nbits, uint32_t (*wcnt)[256], uint32_t* dstart,
+                                               int lo, int nbits, uint32_t (*wcnt)[256], uint32_t* dstart,
                                                uint32_t* scan_sh, unsigned long long** out) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const uint32_t lt = (1u << lane) - 1u;
   const int run = ((n + kSortWarps * 32 - 1) / (kSortWarps * 32)) * 32;  // contiguous keys per warp
   const int r0 = min(n, w * run), r1 = min(n, (w + 1) * run);
-  for (int shift = 0; shift < nbits; shift += 8) {
-    for (int d = tid; d < kSortWarps * 256; d += kSortThreads) (&wcnt[0][0])[d] = 0;
-    __syncthreads();
+  for (int shift = lo; shift < lo + nbits; shift += 8) {
+    for (int d = lane; d < 256; d += 32) wcnt[w][d] = 0;  // each warp clears its own counters
+    __syncwarp();
     for (int base = r0; base < r1; base += 32) {
       const int i = base + lane;
       const bool ok = i < r1;
       const uint32_t d = ok ? (uint32_t)((A[i] >> shift) & 0xFFu) : 0x1000u;
       const uint32_t peers = __match_any_sync(0xffffffffu, d);
       const uint32_t before = ok ? wcnt[w][d] : 0u;
+      RTGS_ASSERT(!ok || d < 256);
       if (ok) rank[i] = before + __popc(peers & lt);
       __syncwarp();
       if (ok && (31 - __clz(peers)) == lane) wcnt[w][d] = before + __popc(peers);
@@ -219,12 +229,12 @@ __device__ __forceinline__ void cta_radix_sort(unsigned long long* A, unsigned l
       uint32_t tot;
       dstart[d] = block_excl_scan(run_w, scan_sh, &tot);
     }
-    __syncthreads();
-    for (int i = tid; i < n; i += kSortThreads) {
+    __syncthreads();  // dstart written after the scan's own barriers
+    for (int i = r0 + lane; i < r1; i += 32) {
       const unsigned long long k = A[i];
       const uint32_t d = (uint32_t)((k >> shift) & 0xFFu);
-      const int ww = i / run;
-      B[dstart[d] + wcnt[ww][d] + rank[i]] = k;
+      RTGS_ASSERT(dstart[d] + wcnt[w][d] + rank[i] < (uint32_t)n);
+      B[dstart[d] + wcnt[w][d] + rank[i]] = k;
     }
     __syncthreads();
     unsigned long long* t = A;
@@ -234,30 +244,13 @@ __device__ __forceinline__ void cta_radix_sort(unsigned long long* A, unsigned l
   *out = A;
 }
 
-__global__ void __launch_bounds__(kSortThreads) k_tile_sort(const uint2* __restrict__ range,
-                                                            unsigned long long* __restrict__ keys,
-                                                            unsigned long long* __restrict__ tmp,
-                                                            uint32_t* __restrict__ grank, int gid_bits,
-                                                            uint32_t* __restrict__ sorted_gid) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ uint32_t wcnt[kSortWarps][256];
-  __shared__ uint32_t dstart[256];
-  __shared__ uint32_t scan_sh[33];
-  __shared__ uint32_t s_zmin, s_zmax;
-  const uint2 rg = range[blockIdx.x];
-  const int n = (int)(rg.y - rg.x);
-  if (n <= 0) return;
+// one tile's list: load, compress, depth-radix-sort, tie fix-up, write gids
+__device__ __forceinline__ void sort_tile(const unsigned long long* __restrict__ seg, unsigned long long* A,
+                                          unsigned long long* B, uint32_t* rk, int n, int gid_bits,
+                                          uint32_t* __restrict__ out_gid, bool copy_in, uint32_t (*wcnt)[256],
+                                          uint32_t* dstart, uint32_t* scan_sh, uint32_t* s_zmm) {
   const int tid = threadIdx.x;
-  unsigned long long* seg = keys + rg.x;
-  if (n == 1) {
-    if (tid == 0) sorted_gid[rg.x] = (uint32_t)(seg[0] & 0xFFFFFFFFull);
-    return;
-  }
-  const bool in_smem = n <= kSortCap;
-  unsigned long long* A = in_smem ? reinterpret_cast<unsigned long long*>(smem) : seg;
-  unsigned long long* B = in_smem ? A + kSortCap : tmp + rg.x;
-  uint32_t* rk = in_smem ? reinterpret_cast<uint32_t*>(A + 2 * kSortCap) : grank + rg.x;
-  if (tid == 0) { s_zmin = 0xFFFFFFFFu; s_zmax = 0u; }
+  if (tid == 0) { s_zmm[0] = 0xFFFFFFFFu; s_zmm[1] = 0u; }
   __syncthreads();
   uint32_t zmin = 0xFFFFFFFFu, zmax = 0u;
   for (int i = tid; i < n; i += kSortThreads) {
@@ -265,13 +258,13 @@ __global__ void __launch_bounds__(kSortThreads) k_tile_sort(const uint2* __restr
     const uint32_t z = (uint32_t)(k >> 32);
     zmin = min(zmin, z);
     zmax = max(zmax, z);
-    if (in_smem) A[i] = k;
+    if (copy_in) A[i] = k;
   }
-  atomicMin(&s_zmin, zmin);
-  atomicMax(&s_zmax, zmax);
+  atomicMin(&s_zmm[0], zmin);
+  atomicMax(&s_zmm[1], zmax);
   __syncthreads();
-  const uint32_t z0 = s_zmin;
-  const uint32_t zr = s_zmax - z0;
+  const uint32_t z0 = s_zmm[0];
+  const uint32_t zr = s_zmm[1] - z0;
   const int zbits = zr ? 32 - __clz(zr) : 0;
   // compress: key' = ((z - zmin) << gid_bits) | gid  (order-preserving for (z, gid))
   for (int i = tid; i < n; i += kSortThreads) {
@@ -280,10 +273,66 @@ __global__ void __launch_bounds__(kSortThreads) k_tile_sort(const uint2* __restr
     A[i] = (zz << gid_bits) | (k & 0xFFFFFFFFull);
   }
   __syncthreads();
+  // radix-sort on the depth bits only (the emission order among equal depths is arbitrary) ...
   unsigned long long* res;
-  cta_radix_sort(A, B, rk, n, zbits + gid_bits, wcnt, dstart, scan_sh, &res);
-  const unsigned long long gmask = (gid_bits >= 64) ? ~0ull : ((1ull << gid_bits) - 1ull);
-  for (int i = tid; i < n; i += kSortThreads) sorted_gid[rg.x + i] = (uint32_t)(res[i] & gmask);
+  cta_radix_sort(A, B, rk, n, gid_bits, zbits, wcnt, dstart, scan_sh, &res);
+  // ... then put every run of equal depth into gid order.  Ties are common on fronto-parallel
+  // surfaces (float32 depths of a wall collide), but runs are short: each run is insertion-sorted
+  // by the thread at its start; a run longer than kMaxRun makes the CTA re-sort the whole list on
+  // all bits (gid bits included), which gives the same unique (zkey, gid) order.
+  constexpr int kMaxRun = 16;
+  bool long_run = false;
+  for (int i = tid; i < n; i += kSortThreads) {
+    const unsigned long long zi = res[i] >> gid_bits;
+    if ((i == 0 || (res[i - 1] >> gid_bits) != zi) && i + 1 < n && (res[i + 1] >> gid_bits) == zi) {
+      int j = i + 1;
+      while (j < n && j - i <= kMaxRun && (res[j] >> gid_bits) == zi) ++j;
+      if (j - i > kMaxRun) {
+        long_run = true;
+      } else {
+        for (int p = i + 1; p < j; ++p) {
+          const unsigned long long k = res[p];
+          int q = p - 1;
+          while (q >= i && res[q] > k) { res[q + 1] = res[q]; --q; }
+          res[q + 1] = k;
+        }
+      }
+    }
+  }
+  if (__syncthreads_or(long_run)) {
+    unsigned long long* other = (res == A) ? B : A;
+    cta_radix_sort(res, other, rk, n, 0, zbits + gid_bits, wcnt, dstart, scan_sh, &res);
+  }
+  const unsigned long long gmask = (1ull << gid_bits) - 1ull;
+  for (int i = tid; i < n; i += kSortThreads) out_gid[i] = (uint32_t)(res[i] & gmask);
+}
+
+__global__ void __launch_bounds__(kSortThreads) k_tile_sort(const uint2* __restrict__ range,
+                                                            unsigned long long* __restrict__ keys,
+                                                            unsigned long long* __restrict__ tmp,
+                                                            uint32_t* __restrict__ grank, int gid_bits,
+                                                            uint32_t* __restrict__ sorted_gid) {
+  extern __shared__ __align__(16) unsigned long long s_keys[];  // [2 * kSortCap] keys + kSortCap ranks
+  __shared__ uint32_t wcnt[kSortWarps][256];
+  __shared__ uint32_t dstart[256];
+  __shared__ uint32_t scan_sh[33];
+  __shared__ uint32_t s_zmm[2];
+  const uint2 rg = range[blockIdx.x];
+  const int n = (int)(rg.y - rg.x);
+  if (n <= 0) return;
+  RTGS_ASSERT(rg.y >= rg.x);
+  unsigned long long* seg = keys + rg.x;
+  if (n == 1) {
+    if (threadIdx.x == 0) sorted_gid[rg.x] = (uint32_t)(seg[0] & 0xFFFFFFFFull);
+    return;
+  }
+  if (n <= kSortCap) {  // shared-memory path: every buffer access below is LDS / STS
+    sort_tile(seg, s_keys, s_keys + kSortCap, reinterpret_cast<uint32_t*>(s_keys + 2 * kSortCap), n, gid_bits,
+              sorted_gid + rg.x, true, wcnt, dstart, scan_sh, s_zmm);
+  } else {              // oversized tile: global-memory ping-pong (correct, slower)
+    sort_tile(seg, seg, tmp + rg.x, grank + rg.x, n, gid_bits, sorted_gid + rg.x, false, wcnt, dstart, scan_sh,
+              s_zmm);
+  }
 }
 
 // ------------------------------------------------------------------------------------------------

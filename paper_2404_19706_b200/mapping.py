@@ -194,11 +194,12 @@ def render_backward_masked(gm: GaussianMap, proj: ProjectedBuffers, bins: BinBuf
 
 def adam_step_unstable(gm: GaussianMap, gid_of_slot: torch.Tensor, grad: torch.Tensor, m: torch.Tensor,
                        v: torch.Tensor, init_geom: torch.Tensor | None, n_transparent: int, w_reg: float,
-                       hparams: _abi.HParams, step: int, eta: torch.Tensor, stream=None):
+                       hparams: _abi.HParams, step: int, eta: torch.Tensor, stream=None,
+                       step_device: torch.Tensor | None = None):
     prm = gm.c_params()
     check(lib().rtgs_adam_step_unstable(C.byref(prm), _p(gid_of_slot), int(gid_of_slot.numel()), _p(gm.flags), _p(grad),
                                         _p(m), _p(v), _p(init_geom), int(n_transparent), float(w_reg), C.byref(hparams),
-                                        int(step), _p(eta), _stream(stream)), "rtgs_adam_step_unstable")
+                                        int(step), _p(step_device), _p(eta), _stream(stream)), "rtgs_adam_step_unstable")
 
 
 def classify_workspace_size(cam: _abi.Camera) -> int:
@@ -238,11 +239,16 @@ class MappingEngine:
         self.gm, self.cam, self.device = gm, cam, device
         n = gm.n
         self.capacity = int(capacity if capacity is not None else max(4 * n, 1 << 16))
+        # the masked iteration and the frame ingest own separate buffers so they can run concurrently
         self.proj = ProjectedBuffers(n, device)
         self.bins = BinBuffers(cam, self.capacity, device)
         self.out = RenderBuffers(cam, device)
-        self.full = RenderBuffers(cam, device)
         self.ws_bin = torch.empty(bin_workspace_size(n, cam, self.capacity), dtype=torch.uint8, device=device)
+        self.proj_full = ProjectedBuffers(n, device)
+        self.bins_full = BinBuffers(cam, self.capacity, device)
+        self.full = RenderBuffers(cam, device)
+        self.ws_bin_full = torch.empty(bin_workspace_size(n, cam, self.capacity), dtype=torch.uint8, device=device)
+        self.side = torch.cuda.Stream(device=device)
         self.ws_cls = torch.empty(classify_workspace_size(cam), dtype=torch.uint8, device=device)
         self.weights = weights
         self.hp = hparams(preset)
@@ -274,13 +280,17 @@ class MappingEngine:
             if n_slots else torch.zeros((1, 10), device=self.device)
         self.ws_bwd = torch.empty(backward_workspace_size(n_slots), dtype=torch.uint8, device=self.device)
         self.step_count = 0
+        self.step_dev = torch.zeros(1, dtype=torch.int32, device=self.device)  # graph-replayable step
 
     # --- the two flows ---------------------------------------------------------------------------
-    def ingest(self, frame_color, frame_depth, pose: _abi.Pose, seed=0, frame_idx=0, stream=None):
-        """A1 -> A2 (all tiles) -> A3/A4 FULL -> A7."""
-        project_gaussians(self.gm, pose, self.cam, self.proj, stream)
-        bin_and_sort(self.proj, self.gm.n, self.cam, None, self.bins, self.ws_bin, stream)
-        render_color_depth(self.gm, self.proj, self.bins, pose, self.cam, RTGS_RENDER_FULL, self.full, stream)
+    def ingest(self, frame_color, frame_depth, pose: _abi.Pose, seed=0, frame_idx=0, stream=None, after_project=None):
+        """A1 -> A2 (all tiles) -> A3/A4 FULL -> A7.  `after_project(stream)` is called once
+        the projection (the last read of the parameters) has been enqueued."""
+        project_gaussians(self.gm, pose, self.cam, self.proj_full, stream)
+        if after_project is not None:
+            after_project(stream)
+        bin_and_sort(self.proj_full, self.gm.n, self.cam, None, self.bins_full, self.ws_bin_full, stream)
+        render_color_depth(self.gm, self.proj_full, self.bins_full, pose, self.cam, RTGS_RENDER_FULL, self.full, stream)
         classify_and_add_pixels(self.full, frame_color, frame_depth, self.gm.flags, self.cam,
                                 add_params(seed=seed, frame_idx=frame_idx), self.pixel_class, self.samples,
                                 self.add_counts, self.ws_cls, stream)
@@ -298,15 +308,42 @@ class MappingEngine:
                                stream)
 
     def optimizer_step(self, stream=None):
+        """A6.  The window step lives on the device (incremented here, read by the kernel), so a
+        captured CUDA graph of the iteration advances the bias correction on every replay."""
         self.step_count += 1
+        s = torch.cuda.current_stream() if stream is None else stream
+        with torch.cuda.stream(s):
+            self.step_dev.add_(1)
         adam_step_unstable(self.gm, self.gid_of_slot, self.grad, self.m, self.v, self.init_geom, self.n_transparent,
-                           self.weights[2], self.hp, self.step_count, self.eta, stream)
+                           self.weights[2], self.hp, self.step_count, self.eta, stream, step_device=self.step_dev)
 
     def iteration(self, frame_color, frame_depth, pose: _abi.Pose, stream=None):
         """One mapping optimisation iteration A0-A6 (the paper's 'mapping / iteration')."""
         self.forward_masked(pose, stream)
         self.backward(frame_color, frame_depth, pose, stream)
         self.optimizer_step(stream)
+
+    def step(self, frame_color, frame_depth, pose: _abi.Pose, ingest_pose=None, seed=0, frame_idx=0,
+             reduce_grads=None):
+        """Frame ingest (A1, A2, A3/A4 FULL, A7) and one masked iteration (A0-A6) on two streams.
+
+        The ingest runs on a side stream concurrently with the iteration on the current stream (the
+        paper runs mapping stages in parallel threads); the only dependency is that the Adam
+        step, which writes the parameters, waits until the ingest's projection has read them.
+        `reduce_grads(grad)` (multi-GPU) runs between the backward and the Adam step."""
+        main = torch.cuda.current_stream()
+        side = self.side
+        side.wait_stream(main)
+        proj_done = torch.cuda.Event()
+        self.ingest(frame_color, frame_depth, ingest_pose or pose, seed=seed, frame_idx=frame_idx, stream=side,
+                    after_project=lambda s: proj_done.record(s))
+        self.forward_masked(pose, main)
+        self.backward(frame_color, frame_depth, pose, main)
+        if reduce_grads is not None:
+            reduce_grads(self.grad)
+        main.wait_event(proj_done)
+        self.optimizer_step(main)
+        main.wait_stream(side)
 
 
 def launch_count() -> int:

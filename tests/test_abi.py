@@ -60,7 +60,7 @@ def test_invalid_arguments_rejected_on_host(L):
     hp = mapping.hparams()
     prm = _abi.Params(None, None, None, None, 0, 3)
     assert L.rtgs_adam_step_unstable(C.byref(prm), None, 0, None, None, None, None, None, 0, 1000.0, C.byref(hp), 0,
-                                     None, None) == 1                  # step must be >= 1
+                                     None, None, None) == 1            # step must be >= 1 (or on the device)
 
 
 def test_workspace_sizes(L):
