@@ -10,8 +10,9 @@
 
 namespace rtgs {
 
-constexpr int kAdamSlots = 16;
 constexpr int kAdamThreads = 256;
+constexpr int kLanesPerSlot = 16;                              // a half-warp owns one slot row
+constexpr int kAdamSlots = kAdamThreads / kLanesPerSlot;      // 16 slots per CTA
 
 struct AdamArgs {
   float* pos;
@@ -28,55 +29,71 @@ struct AdamArgs {
   float reg_coef;  // 2 w_reg / (10 N_t)
   float lr_pos, lr_sh0, lr_shrest, lr_scale, lr_rot;
   float b1, omb1, b2, omb2, eps, bc1, bc2;
-  double beta1, beta2;
+  float log_b1, log_b2;        // for the device-step bias corrections 1 - beta^t = -expm1(t log beta)
   const int32_t* step_device;  // when set, bias corrections are formed from the device step
   uint32_t* eta;
 };
 
+// One half-warp per slot: lane t owns components j = t, t+16, t+32, ... of the row (pos 3, log-scale 3,
+// rot 4, SH 3K), so grad / m / v rows stream coalesced and only j < 16 needs the geometry selects.
 template <int K>
 __global__ void __launch_bounds__(kAdamThreads) k_adam(const AdamArgs a) {
   constexpr int D = 10 + 3 * K;
-  __shared__ int s_gid[kAdamSlots];
-  __shared__ int s_tr[kAdamSlots];
-  __shared__ int s_nz[kAdamSlots];
-  const int s0 = blockIdx.x * kAdamSlots;
-  const int ns = min(kAdamSlots, a.n_slots - s0);
-  if (threadIdx.x < ns) {
-    const int g = a.gid_of_slot[s0 + threadIdx.x];
-    s_gid[threadIdx.x] = g;
-    s_tr[threadIdx.x] = a.flags[g] & 1u;
-    s_nz[threadIdx.x] = 0;
-  }
-  __syncthreads();
+  const int lane = threadIdx.x & 31, t = threadIdx.x & (kLanesPerSlot - 1);
+  const int slot = blockIdx.x * kAdamSlots + (threadIdx.x >> 4);
+  const bool live = slot < a.n_slots;
   float bc1 = a.bc1, bc2 = a.bc2;
   if (a.step_device) {
-    const double t = (double)*a.step_device;
-    bc1 = (float)(1.0 - pow(a.beta1, t));
-    bc2 = (float)(1.0 - pow(a.beta2, t));
+    const float st = (float)*a.step_device;
+    bc1 = -expm1f(st * a.log_b1);
+    bc2 = -expm1f(st * a.log_b2);
   }
-  const size_t base = (size_t)s0 * D;
-  for (int e = threadIdx.x; e < ns * D; e += kAdamThreads) {
-    const int ls = e / D, j = e - ls * D;
-    const size_t gid = (size_t)s_gid[ls];
-    float* p = j < 3 ? a.pos + 3 * gid + j
-                     : (j < 6 ? a.log_scale + 3 * gid + (j - 3)
-                              : (j < 10 ? a.rot + 4 * gid + (j - 6) : a.sh + (size_t)(3 * K) * gid + (j - 10)));
-    const float lr = j < 3 ? a.lr_pos : (j < 6 ? a.lr_scale : (j < 10 ? a.lr_rot : (j < 13 ? a.lr_sh0 : a.lr_shrest)));
-    const size_t o = base + e;
-    float g = a.grad[o];
-    if (j >= 10 && g != 0.f) s_nz[ls] = 1;
-    float th = *p;
-    if (j < 10 && s_tr[ls]) g += a.reg_coef * (th - a.init_geom[(size_t)(s0 + ls) * 10 + j]);  // L_reg (R18)
-    const float mm = a.b1 * a.m[o] + a.omb1 * g;
-    const float vv = a.b2 * a.v[o] + a.omb2 * g * g;
-    a.m[o] = mm;
-    a.v[o] = vv;
-    th -= lr * (mm / bc1) / (sqrtf(vv / bc2) + a.eps);
-    *p = th;
-    a.grad[o] = 0.f;  // consumed
+  const float ibc1 = 1.f / bc1, ibc2 = 1.f / bc2;
+  bool nz = false;
+  if (live) {
+    const size_t gid = (size_t)a.gid_of_slot[slot];
+    const bool transparent = a.flags[gid] & 1u;
+    const size_t row = (size_t)slot * D;
+    float* shrow = a.sh + (size_t)(3 * K) * gid - 10;
+    constexpr int NIT = (D + kLanesPerSlot - 1) / kLanesPerSlot;
+    // all loads of the row are issued before any store (stores could alias later loads otherwise)
+    float g[NIT], mo[NIT], vo[NIT], th[NIT];
+    float* p[NIT];
+#pragma unroll
+    for (int it = 0; it < NIT; ++it) {
+      const int j = min(t + it * kLanesPerSlot, D - 1);
+      if (it == 0 && j < 10)
+        p[it] = j < 3 ? a.pos + 3 * gid + j : (j < 6 ? a.log_scale + 3 * gid + (j - 3) : a.rot + 4 * gid + (j - 6));
+      else
+        p[it] = shrow + j;
+      g[it] = a.grad[row + j];
+      mo[it] = a.m[row + j];
+      vo[it] = a.v[row + j];
+      th[it] = *p[it];
+    }
+    const float th0 = (t < 10 && transparent) ? a.init_geom[(size_t)slot * 10 + t] : 0.f;
+#pragma unroll
+    for (int it = 0; it < NIT; ++it) {
+      const int j = t + it * kLanesPerSlot;
+      if (j >= D) break;
+      const float lr = (it == 0 && j < 10) ? (j < 3 ? a.lr_pos : (j < 6 ? a.lr_scale : a.lr_rot))
+                                           : (j < 13 ? a.lr_sh0 : a.lr_shrest);
+      float gg = g[it];
+      if (j >= 10 && gg != 0.f) nz = true;
+      if (it == 0 && j < 10 && transparent) gg += a.reg_coef * (th[it] - th0);  // L_reg (R18)
+      const float mm = a.b1 * mo[it] + a.omb1 * gg;
+      const float vv = a.b2 * vo[it] + a.omb2 * gg * gg;
+      a.m[row + j] = mm;
+      a.v[row + j] = vv;
+      // theta -= lr m^ / (sqrt(v^) + eps)   (m = 0 whenever v = 0, so the quotient is 0 there)
+      *p[it] = th[it] - lr * __fdividef(mm * ibc1, sqrtf(vv * ibc2) + a.eps);
+      a.grad[row + j] = 0.f;  // consumed
+    }
   }
-  __syncthreads();
-  if (threadIdx.x < ns && s_nz[threadIdx.x]) a.eta[s_gid[threadIdx.x]] += 1u;  // R20
+  // eta += 1 once per slot with a non-zero SH gradient (R20): vote within the half-warp
+  const uint32_t vote = __ballot_sync(0xffffffffu, nz);
+  const uint32_t half = (lane < 16) ? (vote & 0x0000FFFFu) : (vote & 0xFFFF0000u);
+  if (live && t == 0 && half) a.eta[a.gid_of_slot[slot]] += 1u;
 }
 
 cudaError_t launch_adam(const rtgs_params& p, const int32_t* gid_of_slot, int n_slots, const uint8_t* flags,
@@ -95,8 +112,8 @@ cudaError_t launch_adam(const rtgs_params& p, const int32_t* gid_of_slot, int n_
   a.eps = (float)hp.eps;
   a.bc1 = (float)(1.0 - pow(hp.beta1, step));
   a.bc2 = (float)(1.0 - pow(hp.beta2, step));
-  a.beta1 = hp.beta1;
-  a.beta2 = hp.beta2;
+  a.log_b1 = (float)log(hp.beta1);
+  a.log_b2 = (float)log(hp.beta2);
   a.step_device = step_device;
   a.eta = eta;
   const int blocks = (n_slots + kAdamSlots - 1) / kAdamSlots;

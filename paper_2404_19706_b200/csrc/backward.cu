@@ -169,24 +169,26 @@ __global__ void __launch_bounds__(kPipeThreads) k_render_bwd(const BwdArgs a) {
     const int st = b % kPipeStages;
     mbar_wait(&r.full[st], (uint32_t)(b / kPipeStages) & 1u);
     if (!wdone) {
-      const float4* srec = &r.rec[st][0][0];
+      const uint32_t srec = smem_u32(&r.rec[st][0][0]);  // shared addresses, computed once per batch
+      const uint32_t sslot = smem_u32(&sm.slot[st][0]);
       const uint32_t pbase = (uint32_t)(start + b * kPipeBatch);
       const int cnt = min(kPipeBatch, n - b * kPipeBatch);
       for (int g0 = 0; g0 < cnt; g0 += 32) {
         const int j = g0 + lane;
         bool ov = false;
         if (j < cnt) {
-          const float4 r0 = srec[3 * j];
-          const float2 ext = unpack_ext(srec[3 * j + 2].w);
+          const float4 r0 = lds128(srec + 48u * j);
+          const float2 ext = unpack_ext(__uint_as_float(lds32(srec + 48u * j + 44u)));
           ov = (r0.x + ext.x >= bx0) && (r0.x - ext.x <= bx1) && (r0.y + ext.y >= by0) && (r0.y - ext.y <= by1);
         }
         uint32_t m = __ballot_sync(0xffffffffu, ov);
         while (m) {
           const int idx = g0 + __ffs(m) - 1;
           m &= m - 1;
-          const int slot = sm.slot[st][idx];  // warp-uniform
+          const int slot = (int)lds32(sslot + 4u * idx);  // warp-uniform
           // branch-free replay of record idx (identical arithmetic and decisions to the forward)
-          const float4 r0 = srec[3 * idx], r1 = srec[3 * idx + 1], r2 = srec[3 * idx + 2];
+          const uint32_t ra = srec + 48u * idx;
+          const float4 r0 = lds128(ra), r1 = lds128(ra + 16u), r2 = lds128(ra + 32u);
           const bool past = pbase + (uint32_t)idx >= last;  // beyond the last blended entry
           done = done || past;
           PairEval e;
@@ -242,6 +244,7 @@ __global__ void __launch_bounds__(kPipeThreads) k_render_bwd(const BwdArgs a) {
 // ------------------------------------------------------------------------------------------------
 struct PBArgs {
   const float4* rec;
+  const float* recf;  // the same records as floats
   const float* pos;
   const float* log_scale;
   const float* rot;
@@ -304,9 +307,11 @@ __device__ __forceinline__ void sh_basis_one(int k, float x, float y, float z, f
 }
 
 // chain rule for slot s; accumulates the D = 10 + 3K parameter gradients into gout (zeroed)
+// sg: the slot's 16 screen-space sums; par: pos 3, log-scale 3, rot 4, projected rgb 3; shrow: SH
+// row (all staged in shared memory by the kernel with coalesced / bulk copies)
 template <int K>
-__device__ __forceinline__ void project_bwd_slot(const PBArgs& a, int s, float* gout) {
-  const float* sg = a.sgrad + (size_t)s * kSG;
+__device__ __forceinline__ void project_bwd_slot(const PBArgs& a, const float* sg, const float* par,
+                                                 const float* shrow, float* gout) {
   const float4 g0 = *reinterpret_cast<const float4*>(sg);
   const float4 g1 = *reinterpret_cast<const float4*>(sg + 4);
   const float4 g2 = *reinterpret_cast<const float4*>(sg + 8);
@@ -319,21 +324,20 @@ __device__ __forceinline__ void project_bwd_slot(const PBArgs& a, int s, float* 
   if (dMx == 0.f && dMy == 0.f && dA == 0.f && dB == 0.f && dCc == 0.f && drgb[0] == 0.f && drgb[1] == 0.f &&
       drgb[2] == 0.f && dDa == 0.f && dDb0 == 0.f && dDb1 == 0.f && dDb2 == 0.f && dDz == 0.f)
     return;  // nothing reached this slot
-  const int i = a.gid_of_slot[s];
-  const float px = a.pos[3 * i], py = a.pos[3 * i + 1], pz = a.pos[3 * i + 2];
+  const float px = par[0], py = par[1], pz = par[2];
   const double X = fma(a.V[0], (double)px, fma(a.V[1], (double)py, fma(a.V[2], (double)pz, a.tp[0])));
   const double Y = fma(a.V[3], (double)px, fma(a.V[4], (double)py, fma(a.V[5], (double)pz, a.tp[1])));
   const double Z = fma(a.V[6], (double)px, fma(a.V[7], (double)py, fma(a.V[8], (double)pz, a.tp[2])));
   const float x = (float)X, y = (float)Y, z = (float)Z;
   const float* V = a.Vf;
-  const float q0 = a.rot[4 * i], q1 = a.rot[4 * i + 1], q2 = a.rot[4 * i + 2], q3 = a.rot[4 * i + 3];
+  const float q0 = par[6], q1 = par[7], q2 = par[8], q3 = par[9];
   const float qn2 = q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3;
   const float qinv = rsqrtf(qn2);
   const float qw = q0 * qinv, qx = q1 * qinv, qy = q2 * qinv, qz = q3 * qinv;
   float R[3][3] = {{1.f - 2.f * (qy * qy + qz * qz), 2.f * (qx * qy - qw * qz), 2.f * (qx * qz + qw * qy)},
                    {2.f * (qx * qy + qw * qz), 1.f - 2.f * (qx * qx + qz * qz), 2.f * (qy * qz - qw * qx)},
                    {2.f * (qx * qz - qw * qy), 2.f * (qy * qz + qw * qx), 1.f - 2.f * (qx * qx + qy * qy)}};
-  const float l[3] = {a.log_scale[3 * i], a.log_scale[3 * i + 1], a.log_scale[3 * i + 2]};
+  const float l[3] = {par[3], par[4], par[5]};
   const float sc[3] = {expf(l[0]), expf(l[1]), expf(l[2])};
   float M[3][3], Sg[3][3];
   for (int r = 0; r < 3; ++r)
@@ -421,22 +425,19 @@ __device__ __forceinline__ void project_bwd_slot(const PBArgs& a, int s, float* 
   const double vnorm = sqrt(vx * vx + vy * vy + vz * vz);
   const float dirx = (float)(vx / vnorm), diry = (float)(vy / vnorm), dirz = (float)(vz / vnorm);
   // rgb = max(0, raw): the clamp decision (R17) comes from the projected colour (rgb == 0 <=> raw <= 0)
-  const float4 rgbq = a.rec[(size_t)4 * i + 2];
-  const float gc0 = rgbq.x > 0.f ? drgb[0] : 0.f;
-  const float gc1 = rgbq.y > 0.f ? drgb[1] : 0.f;
-  const float gc2 = rgbq.z > 0.f ? drgb[2] : 0.f;
-  // the slot's SH row in registers, loaded with 16-byte vectors when the row is 16-byte aligned
+  const float gc0 = par[10] > 0.f ? drgb[0] : 0.f;
+  const float gc1 = par[11] > 0.f ? drgb[1] : 0.f;
+  const float gc2 = par[12] > 0.f ? drgb[2] : 0.f;
   float shc[3 * K];
-  if constexpr ((3 * K) % 4 == 0) {
-    const float4* s4 = reinterpret_cast<const float4*>(a.sh + (size_t)i * 3 * K);
+  if constexpr ((3 * K) % 4 == 0) {  // 16-byte aligned row: vector reads (conflict-free with the padded pitch)
 #pragma unroll
     for (int q = 0; q < 3 * K / 4; ++q) {
-      const float4 t4 = s4[q];
+      const float4 t4 = reinterpret_cast<const float4*>(shrow)[q];
       shc[4 * q] = t4.x; shc[4 * q + 1] = t4.y; shc[4 * q + 2] = t4.z; shc[4 * q + 3] = t4.w;
     }
   } else {
 #pragma unroll
-    for (int q = 0; q < 3 * K; ++q) shc[q] = a.sh[(size_t)i * 3 * K + q];
+    for (int q = 0; q < 3 * K; ++q) shc[q] = shrow[q];
   }
   float gd0 = 0.f, gd1 = 0.f, gd2 = 0.f;
 #pragma unroll
@@ -490,14 +491,31 @@ __device__ __forceinline__ void project_bwd_slot(const PBArgs& a, int s, float* 
   gout[9] += (gz - dot * qz) * qinv;
 }
 
-// One thread per slot; the 128 slot rows of the CTA are staged in shared memory (pitch D+1,
-// conflict-free) and added to the contiguous grad block with coalesced read-modify-writes.
+// One thread per slot, 128 slots per CTA.  Every input is staged in shared memory first with
+// coalesced loads (screen-space sums, parameters) and one bulk copy per SH row (TMA engine), and the
+// 128 output rows are accumulated into the contiguous grad block with coalesced read-modify-writes.
+template <int K>
+struct PBSmem {
+  static constexpr int D = 10 + 3 * K, LD = D + 1;
+  static constexpr int SHF = 3 * K, SHP = (SHF % 4 == 0) ? SHF + 4 : SHF;  // pitch 52: conflict-free LDS.128
+  float sh[128 * SHP];
+  float out[128 * LD];
+  float sg[128 * kSG];
+  float par[128 * 13];
+  int gid[128];
+  uint64_t bar;
+};
+
 template <int K>
 __global__ void __launch_bounds__(128) k_project_bwd(const PBArgs a) {
-  constexpr int D = 10 + 3 * K, LD = D + 1;
-  __shared__ float s_out[128 * LD];
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s == 0) {  // loss values (device-side, no host sync)
+  using SM = PBSmem<K>;
+  constexpr int D = SM::D, LD = SM::LD, SHF = SM::SHF, SHP = SM::SHP;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SM& sm = *reinterpret_cast<SM*>(smem_raw);
+  const int tid = threadIdx.x;
+  const int s0 = blockIdx.x * 128;
+  const int ns = min(128, a.n_slots - s0);
+  if (blockIdx.x == 0 && tid == 0) {  // loss values (device-side, no host sync)
     const float nP = (float)max(1u, a.counts[1]);
     const float Lc = a.acc[0] / (3.f * nP);
     const float Ld = a.acc[1] / fmaxf(1.f, a.acc[2]);
@@ -506,18 +524,77 @@ __global__ void __launch_bounds__(128) k_project_bwd(const PBArgs a) {
     a.loss_out[2] = a.w_c * Lc + a.w_d * Ld;
     a.loss_out[3] = a.acc[2];
   }
-  float* gout = s_out + threadIdx.x * LD;
+  if (ns <= 0) return;
+  if (tid < ns) sm.gid[tid] = a.gid_of_slot[s0 + tid];
+  if (tid == 0) {
+    mbar_init(&sm.bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if constexpr (SHF % 4 == 0) {
+    if (tid == 0) mbar_arrive_expect_tx(&sm.bar, (uint32_t)(ns * SHF * 4));
+    __syncthreads();
+    if (tid < ns) bulk_g2s(&sm.sh[tid * SHP], a.sh + (size_t)sm.gid[tid] * SHF, SHF * 4, &sm.bar);
+  } else {
+    for (int e = tid; e < ns * SHF; e += 128) {
+      const int ls = e / SHF, j = e - ls * SHF;
+      sm.sh[ls * SHP + j] = a.sh[(size_t)sm.gid[ls] * SHF + j];
+    }
+  }
+  // (loads batched 8 deep before their stores so that many are in flight per thread)
+  constexpr int U = 8;
+  for (int e0 = tid; e0 < ns * kSG; e0 += 128 * U) {
+    float v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * 128;
+      v[u] = e < ns * kSG ? a.sgrad[(size_t)s0 * kSG + e] : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (e0 + u * 128 < ns * kSG) sm.sg[e0 + u * 128] = v[u];
+  }
+  for (int e0 = tid; e0 < ns * 13; e0 += 128 * U) {
+    float v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * 128;
+      v[u] = 0.f;
+      if (e < ns * 13) {
+        const int ls = e / 13, c = e - ls * 13;
+        const size_t g = (size_t)sm.gid[ls];
+        v[u] = c < 3 ? a.pos[3 * g + c]
+                     : (c < 6 ? a.log_scale[3 * g + (c - 3)]
+                              : (c < 10 ? a.rot[4 * g + (c - 6)] : a.recf[16 * g + 8 + (c - 10)]));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (e0 + u * 128 < ns * 13) sm.par[e0 + u * 128] = v[u];
+  }
+  float* gout = sm.out + tid * LD;
 #pragma unroll
   for (int j = 0; j < D; ++j) gout[j] = 0.f;
-  if (s < a.n_slots) project_bwd_slot<K>(a, s, gout);
   __syncthreads();
-  const int s0 = blockIdx.x * blockDim.x;
-  const int ns = min((int)blockDim.x, a.n_slots - s0);
+  if constexpr (SHF % 4 == 0) mbar_wait(&sm.bar, 0);
+  if (tid < ns) project_bwd_slot<K>(a, sm.sg + tid * kSG, sm.par + tid * 13, sm.sh + tid * SHP, gout);
+  __syncthreads();
   float* G = a.grad + (size_t)s0 * D;
-  for (int e = threadIdx.x; e < ns * D; e += blockDim.x) {
-    const int ls = e / D, j = e - ls * D;
-    const float v = s_out[ls * LD + j];
-    if (v != 0.f) G[e] += v;
+  for (int e0 = tid; e0 < ns * D; e0 += 128 * U) {  // coalesced read-modify-write, 8 loads in flight
+    float g[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * 128;
+      g[u] = e < ns * D ? G[e] : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * 128;
+      if (e < ns * D) {
+        const int ls = e / D, j = e - ls * D;
+        G[e] = g[u] + sm.out[ls * LD + j];
+      }
+    }
   }
 }
 
@@ -549,6 +626,7 @@ cudaError_t launch_backward(const rtgs_gaussians& g, const rtgs_projected& proj,
   note_launch();
   PBArgs b;
   b.rec = reinterpret_cast<const float4*>(proj.rec);
+  b.recf = proj.rec;
   b.pos = g.pos; b.log_scale = g.log_scale; b.rot = g.rot; b.sh = g.sh;
   b.K = (g.sh_degree + 1) * (g.sh_degree + 1);
   b.D = 10 + 3 * b.K;
@@ -570,11 +648,19 @@ cudaError_t launch_backward(const rtgs_gaussians& g, const rtgs_projected& proj,
   b.loss_out = loss_out;
   b.counts = fwd.counts;
   const int nb = n_slots > 0 ? (n_slots + 127) / 128 : 1;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_project_bwd<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PBSmem<1>));
+    cudaFuncSetAttribute(k_project_bwd<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PBSmem<4>));
+    cudaFuncSetAttribute(k_project_bwd<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PBSmem<9>));
+    cudaFuncSetAttribute(k_project_bwd<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PBSmem<16>));
+    attr = true;
+  }
   switch (b.K) {
-    case 1: k_project_bwd<1><<<nb, 128, 0, s>>>(b); break;
-    case 4: k_project_bwd<4><<<nb, 128, 0, s>>>(b); break;
-    case 9: k_project_bwd<9><<<nb, 128, 0, s>>>(b); break;
-    default: k_project_bwd<16><<<nb, 128, 0, s>>>(b); break;
+    case 1: k_project_bwd<1><<<nb, 128, sizeof(PBSmem<1>), s>>>(b); break;
+    case 4: k_project_bwd<4><<<nb, 128, sizeof(PBSmem<4>), s>>>(b); break;
+    case 9: k_project_bwd<9><<<nb, 128, sizeof(PBSmem<9>), s>>>(b); break;
+    default: k_project_bwd<16><<<nb, 128, sizeof(PBSmem<16>), s>>>(b); break;
   }
   note_launch();
   return cudaGetLastError();

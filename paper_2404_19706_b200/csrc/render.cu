@@ -145,16 +145,16 @@ __global__ void __launch_bounds__(kPipeThreads) k_render_fwd(const FwdArgs a) {
     const int st = b % kPipeStages;
     mbar_wait(&r.full[st], (uint32_t)(b / kPipeStages) & 1u);
     if (!wdone) {
-      const float4* srec = &r.rec[st][0][0];
-      const uint32_t* sgid = r.gid[st];
+      const uint32_t srec = smem_u32(&r.rec[st][0][0]);  // shared addresses, computed once per batch
+      const uint32_t sgid = smem_u32(&r.gid[st][0]);
       const uint32_t pbase = (uint32_t)(start + b * kPipeBatch + 1);
       const int cnt = min(kPipeBatch, n - b * kPipeBatch);
       for (int g0 = 0; g0 < cnt; g0 += 32) {
         const int j = g0 + lane;
         bool ov = false;
         if (j < cnt) {
-          const float4 r0 = srec[3 * j];
-          const float2 ext = unpack_ext(srec[3 * j + 2].w);
+          const float4 r0 = lds128(srec + 48u * j);
+          const float2 ext = unpack_ext(__uint_as_float(lds32(srec + 48u * j + 44u)));
           ov = (r0.x + ext.x >= bx0) && (r0.x - ext.x <= bx1) && (r0.y + ext.y >= by0) && (r0.y - ext.y <= by1);
         }
         uint32_t m = __ballot_sync(0xffffffffu, ov);
@@ -162,10 +162,11 @@ __global__ void __launch_bounds__(kPipeThreads) k_render_fwd(const FwdArgs a) {
           const int idx = g0 + __ffs(m) - 1;
           m &= m - 1;
           // branch-free body: every lane evaluates, the blend is predicated
-          const float4 r0 = srec[3 * idx], r1 = srec[3 * idx + 1], r2 = srec[3 * idx + 2];
+          const uint32_t ra = srec + 48u * idx;
+          const float4 r0 = lds128(ra), r1 = lds128(ra + 16u), r2 = lds128(ra + 32u);
           PairEval e;
           bool ok = eval_pair(r0, r1, fpx, fpy, e) && !done;
-          if (ok && hit < 0 && e.f > kDeltaAlpha) hit = (int)sgid[idx];  // R9: before termination
+          if (ok && hit < 0 && e.f > kDeltaAlpha) hit = (int)lds32(sgid + 4u * idx);  // R9: before termination
           const float test = __fmul_rn(T, __fsub_rn(1.f, e.f));
           const bool term = ok && (test < kTMin);
           done = done || term;

@@ -39,7 +39,20 @@ __device__ __forceinline__ void pipe_init(PipeRing& r) {
   }
 }
 
-// producer: one lane per record slot; `extra(stage, j, gid, src_index)` may issue more cp.async.
+// explicit shared-space 128-bit load (32-bit shared address: no generic-to-shared conversion in
+// the consumers' inner loops)
+__device__ __forceinline__ float4 lds128(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(v) : "r"(addr));
+  return v;
+}
+
+// producer: one lane per record slot; `extra(stage, j, gid)` may issue more cp.async.
 template <typename Extra, typename Flush>
 __device__ __forceinline__ void pipe_produce(PipeRing& r, const float4* __restrict__ rec,
                                              const uint32_t* __restrict__ sorted_gid, int start, int end,
@@ -56,15 +69,24 @@ __device__ __forceinline__ void pipe_produce(PipeRing& r, const float4* __restri
     }
     if (*((volatile int*)&r.alive) > 0) {
       const int cnt = min(kPipeBatch, n - b * kPipeBatch);
-      for (int j = lane; j < cnt; j += 32) {
-        const int i = start + b * kPipeBatch + j;
-        const uint32_t g = sorted_gid[i];
-        cp_async4(&r.gid[st][j], sorted_gid + i);
-        const float4* src = rec + (size_t)4 * g;
-        cp_async16(&r.rec[st][j][0], src);
-        cp_async16(&r.rec[st][j][1], src + 1);
-        cp_async16(&r.rec[st][j][2], src + 2);
-        extra(st, j, g);
+      constexpr int PER = kPipeBatch / 32;
+      uint32_t g[PER];
+#pragma unroll
+      for (int q = 0; q < PER; ++q) {  // all gid loads of the batch in flight together
+        const int j = lane + 32 * q;
+        g[q] = j < cnt ? sorted_gid[start + b * kPipeBatch + j] : 0u;
+      }
+#pragma unroll
+      for (int q = 0; q < PER; ++q) {
+        const int j = lane + 32 * q;
+        if (j < cnt) {
+          cp_async4(&r.gid[st][j], sorted_gid + start + b * kPipeBatch + j);
+          const float4* src = rec + (size_t)4 * g[q];
+          cp_async16(&r.rec[st][j][0], src);
+          cp_async16(&r.rec[st][j][1], src + 1);
+          cp_async16(&r.rec[st][j][2], src + 2);
+          extra(st, j, g[q]);
+        }
       }
     }
     cp_async_mbar_arrive(&r.full[st]);
