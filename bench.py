@@ -39,7 +39,7 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 100 ms during the timed region."""
+    """nvidia-smi clocks / throttle reasons sampled every 20 ms during the timed region."""
 
     def __init__(self, idx: int):
         self.idx = idx
@@ -51,7 +51,7 @@ class ClockSampler:
              "clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
@@ -160,7 +160,7 @@ def reference_arm(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C3")
@@ -206,6 +206,26 @@ def main():
     dep = torch.as_tensor(dep_h, device="cuda")
     stream = torch.cuda.current_stream()
 
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+    # Stationary workload: every timed step starts from the same map and optimiser state (the first
+    # iteration of a window), restored outside the timed events like the L2 flush.  Without
+    # this, hundreds of Adam steps on one frame drift the unstable Gaussians and change the work.
+    snap = {k: getattr(gm, k).clone() for k in ("pos", "log_scale", "rot", "sh")}
+    snap_eta = eng.eta.clone()
+
+    def restore():
+        for k, v in snap.items():
+            getattr(gm, k).copy_(v)
+        eng.m.zero_()
+        eng.v.zero_()
+        eng.grad.zero_()
+        eng.eta.copy_(snap_eta)
+        eng.step_dev.zero_()
+
+    def between_steps():
+        restore()
+        flush.zero_()
+
     def step(c, d, frame_idx):
         # ingest (side stream) || masked iteration (current stream); Adam waits for the ingest projection
         eng.step(c, d, pose, seed=1234, frame_idx=frame_idx, reduce_grads=allreduce_grads if world > 1 else None)
@@ -237,7 +257,6 @@ def main():
     if max(n_inst, n_inst_iter0) > eng.capacity:
         raise RuntimeError(f"instance capacity {eng.capacity} < {max(n_inst, n_inst_iter0)}")
 
-    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")  # > 126 MB L2
 
     # ---- device-timed region: K steps, L2 flushed between steps (outside the events) -------------
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -247,8 +266,12 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
+        t_spin = time.perf_counter()
+        while time.perf_counter() - t_spin < 0.25:  # keep the GPU busy while nvidia-smi starts sampling
+            run_step(0)
+        torch.cuda.synchronize()
         for i in range(args.steps):
-            flush.zero_()
+            between_steps()
             starts[i].record(stream)
             run_step(i)
             ends[i].record(stream)
@@ -272,7 +295,7 @@ def main():
             e.record(stream)
             ev.setdefault(name, []).append(e)
 
-        flush.zero_()
+        between_steps()
         mark("start")
         P.project_gaussians(gm, pose, cam, eng.proj_full); mark("ingest.project")
         P.bin_and_sort(eng.proj_full, gm.n, cam, None, eng.bins_full, eng.ws_bin_full); mark("ingest.bin_and_sort")
@@ -301,6 +324,18 @@ def main():
             torch.cuda.synchronize()
             pt.append(e0.elapsed_time(e1))
         phases["project_alone_ms"] = statistics.mean(pt)
+        # the FULL render alone (dominant kernel of the step), same protocol
+        rt = []
+        for _ in range(reps):
+            flush.zero_()
+            e0.record(stream)
+            P.render_color_depth(gm, eng.proj_full, eng.bins_full, pose, cam, P.RTGS_RENDER_FULL, eng.full)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            rt.append(e0.elapsed_time(e1))
+        phases["render_full_alone_ms"] = statistics.mean(rt)
+        blends_full = int(eng.full.counts[3].item())
+        blends_masked = int(eng.out.counts[3].item())
         counts_full = None
         counts = eng.out.counts.cpu().numpy().tolist()
         ninst_iter = int(eng.bins.n_instances.item())
@@ -309,25 +344,48 @@ def main():
                               "n_inst_full": n_inst}), file=sys.stderr)
         _ = counts_full
 
-    # ---- e2e: host frame in pinned memory -> device, step, loss + counts back ----------------------
+    # ---- e2e: host frames in pinned memory -> device, step, loss + add counts back to the host ------
+    # Streamed like a live system: the H2D copy of frame i+1 (copy stream, double-buffered staging)
+    # overlaps the step of frame i; each step's copy and its D2H read-back are inside the timed span.
+    n_e2e = max(10, args.steps // 2)
     col_pin = torch.as_tensor(col_h).pin_memory()
     dep_pin = torch.as_tensor(dep_h).pin_memory()
-    loss_h = torch.empty(4, dtype=torch.float32).pin_memory()
-    cnt_h = torch.empty(5, dtype=torch.int32).pin_memory()
-    e2e = []
-    for i in range(max(3, args.steps // 2)):
-        flush.zero_()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        col.copy_(col_pin, non_blocking=True)   # the graph reads the frame from these device buffers
-        dep.copy_(dep_pin, non_blocking=True)
+    loss_h = torch.empty((n_e2e, 4), dtype=torch.float32).pin_memory()
+    cnt_h = torch.empty((n_e2e, 5), dtype=torch.int32).pin_memory()
+    st_col = [torch.empty_like(col) for _ in range(2)]
+    st_dep = [torch.empty_like(dep) for _ in range(2)]
+    copy_stream = torch.cuda.Stream()
+    ev_copied = [torch.cuda.Event() for _ in range(2)]
+    ev_free = [torch.cuda.Event() for _ in range(2)]
+    restore()
+    flush.zero_()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    copy_stream.wait_stream(stream)
+
+    def h2d(i):
+        with torch.cuda.stream(copy_stream):
+            if i >= 2:
+                copy_stream.wait_event(ev_free[i % 2])
+            st_col[i % 2].copy_(col_pin, non_blocking=True)
+            st_dep[i % 2].copy_(dep_pin, non_blocking=True)
+            ev_copied[i % 2].record(copy_stream)
+
+    h2d(0)
+    for i in range(n_e2e):
+        if i + 1 < n_e2e:
+            h2d(i + 1)
+        stream.wait_event(ev_copied[i % 2])
+        col.copy_(st_col[i % 2])   # the graph reads the frame from these device buffers
+        dep.copy_(st_dep[i % 2])
+        ev_free[i % 2].record(stream)
         run_step(i)
-        loss_h.copy_(eng.loss, non_blocking=True)
-        cnt_h.copy_(eng.add_counts, non_blocking=True)
-        b.record(stream)
-        torch.cuda.synchronize()
-        e2e.append(a.elapsed_time(b))
-    t_e2e = statistics.mean(e2e)
+        loss_h[i].copy_(eng.loss, non_blocking=True)
+        cnt_h[i].copy_(eng.add_counts, non_blocking=True)
+    b.record(stream)
+    torch.cuda.synchronize()
+    t_e2e = a.elapsed_time(b) / n_e2e
     if world > 1:
         tt = torch.tensor([t_e2e], device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -335,13 +393,20 @@ def main():
 
     if rank == 0:
         hbm, sm_max, peak_kind = _peaks()
+        clocks = clk.summary()
+        clk_sm_mhz = clocks.get("sm_mhz")
         K = (cfg.sh_degree + 1) ** 2
         # A1 algorithmic bytes per visible Gaussian: read pos 12, log_scale 12, rot 16, opacity 4, SH 12K,
         # write rec 64, zkey 4, rect 8, tiles_touched 4
         bytes_per_g = 12 + 12 + 16 + 4 + 12 * K + 64 + 4 + 8 + 4
         t_proj_s = phases["project_alone_ms"] * 1e-3
         achieved = bytes_per_g * cfg.n / t_proj_s / 1e9
-        clocks = clk.summary()
+        # A3/A4 (dominant kernel): 16 FP32 instructions per blended (pixel, Gaussian) pair;
+        # peak = FP32 issue of 148 SMs x 128 lanes x the sampled SM clock (1 instruction / lane / clock)
+        t_render_s = phases["render_full_alone_ms"] * 1e-3
+        clk_ghz = (clk_sm_mhz or sm_max) * 1e-3
+        alu_peak = 148 * 128 * clk_ghz * 1e9 / 1e12
+        alu_achieved = 16 * blends_full / t_render_s / 1e12
         value = world * 1e3 / t_step
         line = {
             "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
@@ -354,9 +419,16 @@ def main():
                        "l2": "flushed between timed steps (256 MB write); Gaussian SoA 237 MB > L2",
                        "launch": "CUDA graph of the whole step (2 streams)" if graph is not None else "eager",
                        "parallelism": f"dp{world} over keyframe views" if world > 1 else "single GPU"},
-            "roofline": {"kernel": "k_project (A1)", "bound": "hbm", "achieved": achieved, "peak": hbm,
-                         "unit": "GB/s", "frac": achieved / hbm, "traffic": None, "peak_kind": peak_kind,
-                         "bytes_per_gaussian": bytes_per_g},
+            "roofline": {"kernel": "k_render_fwd<FULL> (A3/A4, dominant kernel of the step)", "bound": "alu",
+                         "achieved": alu_achieved, "peak": alu_peak, "unit": "TFLOP/s", "frac": alu_achieved / alu_peak,
+                         "traffic": None, "peak_kind": "derived: 148 SM x 128 FP32 lanes x sampled SM clock",
+                         "algorithmic": f"16 FP32 instr x {blends_full} blends per launch",
+                         "time_ms": phases["render_full_alone_ms"]},
+            "roofline_secondary": [{"kernel": "k_project (A1)", "bound": "hbm", "achieved": achieved, "peak": hbm,
+                                    "unit": "GB/s", "frac": achieved / hbm, "peak_kind": peak_kind,
+                                    "bytes_per_gaussian": bytes_per_g, "time_ms": phases["project_alone_ms"]}],
+            "blends": {"full_per_frame": blends_full, "masked_per_iter": blends_masked,
+                       "full_blends_per_s": blends_full / t_render_s},
             "clocks": clocks,
             "gpu_launches": int(launches),
             "e2e": {"value": world * 1e3 / t_e2e, "unit": "iters/s",

@@ -115,7 +115,9 @@ typedef struct {
   uint8_t* tile_keep;    /* [TX*TY]    1 iff >= 50 % of the tile's pixels are active (R15) */
   uint32_t* tile_list;   /* [TX*TY]    ids of kept tiles (order unspecified)                      */
   uint32_t* counts;      /* [4] device: [0] #kept tiles, [1] |P| (active pixels in kept tiles),
-                                        [2] |M_unstable|, [3] reserved                             */
+                                        [2] |M_unstable| (all three written by COVERAGE), [3] number of
+                                        blended (pixel, Gaussian) pairs of the last FULL / MASKED render
+                                        (NULLABLE in FULL mode)                                    */
 } rtgs_render_out;
 
 /* Target RGBD frame C_k, D_k: color [3][H][W] in [0,1]; depth [H][W] metres, <= 0 or

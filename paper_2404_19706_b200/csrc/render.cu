@@ -139,6 +139,7 @@ __global__ void __launch_bounds__(kPipeThreads) k_render_fwd(const FwdArgs a) {
   float T = 1.f, cr = 0.f, cg = 0.f, cb = 0.f;
   int hit = -1;
   uint32_t last = (uint32_t)start;
+  uint32_t nblend = 0;  // blended (pixel, Gaussian) pairs of this lane (-> counts[3])
   bool wdone = __all_sync(0xffffffffu, done);
   if (wdone && lane == 0) atomicSub(&r.alive, 1);
   for (int b = 0; b < nb; ++b) {
@@ -177,6 +178,7 @@ __global__ void __launch_bounds__(kPipeThreads) k_render_fwd(const FwdArgs a) {
           cb = __fmaf_rn(r2.z, wgt, cb);
           T = ok ? test : T;
           last = ok ? pbase + (uint32_t)idx : last;
+          nblend += ok ? 1u : 0u;
         }
         if (__all_sync(0xffffffffu, done)) {
           wdone = true;
@@ -187,6 +189,10 @@ __global__ void __launch_bounds__(kPipeThreads) k_render_fwd(const FwdArgs a) {
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&r.empty[st]);
+  }
+  if (a.counts) {
+    const uint32_t wsum = __reduce_add_sync(0xffffffffu, nblend);
+    if (lane == 0 && wsum) atomicAdd(const_cast<uint32_t*>(a.counts) + 3, wsum);
   }
 
   if (!want) return;
@@ -251,6 +257,7 @@ cudaError_t launch_render(const rtgs_projected& proj, const rtgs_bins& bins, con
   a.color = out.color; a.trans = out.trans; a.depth = out.depth; a.normal = out.normal;
   a.index = out.index; a.n_contrib = out.n_contrib;
   const int T = a.cam.TX * a.cam.TY;
+  if (out.counts) cudaMemsetAsync(out.counts + 3, 0, 4, s);  // blend counter of this render
   if (masked) k_render_fwd<true><<<T, kPipeThreads, 0, s>>>(a);
   else k_render_fwd<false><<<T, kPipeThreads, 0, s>>>(a);
   note_launch();
