@@ -404,6 +404,11 @@ def main():
         # A3/A4 (dominant kernel): 16 FP32 instructions per blended (pixel, Gaussian) pair;
         # peak = FP32 issue of 148 SMs x 128 lanes x the sampled SM clock (1 instruction / lane / clock)
         t_render_s = phases["render_full_alone_ms"] * 1e-3
+        traffic = {}
+        tp = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tp):
+            with open(tp) as f:
+                traffic = json.load(f)
         clk_ghz = (clk_sm_mhz or sm_max) * 1e-3
         alu_peak = 148 * 128 * clk_ghz * 1e9 / 1e12
         alu_achieved = 16 * blends_full / t_render_s / 1e12
@@ -421,11 +426,12 @@ def main():
                        "parallelism": f"dp{world} over keyframe views" if world > 1 else "single GPU"},
             "roofline": {"kernel": "k_render_fwd<FULL> (A3/A4, dominant kernel of the step)", "bound": "alu",
                          "achieved": alu_achieved, "peak": alu_peak, "unit": "TFLOP/s", "frac": alu_achieved / alu_peak,
-                         "traffic": None, "peak_kind": "derived: 148 SM x 128 FP32 lanes x sampled SM clock",
+                         "traffic": traffic.get("k_render_fwd<FULL>"), "peak_kind": "derived: 148 SM x 128 FP32 lanes x sampled SM clock",
                          "algorithmic": f"16 FP32 instr x {blends_full} blends per launch",
                          "time_ms": phases["render_full_alone_ms"]},
             "roofline_secondary": [{"kernel": "k_project (A1)", "bound": "hbm", "achieved": achieved, "peak": hbm,
                                     "unit": "GB/s", "frac": achieved / hbm, "peak_kind": peak_kind,
+                                    "traffic": traffic.get("k_project"),
                                     "bytes_per_gaussian": bytes_per_g, "time_ms": phases["project_alone_ms"]}],
             "blends": {"full_per_frame": blends_full, "masked_per_iter": blends_masked,
                        "full_blends_per_s": blends_full / t_render_s},
