@@ -189,6 +189,42 @@ def unstable_coverage(proj: dict, unstable: np.ndarray, pixels: np.ndarray, chun
     return cov, marg
 
 
+def unstable_coverage_splat(proj: dict, unstable: np.ndarray, width: int, height: int):
+    """Same result as `unstable_coverage` over the whole image, evaluated only at the pixels of each
+    unstable Gaussian's support rect (R7: the rect contains every pixel where the support test can
+    pass, pinned in tests/test_oracle_projection.py), so full-size frames are affordable.
+    Cross-checked against the dense definition in tests/test_oracle_raster.py.
+    Returns (bool [H, W], margin [H, W])."""
+    cov = np.zeros(height * width, dtype=bool)
+    marg = np.full(height * width, np.inf)
+    rect = proj["rect"]
+    sel = np.nonzero(proj["valid"] & unstable & (rect[:, 0] <= rect[:, 2]) & (rect[:, 1] <= rect[:, 3]))[0]
+    if len(sel) == 0:
+        return cov.reshape(height, width), marg.reshape(height, width)
+    wx = rect[sel, 2] - rect[sel, 0] + 1
+    wy = rect[sel, 3] - rect[sel, 1] + 1
+    cnt = wx * wy
+    g = np.repeat(sel, cnt)
+    k = np.arange(cnt.sum()) - np.repeat(np.cumsum(cnt) - cnt, cnt)
+    px = rect[g, 0] + k % np.repeat(wx, cnt)
+    py = rect[g, 1] + k // np.repeat(wx, cnt)
+    with torch.no_grad():
+        mu = proj["mu"].numpy()[g]
+        con = proj["conic"].numpy()[g]
+        alpha = proj["alpha"].numpy()[g]
+    dx = mu[:, 0] - px
+    dy = mu[:, 1] - py
+    power = -0.5 * (con[:, 0] * dx * dx + con[:, 2] * dy * dy) - con[:, 1] * dx * dy
+    fraw = alpha * np.exp(power)
+    f = np.where(fraw < F_MAX, fraw, F_MAX)
+    passes = (power >= POWER_MIN) & (f >= F_MIN)
+    lin = py * width + px
+    cov[lin[passes]] = True
+    m = np.minimum(_rel(power, POWER_MIN), np.abs(f - F_MIN) / F_MIN)
+    np.minimum.at(marg, lin, m)
+    return cov.reshape(height, width), marg.reshape(height, width)
+
+
 def tile_keep(coverage_img: np.ndarray) -> np.ndarray:
     """P:497 / R15: keep tile iff (#active pixels) >= 0.5 * (#in-image pixels of the tile)."""
     H, W = coverage_img.shape

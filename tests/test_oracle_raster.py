@@ -241,3 +241,19 @@ def test_tile_keep_half_rule():
     assert list(keep) == [False, True, False, False, False, False, False, False, True]
     act = RS.active_set(img, keep)
     assert act.sum() == 128 + 64
+
+
+def test_splat_coverage_equals_dense_definition():
+    from synth import CONFIGS, make_pose, make_scene
+    for name in ("C1b", "T3"):
+        cfg = CONFIGS[name]
+        sc = make_scene(cfg)
+        R, t = make_pose(cfg)
+        c = P.camera(cfg)
+        pr = P.project(P.params_from_scene(sc), R, t, c, sc["sh_degree"])
+        unstable = (sc["flags"] & 2) == 0
+        dense, dm = RS.unstable_coverage(pr, unstable, RS.all_pixels(cfg.width, cfg.height))
+        splat, sm = RS.unstable_coverage_splat(pr, unstable, cfg.width, cfg.height)
+        np.testing.assert_array_equal(splat, dense.reshape(cfg.height, cfg.width))
+        # margins: the splat version sees only rect pixels, so its margin is >= the dense one
+        assert (sm.ravel() >= dm - 1e-15).all()
