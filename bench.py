@@ -334,6 +334,22 @@ def main():
             torch.cuda.synchronize()
             rt.append(e0.elapsed_time(e1))
         phases["render_full_alone_ms"] = statistics.mean(rt)
+        # NEXT f1 (once per window, not part of the step): Eq.9 fusion and the state transitions
+        from paper_2404_19706_b200 import mapping as M
+        e0.record(stream)
+        M.fuse_window(gm, eng.gid_of_slot, eng.before, eng.eta_before, eng.eta)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        phases["window.fuse_ms"] = e0.elapsed_time(e1)
+        flags_keep = gm.flags.clone()
+        e0.record(stream)
+        M.manage_states(eng.full, col, dep, cam, gm.flags, eng.err_count, eng.eta, eng.t_created,
+                        M.state_params(1), eng.state_counts, eng.ws_state)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        phases["window.manage_states_ms"] = e0.elapsed_time(e1)
+        gm.flags.copy_(flags_keep)
+        restore()
         blends_full = int(eng.full.counts[3].item())
         blends_masked = int(eng.out.counts[3].item())
         counts_full = None

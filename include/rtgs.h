@@ -56,7 +56,7 @@ typedef struct {
  *   rot       [n][4]  quaternion (w, x, y, z), normalised inside the forward pass (R3)
  *   opacity   [n]     alpha: 0.99 opaque / 0.1 transparent; never optimised (lr_alpha = 0)
  *   sh        [n][K][3], K = (sh_degree+1)^2, coefficient-major, channel-minor (R2)
- *   flags     [n]     bit0 = transparent, bit1 = stable (eta > delta_eta) */
+ *   flags     [n]     bit0 = transparent, bit1 = stable (eta > delta_eta), bit2 = removed */
 typedef struct {
   const float *pos, *log_scale, *rot, *opacity, *sh;
   const uint8_t *flags;
@@ -242,6 +242,41 @@ rtgs_status rtgs_classify_and_add_pixels(const rtgs_render_out* full, const rtgs
                                          const rtgs_camera* cam, const rtgs_add_params* ap, uint8_t* pixel_class,
                                          uint32_t* samples, uint32_t cap, uint32_t* counts, void* workspace,
                                          size_t workspace_bytes, void* stream);
+
+/* =============================================================================================
+ * NEXT row f1: window fusion and state management, run after each optimisation window.
+ * flags bit2 = removed (an absorbing state; rtgs_project_gaussians culls removed Gaussians).
+ * ============================================================================================= */
+
+/* rtgs_fuse_window (Eq.9): for every slot s (gid = gid_of_slot[s]),
+ *   w = (eta'[gid] - eta_before[s]) / eta'[gid]   (w = 0 when eta' = 0),
+ *   theta = (1 - w) before[s] + w theta'   for all 10 + 3K stored components (pos, log_scale,
+ *   unnormalised quaternion, SH; reading R27: component-wise, the forward normalises q).
+ * before [n_slots][10+3K]: parameters at the start of the window (same row layout as grad). */
+rtgs_status rtgs_fuse_window(rtgs_params* params, const int32_t* gid_of_slot, int32_t n_slots, const float* before,
+                             const uint32_t* eta_before, const uint32_t* eta, void* stream);
+
+/* State thresholds (delta_e, delta_t unstated in the paper: reading R28). */
+typedef struct {
+  float delta_c, delta_d;            /* colour / depth error thresholds (P:273 reuses delta_c, delta_d) */
+  uint32_t delta_e, delta_eta, delta_t;
+  uint32_t frame_idx;                /* k */
+} rtgs_state_params;
+
+/* rtgs_manage_states on the optimised scene's FULL render at frame k:
+ *  1. every pixel with valid depth whose hit Gaussian I^ is stable and whose error exceeds a
+ *     threshold (mean |dRGB| > delta_c, float32 order of A7, or |D^ - D| > delta_d) marks that
+ *     Gaussian; every marked Gaussian gets e += 1 (once per frame, R28);
+ *  2. per Gaussian, from its state at entry: stable with e > delta_e -> unstable (e, eta reset,
+ *     t = k, R29); unstable with eta > delta_eta -> stable; otherwise unstable with
+ *     k - t > delta_t -> removed.  Removed Gaussians are untouched.
+ * err_count, eta, t_created [n] uint32 in/out; flags [n] in/out; counts [4] device out:
+ * #marked, #stable->unstable, #unstable->stable, #removed.  workspace: rtgs_state_workspace_size(n). */
+size_t rtgs_state_workspace_size(int32_t n);
+rtgs_status rtgs_manage_states(const rtgs_render_out* full, const rtgs_frame* frame, const rtgs_camera* cam,
+                               uint8_t* flags, uint32_t* err_count, uint32_t* eta, uint32_t* t_created, int32_t n,
+                               const rtgs_state_params* sp, uint32_t* counts, void* workspace, size_t workspace_bytes,
+                               void* stream);
 
 /* Utilities */
 const char* rtgs_status_string(rtgs_status s);

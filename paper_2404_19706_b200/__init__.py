@@ -7,6 +7,7 @@ fallback: importing the binding and calling it without the built library raises.
 from ._abi import LIB_PATH, RTGSError, lib  # noqa: F401
 from .mapping import (GaussianMap, MappingEngine, ProjectedBuffers, BinBuffers, RenderBuffers,  # noqa: F401
                       project_gaussians, bin_and_sort, render_color_depth, render_backward_masked,
-                      adam_step_unstable, classify_and_add_pixels, make_camera, make_pose, camera_of,
+                      adam_step_unstable, classify_and_add_pixels, fuse_window, manage_states, state_params,
+                      make_camera, make_pose, camera_of,
                       hparams, add_params, launch_count, RTGS_RENDER_FULL, RTGS_RENDER_MASKED,
                       RTGS_RENDER_COVERAGE)

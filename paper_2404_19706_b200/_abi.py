@@ -62,6 +62,11 @@ class AddParams(C.Structure):
                 ("seed", C.c_uint64), ("frame_idx", C.c_uint32)]
 
 
+class StateParams(C.Structure):
+    _fields_ = [("delta_c", C.c_float), ("delta_d", C.c_float), ("delta_e", C.c_uint32), ("delta_eta", C.c_uint32),
+                ("delta_t", C.c_uint32), ("frame_idx", C.c_uint32)]
+
+
 P = C.POINTER
 EXPORTS = {
     "rtgs_project_gaussians": (C.c_int, [P(Gaussians), P(Pose), P(Camera), P(Projected), vp]),
@@ -77,6 +82,10 @@ EXPORTS = {
     "rtgs_classify_workspace_size": (C.c_size_t, [P(Camera)]),
     "rtgs_classify_and_add_pixels": (C.c_int, [P(RenderOut), P(Frame), vp, P(Camera), P(AddParams), vp, vp, C.c_uint32,
                                                vp, vp, C.c_size_t, vp]),
+    "rtgs_fuse_window": (C.c_int, [P(Params), vp, C.c_int32, vp, vp, vp, vp]),
+    "rtgs_state_workspace_size": (C.c_size_t, [C.c_int32]),
+    "rtgs_manage_states": (C.c_int, [P(RenderOut), P(Frame), P(Camera), vp, vp, vp, vp, C.c_int32, P(StateParams), vp,
+                                     vp, C.c_size_t, vp]),
     "rtgs_status_string": (C.c_char_p, [C.c_int]),
     "rtgs_last_cuda_error": (C.c_char_p, []),
     "rtgs_version": (C.c_int32, []),

@@ -146,6 +146,30 @@ rtgs_status rtgs_classify_and_add_pixels(const rtgs_render_out* full, const rtgs
                                 S(stream)));
 }
 
+rtgs_status rtgs_fuse_window(rtgs_params* params, const int32_t* gid_of_slot, int32_t n_slots, const float* before,
+                             const uint32_t* eta_before, const uint32_t* eta, void* stream) {
+  if (!params || n_slots < 0 || params->sh_degree < 0 || params->sh_degree > 3) return RTGS_ERR_INVALID_ARG;
+  if (n_slots > 0 && (!params->pos || !params->log_scale || !params->rot || !params->sh || !gid_of_slot || !before ||
+                      !eta_before || !eta))
+    return RTGS_ERR_INVALID_ARG;
+  return finish(launch_fuse(*params, gid_of_slot, n_slots, before, eta_before, eta, S(stream)));
+}
+
+size_t rtgs_state_workspace_size(int32_t n) { return n < 0 ? 0 : state_workspace_size(n); }
+
+rtgs_status rtgs_manage_states(const rtgs_render_out* full, const rtgs_frame* frame, const rtgs_camera* cam,
+                               uint8_t* flags, uint32_t* err_count, uint32_t* eta, uint32_t* t_created, int32_t n,
+                               const rtgs_state_params* sp, uint32_t* counts, void* workspace, size_t workspace_bytes,
+                               void* stream) {
+  if (!full || !full->color || !full->depth || !full->index || !frame || !frame->color || !frame->depth ||
+      !cam_ok(cam) || !sp || !counts || n < 0)
+    return RTGS_ERR_INVALID_ARG;
+  if (n > 0 && (!flags || !err_count || !eta || !t_created)) return RTGS_ERR_INVALID_ARG;
+  if (!workspace || workspace_bytes < state_workspace_size(n)) return RTGS_ERR_WORKSPACE;
+  return finish(launch_manage_states(*full, *frame, *cam, flags, err_count, eta, t_created, n, *sp, counts, workspace,
+                                     S(stream)));
+}
+
 const char* rtgs_status_string(rtgs_status s) {
   switch (s) {
     case RTGS_OK: return "RTGS_OK";

@@ -44,6 +44,13 @@ cudaError_t launch_classify(const rtgs_render_out& full, const rtgs_frame& frame
                             const rtgs_camera& cam, const rtgs_add_params& ap, uint8_t* cls, uint32_t* samples,
                             uint32_t cap, uint32_t* counts, void* ws, cudaStream_t s);
 
+cudaError_t launch_fuse(const rtgs_params& p, const int32_t* gid_of_slot, int n_slots, const float* before,
+                        const uint32_t* eta_before, const uint32_t* eta, cudaStream_t s);
+size_t state_workspace_size(int n);
+cudaError_t launch_manage_states(const rtgs_render_out& full, const rtgs_frame& frame, const rtgs_camera& cam,
+                                 uint8_t* flags, uint32_t* err, uint32_t* eta, uint32_t* tc, int n,
+                                 const rtgs_state_params& sp, uint32_t* counts, void* ws, cudaStream_t s);
+
 // generic device-wide exclusive scan of uint32 (length known on the host; zeros past the live part)
 size_t scan_workspace_size(size_t len);
 cudaError_t launch_scan(const uint32_t* in, uint32_t* out, size_t len, uint32_t* total, void* ws, cudaStream_t s);

@@ -17,6 +17,7 @@ struct ProjArgs {
   const float* rot;
   const float* opacity;
   const float* sh;
+  const uint8_t* flags;  // nullable; bit2 = removed (NEXT f1)
   int n, K;
   double V[9], tp[3], campos[3];
   float Vz0, Vz1, Vz2, tz;  // float32 key sequence (R8)
@@ -95,7 +96,8 @@ __global__ void __launch_bounds__(kProjThreads) k_project(const ProjArgs a) {
     // R8: float32 key, every product and sum rounded, no FMA
     const float zk = __fadd_rn(__fadd_rn(__fadd_rn(__fmul_rn(a.Vz0, px), __fmul_rn(a.Vz1, py)), __fmul_rn(a.Vz2, pz)), a.tz);
     const float kext = (alpha * 255.f > 1.f) ? fminf(3.f, sqrtf(2.f * logf(255.f * alpha))) : 0.f;
-    if (zk > kNear && kext > 0.f) {
+    const bool removed = a.flags && (a.flags[i] & 4u);
+    if (zk > kNear && kext > 0.f && !removed) {
       // camera frame in float64: p_c = V p + t'
       const double X = fma(a.V[0], (double)px, fma(a.V[1], (double)py, fma(a.V[2], (double)pz, a.tp[0])));
       const double Y = fma(a.V[3], (double)px, fma(a.V[4], (double)py, fma(a.V[5], (double)pz, a.tp[1])));
@@ -215,6 +217,7 @@ cudaError_t launch_project(const rtgs_gaussians& g, const PoseF& pose, const rtg
   if (g.n == 0) return cudaSuccess;
   ProjArgs a;
   a.pos = g.pos; a.log_scale = g.log_scale; a.rot = g.rot; a.opacity = g.opacity; a.sh = g.sh;
+  a.flags = g.flags;
   a.n = g.n;
   a.K = (g.sh_degree + 1) * (g.sh_degree + 1);
   for (int k = 0; k < 9; ++k) { a.V[k] = pose.V[k]; a.Vf[k] = pose.Vf[k]; }

@@ -217,6 +217,33 @@ def classify_and_add_pixels(full: RenderBuffers, frame_color: torch.Tensor, fram
                                              _stream(stream)), "rtgs_classify_and_add_pixels")
 
 
+def fuse_window(gm: GaussianMap, gid_of_slot: torch.Tensor, before: torch.Tensor, eta_before: torch.Tensor,
+                eta: torch.Tensor, stream=None):
+    """NEXT f1: Eq.9 fusion of the window's result with the parameters before the window."""
+    prm = gm.c_params()
+    check(lib().rtgs_fuse_window(C.byref(prm), _p(gid_of_slot), int(gid_of_slot.numel()), _p(before), _p(eta_before),
+                                 _p(eta), _stream(stream)), "rtgs_fuse_window")
+
+
+def state_params(frame_idx: int, delta_c=0.1, delta_d=0.1, delta_e=3, delta_eta=100, delta_t=30) -> _abi.StateParams:
+    return _abi.StateParams(delta_c, delta_d, delta_e, delta_eta, delta_t, frame_idx)
+
+
+def manage_states(full: RenderBuffers, frame_color: torch.Tensor, frame_depth: torch.Tensor, cam: _abi.Camera,
+                  flags: torch.Tensor, err_count: torch.Tensor, eta: torch.Tensor, t_created: torch.Tensor,
+                  sp: _abi.StateParams, counts: torch.Tensor, workspace: torch.Tensor, stream=None):
+    """NEXT f1: error counts from the optimised render and the stable / unstable / removed transitions."""
+    o = full.c_struct()
+    fr = _abi.Frame(_p(frame_color), _p(frame_depth))
+    check(lib().rtgs_manage_states(C.byref(o), C.byref(fr), C.byref(cam), _p(flags), _p(err_count), _p(eta),
+                                   _p(t_created), int(flags.numel()), C.byref(sp), _p(counts), _p(workspace),
+                                   workspace.numel() * workspace.element_size(), _stream(stream)), "rtgs_manage_states")
+
+
+def state_workspace_size(n: int) -> int:
+    return int(lib().rtgs_state_workspace_size(n))
+
+
 def hparams(preset: str = "replica") -> _abi.HParams:
     """Learning rates of P:501: Replica / ScanNet++ vs Azure / TUM."""
     if preset in ("replica", "scannetpp"):
@@ -259,6 +286,10 @@ class MappingEngine:
                                    device=device)
         self.add_counts = torch.zeros(5, dtype=torch.int32, device=device)
         self.eta = torch.zeros(n, dtype=torch.int32, device=device)
+        self.err_count = torch.zeros(n, dtype=torch.int32, device=device)   # e_i
+        self.t_created = torch.zeros(n, dtype=torch.int32, device=device)   # t_i
+        self.state_counts = torch.zeros(4, dtype=torch.int32, device=device)
+        self.ws_state = torch.empty(state_workspace_size(n), dtype=torch.uint8, device=device)
         self.reset_window()
 
     def reset_window(self):
@@ -280,6 +311,11 @@ class MappingEngine:
             if n_slots else torch.zeros((1, 10), device=self.device)
         self.ws_bwd = torch.empty(backward_workspace_size(n_slots), dtype=torch.uint8, device=self.device)
         self.step_count = 0
+        # window start: parameters and eta of the slots, for the Eq.9 fusion at the window end (f1)
+        self.before = torch.cat([self.gm.pos[gid_t], self.gm.log_scale[gid_t], self.gm.rot[gid_t],
+                                 self.gm.sh[gid_t].reshape(n_slots, -1)], 1).contiguous() if n_slots else \
+            torch.zeros((1, D), device=self.device)
+        self.eta_before = self.eta[gid_t].clone() if n_slots else torch.zeros(1, dtype=torch.int32, device=self.device)
         self.step_dev = torch.zeros(1, dtype=torch.int32, device=self.device)  # graph-replayable step
 
     # --- the two flows ---------------------------------------------------------------------------
@@ -322,6 +358,19 @@ class MappingEngine:
         self.forward_masked(pose, stream)
         self.backward(frame_color, frame_depth, pose, stream)
         self.optimizer_step(stream)
+
+    def end_window(self, frame_color, frame_depth, pose: _abi.Pose, frame_idx: int, state=None, stream=None):
+        """NEXT f1, after a window's iterations: Eq.9 fusion with the window-start parameters, then the
+        optimised scene's FULL render at frame k and the state transitions.  The slot set
+        and optimiser state are rebuilt for the next window."""
+        fuse_window(self.gm, self.gid_of_slot, self.before, self.eta_before, self.eta, stream)
+        project_gaussians(self.gm, pose, self.cam, self.proj_full, stream)
+        bin_and_sort(self.proj_full, self.gm.n, self.cam, None, self.bins_full, self.ws_bin_full, stream)
+        render_color_depth(self.gm, self.proj_full, self.bins_full, pose, self.cam, RTGS_RENDER_FULL, self.full, stream)
+        sp = state if state is not None else state_params(frame_idx)
+        manage_states(self.full, frame_color, frame_depth, self.cam, self.gm.flags, self.err_count, self.eta,
+                      self.t_created, sp, self.state_counts, self.ws_state, stream)
+        self.reset_window()
 
     def step(self, frame_color, frame_depth, pose: _abi.Pose, ingest_pose=None, seed=0, frame_idx=0,
              reduce_grads=None):
