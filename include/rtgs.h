@@ -99,6 +99,12 @@ typedef struct {
   uint32_t* tile_range;
   uint32_t* n_instances;
   uint32_t capacity;
+  /* NEXT f3 (rtgs_bin_and_sort_cached writes these; NULL for every other producer of bins):
+   * an entry e with bit 31 set is row r = e & 0x7FFFFFFF of a SUBSET projection (sub_rec [rows][16],
+   * sub_zkey [rows]) of the Gaussian sub_gid[r]; entries without bit 31 are gids of `proj`. */
+  const float* sub_rec;
+  const uint32_t* sub_zkey;
+  const int32_t* sub_gid;
 } rtgs_bins;
 
 enum { RTGS_RENDER_FULL = 0, RTGS_RENDER_MASKED = 1, RTGS_RENDER_COVERAGE = 2 };
@@ -177,7 +183,8 @@ rtgs_status rtgs_bin_and_sort(const rtgs_projected* proj, int32_t n, const rtgs_
  *  mode MASKED:   only the active pixels P = M_unstable ∩ kept tiles (out->active_bits, out->tile_keep,
  *                 out->tile_list, out->counts[0] from a previous COVERAGE call); same outputs, other
  *                 pixels untouched.  Needs proj, bins (binned with the same tile_keep or with all tiles).
- *  mode COVERAGE: M_unstable(u) = [some unstable (flags bit1 clear), non-culled Gaussian has
+ *  mode COVERAGE: M_unstable(u) = [some unstable (flags bit1 clear; every row when g->flags is NULL,
+ *                 e.g. an rtgs_project_subset of the unstable slots), non-culled Gaussian has
  *                 power >= -4.5 and f >= 1/255 at u] (exactly T^_unstable(u) < 1, R16), tile keep
  *                 (>= 50 % of in-image pixels), kept-tile list, counts.  Writes active_bits, tile_keep,
  *                 tile_list, counts; needs proj and g->flags only (bins may be NULL).
@@ -197,6 +204,7 @@ rtgs_status rtgs_render_color_depth(const rtgs_gaussians* g, const rtgs_projecte
  *   gid_of_slot [n_slots] inverse map
  *   grad [n_slots][10+3K] ACCUMULATED (+=): pos 3, log_scale 3, rot 4, sh K*3 (DC first)
  *   loss_out [4] device float, OVERWRITTEN: L_color, L_depth, w_c L_color + w_d L_depth, |P_d|
+ * With f3 bins (bins->sub_rec set) the subset rows must be the slots: bins->sub_gid == gid_of_slot.
  * No gradient flows through discrete choices (hit, 60 deg branch, termination, cut-offs, clamps; R17)
  * nor to opacity (lr_alpha = 0).
  * ------------------------------------------------------------------------------------------- */
@@ -277,6 +285,42 @@ rtgs_status rtgs_manage_states(const rtgs_render_out* full, const rtgs_frame* fr
                                uint8_t* flags, uint32_t* err_count, uint32_t* eta, uint32_t* t_created, int32_t n,
                                const rtgs_state_params* sp, uint32_t* counts, void* workspace, size_t workspace_bytes,
                                void* stream);
+
+/* =============================================================================================
+ * NEXT row f3: window-level stable-projection cache.
+ * During a window the stable Gaussians and the window's poses are fixed (only unstable slots are
+ * optimised), so the stable part of every window frame's (tile, zkey, gid)-sorted lists is built
+ * once from that frame's FULL bins; each iteration re-projects only the unstable slots and merges
+ * them in.  The merged order is the unique (tile, zkey bits, gid) order, so every result equals the
+ * uncached path (rtgs_project_gaussians + rtgs_bin_and_sort) on the same parameters.
+ * ============================================================================================= */
+
+/* rtgs_project_subset: rtgs_project_gaussians for the Gaussians gid_list[0..n_list) only; row i of
+ * every field of `out` describes Gaussian gid_list[i] (out sized for n_list rows).  gid_list entries
+ * must be valid gids (0 <= gid < g->n). */
+rtgs_status rtgs_project_subset(const rtgs_gaussians* g, const int32_t* gid_list, int32_t n_list,
+                                const rtgs_pose* pose, const rtgs_camera* cam, rtgs_projected* out, void* stream);
+
+/* rtgs_stable_cache_build: from FULL bins (every tile, all Gaussians), keep per tile the entries
+ * whose Gaussian is stable (flags bit1), in order.  cache->sorted_gid needs full->capacity entries;
+ * cache->tile_range [TX*TY][2] is written (a tile's stable entries stay inside its full range);
+ * cache->n_instances (nullable) receives the number of stable instances. */
+rtgs_status rtgs_stable_cache_build(const rtgs_bins* full, const uint8_t* flags, const rtgs_camera* cam,
+                                    rtgs_bins* cache, void* stream);
+
+/* rtgs_bin_and_sort_cached: the masked-iteration bins of rtgs_bin_and_sort(..., tile_keep, ...)
+ * without re-projecting the stable Gaussians.  Inputs: `proj` (the frame's full projection; only
+ * zkey of cached gids is read), `cache` (rtgs_stable_cache_build of the same frame), `sub` (the
+ * rtgs_project_subset rows of the unstable Gaussians sub_gid[0..n_sub), which MUST be strictly
+ * increasing), tile_keep (required).  The subset rows of the kept tiles are binned and sorted,
+ * then merged per kept tile with the cached stable list by (zkey bits, gid).  Output entries are
+ * gids (stable) or 0x80000000 | row (subset); on return out->sub_rec / sub_zkey / sub_gid are set to
+ * sub->rec, sub->zkey, sub_gid.  n_instances / capacity as in rtgs_bin_and_sort. */
+size_t rtgs_bin_cached_workspace_size(int32_t n_sub, const rtgs_camera* cam, uint32_t capacity);
+rtgs_status rtgs_bin_and_sort_cached(const rtgs_projected* proj, const rtgs_bins* cache, const rtgs_projected* sub,
+                                     const int32_t* sub_gid, int32_t n_sub, const rtgs_camera* cam,
+                                     const uint8_t* tile_keep, rtgs_bins* out, void* workspace,
+                                     size_t workspace_bytes, void* stream);
 
 /* Utilities */
 const char* rtgs_status_string(rtgs_status s);

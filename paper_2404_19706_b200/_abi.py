@@ -36,7 +36,8 @@ class Projected(C.Structure):
 
 
 class Bins(C.Structure):
-    _fields_ = [("sorted_gid", vp), ("tile_range", vp), ("n_instances", vp), ("capacity", C.c_uint32)]
+    _fields_ = [("sorted_gid", vp), ("tile_range", vp), ("n_instances", vp), ("capacity", C.c_uint32),
+                ("sub_rec", vp), ("sub_zkey", vp), ("sub_gid", vp)]
 
 
 class RenderOut(C.Structure):
@@ -86,6 +87,11 @@ EXPORTS = {
     "rtgs_state_workspace_size": (C.c_size_t, [C.c_int32]),
     "rtgs_manage_states": (C.c_int, [P(RenderOut), P(Frame), P(Camera), vp, vp, vp, vp, C.c_int32, P(StateParams), vp,
                                      vp, C.c_size_t, vp]),
+    "rtgs_project_subset": (C.c_int, [P(Gaussians), vp, C.c_int32, P(Pose), P(Camera), P(Projected), vp]),
+    "rtgs_stable_cache_build": (C.c_int, [P(Bins), vp, P(Camera), P(Bins), vp]),
+    "rtgs_bin_cached_workspace_size": (C.c_size_t, [C.c_int32, P(Camera), C.c_uint32]),
+    "rtgs_bin_and_sort_cached": (C.c_int, [P(Projected), P(Bins), P(Projected), vp, C.c_int32, P(Camera), vp, P(Bins),
+                                           vp, C.c_size_t, vp]),
     "rtgs_status_string": (C.c_char_p, [C.c_int]),
     "rtgs_last_cuda_error": (C.c_char_p, []),
     "rtgs_version": (C.c_int32, []),

@@ -84,12 +84,13 @@ rtgs_status rtgs_render_color_depth(const rtgs_gaussians* g, const rtgs_projecte
                                     rtgs_render_out* out, void* stream) {
   if (!cam_ok(cam) || !out || !pose_ok(pose)) return RTGS_ERR_INVALID_ARG;
   if (mode == RTGS_RENDER_COVERAGE) {
-    if (!g || g->n < 0 || (g->n > 0 && !g->flags) || !proj_ok(proj, g->n)) return RTGS_ERR_INVALID_ARG;
+    if (!g || g->n < 0 || !proj_ok(proj, g->n)) return RTGS_ERR_INVALID_ARG;  // flags NULL: every row
     if (!out->active_bits || !out->tile_keep || !out->tile_list || !out->counts) return RTGS_ERR_INVALID_ARG;
     return finish(launch_coverage(*g, *proj, *cam, *out, S(stream)));
   }
   if (mode != RTGS_RENDER_FULL && mode != RTGS_RENDER_MASKED) return RTGS_ERR_INVALID_ARG;
   if (!proj || !proj->rec || !proj->zkey || !a16(proj->rec) || !bins_ok(bins)) return RTGS_ERR_INVALID_ARG;
+  if (bins->sub_rec && (!bins->sub_zkey || !bins->sub_gid || !a16(bins->sub_rec))) return RTGS_ERR_INVALID_ARG;
   if (!out->color || !out->trans || !out->depth || !out->index || !out->n_contrib) return RTGS_ERR_INVALID_ARG;
   if (mode == RTGS_RENDER_MASKED && (!out->active_bits || !out->tile_list || !out->counts))
     return RTGS_ERR_INVALID_ARG;
@@ -112,6 +113,7 @@ rtgs_status rtgs_render_backward_masked(const rtgs_gaussians* g, const rtgs_proj
   if (!target || !target->color || !target->depth || !w || n_slots < 0 || !loss_out) return RTGS_ERR_INVALID_ARG;
   if (g->n > 0 && !slot_of_gid) return RTGS_ERR_INVALID_ARG;
   if (n_slots > 0 && (!gid_of_slot || !grad)) return RTGS_ERR_INVALID_ARG;
+  if (bins->sub_rec && bins->sub_gid != gid_of_slot) return RTGS_ERR_INVALID_ARG;  // f3: subset rows are the slots
   if (!workspace || workspace_bytes < backward_workspace_size(n_slots) || !a16(workspace)) return RTGS_ERR_WORKSPACE;
   return finish(launch_backward(*g, *proj, *bins, make_pose(*pose), *cam, *fwd, *target, *w, slot_of_gid, gid_of_slot,
                                 n_slots, grad, loss_out, workspace, S(stream)));
@@ -168,6 +170,41 @@ rtgs_status rtgs_manage_states(const rtgs_render_out* full, const rtgs_frame* fr
   if (!workspace || workspace_bytes < state_workspace_size(n)) return RTGS_ERR_WORKSPACE;
   return finish(launch_manage_states(*full, *frame, *cam, flags, err_count, eta, t_created, n, *sp, counts, workspace,
                                      S(stream)));
+}
+
+rtgs_status rtgs_project_subset(const rtgs_gaussians* g, const int32_t* gid_list, int32_t n_list,
+                                const rtgs_pose* pose, const rtgs_camera* cam, rtgs_projected* out, void* stream) {
+  if (!gauss_ok(g, false) || n_list < 0 || !pose_ok(pose) || !cam_ok(cam) || !proj_ok(out, n_list))
+    return RTGS_ERR_INVALID_ARG;
+  if (n_list > 0 && (!gid_list || g->n == 0)) return RTGS_ERR_INVALID_ARG;
+  return finish(launch_project_subset(*g, gid_list, n_list, make_pose(*pose), *cam, *out, S(stream)));
+}
+
+rtgs_status rtgs_stable_cache_build(const rtgs_bins* full, const uint8_t* flags, const rtgs_camera* cam,
+                                    rtgs_bins* cache, void* stream) {
+  if (!bins_ok(full) || !flags || !cam_ok(cam) || !cache || !cache->sorted_gid || !cache->tile_range ||
+      (reinterpret_cast<uintptr_t>(cache->tile_range) & 7u) != 0 || cache->capacity < full->capacity)
+    return RTGS_ERR_INVALID_ARG;
+  return finish(launch_cache_build(*full, flags, *cam, *cache, S(stream)));
+}
+
+size_t rtgs_bin_cached_workspace_size(int32_t n_sub, const rtgs_camera* cam, uint32_t capacity) {
+  if (n_sub < 0 || !cam_ok(cam)) return 0;
+  return bin_cached_workspace_size(n_sub, *cam, capacity);
+}
+
+rtgs_status rtgs_bin_and_sort_cached(const rtgs_projected* proj, const rtgs_bins* cache, const rtgs_projected* sub,
+                                     const int32_t* sub_gid, int32_t n_sub, const rtgs_camera* cam,
+                                     const uint8_t* tile_keep, rtgs_bins* out, void* workspace,
+                                     size_t workspace_bytes, void* stream) {
+  if (!proj || !proj->zkey || !cache || !cache->sorted_gid || !cache->tile_range || n_sub < 0 || !cam_ok(cam) ||
+      !tile_keep || !bins_ok(out) || !proj_ok(sub, n_sub) || (n_sub > 0 && !sub_gid))
+    return RTGS_ERR_INVALID_ARG;
+  if (!workspace || workspace_bytes < bin_cached_workspace_size(n_sub, *cam, out->capacity)) return RTGS_ERR_WORKSPACE;
+  out->sub_rec = sub->rec;
+  out->sub_zkey = sub->zkey;
+  out->sub_gid = sub_gid;
+  return finish(launch_bin_cached(*proj, *cache, *sub, sub_gid, n_sub, *cam, tile_keep, *out, workspace, S(stream)));
 }
 
 const char* rtgs_status_string(rtgs_status s) {

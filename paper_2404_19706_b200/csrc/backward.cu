@@ -48,6 +48,7 @@ size_t backward_workspace_size(int n_slots) { return ((size_t)n_slots * kSG + 8)
 
 struct BwdArgs {
   const float4* rec;
+  const float4* sub_rec;  // NEXT f3: subset rows = slots (entries with kSubBit), else NULL
   const uint32_t* zkey;
   const uint32_t* sorted_gid;
   const uint2* range;
@@ -117,7 +118,7 @@ __global__ void __launch_bounds__(kPipeThreads) k_render_bwd(const BwdArgs a) {
       const float gD = dd > 0.f ? 1.f : (dd < 0.f ? -1.f : 0.f);  // scaled by w_d / |P_d| in K5b
       const int slot = a.slot_of_gid[hit];
       if (slot >= 0 && gD != 0.f) {
-        const float4 pl = a.rec[(size_t)4 * hit + 3];
+        const float4 pl = a.sub_rec ? a.sub_rec[(size_t)4 * slot + 3] : a.rec[(size_t)4 * hit + 3];
         const float rx = (fpx - a.cam.cx) / a.cam.fx, ry = (fpy - a.cam.cy) / a.cam.fy;
         const float ndr = pl.x * rx + pl.y * ry + pl.z;
         const float nn = sqrtf(pl.x * pl.x + pl.y * pl.y + pl.z * pl.z);
@@ -153,9 +154,12 @@ __global__ void __launch_bounds__(kPipeThreads) k_render_bwd(const BwdArgs a) {
 
   if (!consumer) {
     const int32_t* slot_of_gid = a.slot_of_gid;
-    auto extra = [&](int st, int j, uint32_t g) { cp_async4(&sm.slot[st][j], slot_of_gid + g); };
+    // slot of a gid entry via slot_of_gid; a subset entry (f3) carries its slot in the entry itself
+    auto extra = [&](int st, int j, uint32_t g) {
+      if (!(g & kSubBit)) cp_async4(&sm.slot[st][j], slot_of_gid + g);
+    };
     auto flush = [](int, int) {};
-    pipe_produce(r, a.rec, a.sorted_gid, start, end, extra, flush);
+    pipe_produce(r, a.rec, a.sub_rec, a.sorted_gid, start, end, extra, flush);
     return;
   }
 
@@ -171,6 +175,7 @@ __global__ void __launch_bounds__(kPipeThreads) k_render_bwd(const BwdArgs a) {
     if (!wdone) {
       const uint32_t srec = smem_u32(&r.rec[st][0][0]);  // shared addresses, computed once per batch
       const uint32_t sslot = smem_u32(&sm.slot[st][0]);
+      const uint32_t sgid = smem_u32(&r.gid[st][0]);
       const uint32_t pbase = (uint32_t)(start + b * kPipeBatch);
       const int cnt = min(kPipeBatch, n - b * kPipeBatch);
       for (int g0 = 0; g0 < cnt; g0 += 32) {
@@ -185,7 +190,8 @@ __global__ void __launch_bounds__(kPipeThreads) k_render_bwd(const BwdArgs a) {
         while (m) {
           const int idx = g0 + __ffs(m) - 1;
           m &= m - 1;
-          const int slot = (int)lds32(sslot + 4u * idx);  // warp-uniform
+          const uint32_t ent = lds32(sgid + 4u * idx);  // warp-uniform
+          const int slot = (ent & kSubBit) ? (int)(ent & ~kSubBit) : (int)lds32(sslot + 4u * idx);
           // branch-free replay of record idx (identical arithmetic and decisions to the forward)
           const uint32_t ra = srec + 48u * idx;
           const float4 r0 = lds128(ra), r1 = lds128(ra + 16u), r2 = lds128(ra + 32u);
@@ -244,7 +250,8 @@ __global__ void __launch_bounds__(kPipeThreads) k_render_bwd(const BwdArgs a) {
 // ------------------------------------------------------------------------------------------------
 struct PBArgs {
   const float4* rec;
-  const float* recf;  // the same records as floats
+  const float* recf;      // the same records as floats
+  const float* sub_recf;  // NEXT f3: the slots' own records (row = slot), else NULL
   const float* pos;
   const float* log_scale;
   const float* rot;
@@ -565,7 +572,9 @@ __global__ void __launch_bounds__(128) k_project_bwd(const PBArgs a) {
         const size_t g = (size_t)sm.gid[ls];
         v[u] = c < 3 ? a.pos[3 * g + c]
                      : (c < 6 ? a.log_scale[3 * g + (c - 3)]
-                              : (c < 10 ? a.rot[4 * g + (c - 6)] : a.recf[16 * g + 8 + (c - 10)]));
+                              : (c < 10 ? a.rot[4 * g + (c - 6)]
+                                        : (a.sub_recf ? a.sub_recf[16 * (size_t)(s0 + ls) + 8 + (c - 10)]
+                                                      : a.recf[16 * g + 8 + (c - 10)])));
       }
     }
 #pragma unroll
@@ -608,6 +617,7 @@ cudaError_t launch_backward(const rtgs_gaussians& g, const rtgs_projected& proj,
   cudaMemsetAsync(ws, 0, ((size_t)n_slots * kSG + 8) * sizeof(float), s);
   BwdArgs a;
   a.rec = reinterpret_cast<const float4*>(proj.rec);
+  a.sub_rec = reinterpret_cast<const float4*>(bins.sub_rec);
   a.zkey = proj.zkey;
   a.sorted_gid = bins.sorted_gid;
   a.range = reinterpret_cast<const uint2*>(bins.tile_range);
@@ -627,6 +637,7 @@ cudaError_t launch_backward(const rtgs_gaussians& g, const rtgs_projected& proj,
   PBArgs b;
   b.rec = reinterpret_cast<const float4*>(proj.rec);
   b.recf = proj.rec;
+  b.sub_recf = bins.sub_rec;
   b.pos = g.pos; b.log_scale = g.log_scale; b.rot = g.rot; b.sh = g.sh;
   b.K = (g.sh_degree + 1) * (g.sh_degree + 1);
   b.D = 10 + 3 * b.K;

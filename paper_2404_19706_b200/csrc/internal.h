@@ -18,9 +18,19 @@ PoseF make_pose(const rtgs_pose& p);
 cudaError_t launch_project(const rtgs_gaussians& g, const PoseF& pose, const rtgs_camera& cam,
                            const rtgs_projected& out, cudaStream_t s);
 
+cudaError_t launch_project_subset(const rtgs_gaussians& g, const int32_t* gid_list, int n_list, const PoseF& pose,
+                                  const rtgs_camera& cam, const rtgs_projected& out, cudaStream_t s);
+
 size_t bin_workspace_size(int n, const rtgs_camera& cam, uint32_t capacity);
 cudaError_t launch_bin(const rtgs_projected& proj, int n, const rtgs_camera& cam, const uint8_t* keep,
                        const rtgs_bins& out, void* ws, cudaStream_t s);
+
+cudaError_t launch_cache_build(const rtgs_bins& full, const uint8_t* flags, const rtgs_camera& cam,
+                               const rtgs_bins& cache, cudaStream_t s);
+size_t bin_cached_workspace_size(int n_sub, const rtgs_camera& cam, uint32_t capacity);
+cudaError_t launch_bin_cached(const rtgs_projected& proj, const rtgs_bins& cache, const rtgs_projected& sub,
+                              const int32_t* sub_gid, int n_sub, const rtgs_camera& cam, const uint8_t* keep,
+                              const rtgs_bins& out, void* ws, cudaStream_t s);
 
 cudaError_t launch_coverage(const rtgs_gaussians& g, const rtgs_projected& proj, const rtgs_camera& cam,
                             const rtgs_render_out& out, cudaStream_t s);

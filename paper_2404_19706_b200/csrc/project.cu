@@ -3,7 +3,8 @@
 // One thread per Gaussian, 128 Gaussians per CTA.  The SH block of the CTA (128 x 12K bytes, the
 // dominant HBM stream: 192 of 237 B/Gaussian at degree 3) is staged into shared memory by ONE 1D
 // bulk copy (cp.async.bulk, TMA engine) completing on an mbarrier, issued before the geometry math
-// so the copy overlaps it.  Camera-frame position and mu are formed in float64.
+// so the copy overlaps it; 24 KB of shared memory per CTA keeps 6 CTAs (24 warps) per SM resident,
+// enough bytes in flight for the HBM stream.  Camera-frame position and mu are formed in float64.
 #include "common.cuh"
 #include "internal.h"
 
@@ -18,7 +19,8 @@ struct ProjArgs {
   const float* opacity;
   const float* sh;
   const uint8_t* flags;  // nullable; bit2 = removed (NEXT f1)
-  int n, K;
+  const int32_t* subset;  // NEXT f3: row i projects Gaussian subset[i] (NULL: row i = Gaussian i)
+  int n, K;               // n = number of rows
   double V[9], tp[3], campos[3];
   float Vz0, Vz1, Vz2, tz;  // float32 key sequence (R8)
   float Vf[9];
@@ -30,60 +32,93 @@ struct ProjArgs {
   uint32_t* touched;
 };
 
-// coefficient (k, channel ch) of this thread's Gaussian in the transposed shared tile: c[(3k+ch)*kLd]
-constexpr int kLd = 129;  // kProjThreads + 1: conflict-free rows
+// SH colour of one Gaussian from its AoS row c[3k + ch] in shared memory (R2): the 3DGS real basis,
+// constants restated from their closed forms sqrt((2l+1)/4pi ...); per channel the terms are summed
+// in ascending k.  The row is read as 3K/4 float4 (rows of 192 B: 4-way bank conflicts, cheaper than
+// a transpose buffer that would cut the CTAs resident per SM).
 template <int K>
-__device__ __forceinline__ float sh_eval(const float* c, int ch, float x, float y, float z) {
-  // 3DGS real basis (R2), constants restated from their closed forms sqrt((2l+1)/4pi ...)
-#define SHC(k) c[(3 * (k) + ch) * kLd]
-  const float C0 = 0.28209479177387814f, C1 = 0.4886025119029199f;
-  float r = C0 * SHC(0);
-  if (K > 1) r += -C1 * y * SHC(1) + C1 * z * SHC(2) - C1 * x * SHC(3);
+__device__ __forceinline__ float3 sh_eval(const float* c, float x, float y, float z) {
+  float Y[16];
+  Y[0] = 0.28209479177387814f;
+  if (K > 1) {
+    const float C1 = 0.4886025119029199f;
+    Y[1] = -C1 * y; Y[2] = C1 * z; Y[3] = -C1 * x;
+  }
   if (K > 4) {
     const float xx = x * x, yy = y * y, zz = z * z;
-    r += 1.0925484305920792f * x * y * SHC(4) - 1.0925484305920792f * y * z * SHC(5) +
-         0.31539156525252005f * (2.f * zz - xx - yy) * SHC(6) - 1.0925484305920792f * x * z * SHC(7) +
-         0.5462742152960396f * (xx - yy) * SHC(8);
+    Y[4] = 1.0925484305920792f * x * y;
+    Y[5] = -1.0925484305920792f * y * z;
+    Y[6] = 0.31539156525252005f * (2.f * zz - xx - yy);
+    Y[7] = -1.0925484305920792f * x * z;
+    Y[8] = 0.5462742152960396f * (xx - yy);
     if (K > 9) {
-      r += -0.5900435899266435f * y * (3.f * xx - yy) * SHC(9) + 2.890611442640554f * x * y * z * SHC(10) -
-           0.4570457994644658f * y * (4.f * zz - xx - yy) * SHC(11) +
-           0.3731763325901154f * z * (2.f * zz - 3.f * xx - 3.f * yy) * SHC(12) -
-           0.4570457994644658f * x * (4.f * zz - xx - yy) * SHC(13) +
-           1.445305721320277f * z * (xx - yy) * SHC(14) - 0.5900435899266435f * x * (xx - 3.f * yy) * SHC(15);
+      Y[9] = -0.5900435899266435f * y * (3.f * xx - yy);
+      Y[10] = 2.890611442640554f * x * y * z;
+      Y[11] = -0.4570457994644658f * y * (4.f * zz - xx - yy);
+      Y[12] = 0.3731763325901154f * z * (2.f * zz - 3.f * xx - 3.f * yy);
+      Y[13] = -0.4570457994644658f * x * (4.f * zz - xx - yy);
+      Y[14] = 1.445305721320277f * z * (xx - yy);
+      Y[15] = -0.5900435899266435f * x * (xx - 3.f * yy);
     }
   }
-#undef SHC
-  return r;
+  float acc[3] = {0.f, 0.f, 0.f};
+  if constexpr ((3 * K) % 4 == 0) {  // degree 1 and 3: 16 B aligned rows
+    const float4* c4 = reinterpret_cast<const float4*>(c);
+#pragma unroll
+    for (int q = 0; q < 3 * K / 4; ++q) {
+      const float4 v = c4[q];
+      const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int j = 4 * q + u;
+        acc[j % 3] = fmaf(Y[j / 3], e[u], acc[j % 3]);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 3 * K; ++j) acc[j % 3] = fmaf(Y[j / 3], c[j], acc[j % 3]);
+  }
+  return make_float3(acc[0], acc[1], acc[2]);
 }
 
-template <int K>
-__global__ void __launch_bounds__(kProjThreads) k_project(const ProjArgs a) {
-  // s_sh: [kProjThreads][3K] as copied (AoS), then s_t: [3K][kLd] transposed for conflict-free reads
+template <int K, bool SUB>
+__global__ void __launch_bounds__(kProjThreads, 6) k_project(const ProjArgs a) {
+  // s_sh: [kProjThreads][3K] as copied (AoS)
   extern __shared__ __align__(16) float s_sh[];
-  float* s_t = s_sh + kProjThreads * 3 * K;
   __shared__ uint64_t bar;
   const int tid = threadIdx.x;
   const int base = blockIdx.x * kProjThreads;
   const int cnt = min(kProjThreads, a.n - base);
   constexpr int shf = 3 * K;  // floats per Gaussian
-  const uint32_t bytes = (uint32_t)cnt * shf * 4u;
-  const uint32_t bulk = bytes & ~15u;
+  const int i = base + tid;
+  bool live = i < a.n;
+  const size_t gi = SUB ? (size_t)(live ? a.subset[i] : 0) : (size_t)i;  // Gaussian of this row
   if (tid == 0) {
     mbar_init(&bar, 1);
     fence_mbar_init();
   }
   __syncthreads();
-  if (tid == 0) {
-    mbar_arrive_expect_tx(&bar, bulk);
-    if (bulk) bulk_g2s(s_sh, a.sh + (size_t)base * shf, bulk, &bar);
-  }
-  if (tid < (int)((bytes - bulk) >> 2)) {  // <= 3 trailing floats when 12K*cnt % 16 != 0
-    const int o = (bulk >> 2) + tid;
-    s_sh[o] = a.sh[(size_t)base * shf + o];
+  if constexpr (!SUB) {  // contiguous rows: ONE bulk copy of the CTA's SH block
+    const uint32_t bytes = (uint32_t)cnt * shf * 4u;
+    const uint32_t bulk = bytes & ~15u;
+    if (tid == 0) {
+      mbar_arrive_expect_tx(&bar, bulk);
+      if (bulk) bulk_g2s(s_sh, a.sh + (size_t)base * shf, bulk, &bar);
+    }
+    if (tid < (int)((bytes - bulk) >> 2)) {  // <= 3 trailing floats when 12K*cnt % 16 != 0
+      const int o = (bulk >> 2) + tid;
+      s_sh[o] = a.sh[(size_t)base * shf + o];
+    }
+  } else if constexpr (shf % 4 == 0) {  // gathered rows: one bulk copy per row (12K bytes)
+    if (tid == 0) mbar_arrive_expect_tx(&bar, (uint32_t)cnt * shf * 4u);
+    __syncthreads();
+    if (live) bulk_g2s(s_sh + tid * shf, a.sh + gi * shf, shf * 4, &bar);
+  } else {  // rows not 16-byte multiples: plain loads
+    if (tid == 0) mbar_arrive_expect_tx(&bar, 0u);
+    if (live)
+      for (int j = 0; j < shf; ++j) s_sh[tid * shf + j] = a.sh[gi * shf + j];
   }
 
-  const int i = base + tid;
-  bool live = i < a.n;
   float4 r0 = make_float4(0, 0, 0, 0), r1 = r0, r2 = r0, r3 = r0;
   uint32_t zbits = 0xFFFFFFFFu;
   uint2 rect = make_uint2(1u | (1u << 16), 0u);  // empty: (x0,y0) = (1,1) > (x1,y1) = (0,0)
@@ -91,12 +126,16 @@ __global__ void __launch_bounds__(kProjThreads) k_project(const ProjArgs a) {
   float dirx = 0, diry = 0, dirz = 1;
   bool vis = false;
   if (live) {
-    const float px = a.pos[3 * i], py = a.pos[3 * i + 1], pz = a.pos[3 * i + 2];
-    const float alpha = a.opacity[i];
+    // every per-Gaussian load issued up front: one DRAM round trip instead of a dependent chain
+    const float px = a.pos[3 * gi], py = a.pos[3 * gi + 1], pz = a.pos[3 * gi + 2];
+    const float alpha = a.opacity[gi];
+    float qw = a.rot[4 * gi], qx = a.rot[4 * gi + 1], qy = a.rot[4 * gi + 2], qz = a.rot[4 * gi + 3];
+    const float l0 = a.log_scale[3 * gi], l1 = a.log_scale[3 * gi + 1], l2 = a.log_scale[3 * gi + 2];
+    const uint8_t fl = a.flags ? a.flags[gi] : (uint8_t)0;
     // R8: float32 key, every product and sum rounded, no FMA
     const float zk = __fadd_rn(__fadd_rn(__fadd_rn(__fmul_rn(a.Vz0, px), __fmul_rn(a.Vz1, py)), __fmul_rn(a.Vz2, pz)), a.tz);
     const float kext = (alpha * 255.f > 1.f) ? fminf(3.f, sqrtf(2.f * logf(255.f * alpha))) : 0.f;
-    const bool removed = a.flags && (a.flags[i] & 4u);
+    const bool removed = fl & 4u;
     if (zk > kNear && kext > 0.f && !removed) {
       // camera frame in float64: p_c = V p + t'
       const double X = fma(a.V[0], (double)px, fma(a.V[1], (double)py, fma(a.V[2], (double)pz, a.tp[0])));
@@ -104,13 +143,11 @@ __global__ void __launch_bounds__(kProjThreads) k_project(const ProjArgs a) {
       const double Z = fma(a.V[6], (double)px, fma(a.V[7], (double)py, fma(a.V[8], (double)pz, a.tp[2])));
       const float x = (float)X, y = (float)Y, z = (float)Z;
       // Sigma = R_q diag(s^2) R_q^T (R3)
-      float qw = a.rot[4 * i], qx = a.rot[4 * i + 1], qy = a.rot[4 * i + 2], qz = a.rot[4 * i + 3];
       const float qn = rsqrtf(qw * qw + qx * qx + qy * qy + qz * qz);
       qw *= qn; qx *= qn; qy *= qn; qz *= qn;
       const float R00 = 1.f - 2.f * (qy * qy + qz * qz), R01 = 2.f * (qx * qy - qw * qz), R02 = 2.f * (qx * qz + qw * qy);
       const float R10 = 2.f * (qx * qy + qw * qz), R11 = 1.f - 2.f * (qx * qx + qz * qz), R12 = 2.f * (qy * qz - qw * qx);
       const float R20 = 2.f * (qx * qz - qw * qy), R21 = 2.f * (qy * qz + qw * qx), R22 = 1.f - 2.f * (qx * qx + qy * qy);
-      const float l0 = a.log_scale[3 * i], l1 = a.log_scale[3 * i + 1], l2 = a.log_scale[3 * i + 2];
       const float s0 = expf(l0), s1 = expf(l1), s2 = expf(l2);
       const float M00 = R00 * s0, M01 = R01 * s1, M02 = R02 * s2;
       const float M10 = R10 * s0, M11 = R11 * s1, M12 = R12 * s2;
@@ -177,19 +214,13 @@ __global__ void __launch_bounds__(kProjThreads) k_project(const ProjArgs a) {
     }
   }
   mbar_wait(&bar, 0);
-  __syncthreads();  // trailing scalar loads of the tail block
-  // transpose AoS [g][j] -> [j][g] (row pitch kLd): reads consecutive, writes to distinct banks
-  for (int i = tid; i < cnt * shf; i += kProjThreads) {
-    const int g = i / shf, j = i - g * shf;
-    s_t[j * kLd + g] = s_sh[i];
-  }
-  __syncthreads();
+  __syncthreads();  // plain-load rows / trailing floats of the tail block
   if (live) {
     if (vis) {
-      const float* c = s_t + tid;
-      r2.x = fmaxf(0.f, sh_eval<K>(c, 0, dirx, diry, dirz) + 0.5f);
-      r2.y = fmaxf(0.f, sh_eval<K>(c, 1, dirx, diry, dirz) + 0.5f);
-      r2.z = fmaxf(0.f, sh_eval<K>(c, 2, dirx, diry, dirz) + 0.5f);
+      const float3 c = sh_eval<K>(s_sh + tid * 3 * K, dirx, diry, dirz);
+      r2.x = fmaxf(0.f, c.x + 0.5f);
+      r2.y = fmaxf(0.f, c.y + 0.5f);
+      r2.z = fmaxf(0.f, c.z + 0.5f);
     }
     float4* o = a.rec + (size_t)4 * i;
     o[0] = r0; o[1] = r1; o[2] = r2; o[3] = r3;
@@ -212,13 +243,14 @@ PoseF make_pose(const rtgs_pose& p) {
   return f;
 }
 
-cudaError_t launch_project(const rtgs_gaussians& g, const PoseF& pose, const rtgs_camera& cam,
-                           const rtgs_projected& out, cudaStream_t s) {
-  if (g.n == 0) return cudaSuccess;
+static cudaError_t project_impl(const rtgs_gaussians& g, const int32_t* subset, int n_rows, const PoseF& pose,
+                                const rtgs_camera& cam, const rtgs_projected& out, cudaStream_t s) {
+  if (n_rows == 0) return cudaSuccess;
   ProjArgs a;
   a.pos = g.pos; a.log_scale = g.log_scale; a.rot = g.rot; a.opacity = g.opacity; a.sh = g.sh;
   a.flags = g.flags;
-  a.n = g.n;
+  a.subset = subset;
+  a.n = n_rows;
   a.K = (g.sh_degree + 1) * (g.sh_degree + 1);
   for (int k = 0; k < 9; ++k) { a.V[k] = pose.V[k]; a.Vf[k] = pose.Vf[k]; }
   for (int k = 0; k < 3; ++k) { a.tp[k] = pose.tp[k]; a.campos[k] = pose.campos[k]; }
@@ -233,22 +265,31 @@ cudaError_t launch_project(const rtgs_gaussians& g, const PoseF& pose, const rtg
   a.zkey = out.zkey;
   a.rect = reinterpret_cast<uint2*>(out.rect);
   a.touched = out.tiles_touched;
-  const size_t smem = (size_t)(kProjThreads + kLd) * 3 * a.K * sizeof(float);
-  const int blocks = (g.n + kProjThreads - 1) / kProjThreads;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_project<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-    cudaFuncSetAttribute(k_project<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-    attr = true;
-  }
+  const size_t smem = (size_t)kProjThreads * 3 * a.K * sizeof(float);
+  const int blocks = (n_rows + kProjThreads - 1) / kProjThreads;
+  const bool sub = subset != nullptr;
+#define RTGS_PROJ(KK)                                                                        \
+  (sub ? (k_project<KK, true><<<blocks, kProjThreads, smem, s>>>(a), 0)                      \
+       : (k_project<KK, false><<<blocks, kProjThreads, smem, s>>>(a), 0))
   switch (a.K) {
-    case 1: k_project<1><<<blocks, kProjThreads, smem, s>>>(a); break;
-    case 4: k_project<4><<<blocks, kProjThreads, smem, s>>>(a); break;
-    case 9: k_project<9><<<blocks, kProjThreads, smem, s>>>(a); break;
-    default: k_project<16><<<blocks, kProjThreads, smem, s>>>(a); break;
+    case 1: RTGS_PROJ(1); break;
+    case 4: RTGS_PROJ(4); break;
+    case 9: RTGS_PROJ(9); break;
+    default: RTGS_PROJ(16); break;
   }
+#undef RTGS_PROJ
   note_launch();
   return cudaGetLastError();
+}
+
+cudaError_t launch_project(const rtgs_gaussians& g, const PoseF& pose, const rtgs_camera& cam,
+                           const rtgs_projected& out, cudaStream_t s) {
+  return project_impl(g, nullptr, g.n, pose, cam, out, s);
+}
+
+cudaError_t launch_project_subset(const rtgs_gaussians& g, const int32_t* gid_list, int n_list, const PoseF& pose,
+                                  const rtgs_camera& cam, const rtgs_projected& out, cudaStream_t s) {
+  return project_impl(g, gid_list, n_list, pose, cam, out, s);
 }
 
 }  // namespace rtgs

@@ -21,7 +21,7 @@ __global__ void __launch_bounds__(256) k_coverage(const float4* __restrict__ rec
                                                   int n, int W, uint32_t* __restrict__ bits) {
   const int i = blockIdx.x * 256 + threadIdx.x;
   const int lane = threadIdx.x & 31;
-  const bool mine = i < n && !(flags[i] & 2u) && zkey[i] != 0xFFFFFFFFu;
+  const bool mine = i < n && (!flags || !(flags[i] & 2u)) && zkey[i] != 0xFFFFFFFFu;  // NULL: all rows
   // every lane prefetches its own Gaussian; the warp then splats them one by one via shuffles
   uint2 myr = make_uint2(1u | (1u << 16), 0u);
   float4 mya = make_float4(0, 0, 0, 0), myb = mya;
@@ -89,6 +89,9 @@ __global__ void __launch_bounds__(256) k_tile_keep(const uint32_t* __restrict__ 
 struct FwdArgs {
   const float4* rec;
   const uint32_t* zkey;
+  const float4* sub_rec;  // NEXT f3 subset rows (entries with kSubBit), else NULL
+  const uint32_t* sub_zkey;
+  const int32_t* sub_gid;
   const uint32_t* sorted_gid;
   const uint2* range;
   const uint32_t* tile_list;
@@ -120,7 +123,7 @@ __global__ void __launch_bounds__(kPipeThreads) k_render_fwd(const FwdArgs a) {
   const int start = (int)rg.x, end = (int)rg.y;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (w == kProducerWarp) {
-    pipe_produce(r, a.rec, a.sorted_gid, start, end, [](int, int, uint32_t) {}, [](int, int) {});
+    pipe_produce(r, a.rec, a.sub_rec, a.sorted_gid, start, end, [](int, int, uint32_t) {}, [](int, int) {});
     return;
   }
   const int tx = tile % a.cam.TX, ty = tile / a.cam.TX;
@@ -137,7 +140,7 @@ __global__ void __launch_bounds__(kPipeThreads) k_render_fwd(const FwdArgs a) {
   const int nb = n > 0 ? (n + kPipeBatch - 1) / kPipeBatch : 0;
 
   float T = 1.f, cr = 0.f, cg = 0.f, cb = 0.f;
-  int hit = -1;
+  uint32_t hit = 0xFFFFFFFFu;  // list entry of the depth hit (never a valid entry)
   uint32_t last = (uint32_t)start;
   uint32_t nblend = 0;  // blended (pixel, Gaussian) pairs of this lane (-> counts[3])
   bool wdone = __all_sync(0xffffffffu, done);
@@ -167,7 +170,7 @@ __global__ void __launch_bounds__(kPipeThreads) k_render_fwd(const FwdArgs a) {
           const float4 r0 = lds128(ra), r1 = lds128(ra + 16u), r2 = lds128(ra + 32u);
           PairEval e;
           bool ok = eval_pair(r0, r1, fpx, fpy, e) && !done;
-          if (ok && hit < 0 && e.f > kDeltaAlpha) hit = (int)lds32(sgid + 4u * idx);  // R9: before termination
+          if (ok && hit == 0xFFFFFFFFu && e.f > kDeltaAlpha) hit = lds32(sgid + 4u * idx);  // R9: before termination
           const float test = __fmul_rn(T, __fsub_rn(1.f, e.f));
           const bool term = ok && (test < kTMin);
           done = done || term;
@@ -202,21 +205,26 @@ __global__ void __launch_bounds__(kPipeThreads) k_render_fwd(const FwdArgs a) {
   a.color[2 * HW + lin] = cb;
   a.trans[lin] = T;
   a.n_contrib[lin] = last;
-  a.index[lin] = hit;
   float D = -1.f, N0 = 0.f, N1 = 0.f, N2 = 0.f;
-  if (hit >= 0) {
-    const float4 pl = a.rec[(size_t)4 * hit + 3];  // n_c, n_c . p_c
+  int32_t gid = -1;
+  if (hit != 0xFFFFFFFFu) {
+    const bool sub = hit & kSubBit;
+    const uint32_t row = hit & ~kSubBit;
+    gid = sub ? a.sub_gid[row] : (int32_t)hit;
+    const float4 pl = sub ? a.sub_rec[(size_t)4 * row + 3] : a.rec[(size_t)4 * hit + 3];  // n_c, n_c . p_c
+    const float zc = __uint_as_float(sub ? a.sub_zkey[row] : a.zkey[hit]);
     const float rx = (fpx - a.cam.cx) / a.cam.fx, ry = (fpy - a.cam.cy) / a.cam.fy;
     const float ndr = pl.x * rx + pl.y * ry + pl.z;
     const float nn = sqrtf(pl.x * pl.x + pl.y * pl.y + pl.z * pl.z);
     const float cosang = fabsf(ndr) / (sqrtf(rx * rx + ry * ry + 1.f) * nn);
-    D = (cosang > kCos60) ? pl.w / ndr : __uint_as_float(a.zkey[hit]);  // Eq.5 (R10, R11)
+    D = (cosang > kCos60) ? pl.w / ndr : zc;  // Eq.5 (R10, R11)
     const float sg = ndr > 0.f ? -1.f : 1.f;                             // face the viewer (R12)
     const float nx = sg * pl.x, ny = sg * pl.y, nz = sg * pl.z;
     N0 = a.R[0] * nx + a.R[1] * ny + a.R[2] * nz;
     N1 = a.R[3] * nx + a.R[4] * ny + a.R[5] * nz;
     N2 = a.R[6] * nx + a.R[7] * ny + a.R[8] * nz;
   }
+  a.index[lin] = gid;
   a.depth[lin] = D;
   if (a.normal) {
     a.normal[lin] = N0;
@@ -247,6 +255,9 @@ cudaError_t launch_render(const rtgs_projected& proj, const rtgs_bins& bins, con
   FwdArgs a;
   a.rec = reinterpret_cast<const float4*>(proj.rec);
   a.zkey = proj.zkey;
+  a.sub_rec = reinterpret_cast<const float4*>(bins.sub_rec);
+  a.sub_zkey = bins.sub_zkey;
+  a.sub_gid = bins.sub_gid;
   a.sorted_gid = bins.sorted_gid;
   a.range = reinterpret_cast<const uint2*>(bins.tile_range);
   a.tile_list = out.tile_list;

@@ -35,13 +35,21 @@ __global__ void __launch_bounds__(kFuseThreads) k_fuse(const FuseArgs a) {
   // Eq.9: w = (eta'_o - eta_{o-1}) / eta'_o ; no update (eta' = 0) keeps G_{o-1}
   const float w = e1 > 0u ? (float)((double)(e1 - min(e0, e1)) / (double)e1) : 0.f;
   const float* b = a.before + (size_t)slot * D;
-  for (int j = t; j < D; j += kFuseLanes) {
-    float* p = j < 3 ? a.pos + 3 * gid + j
-                     : (j < 6 ? a.log_scale + 3 * gid + (j - 3)
-                              : (j < 10 ? a.rot + 4 * gid + (j - 6) : a.sh + (size_t)(3 * K) * gid + (j - 10)));
-    const float th_new = *p, th_old = b[j];
-    *p = __fmaf_rn(w, th_new - th_old, th_old);  // (1-w) old + w new
+  constexpr int NIT = (D + kFuseLanes - 1) / kFuseLanes;
+  float* p[NIT];
+  float tn[NIT], to[NIT];
+#pragma unroll
+  for (int it = 0; it < NIT; ++it) {  // every load of the row before any store
+    const int j = min(t + it * kFuseLanes, D - 1);
+    p[it] = j < 3 ? a.pos + 3 * gid + j
+                  : (j < 6 ? a.log_scale + 3 * gid + (j - 3)
+                           : (j < 10 ? a.rot + 4 * gid + (j - 6) : a.sh + (size_t)(3 * K) * gid + (j - 10)));
+    tn[it] = *p[it];
+    to[it] = b[j];
   }
+#pragma unroll
+  for (int it = 0; it < NIT; ++it)
+    if (t + it * kFuseLanes < D) *p[it] = __fmaf_rn(w, tn[it] - to[it], to[it]);  // (1-w) old + w new
 }
 
 struct MarkArgs {

@@ -52,9 +52,16 @@ __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
   return v;
 }
 
-// producer: one lane per record slot; `extra(stage, j, gid)` may issue more cp.async.
+// list entries: a gid of `rec`, or (NEXT f3 cached bins) 0x80000000 | row of the subset records
+constexpr uint32_t kSubBit = 0x80000000u;
+__device__ __forceinline__ const float4* entry_rec(const float4* rec, const float4* sub_rec, uint32_t e) {
+  return (e & kSubBit) ? sub_rec + (size_t)4 * (e & ~kSubBit) : rec + (size_t)4 * e;
+}
+
+// producer: one lane per record slot; `extra(stage, j, entry)` may issue more cp.async.
 template <typename Extra, typename Flush>
 __device__ __forceinline__ void pipe_produce(PipeRing& r, const float4* __restrict__ rec,
+                                             const float4* __restrict__ sub_rec,
                                              const uint32_t* __restrict__ sorted_gid, int start, int end,
                                              Extra extra, Flush flush) {
   const int lane = threadIdx.x & 31;
@@ -81,7 +88,7 @@ __device__ __forceinline__ void pipe_produce(PipeRing& r, const float4* __restri
         const int j = lane + 32 * q;
         if (j < cnt) {
           cp_async4(&r.gid[st][j], sorted_gid + start + b * kPipeBatch + j);
-          const float4* src = rec + (size_t)4 * g[q];
+          const float4* src = entry_rec(rec, sub_rec, g[q]);
           cp_async16(&r.rec[st][j][0], src);
           cp_async16(&r.rec[st][j][1], src + 1);
           cp_async16(&r.rec[st][j][2], src + 2);

@@ -11,6 +11,9 @@ under the same names:
     ingest(frame)     A1 project -> A2 bin (all tiles) -> A3/A4 FULL render -> A7 classify
     iteration(frame)  A1 project -> A0 coverage/tile keep -> A2 bin (kept tiles) -> A3/A4 MASKED
                       -> A5 masked backward -> A6 Adam over the unstable Gaussians
+With the NEXT f3 cache (an ingest of the same pose in the current window) the iteration's A1/A2
+touch only the unstable slots: project_subset -> coverage over the slots -> bin_and_sort_cached
+(merge with the frame's cached stable lists).
 """
 from __future__ import annotations
 
@@ -97,9 +100,12 @@ class BinBuffers:
         self.sorted_gid = torch.empty(max(capacity, 1), dtype=torch.int32, device=device)
         self.tile_range = torch.zeros((T, 2), dtype=torch.int32, device=device)
         self.n_instances = torch.zeros(1, dtype=torch.int32, device=device)
+        self.sub = None  # NEXT f3: (sub rec, sub zkey, sub gid) tensors the entries with bit 31 refer to
 
     def c_struct(self):
-        return _abi.Bins(_p(self.sorted_gid), _p(self.tile_range), _p(self.n_instances), self.capacity)
+        sr, sz, sg = self.sub if self.sub is not None else (None, None, None)
+        return _abi.Bins(_p(self.sorted_gid), _p(self.tile_range), _p(self.n_instances), self.capacity, _p(sr), _p(sz),
+                         _p(sg))
 
 
 class RenderBuffers:
@@ -244,6 +250,55 @@ def state_workspace_size(n: int) -> int:
     return int(lib().rtgs_state_workspace_size(n))
 
 
+# ---------------------------------------------------------------------------------------------
+# NEXT f3: window-level stable-projection cache
+# ---------------------------------------------------------------------------------------------
+def project_subset(gm: GaussianMap, gid_list: torch.Tensor, pose: _abi.Pose, cam: _abi.Camera,
+                   proj: ProjectedBuffers, stream=None):
+    """Rows i of `proj` = projection of Gaussian gid_list[i]."""
+    g = gm.c_struct()
+    pr = proj.c_struct()
+    check(lib().rtgs_project_subset(C.byref(g), _p(gid_list), int(gid_list.numel()), C.byref(pose), C.byref(cam),
+                                    C.byref(pr), _stream(stream)), "rtgs_project_subset")
+
+
+def coverage_rows(gm: GaussianMap, proj: ProjectedBuffers, n_rows: int, pose: _abi.Pose, cam: _abi.Camera,
+                  out: RenderBuffers, stream=None):
+    """COVERAGE over every (non-culled) row of a subset projection (flags NULL: all rows unstable)."""
+    g = gm.c_struct()
+    g.flags = None
+    g.n = int(n_rows)
+    pr = proj.c_struct()
+    o = out.c_struct()
+    check(lib().rtgs_render_color_depth(C.byref(g), C.byref(pr), None, C.byref(pose), C.byref(cam),
+                                        RTGS_RENDER_COVERAGE, C.byref(o), _stream(stream)), "rtgs_render_color_depth")
+
+
+def stable_cache_build(full: BinBuffers, flags: torch.Tensor, cam: _abi.Camera, cache: BinBuffers, stream=None):
+    f = full.c_struct()
+    c = cache.c_struct()
+    check(lib().rtgs_stable_cache_build(C.byref(f), _p(flags), C.byref(cam), C.byref(c), _stream(stream)),
+          "rtgs_stable_cache_build")
+
+
+def bin_cached_workspace_size(n_sub: int, cam: _abi.Camera, capacity: int) -> int:
+    return int(lib().rtgs_bin_cached_workspace_size(n_sub, C.byref(cam), capacity))
+
+
+def bin_and_sort_cached(proj: ProjectedBuffers, cache: BinBuffers, sub: ProjectedBuffers, sub_gid: torch.Tensor,
+                        cam: _abi.Camera, tile_keep: torch.Tensor, out: BinBuffers, workspace: torch.Tensor,
+                        stream=None):
+    pr = proj.c_struct()
+    c = cache.c_struct()
+    sp = sub.c_struct()
+    o = out.c_struct()
+    check(lib().rtgs_bin_and_sort_cached(C.byref(pr), C.byref(c), C.byref(sp), _p(sub_gid), int(sub_gid.numel()),
+                                         C.byref(cam), _p(tile_keep), C.byref(o), _p(workspace),
+                                         workspace.numel() * workspace.element_size(), _stream(stream)),
+          "rtgs_bin_and_sort_cached")
+    out.sub = (sub.rec, sub.zkey, sub_gid)
+
+
 def hparams(preset: str = "replica") -> _abi.HParams:
     """Learning rates of P:501: Replica / ScanNet++ vs Azure / TUM."""
     if preset in ("replica", "scannetpp"):
@@ -290,6 +345,12 @@ class MappingEngine:
         self.t_created = torch.zeros(n, dtype=torch.int32, device=device)   # t_i
         self.state_counts = torch.zeros(4, dtype=torch.int32, device=device)
         self.ws_state = torch.empty(state_workspace_size(n), dtype=torch.uint8, device=device)
+        # NEXT f3: the stable part of the last ingested frame's sorted lists (valid for its pose and
+        # until the stable set changes at the window end)
+        self.cache = BinBuffers(cam, self.capacity, device)
+        self.cache_ready = torch.cuda.Event()
+        self.cache_pose = None
+        self.use_cache = True
         self.reset_window()
 
     def reset_window(self):
@@ -317,6 +378,13 @@ class MappingEngine:
             torch.zeros((1, D), device=self.device)
         self.eta_before = self.eta[gid_t].clone() if n_slots else torch.zeros(1, dtype=torch.int32, device=self.device)
         self.step_dev = torch.zeros(1, dtype=torch.int32, device=self.device)  # graph-replayable step
+        # f3: the slots' own projection rows and the cached-binning workspace; the stable set may
+        # have changed, so any cache is invalid until the next ingest
+        self.proj_sub = ProjectedBuffers(n_slots, self.device)
+        self.ws_bin_cached = torch.empty(bin_cached_workspace_size(n_slots, self.cam, self.capacity), dtype=torch.uint8,
+                                         device=self.device)
+        self.cache_pose = None
+        self.proj_iter = self.proj
 
     # --- the two flows ---------------------------------------------------------------------------
     def ingest(self, frame_color, frame_depth, pose: _abi.Pose, seed=0, frame_idx=0, stream=None, after_project=None):
@@ -326,20 +394,39 @@ class MappingEngine:
         if after_project is not None:
             after_project(stream)
         bin_and_sort(self.proj_full, self.gm.n, self.cam, None, self.bins_full, self.ws_bin_full, stream)
+        if self.use_cache:  # f3: the stable lists of this frame, reused by the window's iterations
+            stable_cache_build(self.bins_full, self.gm.flags, self.cam, self.cache, stream)
+            self.cache_ready.record(torch.cuda.current_stream() if stream is None else stream)
+            self.cache_pose = _pose_key(pose)
         render_color_depth(self.gm, self.proj_full, self.bins_full, pose, self.cam, RTGS_RENDER_FULL, self.full, stream)
         classify_and_add_pixels(self.full, frame_color, frame_depth, self.gm.flags, self.cam,
                                 add_params(seed=seed, frame_idx=frame_idx), self.pixel_class, self.samples,
                                 self.add_counts, self.ws_cls, stream)
 
+    def cached(self, pose: _abi.Pose) -> bool:
+        """True when the f3 stable cache holds this pose's lists for the current stable set."""
+        return self.use_cache and self.cache_pose is not None and self.cache_pose == _pose_key(pose)
+
     def forward_masked(self, pose: _abi.Pose, stream=None):
-        """A1 -> A0 -> A2 (kept tiles) -> A3/A4 MASKED (Eq.12)."""
-        project_gaussians(self.gm, pose, self.cam, self.proj, stream)
-        render_color_depth(self.gm, self.proj, None, pose, self.cam, RTGS_RENDER_COVERAGE, self.out, stream)
-        bin_and_sort(self.proj, self.gm.n, self.cam, self.out.tile_keep, self.bins, self.ws_bin, stream)
-        render_color_depth(self.gm, self.proj, self.bins, pose, self.cam, RTGS_RENDER_MASKED, self.out, stream)
+        """A1 -> A0 -> A2 (kept tiles) -> A3/A4 MASKED (Eq.12).  With a valid f3 cache
+        only the unstable slots are projected and binned; the stable lists come from the cache."""
+        if self.cached(pose):
+            project_subset(self.gm, self.gid_of_slot, pose, self.cam, self.proj_sub, stream)
+            coverage_rows(self.gm, self.proj_sub, int(self.gid_of_slot.numel()), pose, self.cam, self.out, stream)
+            (torch.cuda.current_stream() if stream is None else stream).wait_event(self.cache_ready)
+            bin_and_sort_cached(self.proj_full, self.cache, self.proj_sub, self.gid_of_slot, self.cam,
+                                self.out.tile_keep, self.bins, self.ws_bin_cached, stream)
+            self.proj_iter = self.proj_full
+        else:
+            project_gaussians(self.gm, pose, self.cam, self.proj, stream)
+            render_color_depth(self.gm, self.proj, None, pose, self.cam, RTGS_RENDER_COVERAGE, self.out, stream)
+            bin_and_sort(self.proj, self.gm.n, self.cam, self.out.tile_keep, self.bins, self.ws_bin, stream)
+            self.bins.sub = None
+            self.proj_iter = self.proj
+        render_color_depth(self.gm, self.proj_iter, self.bins, pose, self.cam, RTGS_RENDER_MASKED, self.out, stream)
 
     def backward(self, frame_color, frame_depth, pose: _abi.Pose, stream=None):
-        render_backward_masked(self.gm, self.proj, self.bins, pose, self.cam, self.out, frame_color, frame_depth,
+        render_backward_masked(self.gm, self.proj_iter, self.bins, pose, self.cam, self.out, frame_color, frame_depth,
                                self.weights, self.slot_of_gid, self.gid_of_slot, self.grad, self.loss, self.ws_bwd,
                                stream)
 
@@ -393,6 +480,10 @@ class MappingEngine:
         main.wait_event(proj_done)
         self.optimizer_step(main)
         main.wait_stream(side)
+
+
+def _pose_key(pose: _abi.Pose) -> tuple:
+    return tuple(pose.R) + tuple(pose.t)
 
 
 def launch_count() -> int:

@@ -26,7 +26,7 @@ def _declared():
 
 def test_every_declared_symbol_is_exported(L):
     names = _declared()
-    assert len(names) == 16
+    assert len(names) == 20
     for n in names:
         assert hasattr(L, n), n
     from paper_2404_19706_b200 import _abi
@@ -71,3 +71,20 @@ def test_workspace_sizes(L):
     assert 0 < a < b
     assert mapping.backward_workspace_size(100_000) >= 100_000 * 16 * 4
     assert mapping.classify_workspace_size(cam) > 0
+
+
+def test_cache_entry_points_validate_on_host(L):
+    """NEXT f3 calls: null / missing arguments are rejected before any launch (no GPU needed)."""
+    from paper_2404_19706_b200 import _abi, mapping
+    cam = mapping.make_camera(500, 500, 320, 240, 640, 480)
+    pose = mapping.make_pose([[1, 0, 0], [0, 1, 0], [0, 0, 1]], [0, 0, 0])
+    g = _abi.Gaussians(None, None, None, None, None, None, 0, 3)
+    pr = _abi.Projected(None, None, None, None)
+    assert L.rtgs_project_subset(C.byref(g), None, -1, C.byref(pose), C.byref(cam), C.byref(pr), None) == 1
+    assert L.rtgs_project_subset(C.byref(g), None, 5, C.byref(pose), C.byref(cam), C.byref(pr), None) == 1
+    b = _abi.Bins(None, None, None, 0)
+    assert L.rtgs_stable_cache_build(C.byref(b), None, C.byref(cam), C.byref(b), None) == 1
+    assert L.rtgs_bin_and_sort_cached(C.byref(pr), C.byref(b), C.byref(pr), None, 0, C.byref(cam), None, C.byref(b),
+                                      None, 0, None) == 1
+    a = mapping.bin_cached_workspace_size(1000, cam, 1 << 16)
+    assert a > mapping.bin_workspace_size(1000, cam, 1 << 16)
