@@ -90,7 +90,8 @@ rtgs_status rtgs_render_color_depth(const rtgs_gaussians* g, const rtgs_projecte
   }
   if (mode != RTGS_RENDER_FULL && mode != RTGS_RENDER_MASKED) return RTGS_ERR_INVALID_ARG;
   if (!proj || !proj->rec || !proj->zkey || !a16(proj->rec) || !bins_ok(bins)) return RTGS_ERR_INVALID_ARG;
-  if (bins->sub_rec && (!bins->sub_zkey || !bins->sub_gid || !a16(bins->sub_rec))) return RTGS_ERR_INVALID_ARG;
+  // (sub_zkey / sub_gid may be NULL for an empty subset: then no entry carries the subset bit)
+  if (bins->sub_rec && !a16(bins->sub_rec)) return RTGS_ERR_INVALID_ARG;
   if (!out->color || !out->trans || !out->depth || !out->index || !out->n_contrib) return RTGS_ERR_INVALID_ARG;
   if (mode == RTGS_RENDER_MASKED && (!out->active_bits || !out->tile_list || !out->counts))
     return RTGS_ERR_INVALID_ARG;

@@ -166,6 +166,9 @@ __global__ void __launch_bounds__(kPipeThreads) k_render_bwd(const BwdArgs a) {
   bool done = !want;
   const float bx0 = (float)wx0, bx1 = (float)(wx0 + 7), by0 = (float)wy0, by1 = (float)(wy0 + 3);
   const int nb = n > 0 ? (n + kPipeBatch - 1) / kPipeBatch : 0;
+  const uint32_t rec0 = pin(smem_u32(&r.rec[0][0][0])), slot0 = pin(smem_u32(&sm.slot[0][0]));
+  const uint32_t gid0 = pin(smem_u32(&r.gid[0][0]));
+  const int plane = (int)pin((uint32_t)lane);
   float T = 1.f, ar = 0.f, ag = 0.f, ab = 0.f;
   bool wdone = __all_sync(0xffffffffu, done);
   if (wdone && lane == 0) atomicSub(&r.alive, 1);
@@ -173,9 +176,9 @@ __global__ void __launch_bounds__(kPipeThreads) k_render_bwd(const BwdArgs a) {
     const int st = b % kPipeStages;
     mbar_wait(&r.full[st], (uint32_t)(b / kPipeStages) & 1u);
     if (!wdone) {
-      const uint32_t srec = smem_u32(&r.rec[st][0][0]);  // shared addresses, computed once per batch
-      const uint32_t sslot = smem_u32(&sm.slot[st][0]);
-      const uint32_t sgid = smem_u32(&r.gid[st][0]);
+      const uint32_t srec = rec0 + (uint32_t)(st * sizeof(r.rec[0]));  // shared addresses of this stage
+      const uint32_t sslot = slot0 + (uint32_t)(st * sizeof(sm.slot[0]));
+      const uint32_t sgid = gid0 + (uint32_t)(st * sizeof(r.gid[0]));
       const uint32_t pbase = (uint32_t)(start + b * kPipeBatch);
       const int cnt = min(kPipeBatch, n - b * kPipeBatch);
       for (int g0 = 0; g0 < cnt; g0 += 32) {
@@ -211,7 +214,7 @@ __global__ void __launch_bounds__(kPipeThreads) k_render_bwd(const BwdArgs a) {
             float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
             if (ok) {
               // S_i = sum_{j>i} c_j f_j T_j = C^ - prefix_i ;  dC/df_i = c_i T_i - S_i / (1 - f_i)
-              const float inv1mf = 1.f / (1.f - e.f);
+              const float inv1mf = __fdividef(1.f, 1.f - e.f);  // 1 - f >= 0.01
               const float dLdf = gCr * (r2.x * T - (Cr - ar) * inv1mf) + gCg * (r2.y * T - (Cg - ag) * inv1mf) +
                                  gCb * (r2.z * T - (Cb - ab) * inv1mf);
               // f = alpha e^power; the 0.99 cap passes no gradient when active (R17)
@@ -228,8 +231,8 @@ __global__ void __launch_bounds__(kPipeThreads) k_render_bwd(const BwdArgs a) {
               v[7] = gCb * wgt;
             }
             int vj;
-            const float x = warp_reduce8(v, lane, vj);
-            if ((lane & 3) == 0) atomicAdd(a.sgrad + (size_t)slot * kSG + vj, x);  // 8 lanes, 8 values
+            const float x = warp_reduce8(v, plane, vj);
+            if ((plane & 3) == 0) atomicAdd(a.sgrad + (size_t)slot * kSG + vj, x);  // 8 lanes, 8 values
           }
           T = ok ? test : T;
         }

@@ -387,43 +387,70 @@ __global__ void __launch_bounds__(256) k_cache_build(const uint2* __restrict__ f
   }
 }
 
-// one CTA: output ranges of the merged lists, count(t) = keep[t] ? |stable(t)| + |subset(t)| : 0
-__global__ void __launch_bounds__(1024) k_merge_offsets(const uint8_t* __restrict__ keep,
-                                                        const uint2* __restrict__ crange,
-                                                        const uint2* __restrict__ srange, int T, uint32_t cap,
-                                                        uint2* __restrict__ range, uint32_t* __restrict__ n_inst) {
+// one CTA, after k_tile_count of the subset: the subset's own ranges and replica starts (as
+// k_tile_offsets) AND the merged output ranges, count(t) = keep[t] ? |stable(t)| + |subset(t)| : 0
+__global__ void __launch_bounds__(1024) k_merge_offsets(const uint32_t* __restrict__ cnt, const uint8_t* __restrict__ keep,
+                                                        const uint2* __restrict__ crange, int T, uint32_t cap,
+                                                        uint32_t* __restrict__ start, uint2* __restrict__ srange,
+                                                        uint2* __restrict__ orange, uint32_t* __restrict__ n_inst) {
   __shared__ uint32_t sh[33];
-  __shared__ uint32_t carry;
-  if (threadIdx.x == 0) carry = 0;
+  __shared__ uint32_t carry[2];
+  if (threadIdx.x == 0) carry[0] = carry[1] = 0;
   __syncthreads();
   for (int b = 0; b < T; b += 1024 * kOffTiles) {
     const int t0 = b + threadIdx.x * kOffTiles;
-    uint32_t c[kOffTiles], s = 0;
+    uint32_t c[kOffTiles][kRep];
+    uint32_t cl[kOffTiles];
 #pragma unroll
     for (int q = 0; q < kOffTiles; ++q) {
-      c[q] = 0;
+#pragma unroll
+      for (int r = 0; r < kRep; ++r) c[q][r] = (t0 + q < T) ? cnt[(size_t)r * T + t0 + q] : 0u;
+      cl[q] = 0;
       if (t0 + q < T && keep[t0 + q]) {
-        const uint2 a = crange[t0 + q], u = srange[t0 + q];
-        c[q] = (a.y - a.x) + (u.y - u.x);
+        const uint2 a = crange[t0 + q];
+        cl[q] = a.y - a.x;
       }
-      s += c[q];
     }
-    uint32_t tot;
-    uint32_t ex = block_excl_scan(s, sh, &tot) + carry;
+    uint32_t tsum[kOffTiles], s = 0, s2 = 0;
 #pragma unroll
     for (int q = 0; q < kOffTiles; ++q) {
-      if (t0 + q < T) {
-        const uint32_t s0 = ex < cap ? ex : cap;
-        const uint32_t e0 = ex + c[q] < cap ? ex + c[q] : cap;
-        range[t0 + q] = make_uint2(c[q] ? s0 : 0u, c[q] ? e0 : 0u);
+      tsum[q] = 0;
+#pragma unroll
+      for (int r = 0; r < kRep; ++r) tsum[q] += c[q][r];
+      s += tsum[q];
+      cl[q] += tsum[q];  // merged count (the subset was binned on kept tiles only)
+      s2 += cl[q];
+    }
+    uint32_t tot, tot2;
+    uint32_t ex = block_excl_scan(s, sh, &tot) + carry[0];
+    __syncthreads();
+    uint32_t ex2 = block_excl_scan(s2, sh, &tot2) + carry[1];
+#pragma unroll
+    for (int q = 0; q < kOffTiles; ++q) {
+      const int t = t0 + q;
+      if (t < T) {
+        uint32_t o = ex;
+#pragma unroll
+        for (int r = 0; r < kRep; ++r) {
+          start[(size_t)r * T + t] = o;
+          o += c[q][r];
+        }
+        srange[t] = make_uint2(min(ex, cap), min(ex + tsum[q], cap));  // subset keys: capacity entries
+        const uint32_t s0 = ex2 < cap ? ex2 : cap;
+        const uint32_t e0 = ex2 + cl[q] < cap ? ex2 + cl[q] : cap;
+        orange[t] = make_uint2(cl[q] ? s0 : 0u, cl[q] ? e0 : 0u);
       }
-      ex += c[q];
+      ex += tsum[q];
+      ex2 += cl[q];
     }
     __syncthreads();
-    if (threadIdx.x == 0) carry += tot;
+    if (threadIdx.x == 0) {
+      carry[0] += tot;
+      carry[1] += tot2;
+    }
     __syncthreads();
   }
-  if (threadIdx.x == 0) *n_inst = carry;
+  if (threadIdx.x == 0) *n_inst = carry[1];
 }
 
 // number of elements of the sorted key list k[0..n) that are < key (keys are distinct)
@@ -438,25 +465,14 @@ __device__ __forceinline__ int rank_below(KeyAt k, int n, unsigned long long key
   return lo;
 }
 
-constexpr int kMergeCap = 3072;  // merged lists up to this length are ranked from shared memory
-
-// one CTA per tile: merge the cached stable list S (gids) and the sorted subset list U (rows) of a
-// kept tile by (zkey bits, gid); element i of S lands at i + |{u in U : u < S_i}| and vice versa.
-__global__ void __launch_bounds__(256) k_merge(const uint8_t* __restrict__ keep, const uint2* __restrict__ crange,
-                                               const uint32_t* __restrict__ csorted, const uint32_t* __restrict__ zfull,
-                                               const uint2* __restrict__ srange, const uint32_t* __restrict__ ssorted,
-                                               const uint32_t* __restrict__ szkey, const int32_t* __restrict__ sgid,
-                                               const uint2* __restrict__ orange, uint32_t cap,
-                                               uint32_t* __restrict__ out) {
-  __shared__ unsigned long long sk[kMergeCap];
-  const int t = blockIdx.x;
-  if (!keep[t]) return;
-  const uint2 cr = crange[t], sr = srange[t];
-  const int nS = (int)(cr.y - cr.x), nU = (int)(sr.y - sr.x);
-  if (nS + nU == 0) return;
-  const uint32_t o = orange[t].x;
-  const uint32_t* S = csorted + cr.x;
-  const uint32_t* U = ssorted + sr.x;
+// Merge the cached stable list S (gids) and the sorted subset list U (rows) of one tile by
+// (zkey bits, gid): element i of S lands at i + |{u in U : u < S_i}| and vice versa (keys distinct).
+// Keys are ranked from the shared buffer sk when both lists fit, else fetched from global memory.
+__device__ __forceinline__ void merge_tile(const uint32_t* __restrict__ S, int nS, const uint32_t* __restrict__ U,
+                                           int nU, const uint32_t* __restrict__ zfull,
+                                           const uint32_t* __restrict__ szkey, const int32_t* __restrict__ sgid,
+                                           uint32_t o, uint32_t cap, uint32_t* __restrict__ out,
+                                           unsigned long long* sk, int sk_cap) {
   auto keyS = [&](int i) {
     const uint32_t g = S[i];
     return ((unsigned long long)zfull[g] << 32) | g;
@@ -465,30 +481,71 @@ __global__ void __launch_bounds__(256) k_merge(const uint8_t* __restrict__ keep,
     const uint32_t r = U[j];
     return ((unsigned long long)szkey[r] << 32) | (uint32_t)sgid[r];
   };
-  if (nS + nU <= kMergeCap) {
-    for (int i = threadIdx.x; i < nS; i += 256) sk[i] = keyS(i);
-    for (int j = threadIdx.x; j < nU; j += 256) sk[nS + j] = keyU(j);
+  if (nS + nU <= sk_cap) {
+    for (int i = threadIdx.x; i < nS; i += blockDim.x) sk[i] = keyS(i);
+    for (int j = threadIdx.x; j < nU; j += blockDim.x) sk[nS + j] = keyU(j);
     __syncthreads();
     const unsigned long long* kS = sk;
     const unsigned long long* kU = sk + nS;
-    for (int i = threadIdx.x; i < nS; i += 256) {
+    for (int i = threadIdx.x; i < nS; i += blockDim.x) {
       const uint32_t p = o + (uint32_t)(i + rank_below([&](int m) { return kU[m]; }, nU, kS[i]));
       if (p < cap) out[p] = S[i];
     }
-    for (int j = threadIdx.x; j < nU; j += 256) {
+    for (int j = threadIdx.x; j < nU; j += blockDim.x) {
       const uint32_t p = o + (uint32_t)(j + rank_below([&](int m) { return kS[m]; }, nS, kU[j]));
       if (p < cap) out[p] = 0x80000000u | U[j];
     }
   } else {  // long lists: keys fetched from global memory during the searches
-    for (int i = threadIdx.x; i < nS; i += 256) {
+    for (int i = threadIdx.x; i < nS; i += blockDim.x) {
       const uint32_t p = o + (uint32_t)(i + rank_below(keyU, nU, keyS(i)));
       if (p < cap) out[p] = S[i];
     }
-    for (int j = threadIdx.x; j < nU; j += 256) {
+    for (int j = threadIdx.x; j < nU; j += blockDim.x) {
       const uint32_t p = o + (uint32_t)(j + rank_below(keyS, nS, keyU(j)));
       if (p < cap) out[p] = 0x80000000u | U[j];
     }
   }
+}
+
+// one CTA per kept tile: sort the tile's subset instances (as k_tile_sort, rows as ids; the rows
+// are in gid order, so (zkey, row) order is (zkey, gid) order), then merge them with the cached
+// stable list into the output range.  Shared memory: the sort's key buffers, reused by the merge.
+__global__ void __launch_bounds__(kSortThreads) k_sort_merge(const uint8_t* __restrict__ keep,
+                                                             const uint2* __restrict__ srange,
+                                                             unsigned long long* __restrict__ keys,
+                                                             unsigned long long* __restrict__ tmp,
+                                                             uint32_t* __restrict__ grank, int row_bits,
+                                                             uint32_t* __restrict__ ssorted,
+                                                             const uint2* __restrict__ crange,
+                                                             const uint32_t* __restrict__ csorted,
+                                                             const uint32_t* __restrict__ zfull,
+                                                             const uint32_t* __restrict__ szkey,
+                                                             const int32_t* __restrict__ sgid,
+                                                             const uint2* __restrict__ orange, uint32_t cap,
+                                                             uint32_t* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned long long s_keys[];  // [2 * kSortCap] keys + kSortCap ranks
+  __shared__ uint32_t wcnt[kSortWarps][256];
+  __shared__ uint32_t dstart[256];
+  __shared__ uint32_t scan_sh[33];
+  __shared__ uint32_t s_zmm[2];
+  const int t = blockIdx.x;
+  if (!keep[t]) return;
+  const uint2 sr = srange[t], cr = crange[t];
+  const int nU = (int)(sr.y - sr.x), nS = (int)(cr.y - cr.x);
+  if (nS + nU == 0) return;
+  unsigned long long* seg = keys + sr.x;
+  if (nU == 1) {
+    if (threadIdx.x == 0) ssorted[sr.x] = (uint32_t)(seg[0] & 0xFFFFFFFFull);
+  } else if (nU > 1 && nU <= kSortCap) {
+    sort_tile(seg, s_keys, s_keys + kSortCap, reinterpret_cast<uint32_t*>(s_keys + 2 * kSortCap), nU, row_bits,
+              ssorted + sr.x, true, wcnt, dstart, scan_sh, s_zmm);
+  } else if (nU > kSortCap) {
+    sort_tile(seg, seg, tmp + sr.x, grank + sr.x, nU, row_bits, ssorted + sr.x, false, wcnt, dstart, scan_sh,
+              s_zmm);
+  }
+  __syncthreads();  // sorted rows (global) visible to the whole CTA; shared buffers free again
+  merge_tile(csorted + cr.x, nS, ssorted + sr.x, nU, zfull, szkey, sgid, orange[t].x, cap, out, s_keys,
+             (int)(kSortCap * 5 / 2));
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -604,20 +661,36 @@ cudaError_t launch_bin_cached(const rtgs_projected& proj, const rtgs_bins& cache
   uint32_t* sn;
   void* bws;
   carve_cached(n_sub, cam, out.capacity, static_cast<char*>(ws), &ssorted, &srange, &sn, &bws);
-  rtgs_bins sb;
-  sb.sorted_gid = ssorted;
-  sb.tile_range = reinterpret_cast<uint32_t*>(srange);
-  sb.n_instances = sn;
-  sb.capacity = out.capacity;
-  sb.sub_rec = nullptr; sb.sub_zkey = nullptr; sb.sub_gid = nullptr;
-  cudaError_t e = launch_bin(sub, n_sub, cam, keep, sb, bws, s);  // subset rows of the kept tiles, sorted
-  if (e != cudaSuccess) return e;
-  k_merge_offsets<<<1, 1024, 0, s>>>(keep, reinterpret_cast<const uint2*>(cache.tile_range), srange, T, out.capacity,
-                                     reinterpret_cast<uint2*>(out.tile_range), out.n_instances);
-  k_merge<<<T, 256, 0, s>>>(keep, reinterpret_cast<const uint2*>(cache.tile_range), cache.sorted_gid, proj.zkey, srange,
-                            ssorted, sub.zkey, sub_gid, reinterpret_cast<const uint2*>(out.tile_range), out.capacity,
-                            out.sorted_gid);
-  note_launch(2);
+  (void)sn;
+  BinWS w;
+  carve(n_sub, cam, out.capacity, &w, static_cast<char*>(bws));
+  cudaMemsetAsync(w.cnt, 0, (size_t)((char*)w.start - (char*)w.cnt), s);
+  const uint2* rect = reinterpret_cast<const uint2*>(sub.rect);
+  const int nblk = (n_sub + 255) / 256;
+  if (n_sub > 0) {
+    k_tile_count<<<nblk, 256, 0, s>>>(sub.zkey, rect, keep, n_sub, k.TX, T, w.cnt);
+    note_launch();
+  }
+  k_merge_offsets<<<1, 1024, 0, s>>>(w.cnt, keep, reinterpret_cast<const uint2*>(cache.tile_range), T, out.capacity,
+                                     w.start, srange, reinterpret_cast<uint2*>(out.tile_range), out.n_instances);
+  note_launch();
+  if (n_sub > 0) {
+    k_emit<<<nblk, 256, 0, s>>>(sub.zkey, rect, keep, n_sub, k.TX, T, w.start, w.cursor, out.capacity, w.keys);
+    note_launch();
+  }
+  int row_bits = 1;
+  while (row_bits < 32 && (1u << row_bits) < (uint32_t)n_sub) ++row_bits;
+  const size_t smem = (size_t)kSortCap * (8 + 8 + 4);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_sort_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  k_sort_merge<<<T, kSortThreads, smem, s>>>(keep, srange, w.keys, w.tmp, w.grank, row_bits, ssorted,
+                                             reinterpret_cast<const uint2*>(cache.tile_range), cache.sorted_gid,
+                                             proj.zkey, sub.zkey, sub_gid, reinterpret_cast<const uint2*>(out.tile_range),
+                                             out.capacity, out.sorted_gid);
+  note_launch();
   return cudaGetLastError();
 }
 

@@ -39,6 +39,13 @@ __device__ __forceinline__ void pipe_init(PipeRing& r) {
   }
 }
 
+// Keep a loop-invariant value in a register: the compiler otherwise re-derives shared addresses
+// (S2UR SR_CgaCtaId) and lane bits (S2R SR_TID) inside the inner loops, paying their latency there.
+__device__ __forceinline__ uint32_t pin(uint32_t x) {
+  asm volatile("" : "+r"(x));
+  return x;
+}
+
 // explicit shared-space 128-bit load (32-bit shared address: no generic-to-shared conversion in
 // the consumers' inner loops)
 __device__ __forceinline__ float4 lds128(uint32_t addr) {

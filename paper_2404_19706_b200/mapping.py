@@ -359,7 +359,9 @@ class MappingEngine:
         gid = np.nonzero((flags & FLAG_STABLE) == 0)[0].astype(np.int32)
         slot = np.full(self.gm.n, -1, dtype=np.int32)
         slot[gid] = np.arange(len(gid), dtype=np.int32)
-        self.gid_of_slot = torch.as_tensor(gid, device=self.device)
+        # (storage of >= 1 element: a valid pointer even for an empty slot set)
+        self.gid_of_slot = torch.zeros(max(len(gid), 1), dtype=torch.int32, device=self.device)[: len(gid)]
+        self.gid_of_slot.copy_(torch.as_tensor(gid))
         self.slot_of_gid = torch.as_tensor(slot, device=self.device)
         n_slots = len(gid)
         D = 10 + 3 * (self.gm.sh_degree + 1) ** 2

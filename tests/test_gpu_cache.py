@@ -102,8 +102,9 @@ def _engine(api, name, n=None):
     cam = api.camera_of(cfg)
     pose = api.make_pose(R, t)
     eng = api.MappingEngine(gm, cam)
-    col, dep = make_frame(cfg)
-    return cfg, scene, gm, cam, pose, eng, col, dep
+    col, dep = make_frame(cfg, (R, t))
+    return (cfg, scene, gm, cam, pose, eng, torch.as_tensor(col, device="cuda"),
+            torch.as_tensor(dep, device="cuda"))
 
 
 def _run(api, eng, pose, col, dep, cached):
@@ -147,6 +148,7 @@ def _same(a, b):
 def test_cached_iteration_equals_uncached(api, name):
     cfg, scene, gm, cam, pose, eng, col, dep = _engine(api, name)
     base = _run(api, eng, pose, col, dep, cached=False)
+    eng.use_cache = True
     eng.ingest(col, dep, pose)                       # builds the f3 cache for this pose
     cached = _run(api, eng, pose, col, dep, cached=True)
     assert base["counts"][0] > 0 and (cached["bins"] >= 0).all()
