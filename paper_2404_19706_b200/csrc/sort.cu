@@ -124,9 +124,11 @@ __global__ void __launch_bounds__(256) k_tile_count(const uint32_t* __restrict__
                                                     uint32_t* __restrict__ cnt) {
   const int i = blockIdx.x * 256 + threadIdx.x;
   cnt += (size_t)(blockIdx.x & (kRep - 1)) * T;
-  if (i >= n || zkey[i] == 0xFFFFFFFFu) return;
+  if (i >= n) return;
+  const uint32_t z = zkey[i];
+  const uint2 rc = rect[i];  // both loads in flight together
   int tx0, ty0, tx1, ty1;
-  if (!rect_tiles(rect[i], tx0, ty0, tx1, ty1)) return;
+  if (z == 0xFFFFFFFFu || !rect_tiles(rc, tx0, ty0, tx1, ty1)) return;
   for (int ty = ty0; ty <= ty1; ++ty)
     for (int tx = tx0; tx <= tx1; ++tx) {
       const int t = ty * TX + tx;
@@ -136,52 +138,66 @@ __global__ void __launch_bounds__(256) k_tile_count(const uint32_t* __restrict__
 
 // one CTA: tile_range[t] = [start, start + count) (clamped to the capacity), n_instances, and the
 // start of every counter replica inside its tile: start[r][t] = start(t) + sum_{r' < r} cnt[r'][t].
-// Each thread owns kOffTiles consecutive tiles per pass so that all their counter loads are in
-// flight together (one memory round trip per 4096 tiles instead of one per 1024).
+// Passes of kOffChunk tiles: coalesced counter loads (thread owns tiles b + k*1024 + tid), per-tile
+// sums through shared memory to a blocked scan (thread owns 4 consecutive tiles), coalesced stores.
 constexpr int kOffTiles = 4;
+constexpr int kOffChunk = 1024 * kOffTiles;
+
+// exclusive scan of s_v[0..kOffChunk) in place (blocked: thread owns 4 consecutive entries);
+// returns the chunk total; ends with a barrier
+__device__ __forceinline__ uint32_t chunk_scan(uint32_t* s_v, uint32_t* sh) {
+  uint4 v = reinterpret_cast<uint4*>(s_v)[threadIdx.x];
+  uint32_t tot;
+  uint32_t ex = block_excl_scan(v.x + v.y + v.z + v.w, sh, &tot);
+  uint4 o;
+  o.x = ex; ex += v.x;
+  o.y = ex; ex += v.y;
+  o.z = ex; ex += v.z;
+  o.w = ex;
+  reinterpret_cast<uint4*>(s_v)[threadIdx.x] = o;
+  __syncthreads();
+  return tot;
+}
+
 __global__ void __launch_bounds__(1024) k_tile_offsets(const uint32_t* __restrict__ cnt, int T, uint32_t cap,
                                                        uint32_t* __restrict__ start, uint2* __restrict__ range,
                                                        uint32_t* __restrict__ n_inst) {
+  __shared__ __align__(16) uint32_t s_ex[kOffChunk];
   __shared__ uint32_t sh[33];
-  __shared__ uint32_t carry;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  for (int b = 0; b < T; b += 1024 * kOffTiles) {
-    const int t0 = b + threadIdx.x * kOffTiles;
-    uint32_t c[kOffTiles][kRep];
+  uint32_t carry = 0;
+  for (int b = 0; b < T; b += kOffChunk) {
+    uint32_t c[kOffTiles][kRep], tsum[kOffTiles];
 #pragma unroll
-    for (int q = 0; q < kOffTiles; ++q)
+    for (int k = 0; k < kOffTiles; ++k) {
+      const int t = b + k * 1024 + threadIdx.x;
+      tsum[k] = 0;
 #pragma unroll
-      for (int r = 0; r < kRep; ++r) c[q][r] = (t0 + q < T) ? cnt[(size_t)r * T + t0 + q] : 0u;
-    uint32_t tsum[kOffTiles], s = 0;
-#pragma unroll
-    for (int q = 0; q < kOffTiles; ++q) {
-      tsum[q] = 0;
-#pragma unroll
-      for (int r = 0; r < kRep; ++r) tsum[q] += c[q][r];
-      s += tsum[q];
+      for (int r = 0; r < kRep; ++r) {
+        c[k][r] = t < T ? cnt[(size_t)r * T + t] : 0u;
+        tsum[k] += c[k][r];
+      }
+      s_ex[k * 1024 + threadIdx.x] = tsum[k];
     }
-    uint32_t tot;
-    uint32_t ex = block_excl_scan(s, sh, &tot) + carry;
+    __syncthreads();
+    const uint32_t tot = chunk_scan(s_ex, sh);
 #pragma unroll
-    for (int q = 0; q < kOffTiles; ++q) {
-      const int t = t0 + q;
+    for (int k = 0; k < kOffTiles; ++k) {
+      const int t = b + k * 1024 + threadIdx.x;
       if (t < T) {
+        const uint32_t ex = s_ex[k * 1024 + threadIdx.x] + carry;
         uint32_t o = ex;
 #pragma unroll
         for (int r = 0; r < kRep; ++r) {
           start[(size_t)r * T + t] = o;
-          o += c[q][r];
+          o += c[k][r];
         }
         const uint32_t s0 = ex < cap ? ex : cap;
-        const uint32_t e0 = ex + tsum[q] < cap ? ex + tsum[q] : cap;
-        range[t] = make_uint2(tsum[q] ? s0 : 0u, tsum[q] ? e0 : 0u);
+        const uint32_t e0 = ex + tsum[k] < cap ? ex + tsum[k] : cap;
+        range[t] = make_uint2(tsum[k] ? s0 : 0u, tsum[k] ? e0 : 0u);
       }
-      ex += tsum[q];
     }
-    __syncthreads();
-    if (threadIdx.x == 0) carry += tot;
-    __syncthreads();
+    carry += tot;
+    __syncthreads();  // s_ex reused by the next chunk
   }
   if (threadIdx.x == 0) *n_inst = carry;
 }
@@ -196,17 +212,32 @@ __global__ void __launch_bounds__(256) k_emit(const uint32_t* __restrict__ zkey,
   cursor += rep;
   if (i >= n) return;
   const uint32_t z = zkey[i];
-  if (z == 0xFFFFFFFFu) return;
+  const uint2 rc = rect[i];
   int tx0, ty0, tx1, ty1;
-  if (!rect_tiles(rect[i], tx0, ty0, tx1, ty1)) return;
+  if (z == 0xFFFFFFFFu || !rect_tiles(rc, tx0, ty0, tx1, ty1)) return;
   const unsigned long long k = ((unsigned long long)z << 32) | (uint32_t)i;
-  for (int ty = ty0; ty <= ty1; ++ty)
-    for (int tx = tx0; tx <= tx1; ++tx) {
-      const int t = ty * TX + tx;
-      if (keep && !keep[t]) continue;
-      const uint32_t pos = start[t] + atomicAdd(&cursor[t], 1u);
-      if (pos < cap) keys[pos] = k;
+  // tiles in groups of 4: the group's cursor atomics (and start loads) are all in flight before
+  // the first store, instead of one atomic round trip per tile
+  const int w = tx1 - tx0 + 1, nt = w * (ty1 - ty0 + 1);
+  for (int q0 = 0; q0 < nt; q0 += 4) {
+    int t[4];
+    uint32_t base[4], off[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int q = q0 + u;
+      t[u] = q < nt ? (ty0 + q / w) * TX + tx0 + q % w : -1;
+      if (t[u] >= 0 && keep && !keep[t[u]]) t[u] = -1;
     }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (t[u] >= 0) {
+        base[u] = start[t[u]];
+        off[u] = atomicAdd(&cursor[t[u]], 1u);
+      }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (t[u] >= 0 && base[u] + off[u] < cap) keys[base[u] + off[u]] = k;
+  }
 }
 
 // Stable LSD radix sort of n 64-bit keys by one CTA on key bits [lo, lo + nbits) (8-bit digits).
@@ -393,64 +424,58 @@ __global__ void __launch_bounds__(1024) k_merge_offsets(const uint32_t* __restri
                                                         const uint2* __restrict__ crange, int T, uint32_t cap,
                                                         uint32_t* __restrict__ start, uint2* __restrict__ srange,
                                                         uint2* __restrict__ orange, uint32_t* __restrict__ n_inst) {
+  __shared__ __align__(16) uint32_t s_ex[kOffChunk];
+  __shared__ __align__(16) uint32_t s_ex2[kOffChunk];
   __shared__ uint32_t sh[33];
-  __shared__ uint32_t carry[2];
-  if (threadIdx.x == 0) carry[0] = carry[1] = 0;
-  __syncthreads();
-  for (int b = 0; b < T; b += 1024 * kOffTiles) {
-    const int t0 = b + threadIdx.x * kOffTiles;
-    uint32_t c[kOffTiles][kRep];
-    uint32_t cl[kOffTiles];
+  uint32_t carry = 0, carry2 = 0;
+  for (int b = 0; b < T; b += kOffChunk) {
+    uint32_t c[kOffTiles][kRep], tsum[kOffTiles], cl[kOffTiles];
 #pragma unroll
-    for (int q = 0; q < kOffTiles; ++q) {
-#pragma unroll
-      for (int r = 0; r < kRep; ++r) c[q][r] = (t0 + q < T) ? cnt[(size_t)r * T + t0 + q] : 0u;
-      cl[q] = 0;
-      if (t0 + q < T && keep[t0 + q]) {
-        const uint2 a = crange[t0 + q];
-        cl[q] = a.y - a.x;
-      }
-    }
-    uint32_t tsum[kOffTiles], s = 0, s2 = 0;
-#pragma unroll
-    for (int q = 0; q < kOffTiles; ++q) {
-      tsum[q] = 0;
-#pragma unroll
-      for (int r = 0; r < kRep; ++r) tsum[q] += c[q][r];
-      s += tsum[q];
-      cl[q] += tsum[q];  // merged count (the subset was binned on kept tiles only)
-      s2 += cl[q];
-    }
-    uint32_t tot, tot2;
-    uint32_t ex = block_excl_scan(s, sh, &tot) + carry[0];
-    __syncthreads();
-    uint32_t ex2 = block_excl_scan(s2, sh, &tot2) + carry[1];
-#pragma unroll
-    for (int q = 0; q < kOffTiles; ++q) {
-      const int t = t0 + q;
+    for (int k = 0; k < kOffTiles; ++k) {
+      const int t = b + k * 1024 + threadIdx.x;
+      tsum[k] = 0;
+      cl[k] = 0;
+      uint2 a = make_uint2(0u, 0u);
+      uint8_t kp = 0;
       if (t < T) {
+        a = crange[t];
+        kp = keep[t];
+      }
+#pragma unroll
+      for (int r = 0; r < kRep; ++r) {
+        c[k][r] = t < T ? cnt[(size_t)r * T + t] : 0u;
+        tsum[k] += c[k][r];
+      }
+      cl[k] = kp ? (a.y - a.x) + tsum[k] : 0u;  // the subset was binned on kept tiles only
+      s_ex[k * 1024 + threadIdx.x] = tsum[k];
+      s_ex2[k * 1024 + threadIdx.x] = cl[k];
+    }
+    __syncthreads();
+    const uint32_t tot = chunk_scan(s_ex, sh);
+    const uint32_t tot2 = chunk_scan(s_ex2, sh);
+#pragma unroll
+    for (int k = 0; k < kOffTiles; ++k) {
+      const int t = b + k * 1024 + threadIdx.x;
+      if (t < T) {
+        const uint32_t ex = s_ex[k * 1024 + threadIdx.x] + carry;
+        const uint32_t ex2 = s_ex2[k * 1024 + threadIdx.x] + carry2;
         uint32_t o = ex;
 #pragma unroll
         for (int r = 0; r < kRep; ++r) {
           start[(size_t)r * T + t] = o;
-          o += c[q][r];
+          o += c[k][r];
         }
-        srange[t] = make_uint2(min(ex, cap), min(ex + tsum[q], cap));  // subset keys: capacity entries
+        srange[t] = make_uint2(min(ex, cap), min(ex + tsum[k], cap));  // subset keys: capacity entries
         const uint32_t s0 = ex2 < cap ? ex2 : cap;
-        const uint32_t e0 = ex2 + cl[q] < cap ? ex2 + cl[q] : cap;
-        orange[t] = make_uint2(cl[q] ? s0 : 0u, cl[q] ? e0 : 0u);
+        const uint32_t e0 = ex2 + cl[k] < cap ? ex2 + cl[k] : cap;
+        orange[t] = make_uint2(cl[k] ? s0 : 0u, cl[k] ? e0 : 0u);
       }
-      ex += tsum[q];
-      ex2 += cl[q];
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      carry[0] += tot;
-      carry[1] += tot2;
-    }
+    carry += tot;
+    carry2 += tot2;
     __syncthreads();
   }
-  if (threadIdx.x == 0) *n_inst = carry[1];
+  if (threadIdx.x == 0) *n_inst = carry2;
 }
 
 // number of elements of the sorted key list k[0..n) that are < key (keys are distinct)
