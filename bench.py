@@ -199,7 +199,7 @@ def main():
     # each rank optimises the shared map from its own keyframe view (rank 0 = the primary view)
     R, t = make_pose(cfg) if rank == 0 else make_pose(cfg, view=rank)
     col_h, dep_h = make_frame(cfg, (R, t))
-    gm = P.GaussianMap.from_arrays(scene)
+    gm = P.GaussianMap.from_arrays(scene, capacity=cfg.n + 1 + cfg.width * cfg.height // 8)  # room for f2 rows
     cam = P.camera_of(cfg)
     pose = P.make_pose(R, t)
     eng = P.MappingEngine(gm, cam, capacity=4 * cfg.n)
@@ -374,6 +374,17 @@ def main():
         torch.cuda.synchronize()
         phases["window.manage_states_ms"] = e0.elapsed_time(e1)
         gm.flags.copy_(flags_keep)
+        # NEXT f2 (once per frame, not part of the step): insertion for this frame's A7 samples
+        # (grids over the 1M existing Gaussians, exact 3-NN, Eq.11); the map is not resized after
+        P.classify_and_add_pixels(eng.full, col, dep, gm.flags, cam, P.add_params(seed=1234), eng.pixel_class,
+                                  eng.samples, eng.add_counts, eng.ws_cls)
+        hold(0.5)
+        e0.record(stream)
+        eng.insert(col, dep, pose, frame_idx=1, sync=False)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        phases["frame.add_gaussians_ms"] = e0.elapsed_time(e1)
+        insert_result = eng.insert_result.cpu().numpy().tolist()
         restore()
         blends_full = int(eng.full.counts[3].item())
         blends_masked = int(eng.out.counts[3].item())
@@ -486,6 +497,8 @@ def main():
             "phases_ms": {k: round(v, 4) for k, v in phases.items()},
             "iter_ms": round(sum(v for k, v in phases.items() if k.startswith("iter.")), 4),
             "ingest_ms": round(sum(v for k, v in phases.items() if k.startswith("ingest.")), 4),
+            "f2_insert": {"result": dict(zip(["opaque", "transparent", "skipped", "dropped", "n_after"], insert_result)),
+                          "ms": round(phases["frame.add_gaussians_ms"], 4), "in_step": False},
             "active": {"kept_tiles": counts[0], "active_px": counts[1], "instances_full": n_inst,
                        "instances_iter": ninst_iter},
         }

@@ -322,6 +322,50 @@ rtgs_status rtgs_bin_and_sort_cached(const rtgs_projected* proj, const rtgs_bins
                                      const uint8_t* tile_keep, rtgs_bins* out, void* workspace,
                                      size_t workspace_bytes, void* stream);
 
+/* =============================================================================================
+ * NEXT row f2: Gaussian insertion for the sampled add-mask pixels
+ * (P:232 input pre-processing, Supp. A Eq.11; readings R26, R30-R32).
+ * ============================================================================================= */
+
+/* The growable map: the arrays of rtgs_gaussians plus the per-Gaussian state, `capacity` rows
+ * allocated, rows [0, n) live.  eta / err_count / t_created as in rtgs_manage_states. */
+typedef struct {
+  float *pos, *log_scale, *rot, *opacity, *sh;
+  uint8_t* flags;
+  uint32_t *eta, *err_count, *t_created;
+  int32_t n, capacity, sh_degree;
+} rtgs_map;
+
+typedef struct {
+  float normal_guard;          /* 0.1 m: a central-difference neighbour depth further than this from
+                                  D(u) (float32 |D_nb - D| > guard) invalidates the normal (R31)      */
+  float min_scale;             /* 1e-4 m lower clamp of s_1 (R30)                                     */
+  float max_scale_transparent; /* 0.01 m                                                      */
+  float cell;                  /* finest kNN grid cell in metres (<= 0: 0.02); performance only        */
+  uint32_t frame_idx;          /* t = k of the new Gaussians                                  */
+} rtgs_insert_params;
+
+/* rtgs_add_gaussians: for the first min(add_counts[2] + add_counts[3], sample_cap) entries of the
+ * A7 sample list (pixel | action << 30; action 1 opaque alpha 0.99, 2 transparent alpha 0.1) on the
+ * frame (C_k, D_k) at camera->world pose T_{g,k}:
+ *   v = D(u) K^-1 (px, py, 1) (R1), n = normalize((v(u+x) - v(u-x)) x (v(u+y) - v(u-y))) facing the
+ *   camera; sample skipped when a 4-neighbour is off-image / invalid (R24) / beyond the guard or the
+ *   cross product vanishes (R31);  V^g = R v + t, N^g = R n (float64);
+ *   s_1 = max(min_scale, sqrt(max(0, 1/3 sum_i (|V^g - p_i| - (a_i + b_i)/2)))) over the 3 nearest
+ *   non-removed Gaussians of rows [0, n) by (distance, gid), a_i, b_i the two largest exp(log_scale)
+ *   (Eq.11, R26, R30); fewer than 3 candidates: s_1 = 2 D(u) / f_x; transparent: min(s_1, max);
+ *   log_scale = log(s_1, s_1, 0.1 s_1); rotation taking e_z (the shortest axis) to N^g; SH DC
+ *   (c - 0.5) / C0, higher bands 0 (R32); flags = transparent ? 1 : 0 (unstable); eta = e = 0, t = k.
+ * New rows are appended at n, n+1, ... in sample order (rows past `capacity` are dropped).
+ * result [5] device out: #opaque added, #transparent added, #skipped (invalid normal), #dropped
+ * (capacity), n after.  The caller reads result[4] to learn the new n (map->n is not changed).
+ * workspace: rtgs_insert_workspace_size(map->n, sample_cap). */
+size_t rtgs_insert_workspace_size(int32_t n, uint32_t sample_cap);
+rtgs_status rtgs_add_gaussians(const rtgs_map* map, const uint32_t* samples, uint32_t sample_cap,
+                               const uint32_t* add_counts, const rtgs_frame* frame, const rtgs_pose* pose,
+                               const rtgs_camera* cam, const rtgs_insert_params* ip, uint32_t* result,
+                               void* workspace, size_t workspace_bytes, void* stream);
+
 /* Utilities */
 const char* rtgs_status_string(rtgs_status s);
 const char* rtgs_last_cuda_error(void);

@@ -68,6 +68,17 @@ class StateParams(C.Structure):
                 ("delta_t", C.c_uint32), ("frame_idx", C.c_uint32)]
 
 
+class MapRW(C.Structure):
+    _fields_ = [("pos", vp), ("log_scale", vp), ("rot", vp), ("opacity", vp), ("sh", vp), ("flags", vp), ("eta", vp),
+                ("err_count", vp), ("t_created", vp), ("n", C.c_int32), ("capacity", C.c_int32),
+                ("sh_degree", C.c_int32)]
+
+
+class InsertParams(C.Structure):
+    _fields_ = [("normal_guard", C.c_float), ("min_scale", C.c_float), ("max_scale_transparent", C.c_float),
+                ("cell", C.c_float), ("frame_idx", C.c_uint32)]
+
+
 P = C.POINTER
 EXPORTS = {
     "rtgs_project_gaussians": (C.c_int, [P(Gaussians), P(Pose), P(Camera), P(Projected), vp]),
@@ -92,6 +103,9 @@ EXPORTS = {
     "rtgs_bin_cached_workspace_size": (C.c_size_t, [C.c_int32, P(Camera), C.c_uint32]),
     "rtgs_bin_and_sort_cached": (C.c_int, [P(Projected), P(Bins), P(Projected), vp, C.c_int32, P(Camera), vp, P(Bins),
                                            vp, C.c_size_t, vp]),
+    "rtgs_insert_workspace_size": (C.c_size_t, [C.c_int32, C.c_uint32]),
+    "rtgs_add_gaussians": (C.c_int, [P(MapRW), vp, C.c_uint32, vp, P(Frame), P(Pose), P(Camera), P(InsertParams), vp,
+                                     vp, C.c_size_t, vp]),
     "rtgs_status_string": (C.c_char_p, [C.c_int]),
     "rtgs_last_cuda_error": (C.c_char_p, []),
     "rtgs_version": (C.c_int32, []),

@@ -208,6 +208,28 @@ rtgs_status rtgs_bin_and_sort_cached(const rtgs_projected* proj, const rtgs_bins
   return finish(launch_bin_cached(*proj, *cache, *sub, sub_gid, n_sub, *cam, tile_keep, *out, workspace, S(stream)));
 }
 
+size_t rtgs_insert_workspace_size(int32_t n, uint32_t sample_cap) {
+  return n < 0 ? 0 : insert_workspace_size(n, sample_cap);
+}
+
+rtgs_status rtgs_add_gaussians(const rtgs_map* map, const uint32_t* samples, uint32_t sample_cap,
+                               const uint32_t* add_counts, const rtgs_frame* frame, const rtgs_pose* pose,
+                               const rtgs_camera* cam, const rtgs_insert_params* ip, uint32_t* result,
+                               void* workspace, size_t workspace_bytes, void* stream) {
+  if (!map || map->n < 0 || map->capacity < map->n || map->sh_degree < 0 || map->sh_degree > 3 || !pose_ok(pose) ||
+      !cam_ok(cam) || !ip || !result || !add_counts || !frame || !frame->color || !frame->depth)
+    return RTGS_ERR_INVALID_ARG;
+  if (map->capacity > 0 && (!map->pos || !map->log_scale || !map->rot || !map->opacity || !map->sh || !map->flags ||
+                            !map->eta || !map->err_count || !map->t_created))
+    return RTGS_ERR_INVALID_ARG;
+  if (sample_cap > 0 && !samples) return RTGS_ERR_INVALID_ARG;
+  if (!(ip->normal_guard >= 0.f) || !(ip->min_scale > 0.f) || !(ip->max_scale_transparent > 0.f))
+    return RTGS_ERR_INVALID_ARG;
+  if (!workspace || workspace_bytes < insert_workspace_size(map->n, sample_cap)) return RTGS_ERR_WORKSPACE;
+  return finish(launch_insert(*map, samples, sample_cap, add_counts, *frame, make_pose(*pose), *cam, *ip, result,
+                              workspace, S(stream)));
+}
+
 const char* rtgs_status_string(rtgs_status s) {
   switch (s) {
     case RTGS_OK: return "RTGS_OK";

@@ -61,6 +61,11 @@ cudaError_t launch_manage_states(const rtgs_render_out& full, const rtgs_frame& 
                                  uint8_t* flags, uint32_t* err, uint32_t* eta, uint32_t* tc, int n,
                                  const rtgs_state_params& sp, uint32_t* counts, void* ws, cudaStream_t s);
 
+size_t insert_workspace_size(int n, uint32_t sample_cap);
+cudaError_t launch_insert(const rtgs_map& m, const uint32_t* samples, uint32_t cap, const uint32_t* add_counts,
+                          const rtgs_frame& frame, const PoseF& pose, const rtgs_camera& cam,
+                          const rtgs_insert_params& ip, uint32_t* result, void* ws, cudaStream_t s);
+
 // generic device-wide exclusive scan of uint32 (length known on the host; zeros past the live part)
 size_t scan_workspace_size(size_t len);
 cudaError_t launch_scan(const uint32_t* in, uint32_t* out, size_t len, uint32_t* total, void* ws, cudaStream_t s);

@@ -53,9 +53,13 @@ def make_pose(R, t) -> _abi.Pose:
     return _abi.Pose((C.c_double * 9)(*R), (C.c_double * 3)(*t))
 
 
+_MAP_FIELDS = ("pos", "log_scale", "rot", "opacity", "sh", "flags")
+
+
 @dataclasses.dataclass
 class GaussianMap:
-    """Device SoA of the Gaussian map, float32."""
+    """Device SoA of the Gaussian map, float32.  The fields are views of the first n
+    rows of `store` (capacity rows), so Gaussians can be appended (NEXT f2) without reallocation."""
     pos: torch.Tensor
     log_scale: torch.Tensor
     rot: torch.Tensor
@@ -63,15 +67,34 @@ class GaussianMap:
     sh: torch.Tensor
     flags: torch.Tensor  # uint8
     sh_degree: int
+    store: dict | None = None
 
     @property
     def n(self) -> int:
         return int(self.pos.shape[0])
 
+    @property
+    def capacity(self) -> int:
+        return int(self.store["pos"].shape[0]) if self.store is not None else self.n
+
     @classmethod
-    def from_arrays(cls, scene: dict, device="cuda") -> "GaussianMap":
-        f = lambda k: torch.as_tensor(np.ascontiguousarray(scene[k]), device=device).contiguous()
-        return cls(f("pos"), f("log_scale"), f("rot"), f("opacity"), f("sh"), f("flags"), int(scene["sh_degree"]))
+    def from_arrays(cls, scene: dict, device="cuda", capacity: int | None = None) -> "GaussianMap":
+        n = int(np.asarray(scene["pos"]).shape[0])
+        cap = max(int(capacity) if capacity is not None else n, n, 1)
+        store = {}
+        for k in _MAP_FIELDS:
+            a = np.ascontiguousarray(scene[k])
+            t = torch.zeros((cap,) + a.shape[1:], dtype=torch.as_tensor(a[:0]).dtype, device=device)
+            t[:n].copy_(torch.as_tensor(a))
+            store[k] = t
+        return cls(*[store[k][:n] for k in _MAP_FIELDS], int(scene["sh_degree"]), store)
+
+    def resize(self, n: int):
+        """Make rows [0, n) live (n <= capacity): re-slices the views, no copy."""
+        if self.store is None or n > self.capacity:
+            raise ValueError(f"resize to {n} beyond capacity {self.capacity}")
+        for k in _MAP_FIELDS:
+            setattr(self, k, self.store[k][:n])
 
     def c_struct(self) -> _abi.Gaussians:
         return _abi.Gaussians(_p(self.pos), _p(self.log_scale), _p(self.rot), _p(self.opacity), _p(self.sh),
@@ -299,6 +322,34 @@ def bin_and_sort_cached(proj: ProjectedBuffers, cache: BinBuffers, sub: Projecte
     out.sub = (sub.rec, sub.zkey, sub_gid)
 
 
+# ---------------------------------------------------------------------------------------------
+# NEXT f2: Gaussian insertion
+# ---------------------------------------------------------------------------------------------
+def insert_params(frame_idx: int, normal_guard=0.1, min_scale=1e-4, max_scale_transparent=0.01,
+                  cell=0.02) -> _abi.InsertParams:
+    return _abi.InsertParams(normal_guard, min_scale, max_scale_transparent, cell, frame_idx)
+
+
+def insert_workspace_size(n: int, sample_cap: int) -> int:
+    return int(lib().rtgs_insert_workspace_size(n, sample_cap))
+
+
+def add_gaussians(gm: GaussianMap, eta: torch.Tensor, err_count: torch.Tensor, t_created: torch.Tensor,
+                  samples: torch.Tensor, add_counts: torch.Tensor, frame_color: torch.Tensor,
+                  frame_depth: torch.Tensor, pose: _abi.Pose, cam: _abi.Camera, ip: _abi.InsertParams,
+                  result: torch.Tensor, workspace: torch.Tensor, stream=None):
+    """Append the Gaussians of the A7 samples after row gm.n (storage rows of gm / eta / err_count /
+    t_created must reach gm.capacity).  result[4] (device) = the new n; gm is not resized here."""
+    m = _abi.MapRW(_p(gm.store["pos"]), _p(gm.store["log_scale"]), _p(gm.store["rot"]), _p(gm.store["opacity"]),
+                   _p(gm.store["sh"]), _p(gm.store["flags"]), _p(eta), _p(err_count), _p(t_created), gm.n, gm.capacity,
+                   gm.sh_degree)
+    fr = _abi.Frame(_p(frame_color), _p(frame_depth))
+    check(lib().rtgs_add_gaussians(C.byref(m), _p(samples), int(samples.numel()), _p(add_counts), C.byref(fr),
+                                   C.byref(pose), C.byref(cam), C.byref(ip), _p(result), _p(workspace),
+                                   workspace.numel() * workspace.element_size(), _stream(stream)),
+          "rtgs_add_gaussians")
+
+
 def hparams(preset: str = "replica") -> _abi.HParams:
     """Learning rates of P:501: Replica / ScanNet++ vs Azure / TUM."""
     if preset in ("replica", "scannetpp"):
@@ -319,7 +370,7 @@ class MappingEngine:
     def __init__(self, gm: GaussianMap, cam: _abi.Camera, capacity: int | None = None, preset="replica",
                  weights=(1.0, 1.0, 1000.0), sample_cap: int | None = None, device="cuda"):
         self.gm, self.cam, self.device = gm, cam, device
-        n = gm.n
+        n = gm.capacity  # per-Gaussian buffers are sized for the map's storage (f2 appends rows)
         self.capacity = int(capacity if capacity is not None else max(4 * n, 1 << 16))
         # the masked iteration and the frame ingest own separate buffers so they can run concurrently
         self.proj = ProjectedBuffers(n, device)
@@ -340,11 +391,15 @@ class MappingEngine:
         self.samples = torch.zeros(sample_cap if sample_cap is not None else max(HW // 8, 1), dtype=torch.int32,
                                    device=device)
         self.add_counts = torch.zeros(5, dtype=torch.int32, device=device)
-        self.eta = torch.zeros(n, dtype=torch.int32, device=device)
-        self.err_count = torch.zeros(n, dtype=torch.int32, device=device)   # e_i
-        self.t_created = torch.zeros(n, dtype=torch.int32, device=device)   # t_i
+        # per-Gaussian state (storage of capacity rows; the attributes are views of the live rows)
+        self._state_store = {k: torch.zeros(n, dtype=torch.int32, device=device)
+                             for k in ("eta", "err_count", "t_created")}
+        self._view_state()
         self.state_counts = torch.zeros(4, dtype=torch.int32, device=device)
         self.ws_state = torch.empty(state_workspace_size(n), dtype=torch.uint8, device=device)
+        # NEXT f2: insertion workspace and result (#opaque, #transparent, #skipped, #dropped, n after)
+        self.ws_insert = torch.empty(insert_workspace_size(n, self.samples.numel()), dtype=torch.uint8, device=device)
+        self.insert_result = torch.zeros(5, dtype=torch.int32, device=device)
         # NEXT f3: the stable part of the last ingested frame's sorted lists (valid for its pose and
         # until the stable set changes at the window end)
         self.cache = BinBuffers(cam, self.capacity, device)
@@ -352,6 +407,27 @@ class MappingEngine:
         self.cache_pose = None
         self.use_cache = True
         self.reset_window()
+
+    def _view_state(self):
+        n = self.gm.n
+        self.eta = self._state_store["eta"][:n]            # eta_i
+        self.err_count = self._state_store["err_count"][:n]  # e_i
+        self.t_created = self._state_store["t_created"][:n]  # t_i
+
+    def insert(self, frame_color, frame_depth, pose: _abi.Pose, frame_idx: int, stream=None, sync=True):
+        """NEXT f2 after an ingest of the same frame: append the Gaussians of its A7 samples
+        (Eq.11).  With sync=True the new count is read back and the map / state views
+        grow; call reset_window() before optimising so the new (unstable) Gaussians get slots."""
+        add_gaussians(self.gm, self._state_store["eta"], self._state_store["err_count"],
+                      self._state_store["t_created"], self.samples, self.add_counts, frame_color, frame_depth, pose,
+                      self.cam, insert_params(frame_idx), self.insert_result, self.ws_insert, stream)
+        if sync:
+            (torch.cuda.current_stream() if stream is None else stream).synchronize()
+            n_new = int(self.insert_result[4].item())
+            self.gm.resize(n_new)
+            self._view_state()
+        # (the f3 cache stays valid: new Gaussians are unstable, the stable lists are unchanged)
+        return self.insert_result
 
     def reset_window(self):
         """(Re)build the unstable slot set from flags and reset the Adam state (R19: per window)."""
@@ -380,12 +456,11 @@ class MappingEngine:
             torch.zeros((1, D), device=self.device)
         self.eta_before = self.eta[gid_t].clone() if n_slots else torch.zeros(1, dtype=torch.int32, device=self.device)
         self.step_dev = torch.zeros(1, dtype=torch.int32, device=self.device)  # graph-replayable step
-        # f3: the slots' own projection rows and the cached-binning workspace; the stable set may
-        # have changed, so any cache is invalid until the next ingest
+        # f3: the slots' own projection rows and the cached-binning workspace (the cache itself is
+        # invalidated where the stable set changes: end_window)
         self.proj_sub = ProjectedBuffers(n_slots, self.device)
         self.ws_bin_cached = torch.empty(bin_cached_workspace_size(n_slots, self.cam, self.capacity), dtype=torch.uint8,
                                          device=self.device)
-        self.cache_pose = None
         self.proj_iter = self.proj
 
     # --- the two flows ---------------------------------------------------------------------------
@@ -459,6 +534,7 @@ class MappingEngine:
         sp = state if state is not None else state_params(frame_idx)
         manage_states(self.full, frame_color, frame_depth, self.cam, self.gm.flags, self.err_count, self.eta,
                       self.t_created, sp, self.state_counts, self.ws_state, stream)
+        self.cache_pose = None  # the stable set changed: the f3 cache is stale
         self.reset_window()
 
     def step(self, frame_color, frame_depth, pose: _abi.Pose, ingest_pose=None, seed=0, frame_idx=0,

@@ -181,7 +181,7 @@ def test_cache_invalidated_by_pose_and_window(api):
     assert eng.cached(pose)
     R, t = make_pose(cfg, view=1)
     assert not eng.cached(api.make_pose(R, t))
-    eng.reset_window()
+    eng.end_window(col, dep, pose, frame_idx=1)
     assert not eng.cached(pose)
 
 
