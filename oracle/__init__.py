@@ -17,4 +17,4 @@ Pins: see tests/test_oracle_*.py.  Functions without a pin say "parity unpinned"
 docstring; at present none does except the whole-iteration timing trend (Table
 `stable_gaussian_ablation`), which is a performance statement, not a value.
 """
-from . import sh, projection, binning, raster, loss, optim, classify, state, insert  # noqa: F401
+from . import sh, projection, binning, raster, loss, optim, classify, state, insert, icp  # noqa: F401
