@@ -385,6 +385,19 @@ def main():
         torch.cuda.synchronize()
         phases["frame.add_gaussians_ms"] = e0.elapsed_time(e1)
         insert_result = eng.insert_result.cpu().numpy().tolist()
+        # NEXT f4 (once per frame, not part of the step): model render at the previous pose + ICP
+        icp_pose = P.pose_device(R, t)
+        eng.track(dep, pose, init_pose=icp_pose)   # warm (allocates the ICP workspace)
+        icp_pose.copy_(P.pose_device(R, t))
+        torch.cuda.synchronize()
+        hold(0.5)
+        e0.record(stream)
+        eng.track(dep, pose, init_pose=icp_pose)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        phases["frame.track_ms"] = e0.elapsed_time(e1)
+        icp_rows = eng.icp_diag.cpu().numpy().reshape(-1, 4)
+        icp_rows = icp_rows[icp_rows[:, 0] >= 0]
         restore()
         blends_full = int(eng.full.counts[3].item())
         blends_masked = int(eng.out.counts[3].item())
@@ -497,6 +510,8 @@ def main():
             "phases_ms": {k: round(v, 4) for k, v in phases.items()},
             "iter_ms": round(sum(v for k, v in phases.items() if k.startswith("iter.")), 4),
             "ingest_ms": round(sum(v for k, v in phases.items() if k.startswith("ingest.")), 4),
+            "f4_track": {"ms": round(phases["frame.track_ms"], 4), "in_step": False,
+                         "gn_iterations": int(len(icp_rows)), "pairs_last": int(icp_rows[-1][2]) if len(icp_rows) else 0},
             "f2_insert": {"result": dict(zip(["opaque", "transparent", "skipped", "dropped", "n_after"], insert_result)),
                           "ms": round(phases["frame.add_gaussians_ms"], 4), "in_step": False},
             "active": {"kept_tiles": counts[0], "active_px": counts[1], "instances_full": n_inst,

@@ -366,6 +366,41 @@ rtgs_status rtgs_add_gaussians(const rtgs_map* map, const uint32_t* samples, uin
                                const rtgs_camera* cam, const rtgs_insert_params* ip, uint32_t* result,
                                void* workspace, size_t workspace_bytes, void* stream);
 
+/* =============================================================================================
+ * NEXT row f4: frame-to-model point-to-plane ICP tracking (Eq.10, P:278-282;
+ * readings R31, R33-R35).  A second workload on the renderer: the model maps are a FULL render of
+ * the optimised map at the previous pose (rtgs_render_out depth, normal).
+ * ============================================================================================= */
+typedef struct {
+  int32_t levels;        /* pyramid levels 1..4 (3)                                                  */
+  int32_t iters[4];      /* Gauss-Newton iterations per level, [0] = full resolution: {4, 5, 10}     */
+  float normal_guard;    /* 0.1 m (R31)                                                             */
+  double dist_gate;      /* 0.1 m: |T v - m| gate                                                   */
+  double cos_gate;       /* cos 30 deg: n_cur . n_model gate (world frame)                          */
+  double eps;            /* 1e-6: a level stops when |delta| < eps                                  */
+  int32_t min_pairs;     /* 6: a level stops with fewer pairs                                       */
+} rtgs_icp_params;
+
+/* rtgs_icp_track: pyramid of the current depth D_k (R33: per 2x2 block the valid depth closest to
+ * the block mean; f/2, (c - 0.5)/2 per level), float64 vertex / normal maps per level (R31), then
+ * coarse -> fine Gauss-Newton on E(xi) = sum ((T v - m) . n_m)^2: every valid current pixel is
+ * transformed by the running estimate T (pose_io), projected with the level-0 intrinsics into the
+ * model maps at model_pose (u^ = floor(x + 0.5)), paired when D^(u^) > 0, |T v - m| <= dist_gate and
+ * (R n) . n_m >= cos_gate, m = model_pose (D^ K^-1 (u^, 1)), n_m = N^(u^) (R34); delta =
+ * -(J^T J + lambda I)^-1 J^T r with lambda = 1e-6 max diag(J^T J), J = (n_m, p x n_m),
+ * T <- Exp(delta) T (R35).
+ *   depth        [H][W] current frame D_k (metres; <= 0 / non-finite invalid)
+ *   model_depth  [H][W] D^* (-1 = no hit), model_normal [3][H][W] world N^* (rtgs_render_out of a
+ *                FULL render at model_pose)
+ *   pose_io      device double[12]: camera->world R (row-major) then t; in: initial estimate, out: T_k
+ *   diag         device double[4 * sum(iters)]: per iteration (level, E, #pairs, |delta|), level -1
+ *                for iterations skipped after convergence
+ * workspace: rtgs_icp_workspace_size(cam, levels).  No host synchronisation (graph-capturable). */
+size_t rtgs_icp_workspace_size(const rtgs_camera* cam, int32_t levels);
+rtgs_status rtgs_icp_track(const float* depth, const float* model_depth, const float* model_normal,
+                           const rtgs_pose* model_pose, const rtgs_camera* cam, const rtgs_icp_params* params,
+                           double* pose_io, double* diag, void* workspace, size_t workspace_bytes, void* stream);
+
 /* Utilities */
 const char* rtgs_status_string(rtgs_status s);
 const char* rtgs_last_cuda_error(void);

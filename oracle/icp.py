@@ -14,7 +14,8 @@ vertex p = T v is projected with the level-0 intrinsics into the full-resolution
 model pose, u^ = round-half-up of the projection; pairs need a valid model depth (D^* > 0),
 ||p - m|| <= 0.1 m and n_cur . n_model >= cos 30 deg (both world frame); residual r = (p - m) . n_m,
 Jacobian of the left increment T <- Exp(xi) T, xi = (rho, phi): J = (n_m, p x n_m).  R35 solver:
-plain Gauss-Newton, delta = -(J^T J)^-1 J^T r on each level (iterations 10, 5, 4 coarse -> fine),
+Gauss-Newton with a relative damping, delta = -(J^T J + lambda I)^-1 J^T r, lambda = 1e-6 max diag(J^T J)
+(a single visible plane makes J^T J singular; the damping leaves its null space unmoved), on each level (iterations 10, 5, 4 coarse -> fine),
 a level stops when |delta| < 1e-6 or fewer than 6 pairs; T <- Exp(delta) T with the closed-form
 SE(3) exponential.
 
@@ -25,6 +26,7 @@ import math
 import numpy as np
 
 COS30 = math.cos(math.radians(30.0))
+DAMPING = 1e-6  # R35: relative Tikhonov damping, keeps unobservable directions (one plane) at 0
 
 
 def level_camera(cam, l):
@@ -136,16 +138,22 @@ def linearize(V, N, valid, R, t, model, cam0, Rm, tm, dist_gate=0.1, cos_gate=CO
     idx = np.nonzero(valid.ravel())[0]
     v = V.reshape(-1, 3)[idx]
     n = N.reshape(-1, 3)[idx]
-    p = v @ R.T + t
+    # The association decides integers (u^ = floor(x + 0.5); coarse-level pixel centres project
+    # exactly onto x.5 at the model pose), so p, q and x are formed with this exact sequence of
+    # correctly rounded float64 operations (elementwise, no BLAS / FMA), as the kernel does.
+    R = np.asarray(R, np.float64)
+    Rm = np.asarray(Rm, np.float64)
+    p = np.stack([((R[r, 0] * v[:, 0] + R[r, 1] * v[:, 1]) + R[r, 2] * v[:, 2]) + t[r] for r in range(3)], 1)
     nw = n @ R.T
-    q = (p - np.asarray(tm)) @ np.asarray(Rm)  # model camera frame: R_m^T (p - t_m), as row vectors
+    dd = p - np.asarray(tm, np.float64)
+    q = np.stack([(Rm[0, c] * dd[:, 0] + Rm[1, c] * dd[:, 1]) + Rm[2, c] * dd[:, 2] for c in range(3)], 1)
     A = np.zeros((6, 6))
     b = np.zeros(6)
     E = 0.0
     cnt = 0
     with np.errstate(invalid="ignore", divide="ignore"):
-        ux = cam0["fx"] * q[:, 0] / q[:, 2] + cam0["cx"]
-        uy = cam0["fy"] * q[:, 1] / q[:, 2] + cam0["cy"]
+        ux = (cam0["fx"] * q[:, 0]) / q[:, 2] + cam0["cx"]
+        uy = (cam0["fy"] * q[:, 1]) / q[:, 2] + cam0["cy"]
     front = q[:, 2] > 0
     ix = np.floor(np.where(front, ux, -1.0) + 0.5)
     iy = np.floor(np.where(front, uy, -1.0) + 0.5)
@@ -182,7 +190,8 @@ def icp(depth_cur, cam, model, Rm, tm, R0, t0, levels=3, iters=(4, 5, 10), guard
             if cnt < min_pairs:
                 diag.append((l, E, cnt, 0.0))
                 break
-            delta = -np.linalg.solve(A, b)
+            lam = DAMPING * float(np.max(np.diag(A)))
+            delta = -np.linalg.solve(A + lam * np.eye(6), b)
             dR, dt = se3_exp(delta)
             R, t = dR @ R, dR @ t + dt
             nd = float(np.linalg.norm(delta))

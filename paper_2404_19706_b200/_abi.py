@@ -79,6 +79,11 @@ class InsertParams(C.Structure):
                 ("cell", C.c_float), ("frame_idx", C.c_uint32)]
 
 
+class IcpParams(C.Structure):
+    _fields_ = [("levels", C.c_int32), ("iters", C.c_int32 * 4), ("normal_guard", C.c_float), ("dist_gate", C.c_double),
+                ("cos_gate", C.c_double), ("eps", C.c_double), ("min_pairs", C.c_int32)]
+
+
 P = C.POINTER
 EXPORTS = {
     "rtgs_project_gaussians": (C.c_int, [P(Gaussians), P(Pose), P(Camera), P(Projected), vp]),
@@ -106,6 +111,8 @@ EXPORTS = {
     "rtgs_insert_workspace_size": (C.c_size_t, [C.c_int32, C.c_uint32]),
     "rtgs_add_gaussians": (C.c_int, [P(MapRW), vp, C.c_uint32, vp, P(Frame), P(Pose), P(Camera), P(InsertParams), vp,
                                      vp, C.c_size_t, vp]),
+    "rtgs_icp_workspace_size": (C.c_size_t, [P(Camera), C.c_int32]),
+    "rtgs_icp_track": (C.c_int, [vp, vp, vp, P(Pose), P(Camera), P(IcpParams), vp, vp, vp, C.c_size_t, vp]),
     "rtgs_status_string": (C.c_char_p, [C.c_int]),
     "rtgs_last_cuda_error": (C.c_char_p, []),
     "rtgs_version": (C.c_int32, []),

@@ -230,6 +230,26 @@ rtgs_status rtgs_add_gaussians(const rtgs_map* map, const uint32_t* samples, uin
                               workspace, S(stream)));
 }
 
+size_t rtgs_icp_workspace_size(const rtgs_camera* cam, int32_t levels) {
+  if (!cam_ok(cam) || levels < 1 || levels > 4) return 0;
+  return icp_workspace_size(*cam, levels);
+}
+
+rtgs_status rtgs_icp_track(const float* depth, const float* model_depth, const float* model_normal,
+                           const rtgs_pose* model_pose, const rtgs_camera* cam, const rtgs_icp_params* params,
+                           double* pose_io, double* diag, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!depth || !model_depth || !model_normal || !pose_ok(model_pose) || !cam_ok(cam) || !params || !pose_io || !diag)
+    return RTGS_ERR_INVALID_ARG;
+  if (params->levels < 1 || params->levels > 4 || params->min_pairs < 6 || !(params->eps >= 0.0) ||
+      !(params->dist_gate > 0.0) || !(params->cos_gate <= 1.0) || !(params->normal_guard >= 0.f))
+    return RTGS_ERR_INVALID_ARG;
+  for (int l = 0; l < params->levels; ++l)
+    if (params->iters[l] < 0 || params->iters[l] > 1000) return RTGS_ERR_INVALID_ARG;
+  if (!workspace || workspace_bytes < icp_workspace_size(*cam, params->levels)) return RTGS_ERR_WORKSPACE;
+  return finish(launch_icp(depth, model_depth, model_normal, *model_pose, *cam, *params, pose_io, diag, workspace,
+                           S(stream)));
+}
+
 const char* rtgs_status_string(rtgs_status s) {
   switch (s) {
     case RTGS_OK: return "RTGS_OK";

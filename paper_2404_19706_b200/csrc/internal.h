@@ -66,6 +66,11 @@ cudaError_t launch_insert(const rtgs_map& m, const uint32_t* samples, uint32_t c
                           const rtgs_frame& frame, const PoseF& pose, const rtgs_camera& cam,
                           const rtgs_insert_params& ip, uint32_t* result, void* ws, cudaStream_t s);
 
+size_t icp_workspace_size(const rtgs_camera& cam, int levels);
+cudaError_t launch_icp(const float* depth, const float* mdepth, const float* mnormal, const rtgs_pose& model_pose,
+                       const rtgs_camera& cam, const rtgs_icp_params& p, double* pose_io, double* diag, void* ws,
+                       cudaStream_t s);
+
 // generic device-wide exclusive scan of uint32 (length known on the host; zeros past the live part)
 size_t scan_workspace_size(size_t len);
 cudaError_t launch_scan(const uint32_t* in, uint32_t* out, size_t len, uint32_t* total, void* ws, cudaStream_t s);

@@ -350,6 +350,36 @@ def add_gaussians(gm: GaussianMap, eta: torch.Tensor, err_count: torch.Tensor, t
           "rtgs_add_gaussians")
 
 
+# ---------------------------------------------------------------------------------------------
+# NEXT f4: frame-to-model ICP tracking
+# ---------------------------------------------------------------------------------------------
+def icp_params(levels=3, iters=(4, 5, 10), normal_guard=0.1, dist_gate=0.1, angle_gate_deg=30.0, eps=1e-6,
+               min_pairs=6) -> _abi.IcpParams:
+    it = list(iters) + [0] * (4 - len(iters))
+    return _abi.IcpParams(levels, (C.c_int32 * 4)(*it), normal_guard, dist_gate,
+                          float(np.cos(np.radians(angle_gate_deg))), eps, min_pairs)
+
+
+def icp_workspace_size(cam: _abi.Camera, levels: int = 3) -> int:
+    return int(lib().rtgs_icp_workspace_size(C.byref(cam), levels))
+
+
+def pose_device(R, t, device="cuda") -> torch.Tensor:
+    """Device double[12] pose buffer (camera->world R row-major, then t) for icp_track."""
+    return torch.as_tensor(np.concatenate([np.asarray(R, np.float64).reshape(9), np.asarray(t, np.float64)]),
+                           device=device).contiguous()
+
+
+def icp_track(depth: torch.Tensor, model: RenderBuffers, model_pose: _abi.Pose, cam: _abi.Camera,
+              params: _abi.IcpParams, pose_io: torch.Tensor, diag: torch.Tensor, workspace: torch.Tensor,
+              stream=None):
+    """T_k by multi-level point-to-plane ICP of the current depth against a FULL render `model` of the
+    map at model_pose (pose_io: device double[12], in = initial estimate, out = result)."""
+    check(lib().rtgs_icp_track(_p(depth), _p(model.depth), _p(model.normal), C.byref(model_pose), C.byref(cam),
+                               C.byref(params), _p(pose_io), _p(diag), _p(workspace),
+                               workspace.numel() * workspace.element_size(), _stream(stream)), "rtgs_icp_track")
+
+
 def hparams(preset: str = "replica") -> _abi.HParams:
     """Learning rates of P:501: Replica / ScanNet++ vs Azure / TUM."""
     if preset in ("replica", "scannetpp"):
@@ -428,6 +458,27 @@ class MappingEngine:
             self._view_state()
         # (the f3 cache stays valid: new Gaussians are unstable, the stable lists are unchanged)
         return self.insert_result
+
+    def track(self, frame_depth, model_pose: _abi.Pose, init_pose: torch.Tensor | None = None, params=None,
+              stream=None):
+        """NEXT f4: render the optimised map at the previous pose (A1, A2, A3/A4 FULL; depth and world
+        normals) and track the current frame against it by ICP.  Returns the device pose buffer
+        (double[12]) and the per-iteration diagnostics (device)."""
+        params = params or icp_params()
+        if not hasattr(self, "ws_icp"):
+            self.ws_icp = torch.empty(icp_workspace_size(self.cam, 4), dtype=torch.uint8, device=self.device)
+            self.icp_diag = torch.zeros((4 * 40,), dtype=torch.float64, device=self.device)
+        project_gaussians(self.gm, model_pose, self.cam, self.proj_full, stream)
+        bin_and_sort(self.proj_full, self.gm.n, self.cam, None, self.bins_full, self.ws_bin_full, stream)
+        render_color_depth(self.gm, self.proj_full, self.bins_full, model_pose, self.cam, RTGS_RENDER_FULL, self.full,
+                           stream)
+        self.cache_pose = None  # proj_full / bins_full now hold the model pose's frame
+        pose_io = init_pose if init_pose is not None else pose_device(np.asarray(model_pose.R).reshape(3, 3),
+                                                                      np.asarray(model_pose.t), self.device)
+        with torch.cuda.stream(torch.cuda.current_stream() if stream is None else stream):
+            self.icp_diag.fill_(-1.0)  # rows past sum(iters) stay marked unused
+        icp_track(frame_depth, self.full, model_pose, self.cam, params, pose_io, self.icp_diag, self.ws_icp, stream)
+        return pose_io, self.icp_diag
 
     def reset_window(self):
         """(Re)build the unstable slot set from flags and reset the Adam state (R19: per window)."""
