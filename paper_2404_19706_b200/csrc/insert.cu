@@ -6,11 +6,11 @@
 //  2. k_insert_prepare: one thread per sample: vertex and central-difference normal of the pixel
 //     (float64, the 0.1 m guard decided in float32), validity flag for the compaction.
 //  3. scan of the validity flags: new gid = n + rank (sample order, deterministic).
-//  4. k_insert_write: one thread per valid sample: exact 3-NN by (distance, gid) — expanding cube
-//     shells per grid level, stopping when the third distance is <= r h (no unexamined point can
-//     be closer), a brute-force pass only if even the coarsest level cannot certify — then Eq.11's
-//     scale, the disc rotation (shortest axis = normal), SH DC, state; appended with coalesced-
-//     enough row writes (a few thousand samples per frame at most).
+//  4. k_insert_write: one WARP per valid sample: exact 3-NN by (distance, gid) — expanding cube
+//     shells per grid level (lanes split the shell's cells), stopping when the third distance is
+//     <= r h (no unexamined point can be closer), a brute-force pass (lanes split the Gaussians)
+//     only if even the coarsest level cannot certify — then Eq.11's scale, the disc rotation
+//     (shortest axis = normal), SH DC, state, appended at n + rank.
 #include <algorithm>
 #include <cmath>
 
@@ -36,30 +36,41 @@ struct GridLevel {
   uint32_t* sorted;     // [n]
 };
 
+// bucket of Gaussian i at one level (0xFFFFFFFF: not a candidate)
+__device__ __forceinline__ uint32_t grid_bucket(const float* pos, const uint8_t* flags, int n, int i,
+                                                const GridLevel& L) {
+  if (i >= n || (flags[i] & 4u)) return 0xFFFFFFFFu;
+  const int ix = (int)floor((double)pos[3 * i] * L.inv_h), iy = (int)floor((double)pos[3 * i + 1] * L.inv_h),
+            iz = (int)floor((double)pos[3 * i + 2] * L.inv_h);
+  return cell_hash(ix, iy, iz) & L.mask;
+}
+
+// Counting sort by bucket with warp-aggregated atomics: lanes of a warp that share a bucket (common
+// at the coarse levels, where a cell holds thousands of Gaussians) issue one atomic for the group.
 __global__ void __launch_bounds__(256) k_grid_count(const float* __restrict__ pos, const uint8_t* __restrict__ flags,
                                                     int n, GridLevel L, uint32_t* __restrict__ n_cand) {
   const int i = blockIdx.x * 256 + threadIdx.x;
-  bool c = false;
-  if (i < n && !(flags[i] & 4u)) {
-    c = true;
-    const int ix = (int)floor((double)pos[3 * i] * L.inv_h), iy = (int)floor((double)pos[3 * i + 1] * L.inv_h),
-              iz = (int)floor((double)pos[3 * i + 2] * L.inv_h);
-    atomicAdd(&L.cnt[cell_hash(ix, iy, iz) & L.mask], 1u);
-  }
+  const int lane = threadIdx.x & 31;
+  const uint32_t b = grid_bucket(pos, flags, n, i, L);
+  const uint32_t peers = __match_any_sync(0xffffffffu, b);
+  if (b != 0xFFFFFFFFu && (__ffs(peers) - 1) == lane) atomicAdd(&L.cnt[b], (uint32_t)__popc(peers));
   if (n_cand) {
-    const uint32_t s = __reduce_add_sync(0xffffffffu, c ? 1u : 0u);
-    if ((threadIdx.x & 31) == 0 && s) atomicAdd(n_cand, s);
+    const uint32_t s = __popc(__ballot_sync(0xffffffffu, b != 0xFFFFFFFFu));
+    if (lane == 0 && s) atomicAdd(n_cand, s);
   }
 }
 
 __global__ void __launch_bounds__(256) k_grid_scatter(const float* __restrict__ pos, const uint8_t* __restrict__ flags,
                                                       int n, GridLevel L) {
   const int i = blockIdx.x * 256 + threadIdx.x;
-  if (i >= n || (flags[i] & 4u)) return;
-  const int ix = (int)floor((double)pos[3 * i] * L.inv_h), iy = (int)floor((double)pos[3 * i + 1] * L.inv_h),
-            iz = (int)floor((double)pos[3 * i + 2] * L.inv_h);
-  const uint32_t b = cell_hash(ix, iy, iz) & L.mask;
-  L.sorted[L.start[b] + atomicAdd(&L.cursor[b], 1u)] = (uint32_t)i;
+  const int lane = threadIdx.x & 31;
+  const uint32_t b = grid_bucket(pos, flags, n, i, L);
+  const uint32_t peers = __match_any_sync(0xffffffffu, b);
+  const int leader = __ffs(peers) - 1;
+  uint32_t base = 0;
+  if (b != 0xFFFFFFFFu && leader == lane) base = L.start[b] + atomicAdd(&L.cursor[b], (uint32_t)__popc(peers));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  if (b != 0xFFFFFFFFu) L.sorted[base + __popc(peers & ((1u << lane) - 1u))] = (uint32_t)i;
 }
 
 struct InsArgs {
@@ -171,16 +182,44 @@ struct Top3 {
   }
 };
 
+// Warp-wide merge of the lanes' top-3 lists (each sorted): the 3 smallest (d, gid) of the union;
+// every lane returns the same list (duplicates of a gid seen by several lanes count once).
+__device__ Top3 warp_top3(const Top3& mine) {
+  Top3 out;
+  out.init();
+  int head = 0;
+  for (int k = 0; k < 3; ++k) {
+    double dv = head < mine.n ? mine.d[head] : INFINITY;
+    uint32_t gv = head < mine.n ? mine.g[head] : 0xFFFFFFFFu;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double od = __shfl_xor_sync(0xffffffffu, dv, o);
+      const uint32_t og = __shfl_xor_sync(0xffffffffu, gv, o);
+      if (Top3::less(od, og, dv, gv)) { dv = od; gv = og; }
+    }
+    if (gv == 0xFFFFFFFFu) break;
+    out.d[k] = dv;
+    out.g[k] = gv;
+    out.n = k + 1;
+    if (head < mine.n && mine.g[head] == gv) ++head;
+  }
+  return out;
+}
+
+// One WARP per sample: the lanes split the cells of each cube shell (and, in the brute-force
+// fallback, the Gaussians), so the dependent bucket -> position loads of many cells are in flight
+// together; the lanes' top-3 lists are merged after every shell for the certification test.
 __global__ void __launch_bounds__(128) k_insert_write(const InsArgs a) {
-  const uint32_t i = blockIdx.x * 128 + threadIdx.x;
-  if (i >= a.cap || !a.valid[i]) return;
+  const uint32_t i = (blockIdx.x * 128 + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= a.cap || !a.valid[i]) return;  // warp-uniform
   const uint32_t rk = a.rank[i];
   const uint32_t s = a.samples[i];
   const uint32_t pix = s & 0x3FFFFFFFu;
   const bool transparent = (s >> 30) == 2u;
   const size_t g = (size_t)a.n + rk;
   if (g >= (size_t)a.capacity) {
-    atomicAdd(&a.result[3], 1u);
+    if (lane == 0) atomicAdd(&a.result[3], 1u);
     return;
   }
   const double vx = a.vg[3 * i], vy = a.vg[3 * i + 1], vz = a.vg[3 * i + 2];
@@ -192,36 +231,33 @@ __global__ void __launch_bounds__(128) k_insert_write(const InsArgs a) {
   } else {
     Top3 top;
     top.init();
-    auto visit_bucket = [&](const GridLevel& L, uint32_t b) {
-      const uint32_t j0 = L.start[b], j1 = j0 + L.cnt[b];
-      for (uint32_t j = j0; j < j1; ++j) {
-        const uint32_t q = L.sorted[j];
-        const double dx = vx - (double)a.pos[3 * q], dy = vy - (double)a.pos[3 * q + 1], dz = vz - (double)a.pos[3 * q + 2];
-        top.offer(dx * dx + dy * dy + dz * dz, q);
-      }
+    auto offer_point = [&](uint32_t q) {
+      const double dx = vx - (double)a.pos[3 * q], dy = vy - (double)a.pos[3 * q + 1], dz = vz - (double)a.pos[3 * q + 2];
+      top.offer(dx * dx + dy * dy + dz * dz, q);
     };
     bool certified = false;
     for (int l = 0; l < kGridLevels && !certified; ++l) {
       const GridLevel& L = a.lev[l];
       const int cx = (int)floor(vx * L.inv_h), cy = (int)floor(vy * L.inv_h), cz = (int)floor(vz * L.inv_h);
       for (int r = 0; r <= kGridR && !certified; ++r) {
-        for (int dz = -r; dz <= r; ++dz)
-          for (int dy = -r; dy <= r; ++dy)
-            for (int dx = -r; dx <= r; ++dx) {
-              if (max(abs(dx), max(abs(dy), abs(dz))) != r) continue;  // shell only
-              visit_bucket(L, cell_hash(cx + dx, cy + dy, cz + dz) & L.mask);
-            }
+        const int side = 2 * r + 1, ncube = side * side * side;
+        for (int c = lane; c < ncube; c += 32) {
+          const int dx = c % side - r, dy = (c / side) % side - r, dz = c / (side * side) - r;
+          if (max(abs(dx), max(abs(dy), abs(dz))) != r) continue;  // shell only
+          const uint32_t b = cell_hash(cx + dx, cy + dy, cz + dz) & L.mask;
+          const uint32_t j0 = L.start[b], j1 = j0 + L.cnt[b];
+          for (uint32_t j = j0; j < j1; ++j) offer_point(L.sorted[j]);
+        }
+        top = warp_top3(top);
         // every unexamined Gaussian lies in a cell >= r+1 away: farther than r h
         const double rh = (double)r * L.h;
         certified = top.n == 3 && top.d[2] <= rh * rh;
       }
     }
     if (!certified) {  // beyond the coarsest grid's reach: exact brute force (rare)
-      for (int q = 0; q < a.n; ++q) {
-        if (a.flags[q] & 4u) continue;
-        const double dx = vx - (double)a.pos[3 * q], dy = vy - (double)a.pos[3 * q + 1], dz = vz - (double)a.pos[3 * q + 2];
-        top.offer(dx * dx + dy * dy + dz * dz, (uint32_t)q);
-      }
+      for (int q = lane; q < a.n; q += 32)
+        if (!(a.flags[q] & 4u)) offer_point((uint32_t)q);
+      top = warp_top3(top);
     }
     double m = 0.0;
     for (int k = 0; k < 3; ++k) {
@@ -241,6 +277,10 @@ __global__ void __launch_bounds__(128) k_insert_write(const InsArgs a) {
   double qw = 1.0 + nz, qx = -ny, qy = nx, qz = 0.0;
   double qn = sqrt(qw * qw + qx * qx + qy * qy);
   if (!(qn > 1e-12)) { qw = 0.0; qx = 1.0; qy = 0.0; qn = 1.0; }  // n = -e_z: 180 deg about x
+  const size_t HW = (size_t)a.W * a.H;
+  float* shr = a.sh + (size_t)3 * a.K * g;
+  for (int j = 3 + lane; j < 3 * a.K; j += 32) shr[j] = 0.f;
+  if (lane != 0) return;
   a.pos[3 * g] = (float)vx;
   a.pos[3 * g + 1] = (float)vy;
   a.pos[3 * g + 2] = (float)vz;
@@ -253,10 +293,7 @@ __global__ void __launch_bounds__(128) k_insert_write(const InsArgs a) {
   a.rot[4 * g + 2] = (float)(qy / qn);
   a.rot[4 * g + 3] = (float)(qz / qn);
   a.opacity[g] = transparent ? 0.1f : 0.99f;
-  const size_t HW = (size_t)a.W * a.H;
-  float* shr = a.sh + (size_t)3 * a.K * g;
   for (int c = 0; c < 3; ++c) shr[c] = (float)(((double)a.color[c * HW + pix] - 0.5) / kC0);  // R32
-  for (int j = 3; j < 3 * a.K; ++j) shr[j] = 0.f;
   a.flags[g] = transparent ? 1u : 0u;  // unstable (bit1 clear), not removed
   a.eta[g] = 0u;
   a.err[g] = 0u;
@@ -369,7 +406,7 @@ cudaError_t launch_insert(const rtgs_map& m, const uint32_t* samples, uint32_t c
     k_insert_prepare<<<(cap + 255) / 256, 256, 0, s>>>(a);
     cudaError_t e = launch_scan(w.valid, w.rank, cap, w.n_valid, w.scan_ws, s);
     if (e != cudaSuccess) return e;
-    k_insert_write<<<(cap + 127) / 128, 128, 0, s>>>(a);
+    k_insert_write<<<(cap + 3) / 4, 128, 0, s>>>(a);  // one warp per sample
     note_launch(2);
   } else {
     cudaMemsetAsync(w.n_valid, 0, 4, s);
