@@ -170,6 +170,7 @@ def main():
     ap.add_argument("--phases", action="store_true", help="print per-call timings to stderr")
     ap.add_argument("--no-graph", action="store_true", help="launch every step eagerly (no CUDA graph)")
     ap.add_argument("--no-cache", action="store_true", help="iteration without the f3 stable-projection cache")
+    ap.add_argument("--no-restore", action="store_true", help="diagnostic: let the map drift between timed steps")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -225,7 +226,8 @@ def main():
         eng.step_dev.zero_()
 
     def between_steps():
-        restore()
+        if not args.no_restore:
+            restore()
         flush.zero_()
 
     def step(c, d, frame_idx):

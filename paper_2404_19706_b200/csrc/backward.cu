@@ -1,7 +1,8 @@
 // backward.cu — A5: masked L1 loss and its gradient for the unstable Gaussians
 // (O5; Eq.7-8, readings R13, R14, R17).
 //
-// K5 k_render_bwd: one CTA per kept tile (same geometry and batching as the forward).  Each active
+// K5 k_render_bwd: one CTA per half of a kept tile (4 consumer warps + 1 producer; same geometry and
+//   batching as the MASKED forward).  Each active
 //   pixel REPLAYS the forward front to back with the identical arithmetic (eval_pair), so T_i and
 //   every decision are bit-identical to the forward; the colour suffix S_i = C^ - prefix_i comes from
 //   the stored C^.  For every UNSTABLE record a warp touches, the 8 screen-space gradients
@@ -68,24 +69,27 @@ struct BwdArgs {
   float* acc;
 };
 
+constexpr int kBwdWarps = kHalfWarps;  // one CTA per half of a kept tile
+
 struct BwdSmem {
   PipeRing ring;
   int32_t slot[kPipeStages][kPipeBatch];
-  float red[3][kConsumerWarps];
+  float red[3][kBwdWarps];
   uint32_t last_max;
 };
 
-__global__ void __launch_bounds__(kPipeThreads) k_render_bwd(const BwdArgs a) {
+__global__ void __launch_bounds__(32 * (kBwdWarps + 1)) k_render_bwd(const BwdArgs a) {
   __shared__ BwdSmem sm;  // static: stage addresses fold into immediates
   PipeRing& r = sm.ring;
-  if (blockIdx.x >= a.counts[0]) return;
-  const int tile = (int)a.tile_list[blockIdx.x];
+  if ((blockIdx.x >> 1) >= a.counts[0]) return;
+  const int tile = (int)a.tile_list[blockIdx.x >> 1];
+  const int half = blockIdx.x & 1;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  pipe_init(r);
+  pipe_init<kBwdWarps>(r);
   if (tid == 0) sm.last_max = 0;
-  const bool consumer = w < kConsumerWarps;
+  const bool consumer = w < kBwdWarps;
   const int tx = tile % a.cam.TX, ty = tile / a.cam.TX;
-  const int wx0 = tx * kTile + (w & 1) * 8, wy0 = ty * kTile + (w >> 1) * 4;
+  const int wx0 = tx * kTile + (w & 1) * 8, wy0 = ty * kTile + (half * (kBwdWarps / 2) + (w >> 1)) * 4;
   const int px = wx0 + (lane & 7), py = wy0 + (lane >> 3);
   const bool inside = consumer && px < a.cam.W && py < a.cam.H;
   const uint32_t lin = (uint32_t)py * (uint32_t)a.cam.W + (uint32_t)px;
@@ -144,7 +148,7 @@ __global__ void __launch_bounds__(kPipeThreads) k_render_bwd(const BwdArgs a) {
   __syncthreads();
   if (tid < 3) {
     float t = 0.f;
-    for (int k = 0; k < kConsumerWarps; ++k) t += sm.red[tid][k];
+    for (int k = 0; k < kBwdWarps; ++k) t += sm.red[tid][k];
     atomicAdd(a.acc + tid, t);
   }
   const uint2 rg = a.range[tile];
@@ -635,7 +639,7 @@ cudaError_t launch_backward(const rtgs_gaussians& g, const rtgs_projected& proj,
   a.sgrad = sgrad;
   a.acc = acc;
   const int T = a.cam.TX * a.cam.TY;
-  k_render_bwd<<<T, kPipeThreads, 0, s>>>(a);
+  k_render_bwd<<<2 * T, 32 * (kBwdWarps + 1), 0, s>>>(a);
   note_launch();
   PBArgs b;
   b.rec = reinterpret_cast<const float4*>(proj.rec);

@@ -2,8 +2,8 @@
 //             A3/A4 forward colour/transmission blending with the opaque-disc depth (O2/O3;
 //             Eq.1-5, R7-R12).
 //
-// Forward: one CTA per (kept) 16x16 tile = 8 consumer warps (warp w owns an 8x4 pixel block, one
-// pixel per lane) + 1 producer warp streaming the tile's depth-sorted records through a 4-stage
+// Forward: one CTA per 16x16 tile (FULL) or per half of a kept tile (MASKED) = 8 / 4 consumer warps
+// (warp w owns an 8x4 pixel block, one pixel per lane) + 1 producer warp streaming the tile's depth-sorted records through a 4-stage
 // shared-memory ring (tilepipe.cuh).  Each consumer warp culls a batch 32 records at a time against
 // its 8x4 block (ballot over the records' support boxes) and only walks the survivors.  Pixels stop
 // at T (1 - f) < 1e-4; warps stop when all their lanes stopped; the producer stops when all did.
@@ -45,15 +45,22 @@ __global__ void __launch_bounds__(256) k_coverage(const float4* __restrict__ rec
     a.z = __shfl_sync(0xffffffffu, mya.z, src); a.w = __shfl_sync(0xffffffffu, mya.w, src);
     b.x = __shfl_sync(0xffffffffu, myb.x, src); b.y = __shfl_sync(0xffffffffu, myb.y, src);
     b.z = __shfl_sync(0xffffffffu, myb.z, src); b.w = __shfl_sync(0xffffffffu, myb.w, src);
-    const int w = x1 - x0 + 1;
-    const int tot = w * (y1 - y0 + 1);
-    for (int p = lane; p < tot; p += 32) {
-      const int py = y0 + p / w, px = x0 + p % w;
+    const int w = x1 - x0 + 1, h = y1 - y0 + 1;
+    auto splat = [&](int px, int py) {
       PairEval e;
       if (eval_pair(a, b, (float)px, (float)py, e)) {
         const uint32_t lin = (uint32_t)py * (uint32_t)W + (uint32_t)px;
         atomicOr(&bits[lin >> 5], 1u << (lin & 31u));
       }
+    };
+    if (w <= 32) {  // the warp covers rpi = 32 / w rows per step; one division per Gaussian, not per pixel
+      const int rpi = 32 / w;
+      const int ry = lane / w, rx = lane - ry * w;
+      if (ry < rpi)
+        for (int py = y0 + ry; py <= y1; py += rpi) splat(x0 + rx, py);
+    } else {
+      const int tot = w * h;
+      for (int p = lane; p < tot; p += 32) splat(x0 + p % w, y0 + p / w);
     }
   }
 }
@@ -108,26 +115,28 @@ struct FwdArgs {
 };
 
 template <bool MASKED>
-__global__ void __launch_bounds__(kPipeThreads) k_render_fwd(const FwdArgs a) {
+__global__ void __launch_bounds__(32 * ((MASKED ? kHalfWarps : kTileWarps) + 1)) k_render_fwd(const FwdArgs a) {
+  constexpr int NW = MASKED ? kHalfWarps : kTileWarps;  // MASKED: one CTA per half of a kept tile
   __shared__ PipeRing r;  // static: stage addresses fold into immediates
-  int tile;
+  int tile, half = 0;
   if (MASKED) {
-    if (blockIdx.x >= a.counts[0]) return;
-    tile = (int)a.tile_list[blockIdx.x];
+    if ((blockIdx.x >> 1) >= a.counts[0]) return;
+    tile = (int)a.tile_list[blockIdx.x >> 1];
+    half = blockIdx.x & 1;
   } else {
     tile = blockIdx.x;
   }
-  pipe_init(r);
+  pipe_init<NW>(r);
   __syncthreads();
   const uint2 rg = a.range[tile];
   const int start = (int)rg.x, end = (int)rg.y;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (w == kProducerWarp) {
+  if (w == NW) {  // producer warp
     pipe_produce(r, a.rec, a.sub_rec, a.sorted_gid, start, end, [](int, int, uint32_t) {}, [](int, int) {});
     return;
   }
   const int tx = tile % a.cam.TX, ty = tile / a.cam.TX;
-  const int wx0 = tx * kTile + (w & 1) * 8, wy0 = ty * kTile + (w >> 1) * 4;
+  const int wx0 = tx * kTile + (w & 1) * 8, wy0 = ty * kTile + (half * (NW / 2) + (w >> 1)) * 4;
   const int px = wx0 + (lane & 7), py = wy0 + (lane >> 3);
   const bool inside = px < a.cam.W && py < a.cam.H;
   const uint32_t lin = (uint32_t)py * (uint32_t)a.cam.W + (uint32_t)px;
@@ -139,8 +148,9 @@ __global__ void __launch_bounds__(kPipeThreads) k_render_fwd(const FwdArgs a) {
   const int n = end - start;
   const int nb = n > 0 ? (n + kPipeBatch - 1) / kPipeBatch : 0;
 
+  const uint32_t rec0 = pin(smem_u32(&r.rec[0][0][0]));
   float T = 1.f, cr = 0.f, cg = 0.f, cb = 0.f;
-  uint32_t hit = 0xFFFFFFFFu;  // list entry of the depth hit (never a valid entry)
+  int hitpos = -1;  // sorted-list position of the depth hit (the entry is fetched after the loop)
   uint32_t last = (uint32_t)start;
   uint32_t nblend = 0;  // blended (pixel, Gaussian) pairs of this lane (-> counts[3])
   bool wdone = __all_sync(0xffffffffu, done);
@@ -149,8 +159,7 @@ __global__ void __launch_bounds__(kPipeThreads) k_render_fwd(const FwdArgs a) {
     const int st = b % kPipeStages;
     mbar_wait(&r.full[st], (uint32_t)(b / kPipeStages) & 1u);
     if (!wdone) {
-      const uint32_t srec = smem_u32(&r.rec[st][0][0]);  // shared addresses, computed once per batch
-      const uint32_t sgid = smem_u32(&r.gid[st][0]);
+      const uint32_t srec = rec0 + (uint32_t)(st * sizeof(r.rec[0]));  // shared address of this stage
       const uint32_t pbase = (uint32_t)(start + b * kPipeBatch + 1);
       const int cnt = min(kPipeBatch, n - b * kPipeBatch);
       for (int g0 = 0; g0 < cnt; g0 += 32) {
@@ -170,7 +179,8 @@ __global__ void __launch_bounds__(kPipeThreads) k_render_fwd(const FwdArgs a) {
           const float4 r0 = lds128(ra), r1 = lds128(ra + 16u), r2 = lds128(ra + 32u);
           PairEval e;
           bool ok = eval_pair(r0, r1, fpx, fpy, e) && !done;
-          if (ok && hit == 0xFFFFFFFFu && e.f > kDeltaAlpha) hit = lds32(sgid + 4u * idx);  // R9: before termination
+          // R9: the first f > e^-0.5, tested before termination (position only: no load in the loop)
+          hitpos = (ok && hitpos < 0 && e.f > kDeltaAlpha) ? (int)(pbase - 1u) + idx : hitpos;
           const float test = __fmul_rn(T, __fsub_rn(1.f, e.f));
           const bool term = ok && (test < kTMin);
           done = done || term;
@@ -207,6 +217,7 @@ __global__ void __launch_bounds__(kPipeThreads) k_render_fwd(const FwdArgs a) {
   a.n_contrib[lin] = last;
   float D = -1.f, N0 = 0.f, N1 = 0.f, N2 = 0.f;
   int32_t gid = -1;
+  const uint32_t hit = hitpos >= 0 ? a.sorted_gid[hitpos] : 0xFFFFFFFFu;  // list entry of the hit
   if (hit != 0xFFFFFFFFu) {
     const bool sub = hit & kSubBit;
     const uint32_t row = hit & ~kSubBit;
@@ -269,8 +280,8 @@ cudaError_t launch_render(const rtgs_projected& proj, const rtgs_bins& bins, con
   a.index = out.index; a.n_contrib = out.n_contrib;
   const int T = a.cam.TX * a.cam.TY;
   if (out.counts) cudaMemsetAsync(out.counts + 3, 0, 4, s);  // blend counter of this render
-  if (masked) k_render_fwd<true><<<T, kPipeThreads, 0, s>>>(a);
-  else k_render_fwd<false><<<T, kPipeThreads, 0, s>>>(a);
+  if (masked) k_render_fwd<true><<<2 * T, 32 * (kHalfWarps + 1), 0, s>>>(a);
+  else k_render_fwd<false><<<T, 32 * (kTileWarps + 1), 0, s>>>(a);
   note_launch();
   return cudaGetLastError();
 }

@@ -1,7 +1,7 @@
 // tilepipe.cuh — warp-specialised producer/consumer pipeline over one tile's depth-sorted list,
 // shared by the forward render (A3/A4) and the backward replay (A5).
 //
-// CTA = 8 consumer warps (one 8x4 pixel block each, one pixel per lane) + 1 producer warp.
+// CTA = NW consumer warps (one 8x4 pixel block each, one pixel per lane) + 1 producer warp.
 // The producer streams the tile's records in batches of kPipeBatch through a kPipeStages-deep ring
 // in shared memory with cp.async (LDGSTS) and signals each stage on a `full` mbarrier
 // (cp.async.mbarrier.arrive.noinc: the arrival fires when the lane's copies have landed).  Every
@@ -16,9 +16,11 @@ namespace rtgs {
 
 constexpr int kPipeStages = 4;
 constexpr int kPipeBatch = 128;
-constexpr int kConsumerWarps = 8;
-constexpr int kPipeThreads = 32 * (kConsumerWarps + 1);
-constexpr int kProducerWarp = kConsumerWarps;
+// consumer warps per CTA: 8 = a whole 16x16 tile (FULL render: thousands of tiles), 4 = half a tile
+// (MASKED render and backward: only the kept tiles, so half-tile CTAs double the parallelism and
+// even out the per-SM load)
+constexpr int kTileWarps = 8;
+constexpr int kHalfWarps = 4;
 
 struct PipeRing {
   float4 rec[kPipeStages][kPipeBatch][3];  // first 48 B of each record: mu hi/lo, conic', log2 alpha, rgb, ext
@@ -28,13 +30,14 @@ struct PipeRing {
   int alive;                                // consumer warps not yet terminated
 };
 
+template <int NW>
 __device__ __forceinline__ void pipe_init(PipeRing& r) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < kPipeStages; ++s) {
       mbar_init(&r.full[s], 32);
-      mbar_init(&r.empty[s], kConsumerWarps);
+      mbar_init(&r.empty[s], NW);
     }
-    r.alive = kConsumerWarps;
+    r.alive = NW;
     fence_mbar_init();
   }
 }
