@@ -30,7 +30,7 @@ constexpr int kScanItems = 8;
 constexpr int kScanChunk = kScanThreads * kScanItems;  // 2048
 constexpr int kSortThreads = 256;
 constexpr int kSortWarps = kSortThreads / 32;
-constexpr int kSortCap = 2048;  // tile lists up to this length are sorted in shared memory
+constexpr int kSortCap = 1024;  // tile lists up to this length are sorted in shared memory
 constexpr int kRep = 8;         // replicated tile counters: spreads same-address atomics 8 ways
 
 static inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
@@ -357,7 +357,7 @@ __device__ __forceinline__ void sort_tile(const unsigned long long* __restrict__
   for (int i = tid; i < n; i += kSortThreads) out_gid[i] = (uint32_t)(res[i] & gmask);
 }
 
-__global__ void __launch_bounds__(kSortThreads) k_tile_sort(const uint2* __restrict__ range,
+__global__ void __launch_bounds__(kSortThreads, 6) k_tile_sort(const uint2* __restrict__ range,
                                                             unsigned long long* __restrict__ keys,
                                                             unsigned long long* __restrict__ tmp,
                                                             uint32_t* __restrict__ grank, int gid_bits,
