@@ -414,13 +414,18 @@ def main():
     # ---- e2e: host frames in pinned memory -> device, step, loss + add counts back to the host ------
     # Streamed like a live system: the H2D copy of frame i+1 (copy stream, double-buffered staging)
     # overlaps the step of frame i; each step's copy and its D2H read-back are inside the timed span.
+    # The frames arrive sensor-native (8-bit interleaved RGB, 16-bit depth at 5000 units / m, as TUM /
+    # Replica store them) and are decoded on the device (rtgs_decode_rgbd) into the graph's inputs.
     n_e2e = max(10, args.steps // 2)
-    col_pin = torch.as_tensor(col_h).pin_memory()
-    dep_pin = torch.as_tensor(dep_h).pin_memory()
+    DEPTH_SCALE = 5000.0
+    rgb_h = np.clip(np.rint(np.moveaxis(col_h, 0, -1) * 255.0), 0, 255).astype(np.uint8)
+    raw_h = np.clip(np.rint(dep_h * DEPTH_SCALE), 0, 65535).astype(np.uint16)
+    col_pin = torch.as_tensor(rgb_h).pin_memory()
+    dep_pin = torch.as_tensor(raw_h.view(np.int16)).pin_memory()
     loss_h = torch.empty((n_e2e, 4), dtype=torch.float32).pin_memory()
     cnt_h = torch.empty((n_e2e, 5), dtype=torch.int32).pin_memory()
-    st_col = [torch.empty_like(col) for _ in range(2)]
-    st_dep = [torch.empty_like(dep) for _ in range(2)]
+    st_col = [torch.empty_like(col_pin, device="cuda") for _ in range(2)]
+    st_dep = [torch.empty_like(dep_pin, device="cuda") for _ in range(2)]
     copy_stream = torch.cuda.Stream()
     ev_copied = [torch.cuda.Event() for _ in range(2)]
     ev_free = [torch.cuda.Event() for _ in range(2)]
@@ -444,8 +449,7 @@ def main():
         if i + 1 < n_e2e:
             h2d(i + 1)
         stream.wait_event(ev_copied[i % 2])
-        col.copy_(st_col[i % 2])   # the graph reads the frame from these device buffers
-        dep.copy_(st_dep[i % 2])
+        P.decode_rgbd(st_col[i % 2], st_dep[i % 2], DEPTH_SCALE, col, dep)  # into the graph's input buffers
         ev_free[i % 2].record(stream)
         run_step(i)
         loss_h[i].copy_(eng.loss, non_blocking=True)
@@ -508,7 +512,8 @@ def main():
             "clocks": clocks,
             "gpu_launches": int(launches),
             "e2e": {"value": world * 1e3 / t_e2e, "unit": "iters/s",
-                    "h2d_bytes_per_step": int(col_h.nbytes + dep_h.nbytes), "d2h_bytes_per_step": 4 * 4 + 5 * 4},
+                    "h2d_bytes_per_step": int(rgb_h.nbytes + raw_h.nbytes), "d2h_bytes_per_step": 4 * 4 + 5 * 4,
+                    "input": "uint8 RGB + uint16 depth (5000 / m), decoded on the device"},
             "phases_ms": {k: round(v, 4) for k, v in phases.items()},
             "iter_ms": round(sum(v for k, v in phases.items() if k.startswith("iter.")), 4),
             "ingest_ms": round(sum(v for k, v in phases.items() if k.startswith("ingest.")), 4),

@@ -401,6 +401,16 @@ rtgs_status rtgs_icp_track(const float* depth, const float* model_depth, const f
                            const rtgs_pose* model_pose, const rtgs_camera* cam, const rtgs_icp_params* params,
                            double* pose_io, double* diag, void* workspace, size_t workspace_bytes, void* stream);
 
+/* =============================================================================================
+ * Input decode (P:232 input pre-processing): sensor-native RGB-D to the planar float32 frame.
+ * rgb [H][W][3] uint8 interleaved -> color [3][H][W] = rgb * (1/255) (float32 product);
+ * depth_raw [H][W] uint16 -> depth [H][W] = raw * (1/depth_scale) metres (TUM: 5000, Replica:
+ * 6553.5 raw units per metre); raw 0 -> 0 (invalid, R24).  rgb 4-byte aligned, depth_raw 8-byte
+ * aligned, outputs 16-byte aligned.
+ * ============================================================================================= */
+rtgs_status rtgs_decode_rgbd(const uint8_t* rgb, const uint16_t* depth_raw, int32_t width, int32_t height,
+                             float depth_scale, float* color, float* depth, void* stream);
+
 /* Utilities */
 const char* rtgs_status_string(rtgs_status s);
 const char* rtgs_last_cuda_error(void);

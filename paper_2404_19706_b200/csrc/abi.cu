@@ -250,6 +250,18 @@ rtgs_status rtgs_icp_track(const float* depth, const float* model_depth, const f
                            S(stream)));
 }
 
+rtgs_status rtgs_decode_rgbd(const uint8_t* rgb, const uint16_t* depth_raw, int32_t width, int32_t height,
+                             float depth_scale, float* color, float* depth, void* stream) {
+  if (width < 0 || height < 0 || width > 16384 || height > 16384 || !(depth_scale > 0.f) ||
+      !std::isfinite(depth_scale))
+    return RTGS_ERR_INVALID_ARG;
+  if ((size_t)width * height > 0 &&
+      (!rgb || !depth_raw || !color || !depth || !a4(rgb) || (reinterpret_cast<uintptr_t>(depth_raw) & 7u) != 0 ||
+       !a16(color) || !a16(depth)))
+    return RTGS_ERR_INVALID_ARG;
+  return finish(launch_decode(rgb, depth_raw, width, height, depth_scale, color, depth, S(stream)));
+}
+
 const char* rtgs_status_string(rtgs_status s) {
   switch (s) {
     case RTGS_OK: return "RTGS_OK";

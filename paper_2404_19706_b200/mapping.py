@@ -380,6 +380,15 @@ def icp_track(depth: torch.Tensor, model: RenderBuffers, model_pose: _abi.Pose, 
                                workspace.numel() * workspace.element_size(), _stream(stream)), "rtgs_icp_track")
 
 
+def decode_rgbd(rgb: torch.Tensor, depth_raw: torch.Tensor, depth_scale: float, color: torch.Tensor,
+                depth: torch.Tensor, stream=None):
+    """Sensor-native frame (uint8 [H,W,3] RGB, uint16 [H,W] depth in raw units) -> planar float32
+    color [3,H,W] and depth [H,W] metres, on the device."""
+    H, W = int(depth_raw.shape[0]), int(depth_raw.shape[1])
+    check(lib().rtgs_decode_rgbd(_p(rgb), _p(depth_raw), W, H, float(depth_scale), _p(color), _p(depth),
+                                 _stream(stream)), "rtgs_decode_rgbd")
+
+
 def hparams(preset: str = "replica") -> _abi.HParams:
     """Learning rates of P:501: Replica / ScanNet++ vs Azure / TUM."""
     if preset in ("replica", "scannetpp"):
