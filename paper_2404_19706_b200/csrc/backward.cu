@@ -18,6 +18,7 @@
 namespace rtgs {
 
 constexpr int kSG = 16;  // screen-space gradient floats per slot
+constexpr int kDirectLanes = 4;  // <= this many contributing lanes: per-lane vector atomics
 
 // Transpose-reduce of 8 values over a warp in 9 shuffles (instead of 8 x 5): after the call, lane l
 // holds the warp sum of value j = 4*bit4(l) + 2*bit3(l) + bit2(l), identical on the 4 lanes l^{0..3}.
@@ -214,7 +215,8 @@ __global__ void __launch_bounds__(32 * (kBwdWarps + 1)) k_render_bwd(const BwdAr
           ar = __fmaf_rn(r2.x, wgt, ar);
           ag = __fmaf_rn(r2.y, wgt, ag);
           ab = __fmaf_rn(r2.z, wgt, ab);
-          if (slot >= 0 && __any_sync(0xffffffffu, ok)) {
+          const uint32_t okm = __ballot_sync(0xffffffffu, ok);
+          if (slot >= 0 && okm) {
             float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
             if (ok) {
               // S_i = sum_{j>i} c_j f_j T_j = C^ - prefix_i ;  dC/df_i = c_i T_i - S_i / (1 - f_i)
@@ -234,9 +236,19 @@ __global__ void __launch_bounds__(32 * (kBwdWarps + 1)) k_render_bwd(const BwdAr
               v[6] = gCg * wgt;
               v[7] = gCb * wgt;
             }
-            int vj;
-            const float x = warp_reduce8(v, plane, vj);
-            if ((plane & 3) == 0) atomicAdd(a.sgrad + (size_t)slot * kSG + vj, x);  // 8 lanes, 8 values
+            float* sg = a.sgrad + (size_t)slot * kSG;
+            if (__popc(okm) <= kDirectLanes) {
+              // few contributing lanes (the common case for sub-pixel splats): each adds its own 8
+              // values with two vector reductions instead of the 9-shuffle transpose-reduce
+              if (ok) {
+                atomicAdd(reinterpret_cast<float4*>(sg), make_float4(v[0], v[1], v[2], v[3]));
+                atomicAdd(reinterpret_cast<float4*>(sg + 4), make_float4(v[4], v[5], v[6], v[7]));
+              }
+            } else {
+              int vj;
+              const float x = warp_reduce8(v, plane, vj);
+              if ((plane & 3) == 0) atomicAdd(sg + vj, x);  // 8 lanes, 8 values
+            }
           }
           T = ok ? test : T;
         }
