@@ -54,6 +54,7 @@ __global__ void __launch_bounds__(kAdamThreads) k_adam(const AdamArgs a) {
     const size_t gid = (size_t)a.gid_of_slot[slot];
     const bool transparent = a.flags[gid] & 1u;
     const size_t row = (size_t)slot * D;
+    const float th0v = (t < 10 && a.init_geom) ? a.init_geom[(size_t)slot * 10 + t] : 0.f;  // independent of gid
     float* shrow = a.sh + (size_t)(3 * K) * gid - 10;
     constexpr int NIT = (D + kLanesPerSlot - 1) / kLanesPerSlot;
     // all loads of the row are issued before any store (stores could alias later loads otherwise)
@@ -71,7 +72,7 @@ __global__ void __launch_bounds__(kAdamThreads) k_adam(const AdamArgs a) {
       vo[it] = a.v[row + j];
       th[it] = *p[it];
     }
-    const float th0 = (t < 10 && transparent) ? a.init_geom[(size_t)slot * 10 + t] : 0.f;
+    const float th0 = transparent ? th0v : 0.f;
 #pragma unroll
     for (int it = 0; it < NIT; ++it) {
       const int j = t + it * kLanesPerSlot;
