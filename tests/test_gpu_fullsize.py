@@ -184,3 +184,39 @@ def test_colour_gradients_sampled_slots(c3):
         if checked == 6:
             break
     assert checked >= 4
+
+
+def test_cached_iteration_equals_uncached_c3(c3):
+    """The bench's f3 path (stable cache of the ingest + re-projected unstable slots) gives the same
+    bins, masked render and gradients as the uncached iteration at full size."""
+    eng, P = c3["eng"], c3["P"]
+    pose = P.make_pose(c3["R"], c3["t"])
+    tc, td = torch.as_tensor(c3["col"], device="cuda"), torch.as_tensor(c3["dep"], device="cuda")
+
+    def run(cached):
+        eng.grad.zero_()
+        eng.use_cache = cached
+        eng.forward_masked(pose)
+        assert eng.cached(pose) == cached
+        eng.backward(tc, td, pose)
+        torch.cuda.synchronize()
+        I = int(eng.bins.n_instances.item())
+        e = u32(eng.bins.sorted_gid)[:I].astype(np.int64)
+        sub = (e & 0x80000000) != 0
+        e[sub] = eng.gid_of_slot.cpu().numpy()[e[sub] & 0x7FFFFFFF]
+        act = eng.out.active_set().cpu().numpy()
+        return dict(bins=e, act=act, color=eng.out.color.cpu().numpy(), depth=eng.out.depth.cpu().numpy(),
+                    index=eng.out.index.cpu().numpy(), grad=eng.grad.cpu().numpy().copy(),
+                    loss=eng.loss.cpu().numpy().copy())
+
+    a = run(True)
+    b = run(False)
+    eng.use_cache = True
+    np.testing.assert_array_equal(a["bins"], b["bins"])
+    np.testing.assert_array_equal(a["act"], b["act"])
+    act = a["act"]
+    assert np.array_equal(a["color"][:, act], b["color"][:, act])
+    assert np.array_equal(a["depth"][act], b["depth"][act]) and np.array_equal(a["index"][act], b["index"][act])
+    scale = np.abs(b["grad"]).max(0, keepdims=True) + 1e-30
+    assert (np.abs(a["grad"] - b["grad"]) <= 1e-5 * scale).all()
+    np.testing.assert_allclose(a["loss"], b["loss"], rtol=1e-6)
