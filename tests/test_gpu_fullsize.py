@@ -220,3 +220,55 @@ def test_cached_iteration_equals_uncached_c3(c3):
     scale = np.abs(b["grad"]).max(0, keepdims=True) + 1e-30
     assert (np.abs(a["grad"] - b["grad"]) <= 1e-5 * scale).all()
     np.testing.assert_allclose(a["loss"], b["loss"], rtol=1e-6)
+
+
+def test_c4_render_only_sampled():
+    """BASELINE.json configs[3] (ScanNet++-shaped 1752x1168, 4M Gaussians, render-only): the FULL
+    render at sampled pixels vs the oracle (candidates = Gaussians whose support rect holds the
+    pixel), and the instance count vs the oracle's tile rects."""
+    from paper_2404_19706_b200 import build as B
+    B.build()
+    import paper_2404_19706_b200 as P
+    cfg = CONFIGS["C4"]
+    scene = make_scene(cfg)
+    R, t = make_pose(cfg)
+    gm = P.GaussianMap.from_arrays(scene)
+    cam = P.camera_of(cfg)
+    pose = P.make_pose(R, t)
+    from paper_2404_19706_b200 import mapping as M
+    proj = P.ProjectedBuffers(gm.n)
+    cap = 4 * cfg.n
+    bins = P.BinBuffers(cam, cap)
+    ws = torch.empty(M.bin_workspace_size(gm.n, cam, cap), dtype=torch.uint8, device="cuda")
+    rb = P.RenderBuffers(cam)
+    P.project_gaussians(gm, pose, cam, proj)
+    P.bin_and_sort(proj, gm.n, cam, None, bins, ws)
+    P.render_color_depth(gm, proj, bins, pose, cam, P.RTGS_RENDER_FULL, rb)
+    torch.cuda.synchronize()
+    prm = OP.params_from_scene(scene)
+    with torch.no_grad():
+        pr = OP.project(prm, R, t, OP.camera(cfg), scene["sh_degree"])
+    grect = proj.rect.cpu().numpy().astype(np.int64)
+    mism = (grect != pr["rect"]).any(1) & pr["valid"]
+    assert mism.sum() <= 1e-3 * cfg.n
+    I = int(bins.n_instances.item())
+    assert abs(I - int(pr["tiles_touched"][pr["valid"]].sum())) <= 4 * mism.sum() + 4
+    rng = np.random.default_rng(5)
+    pix = np.stack([rng.integers(0, cfg.width, 32), rng.integers(0, cfg.height, 32)], 1)
+    order_all = OR.depth_order(pr)
+    gc, gt, gd, gi = (rb.color.cpu().numpy(), rb.trans.cpu().numpy(), rb.depth.cpu().numpy(),
+                      rb.index.cpu().numpy())
+    excluded = 0
+    for px, py in pix:
+        cand = _candidates(pr, px, py)
+        order = order_all[cand[order_all]]
+        with torch.no_grad():
+            o = OR.render_pixels(pr, np.array([[px, py]]), OP.camera(cfg), R, order=order)
+        if o["margin"][0] < MARGIN:
+            excluded += 1
+            continue
+        assert gi[py, px] == o["index"][0]
+        assert rel_close(gc[:, py, px], o["color"][0].numpy(), 1e-4, 1e-2).all()
+        assert rel_close(gt[py, px], o["trans"][0].item(), 1e-4, 1e-2)
+        assert rel_close(gd[py, px], o["depth"][0].item(), 1e-4, 1.0)
+    assert excluded <= 2
