@@ -407,7 +407,7 @@ class MappingEngine:
     """Device buffers + the per-frame call sequence for one camera and one Gaussian map."""
 
     def __init__(self, gm: GaussianMap, cam: _abi.Camera, capacity: int | None = None, preset="replica",
-                 weights=(1.0, 1.0, 1000.0), sample_cap: int | None = None, device="cuda"):
+                 weights=(1.0, 1.0, 1000.0), sample_cap: int | None = None, device="cuda", cache_frames: int = 1):
         self.gm, self.cam, self.device = gm, cam, device
         n = gm.capacity  # per-Gaussian buffers are sized for the map's storage (f2 appends rows)
         self.capacity = int(capacity if capacity is not None else max(4 * n, 1 << 16))
@@ -441,9 +441,11 @@ class MappingEngine:
         self.insert_result = torch.zeros(5, dtype=torch.int32, device=device)
         # NEXT f3: the stable part of the last ingested frame's sorted lists (valid for its pose and
         # until the stable set changes at the window end)
-        self.cache = BinBuffers(cam, self.capacity, device)
-        self.cache_ready = torch.cuda.Event()
-        self.cache_pose = None
+        # (one per window frame: `cache_frames` frames are kept, least recently ingested replaced first;
+        # slot 0 reuses proj_full so a single-frame engine allocates nothing extra)
+        self.cache_frames = max(1, int(cache_frames))
+        self._fc = [_FrameCache(self.proj_full, BinBuffers(cam, self.capacity, device))]
+        self._fc_clock = 0
         self.use_cache = True
         self.reset_window()
 
@@ -481,7 +483,7 @@ class MappingEngine:
         bin_and_sort(self.proj_full, self.gm.n, self.cam, None, self.bins_full, self.ws_bin_full, stream)
         render_color_depth(self.gm, self.proj_full, self.bins_full, model_pose, self.cam, RTGS_RENDER_FULL, self.full,
                            stream)
-        self.cache_pose = None  # proj_full / bins_full now hold the model pose's frame
+        self._drop_cache(self.proj_full)  # proj_full now holds the model pose's frame
         pose_io = init_pose if init_pose is not None else pose_device(np.asarray(model_pose.R).reshape(3, 3),
                                                                       np.asarray(model_pose.t), self.device)
         with torch.cuda.stream(torch.cuda.current_stream() if stream is None else stream):
@@ -527,33 +529,76 @@ class MappingEngine:
     def ingest(self, frame_color, frame_depth, pose: _abi.Pose, seed=0, frame_idx=0, stream=None, after_project=None):
         """A1 -> A2 (all tiles) -> A3/A4 FULL -> A7.  `after_project(stream)` is called once
         the projection (the last read of the parameters) has been enqueued."""
+        fc = self._cache_slot(pose) if self.use_cache else None
+        if fc is not None:
+            fc.key = None          # rebuilt below
+            self.proj_full = fc.proj
         project_gaussians(self.gm, pose, self.cam, self.proj_full, stream)
         if after_project is not None:
             after_project(stream)
         bin_and_sort(self.proj_full, self.gm.n, self.cam, None, self.bins_full, self.ws_bin_full, stream)
-        if self.use_cache:  # f3: the stable lists of this frame, reused by the window's iterations
-            stable_cache_build(self.bins_full, self.gm.flags, self.cam, self.cache, stream)
-            self.cache_ready.record(torch.cuda.current_stream() if stream is None else stream)
-            self.cache_pose = _pose_key(pose)
+        if fc is not None:  # f3: the stable lists of this frame, reused by the window's iterations
+            stable_cache_build(self.bins_full, self.gm.flags, self.cam, fc.cache, stream)
+            fc.ready.record(torch.cuda.current_stream() if stream is None else stream)
+            fc.key = _pose_key(pose)
         render_color_depth(self.gm, self.proj_full, self.bins_full, pose, self.cam, RTGS_RENDER_FULL, self.full, stream)
         classify_and_add_pixels(self.full, frame_color, frame_depth, self.gm.flags, self.cam,
                                 add_params(seed=seed, frame_idx=frame_idx), self.pixel_class, self.samples,
                                 self.add_counts, self.ws_cls, stream)
 
+    # --- f3 frame caches -------------------------------------------------------------------------
+    def _cache_slot(self, pose: _abi.Pose) -> "_FrameCache":
+        key = _pose_key(pose)
+        for fc in self._fc:
+            if fc.key == key:
+                break
+        else:
+            if len(self._fc) < self.cache_frames:
+                fc = _FrameCache(ProjectedBuffers(self.gm.capacity, self.device),
+                                 BinBuffers(self.cam, self.capacity, self.device))
+                self._fc.append(fc)
+            else:
+                fc = min(self._fc, key=lambda f: f.stamp)   # least recently ingested
+        self._fc_clock += 1
+        fc.stamp = self._fc_clock
+        return fc
+
+    def _lookup_cache(self, pose: _abi.Pose):
+        key = _pose_key(pose)
+        for fc in self._fc:
+            if fc.key is not None and fc.key == key:
+                return fc
+        return None
+
+    def _drop_cache(self, proj=None):
+        """Invalidate the frame caches (all, or the one whose projection buffer is `proj`)."""
+        for fc in self._fc:
+            if proj is None or fc.proj is proj:
+                fc.key = None
+
+    @property
+    def cache(self) -> BinBuffers:
+        """The stable-list cache of the frame currently in proj_full (the last ingested one)."""
+        for fc in self._fc:
+            if fc.proj is self.proj_full:
+                return fc.cache
+        return self._fc[0].cache
+
     def cached(self, pose: _abi.Pose) -> bool:
-        """True when the f3 stable cache holds this pose's lists for the current stable set."""
-        return self.use_cache and self.cache_pose is not None and self.cache_pose == _pose_key(pose)
+        """True when an f3 stable cache holds this pose's lists for the current stable set."""
+        return self.use_cache and self._lookup_cache(pose) is not None
 
     def forward_masked(self, pose: _abi.Pose, stream=None):
         """A1 -> A0 -> A2 (kept tiles) -> A3/A4 MASKED (Eq.12).  With a valid f3 cache
         only the unstable slots are projected and binned; the stable lists come from the cache."""
-        if self.cached(pose):
+        fc = self._lookup_cache(pose) if self.use_cache else None
+        if fc is not None:
             project_subset(self.gm, self.gid_of_slot, pose, self.cam, self.proj_sub, stream)
             coverage_rows(self.gm, self.proj_sub, int(self.gid_of_slot.numel()), pose, self.cam, self.out, stream)
-            (torch.cuda.current_stream() if stream is None else stream).wait_event(self.cache_ready)
-            bin_and_sort_cached(self.proj_full, self.cache, self.proj_sub, self.gid_of_slot, self.cam,
+            (torch.cuda.current_stream() if stream is None else stream).wait_event(fc.ready)
+            bin_and_sort_cached(fc.proj, fc.cache, self.proj_sub, self.gid_of_slot, self.cam,
                                 self.out.tile_keep, self.bins, self.ws_bin_cached, stream)
-            self.proj_iter = self.proj_full
+            self.proj_iter = fc.proj
         else:
             project_gaussians(self.gm, pose, self.cam, self.proj, stream)
             render_color_depth(self.gm, self.proj, None, pose, self.cam, RTGS_RENDER_COVERAGE, self.out, stream)
@@ -594,8 +639,28 @@ class MappingEngine:
         sp = state if state is not None else state_params(frame_idx)
         manage_states(self.full, frame_color, frame_depth, self.cam, self.gm.flags, self.err_count, self.eta,
                       self.t_created, sp, self.state_counts, self.ws_state, stream)
-        self.cache_pose = None  # the stable set changed: the f3 cache is stale
+        self._drop_cache()  # the stable set changed: every f3 cache is stale
         self.reset_window()
+
+    def map_window(self, frames, iterations=50, seed=0, first_frame_idx=0, insert=True):
+        """The paper's mapping window: for every window frame (colour, depth, pose):
+        ingest (A1, A2, A3/A4 FULL, A7, its f3 stable cache) and insert its sampled Gaussians (f2);
+        then a new slot set and `iterations` masked iterations, each on a uniformly sampled window
+        frame (f3-cached when cache_frames >= len(frames)); then Eq.9 fusion and the state
+        transitions on the last frame (f1).  Returns the device loss buffer of the last iteration."""
+        rng = np.random.default_rng(seed)
+        for i, (c, d, pose) in enumerate(frames):
+            self.ingest(c, d, pose, seed=seed, frame_idx=first_frame_idx + i)
+            if insert:
+                self.insert(c, d, pose, frame_idx=first_frame_idx + i)
+        self.reset_window()
+        for _ in range(iterations):
+            c, d, pose = frames[int(rng.integers(len(frames)))]
+            self.iteration(c, d, pose)
+        loss = self.loss.clone()
+        c, d, pose = frames[-1]
+        self.end_window(c, d, pose, frame_idx=first_frame_idx + len(frames) - 1)
+        return loss
 
     def step(self, frame_color, frame_depth, pose: _abi.Pose, ingest_pose=None, seed=0, frame_idx=0,
              reduce_grads=None):
@@ -618,6 +683,17 @@ class MappingEngine:
         main.wait_event(proj_done)
         self.optimizer_step(main)
         main.wait_stream(side)
+
+
+class _FrameCache:
+    """NEXT f3: one window frame's projection (stable rows read by the iterations) and the stable
+    part of its sorted tile lists."""
+
+    def __init__(self, proj: ProjectedBuffers, cache: BinBuffers):
+        self.proj, self.cache = proj, cache
+        self.ready = torch.cuda.Event()
+        self.key = None
+        self.stamp = 0
 
 
 def _pose_key(pose: _abi.Pose) -> tuple:

@@ -4,4 +4,4 @@ This package holds NO arithmetic of the method (no projection, blending, depth r
 optimiser).  It only produces data: Gaussian parameter arrays, camera/pose records and target
 RGBD frames, shaped like the paper's workloads.
 """
-from .scene import CONFIGS, SceneConfig, make_scene, make_frame, make_pose, view_poses  # noqa: F401
+from .scene import CONFIGS, SceneConfig, make_scene, make_frame, make_pose, trajectory_pose, view_poses  # noqa: F401

@@ -190,6 +190,21 @@ def make_pose(cfg: SceneConfig, view: int | None = None):
     return Rw @ Rd, Rw @ td + tw
 
 
+def trajectory_pose(cfg: SceneConfig, k: int):
+    """Pose of frame k of a smooth camera path through the primary view (a 30 fps hand-held scan:
+    1.5 cm and 0.4 deg per frame along a fixed seeded direction), for mapping-window runs."""
+    Rw, tw = _world_transform(cfg)
+    rng = np.random.default_rng(cfg.seed * 131 + 17)
+    axis = rng.normal(size=3)
+    axis /= np.linalg.norm(axis)
+    step = rng.normal(size=3)
+    step *= 0.015 / np.linalg.norm(step)
+    a = math.radians(0.4) * k
+    K = np.array([[0, -axis[2], axis[1]], [axis[2], 0, -axis[0]], [-axis[1], axis[0], 0]])
+    Rd = np.eye(3) + math.sin(a) * K + (1 - math.cos(a)) * K @ K
+    return Rw @ Rd, Rw @ (step * k) + tw
+
+
 def view_poses(cfg: SceneConfig, n_views: int):
     return [make_pose(cfg, v) for v in range(n_views)]
 
