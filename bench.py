@@ -318,9 +318,8 @@ def main():
         if eng.use_cache:  # the iteration through the f3 stable cache, as eng.step runs it
             n_slots = int(eng.gid_of_slot.numel())
             P.project_subset(gm, eng.gid_of_slot, pose, cam, eng.proj_sub); mark("iter.project_subset")
-            P.coverage_rows(gm, eng.proj_sub, n_slots, pose, cam, eng.out); mark("iter.coverage")
-            P.bin_and_sort_cached(eng.proj_full, eng.cache, eng.proj_sub, eng.gid_of_slot, cam, eng.out.tile_keep,
-                                  eng.bins, eng.ws_bin_cached); mark("iter.bin_and_sort_cached")
+            P.coverage_and_bin_cached(eng.proj_full, eng.cache, eng.proj_sub, eng.gid_of_slot, cam, eng.out, eng.bins,
+                                      eng.ws_bin_cached); mark("iter.coverage_and_bin_cached")
             eng.proj_iter = eng.proj_full
         else:
             P.project_gaussians(gm, pose, cam, eng.proj); mark("iter.project")

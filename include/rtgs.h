@@ -411,6 +411,17 @@ rtgs_status rtgs_icp_track(const float* depth, const float* model_depth, const f
 rtgs_status rtgs_decode_rgbd(const uint8_t* rgb, const uint16_t* depth_raw, int32_t width, int32_t height,
                              float depth_scale, float* color, float* depth, void* stream);
 
+/* rtgs_coverage_and_bin_cached: the f3 iteration's A0 + A2 in one call.  The subset rows are binned
+ * over ALL tiles; M_unstable (R16) is decided per tile from those lists (every pixel tests the tile's
+ * unstable instances until its first hit — identical decisions to the COVERAGE mode), giving
+ * active_bits, tile_keep, tile_list and counts[0..2] in `cov`; then the kept tiles are merged with
+ * the cached stable lists exactly as rtgs_bin_and_sort_cached does with that tile_keep.
+ * Workspace: rtgs_bin_cached_workspace_size. */
+rtgs_status rtgs_coverage_and_bin_cached(const rtgs_projected* proj, const rtgs_bins* cache, const rtgs_projected* sub,
+                                         const int32_t* sub_gid, int32_t n_sub, const rtgs_camera* cam,
+                                         rtgs_render_out* cov, rtgs_bins* out, void* workspace,
+                                         size_t workspace_bytes, void* stream);
+
 /* Utilities */
 const char* rtgs_status_string(rtgs_status s);
 const char* rtgs_last_cuda_error(void);

@@ -114,6 +114,8 @@ EXPORTS = {
     "rtgs_icp_workspace_size": (C.c_size_t, [P(Camera), C.c_int32]),
     "rtgs_icp_track": (C.c_int, [vp, vp, vp, P(Pose), P(Camera), P(IcpParams), vp, vp, vp, C.c_size_t, vp]),
     "rtgs_decode_rgbd": (C.c_int, [vp, vp, C.c_int32, C.c_int32, C.c_float, vp, vp, vp]),
+    "rtgs_coverage_and_bin_cached": (C.c_int, [P(Projected), P(Bins), P(Projected), vp, C.c_int32, P(Camera),
+                                               P(RenderOut), P(Bins), vp, C.c_size_t, vp]),
     "rtgs_status_string": (C.c_char_p, [C.c_int]),
     "rtgs_last_cuda_error": (C.c_char_p, []),
     "rtgs_version": (C.c_int32, []),

@@ -262,6 +262,22 @@ rtgs_status rtgs_decode_rgbd(const uint8_t* rgb, const uint16_t* depth_raw, int3
   return finish(launch_decode(rgb, depth_raw, width, height, depth_scale, color, depth, S(stream)));
 }
 
+rtgs_status rtgs_coverage_and_bin_cached(const rtgs_projected* proj, const rtgs_bins* cache, const rtgs_projected* sub,
+                                         const int32_t* sub_gid, int32_t n_sub, const rtgs_camera* cam,
+                                         rtgs_render_out* cov, rtgs_bins* out, void* workspace,
+                                         size_t workspace_bytes, void* stream) {
+  if (!proj || !proj->zkey || !cache || !cache->sorted_gid || !cache->tile_range || n_sub < 0 || !cam_ok(cam) ||
+      !bins_ok(out) || !proj_ok(sub, n_sub) || (n_sub > 0 && (!sub_gid || !a16(sub->rec))) || !cov ||
+      !cov->active_bits || !cov->tile_keep || !cov->tile_list || !cov->counts)
+    return RTGS_ERR_INVALID_ARG;
+  if (!workspace || workspace_bytes < bin_cached_workspace_size(n_sub, *cam, out->capacity)) return RTGS_ERR_WORKSPACE;
+  out->sub_rec = sub->rec;
+  out->sub_zkey = sub->zkey;
+  out->sub_gid = sub_gid;
+  return finish(launch_coverage_bin_cached(*proj, *cache, *sub, sub_gid, n_sub, *cam, *cov, *out, workspace,
+                                           S(stream)));
+}
+
 const char* rtgs_status_string(rtgs_status s) {
   switch (s) {
     case RTGS_OK: return "RTGS_OK";

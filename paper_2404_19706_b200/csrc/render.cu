@@ -90,6 +90,80 @@ __global__ void __launch_bounds__(256) k_tile_keep(const uint32_t* __restrict__ 
   }
 }
 
+// A0 from tile lists (f3 flow): one CTA per tile, one pixel per thread.  The tile's unstable
+// instances (any order: an existence test, R16) are staged 256 at a time; every pixel evaluates them
+// until its first hit.  Large splats are spread over their tiles, so the work is balanced; the tile
+// keep, kept-tile list and counts come out of the same CTA.
+__global__ void __launch_bounds__(256) k_tile_coverage(const uint2* __restrict__ srange,
+                                                       const unsigned long long* __restrict__ keys,
+                                                       const float4* __restrict__ sub_rec, int W, int H, int TX,
+                                                       uint32_t* __restrict__ bits, uint8_t* __restrict__ keep,
+                                                       uint32_t* __restrict__ list, uint32_t* __restrict__ counts) {
+  __shared__ float4 sa[256], sb[256];
+  const int t = blockIdx.x;
+  const int lx = threadIdx.x & 15, ly = threadIdx.x >> 4;
+  const int px = (t % TX) * kTile + lx, py = (t / TX) * kTile + ly;
+  const bool inside = px < W && py < H;
+  const uint2 rg = srange[t];
+  const int n = (int)(rg.y - rg.x);
+  bool cov = false;
+  for (int c0 = 0; c0 < n; c0 += 256) {
+    if (!__syncthreads_or(inside && !cov)) break;  // every pixel of the tile is decided
+    const int cnt = min(256, n - c0);
+    if ((int)threadIdx.x < cnt) {
+      const uint32_t row = (uint32_t)(keys[rg.x + c0 + threadIdx.x] & 0xFFFFFFFFull);
+      sa[threadIdx.x] = sub_rec[(size_t)4 * row];
+      sb[threadIdx.x] = sub_rec[(size_t)4 * row + 1];
+    }
+    __syncthreads();
+    if (inside && !cov)
+      for (int j = 0; j < cnt; ++j) {
+        PairEval e;
+        if (eval_pair(sa[j], sb[j], (float)px, (float)py, e)) {
+          cov = true;
+          break;
+        }
+      }
+    __syncthreads();
+  }
+  const bool act = inside && cov;
+  // active bits: each half-warp is one 16-pixel tile row; its 16 bits go to 1 or 2 mask words
+  const uint32_t bal = __ballot_sync(0xffffffffu, act);
+  const int lane = threadIdx.x & 31;
+  if ((lane & 15) == 0 && py < H) {
+    const uint32_t m16 = (lane ? bal >> 16 : bal) & 0xFFFFu;
+    const int x0 = px;  // lx == 0
+    const int valid = min(16, W - x0);
+    const uint32_t m = m16 & ((valid >= 16) ? 0xFFFFu : ((1u << valid) - 1u));
+    if (m) {
+      const uint32_t b = (uint32_t)py * (uint32_t)W + (uint32_t)x0;
+      const uint32_t sh = b & 31u;
+      atomicOr(&bits[b >> 5], m << sh);
+      if (sh > 16u) atomicOr(&bits[(b >> 5) + 1], m >> (32u - sh));
+    }
+  }
+  const int na = __syncthreads_count(act);
+  const int ni = __syncthreads_count(inside);
+  if (threadIdx.x == 0) {
+    const bool k = 2 * na >= ni;  // P:497 / R15
+    keep[t] = k ? 1 : 0;
+    if (k) {
+      list[atomicAdd(&counts[0], 1u)] = (uint32_t)t;
+      atomicAdd(&counts[1], (uint32_t)na);
+    }
+    if (na) atomicAdd(&counts[2], (uint32_t)na);
+  }
+}
+
+cudaError_t launch_tile_coverage(const uint2* srange, const unsigned long long* keys, const float4* sub_rec,
+                                 const rtgs_camera& cam, const rtgs_render_out& out, cudaStream_t s) {
+  const CamK k = make_cam(cam);
+  k_tile_coverage<<<k.TX * k.TY, 256, 0, s>>>(srange, keys, sub_rec, k.W, k.H, k.TX, out.active_bits, out.tile_keep,
+                                              out.tile_list, out.counts);
+  note_launch();
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------------------------------------
 // A3/A4 forward
 // ------------------------------------------------------------------------------------------------

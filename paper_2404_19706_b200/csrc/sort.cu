@@ -719,4 +719,56 @@ cudaError_t launch_bin_cached(const rtgs_projected& proj, const rtgs_bins& cache
   return cudaGetLastError();
 }
 
+// f3 flow with the coverage computed from the subset's tile lists: bin the subset rows over ALL
+// tiles (count, offsets, emit), decide coverage / tile keep per tile from those lists, then merge the
+// kept tiles with the cached stable lists (offsets, sort + merge).
+cudaError_t launch_coverage_bin_cached(const rtgs_projected& proj, const rtgs_bins& cache, const rtgs_projected& sub,
+                                       const int32_t* sub_gid, int n_sub, const rtgs_camera& cam,
+                                       const rtgs_render_out& cov, const rtgs_bins& out, void* ws, cudaStream_t s) {
+  const CamK k = make_cam(cam);
+  const int T = k.TX * k.TY;
+  uint32_t* ssorted;
+  uint2* srange;
+  uint32_t* sn;
+  void* bws;
+  carve_cached(n_sub, cam, out.capacity, static_cast<char*>(ws), &ssorted, &srange, &sn, &bws);
+  BinWS w;
+  carve(n_sub, cam, out.capacity, &w, static_cast<char*>(bws));
+  cudaMemsetAsync(w.cnt, 0, (size_t)((char*)w.start - (char*)w.cnt), s);
+  cudaMemsetAsync(cov.active_bits, 0, ((size_t)k.W * k.H + 31) / 32 * 4, s);
+  cudaMemsetAsync(cov.counts, 0, 16, s);
+  const uint2* rect = reinterpret_cast<const uint2*>(sub.rect);
+  const int nblk = (n_sub + 255) / 256;
+  if (n_sub > 0) {
+    k_tile_count<<<nblk, 256, 0, s>>>(sub.zkey, rect, nullptr, n_sub, k.TX, T, w.cnt);
+    note_launch();
+  }
+  k_tile_offsets<<<1, 1024, 0, s>>>(w.cnt, T, out.capacity, w.start, srange, sn);
+  note_launch();
+  if (n_sub > 0) {
+    k_emit<<<nblk, 256, 0, s>>>(sub.zkey, rect, nullptr, n_sub, k.TX, T, w.start, w.cursor, out.capacity, w.keys);
+    note_launch();
+  }
+  cudaError_t e = launch_tile_coverage(srange, w.keys, reinterpret_cast<const float4*>(sub.rec), cam, cov, s);
+  if (e != cudaSuccess) return e;
+  const uint8_t* keep = cov.tile_keep;
+  k_merge_offsets<<<1, 1024, 0, s>>>(w.cnt, keep, reinterpret_cast<const uint2*>(cache.tile_range), T, out.capacity,
+                                     w.start, srange, reinterpret_cast<uint2*>(out.tile_range), out.n_instances);
+  note_launch();
+  int row_bits = 1;
+  while (row_bits < 32 && (1u << row_bits) < (uint32_t)n_sub) ++row_bits;
+  const size_t smem = (size_t)kSortCap * (8 + 8 + 4);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_sort_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  k_sort_merge<<<T, kSortThreads, smem, s>>>(keep, srange, w.keys, w.tmp, w.grank, row_bits, ssorted,
+                                             reinterpret_cast<const uint2*>(cache.tile_range), cache.sorted_gid,
+                                             proj.zkey, sub.zkey, sub_gid, reinterpret_cast<const uint2*>(out.tile_range),
+                                             out.capacity, out.sorted_gid);
+  note_launch();
+  return cudaGetLastError();
+}
+
 }  // namespace rtgs

@@ -389,6 +389,22 @@ def decode_rgbd(rgb: torch.Tensor, depth_raw: torch.Tensor, depth_scale: float, 
                                  _stream(stream)), "rtgs_decode_rgbd")
 
 
+def coverage_and_bin_cached(proj: ProjectedBuffers, cache: BinBuffers, sub: ProjectedBuffers, sub_gid: torch.Tensor,
+                            cam: _abi.Camera, cov: RenderBuffers, out: BinBuffers, workspace: torch.Tensor,
+                            stream=None):
+    """f3 iteration A0 + A2: coverage / tile keep from the subset's tile lists, then the cached merge."""
+    pr = proj.c_struct()
+    c = cache.c_struct()
+    sp = sub.c_struct()
+    cv = cov.c_struct()
+    o = out.c_struct()
+    check(lib().rtgs_coverage_and_bin_cached(C.byref(pr), C.byref(c), C.byref(sp), _p(sub_gid),
+                                             int(sub_gid.numel()), C.byref(cam), C.byref(cv), C.byref(o),
+                                             _p(workspace), workspace.numel() * workspace.element_size(),
+                                             _stream(stream)), "rtgs_coverage_and_bin_cached")
+    out.sub = (sub.rec, sub.zkey, sub_gid)
+
+
 def hparams(preset: str = "replica") -> _abi.HParams:
     """Learning rates of P:501: Replica / ScanNet++ vs Azure / TUM."""
     if preset in ("replica", "scannetpp"):
@@ -594,10 +610,9 @@ class MappingEngine:
         fc = self._lookup_cache(pose) if self.use_cache else None
         if fc is not None:
             project_subset(self.gm, self.gid_of_slot, pose, self.cam, self.proj_sub, stream)
-            coverage_rows(self.gm, self.proj_sub, int(self.gid_of_slot.numel()), pose, self.cam, self.out, stream)
             (torch.cuda.current_stream() if stream is None else stream).wait_event(fc.ready)
-            bin_and_sort_cached(fc.proj, fc.cache, self.proj_sub, self.gid_of_slot, self.cam,
-                                self.out.tile_keep, self.bins, self.ws_bin_cached, stream)
+            coverage_and_bin_cached(fc.proj, fc.cache, self.proj_sub, self.gid_of_slot, self.cam, self.out, self.bins,
+                                    self.ws_bin_cached, stream)
             self.proj_iter = fc.proj
         else:
             project_gaussians(self.gm, pose, self.cam, self.proj, stream)
@@ -658,9 +673,18 @@ class MappingEngine:
             c, d, pose = frames[int(rng.integers(len(frames)))]
             self.iteration(c, d, pose)
         loss = self.loss.clone()
+        self.check_capacity()
         c, d, pose = frames[-1]
         self.end_window(c, d, pose, frame_idx=first_frame_idx + len(frames) - 1)
         return loss
+
+    def check_capacity(self):
+        """Raise if the last binnings overflowed the instance capacity (their outputs were truncated:
+        memory-safe but invalid).  One host synchronisation."""
+        worst = max(int(self.bins.n_instances.item()), int(self.bins_full.n_instances.item()))
+        if worst > self.capacity:
+            raise RuntimeError(f"instance capacity {self.capacity} < {worst}: construct the MappingEngine with "
+                               f"capacity >= {worst}")
 
     def step(self, frame_color, frame_depth, pose: _abi.Pose, ingest_pose=None, seed=0, frame_idx=0,
              reduce_grads=None):

@@ -13,7 +13,7 @@ pytestmark = pytest.mark.gpu
 
 def _window(P, cached, frames_np, scene, cfg, iterations=8):
     gm = P.GaussianMap.from_arrays(scene, capacity=scene["pos"].shape[0] + 20000)
-    eng = P.MappingEngine(gm, P.camera_of(cfg), cache_frames=len(frames_np))
+    eng = P.MappingEngine(gm, P.camera_of(cfg), cache_frames=len(frames_np), capacity=4 << 20)
     eng.use_cache = cached
     frames = [(torch.as_tensor(c, device="cuda"), torch.as_tensor(d, device="cuda"), P.make_pose(R, t))
               for (c, d, R, t) in frames_np]
