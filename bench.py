@@ -318,8 +318,10 @@ def main():
         if eng.use_cache:  # the iteration through the f3 stable cache, as eng.step runs it
             n_slots = int(eng.gid_of_slot.numel())
             P.project_subset(gm, eng.gid_of_slot, pose, cam, eng.proj_sub); mark("iter.project_subset")
-            P.coverage_and_bin_cached(eng.proj_full, eng.cache, eng.proj_sub, eng.gid_of_slot, cam, eng.out, eng.bins,
-                                      eng.ws_bin_cached); mark("iter.coverage_and_bin_cached")
+            P.coverage_subset(eng.proj_sub, n_slots, cam, eng.out, eng.capacity, eng.ws_bin_cached)
+            mark("iter.coverage_subset")
+            P.merge_cached(eng.proj_full, eng.cache, eng.proj_sub, eng.gid_of_slot, cam, eng.out, eng.bins,
+                           eng.ws_bin_cached); mark("iter.merge_cached")
             eng.proj_iter = eng.proj_full
         else:
             P.project_gaussians(gm, pose, cam, eng.proj); mark("iter.project")

@@ -422,6 +422,17 @@ rtgs_status rtgs_coverage_and_bin_cached(const rtgs_projected* proj, const rtgs_
                                          rtgs_render_out* cov, rtgs_bins* out, void* workspace,
                                          size_t workspace_bytes, void* stream);
 
+/* The two halves of rtgs_coverage_and_bin_cached, for overlapping the first with the ingest that
+ * builds the cache: rtgs_coverage_subset (bins the subset over all tiles into the workspace and
+ * writes the coverage fields of `cov`; reads no cache) then rtgs_merge_cached (same workspace, the
+ * same sub / n_sub / capacity, cov->tile_keep from the first call). */
+rtgs_status rtgs_coverage_subset(const rtgs_projected* sub, int32_t n_sub, const rtgs_camera* cam, rtgs_render_out* cov,
+                                 uint32_t capacity, void* workspace, size_t workspace_bytes, void* stream);
+rtgs_status rtgs_merge_cached(const rtgs_projected* proj, const rtgs_bins* cache, const rtgs_projected* sub,
+                              const int32_t* sub_gid, int32_t n_sub, const rtgs_camera* cam,
+                              const rtgs_render_out* cov, rtgs_bins* out, void* workspace, size_t workspace_bytes,
+                              void* stream);
+
 /* Utilities */
 const char* rtgs_status_string(rtgs_status s);
 const char* rtgs_last_cuda_error(void);

@@ -9,7 +9,7 @@ from .mapping import (GaussianMap, MappingEngine, ProjectedBuffers, BinBuffers, 
                       project_gaussians, bin_and_sort, render_color_depth, render_backward_masked,
                       adam_step_unstable, classify_and_add_pixels, fuse_window, manage_states, state_params,
                       project_subset, coverage_rows, stable_cache_build, bin_and_sort_cached,
-                      coverage_and_bin_cached,
+                      coverage_and_bin_cached, coverage_subset, merge_cached,
                       add_gaussians, insert_params, icp_track, icp_params, pose_device, decode_rgbd,
                       make_camera, make_pose, camera_of,
                       hparams, add_params, launch_count, RTGS_RENDER_FULL, RTGS_RENDER_MASKED,

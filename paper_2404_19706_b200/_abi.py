@@ -116,6 +116,10 @@ EXPORTS = {
     "rtgs_decode_rgbd": (C.c_int, [vp, vp, C.c_int32, C.c_int32, C.c_float, vp, vp, vp]),
     "rtgs_coverage_and_bin_cached": (C.c_int, [P(Projected), P(Bins), P(Projected), vp, C.c_int32, P(Camera),
                                                P(RenderOut), P(Bins), vp, C.c_size_t, vp]),
+    "rtgs_coverage_subset": (C.c_int, [P(Projected), C.c_int32, P(Camera), P(RenderOut), C.c_uint32, vp, C.c_size_t,
+                                       vp]),
+    "rtgs_merge_cached": (C.c_int, [P(Projected), P(Bins), P(Projected), vp, C.c_int32, P(Camera), P(RenderOut),
+                                    P(Bins), vp, C.c_size_t, vp]),
     "rtgs_status_string": (C.c_char_p, [C.c_int]),
     "rtgs_last_cuda_error": (C.c_char_p, []),
     "rtgs_version": (C.c_int32, []),

@@ -278,6 +278,30 @@ rtgs_status rtgs_coverage_and_bin_cached(const rtgs_projected* proj, const rtgs_
                                            S(stream)));
 }
 
+rtgs_status rtgs_coverage_subset(const rtgs_projected* sub, int32_t n_sub, const rtgs_camera* cam, rtgs_render_out* cov,
+                                 uint32_t capacity, void* workspace, size_t workspace_bytes, void* stream) {
+  if (n_sub < 0 || !cam_ok(cam) || !proj_ok(sub, n_sub) || (n_sub > 0 && !a16(sub->rec)) || !cov ||
+      !cov->active_bits || !cov->tile_keep || !cov->tile_list || !cov->counts)
+    return RTGS_ERR_INVALID_ARG;
+  if (!workspace || workspace_bytes < bin_cached_workspace_size(n_sub, *cam, capacity)) return RTGS_ERR_WORKSPACE;
+  return finish(launch_coverage_subset(*sub, n_sub, *cam, *cov, capacity, workspace, S(stream)));
+}
+
+rtgs_status rtgs_merge_cached(const rtgs_projected* proj, const rtgs_bins* cache, const rtgs_projected* sub,
+                              const int32_t* sub_gid, int32_t n_sub, const rtgs_camera* cam,
+                              const rtgs_render_out* cov, rtgs_bins* out, void* workspace, size_t workspace_bytes,
+                              void* stream) {
+  if (!proj || !proj->zkey || !cache || !cache->sorted_gid || !cache->tile_range || n_sub < 0 || !cam_ok(cam) ||
+      !bins_ok(out) || !proj_ok(sub, n_sub) || (n_sub > 0 && !sub_gid) || !cov || !cov->tile_keep)
+    return RTGS_ERR_INVALID_ARG;
+  if (!workspace || workspace_bytes < bin_cached_workspace_size(n_sub, *cam, out->capacity)) return RTGS_ERR_WORKSPACE;
+  out->sub_rec = sub->rec;
+  out->sub_zkey = sub->zkey;
+  out->sub_gid = sub_gid;
+  return finish(launch_merge_cached(*proj, *cache, *sub, sub_gid, n_sub, *cam, cov->tile_keep, *out, workspace,
+                                    S(stream)));
+}
+
 const char* rtgs_status_string(rtgs_status s) {
   switch (s) {
     case RTGS_OK: return "RTGS_OK";

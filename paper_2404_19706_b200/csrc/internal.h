@@ -34,6 +34,11 @@ cudaError_t launch_bin_cached(const rtgs_projected& proj, const rtgs_bins& cache
 
 cudaError_t launch_tile_coverage(const uint2* srange, const unsigned long long* keys, const float4* sub_rec,
                                  const rtgs_camera& cam, const rtgs_render_out& out, cudaStream_t s);
+cudaError_t launch_coverage_subset(const rtgs_projected& sub, int n_sub, const rtgs_camera& cam,
+                                   const rtgs_render_out& cov, uint32_t capacity, void* ws, cudaStream_t s);
+cudaError_t launch_merge_cached(const rtgs_projected& proj, const rtgs_bins& cache, const rtgs_projected& sub,
+                                const int32_t* sub_gid, int n_sub, const rtgs_camera& cam, const uint8_t* keep,
+                                const rtgs_bins& out, void* ws, cudaStream_t s);
 cudaError_t launch_coverage_bin_cached(const rtgs_projected& proj, const rtgs_bins& cache, const rtgs_projected& sub,
                                        const int32_t* sub_gid, int n_sub, const rtgs_camera& cam,
                                        const rtgs_render_out& cov, const rtgs_bins& out, void* ws, cudaStream_t s);

@@ -719,21 +719,22 @@ cudaError_t launch_bin_cached(const rtgs_projected& proj, const rtgs_bins& cache
   return cudaGetLastError();
 }
 
-// f3 flow with the coverage computed from the subset's tile lists: bin the subset rows over ALL
-// tiles (count, offsets, emit), decide coverage / tile keep per tile from those lists, then merge the
-// kept tiles with the cached stable lists (offsets, sort + merge).
-cudaError_t launch_coverage_bin_cached(const rtgs_projected& proj, const rtgs_bins& cache, const rtgs_projected& sub,
-                                       const int32_t* sub_gid, int n_sub, const rtgs_camera& cam,
-                                       const rtgs_render_out& cov, const rtgs_bins& out, void* ws, cudaStream_t s) {
+// f3 flow with the coverage computed from the subset's tile lists, in two parts so that the first
+// (which does not read the cache) can overlap the frame ingest that builds the cache:
+//   part 1: bin the subset rows over ALL tiles (count, offsets, emit) and decide coverage / tile keep
+//           per tile from those lists; the subset's lists stay in the workspace;
+//   part 2: merge the kept tiles with the cached stable lists (offsets, sort + merge).
+cudaError_t launch_coverage_subset(const rtgs_projected& sub, int n_sub, const rtgs_camera& cam,
+                                   const rtgs_render_out& cov, uint32_t capacity, void* ws, cudaStream_t s) {
   const CamK k = make_cam(cam);
   const int T = k.TX * k.TY;
   uint32_t* ssorted;
   uint2* srange;
   uint32_t* sn;
   void* bws;
-  carve_cached(n_sub, cam, out.capacity, static_cast<char*>(ws), &ssorted, &srange, &sn, &bws);
+  carve_cached(n_sub, cam, capacity, static_cast<char*>(ws), &ssorted, &srange, &sn, &bws);
   BinWS w;
-  carve(n_sub, cam, out.capacity, &w, static_cast<char*>(bws));
+  carve(n_sub, cam, capacity, &w, static_cast<char*>(bws));
   cudaMemsetAsync(w.cnt, 0, (size_t)((char*)w.start - (char*)w.cnt), s);
   cudaMemsetAsync(cov.active_bits, 0, ((size_t)k.W * k.H + 31) / 32 * 4, s);
   cudaMemsetAsync(cov.counts, 0, 16, s);
@@ -743,15 +744,27 @@ cudaError_t launch_coverage_bin_cached(const rtgs_projected& proj, const rtgs_bi
     k_tile_count<<<nblk, 256, 0, s>>>(sub.zkey, rect, nullptr, n_sub, k.TX, T, w.cnt);
     note_launch();
   }
-  k_tile_offsets<<<1, 1024, 0, s>>>(w.cnt, T, out.capacity, w.start, srange, sn);
+  k_tile_offsets<<<1, 1024, 0, s>>>(w.cnt, T, capacity, w.start, srange, sn);
   note_launch();
   if (n_sub > 0) {
-    k_emit<<<nblk, 256, 0, s>>>(sub.zkey, rect, nullptr, n_sub, k.TX, T, w.start, w.cursor, out.capacity, w.keys);
+    k_emit<<<nblk, 256, 0, s>>>(sub.zkey, rect, nullptr, n_sub, k.TX, T, w.start, w.cursor, capacity, w.keys);
     note_launch();
   }
-  cudaError_t e = launch_tile_coverage(srange, w.keys, reinterpret_cast<const float4*>(sub.rec), cam, cov, s);
-  if (e != cudaSuccess) return e;
-  const uint8_t* keep = cov.tile_keep;
+  return launch_tile_coverage(srange, w.keys, reinterpret_cast<const float4*>(sub.rec), cam, cov, s);
+}
+
+cudaError_t launch_merge_cached(const rtgs_projected& proj, const rtgs_bins& cache, const rtgs_projected& sub,
+                                const int32_t* sub_gid, int n_sub, const rtgs_camera& cam, const uint8_t* keep,
+                                const rtgs_bins& out, void* ws, cudaStream_t s) {
+  const CamK k = make_cam(cam);
+  const int T = k.TX * k.TY;
+  uint32_t* ssorted;
+  uint2* srange;
+  uint32_t* sn;
+  void* bws;
+  carve_cached(n_sub, cam, out.capacity, static_cast<char*>(ws), &ssorted, &srange, &sn, &bws);
+  BinWS w;
+  carve(n_sub, cam, out.capacity, &w, static_cast<char*>(bws));
   k_merge_offsets<<<1, 1024, 0, s>>>(w.cnt, keep, reinterpret_cast<const uint2*>(cache.tile_range), T, out.capacity,
                                      w.start, srange, reinterpret_cast<uint2*>(out.tile_range), out.n_instances);
   note_launch();
@@ -769,6 +782,14 @@ cudaError_t launch_coverage_bin_cached(const rtgs_projected& proj, const rtgs_bi
                                              out.capacity, out.sorted_gid);
   note_launch();
   return cudaGetLastError();
+}
+
+cudaError_t launch_coverage_bin_cached(const rtgs_projected& proj, const rtgs_bins& cache, const rtgs_projected& sub,
+                                       const int32_t* sub_gid, int n_sub, const rtgs_camera& cam,
+                                       const rtgs_render_out& cov, const rtgs_bins& out, void* ws, cudaStream_t s) {
+  cudaError_t e = launch_coverage_subset(sub, n_sub, cam, cov, out.capacity, ws, s);
+  if (e != cudaSuccess) return e;
+  return launch_merge_cached(proj, cache, sub, sub_gid, n_sub, cam, cov.tile_keep, out, ws, s);
 }
 
 }  // namespace rtgs

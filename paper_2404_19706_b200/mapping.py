@@ -405,6 +405,30 @@ def coverage_and_bin_cached(proj: ProjectedBuffers, cache: BinBuffers, sub: Proj
     out.sub = (sub.rec, sub.zkey, sub_gid)
 
 
+def coverage_subset(sub: ProjectedBuffers, n_sub: int, cam: _abi.Camera, cov: RenderBuffers, capacity: int,
+                    workspace: torch.Tensor, stream=None):
+    """f3 part 1: coverage / tile keep from the subset's tile lists (left in the workspace)."""
+    sp = sub.c_struct()
+    cv = cov.c_struct()
+    check(lib().rtgs_coverage_subset(C.byref(sp), int(n_sub), C.byref(cam), C.byref(cv), int(capacity), _p(workspace),
+                                     workspace.numel() * workspace.element_size(), _stream(stream)),
+          "rtgs_coverage_subset")
+
+
+def merge_cached(proj: ProjectedBuffers, cache: BinBuffers, sub: ProjectedBuffers, sub_gid: torch.Tensor,
+                 cam: _abi.Camera, cov: RenderBuffers, out: BinBuffers, workspace: torch.Tensor, stream=None):
+    """f3 part 2: merge the kept tiles' subset lists with the cached stable lists."""
+    pr = proj.c_struct()
+    c = cache.c_struct()
+    sp = sub.c_struct()
+    cv = cov.c_struct()
+    o = out.c_struct()
+    check(lib().rtgs_merge_cached(C.byref(pr), C.byref(c), C.byref(sp), _p(sub_gid), int(sub_gid.numel()),
+                                  C.byref(cam), C.byref(cv), C.byref(o), _p(workspace),
+                                  workspace.numel() * workspace.element_size(), _stream(stream)), "rtgs_merge_cached")
+    out.sub = (sub.rec, sub.zkey, sub_gid)
+
+
 def hparams(preset: str = "replica") -> _abi.HParams:
     """Learning rates of P:501: Replica / ScanNet++ vs Azure / TUM."""
     if preset in ("replica", "scannetpp"):
@@ -610,9 +634,11 @@ class MappingEngine:
         fc = self._lookup_cache(pose) if self.use_cache else None
         if fc is not None:
             project_subset(self.gm, self.gid_of_slot, pose, self.cam, self.proj_sub, stream)
+            coverage_subset(self.proj_sub, int(self.gid_of_slot.numel()), self.cam, self.out, self.capacity,
+                            self.ws_bin_cached, stream)
             (torch.cuda.current_stream() if stream is None else stream).wait_event(fc.ready)
-            coverage_and_bin_cached(fc.proj, fc.cache, self.proj_sub, self.gid_of_slot, self.cam, self.out, self.bins,
-                                    self.ws_bin_cached, stream)
+            merge_cached(fc.proj, fc.cache, self.proj_sub, self.gid_of_slot, self.cam, self.out, self.bins,
+                         self.ws_bin_cached, stream)
             self.proj_iter = fc.proj
         else:
             project_gaussians(self.gm, pose, self.cam, self.proj, stream)
