@@ -50,8 +50,11 @@ __global__ void __launch_bounds__(kAdamThreads) k_adam(const AdamArgs a) {
   }
   const float ibc1 = 1.f / bc1, ibc2 = 1.f / bc2;
   bool nz = false;
+  uint32_t eta0 = 0;
+  size_t gid = 0;
   if (live) {
-    const size_t gid = (size_t)a.gid_of_slot[slot];
+    gid = (size_t)a.gid_of_slot[slot];
+    if (t == 0) eta0 = a.eta[gid];  // issued with the row gathers, not after the update
     const bool transparent = a.flags[gid] & 1u;
     const size_t row = (size_t)slot * D;
     const float th0v = (t < 10 && a.init_geom) ? a.init_geom[(size_t)slot * 10 + t] : 0.f;  // independent of gid
@@ -94,7 +97,7 @@ __global__ void __launch_bounds__(kAdamThreads) k_adam(const AdamArgs a) {
   // eta += 1 once per slot with a non-zero SH gradient (R20): vote within the half-warp
   const uint32_t vote = __ballot_sync(0xffffffffu, nz);
   const uint32_t half = (lane < 16) ? (vote & 0x0000FFFFu) : (vote & 0xFFFF0000u);
-  if (live && t == 0 && half) a.eta[a.gid_of_slot[slot]] += 1u;
+  if (live && t == 0 && half) a.eta[gid] = eta0 + 1u;
 }
 
 cudaError_t launch_adam(const rtgs_params& p, const int32_t* gid_of_slot, int n_slots, const uint8_t* flags,
