@@ -403,6 +403,12 @@ def main():
         icp_rows = eng.icp_diag.cpu().numpy().reshape(-1, 4)
         icp_rows = icp_rows[icp_rows[:, 0] >= 0]
         restore()
+        # blended-pair statistic of the FULL render: one extra launch of the counting variant (the
+        # timed step and render_full_alone_ms use the production kernel, which does not count)
+        eng.full.count_blends = True
+        P.render_color_depth(gm, eng.proj_full, eng.bins_full, pose, cam, P.RTGS_RENDER_FULL, eng.full)
+        torch.cuda.synchronize()
+        eng.full.count_blends = False
         blends_full = int(eng.full.counts[3].item())
         blends_masked = int(eng.out.counts[3].item())
         counts_full = None

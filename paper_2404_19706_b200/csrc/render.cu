@@ -188,7 +188,9 @@ struct FwdArgs {
   uint32_t* n_contrib;
 };
 
-template <bool MASKED>
+// COUNT: accumulate the blended-pair statistic counts[3] (only when the caller passes counts in FULL
+// mode; the production FULL render of the mapping step does not, saving 3 instructions per survivor)
+template <bool MASKED, bool COUNT>
 __global__ void __launch_bounds__(32 * ((MASKED ? kHalfWarps : kTileWarps) + 1)) k_render_fwd(const FwdArgs a) {
   constexpr int NW = MASKED ? kHalfWarps : kTileWarps;  // MASKED: one CTA per half of a kept tile
   __shared__ PipeRing r;  // static: stage addresses fold into immediates
@@ -265,7 +267,7 @@ __global__ void __launch_bounds__(32 * ((MASKED ? kHalfWarps : kTileWarps) + 1))
           cb = __fmaf_rn(r2.z, wgt, cb);
           T = ok ? test : T;
           last = ok ? pbase + (uint32_t)idx : last;
-          nblend += ok ? 1u : 0u;
+          if (COUNT) nblend += ok ? 1u : 0u;
         }
         if (__all_sync(0xffffffffu, done)) {
           wdone = true;
@@ -277,7 +279,7 @@ __global__ void __launch_bounds__(32 * ((MASKED ? kHalfWarps : kTileWarps) + 1))
     __syncwarp();
     if (lane == 0) mbar_arrive(&r.empty[st]);
   }
-  if (a.counts) {
+  if (COUNT) {
     const uint32_t wsum = __reduce_add_sync(0xffffffffu, nblend);
     if (lane == 0 && wsum) atomicAdd(const_cast<uint32_t*>(a.counts) + 3, wsum);
   }
@@ -354,8 +356,9 @@ cudaError_t launch_render(const rtgs_projected& proj, const rtgs_bins& bins, con
   a.index = out.index; a.n_contrib = out.n_contrib;
   const int T = a.cam.TX * a.cam.TY;
   if (out.counts) cudaMemsetAsync(out.counts + 3, 0, 4, s);  // blend counter of this render
-  if (masked) k_render_fwd<true><<<2 * T, 32 * (kHalfWarps + 1), 0, s>>>(a);
-  else k_render_fwd<false><<<T, 32 * (kTileWarps + 1), 0, s>>>(a);
+  if (masked) k_render_fwd<true, true><<<2 * T, 32 * (kHalfWarps + 1), 0, s>>>(a);
+  else if (out.counts) k_render_fwd<false, true><<<T, 32 * (kTileWarps + 1), 0, s>>>(a);
+  else k_render_fwd<false, false><<<T, 32 * (kTileWarps + 1), 0, s>>>(a);
   note_launch();
   return cudaGetLastError();
 }

@@ -132,7 +132,7 @@ class BinBuffers:
 
 
 class RenderBuffers:
-    def __init__(self, cam: _abi.Camera, device="cuda", normal=True):
+    def __init__(self, cam: _abi.Camera, device="cuda", normal=True, count_blends=True):
         H, W = cam.height, cam.width
         T = ((W + 15) // 16) * ((H + 15) // 16)
         self.color = torch.zeros((3, H, W), dtype=torch.float32, device=device)
@@ -145,11 +145,14 @@ class RenderBuffers:
         self.tile_keep = torch.zeros(T, dtype=torch.uint8, device=device)
         self.tile_list = torch.zeros(T, dtype=torch.int32, device=device)
         self.counts = torch.zeros(4, dtype=torch.int32, device=device)
+        # FULL mode only counts blended pairs (counts[3]) when asked: the statistic costs instructions
+        self.count_blends = count_blends
 
-    def c_struct(self):
+    def c_struct(self, mode: int | None = None):
+        counts = None if (mode == RTGS_RENDER_FULL and not self.count_blends) else self.counts
         return _abi.RenderOut(_p(self.color), _p(self.trans), _p(self.depth), _p(self.normal), _p(self.index),
                               _p(self.n_contrib), _p(self.active_bits), _p(self.tile_keep), _p(self.tile_list),
-                              _p(self.counts))
+                              _p(counts))
 
     def active_mask(self) -> torch.Tensor:
         """Unpack active_bits into a bool [H, W] image (test / inspection helper)."""
@@ -194,7 +197,7 @@ def render_color_depth(gm: GaussianMap, proj: ProjectedBuffers, bins: BinBuffers
                        cam: _abi.Camera, mode: int, out: RenderBuffers, stream=None):
     g = gm.c_struct()
     pr = proj.c_struct()
-    o = out.c_struct()
+    o = out.c_struct(mode)
     b = bins.c_struct() if bins is not None else None
     check(lib().rtgs_render_color_depth(C.byref(g), C.byref(pr), C.byref(b) if b is not None else None, C.byref(pose),
                                         C.byref(cam), mode, C.byref(o), _stream(stream)), "rtgs_render_color_depth")
@@ -458,7 +461,7 @@ class MappingEngine:
         self.ws_bin = torch.empty(bin_workspace_size(n, cam, self.capacity), dtype=torch.uint8, device=device)
         self.proj_full = ProjectedBuffers(n, device)
         self.bins_full = BinBuffers(cam, self.capacity, device)
-        self.full = RenderBuffers(cam, device)
+        self.full = RenderBuffers(cam, device, count_blends=False)  # production FULL render: no statistic
         self.ws_bin_full = torch.empty(bin_workspace_size(n, cam, self.capacity), dtype=torch.uint8, device=device)
         self.side = torch.cuda.Stream(device=device)
         self.ws_cls = torch.empty(classify_workspace_size(cam), dtype=torch.uint8, device=device)
