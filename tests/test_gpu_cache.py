@@ -141,7 +141,7 @@ def _same(a, b):
     g1, g2 = a["grad"], b["grad"]
     scale = np.abs(g2).max(0, keepdims=True) + 1e-30
     assert (np.abs(g1 - g2) <= 1e-5 * scale).all()
-    np.testing.assert_allclose(a["loss"], b["loss"], rtol=1e-6)
+    np.testing.assert_allclose(a["loss"], b["loss"], rtol=1e-5)  # float32 atomic sum order across CTAs
 
 
 @pytest.mark.parametrize("name", ["C1", "T2", "C2"])

@@ -219,7 +219,7 @@ def test_cached_iteration_equals_uncached_c3(c3):
     assert np.array_equal(a["depth"][act], b["depth"][act]) and np.array_equal(a["index"][act], b["index"][act])
     scale = np.abs(b["grad"]).max(0, keepdims=True) + 1e-30
     assert (np.abs(a["grad"] - b["grad"]) <= 1e-5 * scale).all()
-    np.testing.assert_allclose(a["loss"], b["loss"], rtol=1e-6)
+    np.testing.assert_allclose(a["loss"], b["loss"], rtol=1e-5)  # float32 atomic sum order across CTAs
 
 
 def test_c4_render_only_sampled():
