@@ -487,12 +487,14 @@ def main():
         torch.cuda.synchronize()
         w0, w1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         n_before = gm.n
+        t_host = time.perf_counter()
         w0.record(stream)
         eng.map_window(frames, iterations=50, seed=4, first_frame_idx=16)
         w1.record(stream)
         torch.cuda.synchronize()
+        t_host = (time.perf_counter() - t_host) * 1e3
         t_win = w0.elapsed_time(w1)
-        window = {"frames": len(frames), "iterations": 50, "ms": round(t_win, 3),
+        window = {"frames": len(frames), "iterations": 50, "ms": round(t_win, 3), "host_ms": round(t_host, 3),
                   "mapping_iters_per_s": round(50 * 1e3 / t_win, 1), "gaussians_added": gm.n - n_before,
                   "slots": int(eng.gid_of_slot.numel()),
                   "note": "second window of a smooth 6-frame path: 6 ingests + insertions (host syncs), a new slot "
