@@ -678,13 +678,12 @@ cudaError_t launch_backward(const rtgs_gaussians& g, const rtgs_projected& proj,
   b.loss_out = loss_out;
   b.counts = fwd.counts;
   const int nb = n_slots > 0 ? (n_slots + 127) / 128 : 1;
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr_mask{0};
+  if (first_on_device(attr_mask)) {
     cudaFuncSetAttribute(k_project_bwd<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PBSmem<1>));
     cudaFuncSetAttribute(k_project_bwd<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PBSmem<4>));
     cudaFuncSetAttribute(k_project_bwd<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PBSmem<9>));
     cudaFuncSetAttribute(k_project_bwd<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PBSmem<16>));
-    attr = true;
   }
   switch (b.K) {
     case 1: k_project_bwd<1><<<nb, 128, sizeof(PBSmem<1>), s>>>(b); break;

@@ -6,7 +6,18 @@
 
 #include "rtgs.h"
 
+#include <atomic>
+
 namespace rtgs {
+
+// once per (kernel attribute, device): per-device bit in `mask` (one-time cudaFuncSetAttribute calls
+// must be repeated on every device the process launches on)
+inline bool first_on_device(std::atomic<uint64_t>& mask) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  return (mask.fetch_or(bit) & bit) == 0;
+}
 
 struct PoseF {  // world->camera V = R^T, t' = -R^T t (double and float32 copies), camera centre
   double V[9], tp[3], campos[3];

@@ -626,10 +626,9 @@ cudaError_t launch_bin(const rtgs_projected& proj, int n, const rtgs_camera& cam
     int gid_bits = 1;
     while (gid_bits < 32 && (1u << gid_bits) < (uint32_t)n) ++gid_bits;
     const size_t smem = (size_t)kSortCap * (8 + 8 + 4);
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<uint64_t> attr_mask{0};
+    if (first_on_device(attr_mask)) {
       cudaFuncSetAttribute(k_tile_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr = true;
     }
     k_tile_sort<<<T, kSortThreads, smem, s>>>(reinterpret_cast<const uint2*>(out.tile_range), w.keys, w.tmp, w.grank,
                                               gid_bits, out.sorted_gid);
@@ -706,10 +705,9 @@ cudaError_t launch_bin_cached(const rtgs_projected& proj, const rtgs_bins& cache
   int row_bits = 1;
   while (row_bits < 32 && (1u << row_bits) < (uint32_t)n_sub) ++row_bits;
   const size_t smem = (size_t)kSortCap * (8 + 8 + 4);
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr_mask{0};
+  if (first_on_device(attr_mask)) {
     cudaFuncSetAttribute(k_sort_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
   }
   k_sort_merge<<<T, kSortThreads, smem, s>>>(keep, srange, w.keys, w.tmp, w.grank, row_bits, ssorted,
                                              reinterpret_cast<const uint2*>(cache.tile_range), cache.sorted_gid,
@@ -771,10 +769,9 @@ cudaError_t launch_merge_cached(const rtgs_projected& proj, const rtgs_bins& cac
   int row_bits = 1;
   while (row_bits < 32 && (1u << row_bits) < (uint32_t)n_sub) ++row_bits;
   const size_t smem = (size_t)kSortCap * (8 + 8 + 4);
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr_mask{0};
+  if (first_on_device(attr_mask)) {
     cudaFuncSetAttribute(k_sort_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
   }
   k_sort_merge<<<T, kSortThreads, smem, s>>>(keep, srange, w.keys, w.tmp, w.grank, row_bits, ssorted,
                                              reinterpret_cast<const uint2*>(cache.tile_range), cache.sorted_gid,
