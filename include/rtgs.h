@@ -433,6 +433,19 @@ rtgs_status rtgs_merge_cached(const rtgs_projected* proj, const rtgs_bins* cache
                               const rtgs_render_out* cov, rtgs_bins* out, void* workspace, size_t workspace_bytes,
                               void* stream);
 
+/* =============================================================================================
+ * (e) keyframe global optimisation: the pixels with the top `ratio` (0.4) colour errors of
+ * a keyframe (reading R36).  err = ((|dR| + |dG|) + |dB|) / 3 in float32 between the keyframe's
+ * FULL render `full->color` and its colour `frame_color`; K = round(ratio * H * W) (float64); the K
+ * largest, ties by row-major pixel index (lower first), by an exact radix select on the float bits.
+ * Writes out->active_bits (the selected pixels), out->tile_keep / tile_list (every tile with a
+ * selected pixel) and out->counts[0..2] (#tiles, K, K): the inputs rtgs_render_backward_masked needs
+ * with the FULL render's other fields.
+ * ============================================================================================= */
+size_t rtgs_topk_workspace_size(const rtgs_camera* cam);
+rtgs_status rtgs_topk_error_mask(const float* color_hat, const float* frame_color, const rtgs_camera* cam, double ratio,
+                                 rtgs_render_out* out, void* workspace, size_t workspace_bytes, void* stream);
+
 /* Utilities */
 const char* rtgs_status_string(rtgs_status s);
 const char* rtgs_last_cuda_error(void);

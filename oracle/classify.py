@@ -73,3 +73,21 @@ def classify(color_hat, trans, depth_hat, index, color, depth, flags, delta_T=0.
     counts = np.array([m_s.sum(), m_c.sum(), (action == 1).sum(), (action == 2).sum(), (action == 3).sum()],
                       dtype=np.int64)
     return cls, samples, counts
+
+
+def topk_error_mask(color_hat, color, ratio=0.4):
+    """(e) / P:284 global optimisation: the pixels with the top `ratio` colour errors of a keyframe
+    (reading R36): err = ((|dR| + |dG|) + |dB|) / 3 in float32 (the A7 order), K = round(ratio * H W)
+    (threshold formed in float64, as R22), ties broken by row-major pixel index (lower first).
+    Returns (mask bool [H, W], K)."""
+    f32 = np.float32
+    ch, c = np.asarray(color_hat, dtype=f32), np.asarray(color, dtype=f32)
+    H, W = c.shape[1:]
+    err = ((np.abs(ch[0] - c[0]) + np.abs(ch[1] - c[1])) + np.abs(ch[2] - c[2])) / f32(3.0)
+    K = int(np.floor(ratio * H * W + 0.5))
+    flat = err.ravel()
+    idx = np.arange(H * W)
+    order = np.lexsort((idx, -flat.astype(np.float64)))   # descending error, then ascending index
+    mask = np.zeros(H * W, dtype=bool)
+    mask[order[:K]] = True
+    return mask.reshape(H, W), K

@@ -101,6 +101,8 @@ def project(params: dict, R: np.ndarray, t: np.ndarray, cam: dict, sh_degree: in
     alpha_np = alpha.detach().numpy()
     k_ext = extent_sigmas(alpha_np)
     valid = (z32 > np.float32(NEAR)) & np.isfinite(k_ext)
+    if params.get("flags") is not None:  # NEXT f1 / R29: removed Gaussians (flags bit2) are culled
+        valid &= (np.asarray(params["flags"]) & 4) == 0
 
     # EWA splatting (R4, R5): Sigma' = (J V) Sigma (J V)^T + 0.3 I, V = R^T
     Sigma = covariance(log_scale, rot)
@@ -165,6 +167,7 @@ def params_from_scene(scene: dict, requires_grad: bool = False) -> dict:
         out[k] = tns
     out["pos32"] = np.asarray(scene["pos"], dtype=np.float32)
     out["log_scale32"] = np.asarray(scene["log_scale"], dtype=np.float32)
+    out["flags"] = np.asarray(scene["flags"]) if "flags" in scene else None
     return out
 
 

@@ -302,6 +302,17 @@ rtgs_status rtgs_merge_cached(const rtgs_projected* proj, const rtgs_bins* cache
                                     S(stream)));
 }
 
+size_t rtgs_topk_workspace_size(const rtgs_camera* cam) { return cam_ok(cam) ? topk_workspace_size(*cam) : 0; }
+
+rtgs_status rtgs_topk_error_mask(const float* color_hat, const float* frame_color, const rtgs_camera* cam, double ratio,
+                                 rtgs_render_out* out, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!color_hat || !frame_color || !cam_ok(cam) || !(ratio >= 0.0 && ratio <= 1.0) || !out || !out->active_bits ||
+      !out->tile_keep || !out->tile_list || !out->counts)
+    return RTGS_ERR_INVALID_ARG;
+  if (!workspace || workspace_bytes < topk_workspace_size(*cam)) return RTGS_ERR_WORKSPACE;
+  return finish(launch_topk(color_hat, frame_color, *cam, ratio, *out, workspace, S(stream)));
+}
+
 const char* rtgs_status_string(rtgs_status s) {
   switch (s) {
     case RTGS_OK: return "RTGS_OK";

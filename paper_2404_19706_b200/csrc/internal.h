@@ -96,6 +96,11 @@ cudaError_t launch_icp(const float* depth, const float* mdepth, const float* mno
 cudaError_t launch_decode(const uint8_t* rgb, const uint16_t* raw, int W, int H, float depth_scale, float* color,
                           float* depth, cudaStream_t s);
 
+cudaError_t launch_tile_any(const rtgs_camera& cam, const rtgs_render_out& out, cudaStream_t s);
+size_t topk_workspace_size(const rtgs_camera& cam);
+cudaError_t launch_topk(const float* chat, const float* c, const rtgs_camera& cam, double ratio,
+                        const rtgs_render_out& out, void* ws, cudaStream_t s);
+
 // generic device-wide exclusive scan of uint32 (length known on the host; zeros past the live part)
 size_t scan_workspace_size(size_t len);
 cudaError_t launch_scan(const uint32_t* in, uint32_t* out, size_t len, uint32_t* total, void* ws, cudaStream_t s);

@@ -65,6 +65,7 @@ __global__ void __launch_bounds__(256) k_coverage(const float4* __restrict__ rec
   }
 }
 
+template <bool ANY>  // ANY: keep every tile with an active pixel ((e) top-k masks), else the 50 % rule
 __global__ void __launch_bounds__(256) k_tile_keep(const uint32_t* __restrict__ bits, int W, int H, int TX,
                                                    uint8_t* __restrict__ keep, uint32_t* __restrict__ list,
                                                    uint32_t* __restrict__ counts) {
@@ -79,7 +80,7 @@ __global__ void __launch_bounds__(256) k_tile_keep(const uint32_t* __restrict__ 
   const int na = __syncthreads_count(act);
   const int ni = __syncthreads_count(inside);
   if (threadIdx.x == 0) {
-    const bool k = 2 * na >= ni;  // P:497 / R15: discard tiles with < 50 % active pixels
+    const bool k = ANY ? na > 0 : 2 * na >= ni;  // P:497 / R15: discard tiles with < 50 % active pixels
     keep[t] = k ? 1 : 0;
     if (k) {
       const uint32_t pos = atomicAdd(&counts[0], 1u);
@@ -332,7 +333,16 @@ cudaError_t launch_coverage(const rtgs_gaussians& g, const rtgs_projected& proj,
                                                  k.W, out.active_bits);
     note_launch();
   }
-  k_tile_keep<<<k.TX * k.TY, 256, 0, s>>>(out.active_bits, k.W, k.H, k.TX, out.tile_keep, out.tile_list, out.counts);
+  k_tile_keep<false><<<k.TX * k.TY, 256, 0, s>>>(out.active_bits, k.W, k.H, k.TX, out.tile_keep, out.tile_list,
+                                                 out.counts);
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tile_any(const rtgs_camera& cam, const rtgs_render_out& out, cudaStream_t s) {
+  const CamK k = make_cam(cam);
+  k_tile_keep<true><<<k.TX * k.TY, 256, 0, s>>>(out.active_bits, k.W, k.H, k.TX, out.tile_keep, out.tile_list,
+                                                out.counts);
   note_launch();
   return cudaGetLastError();
 }

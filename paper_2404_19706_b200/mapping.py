@@ -432,6 +432,23 @@ def merge_cached(proj: ProjectedBuffers, cache: BinBuffers, sub: ProjectedBuffer
     out.sub = (sub.rec, sub.zkey, sub_gid)
 
 
+# ---------------------------------------------------------------------------------------------
+# (e) keyframe global optimisation
+# ---------------------------------------------------------------------------------------------
+def topk_workspace_size(cam: _abi.Camera) -> int:
+    return int(lib().rtgs_topk_workspace_size(C.byref(cam)))
+
+
+def topk_error_mask(full: RenderBuffers, frame_color: torch.Tensor, cam: _abi.Camera, ratio: float,
+                    out: RenderBuffers, workspace: torch.Tensor, stream=None):
+    """Active set = the top `ratio` colour-error pixels of the FULL render `full` (written to `out`'s
+    active bits, tile keep / list and counts; `out` may be `full` itself)."""
+    o = out.c_struct()
+    check(lib().rtgs_topk_error_mask(_p(full.color), _p(frame_color), C.byref(cam), float(ratio), C.byref(o),
+                                     _p(workspace), workspace.numel() * workspace.element_size(), _stream(stream)),
+          "rtgs_topk_error_mask")
+
+
 def hparams(preset: str = "replica") -> _abi.HParams:
     """Learning rates of P:501: Replica / ScanNet++ vs Azure / TUM."""
     if preset in ("replica", "scannetpp"):
@@ -714,6 +731,66 @@ class MappingEngine:
         if worst > self.capacity:
             raise RuntimeError(f"instance capacity {self.capacity} < {worst}: construct the MappingEngine with "
                                f"capacity >= {worst}")
+
+    # --- (e) keyframe global optimisation -------------------------------------------------------
+    def _global_state(self):
+        """Slots = every non-removed Gaussian (rebuilt when the map changed); Adam state per call."""
+        n = self.gm.n
+        if getattr(self, "_g_n", None) != n or getattr(self, "_g_flags_sum", None) != int(self.gm.flags.sum()):
+            flags = self.gm.flags.cpu().numpy()
+            gid = np.nonzero((flags & 4) == 0)[0].astype(np.int32)
+            slot = np.full(n, -1, np.int32)
+            slot[gid] = np.arange(len(gid), dtype=np.int32)
+            self.g_gid = torch.zeros(max(len(gid), 1), dtype=torch.int32, device=self.device)[: len(gid)]
+            self.g_gid.copy_(torch.as_tensor(gid))
+            self.g_slot = torch.as_tensor(slot, device=self.device)
+            D = 10 + 3 * (self.gm.sh_degree + 1) ** 2
+            self.g_grad = torch.zeros((max(len(gid), 1), D), dtype=torch.float32, device=self.device)
+            self.g_m = torch.zeros_like(self.g_grad)
+            self.g_v = torch.zeros_like(self.g_grad)
+            self.g_ws_bwd = torch.empty(backward_workspace_size(len(gid)), dtype=torch.uint8, device=self.device)
+            self.g_ntr = int(((flags[gid] & FLAG_TRANSPARENT) != 0).sum())
+            self.g_rb = RenderBuffers(self.cam, self.device, count_blends=False)
+            self.g_ws_topk = torch.empty(topk_workspace_size(self.cam), dtype=torch.uint8, device=self.device)
+            self.g_loss = torch.zeros(4, dtype=torch.float32, device=self.device)
+            self._g_n, self._g_flags_sum = n, int(self.gm.flags.sum())
+
+    def global_backward(self, views, ratio=0.4, stream=None):
+        """(e) P:284, per keyframe view (colour, depth, pose): FULL render (A1, A2, A3/A4), its top
+        `ratio` colour-error pixels (K9), the masked backward over ALL non-removed Gaussians with the
+        loss weights divided by the number of views (the batch loss is the mean over the views),
+        accumulated into g_grad.  Multi-GPU: every rank calls this on its share of the views."""
+        self._global_state()
+        w = tuple(x / max(1, len(views)) for x in self.weights[:2]) + (self.weights[2],)
+        for (c, d, pose) in views:
+            project_gaussians(self.gm, pose, self.cam, self.proj, stream)
+            bin_and_sort(self.proj, self.gm.n, self.cam, None, self.bins, self.ws_bin, stream)
+            self.bins.sub = None
+            render_color_depth(self.gm, self.proj, self.bins, pose, self.cam, RTGS_RENDER_FULL, self.g_rb, stream)
+            topk_error_mask(self.g_rb, c, self.cam, ratio, self.g_rb, self.g_ws_topk, stream)
+            render_backward_masked(self.gm, self.proj, self.bins, pose, self.cam, self.g_rb, c, d, w, self.g_slot,
+                                   self.g_gid, self.g_grad, self.g_loss, self.g_ws_bwd, stream)
+
+    def global_step(self, views, ratio=0.4, lr_scale=0.1, reduce_grads=None, stream=None):
+        """(e) one global optimisation step: global_backward over `views`, the gradient sum
+        over ranks (`reduce_grads(g_grad)`, multi-GPU), then one Adam step of every non-removed
+        Gaussian with the position learning rate 0 and the others x lr_scale (reading R37: fresh
+        moments per global step; L_reg anchors the transparent geometry at its pre-step values)."""
+        self.global_backward(views, ratio, stream)
+        if reduce_grads is not None:
+            reduce_grads(self.g_grad)
+        hp = self.hp
+        ghp = _abi.HParams(0.0, hp.lr_sh0 * lr_scale, hp.lr_shrest * lr_scale, hp.lr_scale * lr_scale,
+                           hp.lr_rot * lr_scale, hp.beta1, hp.beta2, hp.eps)
+        g = self.g_gid.long()
+        init = torch.cat([self.gm.pos[g], self.gm.log_scale[g], self.gm.rot[g]], 1).contiguous() if len(g) else None
+        s = torch.cuda.current_stream() if stream is None else stream
+        with torch.cuda.stream(s):
+            self.g_m.zero_()
+            self.g_v.zero_()
+        adam_step_unstable(self.gm, self.g_gid, self.g_grad, self.g_m, self.g_v, init, self.g_ntr, self.weights[2], ghp,
+                           1, self.eta, stream)
+        return self.g_loss
 
     def step(self, frame_color, frame_depth, pose: _abi.Pose, ingest_pose=None, seed=0, frame_idx=0,
              reduce_grads=None):

@@ -1,0 +1,158 @@
+"""GPU parity of the (e) keyframe global optimisation step: K9 top-40 % colour-error pixel
+selection (bit-exact vs oracle/classify.topk_error_mask on the same render), the masked backward over
+ALL Gaussians summed over keyframe views (the A5 gradient contract vs the oracle's autograd), and
+the Adam step with position learning rate 0 (positions bit-identical) and the other rates x 0.1."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import classify as OC
+from oracle import loss as OL
+from oracle import optim as OO
+from synth import CONFIGS, make_frame, make_pose, make_scene
+from tests.gpu_common import cam_dict, device_map
+from tests.test_gpu_backward import _compare_grads
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def api():
+    from paper_2404_19706_b200 import build as B
+    B.build()
+    import paper_2404_19706_b200 as P
+    return P
+
+
+def _mask_of(rb):
+    return rb.active_mask().cpu().numpy()
+
+
+@pytest.mark.parametrize("name,ratio", [("T2", 0.4), ("C1", 0.4), ("C1", 1.0), ("C1", 0.0)])
+def test_topk_bitexact(api, name, ratio):
+    from paper_2404_19706_b200 import mapping as M
+    cfg = CONFIGS[name]
+    scene = make_scene(cfg)
+    R, t = make_pose(cfg)
+    col, dep = make_frame(cfg, (R, t))
+    gm = device_map(scene)
+    cam = api.camera_of(cfg)
+    pose = api.make_pose(R, t)
+    eng = api.MappingEngine(gm, cam)
+    eng.ingest(torch.as_tensor(col, device="cuda"), torch.as_tensor(dep, device="cuda"), pose)
+    rb = api.RenderBuffers(cam)
+    ws = torch.empty(M.topk_workspace_size(cam), dtype=torch.uint8, device="cuda")
+    api.topk_error_mask(eng.full, torch.as_tensor(col, device="cuda"), cam, ratio, rb, ws)
+    torch.cuda.synchronize()
+    m_o, K = OC.topk_error_mask(eng.full.color.cpu().numpy(), col, ratio)
+    np.testing.assert_array_equal(_mask_of(rb), m_o)
+    c = rb.counts.cpu().numpy()
+    assert c[1] == K == c[2]
+    tiles = np.nonzero(rb.tile_keep.cpu().numpy())[0]
+    assert c[0] == len(tiles) and sorted(rb.tile_list[: c[0]].cpu().numpy().tolist()) == tiles.tolist()
+
+
+def test_topk_ties_by_index(api):
+    # every pixel has the same error: exactly the first K pixels in row-major order
+    from paper_2404_19706_b200 import mapping as M
+    H, W = 37, 53
+    cam = api.make_camera(50, 50, 26, 18, W, H)
+    rb = api.RenderBuffers(cam)
+    rb.color.fill_(0.5)
+    tgt = torch.full((3, H, W), 0.25, device="cuda")
+    ws = torch.empty(M.topk_workspace_size(cam), dtype=torch.uint8, device="cuda")
+    api.topk_error_mask(rb, tgt, cam, 0.4, rb, ws)
+    torch.cuda.synchronize()
+    K = int(np.floor(0.4 * H * W + 0.5))
+    m = _mask_of(rb).ravel()
+    assert m[:K].all() and not m[K:].any()
+
+
+def test_global_step_parity(api):
+    cfg = CONFIGS["C1"]
+    scene = make_scene(cfg)
+    cam_d = cam_dict(cfg)
+    views = []
+    for v in (None, 1):
+        R, t = make_pose(cfg, view=v)
+        col, dep = make_frame(cfg, (R, t))
+        views.append((R, t, col, dep))
+    gm = device_map(scene)
+    cam = api.camera_of(cfg)
+    eng = api.MappingEngine(gm, cam)
+    dev = [(torch.as_tensor(c, device="cuda"), torch.as_tensor(d, device="cuda"), api.make_pose(R, t))
+           for (R, t, c, d) in views]
+    # per-view calls (weights / 1): the accumulated gradient is the sum of the views' gradients
+    masks = []
+    for v in dev:
+        eng.global_backward([v])
+        torch.cuda.synchronize()
+        masks.append(_mask_of(eng.g_rb))
+    gid = eng.g_gid.cpu().numpy()
+    assert len(gid) == scene["pos"].shape[0]                    # every Gaussian is optimised
+    o = 0.0
+    for (R, t, col, dep), act in zip(views, masks):
+        assert act.sum() > 100
+        o = o + OL.iteration_grads(scene, R, t, cam_d, col, dep, act, gid)["grad"]
+    g = eng.g_grad[: len(gid)].cpu().numpy().astype(np.float64)
+    bad = _compare_grads(g, o)
+    assert not bad, bad
+    # the Adam step: positions untouched, the rest moved like the oracle's step with rates x 0.1
+    pos0 = gm.pos.cpu().numpy().copy()
+    K = (scene["sh_degree"] + 1) ** 2
+    theta = np.concatenate([scene["pos"][gid], scene["log_scale"][gid], scene["rot"][gid],
+                            scene["sh"][gid].reshape(len(gid), -1)], 1).astype(np.float64)
+    hp = eng.hp
+    lr = OO.lr_vector(K, 0.0, 0.1 * hp.lr_sh0, 0.1 * hp.lr_shrest, 0.1 * hp.lr_scale, 0.1 * hp.lr_rot)
+    transparent = (scene["flags"][gid] & 1) != 0
+    z = np.zeros_like(theta)
+    th2, _, _, _, gtot = OO.unstable_step(theta, o, z, z.copy(), theta[:, :10].copy(), transparent, 1000.0, lr, 1,
+                                          np.zeros(len(gid), np.int64))
+    eng._global_state()
+    from paper_2404_19706_b200 import _abi
+    ghp = _abi.HParams(0.0, hp.lr_sh0 * 0.1, hp.lr_shrest * 0.1, hp.lr_scale * 0.1, hp.lr_rot * 0.1, hp.beta1,
+                       hp.beta2, hp.eps)
+    g_t = eng.g_gid.long()
+    init = torch.cat([gm.pos[g_t], gm.log_scale[g_t], gm.rot[g_t]], 1).contiguous()
+    eng.g_m.zero_(); eng.g_v.zero_()
+    api.adam_step_unstable(gm, eng.g_gid, eng.g_grad, eng.g_m, eng.g_v, init, eng.g_ntr, 1000.0, ghp, 1, eng.eta)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(gm.pos.cpu().numpy(), pos0)  # "we do not update the position"
+    new = np.concatenate([gm.pos.cpu().numpy()[gid], gm.log_scale.cpu().numpy()[gid], gm.rot.cpu().numpy()[gid],
+                          gm.sh.cpu().numpy()[gid].reshape(len(gid), -1)], 1)
+    sel = np.abs(gtot) > 1e-3 * np.abs(gtot).max(0, keepdims=True)
+    sel[:, :3] = False
+    assert sel.sum() > 100
+    np.testing.assert_allclose(new[sel], th2[sel], rtol=0, atol=2e-7)
+
+
+def test_global_step_runs_and_keeps_positions(api):
+    cfg = CONFIGS["T2"]
+    scene = make_scene(cfg)
+    gm = device_map(scene)
+    eng = api.MappingEngine(gm, api.camera_of(cfg))
+    views = []
+    for v in (None, 1, 2, 3):
+        R, t = make_pose(cfg, view=v)
+        c, d = make_frame(cfg, (R, t))
+        views.append((torch.as_tensor(c, device="cuda"), torch.as_tensor(d, device="cuda"), api.make_pose(R, t)))
+    pos0 = gm.pos.clone()
+    sh0 = gm.sh.clone()
+    loss = eng.global_step(views).cpu().numpy()
+    torch.cuda.synchronize()
+    assert np.isfinite(loss).all()
+    assert torch.equal(gm.pos, pos0) and not torch.equal(gm.sh, sh0)
+
+
+def test_global_slots_exclude_removed(api):
+    cfg = CONFIGS["C1"]
+    scene = make_scene(cfg)
+    scene["flags"] = scene["flags"].copy()
+    scene["flags"][::41] |= 4
+    gm = device_map(scene)
+    eng = api.MappingEngine(gm, api.camera_of(cfg))
+    eng._global_state()
+    gid = eng.g_gid.cpu().numpy()
+    np.testing.assert_array_equal(gid, np.nonzero((scene["flags"] & 4) == 0)[0])
+    slot = eng.g_slot.cpu().numpy()
+    assert (slot[::41] == -1).all() and (slot[gid] == np.arange(len(gid))).all()

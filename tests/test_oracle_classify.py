@@ -66,3 +66,23 @@ def test_samples_are_row_major_and_in_masks():
     assert ((cls.ravel()[pix] & 3) > 0).all()
     assert cnt[0] == ((cls & 3) == 1).sum() and cnt[1] == ((cls & 3) == 2).sum()
     assert cnt[2] + cnt[3] == len(s)
+
+
+def test_topk_error_mask_pins():
+    from oracle.classify import topk_error_mask
+    # all pixels equal error -> exactly 40 %, the first pixels in row-major order
+    ch = np.full((3, 10, 10), 0.5, np.float32)
+    c = np.full((3, 10, 10), 0.25, np.float32)
+    m, K = topk_error_mask(ch, c)
+    assert K == 40 and m.sum() == 40 and m.ravel()[:40].all() and not m.ravel()[40:].any()
+    # distinct errors: exactly the K largest
+    rng = np.random.default_rng(0)
+    ch = rng.uniform(0, 1, (3, 7, 9)).astype(np.float32)
+    c = rng.uniform(0, 1, (3, 7, 9)).astype(np.float32)
+    m, K = topk_error_mask(ch, c, 0.4)
+    err = (np.abs(ch - c).sum(0) / 3).ravel()
+    assert K == round(0.4 * 63) == 25
+    thr = np.sort(err)[::-1][K - 1]
+    assert (err[m.ravel()] >= thr - 1e-7).all() and (err[~m.ravel()] <= thr + 1e-7).all() and m.sum() == K
+    # ratio 1 -> everything, ratio 0 -> nothing
+    assert topk_error_mask(ch, c, 1.0)[0].all() and not topk_error_mask(ch, c, 0.0)[0].any()

@@ -148,3 +148,27 @@ def test_rect_contains_support_and_tiles():
             assert x0 >= xs.min() - 2 and x1 <= xs.max() + 2
     assert (pr["tiles_touched"] == (pr["tile_rect"][:, 2] - pr["tile_rect"][:, 0] + 1)
             * (pr["tile_rect"][:, 3] - pr["tile_rect"][:, 1] + 1) * (pr["tiles_touched"] > 0)).all()
+
+
+def test_removed_gaussians_are_culled():
+    """R29: flags bit2 (removed) is absorbing and culled by A1 (pinned against the same scene with the
+    removed rows deleted: the remaining rows are unchanged)."""
+    import numpy as np
+    import torch
+    from oracle import projection as P
+    from synth import CONFIGS, make_pose, make_scene
+    cfg = CONFIGS["C1"]
+    sc = make_scene(cfg)
+    R, t = make_pose(cfg)
+    sc["flags"] = sc["flags"].copy()
+    sc["flags"][::3] |= 4
+    with torch.no_grad():
+        pr = P.project(P.params_from_scene(sc), R, t, P.camera(cfg), sc["sh_degree"])
+    assert not pr["valid"][::3].any() and (pr["tiles_touched"][::3] == 0).all()
+    keep = np.ones(len(sc["flags"]), bool)
+    keep[::3] = False
+    sub = {k: (v[keep] if isinstance(v, np.ndarray) and v.shape[:1] == keep.shape else v) for k, v in sc.items()}
+    with torch.no_grad():
+        ps = P.project(P.params_from_scene(sub), R, t, P.camera(cfg), sc["sh_degree"])
+    np.testing.assert_array_equal(pr["valid"][keep], ps["valid"])
+    np.testing.assert_array_equal(pr["rect"][keep], ps["rect"])
