@@ -29,3 +29,14 @@ def allreduce_grads(grad: torch.Tensor, group=None) -> torch.Tensor:
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
         dist.all_reduce(grad, op=dist.ReduceOp.SUM, group=group)
     return grad
+
+
+def global_step_distributed(eng, views, group=None, ratio=0.4, lr_scale=0.1):
+    """(e) the keyframe batch over ranks: this rank's contiguous block of `views` (every rank passes
+    the same full list), the batch-mean loss weights (1 / len(views)), one gradient all-reduce, then
+    the identical Adam step on every rank (the parameters stay replicated)."""
+    rank = dist.get_rank(group) if dist.is_available() and dist.is_initialized() else 0
+    world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+    mine = [views[v] for v in view_partition(len(views), world, rank)]
+    return eng.global_step(mine, ratio=ratio, lr_scale=lr_scale, n_total=len(views),
+                           reduce_grads=lambda g: allreduce_grads(g, group))

@@ -755,13 +755,14 @@ class MappingEngine:
             self.g_loss = torch.zeros(4, dtype=torch.float32, device=self.device)
             self._g_n, self._g_flags_sum = n, int(self.gm.flags.sum())
 
-    def global_backward(self, views, ratio=0.4, stream=None):
+    def global_backward(self, views, ratio=0.4, stream=None, n_total=None):
         """(e) P:284, per keyframe view (colour, depth, pose): FULL render (A1, A2, A3/A4), its top
         `ratio` colour-error pixels (K9), the masked backward over ALL non-removed Gaussians with the
         loss weights divided by the number of views (the batch loss is the mean over the views),
         accumulated into g_grad.  Multi-GPU: every rank calls this on its share of the views."""
         self._global_state()
-        w = tuple(x / max(1, len(views)) for x in self.weights[:2]) + (self.weights[2],)
+        nv = n_total if n_total is not None else len(views)   # multi-GPU: the views of ALL ranks
+        w = tuple(x / max(1, nv) for x in self.weights[:2]) + (self.weights[2],)
         for (c, d, pose) in views:
             project_gaussians(self.gm, pose, self.cam, self.proj, stream)
             bin_and_sort(self.proj, self.gm.n, self.cam, None, self.bins, self.ws_bin, stream)
@@ -771,12 +772,12 @@ class MappingEngine:
             render_backward_masked(self.gm, self.proj, self.bins, pose, self.cam, self.g_rb, c, d, w, self.g_slot,
                                    self.g_gid, self.g_grad, self.g_loss, self.g_ws_bwd, stream)
 
-    def global_step(self, views, ratio=0.4, lr_scale=0.1, reduce_grads=None, stream=None):
+    def global_step(self, views, ratio=0.4, lr_scale=0.1, reduce_grads=None, stream=None, n_total=None):
         """(e) one global optimisation step: global_backward over `views`, the gradient sum
         over ranks (`reduce_grads(g_grad)`, multi-GPU), then one Adam step of every non-removed
         Gaussian with the position learning rate 0 and the others x lr_scale (reading R37: fresh
         moments per global step; L_reg anchors the transparent geometry at its pre-step values)."""
-        self.global_backward(views, ratio, stream)
+        self.global_backward(views, ratio, stream, n_total)
         if reduce_grads is not None:
             reduce_grads(self.g_grad)
         hp = self.hp
