@@ -201,7 +201,7 @@ def main():
     # each rank optimises the shared map from its own keyframe view (rank 0 = the primary view)
     R, t = make_pose(cfg) if rank == 0 else make_pose(cfg, view=rank)
     col_h, dep_h = make_frame(cfg, (R, t))
-    gm = P.GaussianMap.from_arrays(scene, capacity=cfg.n + 1 + cfg.width * cfg.height // 4)  # room for f2 rows
+    gm = P.GaussianMap.from_arrays(scene, capacity=cfg.n + 1 + cfg.width * cfg.height // 2)  # room for f2 rows
     cam = P.camera_of(cfg)
     pose = P.make_pose(R, t)
     eng = P.MappingEngine(gm, cam, capacity=4 * cfg.n)
@@ -510,17 +510,19 @@ def main():
         torch.cuda.synchronize()
         w0, w1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         n_before = gm.n
-        t_host = time.perf_counter()
-        w0.record(stream)
-        eng.map_window(frames, iterations=50, seed=4, first_frame_idx=16)
-        w1.record(stream)
-        torch.cuda.synchronize()
-        t_host = (time.perf_counter() - t_host) * 1e3
-        t_win = w0.elapsed_time(w1)
-        window = {"frames": len(frames), "iterations": 50, "ms": round(t_win, 3), "host_ms": round(t_host, 3),
-                  "mapping_iters_per_s": round(50 * 1e3 / t_win, 1), "gaussians_added": gm.n - n_before,
+        t_wins = []
+        for rep in range(3):   # the median of three windows (the eager window has rare host outliers)
+            w0.record(stream)
+            eng.map_window(frames, iterations=50, seed=4 + rep, first_frame_idx=16 + 6 * rep)
+            w1.record(stream)
+            torch.cuda.synchronize()
+            t_wins.append(w0.elapsed_time(w1))
+        t_win = statistics.median(t_wins)
+        window = {"frames": len(frames), "iterations": 50, "ms": round(t_win, 3),
+                  "ms_each": [round(x, 3) for x in t_wins],
+                  "mapping_iters_per_s": round(50 * 1e3 / t_win, 1), "gaussians_added": (gm.n - n_before) // 3,
                   "slots": int(eng.gid_of_slot.numel()),
-                  "note": "second window of a smooth 6-frame path: 6 ingests + insertions (host syncs), a new slot "
+                  "note": "median of windows 2-4 of a smooth 6-frame path: 6 ingests + insertions (host syncs), a new slot "
                           "set, 50 cached iterations on sampled window frames, fusion + states; eager calls, "
                           "span on the device clock; the inserted unstable Gaussians enlarge the masked work"}
 
