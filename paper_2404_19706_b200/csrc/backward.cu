@@ -174,7 +174,11 @@ __global__ void __launch_bounds__(32 * (kBwdWarps + 1)) k_render_bwd(const BwdAr
   const uint32_t rec0 = pin(smem_u32(&r.rec[0][0][0])), slot0 = pin(smem_u32(&sm.slot[0][0]));
   const uint32_t gid0 = pin(smem_u32(&r.gid[0][0]));
   const int plane = (int)pin((uint32_t)lane);
-  float T = 1.f, ar = 0.f, ag = 0.f, ab = 0.f;
+  // dL/df_i = sum_c gC_c (c_i,c T_i - S_i,c / (1 - f_i)), S_i = C^ - prefix_i, folded into scalars:
+  // G_i = sum_c gC_c c_i,c, A = sum_c gC_c prefix_c (one running sum), K0 = sum_c gC_c C^_c, so
+  // dL/df_i = T_i G_i - (K0 - A) / (1 - f_i)
+  const float K0 = __fmaf_rn(gCb, Cb, __fmaf_rn(gCg, Cg, gCr * Cr));
+  float T = 1.f, A = 0.f;
   bool wdone = __all_sync(0xffffffffu, done);
   if (wdone && lane == 0) atomicSub(&r.alive, 1);
   for (int b = 0; b < nb; ++b) {
@@ -212,17 +216,15 @@ __global__ void __launch_bounds__(32 * (kBwdWarps + 1)) k_render_bwd(const BwdAr
           done = done || term;
           ok = ok && !term;
           const float wgt = ok ? __fmul_rn(e.f, T) : 0.f;
-          ar = __fmaf_rn(r2.x, wgt, ar);
-          ag = __fmaf_rn(r2.y, wgt, ag);
-          ab = __fmaf_rn(r2.z, wgt, ab);
+          const float G = __fmaf_rn(gCb, r2.z, __fmaf_rn(gCg, r2.y, gCr * r2.x));
+          A = __fmaf_rn(G, wgt, A);
           const uint32_t okm = __ballot_sync(0xffffffffu, ok);
           if (slot >= 0 && okm) {
             float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
             if (ok) {
               // S_i = sum_{j>i} c_j f_j T_j = C^ - prefix_i ;  dC/df_i = c_i T_i - S_i / (1 - f_i)
               const float inv1mf = __fdividef(1.f, 1.f - e.f);  // 1 - f >= 0.01
-              const float dLdf = gCr * (r2.x * T - (Cr - ar) * inv1mf) + gCg * (r2.y * T - (Cg - ag) * inv1mf) +
-                                 gCb * (r2.z * T - (Cb - ab) * inv1mf);
+              const float dLdf = T * G - (K0 - A) * inv1mf;
               // f = alpha e^power; the 0.99 cap passes no gradient when active (R17)
               const float dLdp = (e.f < kFMax) ? dLdf * e.f : 0.f;
               // power = p2 / log2(e): d power / d dx = (2 A' dx + B' dy) / log2(e) = -(A dx + B dy)
