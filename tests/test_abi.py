@@ -88,3 +88,30 @@ def test_cache_entry_points_validate_on_host(L):
                                       None, 0, None) == 1
     a = mapping.bin_cached_workspace_size(1000, cam, 1 << 16)
     assert a > mapping.bin_workspace_size(1000, cam, 1 << 16)
+
+
+def test_next_row_entry_points_validate_on_host(L):
+    """f2 / f4 / decode / (e) / f3-split calls reject missing or malformed arguments before any launch."""
+    from paper_2404_19706_b200 import _abi, mapping
+    cam = mapping.make_camera(500, 500, 320, 240, 640, 480)
+    pose = mapping.make_pose([[1, 0, 0], [0, 1, 0], [0, 0, 1]], [0, 0, 0])
+    m = _abi.MapRW(None, None, None, None, None, None, None, None, None, 10, 5, 3)   # capacity < n
+    ip = mapping.insert_params(0)
+    fr = _abi.Frame(None, None)
+    assert L.rtgs_add_gaussians(C.byref(m), None, 0, None, C.byref(fr), C.byref(pose), C.byref(cam), C.byref(ip),
+                                None, None, 0, None) == 1
+    p = mapping.icp_params()
+    p.levels = 7                                                                   # > 4 levels
+    assert L.rtgs_icp_track(None, None, None, C.byref(pose), C.byref(cam), C.byref(p), None, None, None, 0, None) == 1
+    assert L.rtgs_decode_rgbd(None, None, 64, 48, 0.0, None, None, None) == 1    # scale must be > 0
+    assert L.rtgs_decode_rgbd(None, None, 0, 0, 5000.0, None, None, None) == 0   # empty frame: nothing to do
+    out = _abi.RenderOut()
+    assert L.rtgs_topk_error_mask(None, None, C.byref(cam), 0.4, C.byref(out), None, 0, None) == 1
+    assert L.rtgs_topk_error_mask(None, None, C.byref(cam), 1.5, C.byref(out), None, 0, None) == 1
+    pr = _abi.Projected(None, None, None, None)
+    assert L.rtgs_coverage_subset(C.byref(pr), 0, C.byref(cam), C.byref(out), 1 << 16, None, 0, None) == 1
+    b = _abi.Bins(None, None, None, 0)
+    assert L.rtgs_merge_cached(C.byref(pr), C.byref(b), C.byref(pr), None, 0, C.byref(cam), C.byref(out), C.byref(b),
+                               None, 0, None) == 1
+    assert mapping.insert_workspace_size(1000, 64) > 0 and mapping.icp_workspace_size(cam, 3) > 0
+    assert mapping.topk_workspace_size(cam) > 0
