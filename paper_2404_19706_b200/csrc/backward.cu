@@ -223,7 +223,8 @@ __global__ void __launch_bounds__(32 * (kBwdWarps + 1)) k_render_bwd(const BwdAr
             float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
             if (ok) {
               // S_i = sum_{j>i} c_j f_j T_j = C^ - prefix_i ;  dC/df_i = c_i T_i - S_i / (1 - f_i)
-              const float inv1mf = __fdividef(1.f, 1.f - e.f);  // 1 - f >= 0.01
+              float inv1mf;  // 1 - f >= 0.01: the approximate reciprocal needs no range fix-up
+              asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv1mf) : "f"(1.f - e.f));
               const float dLdf = T * G - (K0 - A) * inv1mf;
               // f = alpha e^power; the 0.99 cap passes no gradient when active (R17)
               const float dLdp = (e.f < kFMax) ? dLdf * e.f : 0.f;
