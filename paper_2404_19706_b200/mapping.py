@@ -31,7 +31,13 @@ FLAG_STABLE = 2
 
 
 def _p(t: torch.Tensor | None):
-    return None if t is None else C.c_void_p(t.data_ptr())
+    if t is None:
+        return None
+    ptr = t.data_ptr()
+    if ptr == 0 and t.untyped_storage().nbytes() > 0:
+        # an empty view of an allocated store (a map with n = 0): torch reports 0, the store is real
+        ptr = t.untyped_storage().data_ptr() + t.storage_offset() * t.element_size()
+    return C.c_void_p(ptr)
 
 
 def _stream(stream=None):

@@ -52,3 +52,30 @@ def test_window_cached_equals_uncached():
         assert np.abs(a - b).max() <= 1e-4 * max(1.0, np.abs(b).max()), k
     np.testing.assert_array_equal(g1.flags.cpu().numpy(), g0.flags.cpu().numpy())
     np.testing.assert_array_equal(e1.eta.cpu().numpy(), e0.eta.cpu().numpy())
+
+
+def test_mapping_from_an_empty_map():
+    """SLAM starts from nothing: the first frame is all M_s (T^ = 1 > delta_T), its 5 % samples are
+    inserted with the fallback scale (no neighbours yet), and the window optimises them."""
+    from paper_2404_19706_b200 import build as B
+    B.build()
+    import paper_2404_19706_b200 as P
+    from synth import trajectory_pose
+    cfg = CONFIGS["T2"]
+    full = make_scene(cfg)
+    empty = {k: (v[:0] if isinstance(v, np.ndarray) and v.ndim >= 1 and v.shape[0] == full["pos"].shape[0] else v)
+             for k, v in full.items()}
+    gm = P.GaussianMap.from_arrays(empty, capacity=40000)
+    eng = P.MappingEngine(gm, P.camera_of(cfg), cache_frames=3, capacity=1 << 20)
+    frames = []
+    for k in range(3):
+        R, t = trajectory_pose(cfg, k)
+        c, d = make_frame(cfg, (R, t))
+        frames.append((torch.as_tensor(c, device="cuda"), torch.as_tensor(d, device="cuda"), P.make_pose(R, t)))
+    assert gm.n == 0
+    loss = eng.map_window(frames, iterations=10, seed=1).cpu().numpy()
+    torch.cuda.synchronize()
+    assert gm.n > 1000                                   # ~5 % of the valid pixels of three frames
+    assert np.isfinite(loss).all() and loss[0] > 0
+    s = torch.exp(gm.log_scale).cpu().numpy()
+    assert np.isfinite(s).all() and (s > 0).all()
