@@ -102,6 +102,20 @@ class GaussianMap:
         for k in _MAP_FIELDS:
             setattr(self, k, self.store[k][:n])
 
+    def reserve(self, capacity: int):
+        """Grow the storage to `capacity` rows (a device copy of the live rows; views re-sliced)."""
+        if capacity <= self.capacity:
+            return
+        n = self.n
+        store = {}
+        for k in _MAP_FIELDS:
+            old = self.store[k] if self.store is not None else getattr(self, k)
+            t = torch.zeros((capacity,) + tuple(old.shape[1:]), dtype=old.dtype, device=old.device)
+            t[:n].copy_(old[:n])
+            store[k] = t
+        self.store = store
+        self.resize(n)
+
     def c_struct(self) -> _abi.Gaussians:
         return _abi.Gaussians(_p(self.pos), _p(self.log_scale), _p(self.rot), _p(self.opacity), _p(self.sh),
                               _p(self.flags), self.n, self.sh_degree)
@@ -521,10 +535,45 @@ class MappingEngine:
         self.err_count = self._state_store["err_count"][:n]  # e_i
         self.t_created = self._state_store["t_created"][:n]  # t_i
 
-    def insert(self, frame_color, frame_depth, pose: _abi.Pose, frame_idx: int, stream=None, sync=True):
+    def reserve(self, capacity: int):
+        """Grow the map storage and every per-Gaussian buffer to `capacity` rows.  Live rows and the
+        per-Gaussian state are kept; the f3 frame caches are dropped (re-ingest to rebuild them) and
+        the window slots are rebuilt (Adam state reset, R19)."""
+        if capacity <= self.gm.capacity:
+            return
+        torch.cuda.synchronize(self.device)
+        self.gm.reserve(capacity)
+        for k, v in list(self._state_store.items()):
+            t = torch.zeros(capacity, dtype=v.dtype, device=self.device)
+            t[: v.numel()].copy_(v)
+            self._state_store[k] = t
+        self._view_state()
+        n, cam = capacity, self.cam
+        self.proj = ProjectedBuffers(n, self.device)
+        self.proj_full = ProjectedBuffers(n, self.device)
+        self.ws_bin = torch.empty(bin_workspace_size(n, cam, self.capacity), dtype=torch.uint8, device=self.device)
+        self.ws_bin_full = torch.empty(bin_workspace_size(n, cam, self.capacity), dtype=torch.uint8,
+                                       device=self.device)
+        self.ws_state = torch.empty(state_workspace_size(n), dtype=torch.uint8, device=self.device)
+        self.ws_insert = torch.empty(insert_workspace_size(n, self.samples.numel()), dtype=torch.uint8,
+                                     device=self.device)
+        self._fc = [_FrameCache(self.proj_full, self._fc[0].cache)]
+        self._fc_clock = 0
+        self.reset_window()
+
+    def insert(self, frame_color, frame_depth, pose: _abi.Pose, frame_idx: int, stream=None, sync=True,
+               grow: bool = True):
         """NEXT f2 after an ingest of the same frame: append the Gaussians of its A7 samples
         (Eq.11).  With sync=True the new count is read back and the map / state views
-        grow; call reset_window() before optimising so the new (unstable) Gaussians get slots."""
+        grow; call reset_window() before optimising so the new (unstable) Gaussians get slots.
+        With sync and grow, the storage is first enlarged (reserve, x1.5) when the frame's samples
+        may not fit; otherwise rows past the capacity are dropped (counted in result[3])."""
+        if sync and grow:
+            (torch.cuda.current_stream() if stream is None else stream).synchronize()
+            want = self.gm.n + min(int(self.add_counts[2].item()) + int(self.add_counts[3].item()),
+                                   self.samples.numel())
+            if want > self.gm.capacity:
+                self.reserve(max(want, self.gm.capacity * 3 // 2))
         add_gaussians(self.gm, self._state_store["eta"], self._state_store["err_count"],
                       self._state_store["t_created"], self.samples, self.add_counts, frame_color, frame_depth, pose,
                       self.cam, insert_params(frame_idx), self.insert_result, self.ws_insert, stream)
