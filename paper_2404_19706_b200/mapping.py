@@ -561,6 +561,23 @@ class MappingEngine:
         self._fc_clock = 0
         self.reset_window()
 
+    def reserve_instances(self, capacity: int):
+        """Grow the (Gaussian, tile) instance capacity of every binning buffer to `capacity`; the f3
+        frame caches are dropped (re-ingest to rebuild them)."""
+        if capacity <= self.capacity:
+            return
+        torch.cuda.synchronize(self.device)
+        self.capacity = int(capacity)
+        n, cam = self.gm.capacity, self.cam
+        self.bins = BinBuffers(cam, self.capacity, self.device)
+        self.bins_full = BinBuffers(cam, self.capacity, self.device)
+        self.ws_bin = torch.empty(bin_workspace_size(n, cam, self.capacity), dtype=torch.uint8, device=self.device)
+        self.ws_bin_full = torch.empty(bin_workspace_size(n, cam, self.capacity), dtype=torch.uint8,
+                                       device=self.device)
+        self._fc = [_FrameCache(self.proj_full, BinBuffers(cam, self.capacity, self.device))]
+        self._fc_clock = 0
+        self.reset_window()
+
     def insert(self, frame_color, frame_depth, pose: _abi.Pose, frame_idx: int, stream=None, sync=True,
                grow: bool = True):
         """NEXT f2 after an ingest of the same frame: append the Gaussians of its A7 samples
@@ -767,6 +784,10 @@ class MappingEngine:
         rng = np.random.default_rng(seed)
         for i, (c, d, pose) in enumerate(frames):
             self.ingest(c, d, pose, seed=seed, frame_idx=first_frame_idx + i)
+            need = int(self.bins_full.n_instances.item())
+            if need > self.capacity:            # the FULL lists were truncated: grow and redo the frame
+                self.reserve_instances(need * 5 // 4)
+                self.ingest(c, d, pose, seed=seed, frame_idx=first_frame_idx + i)
             if insert:
                 self.insert(c, d, pose, frame_idx=first_frame_idx + i)
         self.reset_window()

@@ -66,7 +66,7 @@ def test_mapping_from_an_empty_map():
     empty = {k: (v[:0] if isinstance(v, np.ndarray) and v.ndim >= 1 and v.shape[0] == full["pos"].shape[0] else v)
              for k, v in full.items()}
     gm = P.GaussianMap.from_arrays(empty, capacity=100)    # insert() grows the storage (reserve)
-    eng = P.MappingEngine(gm, P.camera_of(cfg), cache_frames=3, capacity=1 << 20)
+    eng = P.MappingEngine(gm, P.camera_of(cfg), cache_frames=3, capacity=1000)  # map_window grows it
     frames = []
     for k in range(3):
         R, t = trajectory_pose(cfg, k)
@@ -78,6 +78,7 @@ def test_mapping_from_an_empty_map():
     assert gm.n > 1000                                   # ~5 % of the valid pixels of three frames
     assert gm.capacity >= gm.n and eng.proj.rec.shape[0] >= gm.n and eng.eta.numel() == gm.n
     assert int(eng.insert_result[3].item()) == 0         # nothing dropped
+    assert eng.capacity > 1000 and int(eng.bins_full.n_instances.item()) <= eng.capacity
     assert np.isfinite(loss).all() and loss[0] > 0
     s = torch.exp(gm.log_scale).cpu().numpy()
     assert np.isfinite(s).all() and (s > 0).all()
