@@ -170,6 +170,7 @@ def main():
     ap.add_argument("--phases", action="store_true", help="print per-call timings to stderr")
     ap.add_argument("--no-graph", action="store_true", help="launch every step eagerly (no CUDA graph)")
     ap.add_argument("--no-cache", action="store_true", help="iteration without the f3 stable-projection cache")
+    ap.add_argument("--no-fuse-adam", action="store_true", help="separate A5 backward and A6 Adam calls")
     ap.add_argument("--no-restore", action="store_true", help="diagnostic: let the map drift between timed steps")
     ap.add_argument("--no-window", action="store_true", help="skip the supplementary mapping-window measurement")
     args = ap.parse_args()
@@ -206,6 +207,7 @@ def main():
     pose = P.make_pose(R, t)
     eng = P.MappingEngine(gm, cam, capacity=4 * cfg.n)
     eng.use_cache = not args.no_cache
+    eng.fused_adam = not args.no_fuse_adam
     col = torch.as_tensor(col_h, device="cuda")
     dep = torch.as_tensor(dep_h, device="cuda")
     stream = torch.cuda.current_stream()
@@ -331,8 +333,11 @@ def main():
             eng.proj_iter = eng.proj
         P.render_color_depth(gm, eng.proj_iter, eng.bins, pose, cam, P.RTGS_RENDER_MASKED, eng.out)
         mark("iter.render_masked")
-        eng.backward(col, dep, pose); mark("iter.backward")
-        eng.optimizer_step(); mark("iter.adam")
+        if eng.fused_adam:
+            eng.backward_adam(col, dep, pose); mark("iter.backward_adam")
+        else:
+            eng.backward(col, dep, pose); mark("iter.backward")
+            eng.optimizer_step(); mark("iter.adam")
         torch.cuda.synchronize()
         names = list(ev)
         for a, b in zip(names[:-1], names[1:]):

@@ -232,6 +232,26 @@ rtgs_status rtgs_adam_step_unstable(rtgs_params* params, const int32_t* gid_of_s
                                     const int32_t* step_device, uint32_t* eta, void* stream);
 
 /* ---------------------------------------------------------------------------------------------
+ * A5 + A6 fused — rtgs_backward_adam_unstable (same passages as the two calls above)
+ * Exactly rtgs_render_backward_masked into a zeroed gradient followed by rtgs_adam_step_unstable
+ * with w_reg = w->w_reg, for the case where one backward feeds one Adam step (a single view on one
+ * GPU): the slot gradient stays in shared memory of the chain-rule kernel, which applies the update
+ * (same float32 operations as the stand-alone Adam), so no grad buffer is read, written or zeroed.
+ * `params` must name the arrays of `g` (the parameters are updated in place, the map's other fields
+ * are read only).  Arguments otherwise as in the two calls; workspace = rtgs_backward_workspace_size.
+ * Views that accumulate gradients (the keyframe step (e)) or an all-reduce between backward and
+ * update (multi-GPU) use the two separate calls.
+ * ------------------------------------------------------------------------------------------- */
+rtgs_status rtgs_backward_adam_unstable(const rtgs_gaussians* g, const rtgs_projected* proj, const rtgs_bins* bins,
+                                        const rtgs_pose* pose, const rtgs_camera* cam, const rtgs_render_out* fwd,
+                                        const rtgs_frame* target, const rtgs_loss_weights* w,
+                                        const int32_t* slot_of_gid, const int32_t* gid_of_slot, int32_t n_slots,
+                                        rtgs_params* params, float* m, float* v, const float* init_geom,
+                                        int32_t n_transparent, const rtgs_hparams* hp, int32_t step,
+                                        const int32_t* step_device, uint32_t* eta, float* loss_out, void* workspace,
+                                        size_t workspace_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------------------------
  * A7 — rtgs_classify_and_add_pixels (O7; Eq.6, R21, R22, R24)
  * On a FULL render at the new frame's pose, in float32 with this exact operation order:
  *   valid = isfinite(D) && D > 0

@@ -96,6 +96,9 @@ EXPORTS = {
                                               P(Frame), P(LossWeights), vp, vp, C.c_int32, vp, vp, vp, C.c_size_t, vp]),
     "rtgs_adam_step_unstable": (C.c_int, [P(Params), vp, C.c_int32, vp, vp, vp, vp, vp, C.c_int32, C.c_float, P(HParams),
                                           C.c_int32, vp, vp, vp]),
+    "rtgs_backward_adam_unstable": (C.c_int, [P(Gaussians), P(Projected), P(Bins), P(Pose), P(Camera), P(RenderOut),
+                                              P(Frame), P(LossWeights), vp, vp, C.c_int32, P(Params), vp, vp, vp,
+                                              C.c_int32, P(HParams), C.c_int32, vp, vp, vp, vp, C.c_size_t, vp]),
     "rtgs_classify_workspace_size": (C.c_size_t, [P(Camera)]),
     "rtgs_classify_and_add_pixels": (C.c_int, [P(RenderOut), P(Frame), vp, P(Camera), P(AddParams), vp, vp, C.c_uint32,
                                                vp, vp, C.c_size_t, vp]),

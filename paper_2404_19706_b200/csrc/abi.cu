@@ -120,6 +120,36 @@ rtgs_status rtgs_render_backward_masked(const rtgs_gaussians* g, const rtgs_proj
                                 n_slots, grad, loss_out, workspace, S(stream)));
 }
 
+rtgs_status rtgs_backward_adam_unstable(const rtgs_gaussians* g, const rtgs_projected* proj, const rtgs_bins* bins,
+                                        const rtgs_pose* pose, const rtgs_camera* cam, const rtgs_render_out* fwd,
+                                        const rtgs_frame* target, const rtgs_loss_weights* w,
+                                        const int32_t* slot_of_gid, const int32_t* gid_of_slot, int32_t n_slots,
+                                        rtgs_params* params, float* m, float* v, const float* init_geom,
+                                        int32_t n_transparent, const rtgs_hparams* hp, int32_t step,
+                                        const int32_t* step_device, uint32_t* eta, float* loss_out, void* workspace,
+                                        size_t workspace_bytes, void* stream) {
+  if (!gauss_ok(g, false) || !proj_ok(proj, g ? g->n : 0) || !bins_ok(bins) || !pose_ok(pose) || !cam_ok(cam))
+    return RTGS_ERR_INVALID_ARG;
+  if (!fwd || !fwd->color || !fwd->depth || !fwd->index || !fwd->n_contrib || !fwd->active_bits ||
+      !fwd->tile_list || !fwd->counts)
+    return RTGS_ERR_INVALID_ARG;
+  if (!target || !target->color || !target->depth || !w || n_slots < 0 || !loss_out || !std::isfinite(w->w_reg))
+    return RTGS_ERR_INVALID_ARG;
+  if (!params || !hp || (step < 1 && !step_device) || n_transparent < 0) return RTGS_ERR_INVALID_ARG;
+  // the update is written through `params`, which must be the arrays the backward reads
+  if (params->pos != g->pos || params->log_scale != g->log_scale || params->rot != g->rot || params->sh != g->sh ||
+      params->sh_degree != g->sh_degree)
+    return RTGS_ERR_INVALID_ARG;
+  if (g->n > 0 && !slot_of_gid) return RTGS_ERR_INVALID_ARG;
+  if (n_slots > 0 && (!gid_of_slot || !g->flags || !m || !v || !eta || (n_transparent > 0 && !init_geom)))
+    return RTGS_ERR_INVALID_ARG;
+  if (bins->sub_rec && bins->sub_gid != gid_of_slot) return RTGS_ERR_INVALID_ARG;
+  if (!workspace || workspace_bytes < backward_workspace_size(n_slots) || !a16(workspace)) return RTGS_ERR_WORKSPACE;
+  return finish(launch_backward_adam(*g, *proj, *bins, make_pose(*pose), *cam, *fwd, *target, *w, slot_of_gid,
+                                     gid_of_slot, n_slots, *params, m, v, init_geom, n_transparent, *hp, step,
+                                     step_device, eta, loss_out, workspace, S(stream)));
+}
+
 rtgs_status rtgs_adam_step_unstable(rtgs_params* params, const int32_t* gid_of_slot, int32_t n_slots,
                                     const uint8_t* flags, float* grad, float* m, float* v, const float* init_geom,
                                     int32_t n_transparent, float w_reg, const rtgs_hparams* hp, int32_t step,

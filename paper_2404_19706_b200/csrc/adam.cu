@@ -6,6 +6,7 @@
 // component j is gathered by gid with branch-free address selects.  Per-slot "SH gradient != 0"
 // flags live in shared memory and give eta += 1 once per slot (R20).
 #include "common.cuh"
+#include "adam.cuh"
 #include "internal.h"
 
 namespace rtgs {
@@ -26,11 +27,7 @@ struct AdamArgs {
   float* m;
   float* v;
   const float* init_geom;
-  float reg_coef;  // 2 w_reg / (10 N_t)
-  float lr_pos, lr_sh0, lr_shrest, lr_scale, lr_rot;
-  float b1, omb1, b2, omb2, eps, bc1, bc2;
-  float log_b1, log_b2;        // for the device-step bias corrections 1 - beta^t = -expm1(t log beta)
-  const int32_t* step_device;  // when set, bias corrections are formed from the device step
+  AdamHP h;
   uint32_t* eta;
 };
 
@@ -42,13 +39,7 @@ __global__ void __launch_bounds__(kAdamThreads) k_adam(const AdamArgs a) {
   const int lane = threadIdx.x & 31, t = threadIdx.x & (kLanesPerSlot - 1);
   const int slot = blockIdx.x * kAdamSlots + (threadIdx.x >> 4);
   const bool live = slot < a.n_slots;
-  float bc1 = a.bc1, bc2 = a.bc2;
-  if (a.step_device) {
-    const float st = (float)*a.step_device;
-    bc1 = -expm1f(st * a.log_b1);
-    bc2 = -expm1f(st * a.log_b2);
-  }
-  const float ibc1 = 1.f / bc1, ibc2 = 1.f / bc2;
+  const AdamBC bc = adam_bias(a.h);
   bool nz = false;
   uint32_t eta0 = 0;
   size_t gid = 0;
@@ -80,17 +71,13 @@ __global__ void __launch_bounds__(kAdamThreads) k_adam(const AdamArgs a) {
     for (int it = 0; it < NIT; ++it) {
       const int j = t + it * kLanesPerSlot;
       if (j >= D) break;
-      const float lr = (it == 0 && j < 10) ? (j < 3 ? a.lr_pos : (j < 6 ? a.lr_scale : a.lr_rot))
-                                           : (j < 13 ? a.lr_sh0 : a.lr_shrest);
       float gg = g[it];
       if (j >= 10 && gg != 0.f) nz = true;
-      if (it == 0 && j < 10 && transparent) gg += a.reg_coef * (th[it] - th0);  // L_reg (R18)
-      const float mm = a.b1 * mo[it] + a.omb1 * gg;
-      const float vv = a.b2 * vo[it] + a.omb2 * gg * gg;
+      if (it == 0 && j < 10 && transparent) gg += a.h.reg_coef * (th[it] - th0);  // L_reg (R18)
+      float mm = mo[it], vv = vo[it];
+      *p[it] = adam_one(a.h, bc, adam_lr(a.h, j), th[it], gg, mm, vv);
       a.m[row + j] = mm;
       a.v[row + j] = vv;
-      // theta -= lr m^ / (sqrt(v^) + eps)   (m = 0 whenever v = 0, so the quotient is 0 there)
-      *p[it] = th[it] - lr * __fdividef(mm * ibc1, sqrtf(vv * ibc2) + a.eps);
       a.grad[row + j] = 0.f;  // consumed
     }
   }
@@ -98,6 +85,22 @@ __global__ void __launch_bounds__(kAdamThreads) k_adam(const AdamArgs a) {
   const uint32_t vote = __ballot_sync(0xffffffffu, nz);
   const uint32_t half = (lane < 16) ? (vote & 0x0000FFFFu) : (vote & 0xFFFF0000u);
   if (live && t == 0 && half) a.eta[gid] = eta0 + 1u;
+}
+
+AdamHP make_adam_hp(const rtgs_hparams& hp, int step, const int32_t* step_device, int n_transparent, float w_reg) {
+  AdamHP h;
+  h.lr_pos = hp.lr_pos; h.lr_sh0 = hp.lr_sh0; h.lr_shrest = hp.lr_shrest; h.lr_scale = hp.lr_scale;
+  h.lr_rot = hp.lr_rot;
+  h.b1 = (float)hp.beta1; h.omb1 = (float)(1.0 - hp.beta1);
+  h.b2 = (float)hp.beta2; h.omb2 = (float)(1.0 - hp.beta2);
+  h.eps = (float)hp.eps;
+  h.bc1 = (float)(1.0 - pow(hp.beta1, step));
+  h.bc2 = (float)(1.0 - pow(hp.beta2, step));
+  h.log_b1 = (float)log(hp.beta1);
+  h.log_b2 = (float)log(hp.beta2);
+  h.step_device = step_device;
+  h.reg_coef = n_transparent > 0 ? (float)(2.0 * w_reg / (10.0 * n_transparent)) : 0.f;
+  return h;
 }
 
 cudaError_t launch_adam(const rtgs_params& p, const int32_t* gid_of_slot, int n_slots, const uint8_t* flags,
@@ -109,16 +112,7 @@ cudaError_t launch_adam(const rtgs_params& p, const int32_t* gid_of_slot, int n_
   a.pos = p.pos; a.log_scale = p.log_scale; a.rot = p.rot; a.sh = p.sh;
   a.gid_of_slot = gid_of_slot; a.n_slots = n_slots; a.flags = flags;
   a.grad = grad; a.m = m; a.v = v; a.init_geom = init_geom;
-  a.reg_coef = n_transparent > 0 ? (float)(2.0 * w_reg / (10.0 * n_transparent)) : 0.f;
-  a.lr_pos = hp.lr_pos; a.lr_sh0 = hp.lr_sh0; a.lr_shrest = hp.lr_shrest; a.lr_scale = hp.lr_scale; a.lr_rot = hp.lr_rot;
-  a.b1 = (float)hp.beta1; a.omb1 = (float)(1.0 - hp.beta1);
-  a.b2 = (float)hp.beta2; a.omb2 = (float)(1.0 - hp.beta2);
-  a.eps = (float)hp.eps;
-  a.bc1 = (float)(1.0 - pow(hp.beta1, step));
-  a.bc2 = (float)(1.0 - pow(hp.beta2, step));
-  a.log_b1 = (float)log(hp.beta1);
-  a.log_b2 = (float)log(hp.beta2);
-  a.step_device = step_device;
+  a.h = make_adam_hp(hp, step, step_device, n_transparent, w_reg);
   a.eta = eta;
   const int blocks = (n_slots + kAdamSlots - 1) / kAdamSlots;
   switch ((p.sh_degree + 1) * (p.sh_degree + 1)) {

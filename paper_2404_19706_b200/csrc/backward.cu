@@ -12,6 +12,7 @@
 //   EWA / SH / disc plane to (pos, log_scale, rot, sh) (hand-derived; checked against the
 //   oracle's autograd in tests/test_gpu_backward.py).
 #include "common.cuh"
+#include "adam.cuh"
 #include "internal.h"
 #include "tilepipe.cuh"
 
@@ -292,6 +293,17 @@ struct PBArgs {
   float* loss_out;
   float w_c;
   const uint32_t* counts;
+  // fused A6 (ADAM variant only): the update replaces the grad read-modify-write
+  float* wpos;
+  float* wlog_scale;
+  float* wrot;
+  float* wsh;
+  const uint8_t* flags;
+  float* m;
+  float* v;
+  const float* init_geom;
+  uint32_t* eta;
+  AdamHP h;
 };
 
 // Y_k(d) and its gradient for ONE coefficient k (a compile-time constant after unrolling): the 3DGS
@@ -532,10 +544,11 @@ struct PBSmem {
   float sg[128 * kSG];
   float par[128 * 13];
   int gid[128];
+  uint8_t transparent[128];
   uint64_t bar;
 };
 
-template <int K>
+template <int K, bool ADAM>
 __global__ void __launch_bounds__(128) k_project_bwd(const PBArgs a) {
   using SM = PBSmem<K>;
   constexpr int D = SM::D, LD = SM::LD, SHF = SM::SHF, SHP = SM::SHP;
@@ -555,6 +568,7 @@ __global__ void __launch_bounds__(128) k_project_bwd(const PBArgs a) {
   }
   if (ns <= 0) return;
   if (tid < ns) sm.gid[tid] = a.gid_of_slot[s0 + tid];
+  if (ADAM && tid < ns) sm.transparent[tid] = a.flags[sm.gid[tid]] & 1u;
   if (tid == 0) {
     mbar_init(&sm.bar, 1);
     fence_mbar_init();
@@ -610,30 +624,92 @@ __global__ void __launch_bounds__(128) k_project_bwd(const PBArgs a) {
   if constexpr (SHF % 4 == 0) mbar_wait(&sm.bar, 0);
   if (tid < ns) project_bwd_slot<K>(a, sm.sg + tid * kSG, sm.par + tid * 13, sm.sh + tid * SHP, gout);
   __syncthreads();
-  float* G = a.grad + (size_t)s0 * D;
-  for (int e0 = tid; e0 < ns * D; e0 += 128 * U) {  // coalesced read-modify-write, 8 loads in flight
-    float g[U];
+  if constexpr (ADAM) {
+    // A6 on the staged rows (the same update as k_adam, adam.cuh): the slot gradient never leaves
+    // shared memory; m / v stream coalesced over the CTA's contiguous [ns x D] block, the new
+    // parameters go back into the staging and are written out below.
+    const AdamBC bc = adam_bias(a.h);
+    float* M = a.m + (size_t)s0 * D;
+    float* Vm = a.v + (size_t)s0 * D;
+    for (int e0 = tid; e0 < ns * D; e0 += 128 * U) {
+      float mo[U], vo[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int e = e0 + u * 128;
-      g[u] = e < ns * D ? G[e] : 0.f;
+      for (int u = 0; u < U; ++u) {
+        const int e = e0 + u * 128;
+        mo[u] = e < ns * D ? M[e] : 0.f;
+        vo[u] = e < ns * D ? Vm[e] : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int e = e0 + u * 128;
+        if (e < ns * D) {
+          const int ls = e / D, j = e - ls * D;
+          float gg = sm.out[ls * LD + j];
+          float* pth = j < 10 ? &sm.par[ls * 13 + j] : &sm.sh[ls * SHP + (j - 10)];
+          const float th = *pth;
+          if (j < 10 && sm.transparent[ls]) {  // L_reg (R18)
+            const float th0 = a.init_geom ? a.init_geom[(size_t)(s0 + ls) * 10 + j] : 0.f;
+            gg += a.h.reg_coef * (th - th0);
+          }
+          float mm = mo[u], vv = vo[u];
+          *pth = adam_one(a.h, bc, adam_lr(a.h, j), th, gg, mm, vv);
+          M[e] = mm;
+          Vm[e] = vv;
+        }
+      }
     }
+    __syncthreads();
+    for (int e = tid; e < ns * 10; e += 128) {
+      const int ls = e / 10, c = e - ls * 10;
+      const size_t g = (size_t)sm.gid[ls];
+      float* dst = c < 3 ? a.wpos + 3 * g + c : (c < 6 ? a.wlog_scale + 3 * g + (c - 3) : a.wrot + 4 * g + (c - 6));
+      *dst = sm.par[ls * 13 + c];
+    }
+    for (int e = tid; e < ns * SHF; e += 128) {
+      const int ls = e / SHF, j = e - ls * SHF;
+      a.wsh[(size_t)sm.gid[ls] * SHF + j] = sm.sh[ls * SHP + j];
+    }
+    if (tid < ns) {  // eta += 1 once per slot with a non-zero SH gradient (R20)
+      bool nz = false;
+#pragma unroll 8
+      for (int j = 0; j < SHF; ++j) nz |= sm.out[tid * LD + 10 + j] != 0.f;
+      if (nz) a.eta[sm.gid[tid]] += 1u;
+    }
+  } else {
+    float* G = a.grad + (size_t)s0 * D;
+    for (int e0 = tid; e0 < ns * D; e0 += 128 * U) {  // coalesced read-modify-write, 8 loads in flight
+      float g[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int e = e0 + u * 128;
-      if (e < ns * D) {
-        const int ls = e / D, j = e - ls * D;
-        G[e] = g[u] + sm.out[ls * LD + j];
+      for (int u = 0; u < U; ++u) {
+        const int e = e0 + u * 128;
+        g[u] = e < ns * D ? G[e] : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int e = e0 + u * 128;
+        if (e < ns * D) {
+          const int ls = e / D, j = e - ls * D;
+          G[e] = g[u] + sm.out[ls * LD + j];
+        }
       }
     }
   }
 }
 
-cudaError_t launch_backward(const rtgs_gaussians& g, const rtgs_projected& proj, const rtgs_bins& bins,
-                            const PoseF& pose, const rtgs_camera& cam, const rtgs_render_out& fwd,
-                            const rtgs_frame& target, const rtgs_loss_weights& w, const int32_t* slot_of_gid,
-                            const int32_t* gid_of_slot, int n_slots, float* grad, float* loss_out, void* ws,
-                            cudaStream_t s) {
+struct FusedAdam {  // the A6 operands of the fused variant
+  const rtgs_params* p;
+  float* m;
+  float* v;
+  const float* init_geom;
+  uint32_t* eta;
+  AdamHP h;
+};
+
+static cudaError_t enqueue_backward(const rtgs_gaussians& g, const rtgs_projected& proj, const rtgs_bins& bins,
+                                    const PoseF& pose, const rtgs_camera& cam, const rtgs_render_out& fwd,
+                                    const rtgs_frame& target, const rtgs_loss_weights& w, const int32_t* slot_of_gid,
+                                    const int32_t* gid_of_slot, int n_slots, float* grad, const FusedAdam* fz,
+                                    float* loss_out, void* ws, cudaStream_t s) {
   float* sgrad = static_cast<float*>(ws);
   float* acc = sgrad + (size_t)n_slots * kSG;
   cudaMemsetAsync(ws, 0, ((size_t)n_slots * kSG + 8) * sizeof(float), s);
@@ -680,22 +756,55 @@ cudaError_t launch_backward(const rtgs_gaussians& g, const rtgs_projected& proj,
   b.grad = grad;
   b.loss_out = loss_out;
   b.counts = fwd.counts;
+  if (fz) {
+    b.wpos = fz->p->pos; b.wlog_scale = fz->p->log_scale; b.wrot = fz->p->rot; b.wsh = fz->p->sh;
+    b.flags = g.flags;
+    b.m = fz->m; b.v = fz->v; b.init_geom = fz->init_geom; b.eta = fz->eta;
+    b.h = fz->h;
+  }
   const int nb = n_slots > 0 ? (n_slots + 127) / 128 : 1;
   static std::atomic<uint64_t> attr_mask{0};
   if (first_on_device(attr_mask)) {
-    cudaFuncSetAttribute(k_project_bwd<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PBSmem<1>));
-    cudaFuncSetAttribute(k_project_bwd<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PBSmem<4>));
-    cudaFuncSetAttribute(k_project_bwd<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PBSmem<9>));
-    cudaFuncSetAttribute(k_project_bwd<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PBSmem<16>));
+#define RTGS_PB_ATTR(KK)                                                                                   \
+  cudaFuncSetAttribute(k_project_bwd<KK, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,                \
+                       (int)sizeof(PBSmem<KK>));                                                          \
+  cudaFuncSetAttribute(k_project_bwd<KK, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PBSmem<KK>));
+    RTGS_PB_ATTR(1) RTGS_PB_ATTR(4) RTGS_PB_ATTR(9) RTGS_PB_ATTR(16)
+#undef RTGS_PB_ATTR
   }
+#define RTGS_PB_LAUNCH(KK)                                                                   \
+  if (fz) k_project_bwd<KK, true><<<nb, 128, sizeof(PBSmem<KK>), s>>>(b);                      \
+  else k_project_bwd<KK, false><<<nb, 128, sizeof(PBSmem<KK>), s>>>(b);
   switch (b.K) {
-    case 1: k_project_bwd<1><<<nb, 128, sizeof(PBSmem<1>), s>>>(b); break;
-    case 4: k_project_bwd<4><<<nb, 128, sizeof(PBSmem<4>), s>>>(b); break;
-    case 9: k_project_bwd<9><<<nb, 128, sizeof(PBSmem<9>), s>>>(b); break;
-    default: k_project_bwd<16><<<nb, 128, sizeof(PBSmem<16>), s>>>(b); break;
+    case 1: RTGS_PB_LAUNCH(1) break;
+    case 4: RTGS_PB_LAUNCH(4) break;
+    case 9: RTGS_PB_LAUNCH(9) break;
+    default: RTGS_PB_LAUNCH(16) break;
   }
+#undef RTGS_PB_LAUNCH
   note_launch();
   return cudaGetLastError();
+}
+
+cudaError_t launch_backward(const rtgs_gaussians& g, const rtgs_projected& proj, const rtgs_bins& bins,
+                            const PoseF& pose, const rtgs_camera& cam, const rtgs_render_out& fwd,
+                            const rtgs_frame& target, const rtgs_loss_weights& w, const int32_t* slot_of_gid,
+                            const int32_t* gid_of_slot, int n_slots, float* grad, float* loss_out, void* ws,
+                            cudaStream_t s) {
+  return enqueue_backward(g, proj, bins, pose, cam, fwd, target, w, slot_of_gid, gid_of_slot, n_slots, grad, nullptr,
+                          loss_out, ws, s);
+}
+
+cudaError_t launch_backward_adam(const rtgs_gaussians& g, const rtgs_projected& proj, const rtgs_bins& bins,
+                                 const PoseF& pose, const rtgs_camera& cam, const rtgs_render_out& fwd,
+                                 const rtgs_frame& target, const rtgs_loss_weights& w, const int32_t* slot_of_gid,
+                                 const int32_t* gid_of_slot, int n_slots, const rtgs_params& p, float* m, float* v,
+                                 const float* init_geom, int n_transparent, const rtgs_hparams& hp, int step,
+                                 const int32_t* step_device, uint32_t* eta, float* loss_out, void* ws,
+                                 cudaStream_t s) {
+  FusedAdam fz{&p, m, v, init_geom, eta, make_adam_hp(hp, step, step_device, n_transparent, w.w_reg)};
+  return enqueue_backward(g, proj, bins, pose, cam, fwd, target, w, slot_of_gid, gid_of_slot, n_slots, nullptr, &fz,
+                          loss_out, ws, s);
 }
 
 }  // namespace rtgs

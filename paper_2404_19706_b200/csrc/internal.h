@@ -66,6 +66,14 @@ cudaError_t launch_backward(const rtgs_gaussians& g, const rtgs_projected& proj,
                             const int32_t* gid_of_slot, int n_slots, float* grad, float* loss_out, void* ws,
                             cudaStream_t s);
 
+cudaError_t launch_backward_adam(const rtgs_gaussians& g, const rtgs_projected& proj, const rtgs_bins& bins,
+                                 const PoseF& pose, const rtgs_camera& cam, const rtgs_render_out& fwd,
+                                 const rtgs_frame& target, const rtgs_loss_weights& w, const int32_t* slot_of_gid,
+                                 const int32_t* gid_of_slot, int n_slots, const rtgs_params& p, float* m, float* v,
+                                 const float* init_geom, int n_transparent, const rtgs_hparams& hp, int step,
+                                 const int32_t* step_device, uint32_t* eta, float* loss_out, void* ws,
+                                 cudaStream_t s);
+
 cudaError_t launch_adam(const rtgs_params& p, const int32_t* gid_of_slot, int n_slots, const uint8_t* flags,
                         float* grad, float* m, float* v, const float* init_geom, int n_transparent, float w_reg,
                         const rtgs_hparams& hp, int step, const int32_t* step_device, uint32_t* eta,

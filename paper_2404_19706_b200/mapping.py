@@ -254,6 +254,30 @@ def adam_step_unstable(gm: GaussianMap, gid_of_slot: torch.Tensor, grad: torch.T
                                         int(step), _p(step_device), _p(eta), _stream(stream)), "rtgs_adam_step_unstable")
 
 
+def backward_adam_unstable(gm: GaussianMap, proj: ProjectedBuffers, bins: BinBuffers, pose: _abi.Pose,
+                           cam: _abi.Camera, fwd: RenderBuffers, target_color: torch.Tensor,
+                           target_depth: torch.Tensor, weights: tuple, slot_of_gid: torch.Tensor,
+                           gid_of_slot: torch.Tensor, m: torch.Tensor, v: torch.Tensor, init_geom: torch.Tensor | None,
+                           n_transparent: int, hparams: _abi.HParams, step: int, eta: torch.Tensor,
+                           loss_out: torch.Tensor, workspace: torch.Tensor, stream=None,
+                           step_device: torch.Tensor | None = None):
+    """A5 + A6 fused (one view -> one Adam step): render_backward_masked into a zero gradient, then
+    adam_step_unstable with w_reg = weights[2], without a gradient buffer."""
+    g = gm.c_struct()
+    prm = gm.c_params()
+    pr = proj.c_struct()
+    b = bins.c_struct()
+    o = fwd.c_struct()
+    fr = _abi.Frame(_p(target_color), _p(target_depth))
+    w = _abi.LossWeights(*[float(x) for x in weights])
+    check(lib().rtgs_backward_adam_unstable(C.byref(g), C.byref(pr), C.byref(b), C.byref(pose), C.byref(cam),
+                                            C.byref(o), C.byref(fr), C.byref(w), _p(slot_of_gid), _p(gid_of_slot),
+                                            int(gid_of_slot.numel()), C.byref(prm), _p(m), _p(v), _p(init_geom),
+                                            int(n_transparent), C.byref(hparams), int(step), _p(step_device), _p(eta),
+                                            _p(loss_out), _p(workspace), workspace.numel() * workspace.element_size(),
+                                            _stream(stream)), "rtgs_backward_adam_unstable")
+
+
 def classify_workspace_size(cam: _abi.Camera) -> int:
     return int(lib().rtgs_classify_workspace_size(C.byref(cam)))
 
@@ -527,6 +551,7 @@ class MappingEngine:
         self._fc = [_FrameCache(self.proj_full, BinBuffers(cam, self.capacity, device))]
         self._fc_clock = 0
         self.use_cache = True
+        self.fused_adam = True
         self.reset_window()
 
     def _view_state(self):
@@ -755,11 +780,28 @@ class MappingEngine:
         adam_step_unstable(self.gm, self.gid_of_slot, self.grad, self.m, self.v, self.init_geom, self.n_transparent,
                            self.weights[2], self.hp, self.step_count, self.eta, stream, step_device=self.step_dev)
 
+    def backward_adam(self, frame_color, frame_depth, pose: _abi.Pose, stream=None):
+        """A5 + A6 fused (fused_adam): the slot gradient stays on chip; same result as backward()
+        followed by optimizer_step()."""
+        self.step_count += 1
+        s = torch.cuda.current_stream() if stream is None else stream
+        with torch.cuda.stream(s):
+            self.step_dev.add_(1)
+        backward_adam_unstable(self.gm, self.proj_iter, self.bins, pose, self.cam, self.out, frame_color, frame_depth,
+                               self.weights, self.slot_of_gid, self.gid_of_slot, self.m, self.v, self.init_geom,
+                               self.n_transparent, self.hp, self.step_count, self.eta, self.loss, self.ws_bwd, stream,
+                               step_device=self.step_dev)
+
     def iteration(self, frame_color, frame_depth, pose: _abi.Pose, stream=None):
-        """One mapping optimisation iteration A0-A6 (the paper's 'mapping / iteration')."""
+        """One mapping optimisation iteration A0-A6 (the paper's 'mapping / iteration').  With
+        fused_adam (default) A5 and A6 are one kernel pair; the separate calls remain for gradient
+        accumulation and all-reduce (keyframe step, multi-GPU)."""
         self.forward_masked(pose, stream)
-        self.backward(frame_color, frame_depth, pose, stream)
-        self.optimizer_step(stream)
+        if self.fused_adam:
+            self.backward_adam(frame_color, frame_depth, pose, stream)
+        else:
+            self.backward(frame_color, frame_depth, pose, stream)
+            self.optimizer_step(stream)
 
     def end_window(self, frame_color, frame_depth, pose: _abi.Pose, frame_idx: int, state=None, stream=None):
         """NEXT f1, after a window's iterations: Eq.9 fusion with the window-start parameters, then the
@@ -876,7 +918,8 @@ class MappingEngine:
         The ingest runs on a side stream concurrently with the iteration on the current stream (the
         paper runs mapping stages in parallel threads); the only dependency is that the Adam
         step, which writes the parameters, waits until the ingest's projection has read them.
-        `reduce_grads(grad)` (multi-GPU) runs between the backward and the Adam step."""
+        `reduce_grads(grad)` (multi-GPU) runs between the backward and the Adam step; without it the
+        two are the fused call (fused_adam)."""
         main = torch.cuda.current_stream()
         side = self.side
         side.wait_stream(main)
@@ -884,11 +927,15 @@ class MappingEngine:
         self.ingest(frame_color, frame_depth, ingest_pose or pose, seed=seed, frame_idx=frame_idx, stream=side,
                     after_project=lambda s: proj_done.record(s))
         self.forward_masked(pose, main)
-        self.backward(frame_color, frame_depth, pose, main)
-        if reduce_grads is not None:
-            reduce_grads(self.grad)
-        main.wait_event(proj_done)
-        self.optimizer_step(main)
+        if reduce_grads is None and self.fused_adam:
+            main.wait_event(proj_done)  # (long done: the projection is the ingest's first kernel)
+            self.backward_adam(frame_color, frame_depth, pose, main)
+        else:
+            self.backward(frame_color, frame_depth, pose, main)
+            if reduce_grads is not None:
+                reduce_grads(self.grad)
+            main.wait_event(proj_done)
+            self.optimizer_step(main)
         main.wait_stream(side)
 
 

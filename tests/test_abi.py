@@ -26,7 +26,7 @@ def _declared():
 
 def test_every_declared_symbol_is_exported(L):
     names = _declared()
-    assert len(names) == 30
+    assert len(names) == 31
     for n in names:
         assert hasattr(L, n), n
     from paper_2404_19706_b200 import _abi
@@ -61,6 +61,39 @@ def test_invalid_arguments_rejected_on_host(L):
     prm = _abi.Params(None, None, None, None, 0, 3)
     assert L.rtgs_adam_step_unstable(C.byref(prm), None, 0, None, None, None, None, None, 0, 1000.0, C.byref(hp), 0,
                                      None, None, None) == 1            # step must be >= 1 (or on the device)
+
+
+def test_fused_backward_adam_validates_on_host(L):
+    """rtgs_backward_adam_unstable: the update is written through `params`, which must name the
+    arrays of `g`; mismatches and missing operands are rejected before any launch."""
+    from paper_2404_19706_b200 import _abi, mapping
+    cam = mapping.make_camera(500, 500, 320, 240, 640, 480)
+    pose = mapping.make_pose([[1, 0, 0], [0, 1, 0], [0, 0, 1]], [0, 0, 0])
+    buf = (C.c_float * 64)()
+    fb = C.cast(buf, C.c_void_p)
+    g = _abi.Gaussians(fb, fb, fb, fb, fb, fb, 0, 3)
+    pr = _abi.Projected(fb, fb, fb, fb)
+    b = _abi.Bins(fb, fb, fb, 16)
+    out = _abi.RenderOut()
+    for f in ("color", "trans", "depth", "normal", "index", "n_contrib", "active_bits", "tile_keep", "tile_list",
+              "counts"):
+        if hasattr(out, f):
+            setattr(out, f, fb)
+    fr = _abi.Frame(fb, fb)
+    w = _abi.LossWeights(1.0, 1.0, 1000.0)
+    hp = mapping.hparams()
+    args = lambda prm, step=1, ws=fb, wsb=1 << 12: (C.byref(g), C.byref(pr), C.byref(b), C.byref(pose), C.byref(cam),
+                                                    C.byref(out), C.byref(fr), C.byref(w), None, None, 0,
+                                                    C.byref(prm), None, None, None, 0, C.byref(hp), step, None, None,
+                                                    fb, ws, wsb, None)
+    other = (C.c_float * 64)()
+    bad = _abi.Params(C.cast(other, C.c_void_p), fb, fb, fb, 0, 3)   # pos is not g's pos
+    assert L.rtgs_backward_adam_unstable(*args(bad)) == 1
+    wrong_deg = _abi.Params(fb, fb, fb, fb, 0, 2)
+    assert L.rtgs_backward_adam_unstable(*args(wrong_deg)) == 1
+    ok = _abi.Params(fb, fb, fb, fb, 0, 3)
+    assert L.rtgs_backward_adam_unstable(*args(ok, step=0)) == 1       # step >= 1 or on the device
+    assert L.rtgs_backward_adam_unstable(*args(ok, ws=None)) == 4      # RTGS_ERR_WORKSPACE
 
 
 def test_workspace_sizes(L):
