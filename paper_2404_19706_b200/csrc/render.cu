@@ -101,12 +101,17 @@ __global__ void __launch_bounds__(256) k_tile_coverage(const uint2* __restrict__
                                                        uint32_t* __restrict__ bits, uint8_t* __restrict__ keep,
                                                        uint32_t* __restrict__ list, uint32_t* __restrict__ counts) {
   __shared__ float4 sa[256], sb[256];
+  __shared__ float se[256];
   const int t = blockIdx.x;
   const int lx = threadIdx.x & 15, ly = threadIdx.x >> 4;
   const int px = (t % TX) * kTile + lx, py = (t / TX) * kTile + ly;
   const bool inside = px < W && py < H;
   const uint2 rg = srange[t];
   const int n = (int)(rg.y - rg.x);
+  const int lane = threadIdx.x & 31;
+  // this warp's pixel box (two tile rows): the render's bounding-box cull, then exact tests
+  const float bx0 = (float)((t % TX) * kTile), bx1 = bx0 + (float)(kTile - 1);
+  const float by0 = (float)((t / TX) * kTile + 2 * (threadIdx.x >> 5)), by1 = by0 + 1.f;
   bool cov = false;
   for (int c0 = 0; c0 < n; c0 += 256) {
     if (!__syncthreads_or(inside && !cov)) break;  // every pixel of the tile is decided
@@ -115,22 +120,33 @@ __global__ void __launch_bounds__(256) k_tile_coverage(const uint2* __restrict__
       const uint32_t row = (uint32_t)(keys[rg.x + c0 + threadIdx.x] & 0xFFFFFFFFull);
       sa[threadIdx.x] = sub_rec[(size_t)4 * row];
       sb[threadIdx.x] = sub_rec[(size_t)4 * row + 1];
+      se[threadIdx.x] = sub_rec[(size_t)4 * row + 2].w;
     }
     __syncthreads();
-    if (inside && !cov)
-      for (int j = 0; j < cnt; ++j) {
-        PairEval e;
-        if (eval_pair(sa[j], sb[j], (float)px, (float)py, e)) {
-          cov = true;
-          break;
-        }
+    bool wdone = __all_sync(0xffffffffu, !inside || cov);
+    for (int g0 = 0; g0 < cnt && !wdone; g0 += 32) {
+      const int j = g0 + lane;
+      bool ov = false;
+      if (j < cnt) {
+        const float4 r0 = sa[j];
+        const float2 ext = unpack_ext(se[j]);
+        ov = (r0.x + ext.x >= bx0) && (r0.x - ext.x <= bx1) && (r0.y + ext.y >= by0) && (r0.y - ext.y <= by1);
       }
+      uint32_t m = __ballot_sync(0xffffffffu, ov);
+      while (m) {
+        const int idx = g0 + __ffs(m) - 1;
+        m &= m - 1;
+        PairEval e;
+        const bool hit = eval_pair(sa[idx], sb[idx], (float)px, (float)py, e);
+        cov = cov || (inside && hit);
+      }
+      wdone = __all_sync(0xffffffffu, !inside || cov);
+    }
     __syncthreads();
   }
   const bool act = inside && cov;
   // active bits: each half-warp is one 16-pixel tile row; its 16 bits go to 1 or 2 mask words
   const uint32_t bal = __ballot_sync(0xffffffffu, act);
-  const int lane = threadIdx.x & 31;
   if ((lane & 15) == 0 && py < H) {
     const uint32_t m16 = (lane ? bal >> 16 : bal) & 0xFFFFu;
     const int x0 = px;  // lx == 0
