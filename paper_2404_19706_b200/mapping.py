@@ -648,38 +648,70 @@ class MappingEngine:
         icp_track(frame_depth, self.full, model_pose, self.cam, params, pose_io, self.icp_diag, self.ws_icp, stream)
         return pose_io, self.icp_diag
 
+    def _buf(self, name: str, rows: int, tail: tuple = (), dtype=torch.float32, cap_rows: int | None = None):
+        """First `rows` rows of a persistent device buffer that only grows (to >= cap_rows, x1.25), so
+        successive windows with different slot counts reuse their memory instead of reallocating."""
+        b = self._bufs.get(name)
+        if b is None or b.shape[0] < rows or tuple(b.shape[1:]) != tuple(tail) or b.dtype != dtype:
+            cap = max(rows, 1, int(b.shape[0] * 1.25) if b is not None and tuple(b.shape[1:]) == tuple(tail) else 0,
+                      cap_rows or 0)
+            b = torch.empty((cap,) + tuple(tail), dtype=dtype, device=self.device)
+            self._bufs[name] = b
+        return b[:rows]
+
     def reset_window(self):
-        """(Re)build the unstable slot set from flags and reset the Adam state (R19: per window)."""
-        flags = self.gm.flags.cpu().numpy()
-        gid = np.nonzero((flags & FLAG_STABLE) == 0)[0].astype(np.int32)
-        slot = np.full(self.gm.n, -1, dtype=np.int32)
-        slot[gid] = np.arange(len(gid), dtype=np.int32)
-        # (storage of >= 1 element: a valid pointer even for an empty slot set)
-        self.gid_of_slot = torch.zeros(max(len(gid), 1), dtype=torch.int32, device=self.device)[: len(gid)]
-        self.gid_of_slot.copy_(torch.as_tensor(gid))
-        self.slot_of_gid = torch.as_tensor(slot, device=self.device)
-        n_slots = len(gid)
+        """(Re)build the unstable slot set from flags and reset the Adam state (R19: per window).
+        On the device (one host synchronisation for the slot count); buffers are reused across windows."""
+        if not hasattr(self, "_bufs"):
+            self._bufs = {}
+        n = self.gm.n
+        flags = self.gm.flags
+        gid_t = torch.nonzero((flags & FLAG_STABLE) == 0).flatten()  # (the host learns the count here)
+        n_slots = int(gid_t.numel())
+        cap = self.gm.capacity  # slot-indexed buffers hold the whole storage: no window reallocates them
+        self.n_transparent = int(((flags[gid_t] & FLAG_TRANSPARENT) != 0).sum()) if n_slots else 0
+        self.gid_of_slot = self._buf("gid_of_slot", n_slots, (), torch.int32, cap_rows=cap)
+        self.gid_of_slot.copy_(gid_t)
+        self.slot_of_gid = self._buf("slot_of_gid", n, (), torch.int32, cap_rows=cap)
+        self.slot_of_gid.fill_(-1)
+        if n_slots:
+            self.slot_of_gid[gid_t] = torch.arange(n_slots, dtype=torch.int32, device=self.device)
         D = 10 + 3 * (self.gm.sh_degree + 1) ** 2
-        self.grad = torch.zeros((max(n_slots, 1), D), dtype=torch.float32, device=self.device)
-        self.m = torch.zeros_like(self.grad)
-        self.v = torch.zeros_like(self.grad)
-        self.n_transparent = int(((flags[gid] & FLAG_TRANSPARENT) != 0).sum())
-        gid_t = self.gid_of_slot.long()
-        self.init_geom = torch.cat([self.gm.pos[gid_t], self.gm.log_scale[gid_t], self.gm.rot[gid_t]], 1).contiguous() \
-            if n_slots else torch.zeros((1, 10), device=self.device)
-        self.ws_bwd = torch.empty(backward_workspace_size(n_slots), dtype=torch.uint8, device=self.device)
+        rows = max(n_slots, 1)
+        self.grad = self._buf("grad", rows, (D,), cap_rows=cap)
+        self.m = self._buf("m", rows, (D,), cap_rows=cap)
+        self.v = self._buf("v", rows, (D,), cap_rows=cap)
+        for t in (self.grad, self.m, self.v):
+            t.zero_()
+        # window start: parameters and eta of the slots, for L_reg (init_geom) and the Eq.9 fusion at
+        # the window end (f1)
+        self.before = self._buf("before", rows, (D,), cap_rows=cap)
+        self.eta_before = self._buf("eta_before", rows, (), torch.int32, cap_rows=cap)
+        if n_slots:
+            for k, (c0, c1) in (("pos", (0, 3)), ("log_scale", (3, 6)), ("rot", (6, 10))):
+                self.before[:, c0:c1] = getattr(self.gm, k)[gid_t]
+            shg = self._buf("sh_gather", n_slots, (D - 10,), cap_rows=cap)
+            torch.index_select(self.gm.sh.reshape(n, D - 10), 0, gid_t, out=shg)
+            self.before[:, 10:] = shg
+            torch.index_select(self.eta, 0, gid_t, out=self.eta_before)
+        else:
+            self.before.zero_()
+            self.eta_before.zero_()
+        self.init_geom = self._buf("init_geom", rows, (10,), cap_rows=cap)
+        self.init_geom.copy_(self.before[:, :10])
+        self.ws_bwd = self._buf("ws_bwd", backward_workspace_size(n_slots), (), torch.uint8,
+                                cap_rows=backward_workspace_size(cap))
         self.step_count = 0
-        # window start: parameters and eta of the slots, for the Eq.9 fusion at the window end (f1)
-        self.before = torch.cat([self.gm.pos[gid_t], self.gm.log_scale[gid_t], self.gm.rot[gid_t],
-                                 self.gm.sh[gid_t].reshape(n_slots, -1)], 1).contiguous() if n_slots else \
-            torch.zeros((1, D), device=self.device)
-        self.eta_before = self.eta[gid_t].clone() if n_slots else torch.zeros(1, dtype=torch.int32, device=self.device)
-        self.step_dev = torch.zeros(1, dtype=torch.int32, device=self.device)  # graph-replayable step
+        if getattr(self, "step_dev", None) is None:
+            self.step_dev = torch.zeros(1, dtype=torch.int32, device=self.device)  # graph-replayable step
+        else:
+            self.step_dev.zero_()
         # f3: the slots' own projection rows and the cached-binning workspace (the cache itself is
         # invalidated where the stable set changes: end_window)
-        self.proj_sub = ProjectedBuffers(n_slots, self.device)
-        self.ws_bin_cached = torch.empty(bin_cached_workspace_size(n_slots, self.cam, self.capacity), dtype=torch.uint8,
-                                         device=self.device)
+        if getattr(self, "proj_sub", None) is None or self.proj_sub.rec.shape[0] < n_slots:
+            self.proj_sub = ProjectedBuffers(max(n_slots, cap), self.device)
+        self.ws_bin_cached = self._buf("ws_bin_cached", bin_cached_workspace_size(n_slots, self.cam, self.capacity), (),
+                                       torch.uint8, cap_rows=bin_cached_workspace_size(cap, self.cam, self.capacity))
         self.proj_iter = self.proj
 
     # --- the two flows ---------------------------------------------------------------------------

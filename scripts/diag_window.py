@@ -30,11 +30,14 @@ def main():
         print(f"{label:28s} {1e3 * (time.perf_counter() - t0):9.3f} ms", flush=True)
         return r
 
+    eng.map_window(frames, iterations=50, seed=1, first_frame_idx=0)   # warm: caches allocated, map grown
+    print("--- second window ---")
     for i, (c, d, pose) in enumerate(frames):
         tm(f"ingest {i}", lambda: eng.ingest(c, d, pose, frame_idx=i))
         r = tm(f"insert {i}", lambda: eng.insert(c, d, pose, frame_idx=i))
         print("   result", r.cpu().numpy().tolist())
     tm("reset_window", eng.reset_window)
+    tm("reset_window (again)", eng.reset_window)
     print("   slots", int(eng.gid_of_slot.numel()))
     rng = np.random.default_rng(0)
     for k in range(5):
@@ -46,6 +49,19 @@ def main():
         eng.iteration(c, d, pose)
     torch.cuda.synchronize()
     print(f"45 iterations              {1e3 * (time.perf_counter() - t0):9.3f} ms")
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    names = ["forward_masked", "backward_adam"]
+    acc = {k: 0.0 for k in names}
+    for k in range(10):
+        c, d, pose = frames[int(rng.integers(6))]
+        torch.cuda.synchronize()
+        e0.record(); eng.forward_masked(pose); e1.record(); torch.cuda.synchronize()
+        acc["forward_masked"] += e0.elapsed_time(e1) / 10
+        e0.record(); eng.backward_adam(c, d, pose); e1.record(); torch.cuda.synchronize()
+        acc["backward_adam"] += e0.elapsed_time(e1) / 10
+    print("device ms per iteration part", {k: round(v, 3) for k, v in acc.items()})
+    print("kept tiles", int(eng.out.counts[0].item()), "active px", int(eng.out.counts[2].item()),
+          "instances", int(eng.bins.n_instances.item()))
     c, d, pose = frames[-1]
     tm("end_window", lambda: eng.end_window(c, d, pose, frame_idx=5))
 
