@@ -412,8 +412,11 @@ def main():
         # timed step and render_full_alone_ms use the production kernel, which does not count)
         eng.full.count_blends = True
         P.render_color_depth(gm, eng.proj_full, eng.bins_full, pose, cam, P.RTGS_RENDER_FULL, eng.full)
+        eng.out.count_blends = True   # and of the last iteration's MASKED render (same lists)
+        P.render_color_depth(gm, eng.proj_iter, eng.bins, pose, cam, P.RTGS_RENDER_MASKED, eng.out)
         torch.cuda.synchronize()
         eng.full.count_blends = False
+        eng.out.count_blends = False
         blends_full = int(eng.full.counts[3].item())
         blends_masked = int(eng.out.counts[3].item())
         counts_full = None

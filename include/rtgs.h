@@ -108,6 +108,9 @@ typedef struct {
 } rtgs_bins;
 
 enum { RTGS_RENDER_FULL = 0, RTGS_RENDER_MASKED = 1, RTGS_RENDER_COVERAGE = 2 };
+/* OR-ed into FULL or MASKED: also count the blended (pixel, Gaussian) pairs into counts[3] (a
+ * statistic; the production renders leave it off, it costs instructions per blended pair). */
+enum { RTGS_RENDER_COUNT = 16 };
 
 /* Render buffers (O2-O4).  Which fields are read / written depends on the mode, see the call. */
 typedef struct {
@@ -123,7 +126,8 @@ typedef struct {
   uint32_t* counts;      /* [4] device: [0] #kept tiles, [1] |P| (active pixels in kept tiles),
                                         [2] |M_unstable| (all three written by COVERAGE), [3] number of
                                         blended (pixel, Gaussian) pairs of the last FULL / MASKED render
-                                        (NULLABLE in FULL mode)                                    */
+                                        made with RTGS_RENDER_COUNT (zeroed by COVERAGE); NULLABLE in
+                                        FULL mode without RTGS_RENDER_COUNT                           */
 } rtgs_render_out;
 
 /* Target RGBD frame C_k, D_k: color [3][H][W] in [0,1]; depth [H][W] metres, <= 0 or
@@ -188,6 +192,8 @@ rtgs_status rtgs_bin_and_sort(const rtgs_projected* proj, int32_t n, const rtgs_
  *                 power >= -4.5 and f >= 1/255 at u] (exactly T^_unstable(u) < 1, R16), tile keep
  *                 (>= 50 % of in-image pixels), kept-tile list, counts.  Writes active_bits, tile_keep,
  *                 tile_list, counts; needs proj and g->flags only (bins may be NULL).
+ *  FULL or MASKED | RTGS_RENDER_COUNT: also accumulate the blended-pair count into counts[3] (reset
+ *                 at the start of the call); without the flag counts[3] is not touched.
  * Blending per pixel in (zkey, gid) order: skip if power < -4.5 or f = min(0.99, alpha e^power) < 1/255;
  * the first f > e^-0.5 is the depth hit (tested before termination, R9); stop when T (1-f) < 1e-4.
  * ------------------------------------------------------------------------------------------- */

@@ -88,14 +88,18 @@ rtgs_status rtgs_render_color_depth(const rtgs_gaussians* g, const rtgs_projecte
     if (!out->active_bits || !out->tile_keep || !out->tile_list || !out->counts) return RTGS_ERR_INVALID_ARG;
     return finish(launch_coverage(*g, *proj, *cam, *out, S(stream)));
   }
+  const bool count = (mode & RTGS_RENDER_COUNT) != 0;
+  mode &= ~RTGS_RENDER_COUNT;
   if (mode != RTGS_RENDER_FULL && mode != RTGS_RENDER_MASKED) return RTGS_ERR_INVALID_ARG;
+  if (count && !out->counts) return RTGS_ERR_INVALID_ARG;
   if (!proj || !proj->rec || !proj->zkey || !a16(proj->rec) || !bins_ok(bins)) return RTGS_ERR_INVALID_ARG;
   // (sub_zkey / sub_gid may be NULL for an empty subset: then no entry carries the subset bit)
   if (bins->sub_rec && !a16(bins->sub_rec)) return RTGS_ERR_INVALID_ARG;
   if (!out->color || !out->trans || !out->depth || !out->index || !out->n_contrib) return RTGS_ERR_INVALID_ARG;
   if (mode == RTGS_RENDER_MASKED && (!out->active_bits || !out->tile_list || !out->counts))
     return RTGS_ERR_INVALID_ARG;
-  return finish(launch_render(*proj, *bins, make_pose(*pose), *cam, mode == RTGS_RENDER_MASKED, *out, S(stream)));
+  return finish(launch_render(*proj, *bins, make_pose(*pose), *cam, mode == RTGS_RENDER_MASKED, count, *out,
+                              S(stream)));
 }
 
 size_t rtgs_backward_workspace_size(int32_t n_slots) { return n_slots < 0 ? 0 : backward_workspace_size(n_slots); }

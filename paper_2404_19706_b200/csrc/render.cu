@@ -205,8 +205,8 @@ struct FwdArgs {
   uint32_t* n_contrib;
 };
 
-// COUNT: accumulate the blended-pair statistic counts[3] (only when the caller passes counts in FULL
-// mode; the production FULL render of the mapping step does not, saving 3 instructions per survivor)
+// COUNT: accumulate the blended-pair statistic counts[3] (RTGS_RENDER_COUNT; the production renders of
+// the mapping step do not, saving 3 instructions per survivor)
 template <bool MASKED, bool COUNT>
 __global__ void __launch_bounds__(32 * ((MASKED ? kHalfWarps : kTileWarps) + 1)) k_render_fwd(const FwdArgs a) {
   constexpr int NW = MASKED ? kHalfWarps : kTileWarps;  // MASKED: one CTA per half of a kept tile
@@ -364,7 +364,7 @@ cudaError_t launch_tile_any(const rtgs_camera& cam, const rtgs_render_out& out, 
 }
 
 cudaError_t launch_render(const rtgs_projected& proj, const rtgs_bins& bins, const PoseF& pose,
-                          const rtgs_camera& cam, int masked, const rtgs_render_out& out, cudaStream_t s) {
+                          const rtgs_camera& cam, int masked, bool count, const rtgs_render_out& out, cudaStream_t s) {
   FwdArgs a;
   a.rec = reinterpret_cast<const float4*>(proj.rec);
   a.zkey = proj.zkey;
@@ -381,9 +381,10 @@ cudaError_t launch_render(const rtgs_projected& proj, const rtgs_bins& bins, con
   a.color = out.color; a.trans = out.trans; a.depth = out.depth; a.normal = out.normal;
   a.index = out.index; a.n_contrib = out.n_contrib;
   const int T = a.cam.TX * a.cam.TY;
-  if (out.counts) cudaMemsetAsync(out.counts + 3, 0, 4, s);  // blend counter of this render
-  if (masked) k_render_fwd<true, true><<<2 * T, 32 * (kHalfWarps + 1), 0, s>>>(a);
-  else if (out.counts) k_render_fwd<false, true><<<T, 32 * (kTileWarps + 1), 0, s>>>(a);
+  if (count) cudaMemsetAsync(out.counts + 3, 0, 4, s);  // blend counter of this render
+  if (masked && count) k_render_fwd<true, true><<<2 * T, 32 * (kHalfWarps + 1), 0, s>>>(a);
+  else if (masked) k_render_fwd<true, false><<<2 * T, 32 * (kHalfWarps + 1), 0, s>>>(a);
+  else if (count) k_render_fwd<false, true><<<T, 32 * (kTileWarps + 1), 0, s>>>(a);
   else k_render_fwd<false, false><<<T, 32 * (kTileWarps + 1), 0, s>>>(a);
   note_launch();
   return cudaGetLastError();

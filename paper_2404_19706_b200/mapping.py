@@ -24,7 +24,7 @@ import numpy as np
 import torch
 
 from . import _abi
-from ._abi import RTGS_RENDER_COVERAGE, RTGS_RENDER_FULL, RTGS_RENDER_MASKED, check, lib
+from ._abi import RTGS_RENDER_COUNT, RTGS_RENDER_COVERAGE, RTGS_RENDER_FULL, RTGS_RENDER_MASKED, check, lib
 
 FLAG_TRANSPARENT = 1
 FLAG_STABLE = 2
@@ -165,14 +165,14 @@ class RenderBuffers:
         self.tile_keep = torch.zeros(T, dtype=torch.uint8, device=device)
         self.tile_list = torch.zeros(T, dtype=torch.int32, device=device)
         self.counts = torch.zeros(4, dtype=torch.int32, device=device)
-        # FULL mode only counts blended pairs (counts[3]) when asked: the statistic costs instructions
+        # FULL / MASKED renders count blended pairs (counts[3], RTGS_RENDER_COUNT) only when asked: the
+        # statistic costs instructions per blended pair
         self.count_blends = count_blends
 
     def c_struct(self, mode: int | None = None):
-        counts = None if (mode == RTGS_RENDER_FULL and not self.count_blends) else self.counts
         return _abi.RenderOut(_p(self.color), _p(self.trans), _p(self.depth), _p(self.normal), _p(self.index),
                               _p(self.n_contrib), _p(self.active_bits), _p(self.tile_keep), _p(self.tile_list),
-                              _p(counts))
+                              _p(self.counts))
 
     def active_mask(self) -> torch.Tensor:
         """Unpack active_bits into a bool [H, W] image (test / inspection helper)."""
@@ -219,6 +219,8 @@ def render_color_depth(gm: GaussianMap, proj: ProjectedBuffers, bins: BinBuffers
     pr = proj.c_struct()
     o = out.c_struct(mode)
     b = bins.c_struct() if bins is not None else None
+    if out.count_blends and mode in (RTGS_RENDER_FULL, RTGS_RENDER_MASKED):
+        mode |= RTGS_RENDER_COUNT
     check(lib().rtgs_render_color_depth(C.byref(g), C.byref(pr), C.byref(b) if b is not None else None, C.byref(pose),
                                         C.byref(cam), mode, C.byref(o), _stream(stream)), "rtgs_render_color_depth")
 
@@ -518,7 +520,7 @@ class MappingEngine:
         # the masked iteration and the frame ingest own separate buffers so they can run concurrently
         self.proj = ProjectedBuffers(n, device)
         self.bins = BinBuffers(cam, self.capacity, device)
-        self.out = RenderBuffers(cam, device)
+        self.out = RenderBuffers(cam, device, count_blends=False)  # production MASKED render: no statistic
         self.ws_bin = torch.empty(bin_workspace_size(n, cam, self.capacity), dtype=torch.uint8, device=device)
         self.proj_full = ProjectedBuffers(n, device)
         self.bins_full = BinBuffers(cam, self.capacity, device)
