@@ -310,8 +310,8 @@ def main():
         between_steps()
         hold(5.0)
         mark("start")
-        P.project_gaussians(gm, pose, cam, eng.proj_full); mark("ingest.project")
-        P.bin_and_sort(eng.proj_full, gm.n, cam, None, eng.bins_full, eng.ws_bin_full); mark("ingest.bin_and_sort")
+        P.project_and_bin(gm, pose, cam, eng.proj_full, eng.bins_full, eng.ws_bin_full)
+        mark("ingest.project_and_bin")
         if eng.use_cache:
             P.stable_cache_build(eng.bins_full, gm.flags, cam, eng.cache); mark("ingest.cache_build")
         P.render_color_depth(gm, eng.proj_full, eng.bins_full, pose, cam, P.RTGS_RENDER_FULL, eng.full); mark("ingest.render_full")

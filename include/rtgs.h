@@ -171,14 +171,24 @@ rtgs_status rtgs_project_gaussians(const rtgs_gaussians* g, const rtgs_pose* pos
  * A2 — rtgs_bin_and_sort (O8, R7, R8, R15)
  * Instances (tile, gid) for every tile of every Gaussian's tile rect — restricted to tiles with
  * tile_keep[t] != 0 when tile_keep is non-NULL — ordered by (tile, zkey bits, gid).  Implementation:
- * stable compaction of the Gaussians with >= 1 instance, LSD radix sort of their depth keys, emission
- * in depth order, stable LSD radix sort of the instances by tile id.  Reads proj->zkey, proj->rect.
- * `n_instances` receives I; if I > capacity the output is truncated (see rtgs_bins).
+ * per-tile counts (replicated counters), one-CTA scan into tile ranges, emission of (zkey, gid)
+ * pairs into the ranges, one CTA per tile sorting its pairs (LSD radix on the varying depth bits,
+ * then gid) — the order is unique, so the result is deterministic although the emission is not.
+ * Reads proj->zkey, proj->rect.  `n_instances` receives I; if I > capacity the output is truncated
+ * (see rtgs_bins).
  * ------------------------------------------------------------------------------------------- */
 size_t rtgs_bin_workspace_size(int32_t n, const rtgs_camera* cam, uint32_t capacity);
 rtgs_status rtgs_bin_and_sort(const rtgs_projected* proj, int32_t n, const rtgs_camera* cam,
                               const uint8_t* tile_keep, rtgs_bins* out, void* workspace, size_t workspace_bytes,
                               void* stream);
+
+/* A1 + A2 fused — rtgs_project_and_bin: exactly rtgs_project_gaussians followed by rtgs_bin_and_sort
+ * over all tiles (tile_keep NULL) — the frame ingest's pair — with the per-tile counting of the
+ * binning done by the projection kernel (no second pass over zkey / rect).  Workspace as
+ * rtgs_bin_workspace_size(g->n, cam, out->capacity). */
+rtgs_status rtgs_project_and_bin(const rtgs_gaussians* g, const rtgs_pose* pose, const rtgs_camera* cam,
+                                 rtgs_projected* proj, rtgs_bins* out, void* workspace, size_t workspace_bytes,
+                                 void* stream);
 
 /* ---------------------------------------------------------------------------------------------
  * A0/A3/A4 — rtgs_render_color_depth (O2-O4; Eq.1-5, Eq.12, R7-R12, R15, R16)

@@ -6,7 +6,7 @@ fallback: importing the binding and calling it without the built library raises.
 """
 from ._abi import LIB_PATH, RTGSError, lib  # noqa: F401
 from .mapping import (GaussianMap, MappingEngine, ProjectedBuffers, BinBuffers, RenderBuffers,  # noqa: F401
-                      project_gaussians, bin_and_sort, render_color_depth, render_backward_masked,
+                      project_gaussians, bin_and_sort, project_and_bin, render_color_depth, render_backward_masked,
                       adam_step_unstable, classify_and_add_pixels, fuse_window, manage_states, state_params,
                       project_subset, coverage_rows, stable_cache_build, bin_and_sort_cached,
                       coverage_and_bin_cached, coverage_subset, merge_cached,

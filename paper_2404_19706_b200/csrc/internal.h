@@ -10,6 +10,8 @@
 
 namespace rtgs {
 
+constexpr int kRep = 8;  // replicated per-tile counters of the binning: spreads same-address atomics 8 ways
+
 // once per (kernel attribute, device): per-device bit in `mask` (one-time cudaFuncSetAttribute calls
 // must be repeated on every device the process launches on)
 inline bool first_on_device(std::atomic<uint64_t>& mask) {
@@ -28,6 +30,12 @@ PoseF make_pose(const rtgs_pose& p);
 
 cudaError_t launch_project(const rtgs_gaussians& g, const PoseF& pose, const rtgs_camera& cam,
                            const rtgs_projected& out, cudaStream_t s);
+
+// the projection with the binning's per-tile counts fused in (replica (i >> 8) & (kRep - 1), as k_tile_count)
+cudaError_t launch_project_count(const rtgs_gaussians& g, const PoseF& pose, const rtgs_camera& cam,
+                                 const rtgs_projected& out, uint32_t* cnt, cudaStream_t s);
+cudaError_t launch_project_bin(const rtgs_gaussians& g, const PoseF& pose, const rtgs_camera& cam,
+                               const rtgs_projected& proj, const rtgs_bins& out, void* ws, cudaStream_t s);
 
 cudaError_t launch_project_subset(const rtgs_gaussians& g, const int32_t* gid_list, int n_list, const PoseF& pose,
                                   const rtgs_camera& cam, const rtgs_projected& out, cudaStream_t s);

@@ -30,6 +30,8 @@ struct ProjArgs {
   uint32_t* zkey;
   uint2* rect;  // 4 x int16
   uint32_t* touched;
+  uint32_t* cnt;  // fused A2 count (launch_project_bin): replicated per-tile counters, else NULL
+  int TX, T;
 };
 
 // SH colour of one Gaussian from its AoS row c[3k + ch] in shared memory (R2): the 3DGS real basis,
@@ -227,6 +229,13 @@ __global__ void __launch_bounds__(kProjThreads, 6) k_project(const ProjArgs a) {
     a.zkey[i] = zbits;
     a.rect[i] = rect;
     a.touched[i] = touched;
+    if (!SUB && a.cnt && vis) {  // A2 count, as k_tile_count (same tiles, same replica of Gaussian i)
+      uint32_t* c = a.cnt + (size_t)((i >> 8) & (kRep - 1)) * a.T;
+      const int tx0 = (int)(rect.x & 0xFFFF) / kTile, ty0 = (int)(rect.x >> 16) / kTile;
+      const int tx1 = (int)(rect.y & 0xFFFF) / kTile, ty1 = (int)(rect.y >> 16) / kTile;
+      for (int ty = ty0; ty <= ty1; ++ty)
+        for (int tx = tx0; tx <= tx1; ++tx) atomicAdd(&c[ty * a.TX + tx], 1u);
+    }
   }
 }
 
@@ -244,7 +253,8 @@ PoseF make_pose(const rtgs_pose& p) {
 }
 
 static cudaError_t project_impl(const rtgs_gaussians& g, const int32_t* subset, int n_rows, const PoseF& pose,
-                                const rtgs_camera& cam, const rtgs_projected& out, cudaStream_t s) {
+                                const rtgs_camera& cam, const rtgs_projected& out, cudaStream_t s,
+                                uint32_t* cnt = nullptr) {
   if (n_rows == 0) return cudaSuccess;
   ProjArgs a;
   a.pos = g.pos; a.log_scale = g.log_scale; a.rot = g.rot; a.opacity = g.opacity; a.sh = g.sh;
@@ -265,6 +275,9 @@ static cudaError_t project_impl(const rtgs_gaussians& g, const int32_t* subset, 
   a.zkey = out.zkey;
   a.rect = reinterpret_cast<uint2*>(out.rect);
   a.touched = out.tiles_touched;
+  a.cnt = cnt;
+  a.TX = a.cam.TX;
+  a.T = a.cam.TX * a.cam.TY;
   const size_t smem = (size_t)kProjThreads * 3 * a.K * sizeof(float);
   const int blocks = (n_rows + kProjThreads - 1) / kProjThreads;
   const bool sub = subset != nullptr;
@@ -285,6 +298,11 @@ static cudaError_t project_impl(const rtgs_gaussians& g, const int32_t* subset, 
 cudaError_t launch_project(const rtgs_gaussians& g, const PoseF& pose, const rtgs_camera& cam,
                            const rtgs_projected& out, cudaStream_t s) {
   return project_impl(g, nullptr, g.n, pose, cam, out, s);
+}
+
+cudaError_t launch_project_count(const rtgs_gaussians& g, const PoseF& pose, const rtgs_camera& cam,
+                                 const rtgs_projected& out, uint32_t* cnt, cudaStream_t s) {
+  return project_impl(g, nullptr, g.n, pose, cam, out, s, cnt);
 }
 
 cudaError_t launch_project_subset(const rtgs_gaussians& g, const int32_t* gid_list, int n_list, const PoseF& pose,

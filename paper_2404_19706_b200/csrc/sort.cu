@@ -31,7 +31,6 @@ constexpr int kScanChunk = kScanThreads * kScanItems;  // 2048
 constexpr int kSortThreads = 256;
 constexpr int kSortWarps = kSortThreads / 32;
 constexpr int kSortCap = 1024;  // tile lists up to this length are sorted in shared memory
-constexpr int kRep = 8;         // replicated tile counters: spreads same-address atomics 8 ways
 
 static inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
@@ -604,19 +603,12 @@ size_t bin_workspace_size(int n, const rtgs_camera& cam, uint32_t capacity) {
   return carve(n, cam, capacity, nullptr, nullptr);
 }
 
-cudaError_t launch_bin(const rtgs_projected& proj, int n, const rtgs_camera& cam, const uint8_t* keep,
-                       const rtgs_bins& out, void* ws, cudaStream_t s) {
-  const CamK k = make_cam(cam);
+// offsets, emission and per-tile sort, once the replicated per-tile counts are in w.cnt
+static cudaError_t bin_from_counts(const rtgs_projected& proj, int n, const CamK& k, const uint8_t* keep,
+                                   const rtgs_bins& out, const BinWS& w, cudaStream_t s) {
   const int T = k.TX * k.TY;
-  BinWS w;
-  carve(n, cam, out.capacity, &w, static_cast<char*>(ws));
-  cudaMemsetAsync(w.cnt, 0, (size_t)((char*)w.start - (char*)w.cnt), s);
   const uint2* rect = reinterpret_cast<const uint2*>(proj.rect);
   const int nblk = (n + 255) / 256;
-  if (n > 0) {
-    k_tile_count<<<nblk, 256, 0, s>>>(proj.zkey, rect, keep, n, k.TX, T, w.cnt);
-    note_launch();
-  }
   k_tile_offsets<<<1, 1024, 0, s>>>(w.cnt, T, out.capacity, w.start, reinterpret_cast<uint2*>(out.tile_range),
                                     out.n_instances);
   note_launch();
@@ -635,6 +627,33 @@ cudaError_t launch_bin(const rtgs_projected& proj, int n, const rtgs_camera& cam
     note_launch();
   }
   return cudaGetLastError();
+}
+
+cudaError_t launch_bin(const rtgs_projected& proj, int n, const rtgs_camera& cam, const uint8_t* keep,
+                       const rtgs_bins& out, void* ws, cudaStream_t s) {
+  const CamK k = make_cam(cam);
+  const int T = k.TX * k.TY;
+  BinWS w;
+  carve(n, cam, out.capacity, &w, static_cast<char*>(ws));
+  cudaMemsetAsync(w.cnt, 0, (size_t)((char*)w.start - (char*)w.cnt), s);
+  const uint2* rect = reinterpret_cast<const uint2*>(proj.rect);
+  const int nblk = (n + 255) / 256;
+  if (n > 0) {
+    k_tile_count<<<nblk, 256, 0, s>>>(proj.zkey, rect, keep, n, k.TX, T, w.cnt);
+    note_launch();
+  }
+  return bin_from_counts(proj, n, k, keep, out, w, s);
+}
+
+cudaError_t launch_project_bin(const rtgs_gaussians& g, const PoseF& pose, const rtgs_camera& cam,
+                               const rtgs_projected& proj, const rtgs_bins& out, void* ws, cudaStream_t s) {
+  const CamK k = make_cam(cam);
+  BinWS w;
+  carve(g.n, cam, out.capacity, &w, static_cast<char*>(ws));
+  cudaMemsetAsync(w.cnt, 0, (size_t)((char*)w.start - (char*)w.cnt), s);
+  const cudaError_t e = launch_project_count(g, pose, cam, proj, w.cnt, s);
+  if (e != cudaSuccess) return e;
+  return bin_from_counts(proj, g.n, k, nullptr, out, w, s);
 }
 
 cudaError_t launch_cache_build(const rtgs_bins& full, const uint8_t* flags, const rtgs_camera& cam,

@@ -213,6 +213,18 @@ def bin_and_sort(proj: ProjectedBuffers, n: int, cam: _abi.Camera, tile_keep: to
                                   workspace.numel() * workspace.element_size(), _stream(stream)), "rtgs_bin_and_sort")
 
 
+def project_and_bin(gm: GaussianMap, pose: _abi.Pose, cam: _abi.Camera, proj: ProjectedBuffers, bins: BinBuffers,
+                    workspace: torch.Tensor, stream=None):
+    """A1 + A2 (all tiles) in one call: the projection kernel also counts the tile instances."""
+    g = gm.c_struct()
+    pr = proj.c_struct()
+    b = bins.c_struct()
+    check(lib().rtgs_project_and_bin(C.byref(g), C.byref(pose), C.byref(cam), C.byref(pr), C.byref(b), _p(workspace),
+                                     workspace.numel() * workspace.element_size(), _stream(stream)),
+          "rtgs_project_and_bin")
+    bins.sub = None
+
+
 def render_color_depth(gm: GaussianMap, proj: ProjectedBuffers, bins: BinBuffers | None, pose: _abi.Pose,
                        cam: _abi.Camera, mode: int, out: RenderBuffers, stream=None):
     g = gm.c_struct()
@@ -724,10 +736,9 @@ class MappingEngine:
         if fc is not None:
             fc.key = None          # rebuilt below
             self.proj_full = fc.proj
-        project_gaussians(self.gm, pose, self.cam, self.proj_full, stream)
+        project_and_bin(self.gm, pose, self.cam, self.proj_full, self.bins_full, self.ws_bin_full, stream)
         if after_project is not None:
             after_project(stream)
-        bin_and_sort(self.proj_full, self.gm.n, self.cam, None, self.bins_full, self.ws_bin_full, stream)
         if fc is not None:  # f3: the stable lists of this frame, reused by the window's iterations
             stable_cache_build(self.bins_full, self.gm.flags, self.cam, fc.cache, stream)
             fc.ready.record(torch.cuda.current_stream() if stream is None else stream)
