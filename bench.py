@@ -310,10 +310,9 @@ def main():
         between_steps()
         hold(5.0)
         mark("start")
-        P.project_and_bin(gm, pose, cam, eng.proj_full, eng.bins_full, eng.ws_bin_full)
-        mark("ingest.project_and_bin")
-        if eng.use_cache:
-            P.stable_cache_build(eng.bins_full, gm.flags, cam, eng.cache); mark("ingest.cache_build")
+        P.project_and_bin(gm, pose, cam, eng.proj_full, eng.bins_full, eng.ws_bin_full,
+                          cache=eng.cache if eng.use_cache else None)
+        mark("ingest.project_bin_cache")
         P.render_color_depth(gm, eng.proj_full, eng.bins_full, pose, cam, P.RTGS_RENDER_FULL, eng.full); mark("ingest.render_full")
         P.classify_and_add_pixels(eng.full, col, dep, gm.flags, cam, P.add_params(seed=1234), eng.pixel_class,
                                   eng.samples, eng.add_counts, eng.ws_cls); mark("ingest.classify")

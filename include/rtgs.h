@@ -184,11 +184,13 @@ rtgs_status rtgs_bin_and_sort(const rtgs_projected* proj, int32_t n, const rtgs_
 
 /* A1 + A2 fused — rtgs_project_and_bin: exactly rtgs_project_gaussians followed by rtgs_bin_and_sort
  * over all tiles (tile_keep NULL) — the frame ingest's pair — with the per-tile counting of the
- * binning done by the projection kernel (no second pass over zkey / rect).  Workspace as
+ * binning done by the projection kernel (no second pass over zkey / rect).  With `cache` non-NULL
+ * (NEXT f3; needs g->flags) the per-tile sort also writes the stable-entry cache, exactly as a
+ * following rtgs_stable_cache_build(out, g->flags, cam, cache).  Workspace as
  * rtgs_bin_workspace_size(g->n, cam, out->capacity). */
 rtgs_status rtgs_project_and_bin(const rtgs_gaussians* g, const rtgs_pose* pose, const rtgs_camera* cam,
-                                 rtgs_projected* proj, rtgs_bins* out, void* workspace, size_t workspace_bytes,
-                                 void* stream);
+                                 rtgs_projected* proj, rtgs_bins* out, rtgs_bins* cache, void* workspace,
+                                 size_t workspace_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------------------------
  * A0/A3/A4 — rtgs_render_color_depth (O2-O4; Eq.1-5, Eq.12, R7-R12, R15, R16)

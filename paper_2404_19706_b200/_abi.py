@@ -90,7 +90,8 @@ EXPORTS = {
     "rtgs_project_gaussians": (C.c_int, [P(Gaussians), P(Pose), P(Camera), P(Projected), vp]),
     "rtgs_bin_workspace_size": (C.c_size_t, [C.c_int32, P(Camera), C.c_uint32]),
     "rtgs_bin_and_sort": (C.c_int, [P(Projected), C.c_int32, P(Camera), vp, P(Bins), vp, C.c_size_t, vp]),
-    "rtgs_project_and_bin": (C.c_int, [P(Gaussians), P(Pose), P(Camera), P(Projected), P(Bins), vp, C.c_size_t, vp]),
+    "rtgs_project_and_bin": (C.c_int, [P(Gaussians), P(Pose), P(Camera), P(Projected), P(Bins), P(Bins), vp,
+                                       C.c_size_t, vp]),
     "rtgs_render_color_depth": (C.c_int, [P(Gaussians), P(Projected), P(Bins), P(Pose), P(Camera), C.c_int32,
                                           P(RenderOut), vp]),
     "rtgs_backward_workspace_size": (C.c_size_t, [C.c_int32]),

@@ -80,12 +80,15 @@ rtgs_status rtgs_bin_and_sort(const rtgs_projected* proj, int32_t n, const rtgs_
 }
 
 rtgs_status rtgs_project_and_bin(const rtgs_gaussians* g, const rtgs_pose* pose, const rtgs_camera* cam,
-                                 rtgs_projected* proj, rtgs_bins* out, void* workspace, size_t workspace_bytes,
-                                 void* stream) {
+                                 rtgs_projected* proj, rtgs_bins* out, rtgs_bins* cache, void* workspace,
+                                 size_t workspace_bytes, void* stream) {
   if (!gauss_ok(g, false) || !pose_ok(pose) || !cam_ok(cam) || !proj_ok(proj, g ? g->n : 0) || !bins_ok(out))
     return RTGS_ERR_INVALID_ARG;
+  if (cache && (!g->flags || !cache->sorted_gid || !cache->tile_range ||
+                (reinterpret_cast<uintptr_t>(cache->tile_range) & 7u) != 0 || cache->capacity < out->capacity))
+    return RTGS_ERR_INVALID_ARG;
   if (!workspace || workspace_bytes < bin_workspace_size(g->n, *cam, out->capacity)) return RTGS_ERR_WORKSPACE;
-  return finish(launch_project_bin(*g, make_pose(*pose), *cam, *proj, *out, workspace, S(stream)));
+  return finish(launch_project_bin(*g, make_pose(*pose), *cam, *proj, *out, cache, workspace, S(stream)));
 }
 
 rtgs_status rtgs_render_color_depth(const rtgs_gaussians* g, const rtgs_projected* proj, const rtgs_bins* bins,

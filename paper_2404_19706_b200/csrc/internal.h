@@ -35,7 +35,8 @@ cudaError_t launch_project(const rtgs_gaussians& g, const PoseF& pose, const rtg
 cudaError_t launch_project_count(const rtgs_gaussians& g, const PoseF& pose, const rtgs_camera& cam,
                                  const rtgs_projected& out, uint32_t* cnt, cudaStream_t s);
 cudaError_t launch_project_bin(const rtgs_gaussians& g, const PoseF& pose, const rtgs_camera& cam,
-                               const rtgs_projected& proj, const rtgs_bins& out, void* ws, cudaStream_t s);
+                               const rtgs_projected& proj, const rtgs_bins& out, const rtgs_bins* cache, void* ws,
+                               cudaStream_t s);
 
 cudaError_t launch_project_subset(const rtgs_gaussians& g, const int32_t* gid_list, int n_list, const PoseF& pose,
                                   const rtgs_camera& cam, const rtgs_projected& out, cudaStream_t s);

@@ -356,11 +356,54 @@ __device__ __forceinline__ void sort_tile(const unsigned long long* __restrict__
   for (int i = tid; i < n; i += kSortThreads) out_gid[i] = (uint32_t)(res[i] & gmask);
 }
 
+// NEXT f3 fused into the FULL binning: ordered compaction of the tile's stable entries (flags bit 1)
+// of the sorted list `g` [n] into csorted[base ...] (the cache lives in the FULL lists' index space,
+// as k_cache_build); returns nothing, writes crange[tile] and adds to n_stable.
+__device__ __forceinline__ void stable_compact(const uint32_t* __restrict__ g, int n, const uint8_t* __restrict__ flags,
+                                               uint32_t base, uint32_t* __restrict__ csorted, uint2* crange, int tile,
+                                               uint32_t* __restrict__ n_stable, uint32_t* scan_sh) {
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  uint32_t o = base;
+  for (int b = 0; b < n; b += kSortThreads) {
+    const int i = b + tid;
+    uint32_t gi = 0;
+    bool st = false;
+    if (i < n) {
+      gi = g[i];
+      st = (flags[gi] & 2u) != 0;
+    }
+    const uint32_t m = __ballot_sync(0xffffffffu, st);
+    if (lane == 0) scan_sh[w] = __popc(m);
+    __syncthreads();
+    uint32_t before = 0, tot = 0;
+#pragma unroll
+    for (int k = 0; k < kSortWarps; ++k) {
+      const uint32_t c = scan_sh[k];
+      before += k < w ? c : 0u;
+      tot += c;
+    }
+    if (st) csorted[o + before + __popc(m & ((1u << lane) - 1u))] = gi;
+    o += tot;
+    __syncthreads();  // scan_sh reused
+  }
+  if (tid == 0) {
+    crange[tile] = make_uint2(base, o);
+    if (n_stable && o > base) atomicAdd(n_stable, o - base);
+  }
+}
+
+struct StableOut {  // NEXT f3 cache written by the FULL binning (flags NULL: none)
+  const uint8_t* flags;
+  uint32_t* csorted;
+  uint2* crange;
+  uint32_t* n_stable;
+};
+
 __global__ void __launch_bounds__(kSortThreads, 6) k_tile_sort(const uint2* __restrict__ range,
                                                             unsigned long long* __restrict__ keys,
                                                             unsigned long long* __restrict__ tmp,
                                                             uint32_t* __restrict__ grank, int gid_bits,
-                                                            uint32_t* __restrict__ sorted_gid) {
+                                                            uint32_t* __restrict__ sorted_gid, const StableOut so) {
   extern __shared__ __align__(16) unsigned long long s_keys[];  // [2 * kSortCap] keys + kSortCap ranks
   __shared__ uint32_t wcnt[kSortWarps][256];
   __shared__ uint32_t dstart[256];
@@ -368,11 +411,23 @@ __global__ void __launch_bounds__(kSortThreads, 6) k_tile_sort(const uint2* __re
   __shared__ uint32_t s_zmm[2];
   const uint2 rg = range[blockIdx.x];
   const int n = (int)(rg.y - rg.x);
-  if (n <= 0) return;
+  if (n <= 0) {
+    if (so.flags && threadIdx.x == 0) so.crange[blockIdx.x] = make_uint2(rg.x, rg.x);
+    return;
+  }
   RTGS_ASSERT(rg.y >= rg.x);
   unsigned long long* seg = keys + rg.x;
   if (n == 1) {
-    if (threadIdx.x == 0) sorted_gid[rg.x] = (uint32_t)(seg[0] & 0xFFFFFFFFull);
+    if (threadIdx.x == 0) {
+      const uint32_t g = (uint32_t)(seg[0] & 0xFFFFFFFFull);
+      sorted_gid[rg.x] = g;
+      if (so.flags) {
+        const bool st = (so.flags[g] & 2u) != 0;
+        if (st) so.csorted[rg.x] = g;
+        so.crange[blockIdx.x] = make_uint2(rg.x, rg.x + (st ? 1u : 0u));
+        if (st && so.n_stable) atomicAdd(so.n_stable, 1u);
+      }
+    }
     return;
   }
   if (n <= kSortCap) {  // shared-memory path: every buffer access below is LDS / STS
@@ -381,6 +436,10 @@ __global__ void __launch_bounds__(kSortThreads, 6) k_tile_sort(const uint2* __re
   } else {              // oversized tile: global-memory ping-pong (correct, slower)
     sort_tile(seg, seg, tmp + rg.x, grank + rg.x, n, gid_bits, sorted_gid + rg.x, false, wcnt, dstart, scan_sh,
               s_zmm);
+  }
+  if (so.flags) {
+    __syncthreads();  // the sorted gids of this tile are written (read back through L1 / L2 below)
+    stable_compact(sorted_gid + rg.x, n, so.flags, rg.x, so.csorted, so.crange, blockIdx.x, so.n_stable, scan_sh);
   }
 }
 
@@ -605,7 +664,8 @@ size_t bin_workspace_size(int n, const rtgs_camera& cam, uint32_t capacity) {
 
 // offsets, emission and per-tile sort, once the replicated per-tile counts are in w.cnt
 static cudaError_t bin_from_counts(const rtgs_projected& proj, int n, const CamK& k, const uint8_t* keep,
-                                   const rtgs_bins& out, const BinWS& w, cudaStream_t s) {
+                                   const rtgs_bins& out, const BinWS& w, cudaStream_t s,
+                                   const StableOut so = StableOut{nullptr, nullptr, nullptr, nullptr}) {
   const int T = k.TX * k.TY;
   const uint2* rect = reinterpret_cast<const uint2*>(proj.rect);
   const int nblk = (n + 255) / 256;
@@ -623,8 +683,10 @@ static cudaError_t bin_from_counts(const rtgs_projected& proj, int n, const CamK
       cudaFuncSetAttribute(k_tile_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     }
     k_tile_sort<<<T, kSortThreads, smem, s>>>(reinterpret_cast<const uint2*>(out.tile_range), w.keys, w.tmp, w.grank,
-                                              gid_bits, out.sorted_gid);
+                                              gid_bits, out.sorted_gid, so);
     note_launch();
+  } else if (so.flags) {  // empty map: every cached tile range is empty
+    cudaMemsetAsync(so.crange, 0, (size_t)T * sizeof(uint2), s);
   }
   return cudaGetLastError();
 }
@@ -646,14 +708,20 @@ cudaError_t launch_bin(const rtgs_projected& proj, int n, const rtgs_camera& cam
 }
 
 cudaError_t launch_project_bin(const rtgs_gaussians& g, const PoseF& pose, const rtgs_camera& cam,
-                               const rtgs_projected& proj, const rtgs_bins& out, void* ws, cudaStream_t s) {
+                               const rtgs_projected& proj, const rtgs_bins& out, const rtgs_bins* cache, void* ws,
+                               cudaStream_t s) {
   const CamK k = make_cam(cam);
   BinWS w;
   carve(g.n, cam, out.capacity, &w, static_cast<char*>(ws));
   cudaMemsetAsync(w.cnt, 0, (size_t)((char*)w.start - (char*)w.cnt), s);
+  StableOut so{nullptr, nullptr, nullptr, nullptr};
+  if (cache) {
+    so = StableOut{g.flags, cache->sorted_gid, reinterpret_cast<uint2*>(cache->tile_range), cache->n_instances};
+    if (cache->n_instances) cudaMemsetAsync(cache->n_instances, 0, 4, s);
+  }
   const cudaError_t e = launch_project_count(g, pose, cam, proj, w.cnt, s);
   if (e != cudaSuccess) return e;
-  return bin_from_counts(proj, g.n, k, nullptr, out, w, s);
+  return bin_from_counts(proj, g.n, k, nullptr, out, w, s, so);
 }
 
 cudaError_t launch_cache_build(const rtgs_bins& full, const uint8_t* flags, const rtgs_camera& cam,

@@ -214,12 +214,15 @@ def bin_and_sort(proj: ProjectedBuffers, n: int, cam: _abi.Camera, tile_keep: to
 
 
 def project_and_bin(gm: GaussianMap, pose: _abi.Pose, cam: _abi.Camera, proj: ProjectedBuffers, bins: BinBuffers,
-                    workspace: torch.Tensor, stream=None):
-    """A1 + A2 (all tiles) in one call: the projection kernel also counts the tile instances."""
+                    workspace: torch.Tensor, stream=None, cache: BinBuffers | None = None):
+    """A1 + A2 (all tiles) in one call: the projection kernel also counts the tile instances; with
+    `cache` the tile sort also writes the f3 stable cache (as stable_cache_build)."""
     g = gm.c_struct()
     pr = proj.c_struct()
     b = bins.c_struct()
-    check(lib().rtgs_project_and_bin(C.byref(g), C.byref(pose), C.byref(cam), C.byref(pr), C.byref(b), _p(workspace),
+    c = cache.c_struct() if cache is not None else None
+    check(lib().rtgs_project_and_bin(C.byref(g), C.byref(pose), C.byref(cam), C.byref(pr), C.byref(b),
+                                     C.byref(c) if c is not None else None, _p(workspace),
                                      workspace.numel() * workspace.element_size(), _stream(stream)),
           "rtgs_project_and_bin")
     bins.sub = None
@@ -736,11 +739,13 @@ class MappingEngine:
         if fc is not None:
             fc.key = None          # rebuilt below
             self.proj_full = fc.proj
-        project_and_bin(self.gm, pose, self.cam, self.proj_full, self.bins_full, self.ws_bin_full, stream)
+        # (f3: with a frame cache the tile sort also writes this frame's stable lists, reused by the
+        # window's iterations)
+        project_and_bin(self.gm, pose, self.cam, self.proj_full, self.bins_full, self.ws_bin_full, stream,
+                        cache=fc.cache if fc is not None else None)
         if after_project is not None:
             after_project(stream)
-        if fc is not None:  # f3: the stable lists of this frame, reused by the window's iterations
-            stable_cache_build(self.bins_full, self.gm.flags, self.cam, fc.cache, stream)
+        if fc is not None:
             fc.ready.record(torch.cuda.current_stream() if stream is None else stream)
             fc.key = _pose_key(pose)
         render_color_depth(self.gm, self.proj_full, self.bins_full, pose, self.cam, RTGS_RENDER_FULL, self.full, stream)

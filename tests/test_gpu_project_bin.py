@@ -1,6 +1,6 @@
 """rtgs_project_and_bin (A1 + A2 with the tile counting fused into the projection kernel) equals
 rtgs_project_gaussians followed by rtgs_bin_and_sort bit for bit (projected records, keys, rects,
-tile ranges, sorted lists, instance count).  The separate pair is pinned to the oracle in
+tile ranges, sorted lists, instance count); with a cache it also equals rtgs_stable_cache_build.  The separate pair is pinned to the oracle in
 test_gpu_parity.py (projection within tolerance, binning bit-exact)."""
 import numpy as np
 import pytest
@@ -54,3 +54,19 @@ def test_project_and_bin_equals_the_pair(api, name, empty, removed):
     assert (ni > 0) == (n > 0)
     assert torch.equal(ba.tile_range, bb.tile_range)
     assert torch.equal(ba.sorted_gid[:ni], bb.sorted_gid[:ni])
+    # with the f3 cache: the same stable lists as rtgs_stable_cache_build on the pair's bins
+    ca, cb = M.BinBuffers(cam, cap), M.BinBuffers(cam, cap)
+    api.stable_cache_build(ba, gm.flags, cam, ca)
+    pc, bc = M.ProjectedBuffers(n), M.BinBuffers(cam, cap)
+    api.project_and_bin(gm, pose, cam, pc, bc, ws2, cache=cb)
+    torch.cuda.synchronize()
+    assert torch.equal(bc.tile_range, ba.tile_range) and torch.equal(bc.sorted_gid[:ni], ba.sorted_gid[:ni])
+    assert torch.equal(ca.tile_range, cb.tile_range)
+    assert int(ca.n_instances.item()) == int(cb.n_instances.item())
+    rg = ca.tile_range.cpu().numpy()
+    a, b = ca.sorted_gid.cpu().numpy(), cb.sorted_gid.cpu().numpy()
+    for s0, s1 in rg:
+        assert np.array_equal(a[s0:s1], b[s0:s1])
+    if n:
+        fl = gm.flags.cpu().numpy()
+        assert int(ca.n_instances.item()) == sum(int(((fl[a[s0:s1]] & 2) != 0).sum()) for s0, s1 in rg)
