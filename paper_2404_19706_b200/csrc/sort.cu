@@ -91,6 +91,23 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_down(const uint32_t* __re
   }
 }
 
+// short arrays (per-block counts, <= kScanSmall): one CTA, 1024 values per pass, one launch
+constexpr size_t kScanSmall = 16384;
+__global__ void __launch_bounds__(1024) k_scan_small(const uint32_t* __restrict__ in, int len,
+                                                     uint32_t* __restrict__ out, uint32_t* total) {
+  __shared__ uint32_t sh[33];
+  uint32_t carry = 0;
+  for (int b = 0; b < len; b += 1024) {
+    const int i = b + threadIdx.x;
+    const uint32_t v = i < len ? in[i] : 0u;
+    uint32_t tot;
+    const uint32_t ex = block_excl_scan(v, sh, &tot);
+    if (i < len) out[i] = ex + carry;
+    carry += tot;
+  }
+  if (threadIdx.x == 0 && total) *total = carry;
+}
+
 size_t scan_workspace_size(size_t len) { return align_up(((len + kScanChunk - 1) / kScanChunk + 1) * 4); }
 
 cudaError_t launch_scan(const uint32_t* in, uint32_t* out, size_t len, uint32_t* total, void* ws, cudaStream_t s) {
@@ -98,6 +115,11 @@ cudaError_t launch_scan(const uint32_t* in, uint32_t* out, size_t len, uint32_t*
   uint32_t* sums = static_cast<uint32_t*>(ws);
   if (nb == 0) {
     if (total) cudaMemsetAsync(total, 0, 4, s);
+    return cudaGetLastError();
+  }
+  if (len <= kScanSmall) {
+    k_scan_small<<<1, 1024, 0, s>>>(in, (int)len, out, total);
+    note_launch();
     return cudaGetLastError();
   }
   k_scan_reduce<<<nb, kScanThreads, 0, s>>>(in, len, sums);
