@@ -940,6 +940,48 @@ class MappingEngine:
             render_backward_masked(self.gm, self.proj, self.bins, pose, self.cam, self.g_rb, c, d, w, self.g_slot,
                                    self.g_gid, self.g_grad, self.g_loss, self.g_ws_bwd, stream)
 
+    def _global_hparams(self, lr_scale):
+        hp = self.hp
+        return _abi.HParams(0.0, hp.lr_sh0 * lr_scale, hp.lr_shrest * lr_scale, hp.lr_scale * lr_scale,
+                            hp.lr_rot * lr_scale, hp.beta1, hp.beta2, hp.eps)
+
+    def global_adam_shard(self, grad_rows: torch.Tensor, r0: int, r1: int, lr_scale=0.1, stream=None):
+        """(e) sharded over ranks: the Adam step of the global slots [r0, r1) (clipped to the slot
+        count) with their summed gradient rows `grad_rows` [>= r1 - r0, D] (consumed); writes those
+        Gaussians' parameters and eta on this map and returns them packed as rows [r1 - r0, D + 1]
+        (pos, log_scale, rot, sh, then eta's int32 bits as float32) for the all-gather."""
+        S = int(self.g_gid.numel())
+        D = self.g_grad.shape[1]
+        a, b = min(r0, S), min(r1, S)
+        packed = torch.zeros((r1 - r0, D + 1), dtype=torch.float32, device=self.device)
+        if b > a:
+            gid = self.g_gid[a:b]
+            g = gid.long()
+            init = torch.cat([self.gm.pos[g], self.gm.log_scale[g], self.gm.rot[g]], 1).contiguous()
+            m = torch.zeros((b - a, D), dtype=torch.float32, device=self.device)
+            v = torch.zeros_like(m)
+            adam_step_unstable(self.gm, gid, grad_rows[: b - a], m, v, init, self.g_ntr, self.weights[2],
+                               self._global_hparams(lr_scale), 1, self.eta, stream)
+            packed[: b - a, :10] = torch.cat([self.gm.pos[g], self.gm.log_scale[g], self.gm.rot[g]], 1)
+            packed[: b - a, 10:D] = self.gm.sh[g].reshape(b - a, D - 10)
+            packed[: b - a, D] = self.eta[g].view(torch.float32)
+        return packed
+
+    def global_apply_rows(self, packed: torch.Tensor):
+        """Write all-gathered packed rows (global slots [0, S); padding rows past S ignored) into the
+        map: parameters and eta of every optimised Gaussian (bit-exact copies of the owners' results)."""
+        S = int(self.g_gid.numel())
+        if S == 0:
+            return
+        D = self.g_grad.shape[1]
+        rows = packed[:S]
+        g = self.g_gid.long()
+        self.gm.pos[g] = rows[:, 0:3]
+        self.gm.log_scale[g] = rows[:, 3:6]
+        self.gm.rot[g] = rows[:, 6:10]
+        self.gm.sh[g] = rows[:, 10:D].reshape(S, -1, 3)
+        self.eta[g] = rows[:, D].contiguous().view(torch.int32)
+
     def global_step(self, views, ratio=0.4, lr_scale=0.1, reduce_grads=None, stream=None, n_total=None):
         """(e) one global optimisation step: global_backward over `views`, the gradient sum
         over ranks (`reduce_grads(g_grad)`, multi-GPU), then one Adam step of every non-removed
@@ -948,9 +990,7 @@ class MappingEngine:
         self.global_backward(views, ratio, stream, n_total)
         if reduce_grads is not None:
             reduce_grads(self.g_grad)
-        hp = self.hp
-        ghp = _abi.HParams(0.0, hp.lr_sh0 * lr_scale, hp.lr_shrest * lr_scale, hp.lr_scale * lr_scale,
-                           hp.lr_rot * lr_scale, hp.beta1, hp.beta2, hp.eps)
+        ghp = self._global_hparams(lr_scale)
         g = self.g_gid.long()
         init = torch.cat([self.gm.pos[g], self.gm.log_scale[g], self.gm.rot[g]], 1).contiguous() if len(g) else None
         s = torch.cuda.current_stream() if stream is None else stream

@@ -1,4 +1,5 @@
-"""World-size-2 gloo test of the multi-GPU host logic (view partition + gradient all-reduce)."""
+"""World-size-2 gloo tests of the multi-GPU host logic (view partition, gradient all-reduce, the
+sharded optimiser's row reduce-scatter / all-gather)."""
 import os
 
 import numpy as np
@@ -47,3 +48,47 @@ def test_gloo_allreduce_equals_sum_over_all_views():
     for _, g, ref in res:
         np.testing.assert_allclose(g, ref, rtol=1e-5, atol=1e-5)
     np.testing.assert_array_equal(res[0][1], res[1][1])
+
+
+def _shard_worker(rank, world, port, q):
+    from paper_2404_19706_b200.dist import all_gather_rows, reduce_scatter_rows, shard_rows
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    S, D = 37, 5
+    rng = np.random.default_rng(rank)
+    mine = rng.normal(size=(S, D)).astype(np.float32)      # this rank's gradient of every slot
+    per, padded = shard_rows(S, world)
+    full = torch.zeros((padded, D))
+    full[:S] = torch.as_tensor(mine)
+    block = reduce_scatter_rows(full, world, rank)
+    upd = block * 2.0 + rank                                 # stand-in for the per-block optimiser
+    gathered = all_gather_rows(upd, world)
+    q.put((rank, per, block.numpy().copy(), gathered.numpy().copy()))
+    dist.destroy_process_group()
+
+
+def test_gloo_sharded_rows_round_trip():
+    """reduce-scatter (emulated on gloo) hands each rank the summed rows of its block; the
+    all-gather returns every rank's updated block in rank order (padding rows included)."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 30500 + (os.getpid() % 1000)
+    ps = [ctx.Process(target=_shard_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = sorted([q.get(timeout=120) for _ in range(world)], key=lambda r: r[0])
+    for p in ps:
+        p.join(timeout=60)
+    S, D = 37, 5
+    total = sum(np.random.default_rng(r).normal(size=(S, D)).astype(np.float32) for r in range(world))
+    per = res[0][1]
+    assert per == 19
+    padded = np.zeros((per * world, D), np.float32)
+    padded[:S] = total
+    for rank, _, block, gathered in res:
+        np.testing.assert_allclose(block, padded[rank * per:(rank + 1) * per], rtol=1e-6, atol=1e-6)
+    expect = np.concatenate([res[r][2] * 2.0 + r for r in range(world)], 0)
+    for _, _, _, gathered in res:
+        np.testing.assert_allclose(gathered, expect, rtol=1e-6)

@@ -156,3 +156,43 @@ def test_global_slots_exclude_removed(api):
     np.testing.assert_array_equal(gid, np.nonzero((scene["flags"] & 4) == 0)[0])
     slot = eng.g_slot.cpu().numpy()
     assert (slot[::41] == -1).all() and (slot[gid] == np.arange(len(gid))).all()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_optimizer_equals_replicated(api, world):
+    """The sharded (e) step (reduce-scatter -> Adam on each rank's slot block -> all-gather) gives
+    every rank the map the replicated step computes, bit for bit: `world` ranks emulated in one
+    process on the same summed gradient (the collectives are covered by test_dist_cpu.py)."""
+    from paper_2404_19706_b200.dist import shard_rows
+    cfg = CONFIGS["T2"]
+    scene = make_scene(cfg)
+    views = []
+    for v in (None, 1):
+        R, t = make_pose(cfg, view=v)
+        c, d = make_frame(cfg, (R, t))
+        views.append((torch.as_tensor(c, device="cuda"), torch.as_tensor(d, device="cuda"), api.make_pose(R, t)))
+    engs = [api.MappingEngine(device_map(scene), api.camera_of(cfg)) for _ in range(world + 1)]
+    engs[0].global_backward(views)
+    G = engs[0].g_grad.clone()              # the summed gradient (computed once: atomics order aside)
+    S, D = G.shape
+    for e in engs[1:]:
+        e._global_state()
+    # replicated reference: one block covering every slot
+    ref = engs[0]
+    ref.g_grad.zero_()
+    ref.global_apply_rows(ref.global_adam_shard(G.clone(), 0, S))
+    # sharded: rank r optimises rows [r per, (r+1) per), then every rank applies the gathered rows
+    per, padded = shard_rows(S, world)
+    full = torch.zeros((padded, D), device="cuda")
+    full[:S] = G
+    packed = [engs[1 + r].global_adam_shard(full[r * per:(r + 1) * per].clone(), r * per, (r + 1) * per)
+              for r in range(world)]
+    gathered = torch.cat(packed, 0)
+    for e in engs[1:]:
+        e.global_apply_rows(gathered)
+    torch.cuda.synchronize()
+    for e in engs[1:]:
+        for k in ("pos", "log_scale", "rot", "sh", "opacity"):
+            assert torch.equal(getattr(e.gm, k), getattr(ref.gm, k)), k
+        assert torch.equal(e.eta, ref.eta)
+    assert not torch.equal(ref.gm.sh, torch.as_tensor(scene["sh"], device="cuda"))
