@@ -140,11 +140,18 @@ __device__ __forceinline__ bool rect_tiles(uint2 r, int& tx0, int& ty0, int& tx1
   return true;
 }
 
+// REP: replicated counters (kRep for the whole map's binning; kSubRep for the small unstable subset,
+// whose atomics contend less, so its single-CTA scans read fewer counters)
+#ifndef RTGS_SUBREP
+#define RTGS_SUBREP 1
+#endif
+constexpr int kSubRep = RTGS_SUBREP;
+template <int REP>
 __global__ void __launch_bounds__(256) k_tile_count(const uint32_t* __restrict__ zkey, const uint2* __restrict__ rect,
                                                     const uint8_t* __restrict__ keep, int n, int TX, int T,
                                                     uint32_t* __restrict__ cnt) {
   const int i = blockIdx.x * 256 + threadIdx.x;
-  cnt += (size_t)(blockIdx.x & (kRep - 1)) * T;
+  cnt += (size_t)(blockIdx.x & (REP - 1)) * T;
   if (i >= n) return;
   const uint32_t z = zkey[i];
   const uint2 rc = rect[i];  // both loads in flight together
@@ -180,6 +187,7 @@ __device__ __forceinline__ uint32_t chunk_scan(uint32_t* s_v, uint32_t* sh) {
   return tot;
 }
 
+template <int REP>
 __global__ void __launch_bounds__(1024) k_tile_offsets(const uint32_t* __restrict__ cnt, int T, uint32_t cap,
                                                        uint32_t* __restrict__ start, uint2* __restrict__ range,
                                                        uint32_t* __restrict__ n_inst) {
@@ -187,13 +195,13 @@ __global__ void __launch_bounds__(1024) k_tile_offsets(const uint32_t* __restric
   __shared__ uint32_t sh[33];
   uint32_t carry = 0;
   for (int b = 0; b < T; b += kOffChunk) {
-    uint32_t c[kOffTiles][kRep], tsum[kOffTiles];
+    uint32_t c[kOffTiles][REP], tsum[kOffTiles];
 #pragma unroll
     for (int k = 0; k < kOffTiles; ++k) {
       const int t = b + k * 1024 + threadIdx.x;
       tsum[k] = 0;
 #pragma unroll
-      for (int r = 0; r < kRep; ++r) {
+      for (int r = 0; r < REP; ++r) {
         c[k][r] = t < T ? cnt[(size_t)r * T + t] : 0u;
         tsum[k] += c[k][r];
       }
@@ -208,7 +216,7 @@ __global__ void __launch_bounds__(1024) k_tile_offsets(const uint32_t* __restric
         const uint32_t ex = s_ex[k * 1024 + threadIdx.x] + carry;
         uint32_t o = ex;
 #pragma unroll
-        for (int r = 0; r < kRep; ++r) {
+        for (int r = 0; r < REP; ++r) {
           start[(size_t)r * T + t] = o;
           o += c[k][r];
         }
@@ -223,12 +231,13 @@ __global__ void __launch_bounds__(1024) k_tile_offsets(const uint32_t* __restric
   if (threadIdx.x == 0) *n_inst = carry;
 }
 
+template <int REP>
 __global__ void __launch_bounds__(256) k_emit(const uint32_t* __restrict__ zkey, const uint2* __restrict__ rect,
                                               const uint8_t* __restrict__ keep, int n, int TX, int T,
                                               const uint32_t* __restrict__ start, uint32_t* __restrict__ cursor,
                                               uint32_t cap, unsigned long long* __restrict__ keys) {
   const int i = blockIdx.x * 256 + threadIdx.x;
-  const size_t rep = (size_t)(blockIdx.x & (kRep - 1)) * T;  // same replica as k_tile_count
+  const size_t rep = (size_t)(blockIdx.x & (REP - 1)) * T;  // same replica as k_tile_count
   start += rep;
   cursor += rep;
   if (i >= n) return;
@@ -500,6 +509,7 @@ __global__ void __launch_bounds__(256) k_cache_build(const uint2* __restrict__ f
 
 // one CTA, after k_tile_count of the subset: the subset's own ranges and replica starts (as
 // k_tile_offsets) AND the merged output ranges, count(t) = keep[t] ? |stable(t)| + |subset(t)| : 0
+template <int REP>
 __global__ void __launch_bounds__(1024) k_merge_offsets(const uint32_t* __restrict__ cnt, const uint8_t* __restrict__ keep,
                                                         const uint2* __restrict__ crange, int T, uint32_t cap,
                                                         uint32_t* __restrict__ start, uint2* __restrict__ srange,
@@ -509,7 +519,7 @@ __global__ void __launch_bounds__(1024) k_merge_offsets(const uint32_t* __restri
   __shared__ uint32_t sh[33];
   uint32_t carry = 0, carry2 = 0;
   for (int b = 0; b < T; b += kOffChunk) {
-    uint32_t c[kOffTiles][kRep], tsum[kOffTiles], cl[kOffTiles];
+    uint32_t c[kOffTiles][REP], tsum[kOffTiles], cl[kOffTiles];
 #pragma unroll
     for (int k = 0; k < kOffTiles; ++k) {
       const int t = b + k * 1024 + threadIdx.x;
@@ -522,7 +532,7 @@ __global__ void __launch_bounds__(1024) k_merge_offsets(const uint32_t* __restri
         kp = keep[t];
       }
 #pragma unroll
-      for (int r = 0; r < kRep; ++r) {
+      for (int r = 0; r < REP; ++r) {
         c[k][r] = t < T ? cnt[(size_t)r * T + t] : 0u;
         tsum[k] += c[k][r];
       }
@@ -541,7 +551,7 @@ __global__ void __launch_bounds__(1024) k_merge_offsets(const uint32_t* __restri
         const uint32_t ex2 = s_ex2[k * 1024 + threadIdx.x] + carry2;
         uint32_t o = ex;
 #pragma unroll
-        for (int r = 0; r < kRep; ++r) {
+        for (int r = 0; r < REP; ++r) {
           start[(size_t)r * T + t] = o;
           o += c[k][r];
         }
@@ -691,11 +701,11 @@ static cudaError_t bin_from_counts(const rtgs_projected& proj, int n, const CamK
   const int T = k.TX * k.TY;
   const uint2* rect = reinterpret_cast<const uint2*>(proj.rect);
   const int nblk = (n + 255) / 256;
-  k_tile_offsets<<<1, 1024, 0, s>>>(w.cnt, T, out.capacity, w.start, reinterpret_cast<uint2*>(out.tile_range),
+  k_tile_offsets<kRep><<<1, 1024, 0, s>>>(w.cnt, T, out.capacity, w.start, reinterpret_cast<uint2*>(out.tile_range),
                                     out.n_instances);
   note_launch();
   if (n > 0) {
-    k_emit<<<nblk, 256, 0, s>>>(proj.zkey, rect, keep, n, k.TX, T, w.start, w.cursor, out.capacity, w.keys);
+    k_emit<kRep><<<nblk, 256, 0, s>>>(proj.zkey, rect, keep, n, k.TX, T, w.start, w.cursor, out.capacity, w.keys);
     note_launch();
     int gid_bits = 1;
     while (gid_bits < 32 && (1u << gid_bits) < (uint32_t)n) ++gid_bits;
@@ -723,7 +733,7 @@ cudaError_t launch_bin(const rtgs_projected& proj, int n, const rtgs_camera& cam
   const uint2* rect = reinterpret_cast<const uint2*>(proj.rect);
   const int nblk = (n + 255) / 256;
   if (n > 0) {
-    k_tile_count<<<nblk, 256, 0, s>>>(proj.zkey, rect, keep, n, k.TX, T, w.cnt);
+    k_tile_count<kRep><<<nblk, 256, 0, s>>>(proj.zkey, rect, keep, n, k.TX, T, w.cnt);
     note_launch();
   }
   return bin_from_counts(proj, n, k, keep, out, w, s);
@@ -801,14 +811,14 @@ cudaError_t launch_bin_cached(const rtgs_projected& proj, const rtgs_bins& cache
   const uint2* rect = reinterpret_cast<const uint2*>(sub.rect);
   const int nblk = (n_sub + 255) / 256;
   if (n_sub > 0) {
-    k_tile_count<<<nblk, 256, 0, s>>>(sub.zkey, rect, keep, n_sub, k.TX, T, w.cnt);
+    k_tile_count<kSubRep><<<nblk, 256, 0, s>>>(sub.zkey, rect, keep, n_sub, k.TX, T, w.cnt);
     note_launch();
   }
-  k_merge_offsets<<<1, 1024, 0, s>>>(w.cnt, keep, reinterpret_cast<const uint2*>(cache.tile_range), T, out.capacity,
+  k_merge_offsets<kSubRep><<<1, 1024, 0, s>>>(w.cnt, keep, reinterpret_cast<const uint2*>(cache.tile_range), T, out.capacity,
                                      w.start, srange, reinterpret_cast<uint2*>(out.tile_range), out.n_instances);
   note_launch();
   if (n_sub > 0) {
-    k_emit<<<nblk, 256, 0, s>>>(sub.zkey, rect, keep, n_sub, k.TX, T, w.start, w.cursor, out.capacity, w.keys);
+    k_emit<kSubRep><<<nblk, 256, 0, s>>>(sub.zkey, rect, keep, n_sub, k.TX, T, w.start, w.cursor, out.capacity, w.keys);
     note_launch();
   }
   int row_bits = 1;
@@ -848,13 +858,13 @@ cudaError_t launch_coverage_subset(const rtgs_projected& sub, int n_sub, const r
   const uint2* rect = reinterpret_cast<const uint2*>(sub.rect);
   const int nblk = (n_sub + 255) / 256;
   if (n_sub > 0) {
-    k_tile_count<<<nblk, 256, 0, s>>>(sub.zkey, rect, nullptr, n_sub, k.TX, T, w.cnt);
+    k_tile_count<kSubRep><<<nblk, 256, 0, s>>>(sub.zkey, rect, nullptr, n_sub, k.TX, T, w.cnt);
     note_launch();
   }
-  k_tile_offsets<<<1, 1024, 0, s>>>(w.cnt, T, capacity, w.start, srange, sn);
+  k_tile_offsets<kSubRep><<<1, 1024, 0, s>>>(w.cnt, T, capacity, w.start, srange, sn);
   note_launch();
   if (n_sub > 0) {
-    k_emit<<<nblk, 256, 0, s>>>(sub.zkey, rect, nullptr, n_sub, k.TX, T, w.start, w.cursor, capacity, w.keys);
+    k_emit<kSubRep><<<nblk, 256, 0, s>>>(sub.zkey, rect, nullptr, n_sub, k.TX, T, w.start, w.cursor, capacity, w.keys);
     note_launch();
   }
   return launch_tile_coverage(srange, w.keys, reinterpret_cast<const float4*>(sub.rec), cam, cov, s);
@@ -872,7 +882,7 @@ cudaError_t launch_merge_cached(const rtgs_projected& proj, const rtgs_bins& cac
   carve_cached(n_sub, cam, out.capacity, static_cast<char*>(ws), &ssorted, &srange, &sn, &bws);
   BinWS w;
   carve(n_sub, cam, out.capacity, &w, static_cast<char*>(bws));
-  k_merge_offsets<<<1, 1024, 0, s>>>(w.cnt, keep, reinterpret_cast<const uint2*>(cache.tile_range), T, out.capacity,
+  k_merge_offsets<kSubRep><<<1, 1024, 0, s>>>(w.cnt, keep, reinterpret_cast<const uint2*>(cache.tile_range), T, out.capacity,
                                      w.start, srange, reinterpret_cast<uint2*>(out.tile_range), out.n_instances);
   note_launch();
   int row_bits = 1;
