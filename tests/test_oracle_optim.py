@@ -65,3 +65,15 @@ def test_reg_gradient_and_eta():
     assert list(eta2 - eta) == [0, 1, 0, 0, 0, 0]
     # stable rows of L_reg are untouched, and a zero gradient leaves the parameter in place
     assert np.all(th2[3] == theta[3])
+
+
+def test_reg_loss_closed_form():
+    """L_reg (R18): mean over the 10 N_t geometry scalars of the transparent slots only."""
+    import torch
+
+    from oracle.optim import reg_loss
+    th = torch.tensor([[1.0] * 10, [2.0] * 10, [5.0] * 10], dtype=torch.float64)
+    th0 = torch.zeros_like(th)
+    transparent = np.array([True, False, True])
+    assert float(reg_loss(th, th0, transparent)) == (10 * 1.0 + 10 * 25.0) / 20
+    assert float(reg_loss(th, th0, np.array([False, False, False]))) == 0.0

@@ -172,3 +172,15 @@ def test_removed_gaussians_are_culled():
         ps = P.project(P.params_from_scene(sub), R, t, P.camera(cfg), sc["sh_degree"])
     np.testing.assert_array_equal(pr["valid"][keep], ps["valid"])
     np.testing.assert_array_equal(pr["rect"][keep], ps["rect"])
+
+
+def test_extent_sigmas_closed_form():
+    """R7: k = min(3, sqrt(2 ln(255 alpha))) standard deviations; no support when 255 alpha <= 1."""
+    import math
+
+    from oracle.projection import extent_sigmas
+    k = extent_sigmas(np.array([1.0, 0.1, 0.02, 1.0 / 255.0, 0.001]))
+    assert k[0] == 3.0                                         # sqrt(2 ln 255) = 3.33 > 3
+    assert abs(k[1] - math.sqrt(2.0 * math.log(25.5))) < 1e-15
+    assert abs(k[2] - math.sqrt(2.0 * math.log(5.1))) < 1e-15
+    assert np.isnan(k[3]) and np.isnan(k[4])

@@ -257,3 +257,11 @@ def test_splat_coverage_equals_dense_definition():
         np.testing.assert_array_equal(splat, dense.reshape(cfg.height, cfg.width))
         # margins: the splat version sees only rect pixels, so its margin is >= the dense one
         assert (sm.ravel() >= dm - 1e-15).all()
+
+
+def test_depth_order_ties_by_gid():
+    """R8: non-culled Gaussians in (float32 z-key bits, gid) order; culled ones are absent."""
+    from oracle.raster import depth_order
+    z = np.array([2.0, 1.0, 2.0, 0.5, 1.0], np.float32)
+    proj = {"valid": np.array([True, True, True, False, True]), "zkey32": z}
+    assert depth_order(proj).tolist() == [1, 4, 0, 2]
