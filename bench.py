@@ -577,7 +577,14 @@ def main():
             "roofline_secondary": [{"kernel": "k_project (A1)", "bound": "hbm", "achieved": achieved, "peak": hbm,
                                     "unit": "GB/s", "frac": achieved / hbm, "peak_kind": peak_kind,
                                     "traffic": traffic.get("k_project"),
-                                    "bytes_per_gaussian": bytes_per_g, "time_ms": phases["project_alone_ms"]}],
+                                    "bytes_per_gaussian": bytes_per_g, "time_ms": phases["project_alone_ms"]}]
+            + ([{"kernel": "k_render_fwd<FULL> (A3/A4)", "bound": "issue",
+                 "achieved": traffic["k_render_fwd<FULL>_warp_inst"] / t_render_s / 1e12,
+                 "peak": 4 * 148 * clk_ghz * 1e9 / 1e12, "unit": "T warp-instr/s",
+                 "frac": traffic["k_render_fwd<FULL>_warp_inst"] / t_render_s / (4 * 148 * clk_ghz * 1e9),
+                 "peak_kind": "derived: 4 issue slots / clock / SM x 148 SM x sampled SM clock",
+                 "algorithmic": "warp instructions executed per launch (ncu smsp__inst_executed.sum, profiles/traffic.json)",
+                 "time_ms": phases["render_full_alone_ms"]}] if "k_render_fwd<FULL>_warp_inst" in traffic else []),
             "blends": {"full_per_frame": blends_full, "masked_per_iter": blends_masked,
                        "full_blends_per_s": blends_full / t_render_s},
             "clocks": clocks,
