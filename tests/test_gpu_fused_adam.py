@@ -4,7 +4,8 @@ same float32 update (adam.cuh), but the backward's screen-space sums are float a
 differs from run to run, so gradients agree to rounding, not bitwise.  Adam's first step is
 lr * sign(g) where |g| is tiny, so the comparison uses the coordinates whose gradient is clearly
 non-zero (|g| > 1e-3 max|g| per component, as test_gpu_backward.py::test_iteration_end_to_end):
-there the parameters agree to 1e-7, the moments to 1e-3 relative; eta and the loss agree.  The
+there the parameters agree to 1e-7, the moments to 2e-3 / 4e-3 relative (m / v, with a floor at
+1e-4 of the component's largest value); eta and the loss agree.  The
 separate path is pinned to the oracle in test_gpu_backward.py, whose end-to-end test runs the
 fused default."""
 import numpy as np
@@ -72,9 +73,13 @@ def test_fused_equals_separate(api, name, deg, cache):
     zero = g == 0
     np.testing.assert_array_equal(a[zero], b[zero])          # no gradient: not moved by either
     ns = len(gid)
-    for k in ("m", "v"):
+    # atomic-order noise of cancelling sums: relative to the value, with a floor at 1e-4 of the
+    # component's largest magnitude; v ~ g^2 doubles the relative noise of g
+    for k, rt in (("m", 2e-3), ("v", 4e-3)):
         x, y = getattr(ef, k)[:ns].cpu().numpy(), getattr(es, k)[:ns].cpu().numpy()
-        np.testing.assert_allclose(x[sel], y[sel], rtol=1e-3, atol=0)  # atomic-order noise of cancelling sums
+        floor = 1e-4 * np.abs(y).max(0, keepdims=True)
+        bad = sel & (np.abs(x - y) > rt * np.abs(y) + floor)
+        assert not bad.any(), (k, int(bad.sum()))
         assert np.array_equal(x[zero], y[zero])
     assert np.array_equal(ef.eta.cpu().numpy(), es.eta.cpu().numpy())
     np.testing.assert_allclose(ef.loss.cpu().numpy(), es.loss.cpu().numpy(), rtol=1e-5)
