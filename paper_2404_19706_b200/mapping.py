@@ -932,9 +932,7 @@ class MappingEngine:
         nv = n_total if n_total is not None else len(views)   # multi-GPU: the views of ALL ranks
         w = tuple(x / max(1, nv) for x in self.weights[:2]) + (self.weights[2],)
         for (c, d, pose) in views:
-            project_gaussians(self.gm, pose, self.cam, self.proj, stream)
-            bin_and_sort(self.proj, self.gm.n, self.cam, None, self.bins, self.ws_bin, stream)
-            self.bins.sub = None
+            project_and_bin(self.gm, pose, self.cam, self.proj, self.bins, self.ws_bin, stream)
             render_color_depth(self.gm, self.proj, self.bins, pose, self.cam, RTGS_RENDER_FULL, self.g_rb, stream)
             topk_error_mask(self.g_rb, c, self.cam, ratio, self.g_rb, self.g_ws_topk, stream)
             render_backward_masked(self.gm, self.proj, self.bins, pose, self.cam, self.g_rb, c, d, w, self.g_slot,
@@ -957,10 +955,10 @@ class MappingEngine:
         if b > a:
             gid = self.g_gid[a:b]
             g = gid.long()
-            init = torch.cat([self.gm.pos[g], self.gm.log_scale[g], self.gm.rot[g]], 1).contiguous()
             m = torch.zeros((b - a, D), dtype=torch.float32, device=self.device)
             v = torch.zeros_like(m)
-            adam_step_unstable(self.gm, gid, grad_rows[: b - a], m, v, init, self.g_ntr, self.weights[2],
+            # (L_reg has a zero gradient in a single step from the anchor: see global_step)
+            adam_step_unstable(self.gm, gid, grad_rows[: b - a], m, v, None, 0, self.weights[2],
                                self._global_hparams(lr_scale), 1, self.eta, stream)
             packed[: b - a, :10] = torch.cat([self.gm.pos[g], self.gm.log_scale[g], self.gm.rot[g]], 1)
             packed[: b - a, 10:D] = self.gm.sh[g].reshape(b - a, D - 10)
@@ -991,13 +989,14 @@ class MappingEngine:
         if reduce_grads is not None:
             reduce_grads(self.g_grad)
         ghp = self._global_hparams(lr_scale)
-        g = self.g_gid.long()
-        init = torch.cat([self.gm.pos[g], self.gm.log_scale[g], self.gm.rot[g]], 1).contiguous() if len(g) else None
         s = torch.cuda.current_stream() if stream is None else stream
         with torch.cuda.stream(s):
             self.g_m.zero_()
             self.g_v.zero_()
-        adam_step_unstable(self.gm, self.g_gid, self.g_grad, self.g_m, self.g_v, init, self.g_ntr, self.weights[2], ghp,
+        # L_reg (R18) anchors the transparent geometry at its values before this step, and the step
+        # is a single Adam update evaluated there: theta == theta_0, so dL_reg/dtheta is exactly 0 and
+        # no anchor copy is made (n_transparent 0 switches the term off; bit-identical result)
+        adam_step_unstable(self.gm, self.g_gid, self.g_grad, self.g_m, self.g_v, None, 0, self.weights[2], ghp,
                            1, self.eta, stream)
         return self.g_loss
 
