@@ -10,7 +10,9 @@ bench's launch configuration, on outputs the oracle can compute one by one:
     contains the pixel is a candidate: the rect contains the support, R7);
   * colour-loss gradients of 6 sampled unstable slots (autograd of the oracle restricted to the
     Gaussians that reach the slot's footprint pixels; w_d = 0 so the normalisation |P| is the
-    oracle's own).
+    oracle's own);
+  * the f3-cached iteration equals the uncached one, and the bench's fused backward + Adam equals
+    the separate calls, at full size.
 """
 import numpy as np
 import pytest
@@ -220,6 +222,48 @@ def test_cached_iteration_equals_uncached_c3(c3):
     scale = np.abs(b["grad"]).max(0, keepdims=True) + 1e-30
     assert (np.abs(a["grad"] - b["grad"]) <= 1e-5 * scale).all()
     np.testing.assert_allclose(a["loss"], b["loss"], rtol=1e-5)  # float32 atomic sum order across CTAs
+
+
+def test_fused_adam_step_c3(c3):
+    """The bench's fused A5 + A6 call at full size equals the separate backward + Adam step from the
+    same state: parameters on the coordinates with a clearly non-zero gradient to 1e-7 (Adam's first
+    step is lr * sign(g)), untouched coordinates unchanged, eta identical."""
+    eng, P, gm = c3["eng"], c3["P"], c3["eng"].gm
+    pose = P.make_pose(c3["R"], c3["t"])
+    tc, td = torch.as_tensor(c3["col"], device="cuda"), torch.as_tensor(c3["dep"], device="cuda")
+    gid = eng.gid_of_slot.long()
+    keys = ("pos", "log_scale", "rot", "sh")
+    snap = {k: getattr(gm, k).clone() for k in keys}
+    eta0 = eng.eta.clone()
+
+    def rows():
+        return torch.cat([getattr(gm, k)[gid].reshape(len(gid), -1) for k in keys], 1).cpu().numpy()
+
+    def reset():
+        for k in keys:
+            getattr(gm, k).copy_(snap[k])
+        eng.eta.copy_(eta0)
+        eng.m.zero_(); eng.v.zero_(); eng.grad.zero_(); eng.step_dev.zero_()
+        eng.step_count = 0
+
+    reset()
+    eng.forward_masked(pose)
+    eng.backward(tc, td, pose)
+    g = eng.grad[: len(gid)].cpu().numpy().copy()
+    eng.optimizer_step()
+    torch.cuda.synchronize()
+    sep, eta_s = rows(), eng.eta.cpu().numpy().copy()
+    reset()
+    eng.forward_masked(pose)
+    eng.backward_adam(tc, td, pose)
+    torch.cuda.synchronize()
+    fus, eta_f = rows(), eng.eta.cpu().numpy().copy()
+    reset()
+    sel = np.abs(g) > 1e-3 * np.abs(g).max(0, keepdims=True)
+    assert sel.sum() > 10000
+    np.testing.assert_allclose(fus[sel], sep[sel], rtol=0, atol=1e-7)
+    np.testing.assert_array_equal(fus[g == 0], sep[g == 0])
+    np.testing.assert_array_equal(eta_f, eta_s)
 
 
 def test_c4_render_only_sampled():
