@@ -1,5 +1,5 @@
 """Summarise an ncu report (raw page) into a compact per-kernel table: time, DRAM bytes, issue
-activity, occupancy and the top stall reasons.  Usage: python scripts/ncu_summary.py report.ncu-rep"""
+activity, occupancy, L2 / shared-memory pipe throughput, L2 atomic sectors and the top stall reasons.  Usage: python scripts/ncu_summary.py report.ncu-rep"""
 import csv
 import io
 import subprocess
@@ -18,6 +18,10 @@ KEYS = [
     ("fma_%", "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", 1),
     ("smem_conf", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", 1),
     ("L2_MB", "lts__t_bytes.sum", None),
+    ("L2_%", "lts__throughput.avg.pct_of_peak_sustained_elapsed", 1),
+    ("smem_%", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed", 1),
+    ("red_sectors_M", "lts__t_sectors_srcunit_tex_op_red.sum", 1e-6),
+    ("atom_sectors_M", "lts__t_sectors_srcunit_tex_op_atom.sum", 1e-6),
 ]
 
 
