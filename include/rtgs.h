@@ -119,7 +119,9 @@ typedef struct {
   float* depth;          /* [H][W]     D^ (Eq.5); -1 where no opaque disc is hit                  */
   float* normal;         /* [3][H][W]  N^ world frame, zero without hit; NULLABLE         */
   int32_t* index;        /* [H][W]     I^: gid of the hit Gaussian or -1                  */
-  uint32_t* n_contrib;   /* [H][W]     sorted-list position just past the last blended entry      */
+  uint32_t* n_contrib;   /* [H][W]     sorted-list position just past the last blended entry (the
+                                        backward's stop); NULLABLE for a FULL render without
+                                        RTGS_RENDER_COUNT, which then skips tracking it              */
   uint32_t* active_bits; /* [ceil(H*W/32)]  M_unstable (Eq.12) — COVERAGE output, MASKED input     */
   uint8_t* tile_keep;    /* [TX*TY]    1 iff >= 50 % of the tile's pixels are active (R15) */
   uint32_t* tile_list;   /* [TX*TY]    ids of kept tiles (order unspecified)                      */

@@ -107,7 +107,8 @@ rtgs_status rtgs_render_color_depth(const rtgs_gaussians* g, const rtgs_projecte
   if (!proj || !proj->rec || !proj->zkey || !a16(proj->rec) || !bins_ok(bins)) return RTGS_ERR_INVALID_ARG;
   // (sub_zkey / sub_gid may be NULL for an empty subset: then no entry carries the subset bit)
   if (bins->sub_rec && !a16(bins->sub_rec)) return RTGS_ERR_INVALID_ARG;
-  if (!out->color || !out->trans || !out->depth || !out->index || !out->n_contrib) return RTGS_ERR_INVALID_ARG;
+  if (!out->color || !out->trans || !out->depth || !out->index) return RTGS_ERR_INVALID_ARG;
+  if (!out->n_contrib && (mode == RTGS_RENDER_MASKED || count)) return RTGS_ERR_INVALID_ARG;
   if (mode == RTGS_RENDER_MASKED && (!out->active_bits || !out->tile_list || !out->counts))
     return RTGS_ERR_INVALID_ARG;
   return finish(launch_render(*proj, *bins, make_pose(*pose), *cam, mode == RTGS_RENDER_MASKED, count, *out,

@@ -207,7 +207,9 @@ struct FwdArgs {
 
 // COUNT: accumulate the blended-pair statistic counts[3] (RTGS_RENDER_COUNT; the production renders of
 // the mapping step do not, saving 3 instructions per survivor)
-template <bool MASKED, bool COUNT>
+// LAST: track n_contrib (the sorted-list position past the last blended entry, which the backward
+// needs); a FULL render for the add masks / tracking only passes n_contrib = NULL and skips it
+template <bool MASKED, bool COUNT, bool LAST = true>
 __global__ void __launch_bounds__(32 * ((MASKED ? kHalfWarps : kTileWarps) + 1)) k_render_fwd(const FwdArgs a) {
   constexpr int NW = MASKED ? kHalfWarps : kTileWarps;  // MASKED: one CTA per half of a kept tile
   __shared__ PipeRing r;  // static: stage addresses fold into immediates
@@ -283,7 +285,7 @@ __global__ void __launch_bounds__(32 * ((MASKED ? kHalfWarps : kTileWarps) + 1))
           cg = __fmaf_rn(r2.y, wgt, cg);
           cb = __fmaf_rn(r2.z, wgt, cb);
           T = ok ? test : T;
-          last = ok ? pbase + (uint32_t)idx : last;
+          if (LAST) last = ok ? pbase + (uint32_t)idx : last;
           if (COUNT) nblend += ok ? 1u : 0u;
         }
         if (__all_sync(0xffffffffu, done)) {
@@ -307,7 +309,7 @@ __global__ void __launch_bounds__(32 * ((MASKED ? kHalfWarps : kTileWarps) + 1))
   a.color[HW + lin] = cg;
   a.color[2 * HW + lin] = cb;
   a.trans[lin] = T;
-  a.n_contrib[lin] = last;
+  if (LAST) a.n_contrib[lin] = last;
   float D = -1.f, N0 = 0.f, N1 = 0.f, N2 = 0.f;
   int32_t gid = -1;
   const uint32_t hit = hitpos >= 0 ? a.sorted_gid[hitpos] : 0xFFFFFFFFu;  // list entry of the hit
@@ -385,7 +387,8 @@ cudaError_t launch_render(const rtgs_projected& proj, const rtgs_bins& bins, con
   if (masked && count) k_render_fwd<true, true><<<2 * T, 32 * (kHalfWarps + 1), 0, s>>>(a);
   else if (masked) k_render_fwd<true, false><<<2 * T, 32 * (kHalfWarps + 1), 0, s>>>(a);
   else if (count) k_render_fwd<false, true><<<T, 32 * (kTileWarps + 1), 0, s>>>(a);
-  else k_render_fwd<false, false><<<T, 32 * (kTileWarps + 1), 0, s>>>(a);
+  else if (out.n_contrib) k_render_fwd<false, false><<<T, 32 * (kTileWarps + 1), 0, s>>>(a);
+  else k_render_fwd<false, false, false><<<T, 32 * (kTileWarps + 1), 0, s>>>(a);
   note_launch();
   return cudaGetLastError();
 }

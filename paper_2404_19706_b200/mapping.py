@@ -168,10 +168,14 @@ class RenderBuffers:
         # FULL / MASKED renders count blended pairs (counts[3], RTGS_RENDER_COUNT) only when asked: the
         # statistic costs instructions per blended pair
         self.count_blends = count_blends
+        # n_contrib is what a backward over this render needs; a FULL render used only for the add
+        # masks / state decisions / tracking can skip tracking it
+        self.track_last = True
 
     def c_struct(self, mode: int | None = None):
+        nc = self.n_contrib if (self.track_last or self.count_blends or mode != RTGS_RENDER_FULL) else None
         return _abi.RenderOut(_p(self.color), _p(self.trans), _p(self.depth), _p(self.normal), _p(self.index),
-                              _p(self.n_contrib), _p(self.active_bits), _p(self.tile_keep), _p(self.tile_list),
+                              _p(nc), _p(self.active_bits), _p(self.tile_keep), _p(self.tile_list),
                               _p(self.counts))
 
     def active_mask(self) -> torch.Tensor:
@@ -540,6 +544,7 @@ class MappingEngine:
         self.proj_full = ProjectedBuffers(n, device)
         self.bins_full = BinBuffers(cam, self.capacity, device)
         self.full = RenderBuffers(cam, device, count_blends=False)  # production FULL render: no statistic
+        self.full.track_last = False  # (A7, f1 states and f4 tracking read no n_contrib)
         self.ws_bin_full = torch.empty(bin_workspace_size(n, cam, self.capacity), dtype=torch.uint8, device=device)
         self.side = torch.cuda.Stream(device=device)
         self.ws_cls = torch.empty(classify_workspace_size(cam), dtype=torch.uint8, device=device)
