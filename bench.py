@@ -313,7 +313,7 @@ def main():
         P.project_and_bin(gm, pose, cam, eng.proj_full, eng.bins_full, eng.ws_bin_full,
                           cache=eng.cache if eng.use_cache else None)
         mark("ingest.project_bin_cache")
-        P.render_color_depth(gm, eng.proj_full, eng.bins_full, pose, cam, P.RTGS_RENDER_FULL, eng.full); mark("ingest.render_full")
+        P.render_color_depth(gm, eng.proj_full, eng.bins_full, pose, cam, P.RTGS_RENDER_FULL, eng.full, normals=False); mark("ingest.render_full")
         P.classify_and_add_pixels(eng.full, col, dep, gm.flags, cam, P.add_params(seed=1234), eng.pixel_class,
                                   eng.samples, eng.add_counts, eng.ws_cls); mark("ingest.classify")
         if eng.use_cache:  # the iteration through the f3 stable cache, as eng.step runs it
@@ -360,7 +360,7 @@ def main():
             flush.zero_()
             hold(0.5)
             e0.record(stream)
-            P.render_color_depth(gm, eng.proj_full, eng.bins_full, pose, cam, P.RTGS_RENDER_FULL, eng.full)
+            P.render_color_depth(gm, eng.proj_full, eng.bins_full, pose, cam, P.RTGS_RENDER_FULL, eng.full, normals=False)
             e1.record(stream)
             torch.cuda.synchronize()
             rt.append(e0.elapsed_time(e1))

@@ -233,10 +233,13 @@ def project_and_bin(gm: GaussianMap, pose: _abi.Pose, cam: _abi.Camera, proj: Pr
 
 
 def render_color_depth(gm: GaussianMap, proj: ProjectedBuffers, bins: BinBuffers | None, pose: _abi.Pose,
-                       cam: _abi.Camera, mode: int, out: RenderBuffers, stream=None):
+                       cam: _abi.Camera, mode: int, out: RenderBuffers, stream=None, normals: bool = True):
+    """A0 / A3-A4.  normals=False leaves out.normal untouched (the normal map is for tracking)."""
     g = gm.c_struct()
     pr = proj.c_struct()
     o = out.c_struct(mode)
+    if not normals:
+        o.normal = None
     b = bins.c_struct() if bins is not None else None
     if out.count_blends and mode in (RTGS_RENDER_FULL, RTGS_RENDER_MASKED):
         mode |= RTGS_RENDER_COUNT
@@ -753,7 +756,8 @@ class MappingEngine:
         if fc is not None:
             fc.ready.record(torch.cuda.current_stream() if stream is None else stream)
             fc.key = _pose_key(pose)
-        render_color_depth(self.gm, self.proj_full, self.bins_full, pose, self.cam, RTGS_RENDER_FULL, self.full, stream)
+        render_color_depth(self.gm, self.proj_full, self.bins_full, pose, self.cam, RTGS_RENDER_FULL, self.full, stream,
+                           normals=False)  # (A7 reads no normals; track() renders its own)
         classify_and_add_pixels(self.full, frame_color, frame_depth, self.gm.flags, self.cam,
                                 add_params(seed=seed, frame_idx=frame_idx), self.pixel_class, self.samples,
                                 self.add_counts, self.ws_cls, stream)
@@ -865,7 +869,8 @@ class MappingEngine:
         fuse_window(self.gm, self.gid_of_slot, self.before, self.eta_before, self.eta, stream)
         project_gaussians(self.gm, pose, self.cam, self.proj_full, stream)
         bin_and_sort(self.proj_full, self.gm.n, self.cam, None, self.bins_full, self.ws_bin_full, stream)
-        render_color_depth(self.gm, self.proj_full, self.bins_full, pose, self.cam, RTGS_RENDER_FULL, self.full, stream)
+        render_color_depth(self.gm, self.proj_full, self.bins_full, pose, self.cam, RTGS_RENDER_FULL, self.full, stream,
+                           normals=False)
         sp = state if state is not None else state_params(frame_idx)
         manage_states(self.full, frame_color, frame_depth, self.cam, self.gm.flags, self.err_count, self.eta,
                       self.t_created, sp, self.state_counts, self.ws_state, stream)
