@@ -568,7 +568,7 @@ def main():
         tp = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tp):
             with open(tp) as f:
-                traffic = json.load(f)
+                traffic = json.load(f).get(cfg.name, {})  # ncu counts of this workload, if captured
         clk_ghz = (clk_sm_mhz or sm_max) * 1e-3
         alu_peak = 148 * 128 * clk_ghz * 1e9 / 1e12
         alu_achieved = 16 * blends_full / t_render_s / 1e12
