@@ -887,9 +887,13 @@ class MappingEngine:
         for i, (c, d, pose) in enumerate(frames):
             self.ingest(c, d, pose, seed=seed, frame_idx=first_frame_idx + i)
             need = int(self.bins_full.n_instances.item())
-            if need > self.capacity:            # the FULL lists were truncated: grow and redo the frame
-                self.reserve_instances(need * 5 // 4)
-                self.ingest(c, d, pose, seed=seed, frame_idx=first_frame_idx + i)
+            # keep 25 % headroom over the FULL lists: the window's iterations bin the map as it is after
+            # ALL the window's insertions, which can exceed an earlier frame's FULL count
+            if need * 5 // 4 > self.capacity:
+                truncated = need > self.capacity
+                self.reserve_instances(need * 3 // 2)
+                if truncated:                   # the FULL lists were cut short: redo the frame
+                    self.ingest(c, d, pose, seed=seed, frame_idx=first_frame_idx + i)
             if insert:
                 self.insert(c, d, pose, frame_idx=first_frame_idx + i)
         self.reset_window()
