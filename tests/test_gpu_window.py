@@ -82,3 +82,25 @@ def test_mapping_from_an_empty_map():
     assert np.isfinite(loss).all() and loss[0] > 0
     s = torch.exp(gm.log_scale).cpu().numpy()
     assert np.isfinite(s).all() and (s > 0).all()
+
+
+def test_window_grows_instance_capacity_ahead_of_the_iterations():
+    """Regression: with an instance capacity just above the first FULL lists, the iterations (which bin
+    the map after ALL the window's insertions) must not overflow: map_window keeps 25 % headroom."""
+    from paper_2404_19706_b200 import build as B
+    B.build()
+    import paper_2404_19706_b200 as P
+    from synth import trajectory_pose
+    cfg = CONFIGS["T2"]
+    scene = make_scene(cfg)
+    gm = P.GaussianMap.from_arrays(scene, capacity=scene["pos"].shape[0] + 20000)
+    eng = P.MappingEngine(gm, P.camera_of(cfg), cache_frames=6, capacity=4 * cfg.n)
+    frames = []
+    for k in range(6):
+        R, t = trajectory_pose(cfg, k)
+        c, d = make_frame(cfg, (R, t))
+        frames.append((torch.as_tensor(c, device="cuda"), torch.as_tensor(d, device="cuda"), P.make_pose(R, t)))
+    for w in range(2):
+        loss = eng.map_window(frames, iterations=10, seed=w, first_frame_idx=6 * w).cpu().numpy()
+        assert np.isfinite(loss).all()
+    assert int(eng.bins.n_instances.item()) <= eng.capacity
