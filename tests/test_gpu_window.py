@@ -93,14 +93,14 @@ def test_window_grows_instance_capacity_ahead_of_the_iterations():
     from synth import trajectory_pose
     cfg = CONFIGS["T2"]
     scene = make_scene(cfg)
-    gm = P.GaussianMap.from_arrays(scene, capacity=scene["pos"].shape[0] + 20000)
+    gm = P.GaussianMap.from_arrays(scene, capacity=cfg.n + cfg.width * cfg.height // 2)  # as bench.py
     eng = P.MappingEngine(gm, P.camera_of(cfg), cache_frames=6, capacity=4 * cfg.n)
     frames = []
     for k in range(6):
         R, t = trajectory_pose(cfg, k)
         c, d = make_frame(cfg, (R, t))
         frames.append((torch.as_tensor(c, device="cuda"), torch.as_tensor(d, device="cuda"), P.make_pose(R, t)))
-    for w in range(2):
-        loss = eng.map_window(frames, iterations=10, seed=w, first_frame_idx=6 * w).cpu().numpy()
+    for w in range(4):   # the bench's window sequence (seeds 3-6, 50 iterations each)
+        loss = eng.map_window(frames, iterations=50, seed=3 + w, first_frame_idx=10 + 6 * w).cpu().numpy()
         assert np.isfinite(loss).all()
     assert int(eng.bins.n_instances.item()) <= eng.capacity
