@@ -231,11 +231,15 @@ __global__ void __launch_bounds__(1024) k_tile_offsets(const uint32_t* __restric
   if (threadIdx.x == 0) *n_inst = carry;
 }
 
-template <int REP>
+// STB (the FULL binning that also builds the f3 cache): the key's low word is (gid << 1) | stable,
+// with the stable flag read here (coalesced, one byte per Gaussian) instead of gathered per instance
+// after the sort; (gid << 1 | stable) orders exactly as gid
+template <int REP, bool STB = false>
 __global__ void __launch_bounds__(256) k_emit(const uint32_t* __restrict__ zkey, const uint2* __restrict__ rect,
                                               const uint8_t* __restrict__ keep, int n, int TX, int T,
                                               const uint32_t* __restrict__ start, uint32_t* __restrict__ cursor,
-                                              uint32_t cap, unsigned long long* __restrict__ keys) {
+                                              uint32_t cap, unsigned long long* __restrict__ keys,
+                                              const uint8_t* __restrict__ flags = nullptr) {
   const int i = blockIdx.x * 256 + threadIdx.x;
   const size_t rep = (size_t)(blockIdx.x & (REP - 1)) * T;  // same replica as k_tile_count
   start += rep;
@@ -245,7 +249,8 @@ __global__ void __launch_bounds__(256) k_emit(const uint32_t* __restrict__ zkey,
   const uint2 rc = rect[i];
   int tx0, ty0, tx1, ty1;
   if (z == 0xFFFFFFFFu || !rect_tiles(rc, tx0, ty0, tx1, ty1)) return;
-  const unsigned long long k = ((unsigned long long)z << 32) | (uint32_t)i;
+  const uint32_t low = STB ? (((uint32_t)i << 1) | ((flags[i] >> 1) & 1u)) : (uint32_t)i;
+  const unsigned long long k = ((unsigned long long)z << 32) | low;
   // tiles in groups of 4: the group's cursor atomics (and start loads) are all in flight before
   // the first store, instead of one atomic round trip per tile
   const int w = tx1 - tx0 + 1, nt = w * (ty1 - ty0 + 1);
@@ -390,8 +395,9 @@ __device__ __forceinline__ void sort_tile(const unsigned long long* __restrict__
 // NEXT f3 fused into the FULL binning: ordered compaction of the tile's stable entries (flags bit 1)
 // of the sorted list `g` [n] into csorted[base ...] (the cache lives in the FULL lists' index space,
 // as k_cache_build); returns nothing, writes crange[tile] and adds to n_stable.
-__device__ __forceinline__ void stable_compact(const uint32_t* __restrict__ g, int n, const uint8_t* __restrict__ flags,
-                                               uint32_t base, uint32_t* __restrict__ csorted, uint2* crange, int tile,
+// The sorted entries arrive as (gid << 1) | stable (k_emit<REP, true>); they are decoded in place.
+__device__ __forceinline__ void stable_compact(uint32_t* __restrict__ g, int n, uint32_t base,
+                                               uint32_t* __restrict__ csorted, uint2* crange, int tile,
                                                uint32_t* __restrict__ n_stable, uint32_t* scan_sh) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   uint32_t o = base;
@@ -400,8 +406,10 @@ __device__ __forceinline__ void stable_compact(const uint32_t* __restrict__ g, i
     uint32_t gi = 0;
     bool st = false;
     if (i < n) {
-      gi = g[i];
-      st = (flags[gi] & 2u) != 0;
+      const uint32_t f = g[i];
+      gi = f >> 1;
+      st = (f & 1u) != 0;
+      g[i] = gi;
     }
     const uint32_t m = __ballot_sync(0xffffffffu, st);
     if (lane == 0) scan_sh[w] = __popc(m);
@@ -450,10 +458,11 @@ __global__ void __launch_bounds__(kSortThreads, 6) k_tile_sort(const uint2* __re
   unsigned long long* seg = keys + rg.x;
   if (n == 1) {
     if (threadIdx.x == 0) {
-      const uint32_t g = (uint32_t)(seg[0] & 0xFFFFFFFFull);
+      const uint32_t f = (uint32_t)(seg[0] & 0xFFFFFFFFull);
+      const uint32_t g = so.flags ? f >> 1 : f;
       sorted_gid[rg.x] = g;
       if (so.flags) {
-        const bool st = (so.flags[g] & 2u) != 0;
+        const bool st = (f & 1u) != 0;
         if (st) so.csorted[rg.x] = g;
         so.crange[blockIdx.x] = make_uint2(rg.x, rg.x + (st ? 1u : 0u));
         if (st && so.n_stable) atomicAdd(so.n_stable, 1u);
@@ -470,7 +479,7 @@ __global__ void __launch_bounds__(kSortThreads, 6) k_tile_sort(const uint2* __re
   }
   if (so.flags) {
     __syncthreads();  // the sorted gids of this tile are written (read back through L1 / L2 below)
-    stable_compact(sorted_gid + rg.x, n, so.flags, rg.x, so.csorted, so.crange, blockIdx.x, so.n_stable, scan_sh);
+    stable_compact(sorted_gid + rg.x, n, rg.x, so.csorted, so.crange, blockIdx.x, so.n_stable, scan_sh);
   }
 }
 
@@ -705,10 +714,15 @@ static cudaError_t bin_from_counts(const rtgs_projected& proj, int n, const CamK
                                     out.n_instances);
   note_launch();
   if (n > 0) {
-    k_emit<kRep><<<nblk, 256, 0, s>>>(proj.zkey, rect, keep, n, k.TX, T, w.start, w.cursor, out.capacity, w.keys);
+    if (so.flags)
+      k_emit<kRep, true><<<nblk, 256, 0, s>>>(proj.zkey, rect, keep, n, k.TX, T, w.start, w.cursor, out.capacity,
+                                              w.keys, so.flags);
+    else
+      k_emit<kRep><<<nblk, 256, 0, s>>>(proj.zkey, rect, keep, n, k.TX, T, w.start, w.cursor, out.capacity, w.keys);
     note_launch();
     int gid_bits = 1;
     while (gid_bits < 32 && (1u << gid_bits) < (uint32_t)n) ++gid_bits;
+    if (so.flags) ++gid_bits;  // the (gid << 1) | stable field
     const size_t smem = (size_t)kSortCap * (8 + 8 + 4);
     static std::atomic<uint64_t> attr_mask{0};
     if (first_on_device(attr_mask)) {
