@@ -1,16 +1,17 @@
 // project.cu — A1: per-Gaussian EWA projection (O1; Eq.2, readings R2-R8, R12).
 //
-// One thread per Gaussian, 128 Gaussians per CTA.  The SH block of the CTA (128 x 12K bytes, the
+// One thread per Gaussian, 64 Gaussians per CTA.  The SH block of the CTA (64 x 12K bytes, the
 // dominant HBM stream: 192 of 237 B/Gaussian at degree 3) is staged into shared memory by ONE 1D
 // bulk copy (cp.async.bulk, TMA engine) completing on an mbarrier, issued before the geometry math
-// so the copy overlaps it; 24 KB of shared memory per CTA keeps 6 CTAs (24 warps) per SM resident,
-// enough bytes in flight for the HBM stream.  Camera-frame position and mu are formed in float64.
+// so the copy overlaps it; 12 KB of shared memory per CTA keeps 12 CTAs (24 warps) per SM resident,
+// and the smaller CTAs keep more independent bulk copies in flight (measured: 56 vs 59 us for
+// 128-thread CTAs at 6 per SM).  Camera-frame position and mu are formed in float64.
 #include "common.cuh"
 #include "internal.h"
 
 namespace rtgs {
 
-constexpr int kProjThreads = 128;
+constexpr int kProjThreads = 64;
 
 struct ProjArgs {
   const float* pos;
@@ -84,7 +85,7 @@ __device__ __forceinline__ float3 sh_eval(const float* c, float x, float y, floa
 }
 
 template <int K, bool SUB>
-__global__ void __launch_bounds__(kProjThreads, 6) k_project(const ProjArgs a) {
+__global__ void __launch_bounds__(kProjThreads, 12) k_project(const ProjArgs a) {
   // s_sh: [kProjThreads][3K] as copied (AoS)
   extern __shared__ __align__(16) float s_sh[];
   __shared__ uint64_t bar;
