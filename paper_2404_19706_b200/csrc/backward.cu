@@ -532,31 +532,33 @@ __device__ __forceinline__ void project_bwd_slot(const PBArgs& a, const float* s
   gout[9] += (gz - dot * qz) * qinv;
 }
 
-// One thread per slot, 128 slots per CTA.  Every input is staged in shared memory first with
+constexpr int kPBS = 32;  // slots per k_project_bwd CTA, one thread each (swept 32 / 64 / 128: ~equal, 32 marginally best)
+
+// One thread per slot, kPBS slots per CTA.  Every input is staged in shared memory first with
 // coalesced loads (screen-space sums, parameters) and one bulk copy per SH row (TMA engine), and the
-// 128 output rows are accumulated into the contiguous grad block with coalesced read-modify-writes.
+// kPBS output rows are accumulated into the contiguous grad block with coalesced read-modify-writes.
 template <int K>
 struct PBSmem {
   static constexpr int D = 10 + 3 * K, LD = D + 1;
   static constexpr int SHF = 3 * K, SHP = (SHF % 4 == 0) ? SHF + 4 : SHF;  // pitch 52: conflict-free LDS.128
-  float sh[128 * SHP];
-  float out[128 * LD];
-  float sg[128 * kSG];
-  float par[128 * 13];
-  int gid[128];
-  uint8_t transparent[128];
+  float sh[kPBS * SHP];
+  float out[kPBS * LD];
+  float sg[kPBS * kSG];
+  float par[kPBS * 13];
+  int gid[kPBS];
+  uint8_t transparent[kPBS];
   uint64_t bar;
 };
 
 template <int K, bool ADAM>
-__global__ void __launch_bounds__(128) k_project_bwd(const PBArgs a) {
+__global__ void __launch_bounds__(kPBS) k_project_bwd(const PBArgs a) {
   using SM = PBSmem<K>;
   constexpr int D = SM::D, LD = SM::LD, SHF = SM::SHF, SHP = SM::SHP;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SM& sm = *reinterpret_cast<SM*>(smem_raw);
   const int tid = threadIdx.x;
-  const int s0 = blockIdx.x * 128;
-  const int ns = min(128, a.n_slots - s0);
+  const int s0 = blockIdx.x * kPBS;
+  const int ns = min(kPBS, a.n_slots - s0);
   if (blockIdx.x == 0 && tid == 0) {  // loss values (device-side, no host sync)
     const float nP = (float)max(1u, a.counts[1]);
     const float Lc = a.acc[0] / (3.f * nP);
@@ -579,29 +581,29 @@ __global__ void __launch_bounds__(128) k_project_bwd(const PBArgs a) {
     __syncthreads();
     if (tid < ns) bulk_g2s(&sm.sh[tid * SHP], a.sh + (size_t)sm.gid[tid] * SHF, SHF * 4, &sm.bar);
   } else {
-    for (int e = tid; e < ns * SHF; e += 128) {
+    for (int e = tid; e < ns * SHF; e += kPBS) {
       const int ls = e / SHF, j = e - ls * SHF;
       sm.sh[ls * SHP + j] = a.sh[(size_t)sm.gid[ls] * SHF + j];
     }
   }
   // (loads batched 8 deep before their stores so that many are in flight per thread)
   constexpr int U = 8;
-  for (int e0 = tid; e0 < ns * kSG; e0 += 128 * U) {
+  for (int e0 = tid; e0 < ns * kSG; e0 += kPBS * U) {
     float v[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int e = e0 + u * 128;
+      const int e = e0 + u * kPBS;
       v[u] = e < ns * kSG ? a.sgrad[(size_t)s0 * kSG + e] : 0.f;
     }
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      if (e0 + u * 128 < ns * kSG) sm.sg[e0 + u * 128] = v[u];
+      if (e0 + u * kPBS < ns * kSG) sm.sg[e0 + u * kPBS] = v[u];
   }
-  for (int e0 = tid; e0 < ns * 13; e0 += 128 * U) {
+  for (int e0 = tid; e0 < ns * 13; e0 += kPBS * U) {
     float v[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int e = e0 + u * 128;
+      const int e = e0 + u * kPBS;
       v[u] = 0.f;
       if (e < ns * 13) {
         const int ls = e / 13, c = e - ls * 13;
@@ -615,7 +617,7 @@ __global__ void __launch_bounds__(128) k_project_bwd(const PBArgs a) {
     }
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      if (e0 + u * 128 < ns * 13) sm.par[e0 + u * 128] = v[u];
+      if (e0 + u * kPBS < ns * 13) sm.par[e0 + u * kPBS] = v[u];
   }
   float* gout = sm.out + tid * LD;
 #pragma unroll
@@ -631,17 +633,17 @@ __global__ void __launch_bounds__(128) k_project_bwd(const PBArgs a) {
     const AdamBC bc = adam_bias(a.h);
     float* M = a.m + (size_t)s0 * D;
     float* Vm = a.v + (size_t)s0 * D;
-    for (int e0 = tid; e0 < ns * D; e0 += 128 * U) {
+    for (int e0 = tid; e0 < ns * D; e0 += kPBS * U) {
       float mo[U], vo[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int e = e0 + u * 128;
+        const int e = e0 + u * kPBS;
         mo[u] = e < ns * D ? M[e] : 0.f;
         vo[u] = e < ns * D ? Vm[e] : 0.f;
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int e = e0 + u * 128;
+        const int e = e0 + u * kPBS;
         if (e < ns * D) {
           const int ls = e / D, j = e - ls * D;
           float gg = sm.out[ls * LD + j];
@@ -659,13 +661,13 @@ __global__ void __launch_bounds__(128) k_project_bwd(const PBArgs a) {
       }
     }
     __syncthreads();
-    for (int e = tid; e < ns * 10; e += 128) {
+    for (int e = tid; e < ns * 10; e += kPBS) {
       const int ls = e / 10, c = e - ls * 10;
       const size_t g = (size_t)sm.gid[ls];
       float* dst = c < 3 ? a.wpos + 3 * g + c : (c < 6 ? a.wlog_scale + 3 * g + (c - 3) : a.wrot + 4 * g + (c - 6));
       *dst = sm.par[ls * 13 + c];
     }
-    for (int e = tid; e < ns * SHF; e += 128) {
+    for (int e = tid; e < ns * SHF; e += kPBS) {
       const int ls = e / SHF, j = e - ls * SHF;
       a.wsh[(size_t)sm.gid[ls] * SHF + j] = sm.sh[ls * SHP + j];
     }
@@ -677,16 +679,16 @@ __global__ void __launch_bounds__(128) k_project_bwd(const PBArgs a) {
     }
   } else {
     float* G = a.grad + (size_t)s0 * D;
-    for (int e0 = tid; e0 < ns * D; e0 += 128 * U) {  // coalesced read-modify-write, 8 loads in flight
+    for (int e0 = tid; e0 < ns * D; e0 += kPBS * U) {  // coalesced read-modify-write, 8 loads in flight
       float g[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int e = e0 + u * 128;
+        const int e = e0 + u * kPBS;
         g[u] = e < ns * D ? G[e] : 0.f;
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int e = e0 + u * 128;
+        const int e = e0 + u * kPBS;
         if (e < ns * D) {
           const int ls = e / D, j = e - ls * D;
           G[e] = g[u] + sm.out[ls * LD + j];
@@ -762,7 +764,7 @@ static cudaError_t enqueue_backward(const rtgs_gaussians& g, const rtgs_projecte
     b.m = fz->m; b.v = fz->v; b.init_geom = fz->init_geom; b.eta = fz->eta;
     b.h = fz->h;
   }
-  const int nb = n_slots > 0 ? (n_slots + 127) / 128 : 1;
+  const int nb = n_slots > 0 ? (n_slots + kPBS - 1) / kPBS : 1;
   static std::atomic<uint64_t> attr_mask{0};
   if (first_on_device(attr_mask)) {
 #define RTGS_PB_ATTR(KK)                                                                                   \
@@ -773,8 +775,8 @@ static cudaError_t enqueue_backward(const rtgs_gaussians& g, const rtgs_projecte
 #undef RTGS_PB_ATTR
   }
 #define RTGS_PB_LAUNCH(KK)                                                                   \
-  if (fz) k_project_bwd<KK, true><<<nb, 128, sizeof(PBSmem<KK>), s>>>(b);                      \
-  else k_project_bwd<KK, false><<<nb, 128, sizeof(PBSmem<KK>), s>>>(b);
+  if (fz) k_project_bwd<KK, true><<<nb, kPBS, sizeof(PBSmem<KK>), s>>>(b);                      \
+  else k_project_bwd<KK, false><<<nb, kPBS, sizeof(PBSmem<KK>), s>>>(b);
   switch (b.K) {
     case 1: RTGS_PB_LAUNCH(1) break;
     case 4: RTGS_PB_LAUNCH(4) break;
