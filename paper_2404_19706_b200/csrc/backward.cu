@@ -72,6 +72,8 @@ struct BwdArgs {
 };
 
 constexpr int kBwdWarps = kHalfWarps;  // one CTA per half of a kept tile
+constexpr int kBwdParts = kTile / (2 * kBwdWarps);  // CTAs per kept tile (each 16 x 2*kBwdWarps px)
+static_assert(kBwdParts == 2 || kBwdParts == 4, "the backward splits a tile in 2 or 4 row bands");
 
 struct BwdSmem {
   PipeRing ring;
@@ -83,9 +85,9 @@ struct BwdSmem {
 __global__ void __launch_bounds__(32 * (kBwdWarps + 1)) k_render_bwd(const BwdArgs a) {
   __shared__ BwdSmem sm;  // static: stage addresses fold into immediates
   PipeRing& r = sm.ring;
-  if ((blockIdx.x >> 1) >= a.counts[0]) return;
-  const int tile = (int)a.tile_list[blockIdx.x >> 1];
-  const int half = blockIdx.x & 1;
+  if ((int)(blockIdx.x / kBwdParts) >= (int)a.counts[0]) return;
+  const int tile = (int)a.tile_list[blockIdx.x / kBwdParts];
+  const int half = blockIdx.x % kBwdParts;  // row band of the tile
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   pipe_init<kBwdWarps>(r);
   if (tid == 0) sm.last_max = 0;
@@ -732,7 +734,7 @@ static cudaError_t enqueue_backward(const rtgs_gaussians& g, const rtgs_projecte
   a.sgrad = sgrad;
   a.acc = acc;
   const int T = a.cam.TX * a.cam.TY;
-  k_render_bwd<<<2 * T, 32 * (kBwdWarps + 1), 0, s>>>(a);
+  k_render_bwd<<<kBwdParts * T, 32 * (kBwdWarps + 1), 0, s>>>(a);
   note_launch();
   PBArgs b;
   b.rec = reinterpret_cast<const float4*>(proj.rec);
