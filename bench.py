@@ -120,13 +120,38 @@ def cpu_baseline(cfg_name: str, n_pixels: int = 48, seed: int = 0):
     py = rng.integers(0, cfg.height, n_pixels)
     pix = np.stack([px, py], 1)
     t1 = time.perf_counter()
+    with torch.no_grad():
+        OR.render_pixels(proj, pix, cam, R, chunk=4, want_margin=False)
+    t_fwd = time.perf_counter() - t1
+    t1 = time.perf_counter()
     out = OR.render_pixels(proj, pix, cam, R, chunk=4, want_margin=False)
     Ct = torch.as_tensor(col[:, py, px].T.astype(np.float64))
     L = (out["color"] - Ct).abs().sum() / (3.0 * n_pixels)
     L.backward()
     t_pix = time.perf_counter() - t1
     # |P| of the C3 iteration ~ the slab share of the image (measured by the GPU arm and passed in)
-    return dict(t_proj=t_proj, t_pix=t_pix, n_pixels=n_pixels, threads=threads)
+    return dict(t_proj=t_proj, t_fwd=t_fwd, t_pix=t_pix, n_pixels=n_pixels, threads=threads)
+
+
+def oracle_step_seconds(r, cfg, n_active):
+    """The oracle doing the bench's step: ingest (projection of all Gaussians + forward render of every
+    pixel) + one uncached mapping iteration (projection again + render/backward of the active pixels)."""
+    n = r["n_pixels"]
+    return 2.0 * r["t_proj"] + r["t_fwd"] * cfg.width * cfg.height / n + r["t_pix"] * n_active / n
+
+
+ORACLE_SAMPLE = ("projection of all {n} Gaussians + forward render of {k} pixels + render/backward of {k} "
+                 "active pixels (float64 torch CPU), extrapolated to the step: 2 projections + forward of all "
+                 "{wh} pixels + render/backward of |P| = {p} active pixels")
+
+
+def workload_name(cfg, cached=True):
+    head = (f"{cfg.name} Replica-shaped {cfg.width}x{cfg.height}, {cfg.n} Gaussians (10% transparent), "
+            f"{int(cfg.frac_unstable * 100)}% unstable slab, SH deg {cfg.sh_degree}; ")
+    if cached:
+        return head + ("step = frame ingest (A1,A2,A3/A4 FULL,A7, f3 stable cache) + one masked mapping "
+                       "iteration (A1 on the unstable slots,A0,A2 merged with the cache,A3/A4,A5,A6)")
+    return head + "step = frame ingest (A1,A2,A3/A4 FULL,A7) + one masked mapping iteration (A1,A0,A2,A3/A4,A5,A6)"
 
 
 def reference_arm(args, rank, world):
@@ -135,11 +160,12 @@ def reference_arm(args, rank, world):
         return
     from synth import CONFIGS
     cfg = CONFIGS[args.config]
-    n_active = args.active_pixels or int(0.12 * cfg.width * cfg.height)
+    # |P| of the C3 step as the GPU arm measures it (bench line `active.active_px`), else 12 % of the image
+    n_active = args.active_pixels or (83249 if args.config == "C3" else int(0.12 * cfg.width * cfg.height))
     times = []
     for s in range(args.warmup + args.steps):
         r = cpu_baseline(args.config, n_pixels=args.ref_pixels, seed=s)
-        t_iter = r["t_proj"] + r["t_pix"] * n_active / r["n_pixels"]
+        t_iter = oracle_step_seconds(r, cfg, n_active)
         if s >= args.warmup:
             times.append(t_iter)
     t = statistics.mean(times)
@@ -147,12 +173,11 @@ def reference_arm(args, rank, world):
     line = {"metric": METRIC, "value": v, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * t, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{args.config} Replica-shaped 1200x680, 1M Gaussians, 10% unstable, full mapping "
-                                   "iteration (oracle sample extrapolated)", "l2": "n/a (CPU)"},
+            "config": {"workload": workload_name(cfg), "l2": "n/a (CPU)"},
             "impl": "reference",
             "cpu_baseline": {"value": v, "unit": "iters/s", "cores": r["threads"], "kind": "oracle",
-                             "sample": f"projection of all {cfg.n} Gaussians + render/backward of {args.ref_pixels} "
-                                       f"active pixels, extrapolated to {n_active} active pixels"},
+                             "sample": ORACLE_SAMPLE.format(n=cfg.n, k=args.ref_pixels, wh=cfg.width * cfg.height,
+                                                            p=n_active)},
             "e2e": {"value": v, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -577,13 +602,7 @@ def main():
             "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"{cfg.name} Replica-shaped {cfg.width}x{cfg.height}, {cfg.n} Gaussians "
-                                   f"(10% transparent), {int(cfg.frac_unstable * 100)}% unstable slab, SH deg "
-                                   f"{cfg.sh_degree}; step = frame ingest (A1,A2,A3/A4 FULL,A7, f3 stable cache) "
-                                   "+ one masked mapping iteration (A1 on the unstable slots,A0,A2 merged with the "
-                                   "cache,A3/A4,A5,A6)" if eng.use_cache else
-                                   f"{cfg.sh_degree}; step = frame ingest (A1,A2,A3/A4 FULL,A7) + one masked "
-                                   "mapping iteration (A1,A0,A2,A3/A4,A5,A6)",
+            "config": {"workload": workload_name(cfg, eng.use_cache),
                        "l2": "flushed between timed steps (256 MB write); Gaussian SoA 237 MB > L2",
                        "launch": "CUDA graph of the whole step (2 streams)" if graph is not None else "eager",
                        "parallelism": f"dp{world} over keyframe views" if world > 1 else "single GPU"},
@@ -629,11 +648,10 @@ def main():
         if world == 1 and not args.no_cpu_baseline:
             try:
                 r = cpu_baseline(args.config, n_pixels=args.ref_pixels)
-                t_cpu = r["t_proj"] + r["t_pix"] * max(counts[1], 1) / r["n_pixels"]
+                t_cpu = oracle_step_seconds(r, cfg, max(counts[1], 1))
                 line["cpu_baseline"] = {"value": 1.0 / t_cpu, "unit": "iters/s", "cores": r["threads"], "kind": "oracle",
-                                        "sample": f"projection of all {cfg.n} Gaussians + render/backward of "
-                                                  f"{r['n_pixels']} active pixels (float64 torch CPU), extrapolated to "
-                                                  f"|P| = {counts[1]} active pixels"}
+                                        "sample": ORACLE_SAMPLE.format(n=cfg.n, k=r["n_pixels"], wh=cfg.width * cfg.height,
+                                                                       p=counts[1])}
             except Exception as e:  # report, never fake
                 line["cpu_baseline"] = {"value": None, "error": repr(e)[:200]}
         print(json.dumps(line), flush=True)
