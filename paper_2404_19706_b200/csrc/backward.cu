@@ -349,9 +349,11 @@ __device__ __forceinline__ void sh_basis_one(int k, float x, float y, float z, f
   }
 }
 
-// chain rule for slot s; accumulates the D = 10 + 3K parameter gradients into gout (zeroed)
-// sg: the slot's 16 screen-space sums; par: pos 3, log-scale 3, rot 4, projected rgb 3; shrow: SH
-// row (all staged in shared memory by the kernel with coalesced / bulk copies)
+// chain rule for slot s; accumulates the 10 geometry gradients into gout[0..9] (zeroed) and stores the
+// SH basis Y_k (gout[10..10+K)) and the clamped colour gradient gc (gout[10+K..13+K)): the 3K SH
+// gradients are the products Y_k * gc_c (sh_grad below), so the staging holds 13 + K floats, not 10 + 3K.
+// sg: the slot's 16 screen-space sums; par: pos 3, log-scale 3, rot 4, projected rgb 3 (staged in
+// shared memory with coalesced loads); shrow: the SH row, read straight from global memory
 template <int K>
 __device__ __forceinline__ void project_bwd_slot(const PBArgs& a, const float* sg, const float* par,
                                                  const float* shrow, float* gout) {
@@ -487,9 +489,7 @@ __device__ __forceinline__ void project_bwd_slot(const PBArgs& a, const float* s
   for (int kk = 0; kk < K; ++kk) {
     float Y, Yx, Yy, Yz;
     sh_basis_one(kk, dirx, diry, dirz, Y, Yx, Yy, Yz);
-    gout[10 + 3 * kk] += Y * gc0;
-    gout[10 + 3 * kk + 1] += Y * gc1;
-    gout[10 + 3 * kk + 2] += Y * gc2;
+    gout[10 + kk] = Y;  // SH gradient (kk, c) = Y_kk * gc_c, formed by the consumer (compact staging)
     const float c = shc[3 * kk] * gc0 + shc[3 * kk + 1] * gc1 + shc[3 * kk + 2] * gc2;
     gd0 += Yx * c;
     gd1 += Yy * c;
@@ -502,6 +502,7 @@ __device__ __forceinline__ void project_bwd_slot(const PBArgs& a, const float* s
     gp1 += (gd1 - dd * diry) * inv;
     gp2 += (gd2 - dd * dirz) * inv;
   }
+  gout[10 + K] = gc0; gout[10 + K + 1] = gc1; gout[10 + K + 2] = gc2;
   gout[0] += gp0; gout[1] += gp1; gout[2] += gp2;
   // Sigma = M M^T, M = R diag(s): dL/dM = 2 dSig M
   float dM[3][3];
@@ -541,9 +542,8 @@ constexpr int kPBS = 32;  // slots per k_project_bwd CTA, one thread each (swept
 // kPBS output rows are accumulated into the contiguous grad block with coalesced read-modify-writes.
 template <int K>
 struct PBSmem {
-  static constexpr int D = 10 + 3 * K, LD = D + 1;
-  static constexpr int SHF = 3 * K, SHP = (SHF % 4 == 0) ? SHF + 4 : SHF;  // pitch 52: conflict-free LDS.128
-  float sh[kPBS * SHP];
+  static constexpr int D = 10 + 3 * K, LD = (13 + K) | 1;  // compact row: 10 geometry, K basis, 3 gc
+  static constexpr int SHF = 3 * K;
   float out[kPBS * LD];
   float sg[kPBS * kSG];
   float par[kPBS * 13];
@@ -552,10 +552,20 @@ struct PBSmem {
   uint64_t bar;
 };
 
+// gradient j (0 <= j < 10 + 3K) of a compact staging row
+template <int K>
+__device__ __forceinline__ float sh_grad(const float* row, int j) {
+  if (j < 10) return row[j];
+  const int kk = (j - 10) / 3, c = (j - 10) - 3 * kk;
+  return row[10 + kk] * row[10 + K + c];
+}
+
+// 22 resident 32-slot CTAs per SM (<= 88 registers, ~8 KB shared): 148 x 22 x 32 = 104k slots in
+// one wave, so the C3 iteration's 100k unstable slots do not pay a second wave of CTA latency
 template <int K, bool ADAM>
-__global__ void __launch_bounds__(kPBS) k_project_bwd(const PBArgs a) {
+__global__ void __launch_bounds__(kPBS, 22) k_project_bwd(const PBArgs a) {
   using SM = PBSmem<K>;
-  constexpr int D = SM::D, LD = SM::LD, SHF = SM::SHF, SHP = SM::SHP;
+  constexpr int D = SM::D, LD = SM::LD, SHF = SM::SHF;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SM& sm = *reinterpret_cast<SM*>(smem_raw);
   const int tid = threadIdx.x;
@@ -573,21 +583,7 @@ __global__ void __launch_bounds__(kPBS) k_project_bwd(const PBArgs a) {
   if (ns <= 0) return;
   if (tid < ns) sm.gid[tid] = a.gid_of_slot[s0 + tid];
   if (ADAM && tid < ns) sm.transparent[tid] = a.flags[sm.gid[tid]] & 1u;
-  if (tid == 0) {
-    mbar_init(&sm.bar, 1);
-    fence_mbar_init();
-  }
   __syncthreads();
-  if constexpr (SHF % 4 == 0) {
-    if (tid == 0) mbar_arrive_expect_tx(&sm.bar, (uint32_t)(ns * SHF * 4));
-    __syncthreads();
-    if (tid < ns) bulk_g2s(&sm.sh[tid * SHP], a.sh + (size_t)sm.gid[tid] * SHF, SHF * 4, &sm.bar);
-  } else {
-    for (int e = tid; e < ns * SHF; e += kPBS) {
-      const int ls = e / SHF, j = e - ls * SHF;
-      sm.sh[ls * SHP + j] = a.sh[(size_t)sm.gid[ls] * SHF + j];
-    }
-  }
   // (loads batched 8 deep before their stores so that many are in flight per thread)
   constexpr int U = 8;
   for (int e0 = tid; e0 < ns * kSG; e0 += kPBS * U) {
@@ -623,10 +619,9 @@ __global__ void __launch_bounds__(kPBS) k_project_bwd(const PBArgs a) {
   }
   float* gout = sm.out + tid * LD;
 #pragma unroll
-  for (int j = 0; j < D; ++j) gout[j] = 0.f;
+  for (int j = 0; j < 13 + K; ++j) gout[j] = 0.f;
   __syncthreads();
-  if constexpr (SHF % 4 == 0) mbar_wait(&sm.bar, 0);
-  if (tid < ns) project_bwd_slot<K>(a, sm.sg + tid * kSG, sm.par + tid * 13, sm.sh + tid * SHP, gout);
+  if (tid < ns) project_bwd_slot<K>(a, sm.sg + tid * kSG, sm.par + tid * 13, a.sh + (size_t)sm.gid[tid] * SHF, gout);
   __syncthreads();
   if constexpr (ADAM) {
     // A6 on the staged rows (the same update as k_adam, adam.cuh): the slot gradient never leaves
@@ -648,15 +643,17 @@ __global__ void __launch_bounds__(kPBS) k_project_bwd(const PBArgs a) {
         const int e = e0 + u * kPBS;
         if (e < ns * D) {
           const int ls = e / D, j = e - ls * D;
-          float gg = sm.out[ls * LD + j];
-          float* pth = j < 10 ? &sm.par[ls * 13 + j] : &sm.sh[ls * SHP + (j - 10)];
-          const float th = *pth;
+          float gg = sh_grad<K>(sm.out + ls * LD, j);
+          const size_t shi = (size_t)sm.gid[ls] * SHF + (j - 10);
+          const float th = j < 10 ? sm.par[ls * 13 + j] : a.sh[shi];
           if (j < 10 && sm.transparent[ls]) {  // L_reg (R18)
             const float th0 = a.init_geom ? a.init_geom[(size_t)(s0 + ls) * 10 + j] : 0.f;
             gg += a.h.reg_coef * (th - th0);
           }
           float mm = mo[u], vv = vo[u];
-          *pth = adam_one(a.h, bc, adam_lr(a.h, j), th, gg, mm, vv);
+          const float nt = adam_one(a.h, bc, adam_lr(a.h, j), th, gg, mm, vv);
+          if (j < 10) sm.par[ls * 13 + j] = nt;
+          else a.wsh[shi] = nt;
           M[e] = mm;
           Vm[e] = vv;
         }
@@ -669,14 +666,10 @@ __global__ void __launch_bounds__(kPBS) k_project_bwd(const PBArgs a) {
       float* dst = c < 3 ? a.wpos + 3 * g + c : (c < 6 ? a.wlog_scale + 3 * g + (c - 3) : a.wrot + 4 * g + (c - 6));
       *dst = sm.par[ls * 13 + c];
     }
-    for (int e = tid; e < ns * SHF; e += kPBS) {
-      const int ls = e / SHF, j = e - ls * SHF;
-      a.wsh[(size_t)sm.gid[ls] * SHF + j] = sm.sh[ls * SHP + j];
-    }
     if (tid < ns) {  // eta += 1 once per slot with a non-zero SH gradient (R20)
       bool nz = false;
 #pragma unroll 8
-      for (int j = 0; j < SHF; ++j) nz |= sm.out[tid * LD + 10 + j] != 0.f;
+      for (int j = 0; j < SHF; ++j) nz |= sh_grad<K>(sm.out + tid * LD, 10 + j) != 0.f;
       if (nz) a.eta[sm.gid[tid]] += 1u;
     }
   } else {
@@ -693,7 +686,7 @@ __global__ void __launch_bounds__(kPBS) k_project_bwd(const PBArgs a) {
         const int e = e0 + u * kPBS;
         if (e < ns * D) {
           const int ls = e / D, j = e - ls * D;
-          G[e] = g[u] + sm.out[ls * LD + j];
+          G[e] = g[u] + sh_grad<K>(sm.out + ls * LD, j);
         }
       }
     }
