@@ -537,9 +537,10 @@ __device__ __forceinline__ void project_bwd_slot(const PBArgs& a, const float* s
 
 constexpr int kPBS = 32;  // slots per k_project_bwd CTA, one thread each (swept 32 / 64 / 128: ~equal, 32 marginally best)
 
-// One thread per slot, kPBS slots per CTA.  Every input is staged in shared memory first with
-// coalesced loads (screen-space sums, parameters) and one bulk copy per SH row (TMA engine), and the
-// kPBS output rows are accumulated into the contiguous grad block with coalesced read-modify-writes.
+// One thread per slot, kPBS slots per CTA.  The screen-space sums and the geometry parameters are
+// staged in shared memory with coalesced loads; each thread reads its SH row straight from global
+// memory (LDG.128; staging it cost residency: DESIGN.md §10), and the kPBS compact gradient rows are
+// accumulated into the contiguous grad block with coalesced read-modify-writes.
 template <int K>
 struct PBSmem {
   static constexpr int D = 10 + 3 * K, LD = (13 + K) | 1;  // compact row: 10 geometry, K basis, 3 gc
@@ -624,7 +625,8 @@ __global__ void __launch_bounds__(kPBS, 22) k_project_bwd(const PBArgs a) {
   if (tid < ns) project_bwd_slot<K>(a, sm.sg + tid * kSG, sm.par + tid * 13, a.sh + (size_t)sm.gid[tid] * SHF, gout);
   __syncthreads();
   if constexpr (ADAM) {
-    // A6 on the staged rows (the same update as k_adam, adam.cuh): the slot gradient never leaves
+    // A6 on the staged rows (the same update as k_adam, adam.cuh; SH updated in place in global
+    // memory, each element read and written by one thread): the slot gradient never leaves
     // shared memory; m / v stream coalesced over the CTA's contiguous [ns x D] block, the new
     // parameters go back into the staging and are written out below.
     const AdamBC bc = adam_bias(a.h);
