@@ -60,9 +60,48 @@ def slot_grads(params: dict, gid_of_slot: np.ndarray) -> np.ndarray:
 
 
 def iteration_grads(scene, R, t, cam, target_color, target_depth, active_img, gid_of_slot,
-                    w_c=1.0, w_d=1.0):
+                    w_c=1.0, w_d=1.0, mass=False):
+    """Gradients of L in the slot layout; with mass=True also the absolute gradient mass
+    M[slot, coord] = sum_{u in P} |d l_u / d theta| of the per-pixel loss terms l_u (sum_u l_u = L),
+    the scale a float32 sum of those per-pixel terms is rounded against.
+
+    The mass is evaluated exactly, group by group: pixels are split into the S x S residue classes of
+    (px mod S, py mod S) with S = the largest support-rect side of the non-culled Gaussians, so two
+    pixels of one class never lie in the same Gaussian's rect (R7: the rect holds the whole support,
+    and l_u depends on Gaussian i only if u lies in rect_i).  The gradient of a class's summed loss
+    therefore has, per coordinate, a single non-zero pixel term, and |sum| = sum |.| there."""
     res = iteration_loss(scene, R, t, cam, target_color, target_depth, active_img, w_c, w_d)
     if res["n_P"]:
         res["L"].backward()
     res["grad"] = slot_grads(res["params"], gid_of_slot)
+    if mass:
+        res["mass"] = _abs_mass(scene, R, t, cam, target_color, target_depth, active_img, gid_of_slot, w_c, w_d,
+                                res)
     return res
+
+
+def _abs_mass(scene, R, t, cam, target_color, target_depth, active_img, gid_of_slot, w_c, w_d, res):
+    M = np.zeros_like(res["grad"])
+    n_p, n_pd = res["n_P"], res["n_Pd"]
+    if n_p == 0:
+        return M
+    pr = res["proj"]
+    rect = pr["rect"][pr["valid"] & (pr["tiles_touched"] > 0)]
+    S = int(max(1, (rect[:, 2] - rect[:, 0] + 1).max(initial=1), (rect[:, 3] - rect[:, 1] + 1).max(initial=1)))
+    pix = res["pixels"]
+    cls = (pix[:, 1] % S) * S + (pix[:, 0] % S)
+    C_all = np.asarray(target_color, dtype=np.float64)
+    D_all = np.asarray(target_depth, dtype=np.float64)
+    for c in np.unique(cls):
+        sub = pix[cls == c]
+        params = projection.params_from_scene(scene, requires_grad=True)
+        proj = projection.project(params, R, t, cam, scene["sh_degree"])
+        out = raster.render_pixels(proj, sub, cam, R, want_margin=False)
+        C_t = torch.as_tensor(C_all[:, sub[:, 1], sub[:, 0]].T)
+        D_np = D_all[sub[:, 1], sub[:, 0]]
+        dval = torch.as_tensor((out["index"] >= 0) & np.isfinite(D_np) & (D_np > 0))
+        l = (w_c / (3.0 * n_p)) * (out["color"] - C_t).abs().sum() + (w_d / max(n_pd, 1)) * torch.where(
+            dval, (out["depth"] - torch.as_tensor(D_np)).abs(), torch.zeros(len(sub), dtype=torch.float64)).sum()
+        l.backward()
+        M += np.abs(slot_grads(params, gid_of_slot))
+    return M

@@ -3,9 +3,9 @@
 //
 // K5 k_render_bwd: one CTA per half of a kept tile (4 consumer warps + 1 producer; same geometry and
 //   batching as the MASKED forward).  Each active
-//   pixel REPLAYS the forward front to back with the identical arithmetic (eval_pair), so T_i and
-//   every decision are bit-identical to the forward; the colour suffix S_i = C^ - prefix_i comes from
-//   the stored C^.  For every UNSTABLE record a warp touches, the 8 screen-space gradients
+//   pixel walks its blended entries BACK TO FRONT with the forward's arithmetic (eval_pair), so every
+//   decision is the forward's; T_i is recovered from the stored T^ by division and the colour suffix
+//   S_i is summed from the back (no C^ - prefix cancellation).  For every UNSTABLE record a warp touches, the 8 screen-space gradients
 //   (mu 2, conic 3, rgb 3) are reduced over the warp with shuffles and added with one red.global
 //   per value.  Depth gradients go to the single hit Gaussian of each pixel (Eq.4-5).
 // K5b k_project_bwd: one thread per slot: chain rule from the screen-space gradients through
@@ -59,6 +59,7 @@ struct BwdArgs {
   const uint32_t* counts;
   const uint32_t* active;
   const float* color;
+  const float* trans;
   const float* depth;
   const int32_t* index;
   const uint32_t* n_contrib;
@@ -126,19 +127,30 @@ __global__ void __launch_bounds__(32 * (kBwdWarps + 1)) k_render_bwd(const BwdAr
       const float gD = dd > 0.f ? 1.f : (dd < 0.f ? -1.f : 0.f);  // scaled by w_d / |P_d| in K5b
       const int slot = a.slot_of_gid[hit];
       if (slot >= 0 && gD != 0.f) {
-        const float4 pl = a.sub_rec ? a.sub_rec[(size_t)4 * slot + 3] : a.rec[(size_t)4 * hit + 3];
+        const float4* hr = a.sub_rec ? a.sub_rec + (size_t)4 * slot : a.rec + (size_t)4 * hit;
+        const float4 pl = hr[3];  // n_c, n_c . p_c
         const float rx = (fpx - a.cam.cx) / a.cam.fx, ry = (fpy - a.cam.cy) / a.cam.fy;
         const float ndr = pl.x * rx + pl.y * ry + pl.z;
         const float nn = sqrtf(pl.x * pl.x + pl.y * pl.y + pl.z * pl.z);
         const float cosang = fabsf(ndr) / (sqrtf(rx * rx + ry * ry + 1.f) * nn);
         float* sg = a.sgrad + (size_t)slot * kSG;
         if (cosang > kCos60) {
-          // D = (n.p)/(n.r): dD/dp_c = n/(n.r), dD/dn_c = (p_c - D r)/(n.r)
+          // D = (n.p)/(n.r): dD/dp_c = n/(n.r), dD/dn_c = (p_c - D r)/(n.r).  p_c - D r is the
+          // in-plane offset from the ray's hit to the disc centre (mm) between two ~metre vectors:
+          // formed from the small pixel offset delta = ((mu_x - u_x)/f_x, (mu_y - u_y)/f_y, 0)
+          // (p_c = z_c (r + delta)):  p_c - D r = z_c (delta - (n.delta / n.r) r),
+          // z_c = D (n.r) / (n.r + n.delta), so no metre-sized terms cancel in the sums.
           const float q = gD / ndr;
+          const float4 m = hr[0];  // mu hi, lo
+          const float ddx = __fadd_rn(__fsub_rn(m.x, fpx), m.z) / a.cam.fx;
+          const float ddy = __fadd_rn(__fsub_rn(m.y, fpy), m.w) / a.cam.fy;
+          const float ndd = pl.x * ddx + pl.y * ddy;
+          const float kk = ndd / ndr;
+          const float qz = q * (Dh * ndr / (ndr + ndd));  // q z_c
           atomicAdd(sg + 8, q);
-          atomicAdd(sg + 9, q * Dh * rx);
-          atomicAdd(sg + 10, q * Dh * ry);
-          atomicAdd(sg + 11, q * Dh);
+          atomicAdd(sg + 9, qz * (ddx - kk * rx));
+          atomicAdd(sg + 10, qz * (ddy - kk * ry));
+          atomicAdd(sg + 11, -qz * kk);
         } else {
           atomicAdd(sg + 12, gD);  // D = z: dD/dp_c = e_z
         }
@@ -167,68 +179,67 @@ __global__ void __launch_bounds__(32 * (kBwdWarps + 1)) k_render_bwd(const BwdAr
       if (!(g & kSubBit)) cp_async4(&sm.slot[st][j], slot_of_gid + g);
     };
     auto flush = [](int, int) {};
-    pipe_produce(r, a.rec, a.sub_rec, a.sorted_gid, start, end, extra, flush);
+    pipe_produce<true>(r, a.rec, a.sub_rec, a.sorted_gid, start, end, extra, flush);
     return;
   }
 
-  bool done = !want;
+  // BACK-TO-FRONT pass over the pixel's blended entries (positions < last, the forward's n_contrib):
+  // the decisions are the forward's (eval_pair is the same arithmetic; termination is encoded in
+  // `last`), and T_i is recovered from the stored final T^ as T_i = T_{i+1} / (1 - f_i).  With
+  // G_i = sum_c gC_c c_i,c the colour cotangent of entry i, the colour seen BEHIND entry i is
+  //   B_i = sum_{j>i} G_j f_j prod_{i<k<j} (1 - f_k),   B_{i-1} = f_i G_i + (1 - f_i) B_i,  B_last = 0
+  // (black background, R23) -- a convex-combination recursion from the back, no division by T -- and
+  //   dL/df_i = sum_c gC_c (c_i,c T_i - S_i,c / (1 - f_i)) = T_i (G_i - B_i)      (Eq.1, Eq.3)
+  // since S_i = T_{i+1} B_i.  The difference G_i - B_i is the pixel's own cancellation (a Gaussian in
+  // front of a similar colour); forming it between two O(1) values keeps its error at float32
+  // rounding of G, not of the T-scaled partial sums (no C^ - prefix, no S / (1 - f) amplification).
   const float bx0 = (float)wx0, bx1 = (float)(wx0 + 7), by0 = (float)wy0, by1 = (float)(wy0 + 3);
   const int nb = n > 0 ? (n + kPipeBatch - 1) / kPipeBatch : 0;
   const uint32_t rec0 = pin(smem_u32(&r.rec[0][0][0])), slot0 = pin(smem_u32(&sm.slot[0][0]));
   const uint32_t gid0 = pin(smem_u32(&r.gid[0][0]));
   const int plane = (int)pin((uint32_t)lane);
-  // dL/df_i = sum_c gC_c (c_i,c T_i - S_i,c / (1 - f_i)), S_i = C^ - prefix_i, folded into scalars:
-  // G_i = sum_c gC_c c_i,c, A = sum_c gC_c prefix_c (one running sum), K0 = sum_c gC_c C^_c, so
-  // dL/df_i = T_i G_i - (K0 - A) / (1 - f_i)
-  const float K0 = __fmaf_rn(gCb, Cb, __fmaf_rn(gCg, Cg, gCr * Cr));
-  float T = 1.f, A = 0.f;
-  bool wdone = __all_sync(0xffffffffu, done);
-  if (wdone && lane == 0) atomicSub(&r.alive, 1);
+  float T = want ? a.trans[lin] : 1.f;  // T after the last blended entry = the forward's T^
+  float B = 0.f;                         // colour cotangent behind the current entry
+  const uint32_t mylast = want ? last : 0u;
+  const uint32_t wlast = __reduce_max_sync(0xffffffffu, mylast);  // this warp's entries: [start, wlast)
   for (int b = 0; b < nb; ++b) {
     const int st = b % kPipeStages;
     mbar_wait(&r.full[st], (uint32_t)(b / kPipeStages) & 1u);
-    if (!wdone) {
+    const int lo = pipe_batch_lo(true, start, end, b);
+    if ((uint32_t)lo < wlast) {  // warp-uniform: the batch holds entries of this warp's pixels
       const uint32_t srec = rec0 + (uint32_t)(st * sizeof(r.rec[0]));  // shared addresses of this stage
       const uint32_t sslot = slot0 + (uint32_t)(st * sizeof(sm.slot[0]));
       const uint32_t sgid = gid0 + (uint32_t)(st * sizeof(r.gid[0]));
-      const uint32_t pbase = (uint32_t)(start + b * kPipeBatch);
-      const int cnt = min(kPipeBatch, n - b * kPipeBatch);
-      for (int g0 = 0; g0 < cnt; g0 += 32) {
+      const int cnt = pipe_batch_cnt(true, start, end, b);
+      for (int g0 = (cnt - 1) & ~31; g0 >= 0; g0 -= 32) {
         const int j = g0 + lane;
         bool ov = false;
-        if (j < cnt) {
+        if (j < cnt && (uint32_t)(lo + j) < wlast) {
           const float4 r0 = lds128(srec + 48u * j);
           const float2 ext = unpack_ext(__uint_as_float(lds32(srec + 48u * j + 44u)));
           ov = (r0.x + ext.x >= bx0) && (r0.x - ext.x <= bx1) && (r0.y + ext.y >= by0) && (r0.y - ext.y <= by1);
         }
         uint32_t m = __ballot_sync(0xffffffffu, ov);
         while (m) {
-          const int idx = g0 + __ffs(m) - 1;
-          m &= m - 1;
+          const int bit = 31 - __clz(m);  // back to front
+          m ^= 1u << bit;
+          const int idx = g0 + bit;
           const uint32_t ent = lds32(sgid + 4u * idx);  // warp-uniform
           const int slot = (ent & kSubBit) ? (int)(ent & ~kSubBit) : (int)lds32(sslot + 4u * idx);
-          // branch-free replay of record idx (identical arithmetic and decisions to the forward)
           const uint32_t ra = srec + 48u * idx;
           const float4 r0 = lds128(ra), r1 = lds128(ra + 16u), r2 = lds128(ra + 32u);
-          const bool past = pbase + (uint32_t)idx >= last;  // beyond the last blended entry
-          done = done || past;
           PairEval e;
-          bool ok = eval_pair(r0, r1, fpx, fpy, e) && !done;
-          const float test = __fmul_rn(T, __fsub_rn(1.f, e.f));
-          const bool term = ok && (test < kTMin);
-          done = done || term;
-          ok = ok && !term;
-          const float wgt = ok ? __fmul_rn(e.f, T) : 0.f;
+          // blended in the forward <=> passes the support test and lies before the pixel's `last`
+          const bool ok = eval_pair(r0, r1, fpx, fpy, e) && ((uint32_t)(lo + idx) < mylast);
+          const float inv1mf = __frcp_rn(__fsub_rn(1.f, e.f));  // IEEE reciprocal; 1 - f >= 0.01
+          const float Ti = ok ? __fmul_rn(T, inv1mf) : T;        // T before entry i
+          const float wgt = ok ? __fmul_rn(e.f, Ti) : 0.f;
           const float G = __fmaf_rn(gCb, r2.z, __fmaf_rn(gCg, r2.y, gCr * r2.x));
-          A = __fmaf_rn(G, wgt, A);
           const uint32_t okm = __ballot_sync(0xffffffffu, ok);
           if (slot >= 0 && okm) {
             float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
             if (ok) {
-              // S_i = sum_{j>i} c_j f_j T_j = C^ - prefix_i ;  dC/df_i = c_i T_i - S_i / (1 - f_i)
-              float inv1mf;  // 1 - f >= 0.01: the approximate reciprocal needs no range fix-up
-              asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv1mf) : "f"(1.f - e.f));
-              const float dLdf = T * G - (K0 - A) * inv1mf;
+              const float dLdf = __fmul_rn(Ti, __fsub_rn(G, B));
               // f = alpha e^power; the 0.99 cap passes no gradient when active (R17)
               const float dLdp = (e.f < kFMax) ? dLdf * e.f : 0.f;
               // power = p2 / log2(e): d power / d dx = (2 A' dx + B' dy) / log2(e) = -(A dx + B dy)
@@ -256,12 +267,8 @@ __global__ void __launch_bounds__(32 * (kBwdWarps + 1)) k_render_bwd(const BwdAr
               if ((plane & 3) == 0) atomicAdd(sg + vj, x);  // 8 lanes, 8 values
             }
           }
-          T = ok ? test : T;
-        }
-        if (__all_sync(0xffffffffu, done)) {
-          wdone = true;
-          if (lane == 0) atomicSub(&r.alive, 1);
-          break;
+          B = ok ? __fmaf_rn(e.f, __fsub_rn(G, B), B) : B;  // f G + (1 - f) B
+          T = Ti;
         }
       }
     }
@@ -309,17 +316,19 @@ struct PBArgs {
 };
 
 // Y_k(d) and its gradient for ONE coefficient k (a compile-time constant after unrolling): the 3DGS
-// real basis (R2), constants restated from their closed forms.
-__device__ __forceinline__ void sh_basis_one(int k, float x, float y, float z, float& Y, float& dx, float& dy,
-                                             float& dz) {
-  const float C0 = 0.28209479177387814f, C1 = 0.4886025119029199f;
-  const float C20 = 1.0925484305920792f, C21 = -1.0925484305920792f, C22 = 0.31539156525252005f,
-              C23 = -1.0925484305920792f, C24 = 0.5462742152960396f;
-  const float C30 = -0.5900435899266435f, C31 = 2.890611442640554f, C32 = -0.4570457994644658f,
-              C33 = 0.3731763325901154f, C34 = -0.4570457994644658f, C35 = 1.445305721320277f,
-              C36 = -0.5900435899266435f;
-  const float xx = x * x, yy = y * y, zz = z * z;
-  dx = dy = dz = 0.f;
+// real basis (R2), constants restated from their closed forms.  Evaluated in double by the chain rule:
+// the higher bands cancel (2z^2 - x^2 - y^2, x^2 - y^2, ...), and a float32 direction would carry
+// that cancellation's relative error into the SH gradient Y_k * dL/drgb.
+template <typename S>
+__device__ __forceinline__ void sh_basis_one(int k, S x, S y, S z, S& Y, S& dx, S& dy, S& dz) {
+  const S C0 = 0.28209479177387814, C1 = 0.4886025119029199;
+  const S C20 = 1.0925484305920792, C21 = -1.0925484305920792, C22 = 0.31539156525252005,
+          C23 = -1.0925484305920792, C24 = 0.5462742152960396;
+  const S C30 = -0.5900435899266435, C31 = 2.890611442640554, C32 = -0.4570457994644658,
+          C33 = 0.3731763325901154, C34 = -0.4570457994644658, C35 = 1.445305721320277,
+          C36 = -0.5900435899266435;
+  const S xx = x * x, yy = y * y, zz = z * z;
+  dx = dy = dz = S(0);
   switch (k) {
     case 0: Y = C0; break;
     case 1: Y = -C1 * y; dy = -C1; break;
@@ -327,25 +336,25 @@ __device__ __forceinline__ void sh_basis_one(int k, float x, float y, float z, f
     case 3: Y = -C1 * x; dx = -C1; break;
     case 4: Y = C20 * x * y; dx = C20 * y; dy = C20 * x; break;
     case 5: Y = C21 * y * z; dy = C21 * z; dz = C21 * y; break;
-    case 6: Y = C22 * (2.f * zz - xx - yy); dx = -2.f * C22 * x; dy = -2.f * C22 * y; dz = 4.f * C22 * z; break;
+    case 6: Y = C22 * (2.0 * zz - xx - yy); dx = -2.0 * C22 * x; dy = -2.0 * C22 * y; dz = 4.0 * C22 * z; break;
     case 7: Y = C23 * x * z; dx = C23 * z; dz = C23 * x; break;
-    case 8: Y = C24 * (xx - yy); dx = 2.f * C24 * x; dy = -2.f * C24 * y; break;
-    case 9: Y = C30 * y * (3.f * xx - yy); dx = 6.f * C30 * x * y; dy = C30 * (3.f * xx - 3.f * yy); break;
+    case 8: Y = C24 * (xx - yy); dx = 2.0 * C24 * x; dy = -2.0 * C24 * y; break;
+    case 9: Y = C30 * y * (3.0 * xx - yy); dx = 6.0 * C30 * x * y; dy = C30 * (3.0 * xx - 3.0 * yy); break;
     case 10: Y = C31 * x * y * z; dx = C31 * y * z; dy = C31 * x * z; dz = C31 * x * y; break;
     case 11:
-      Y = C32 * y * (4.f * zz - xx - yy);
-      dx = -2.f * C32 * x * y; dy = C32 * (4.f * zz - xx - 3.f * yy); dz = 8.f * C32 * y * z;
+      Y = C32 * y * (4.0 * zz - xx - yy);
+      dx = -2.0 * C32 * x * y; dy = C32 * (4.0 * zz - xx - 3.0 * yy); dz = 8.0 * C32 * y * z;
       break;
     case 12:
-      Y = C33 * z * (2.f * zz - 3.f * xx - 3.f * yy);
-      dx = -6.f * C33 * x * z; dy = -6.f * C33 * y * z; dz = C33 * (6.f * zz - 3.f * xx - 3.f * yy);
+      Y = C33 * z * (2.0 * zz - 3.0 * xx - 3.0 * yy);
+      dx = -6.0 * C33 * x * z; dy = -6.0 * C33 * y * z; dz = C33 * (6.0 * zz - 3.0 * xx - 3.0 * yy);
       break;
     case 13:
-      Y = C34 * x * (4.f * zz - xx - yy);
-      dx = C34 * (4.f * zz - 3.f * xx - yy); dy = -2.f * C34 * x * y; dz = 8.f * C34 * x * z;
+      Y = C34 * x * (4.0 * zz - xx - yy);
+      dx = C34 * (4.0 * zz - 3.0 * xx - yy); dy = -2.0 * C34 * x * y; dz = 8.0 * C34 * x * z;
       break;
-    case 14: Y = C35 * z * (xx - yy); dx = 2.f * C35 * x * z; dy = -2.f * C35 * y * z; dz = C35 * (xx - yy); break;
-    default: Y = C36 * x * (xx - 3.f * yy); dx = C36 * (3.f * xx - 3.f * yy); dy = -6.f * C36 * x * y; break;
+    case 14: Y = C35 * z * (xx - yy); dx = 2.0 * C35 * x * z; dy = -2.0 * C35 * y * z; dz = C35 * (xx - yy); break;
+    default: Y = C36 * x * (xx - 3.0 * yy); dx = C36 * (3.0 * xx - 3.0 * yy); dy = -6.0 * C36 * x * y; break;
   }
 }
 
@@ -354,6 +363,20 @@ __device__ __forceinline__ void sh_basis_one(int k, float x, float y, float z, f
 // gradients are the products Y_k * gc_c (sh_grad below), so the staging holds 13 + K floats, not 10 + 3K.
 // sg: the slot's 16 screen-space sums; par: pos 3, log-scale 3, rot 4, projected rgb 3 (staged in
 // shared memory with coalesced loads); shrow: the SH row, read straight from global memory
+// Precision of the geometry part of the chain rule: float32 (the default) passes the strict gradient
+// contract once K5 forms its sums without cancellation (behind-colour recursion, in-plane depth
+// offsets); RTGS_BWD_F64=1 runs it in double (12 CTAs / SM without spills) for diagnosis.
+#ifndef RTGS_BWD_F64
+#define RTGS_BWD_F64 0
+#endif
+#if RTGS_BWD_F64
+using Fp = double;
+#define RTGS_PB_V a.V
+#else
+using Fp = float;
+#define RTGS_PB_V a.Vf
+#endif
+
 template <int K>
 __device__ __forceinline__ void project_bwd_slot(const PBArgs& a, const float* sg, const float* par,
                                                  const float* shrow, float* gout) {
@@ -364,111 +387,113 @@ __device__ __forceinline__ void project_bwd_slot(const PBArgs& a, const float* s
   const float dscale = a.w_d / fmaxf(1.f, a.acc[2]);
   const float dMx = g0.x, dMy = g0.y, dA = g0.z, dB = g0.w, dCc = g1.x;
   const float drgb[3] = {g1.y, g1.z, g1.w};
+  // depth: A = sum q, E = sum q (p_c - D r) (the in-plane offsets, formed per pixel in K5), C = sum g_D
   const float dDa = g2.x * dscale, dDb0 = g2.y * dscale, dDb1 = g2.z * dscale, dDb2 = g2.w * dscale;
   const float dDz = gz2 * dscale;
   if (dMx == 0.f && dMy == 0.f && dA == 0.f && dB == 0.f && dCc == 0.f && drgb[0] == 0.f && drgb[1] == 0.f &&
       drgb[2] == 0.f && dDa == 0.f && dDb0 == 0.f && dDb1 == 0.f && dDb2 == 0.f && dDz == 0.f)
     return;  // nothing reached this slot
-  const float px = par[0], py = par[1], pz = par[2];
+  const Fp px = par[0], py = par[1], pz = par[2];
   const double X = fma(a.V[0], (double)px, fma(a.V[1], (double)py, fma(a.V[2], (double)pz, a.tp[0])));
   const double Y = fma(a.V[3], (double)px, fma(a.V[4], (double)py, fma(a.V[5], (double)pz, a.tp[1])));
   const double Z = fma(a.V[6], (double)px, fma(a.V[7], (double)py, fma(a.V[8], (double)pz, a.tp[2])));
-  const float x = (float)X, y = (float)Y, z = (float)Z;
-  const float* V = a.Vf;
-  const float q0 = par[6], q1 = par[7], q2 = par[8], q3 = par[9];
-  const float qn2 = q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3;
-  const float qinv = rsqrtf(qn2);
-  const float qw = q0 * qinv, qx = q1 * qinv, qy = q2 * qinv, qz = q3 * qinv;
-  float R[3][3] = {{1.f - 2.f * (qy * qy + qz * qz), 2.f * (qx * qy - qw * qz), 2.f * (qx * qz + qw * qy)},
+  const Fp x = (Fp)X, y = (Fp)Y, z = (Fp)Z;
+  const Fp* V = RTGS_PB_V;
+  const Fp q0 = par[6], q1 = par[7], q2 = par[8], q3 = par[9];
+  const Fp qn2 = q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3;
+  const Fp qinv = Fp(1) / sqrt(qn2);
+  const Fp qw = q0 * qinv, qx = q1 * qinv, qy = q2 * qinv, qz = q3 * qinv;
+  Fp R[3][3] = {{1.f - 2.f * (qy * qy + qz * qz), 2.f * (qx * qy - qw * qz), 2.f * (qx * qz + qw * qy)},
                    {2.f * (qx * qy + qw * qz), 1.f - 2.f * (qx * qx + qz * qz), 2.f * (qy * qz - qw * qx)},
                    {2.f * (qx * qz - qw * qy), 2.f * (qy * qz + qw * qx), 1.f - 2.f * (qx * qx + qy * qy)}};
-  const float l[3] = {par[3], par[4], par[5]};
-  const float sc[3] = {expf(l[0]), expf(l[1]), expf(l[2])};
-  float M[3][3], Sg[3][3];
+  const Fp l[3] = {par[3], par[4], par[5]};
+  const Fp sc[3] = {exp(l[0]), exp(l[1]), exp(l[2])};
+  Fp M[3][3], Sg[3][3];
   for (int r = 0; r < 3; ++r)
     for (int c = 0; c < 3; ++c) M[r][c] = R[r][c] * sc[c];
   for (int r = 0; r < 3; ++r)
     for (int c = 0; c < 3; ++c) Sg[r][c] = M[r][0] * M[c][0] + M[r][1] * M[c][1] + M[r][2] * M[c][2];
-  const float iz = 1.f / z;
-  const float ux = x * iz, uy = y * iz;
+  const Fp iz = 1.f / z;
+  const Fp ux = x * iz, uy = y * iz;
   const bool clx = ux < a.limx0 || ux > a.limx1, cly = uy < a.limy0 || uy > a.limy1;
-  const float limx = fminf(fmaxf(ux, a.limx0), a.limx1), limy = fminf(fmaxf(uy, a.limy0), a.limy1);
-  const float xc = z * limx, yc = z * limy;
-  const float fx = a.cam.fx, fy = a.cam.fy;
-  float J[2][3] = {{fx * iz, 0.f, -fx * xc * iz * iz}, {0.f, fy * iz, -fy * yc * iz * iz}};
-  float Tm[2][3];
+  const Fp limx = fmin(fmax(ux, (Fp)a.limx0), (Fp)a.limx1), limy = fmin(fmax(uy, (Fp)a.limy0), (Fp)a.limy1);
+  const Fp xc = z * limx, yc = z * limy;
+  const Fp fx = a.cam.fx, fy = a.cam.fy;
+  Fp J[2][3] = {{fx * iz, 0.f, -fx * xc * iz * iz}, {0.f, fy * iz, -fy * yc * iz * iz}};
+  Fp Tm[2][3];
   for (int r = 0; r < 2; ++r)
     for (int c = 0; c < 3; ++c) Tm[r][c] = J[r][0] * V[c] + J[r][1] * V[3 + c] + J[r][2] * V[6 + c];
-  float TS[2][3];
+  Fp TS[2][3];
   for (int r = 0; r < 2; ++r)
     for (int c = 0; c < 3; ++c) TS[r][c] = Tm[r][0] * Sg[0][c] + Tm[r][1] * Sg[1][c] + Tm[r][2] * Sg[2][c];
-  const float ca = TS[0][0] * Tm[0][0] + TS[0][1] * Tm[0][1] + TS[0][2] * Tm[0][2] + kDilation;
-  const float cb = TS[0][0] * Tm[1][0] + TS[0][1] * Tm[1][1] + TS[0][2] * Tm[1][2];
-  const float cc = TS[1][0] * Tm[1][0] + TS[1][1] * Tm[1][1] + TS[1][2] * Tm[1][2] + kDilation;
+  const Fp ca = TS[0][0] * Tm[0][0] + TS[0][1] * Tm[0][1] + TS[0][2] * Tm[0][2] + kDilation;
+  const Fp cb = TS[0][0] * Tm[1][0] + TS[0][1] * Tm[1][1] + TS[0][2] * Tm[1][2];
+  const Fp cc = TS[1][0] * Tm[1][0] + TS[1][1] * Tm[1][1] + TS[1][2] * Tm[1][2] + kDilation;
   const double det = (double)ca * cc - (double)cb * cb;
-  const float Qa = (float)(cc / det), Qb = (float)(-cb / det), Qc = (float)(ca / det);
+  const Fp Qa = (Fp)(cc / det), Qb = (Fp)(-cb / det), Qc = (Fp)(ca / det);
 
   // conic -> Sigma2D: dL/dSigma' = -Q G Q, G = [[dA, dB/2], [dB/2, dC]]
-  const float G01 = 0.5f * dB;
-  const float QG00 = Qa * dA + Qb * G01, QG01 = Qa * G01 + Qb * dCc;
-  const float QG10 = Qb * dA + Qc * G01, QG11 = Qb * G01 + Qc * dCc;
-  const float dS00 = -(QG00 * Qa + QG01 * Qb), dS01 = -(QG00 * Qb + QG01 * Qc);
-  const float dS11 = -(QG10 * Qb + QG11 * Qc);
-  const float dSp[2][2] = {{dS00, dS01}, {dS01, dS11}};
+  const Fp G01 = 0.5f * dB;
+  const Fp QG00 = Qa * dA + Qb * G01, QG01 = Qa * G01 + Qb * dCc;
+  const Fp QG10 = Qb * dA + Qc * G01, QG11 = Qb * G01 + Qc * dCc;
+  const Fp dS00 = -(QG00 * Qa + QG01 * Qb), dS01 = -(QG00 * Qb + QG01 * Qc);
+  const Fp dS11 = -(QG10 * Qb + QG11 * Qc);
+  const Fp dSp[2][2] = {{dS00, dS01}, {dS01, dS11}};
   // Sigma' = T Sigma T^T: dL/dSigma = T^T dS' T ; dL/dT = 2 dS' T Sigma
-  float dSig[3][3];
+  Fp dSig[3][3];
   for (int r = 0; r < 3; ++r)
     for (int c = 0; c < 3; ++c) {
-      float v = 0.f;
+      Fp v = 0.f;
       for (int p = 0; p < 2; ++p)
         for (int q = 0; q < 2; ++q) v += Tm[p][r] * dSp[p][q] * Tm[q][c];
       dSig[r][c] = v;
     }
-  float dT[2][3];
+  Fp dT[2][3];
   for (int r = 0; r < 2; ++r)
     for (int c = 0; c < 3; ++c) dT[r][c] = 2.f * (dSp[r][0] * TS[0][c] + dSp[r][1] * TS[1][c]);
   // T = J V: dL/dJ = dT V^T
-  float dJ[2][3];
+  Fp dJ[2][3];
   for (int r = 0; r < 2; ++r)
     for (int c = 0; c < 3; ++c) dJ[r][c] = dT[r][0] * V[3 * c] + dT[r][1] * V[3 * c + 1] + dT[r][2] * V[3 * c + 2];
   // J(x', y', z), x' = z clamp(x/z) (R5)
-  float dx = 0.f, dy = 0.f, dz = 0.f;
+  Fp dx = 0.f, dy = 0.f, dz = 0.f;
   dz += dJ[0][0] * (-fx * iz * iz) + dJ[0][2] * (2.f * fx * xc * iz * iz * iz);
   dz += dJ[1][1] * (-fy * iz * iz) + dJ[1][2] * (2.f * fy * yc * iz * iz * iz);
-  const float dxc = dJ[0][2] * (-fx * iz * iz), dyc = dJ[1][2] * (-fy * iz * iz);
+  const Fp dxc = dJ[0][2] * (-fx * iz * iz), dyc = dJ[1][2] * (-fy * iz * iz);
   if (clx) dz += dxc * limx; else dx += dxc;
   if (cly) dz += dyc * limy; else dy += dyc;
   // mu = (fx x/z + cx, fy y/z + cy)
   dx += dMx * fx * iz;
   dy += dMy * fy * iz;
   dz += -dMx * fx * x * iz * iz - dMy * fy * y * iz * iz;
-  // depth (Eq.4-5): dL/dp_c += dDa n_c + dDz e_z ; dL/dn_c = dDa p_c - dDb
+  // depth (Eq.4-5): dL/dp_c += dDa n_c + dDz e_z ; dL/dn_c = sum q (p_c - D r) = E
   int k = 2;
   if (l[1] < l[k]) k = 1;
   if (l[0] < l[k]) k = 0;
   // (selects, not dynamic indexing: keeps R / GR in registers)
-  const float nwx = k == 0 ? R[0][0] : (k == 1 ? R[0][1] : R[0][2]);
-  const float nwy = k == 0 ? R[1][0] : (k == 1 ? R[1][1] : R[1][2]);
-  const float nwz = k == 0 ? R[2][0] : (k == 1 ? R[2][1] : R[2][2]);
-  const float ncx = V[0] * nwx + V[1] * nwy + V[2] * nwz;
-  const float ncy = V[3] * nwx + V[4] * nwy + V[5] * nwz;
-  const float ncz = V[6] * nwx + V[7] * nwy + V[8] * nwz;
+  const Fp nwx = k == 0 ? R[0][0] : (k == 1 ? R[0][1] : R[0][2]);
+  const Fp nwy = k == 0 ? R[1][0] : (k == 1 ? R[1][1] : R[1][2]);
+  const Fp nwz = k == 0 ? R[2][0] : (k == 1 ? R[2][1] : R[2][2]);
+  const Fp ncx = V[0] * nwx + V[1] * nwy + V[2] * nwz;
+  const Fp ncy = V[3] * nwx + V[4] * nwy + V[5] * nwz;
+  const Fp ncz = V[6] * nwx + V[7] * nwy + V[8] * nwz;
   dx += dDa * ncx;
   dy += dDa * ncy;
   dz += dDa * ncz + dDz;
-  const float dncx = dDa * x - dDb0, dncy = dDa * y - dDb1, dncz = dDa * z - dDb2;
+  const Fp dncx = dDb0, dncy = dDb1, dncz = dDb2;
   // world position: p_c = V (p - t)  ->  dL/dp = V^T dL/dp_c
-  float gp0 = V[0] * dx + V[3] * dy + V[6] * dz;
-  float gp1 = V[1] * dx + V[4] * dy + V[7] * dz;
-  float gp2 = V[2] * dx + V[5] * dy + V[8] * dz;
+  Fp gp0 = V[0] * dx + V[3] * dy + V[6] * dz;
+  Fp gp1 = V[1] * dx + V[4] * dy + V[7] * dz;
+  Fp gp2 = V[2] * dx + V[5] * dy + V[8] * dz;
   // dL/dn_world = V^T dL/dn_c
-  const float dnw0 = V[0] * dncx + V[3] * dncy + V[6] * dncz;
-  const float dnw1 = V[1] * dncx + V[4] * dncy + V[7] * dncz;
-  const float dnw2 = V[2] * dncx + V[5] * dncy + V[8] * dncz;
+  const Fp dnw0 = V[0] * dncx + V[3] * dncy + V[6] * dncz;
+  const Fp dnw1 = V[1] * dncx + V[4] * dncy + V[7] * dncz;
+  const Fp dnw2 = V[2] * dncx + V[5] * dncy + V[8] * dncz;
   // SH colour: rgb = max(0, sum_k Y_k(d) sh_k + 0.5), d = (p - campos)/|p - campos|
   const double vx = (double)px - a.campos[0], vy = (double)py - a.campos[1], vz = (double)pz - a.campos[2];
   const double vnorm = sqrt(vx * vx + vy * vy + vz * vz);
-  const float dirx = (float)(vx / vnorm), diry = (float)(vy / vnorm), dirz = (float)(vz / vnorm);
+  const double ddx = vx / vnorm, ddy = vy / vnorm, ddz = vz / vnorm;
+  const float dirx = (float)ddx, diry = (float)ddy, dirz = (float)ddz;
   // rgb = max(0, raw): the clamp decision (R17) comes from the projected colour (rgb == 0 <=> raw <= 0)
   const float gc0 = par[10] > 0.f ? drgb[0] : 0.f;
   const float gc1 = par[11] > 0.f ? drgb[1] : 0.f;
@@ -487,8 +512,9 @@ __device__ __forceinline__ void project_bwd_slot(const PBArgs& a, const float* s
   float gd0 = 0.f, gd1 = 0.f, gd2 = 0.f;
 #pragma unroll
   for (int kk = 0; kk < K; ++kk) {
-    float Y, Yx, Yy, Yz;
-    sh_basis_one(kk, dirx, diry, dirz, Y, Yx, Yy, Yz);
+    double Yd, Yxd, Yyd, Yzd;
+    sh_basis_one<double>(kk, ddx, ddy, ddz, Yd, Yxd, Yyd, Yzd);
+    const float Y = (float)Yd, Yx = (float)Yxd, Yy = (float)Yyd, Yz = (float)Yzd;
     gout[10 + kk] = Y;  // SH gradient (kk, c) = Y_kk * gc_c, formed by the consumer (compact staging)
     const float c = shc[3 * kk] * gc0 + shc[3 * kk + 1] * gc1 + shc[3 * kk + 2] * gc2;
     gd0 += Yx * c;
@@ -505,14 +531,14 @@ __device__ __forceinline__ void project_bwd_slot(const PBArgs& a, const float* s
   gout[10 + K] = gc0; gout[10 + K + 1] = gc1; gout[10 + K + 2] = gc2;
   gout[0] += gp0; gout[1] += gp1; gout[2] += gp2;
   // Sigma = M M^T, M = R diag(s): dL/dM = 2 dSig M
-  float dM[3][3];
+  Fp dM[3][3];
   for (int r = 0; r < 3; ++r)
     for (int c = 0; c < 3; ++c) dM[r][c] = 2.f * (dSig[r][0] * M[0][c] + dSig[r][1] * M[1][c] + dSig[r][2] * M[2][c]);
   for (int c = 0; c < 3; ++c) {
-    const float dsc = dM[0][c] * R[0][c] + dM[1][c] * R[1][c] + dM[2][c] * R[2][c];
+    const Fp dsc = dM[0][c] * R[0][c] + dM[1][c] * R[1][c] + dM[2][c] * R[2][c];
     gout[3 + c] += dsc * sc[c];  // s = exp(log_scale)
   }
-  float GR[3][3];
+  Fp GR[3][3];
   for (int r = 0; r < 3; ++r)
     for (int c = 0; c < 3; ++c) GR[r][c] = dM[r][c] * sc[c];
 #pragma unroll
@@ -520,15 +546,15 @@ __device__ __forceinline__ void project_bwd_slot(const PBArgs& a, const float* s
     if (c == k) { GR[0][c] += dnw0; GR[1][c] += dnw1; GR[2][c] += dnw2; }
   }
   // rotation matrix of the unit quaternion
-  const float gw = 2.f * (-qz * GR[0][1] + qy * GR[0][2] + qz * GR[1][0] - qx * GR[1][2] - qy * GR[2][0] + qx * GR[2][1]);
-  const float gx = 2.f * (qy * GR[0][1] + qz * GR[0][2] + qy * GR[1][0] - 2.f * qx * GR[1][1] - qw * GR[1][2] +
+  const Fp gw = 2.f * (-qz * GR[0][1] + qy * GR[0][2] + qz * GR[1][0] - qx * GR[1][2] - qy * GR[2][0] + qx * GR[2][1]);
+  const Fp gx = 2.f * (qy * GR[0][1] + qz * GR[0][2] + qy * GR[1][0] - 2.f * qx * GR[1][1] - qw * GR[1][2] +
                           qz * GR[2][0] + qw * GR[2][1] - 2.f * qx * GR[2][2]);
-  const float gy = 2.f * (-2.f * qy * GR[0][0] + qx * GR[0][1] + qw * GR[0][2] + qx * GR[1][0] + qz * GR[1][2] -
+  const Fp gy = 2.f * (-2.f * qy * GR[0][0] + qx * GR[0][1] + qw * GR[0][2] + qx * GR[1][0] + qz * GR[1][2] -
                           qw * GR[2][0] + qz * GR[2][1] - 2.f * qy * GR[2][2]);
-  const float gz = 2.f * (-2.f * qz * GR[0][0] - qw * GR[0][1] + qx * GR[0][2] + qw * GR[1][0] - 2.f * qz * GR[1][1] +
+  const Fp gz = 2.f * (-2.f * qz * GR[0][0] - qw * GR[0][1] + qx * GR[0][2] + qw * GR[1][0] - 2.f * qz * GR[1][1] +
                           qy * GR[1][2] + qx * GR[2][0] + qy * GR[2][1]);
   // through q = q~/|q~|
-  const float dot = gw * qw + gx * qx + gy * qy + gz * qz;
+  const Fp dot = gw * qw + gx * qx + gy * qy + gz * qz;
   gout[6] += (gw - dot * qw) * qinv;
   gout[7] += (gx - dot * qx) * qinv;
   gout[8] += (gy - dot * qy) * qinv;
@@ -564,7 +590,7 @@ __device__ __forceinline__ float sh_grad(const float* row, int j) {
 // 22 resident 32-slot CTAs per SM (<= 88 registers, ~8 KB shared): 148 x 22 x 32 = 104k slots in
 // one wave, so the C3 iteration's 100k unstable slots do not pay a second wave of CTA latency
 template <int K, bool ADAM>
-__global__ void __launch_bounds__(kPBS, 22) k_project_bwd(const PBArgs a) {
+__global__ void __launch_bounds__(kPBS, RTGS_BWD_F64 ? 12 : 22) k_project_bwd(const PBArgs a) {
   using SM = PBSmem<K>;
   constexpr int D = SM::D, LD = SM::LD, SHF = SM::SHF;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -721,7 +747,7 @@ static cudaError_t enqueue_backward(const rtgs_gaussians& g, const rtgs_projecte
   a.tile_list = fwd.tile_list;
   a.counts = fwd.counts;
   a.active = fwd.active_bits;
-  a.color = fwd.color; a.depth = fwd.depth; a.index = fwd.index; a.n_contrib = fwd.n_contrib;
+  a.color = fwd.color; a.trans = fwd.trans; a.depth = fwd.depth; a.index = fwd.index; a.n_contrib = fwd.n_contrib;
   a.tcolor = target.color; a.tdepth = target.depth;
   a.slot_of_gid = slot_of_gid;
   a.cam = make_cam(cam);

@@ -69,7 +69,16 @@ __device__ __forceinline__ const float4* entry_rec(const float4* rec, const floa
 }
 
 // producer: one lane per record slot; `extra(stage, j, entry)` may issue more cp.async.
-template <typename Extra, typename Flush>
+// REV: the batches run back to front (batch b holds positions [max(start, end - 128 (b+1)), end - 128 b),
+// in list order inside the stage) for the backward's back-to-front pass.
+__device__ __forceinline__ int pipe_batch_lo(bool rev, int start, int end, int b) {
+  return rev ? max(start, end - (b + 1) * kPipeBatch) : start + b * kPipeBatch;
+}
+__device__ __forceinline__ int pipe_batch_cnt(bool rev, int start, int end, int b) {
+  return rev ? (end - b * kPipeBatch) - max(start, end - (b + 1) * kPipeBatch)
+             : min(kPipeBatch, end - start - b * kPipeBatch);
+}
+template <bool REV = false, typename Extra, typename Flush>
 __device__ __forceinline__ void pipe_produce(PipeRing& r, const float4* __restrict__ rec,
                                              const float4* __restrict__ sub_rec,
                                              const uint32_t* __restrict__ sorted_gid, int start, int end,
@@ -85,19 +94,20 @@ __device__ __forceinline__ void pipe_produce(PipeRing& r, const float4* __restri
       flush(st, b - kPipeStages);
     }
     if (*((volatile int*)&r.alive) > 0) {
-      const int cnt = min(kPipeBatch, n - b * kPipeBatch);
+      const int lo = pipe_batch_lo(REV, start, end, b);
+      const int cnt = pipe_batch_cnt(REV, start, end, b);
       constexpr int PER = kPipeBatch / 32;
       uint32_t g[PER];
 #pragma unroll
       for (int q = 0; q < PER; ++q) {  // all gid loads of the batch in flight together
         const int j = lane + 32 * q;
-        g[q] = j < cnt ? sorted_gid[start + b * kPipeBatch + j] : 0u;
+        g[q] = j < cnt ? sorted_gid[lo + j] : 0u;
       }
 #pragma unroll
       for (int q = 0; q < PER; ++q) {
         const int j = lane + 32 * q;
         if (j < cnt) {
-          cp_async4(&r.gid[st][j], sorted_gid + start + b * kPipeBatch + j);
+          cp_async4(&r.gid[st][j], sorted_gid + lo + j);
           const float4* src = entry_rec(rec, sub_rec, g[q]);
           cp_async16(&r.rec[st][j][0], src);
           cp_async16(&r.rec[st][j][1], src + 1);

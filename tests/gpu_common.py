@@ -19,7 +19,12 @@ def device_map(scene):
 
 
 def cam_dict(cfg):
-    return OP.camera(cfg)
+    """The oracle's camera: the intrinsics as the C ABI receives them (rtgs_camera holds float32 fx, fy,
+    cx, cy; e.g. TUM's c_y = 255.3 is 255.300003 there), so both sides see identical inputs."""
+    c = OP.camera(cfg)
+    for k in ("fx", "fy", "cx", "cy"):
+        c[k] = float(np.float32(c[k]))
+    return c
 
 
 def oracle_project(scene, R, t, cam):
@@ -48,7 +53,7 @@ def compare_render(gpu: dict, orc: dict, mask: np.ndarray, what=""):
     ok = rel_close(gpu["trans"][safe], ot[safe], 1e-4, 1e-2)
     assert ok.all(), f"{what} trans: {(~ok).sum()} bad, max err {np.abs(gpu['trans'][safe] - ot[safe]).max()}"
     od = orc["depth"].detach().numpy()
-    ok = rel_close(gpu["depth"][safe], od[safe], 1e-4, 1.0)
+    ok = rel_close(gpu["depth"][safe], od[safe], 1e-4, 1e-3)
     assert ok.all(), f"{what} depth: {(~ok).sum()} bad, max err {np.abs(gpu['depth'][safe] - od[safe]).max()}"
     hit = safe & (orc["index"] >= 0)
     on = orc["normal"].detach().numpy()

@@ -1,5 +1,6 @@
-"""Full-size parity (BASELINE.json configs[2], C3: 1200x680, 1M Gaussians, 10 % unstable) in the
-bench's launch configuration, on outputs the oracle can compute one by one:
+"""Full-size parity in the bench's launch configuration, on outputs the oracle can compute one by one,
+for BASELINE.json configs[2] (C3: Replica-shaped 1200x680, 1M Gaussians, 10 % unstable) and
+configs[1] (C2: TUM-shaped 640x480, 200k Gaussians, 20 % unstable, TUM-like depth noise and holes):
 
   * projection of 4096 sampled Gaussians (all fields);
   * unstable coverage over the WHOLE frame (oracle evaluates every unstable support rect), tile keep,
@@ -8,9 +9,11 @@ bench's launch configuration, on outputs the oracle can compute one by one:
     differences at integer boundaries);
   * FULL-render colour / T / depth / index at 64 sampled pixels (every Gaussian whose support rect
     contains the pixel is a candidate: the rect contains the support, R7);
-  * colour-loss gradients of 6 sampled unstable slots (autograd of the oracle restricted to the
-    Gaussians that reach the slot's footprint pixels; w_d = 0 so the normalisation |P| is the
-    oracle's own);
+  * the masked iteration's loss: |P|, |P_d| and L_c, L_d over the WHOLE active set (oracle render of
+    every active pixel, tile by tile with the tile's candidates);
+  * colour + depth gradients (w_c = w_d = 1) of 32 sampled unstable slots, each coordinate within
+    1e-3 max(|o|, 1e-2 M) (o and the absolute mass M summed pixel by pixel from
+    per-pixel oracle autograd over the slot's footprint);
   * the f3-cached iteration equals the uncached one, and the bench's fused backward + Adam equals
     the separate calls, at full size.
 """
@@ -22,24 +25,24 @@ from oracle import binning as OB
 from oracle import projection as OP
 from oracle import raster as OR
 from synth import CONFIGS, make_frame, make_pose, make_scene
-from tests.gpu_common import MARGIN, rel_close, u32
+from tests.gpu_common import MARGIN, cam_dict, rel_close, u32
 
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(scope="module")
-def c3():
+@pytest.fixture(scope="module", params=["C3", "C2"])
+def c3(request):
     from paper_2404_19706_b200 import build as B
     B.build()
     import paper_2404_19706_b200 as P
-    cfg = CONFIGS["C3"]
+    cfg = CONFIGS[request.param]
     scene = make_scene(cfg)
     R, t = make_pose(cfg)
     col, dep = make_frame(cfg)
     gm = P.GaussianMap.from_arrays(scene)
     cam = P.camera_of(cfg)
     pose = P.make_pose(R, t)
-    eng = P.MappingEngine(gm, cam, capacity=4 * cfg.n, weights=(1.0, 0.0, 1000.0))
+    eng = P.MappingEngine(gm, cam, capacity=4 * cfg.n, weights=(1.0, 1.0, 1000.0))
     tc, td = torch.as_tensor(col, device="cuda"), torch.as_tensor(dep, device="cuda")
     eng.ingest(tc, td, pose)            # side-by-side buffers exactly as in MappingEngine.step
     eng.forward_masked(pose)
@@ -47,7 +50,7 @@ def c3():
     torch.cuda.synchronize()
     prm = OP.params_from_scene(scene)
     with torch.no_grad():
-        pr = OP.project(prm, R, t, OP.camera(cfg), scene["sh_degree"])
+        pr = OP.project(prm, R, t, cam_dict(cfg), scene["sh_degree"])
     return dict(P=P, cfg=cfg, scene=scene, R=R, t=t, col=col, dep=dep, eng=eng, pr=pr)
 
 
@@ -80,7 +83,7 @@ def test_coverage_whole_frame(c3):
     g = eng.out.active_mask().cpu().numpy()
     safe = marg >= MARGIN
     assert ((g == cov) | ~safe).all()
-    assert (~safe).sum() <= 2e-3 * safe.size
+    assert (~safe).sum() <= 1e-3 * safe.size
     keep = OR.tile_keep(cov)
     np.testing.assert_array_equal(eng.out.tile_keep.cpu().numpy().astype(bool), keep)
     counts = eng.out.counts.cpu().numpy()
@@ -127,31 +130,102 @@ def test_full_render_sampled_pixels(c3):
         cand = _candidates(pr, px, py)
         order = order_all[cand[order_all]]
         with torch.no_grad():
-            o = OR.render_pixels(pr, np.array([[px, py]]), OP.camera(cfg), R, order=order)
+            o = OR.render_pixels(pr, np.array([[px, py]]), cam_dict(cfg), R, order=order)
         if o["margin"][0] < MARGIN:
             excluded += 1
             continue
         assert gi[py, px] == o["index"][0]
         assert rel_close(gc[:, py, px], o["color"][0].numpy(), 1e-4, 1e-2).all()
         assert rel_close(gt[py, px], o["trans"][0].item(), 1e-4, 1e-2)
-        assert rel_close(gd[py, px], o["depth"][0].item(), 1e-4, 1.0)
+        assert rel_close(gd[py, px], o["depth"][0].item(), 1e-4, 1e-3)
     assert excluded <= 2
 
 
-def test_colour_gradients_sampled_slots(c3):
-    eng, pr, cfg, scene, R, t = c3["eng"], c3["pr"], c3["cfg"], c3["scene"], c3["R"], c3["t"]
-    unstable = (scene["flags"] & 2) == 0
+def _active(c3):
     if "active" not in c3:
+        pr, cfg, scene = c3["pr"], c3["cfg"], c3["scene"]
+        unstable = (scene["flags"] & 2) == 0
         cov, _ = OR.unstable_coverage_splat(pr, unstable, cfg.width, cfg.height)
         c3["active"] = OR.active_set(cov, OR.tile_keep(cov))
-    act = c3["active"]
-    nP = int(act.sum())
+    return c3["active"]
+
+
+def _oracle_active_render(c3):
+    """Oracle render of every active pixel, tile by tile: the candidates of a tile are the Gaussians
+    whose support rect overlaps it (R7), in the oracle's (key, gid) order."""
+    if "orender" in c3:
+        return c3["orender"]
+    pr, cfg, R = c3["pr"], c3["cfg"], c3["R"]
+    act = _active(c3)
+    order_all = OR.depth_order(pr)
+    rect = pr["rect"]
+    depth = np.full(act.shape, np.nan)
+    color = np.full((3,) + act.shape, np.nan)
+    index = np.full(act.shape, -2, np.int64)
+    margin = np.full(act.shape, np.inf)
+    tx, ty = cfg.tiles
+    for t in range(tx * ty):
+        i, j = t % tx, t // tx
+        ys, xs = np.nonzero(act[16 * j:16 * j + 16, 16 * i:16 * i + 16])
+        if len(xs) == 0:
+            continue
+        xs, ys = xs + 16 * i, ys + 16 * j
+        x0, x1, y0, y1 = xs.min(), xs.max(), ys.min(), ys.max()
+        cand = pr["valid"] & (rect[:, 0] <= x1) & (rect[:, 2] >= x0) & (rect[:, 1] <= y1) & (rect[:, 3] >= y0)
+        order = order_all[cand[order_all]]
+        with torch.no_grad():
+            o = OR.render_pixels(pr, np.stack([xs, ys], 1), cam_dict(cfg), R, order=order)
+        depth[ys, xs] = o["depth"].numpy()
+        color[:, ys, xs] = o["color"].numpy().T
+        index[ys, xs] = o["index"]
+        margin[ys, xs] = o["margin"]
+    c3["orender"] = dict(depth=depth, color=color, index=index, margin=margin)
+    return c3["orender"]
+
+
+def test_masked_loss_whole_active_set(c3):
+    """Eq.7 over the whole P: |P|, |P_d| = #{u in P : D^ != -1, D > 0} (R13, R14) and L_c, L_d."""
+    eng, cfg = c3["eng"], c3["cfg"]
+    act = _active(c3)
+    o = _oracle_active_render(c3)
+    D = c3["dep"].astype(np.float64)
+    C = c3["col"].astype(np.float64)
+    safe = o["margin"][act] >= MARGIN
+    assert (~safe).sum() <= 1e-3 * act.sum()
+    pd = (o["index"] >= 0) & np.isfinite(D) & (D > 0) & act
+    loss = eng.loss.cpu().numpy().astype(np.float64)
+    n_p = int(act.sum())
+    # excluded (near-decision) pixels may decide the hit differently: count them as the slack
+    n_unsafe = int((~safe).sum())
+    assert abs(int(loss[3]) - int(pd.sum())) <= n_unsafe, (loss[3], pd.sum(), n_unsafe)
+    Lc = np.abs(o["color"][:, act] - C[:, act]).sum() / (3.0 * n_p)
+    Ld = np.abs(o["depth"][pd] - D[pd]).sum() / max(1, int(pd.sum()))
+    # float32 sums over ~1e5 pixels in atomic order; unsafe pixels bound the decision slack
+    assert abs(loss[0] - Lc) <= 1e-5 * Lc + 3.0 * n_unsafe / (3.0 * n_p)
+    assert abs(loss[1] - Ld) <= 1e-5 * Ld + 10.0 * n_unsafe / max(1, int(pd.sum()))
+
+
+def test_gradients_sampled_slots(c3):
+    """Colour + depth gradients (w_c = w_d = 1) of 32 sampled unstable slots against the oracle,
+    every coordinate within 1e-3 max(|o|, 1e-2 M).  o and M = sum_u |d l_u / d theta|
+    are summed over the slot's footprint pixels u in P (the only pixels whose loss term depends on the
+    slot: its support rect, R7), each l_u by oracle autograd on the pixel's candidate Gaussians, with
+    the normalisations |P| and |P_d| of the whole active set (test_masked_loss_whole_active_set)."""
+    eng, pr, cfg, scene, R, t = c3["eng"], c3["pr"], c3["cfg"], c3["scene"], c3["R"], c3["t"]
+    act = _active(c3)
+    o_img = _oracle_active_render(c3)
+    D = c3["dep"].astype(np.float64)
+    C = c3["col"].astype(np.float64)
+    n_p = int(act.sum())
+    pd_img = (o_img["index"] >= 0) & np.isfinite(D) & (D > 0) & act
+    n_pd = int(pd_img.sum())
     gid_of_slot = eng.gid_of_slot.cpu().numpy()
     G = eng.grad[: len(gid_of_slot)].cpu().numpy().astype(np.float64)
     rng = np.random.default_rng(4)
     live = np.nonzero(np.abs(G[:, 10:13]).sum(1) > 0)[0]
-    checked = 0
-    for s in rng.permutation(live)[:40]:
+    keys = ("pos", "log_scale", "rot", "sh")
+    checked, skipped, with_depth = 0, 0, 0
+    for s in rng.permutation(live):
         g = gid_of_slot[s]
         x0, y0, x1, y1 = pr["rect"][g]
         ys, xs = np.mgrid[y0:y1 + 1, x0:x1 + 1]
@@ -159,33 +233,51 @@ def test_colour_gradients_sampled_slots(c3):
         fp = fp[act[fp[:, 1], fp[:, 0]]]
         if len(fp) == 0:
             continue
-        sub = np.zeros(cfg.n, dtype=bool)
-        for px, py in fp:
-            sub |= _candidates(pr, px, py)
-        sub_idx = np.nonzero(sub)[0]                       # ascending gid: tie order preserved
-        sub_scene = {k: (v[sub_idx] if isinstance(v, np.ndarray) and v.shape[:1] == (cfg.n,) else v)
-                     for k, v in scene.items()}
-        prm = OP.params_from_scene(sub_scene, requires_grad=True)
-        spr = OP.project(prm, R, t, OP.camera(cfg), scene["sh_degree"])
-        out = OR.render_pixels(spr, fp, OP.camera(cfg), R)
-        if (out["margin"] < MARGIN).any():
+        if (o_img["margin"][fp[:, 1], fp[:, 0]] < MARGIN).any():
+            skipped += 1
             continue
-        tcol = torch.as_tensor(c3["col"][:, fp[:, 1], fp[:, 0]].T.astype(np.float64))
-        diff = out["color"] - tcol
-        if (diff.detach().abs() < 1e-5).any():
-            continue                                       # an L1 kink within float32 reach
-        L = diff.abs().sum() / (3.0 * nP)
-        L.backward()
-        li = int(np.searchsorted(sub_idx, g))
-        o = torch.cat([prm[k].grad[li].reshape(-1) for k in ("pos", "log_scale", "rot", "sh")]).numpy()
+        o = np.zeros(G.shape[1])
+        M = np.zeros(G.shape[1])
+        kink = False
+        depth_terms = 0
+        for px, py in fp:
+            cand = np.nonzero(_candidates(pr, px, py))[0]          # ascending gid: tie order kept
+            sub = {k: (v[cand] if isinstance(v, np.ndarray) and v.shape[:1] == (cfg.n,) else v)
+                   for k, v in scene.items()}
+            li = int(np.searchsorted(cand, g))
+            prm = OP.params_from_scene(sub, requires_grad=True)
+            spr = OP.project(prm, R, t, cam_dict(cfg), scene["sh_degree"])
+            out = OR.render_pixels(spr, np.array([[px, py]]), cam_dict(cfg), R, want_margin=False)
+            diff = out["color"][0] - torch.as_tensor(C[:, py, px])
+            if (diff.detach().abs() < 1e-5).any():
+                kink = True                                        # an L1 kink within float32 reach
+                break
+            lu = diff.abs().sum() / (3.0 * n_p)
+            if pd_img[py, px]:
+                dd = out["depth"][0] - D[py, px]
+                if abs(dd.item()) < 1e-5:
+                    kink = True
+                    break
+                lu = lu + dd.abs() / n_pd
+                depth_terms += int(out["index"][0] == li)   # the slot is this pixel's depth hit
+            lu.backward()
+            gu = torch.cat([prm[k].grad[li].reshape(-1) for k in keys]).numpy()
+            o += gu
+            M += np.abs(gu)
+        if kink:
+            skipped += 1
+            continue
         gg = G[s]
-        tol = 1e-3 * np.maximum(np.abs(o), 1e-2 * np.abs(o).max())
-        assert (np.abs(gg - o) <= 10 * tol).all(), (s, np.abs(gg - o).max(), np.abs(o).max())
-        assert (np.abs(gg - o) <= tol).mean() >= 0.95
+        tol = 1e-3 * np.maximum(np.abs(o), 1e-2 * M)
+        err = np.abs(gg - o)
+        assert (err <= tol).all(), (s, int(np.argmax(err / np.maximum(tol, 1e-30))),
+                                    float((err / np.maximum(tol, 1e-30)).max()), gg, o)
         checked += 1
-        if checked == 6:
+        with_depth += depth_terms > 0
+        if checked == 32:
             break
-    assert checked >= 4
+    assert checked == 32, (checked, skipped)
+    assert with_depth >= 8, with_depth   # the depth-gradient path (Eq.4-5) is exercised
 
 
 def test_cached_iteration_equals_uncached_c3(c3):
@@ -291,7 +383,7 @@ def test_c4_render_only_sampled():
     torch.cuda.synchronize()
     prm = OP.params_from_scene(scene)
     with torch.no_grad():
-        pr = OP.project(prm, R, t, OP.camera(cfg), scene["sh_degree"])
+        pr = OP.project(prm, R, t, cam_dict(cfg), scene["sh_degree"])
     grect = proj.rect.cpu().numpy().astype(np.int64)
     mism = (grect != pr["rect"]).any(1) & pr["valid"]
     assert mism.sum() <= 1e-3 * cfg.n
@@ -307,12 +399,12 @@ def test_c4_render_only_sampled():
         cand = _candidates(pr, px, py)
         order = order_all[cand[order_all]]
         with torch.no_grad():
-            o = OR.render_pixels(pr, np.array([[px, py]]), OP.camera(cfg), R, order=order)
+            o = OR.render_pixels(pr, np.array([[px, py]]), cam_dict(cfg), R, order=order)
         if o["margin"][0] < MARGIN:
             excluded += 1
             continue
         assert gi[py, px] == o["index"][0]
         assert rel_close(gc[:, py, px], o["color"][0].numpy(), 1e-4, 1e-2).all()
         assert rel_close(gt[py, px], o["trans"][0].item(), 1e-4, 1e-2)
-        assert rel_close(gd[py, px], o["depth"][0].item(), 1e-4, 1.0)
+        assert rel_close(gd[py, px], o["depth"][0].item(), 1e-4, 1e-3)
     assert excluded <= 2

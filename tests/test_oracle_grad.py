@@ -115,3 +115,39 @@ def test_zero_cotangent_gives_zero_gradient():
                              np.ones((30, 40), bool), np.arange(len(sc["pos"])))
     assert res["n_P"] == 1200
     assert np.abs(res["grad"]).max() == 0.0
+
+
+def test_absolute_mass_equals_per_pixel_brute_force():
+    # M = sum_u |d l_u / d theta| (the scale of the GPU gradient contract): the grouped
+    # evaluation in oracle/loss.py against one autograd pass per active pixel, and M >= |grad| with
+    # equality where every pixel term has the same sign.
+    c = cam(40, 30, 45.0)
+    sc = _fd_scene(23, n=10)
+    prm0 = P.params_from_scene(sc)
+    pr0 = P.project(prm0, np.eye(3), np.zeros(3), c, 1)
+    img = RS.render_image(pr0, c, np.eye(3))
+    rng = np.random.default_rng(6)
+    tc = img["color"].numpy() + 0.05 * rng.choice([-1, 1], size=(3, 30, 40))
+    td = np.where(img["depth"].numpy() > 0, img["depth"].numpy() + 0.05 * rng.choice([-1, 1], size=(30, 40)), 0.0)
+    active = np.zeros((30, 40), bool)
+    active[5:25:2, 4:36:3] = True
+    gid = np.arange(len(sc["pos"]))
+    res = LS.iteration_grads(sc, np.eye(3), np.zeros(3), c, tc, td, active, gid, mass=True)
+    n_p, n_pd = res["n_P"], res["n_Pd"]
+    brute = np.zeros_like(res["grad"])
+    total = np.zeros_like(res["grad"])
+    for (px, py) in LS.active_pixels(active):
+        prm = P.params_from_scene(sc, requires_grad=True)
+        pr = P.project(prm, np.eye(3), np.zeros(3), c, 1)
+        out = RS.render_pixels(pr, np.array([[px, py]]), c, np.eye(3), want_margin=False)
+        lu = (out["color"][0] - torch.as_tensor(tc[:, py, px])).abs().sum() / (3.0 * n_p)
+        if out["index"][0] >= 0 and td[py, px] > 0:
+            lu = lu + (out["depth"][0] - td[py, px]).abs() / n_pd
+        lu.backward()
+        gu = LS.slot_grads(prm, gid)
+        brute += np.abs(gu)
+        total += gu
+    np.testing.assert_allclose(res["mass"], brute, rtol=1e-10, atol=1e-15)
+    np.testing.assert_allclose(res["grad"], total, rtol=1e-9, atol=1e-14)
+    assert (np.abs(res["grad"]) <= res["mass"] * (1 + 1e-12) + 1e-18).all()
+    assert (res["mass"] > np.abs(res["grad"]) * (1 + 1e-6)).any()   # some terms cancel
