@@ -111,6 +111,11 @@ enum { RTGS_RENDER_FULL = 0, RTGS_RENDER_MASKED = 1, RTGS_RENDER_COVERAGE = 2 };
 /* OR-ed into FULL or MASKED: also count the blended (pixel, Gaussian) pairs into counts[3] (a
  * statistic; the production renders leave it off, it costs instructions per blended pair). */
 enum { RTGS_RENDER_COUNT = 16 };
+/* OR-ed into FULL or MASKED: evaluate every (pixel, Gaussian) pair of the 8x4 pixel blocks whose
+ * support box overlaps the Gaussian (the dense consumer) instead of only the pixels of its support
+ * span mask.  Identical results by construction (the span mask is a superset of the support);
+ * a verification mode for the tests, slower. */
+enum { RTGS_RENDER_DENSE = 32 };
 
 /* Render buffers (O2-O4).  Which fields are read / written depends on the mode, see the call. */
 typedef struct {

@@ -14,4 +14,4 @@ from .mapping import (GaussianMap, MappingEngine, ProjectedBuffers, BinBuffers, 
                       topk_error_mask,
                       make_camera, make_pose, camera_of,
                       hparams, add_params, launch_count, RTGS_RENDER_FULL, RTGS_RENDER_MASKED,
-                      RTGS_RENDER_COVERAGE, RTGS_RENDER_COUNT)
+                      RTGS_RENDER_COVERAGE, RTGS_RENDER_COUNT, RTGS_RENDER_DENSE)

@@ -9,6 +9,7 @@ LIB_PATH = os.path.join(_HERE, "librtgs.so")
 
 RTGS_RENDER_FULL, RTGS_RENDER_MASKED, RTGS_RENDER_COVERAGE = 0, 1, 2
 RTGS_RENDER_COUNT = 16  # OR-ed into FULL / MASKED: count blended pairs into counts[3]
+RTGS_RENDER_DENSE = 32  # OR-ed into FULL / MASKED: the dense consumer (verification of the span masks)
 STATUS = {0: "RTGS_OK", 1: "RTGS_ERR_INVALID_ARG", 2: "RTGS_ERR_CAPACITY", 3: "RTGS_ERR_CUDA", 4: "RTGS_ERR_WORKSPACE"}
 
 vp = C.c_void_p

@@ -101,7 +101,8 @@ rtgs_status rtgs_render_color_depth(const rtgs_gaussians* g, const rtgs_projecte
     return finish(launch_coverage(*g, *proj, *cam, *out, S(stream)));
   }
   const bool count = (mode & RTGS_RENDER_COUNT) != 0;
-  mode &= ~RTGS_RENDER_COUNT;
+  const bool dense = (mode & RTGS_RENDER_DENSE) != 0;
+  mode &= ~(RTGS_RENDER_COUNT | RTGS_RENDER_DENSE);
   if (mode != RTGS_RENDER_FULL && mode != RTGS_RENDER_MASKED) return RTGS_ERR_INVALID_ARG;
   if (count && !out->counts) return RTGS_ERR_INVALID_ARG;
   if (!proj || !proj->rec || !proj->zkey || !a16(proj->rec) || !bins_ok(bins)) return RTGS_ERR_INVALID_ARG;
@@ -112,7 +113,7 @@ rtgs_status rtgs_render_color_depth(const rtgs_gaussians* g, const rtgs_projecte
   if (mode == RTGS_RENDER_MASKED && (!out->active_bits || !out->tile_list || !out->counts))
     return RTGS_ERR_INVALID_ARG;
   return finish(launch_render(*proj, *bins, make_pose(*pose), *cam, mode == RTGS_RENDER_MASKED, count, *out,
-                              S(stream)));
+                              S(stream), dense));
 }
 
 size_t rtgs_backward_workspace_size(int32_t n_slots) { return n_slots < 0 ? 0 : backward_workspace_size(n_slots); }

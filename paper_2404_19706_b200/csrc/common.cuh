@@ -72,6 +72,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       "r"(phase)
       : "memory");
 }
+// the same wait, but the waiting warp is suspended in try_wait (up to the time hint) instead of
+// re-issuing the probe: consumer warps that run ahead of the producer / the slowest warp of the CTA
+// leave their issue slots to the warps still working
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase), "r"(1000000u)
+      : "memory");
+}
 __device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, uint32_t bytes, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(

@@ -66,7 +66,8 @@ cudaError_t launch_coverage_bin_cached(const rtgs_projected& proj, const rtgs_bi
 cudaError_t launch_coverage(const rtgs_gaussians& g, const rtgs_projected& proj, const rtgs_camera& cam,
                             const rtgs_render_out& out, cudaStream_t s);
 cudaError_t launch_render(const rtgs_projected& proj, const rtgs_bins& bins, const PoseF& pose,
-                          const rtgs_camera& cam, int masked, bool count, const rtgs_render_out& out, cudaStream_t s);
+                          const rtgs_camera& cam, int masked, bool count, const rtgs_render_out& out, cudaStream_t s,
+                          bool dense = false);
 
 size_t backward_workspace_size(int n_slots);
 cudaError_t launch_backward(const rtgs_gaussians& g, const rtgs_projected& proj, const rtgs_bins& bins,

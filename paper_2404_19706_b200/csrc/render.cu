@@ -5,8 +5,11 @@
 // Forward: one CTA per 16x16 tile (FULL) or per half of a kept tile (MASKED) = 8 / 4 consumer warps
 // (warp w owns an 8x4 pixel block, one pixel per lane) + 1 producer warp streaming the tile's depth-sorted records through a 4-stage
 // shared-memory ring (tilepipe.cuh).  Each consumer warp culls a batch 32 records at a time against
-// its 8x4 block (ballot over the records' support boxes) and only walks the survivors.  Pixels stop
-// at T (1 - f) < 1e-4; warps stop when all their lanes stopped; the producer stops when all did.
+// its 8x4 block (ballot over the records' support boxes); for the survivors it builds exact support
+// span masks (one per survivor, transposed to one bit list per pixel) and each lane walks only its
+// own pixel's pairs (the span path below; RTGS_RENDER_DENSE keeps the dense walk for verification).
+// Pixels stop at T (1 - f) < 1e-4; warps stop when all their lanes stopped; the producer stops when
+// all did.
 #include "common.cuh"
 #include "internal.h"
 #include "tilepipe.cuh"
@@ -184,6 +187,65 @@ cudaError_t launch_tile_coverage(const uint2* srange, const unsigned long long* 
 // ------------------------------------------------------------------------------------------------
 // A3/A4 forward
 // ------------------------------------------------------------------------------------------------
+// Span-mask path (round 2).  Per 8x4 warp block the dense path evaluated every surviving (record, block)
+// pair on all 32 lanes although ~5 lanes blend (sub-pixel splats): 45 instructions x 32 lanes per
+// survivor.  Instead, per batch of bbox survivors:
+//   1. lane l takes survivor l and computes the exact 32-bit pixel mask of its support over the block
+//      (support_mask: per pixel row, the x interval where p2 >= max(p2_min, log2(1/255) - log2 alpha),
+//      a quadratic in dx, enlarged by a safety margin so it is a SUPERSET of the pixels that pass
+//      eval_pair: a pixel outside it cannot pass, a pixel inside is still decided by eval_pair);
+//   2. one 32x32 bit transpose (5 shuffles) turns "survivor l covers pixels" into "pixel p is covered
+//      by survivors" (bit l, in depth order);
+//   3. each lane walks ITS OWN set bits front to back (divergent loop: the warp iterates the maximum
+//      per-lane count, not the survivor count), with the unchanged eval_pair / blend arithmetic, so
+//      every decision and every value are bitwise those of the dense path (RTGS_RENDER_DENSE checks).
+
+// 32x32 bit-matrix transpose across the warp: in, lane i holds row i (bit c = M[i][c]); out, lane p
+// holds column p (bit j = M[j][p]).  Recursive block swaps, 5 shuffles.
+__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, uint32_t lane) {
+  const uint32_t M[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+  for (int i = 0; i < 5; ++i) {
+    const uint32_t s = 16u >> i, m = M[i];
+    const uint32_t y = __shfl_xor_sync(0xffffffffu, x, (int)s);
+    x = (lane & s) ? ((x & ~m) | ((y & ~m) >> s)) : ((x & m) | ((y & m) << s));
+  }
+  return x;
+}
+
+// Pixels of the 8x4 block (bx0, by0) (bit 8*row + col) that MAY pass eval_pair for record (a, c)
+// (a = mu hi/lo, c = (A', B', C', log2 alpha), p2 = A' dx^2 + B' dx dy + C' dy^2, dx = mu_x - u_x).
+// For pixel row y (dy = mu_y - y) the support p2 >= pm is the dx interval centred at B' dy / (2A')
+// (x = mu_x - dx) of half-width sqrt(disc) / (2|A'|), disc = 4 A' pm - dy^2 (4 A'C' - B'^2).  The
+// threshold is lowered by 1 % + 0.01 (a 0.5 %-larger ellipse) and the interval widened by 0.02 px, far
+// beyond the float32 rounding of this computation and of eval_pair, so the mask is a superset.
+__device__ __forceinline__ uint32_t support_mask(const float4 a, const float4 c, float bx0, float by0) {
+  const float mx = a.x + a.z, my = a.y + a.w;
+  const float pmin = fmaxf(kP2Min, kLog2FMin - c.w);
+  const float pm = __fmaf_rn(pmin, 1.01f, -0.01f);
+  const float D0 = 4.f * c.x * pm;                       // > 0 (A' < 0, pm < 0)
+  const float D2 = __fmaf_rn(4.f * c.x, c.z, -c.y * c.y); // 4 A'C' - B'^2 > 0
+  const float inv2a = -0.5f / c.x;                       // 1 / (2 |A'|)
+  const float xs = -c.y * inv2a;                         // x centre = mu_x + xs dy
+  uint32_t m = 0u;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float dy = my - (by0 + (float)k);
+    const float disc = __fmaf_rn(-D2, dy * dy, D0);
+    if (disc >= 0.f) {
+      float sq;
+      asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(sq) : "f"(disc));  // ~2 ulp: inside the 0.02 px margin
+      const float h = __fmaf_rn(sq, inv2a, 0.02f);
+      const float xc = __fmaf_rn(xs, dy, mx) - bx0;
+      const int lo = (int)ceilf(fmaxf(xc - h, -1.f));
+      const int hi = (int)floorf(fminf(xc + h, 8.f));
+      const int l0 = max(lo, 0), h0 = min(hi, 7);
+      if (l0 <= h0) m |= ((0xFFu >> (7 - (h0 - l0))) << l0) << (8 * k);
+    }
+  }
+  return m;
+}
+
 struct FwdArgs {
   const float4* rec;
   const uint32_t* zkey;
@@ -209,10 +271,16 @@ struct FwdArgs {
 // the mapping step do not, saving 3 instructions per survivor)
 // LAST: track n_contrib (the sorted-list position past the last blended entry, which the backward
 // needs); a FULL render for the add masks / tracking only passes n_contrib = NULL and skips it
-template <bool MASKED, bool COUNT, bool LAST = true>
-__global__ void __launch_bounds__(32 * ((MASKED ? kHalfWarps : kTileWarps) + 1)) k_render_fwd(const FwdArgs a) {
+// SPAN: the span-mask consumer (default); false = the dense consumer (RTGS_RENDER_DENSE, verification)
+#ifndef RTGS_SPAN_MINB
+#define RTGS_SPAN_MINB 5
+#endif
+template <bool MASKED, bool COUNT, bool LAST = true, bool SPAN = true>
+__global__ void __launch_bounds__(32 * ((MASKED ? kHalfWarps : kTileWarps) + 1),
+                                  SPAN && !MASKED ? RTGS_SPAN_MINB : 1) k_render_fwd(const FwdArgs a) {
   constexpr int NW = MASKED ? kHalfWarps : kTileWarps;  // MASKED: one CTA per half of a kept tile
   __shared__ PipeRing r;  // static: stage addresses fold into immediates
+  __shared__ uint8_t survq[SPAN ? NW : 1][kPipeBatch];  // per warp: the stage's bbox survivors, in order
   int tile, half = 0;
   if (MASKED) {
     if ((blockIdx.x >> 1) >= a.counts[0]) return;
@@ -250,53 +318,125 @@ __global__ void __launch_bounds__(32 * ((MASKED ? kHalfWarps : kTileWarps) + 1))
   uint32_t nblend = 0;  // blended (pixel, Gaussian) pairs of this lane (-> counts[3])
   bool wdone = __all_sync(0xffffffffu, done);
   if (wdone && lane == 0) atomicSub(&r.alive, 1);
-  for (int b = 0; b < nb; ++b) {
-    const int st = b % kPipeStages;
-    mbar_wait(&r.full[st], (uint32_t)(b / kPipeStages) & 1u);
-    if (!wdone) {
-      const uint32_t srec = rec0 + (uint32_t)(st * sizeof(r.rec[0]));  // shared address of this stage
-      const uint32_t pbase = (uint32_t)(start + b * kPipeBatch + 1);
-      const int cnt = min(kPipeBatch, n - b * kPipeBatch);
-      for (int g0 = 0; g0 < cnt; g0 += 32) {
-        const int j = g0 + lane;
-        bool ov = false;
-        if (j < cnt) {
-          const float4 r0 = lds128(srec + 48u * j);
-          const float2 ext = unpack_ext(__uint_as_float(lds32(srec + 48u * j + 44u)));
-          ov = (r0.x + ext.x >= bx0) && (r0.x - ext.x <= bx1) && (r0.y + ext.y >= by0) && (r0.y - ext.y <= by1);
+  if constexpr (SPAN) {
+    const uint32_t q0 = pin(smem_u32(&survq[w][0]));
+    for (int b = 0; b < nb; ++b) {
+      const int st = b % kPipeStages;
+      mbar_wait_sleep(&r.full[st], (uint32_t)(b / kPipeStages) & 1u);
+      if (!wdone) {
+        const uint32_t srec = rec0 + (uint32_t)(st * sizeof(r.rec[0]));  // shared address of this stage
+        const uint32_t pbase = (uint32_t)(start + b * kPipeBatch + 1);
+        const int cnt = min(kPipeBatch, n - b * kPipeBatch);
+        // 1. bbox survivors of the stage, in list order
+        int nq = 0;
+        for (int g0 = 0; g0 < cnt; g0 += 32) {
+          const int j = g0 + lane;
+          bool ov = false;
+          if (j < cnt) {
+            const float4 r0 = lds128(srec + 48u * j);
+            const float2 ext = unpack_ext(__uint_as_float(lds32(srec + 48u * j + 44u)));
+            ov = (r0.x + ext.x >= bx0) && (r0.x - ext.x <= bx1) && (r0.y + ext.y >= by0) && (r0.y - ext.y <= by1);
+          }
+          const uint32_t bal = __ballot_sync(0xffffffffu, ov);
+          if (ov) sts8(q0 + (uint32_t)(nq + __popc(bal & ((1u << lane) - 1u))), (uint32_t)j);
+          nq += __popc(bal);
         }
-        uint32_t m = __ballot_sync(0xffffffffu, ov);
-        while (m) {
-          const int idx = g0 + __ffs(m) - 1;
-          m &= m - 1;
-          // branch-free body: every lane evaluates, the blend is predicated
-          const uint32_t ra = srec + 48u * idx;
-          const float4 r0 = lds128(ra), r1 = lds128(ra + 16u), r2 = lds128(ra + 32u);
-          PairEval e;
-          bool ok = eval_pair(r0, r1, fpx, fpy, e) && !done;
-          // R9: the first f > e^-0.5, tested before termination (position only: no load in the loop)
-          hitpos = (ok && hitpos < 0 && e.f > kDeltaAlpha) ? (int)(pbase - 1u) + idx : hitpos;
-          const float test = __fmul_rn(T, __fsub_rn(1.f, e.f));
-          const bool term = ok && (test < kTMin);
-          done = done || term;
-          ok = ok && !term;
-          const float wgt = ok ? __fmul_rn(e.f, T) : 0.f;
-          cr = __fmaf_rn(r2.x, wgt, cr);
-          cg = __fmaf_rn(r2.y, wgt, cg);
-          cb = __fmaf_rn(r2.z, wgt, cb);
-          T = ok ? test : T;
-          if (LAST) last = ok ? pbase + (uint32_t)idx : last;
-          if (COUNT) nblend += ok ? 1u : 0u;
-        }
-        if (__all_sync(0xffffffffu, done)) {
-          wdone = true;
-          if (lane == 0) atomicSub(&r.alive, 1);
-          break;
+        __syncwarp();
+        // 2. rounds of <= 32 survivors: support masks, transpose, per-lane walk of the own bits
+        for (int q = 0; q < nq; q += 32) {
+          uint32_t pm = 0u;
+          if (q + lane < nq) {
+            const uint32_t ra = srec + 48u * lds8(q0 + (uint32_t)(q + lane));
+            pm = support_mask(lds128(ra), lds128(ra + 16u), bx0, by0);
+          }
+          uint32_t lm = warp_transpose32(pm, (uint32_t)lane);
+          if (done) lm = 0u;
+          // warp-uniform trip count (the largest per-lane bit count): the body is predicated, not
+          // a divergent branch, so no reconvergence bookkeeping per iteration
+          const int trips = __reduce_max_sync(0xffffffffu, (uint32_t)__popc(lm));
+          for (int it = 0; it < trips; ++it) {
+            const bool has = lm != 0u;
+            const int jj = __ffs(lm) - 1;  // -1 without bits: survivor q is read and discarded
+            lm &= lm - 1u;
+            const uint32_t idx = lds8(q0 + (uint32_t)(q + max(jj, 0)));
+            const uint32_t ra = srec + 48u * idx;
+            const float4 r0 = lds128(ra), r1 = lds128(ra + 16u), r2 = lds128(ra + 32u);
+            PairEval e;
+            bool ok = eval_pair(r0, r1, fpx, fpy, e) && has;
+            // R9: the first f > e^-0.5, tested before termination
+            hitpos = (ok && hitpos < 0 && e.f > kDeltaAlpha) ? (int)(pbase - 1u + idx) : hitpos;
+            const float test = __fmul_rn(T, __fsub_rn(1.f, e.f));
+            const bool term = ok && (test < kTMin);
+            done = done || term;
+            lm = term ? 0u : lm;
+            ok = ok && !term;
+            const float wgt = ok ? __fmul_rn(e.f, T) : 0.f;
+            cr = __fmaf_rn(r2.x, wgt, cr);
+            cg = __fmaf_rn(r2.y, wgt, cg);
+            cb = __fmaf_rn(r2.z, wgt, cb);
+            T = ok ? test : T;
+            if (LAST) last = ok ? pbase + idx : last;
+            if (COUNT) nblend += ok ? 1u : 0u;
+          }
+          if (__all_sync(0xffffffffu, done)) {
+            wdone = true;
+            if (lane == 0) atomicSub(&r.alive, 1);
+            break;
+          }
         }
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&r.empty[st]);
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&r.empty[st]);
+  } else {
+    for (int b = 0; b < nb; ++b) {
+      const int st = b % kPipeStages;
+      mbar_wait(&r.full[st], (uint32_t)(b / kPipeStages) & 1u);
+      if (!wdone) {
+        const uint32_t srec = rec0 + (uint32_t)(st * sizeof(r.rec[0]));  // shared address of this stage
+        const uint32_t pbase = (uint32_t)(start + b * kPipeBatch + 1);
+        const int cnt = min(kPipeBatch, n - b * kPipeBatch);
+        for (int g0 = 0; g0 < cnt; g0 += 32) {
+          const int j = g0 + lane;
+          bool ov = false;
+          if (j < cnt) {
+            const float4 r0 = lds128(srec + 48u * j);
+            const float2 ext = unpack_ext(__uint_as_float(lds32(srec + 48u * j + 44u)));
+            ov = (r0.x + ext.x >= bx0) && (r0.x - ext.x <= bx1) && (r0.y + ext.y >= by0) && (r0.y - ext.y <= by1);
+          }
+          uint32_t m = __ballot_sync(0xffffffffu, ov);
+          while (m) {
+            const int idx = g0 + __ffs(m) - 1;
+            m &= m - 1;
+            // branch-free body: every lane evaluates, the blend is predicated
+            const uint32_t ra = srec + 48u * idx;
+            const float4 r0 = lds128(ra), r1 = lds128(ra + 16u), r2 = lds128(ra + 32u);
+            PairEval e;
+            bool ok = eval_pair(r0, r1, fpx, fpy, e) && !done;
+            // R9: the first f > e^-0.5, tested before termination (position only: no load in the loop)
+            hitpos = (ok && hitpos < 0 && e.f > kDeltaAlpha) ? (int)(pbase - 1u) + idx : hitpos;
+            const float test = __fmul_rn(T, __fsub_rn(1.f, e.f));
+            const bool term = ok && (test < kTMin);
+            done = done || term;
+            ok = ok && !term;
+            const float wgt = ok ? __fmul_rn(e.f, T) : 0.f;
+            cr = __fmaf_rn(r2.x, wgt, cr);
+            cg = __fmaf_rn(r2.y, wgt, cg);
+            cb = __fmaf_rn(r2.z, wgt, cb);
+            T = ok ? test : T;
+            if (LAST) last = ok ? pbase + (uint32_t)idx : last;
+            if (COUNT) nblend += ok ? 1u : 0u;
+          }
+          if (__all_sync(0xffffffffu, done)) {
+            wdone = true;
+            if (lane == 0) atomicSub(&r.alive, 1);
+            break;
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&r.empty[st]);
+    }
   }
   if (COUNT) {
     const uint32_t wsum = __reduce_add_sync(0xffffffffu, nblend);
@@ -366,7 +506,8 @@ cudaError_t launch_tile_any(const rtgs_camera& cam, const rtgs_render_out& out, 
 }
 
 cudaError_t launch_render(const rtgs_projected& proj, const rtgs_bins& bins, const PoseF& pose,
-                          const rtgs_camera& cam, int masked, bool count, const rtgs_render_out& out, cudaStream_t s) {
+                          const rtgs_camera& cam, int masked, bool count, const rtgs_render_out& out, cudaStream_t s,
+                          bool dense) {
   FwdArgs a;
   a.rec = reinterpret_cast<const float4*>(proj.rec);
   a.zkey = proj.zkey;
@@ -384,11 +525,16 @@ cudaError_t launch_render(const rtgs_projected& proj, const rtgs_bins& bins, con
   a.index = out.index; a.n_contrib = out.n_contrib;
   const int T = a.cam.TX * a.cam.TY;
   if (count) cudaMemsetAsync(out.counts + 3, 0, 4, s);  // blend counter of this render
-  if (masked && count) k_render_fwd<true, true><<<2 * T, 32 * (kHalfWarps + 1), 0, s>>>(a);
-  else if (masked) k_render_fwd<true, false><<<2 * T, 32 * (kHalfWarps + 1), 0, s>>>(a);
-  else if (count) k_render_fwd<false, true><<<T, 32 * (kTileWarps + 1), 0, s>>>(a);
-  else if (out.n_contrib) k_render_fwd<false, false><<<T, 32 * (kTileWarps + 1), 0, s>>>(a);
-  else k_render_fwd<false, false, false><<<T, 32 * (kTileWarps + 1), 0, s>>>(a);
+  const dim3 gm(2 * T), bm(32 * (kHalfWarps + 1)), gf(T), bf(32 * (kTileWarps + 1));
+  if (dense) {  // verification: the dense consumer (RTGS_RENDER_DENSE)
+    if (masked) k_render_fwd<true, true, true, false><<<gm, bm, 0, s>>>(a);
+    else if (count || out.n_contrib) k_render_fwd<false, true, true, false><<<gf, bf, 0, s>>>(a);
+    else k_render_fwd<false, true, false, false><<<gf, bf, 0, s>>>(a);
+  } else if (masked && count) k_render_fwd<true, true><<<gm, bm, 0, s>>>(a);
+  else if (masked) k_render_fwd<true, false><<<gm, bm, 0, s>>>(a);
+  else if (count) k_render_fwd<false, true><<<gf, bf, 0, s>>>(a);
+  else if (out.n_contrib) k_render_fwd<false, false><<<gf, bf, 0, s>>>(a);
+  else k_render_fwd<false, false, false><<<gf, bf, 0, s>>>(a);
   note_launch();
   return cudaGetLastError();
 }

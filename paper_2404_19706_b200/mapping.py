@@ -24,7 +24,7 @@ import numpy as np
 import torch
 
 from . import _abi
-from ._abi import RTGS_RENDER_COUNT, RTGS_RENDER_COVERAGE, RTGS_RENDER_FULL, RTGS_RENDER_MASKED, check, lib
+from ._abi import RTGS_RENDER_COUNT, RTGS_RENDER_DENSE, RTGS_RENDER_COVERAGE, RTGS_RENDER_FULL, RTGS_RENDER_MASKED, check, lib
 
 FLAG_TRANSPARENT = 1
 FLAG_STABLE = 2
@@ -233,8 +233,10 @@ def project_and_bin(gm: GaussianMap, pose: _abi.Pose, cam: _abi.Camera, proj: Pr
 
 
 def render_color_depth(gm: GaussianMap, proj: ProjectedBuffers, bins: BinBuffers | None, pose: _abi.Pose,
-                       cam: _abi.Camera, mode: int, out: RenderBuffers, stream=None, normals: bool = True):
-    """A0 / A3-A4.  normals=False leaves out.normal untouched (the normal map is for tracking)."""
+                       cam: _abi.Camera, mode: int, out: RenderBuffers, stream=None, normals: bool = True,
+                       dense: bool = False):
+    """A0 / A3-A4.  normals=False leaves out.normal untouched (the normal map is for tracking);
+    dense=True selects the dense verification consumer (RTGS_RENDER_DENSE)."""
     g = gm.c_struct()
     pr = proj.c_struct()
     o = out.c_struct(mode)
@@ -243,6 +245,8 @@ def render_color_depth(gm: GaussianMap, proj: ProjectedBuffers, bins: BinBuffers
     b = bins.c_struct() if bins is not None else None
     if out.count_blends and mode in (RTGS_RENDER_FULL, RTGS_RENDER_MASKED):
         mode |= RTGS_RENDER_COUNT
+    if dense and mode != RTGS_RENDER_COVERAGE:
+        mode |= RTGS_RENDER_DENSE
     check(lib().rtgs_render_color_depth(C.byref(g), C.byref(pr), C.byref(b) if b is not None else None, C.byref(pose),
                                         C.byref(cam), mode, C.byref(o), _stream(stream)), "rtgs_render_color_depth")
 
