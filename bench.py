@@ -1,15 +1,21 @@
 #!/usr/bin/env python
 """Benchmark of the RTG-SLAM mapping hot path on B200 (contract: DESIGN.md §7).
 
-One STEP = one pass of every §8(a) row over one synthetic C3 (Replica-shaped, 1200x680, 1M Gaussians,
-10 % unstable) frame:
-    ingest     A1 project -> A2 bin (all tiles) -> A3/A4 FULL render -> A7 classify + sample
-    iteration  A1 project -> A0 coverage + tile keep -> A2 bin (kept tiles) -> A3/A4 MASKED render
-               -> A5 masked backward -> [N>1: NCCL all-reduce of the slot gradients] -> A6 Adam
-`value` counts one mapping iteration per step (each step also carries a full frame ingest, so it is
-conservative w.r.t. the paper's 'mapping / iteration').
+Workloads (BASELINE.json configs; `--config`, default C3 at one GPU and C5 under torchrun):
+  C3 / C2  one STEP = one pass of every §8(a) row over one synthetic frame:
+      ingest     A1 project -> A2 bin (all tiles) -> A3/A4 FULL render -> A7 classify + sample
+      iteration  A1 project -> A0 coverage + tile keep -> A2 bin (kept tiles) -> A3/A4 MASKED render
+                 -> A5 masked backward -> A6 Adam
+      `value` counts one mapping iteration per step (each step also carries a full frame ingest, so
+      it is conservative w.r.t. the paper's 'mapping / iteration').
+  C4       render-only novel views: A1 + A2 + A3/A4 FULL per step (frames/s).
+  C5       the keyframe batch: 64 C3 views split over N ranks; per view a FULL
+           render, its top-40 % colour-error pixels and the masked backward over ALL Gaussians; an
+           in-place NCCL reduce-scatter of the gradients, Adam on each rank's block of rows, in-place
+           NCCL all-gathers of the map (dist.global_step_sharded).  `value` = views/s of the whole job
+           (strong scaling: the 64-view batch is fixed), plus T_1 / (N T_N) measured in the same run.
 
-    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+    python bench.py [--gpus N --steps K --warmup W] [--config C2|C3|C4|C5] [--impl reference]
 """
 from __future__ import annotations
 
@@ -99,87 +105,180 @@ def _scene(cfg_name):
     return _SCENES[cfg_name]
 
 
-def cpu_baseline(cfg_name: str, n_pixels: int = 48, seed: int = 0):
-    """The oracle (float64 CPU, as it stands) on a bounded sample of the same workload: projection of
-    ALL Gaussians + render and autograd backward of `n_pixels` active pixels; extrapolated linearly in
-    the active-pixel count to one full mapping iteration."""
+def _oracle_active_count(cfg_name):
+    """|P| of the config's primary-view iteration by the ORACLE (O4 coverage by splatting the unstable
+    support rects, the 50 % tile rule): the workload size the CPU leg extrapolates to (setup, untimed)."""
     import torch
     from oracle import projection as OP, raster as OR
+    cfg, scene, R, t, _ = _scene(cfg_name)
+    with torch.no_grad():
+        pr = OP.project(OP.params_from_scene(scene), R, t, OP.camera(cfg), scene["sh_degree"])
+    cov, _ = OR.unstable_coverage_splat(pr, (scene["flags"] & 2) == 0, cfg.width, cfg.height)
+    return int(OR.active_set(cov, OR.tile_keep(cov)).sum())
+
+
+def oracle_sample(cfg_name: str, k_fwd: int, k_bwd: int, seed: int = 0):
+    """The oracle (float64 CPU, as it stands) on a bounded sample of the step: projection of ALL
+    Gaussians, the forward render (Eq.1-5) of `k_fwd` pixels, and the masked iteration's loss (colour
+    AND depth, Eq.7 with the full-frame normalisations) + autograd backward over `k_bwd` active
+    pixels (the projection is part of the autograd graph, as in the iteration).  Returns the timings
+    of the three parts."""
+    import torch
+    from oracle import loss as OL, projection as OP, raster as OR
     cfg, scene, R, t, (col, dep) = _scene(cfg_name)
     cam = OP.camera(cfg)
     threads = torch.get_num_threads()
-    t0 = time.perf_counter()
-    prm = OP.params_from_scene(scene, requires_grad=True)
-    proj = OP.project(prm, R, t, cam, scene["sh_degree"])
-    t_proj = time.perf_counter() - t0
-    # active pixels of the slab: sample among pixels covered by unstable Gaussians (right border)
     rng = np.random.default_rng(seed)
-    u = scene["u_img"][(scene["flags"] & 2) == 0]
-    x_lo = int(np.percentile(u, 5))
-    px = rng.integers(max(x_lo, 0), cfg.width, n_pixels)
-    py = rng.integers(0, cfg.height, n_pixels)
-    pix = np.stack([px, py], 1)
+    t0 = time.perf_counter()
+    with torch.no_grad():
+        proj = OP.project(OP.params_from_scene(scene), R, t, cam, scene["sh_degree"])
+    t_proj = time.perf_counter() - t0
+    pix = np.stack([rng.integers(0, cfg.width, k_fwd), rng.integers(0, cfg.height, k_fwd)], 1)
     t1 = time.perf_counter()
     with torch.no_grad():
-        OR.render_pixels(proj, pix, cam, R, chunk=4, want_margin=False)
+        OR.render_pixels(proj, pix, cam, R, chunk=8, want_margin=False)
     t_fwd = time.perf_counter() - t1
-    t1 = time.perf_counter()
-    out = OR.render_pixels(proj, pix, cam, R, chunk=4, want_margin=False)
-    Ct = torch.as_tensor(col[:, py, px].T.astype(np.float64))
-    L = (out["color"] - Ct).abs().sum() / (3.0 * n_pixels)
-    L.backward()
-    t_pix = time.perf_counter() - t1
-    # |P| of the C3 iteration ~ the slab share of the image (measured by the GPU arm and passed in)
-    return dict(t_proj=t_proj, t_fwd=t_fwd, t_pix=t_pix, n_pixels=n_pixels, threads=threads)
+    # active pixels: the slab (the unstable Gaussians' image-x range, P:128-131)
+    u = scene["u_img"][(scene["flags"] & 2) == 0]
+    x_lo = int(np.percentile(u, 5))
+    act = np.zeros((cfg.height, cfg.width), bool)
+    act[rng.integers(0, cfg.height, k_bwd), rng.integers(max(x_lo, 0), cfg.width, k_bwd)] = True
+    t2 = time.perf_counter()
+    res = OL.iteration_loss(scene, R, t, cam, col, dep, act)
+    res["L"].backward()
+    t_bwd = time.perf_counter() - t2
+    return dict(t_proj=t_proj, t_fwd=t_fwd, t_bwd=t_bwd, k_fwd=k_fwd, k_bwd=int(act.sum()), threads=threads,
+                t_sample=time.perf_counter() - t0)
 
 
 def oracle_step_seconds(r, cfg, n_active):
-    """The oracle doing the bench's step: ingest (projection of all Gaussians + forward render of every
-    pixel) + one uncached mapping iteration (projection again + render/backward of the active pixels)."""
-    n = r["n_pixels"]
-    return 2.0 * r["t_proj"] + r["t_fwd"] * cfg.width * cfg.height / n + r["t_pix"] * n_active / n
+    """The oracle doing the bench's step, extrapolated from the sample: ingest (projection of all
+    Gaussians + forward render of every pixel) + one uncached mapping iteration (projection again,
+    part of the timed backward sample, + render / loss / backward of the |P| active pixels)."""
+    return (r["t_proj"] + r["t_fwd"] * cfg.width * cfg.height / r["k_fwd"]
+            + r["t_bwd"] * n_active / r["k_bwd"])
 
 
-ORACLE_SAMPLE = ("projection of all {n} Gaussians + forward render of {k} pixels + render/backward of {k} "
-                 "active pixels (float64 torch CPU), extrapolated to the step: 2 projections + forward of all "
-                 "{wh} pixels + render/backward of |P| = {p} active pixels")
+ORACLE_SAMPLE = ("per step: projection of all {n} Gaussians + forward render of {kf} pixels + colour+depth loss "
+                 "and autograd backward of {kb} active pixels (float64 torch CPU, {th} threads), {ts:.1f} s; "
+                 "extrapolated linearly to the step (projection + forward of all {wh} pixels + iteration over "
+                 "|P| = {p} active pixels, |P| from the oracle's own coverage)")
+
+
+def oracle_c1_measured():
+    """Supplementary, MEASURED (no extrapolation): the oracle's whole C1 step (BASELINE configs[0]):
+    ingest (projection, FULL render of every pixel, Eq.6 classify) + one iteration (coverage + tile
+    keep, projection + render + loss + backward of P, Adam) - on all host threads and on one."""
+    import torch
+    from oracle import classify as OC, loss as OL, optim as OO, projection as OP, raster as OR
+    from synth import CONFIGS, make_frame, make_pose, make_scene
+    cfg = CONFIGS["C1"]
+    scene = make_scene(cfg)
+    R, t = make_pose(cfg)
+    col, dep = make_frame(cfg)
+    cam = OP.camera(cfg)
+    K = (scene["sh_degree"] + 1) ** 2
+
+    def step():
+        with torch.no_grad():
+            pr = OP.project(OP.params_from_scene(scene), R, t, cam, scene["sh_degree"])
+            img = OR.render_image(pr, cam, R, want_margin=False)
+        OC.classify(img["color"].numpy(), img["trans"].numpy(), img["depth"].numpy(), img["index"], col, dep,
+                    scene["flags"])
+        unstable = (scene["flags"] & 2) == 0
+        cov, _ = OR.unstable_coverage(pr, unstable, OR.all_pixels(cfg.width, cfg.height))
+        cov = cov.reshape(cfg.height, cfg.width)
+        act = OR.active_set(cov, OR.tile_keep(cov))
+        gid = np.nonzero(unstable)[0]
+        res = OL.iteration_grads(scene, R, t, cam, col, dep, act, gid)
+        theta = np.concatenate([scene["pos"][gid], scene["log_scale"][gid], scene["rot"][gid],
+                                scene["sh"][gid].reshape(len(gid), -1)], 1).astype(np.float64)
+        z = np.zeros_like(theta)
+        OO.unstable_step(theta, res["grad"], z, z.copy(), theta[:, :10].copy(), (scene["flags"][gid] & 1) != 0,
+                         1000.0, OO.lr_vector(K, 1e-3, 5e-4, 2.5e-5, 4e-3, 1e-3), 1, np.zeros(len(gid), np.int64))
+
+    out = {}
+    nt = torch.get_num_threads()
+    for label, threads in (("all_threads", nt), ("one_thread", 1)):
+        torch.set_num_threads(threads)
+        step()  # warm
+        t0 = time.perf_counter()
+        step()
+        out[label] = {"s_per_step": round(time.perf_counter() - t0, 3), "threads": threads}
+    torch.set_num_threads(nt)
+    return out
+
+
+def reference_arm(args, rank, world):
+    """--impl reference: the oracle timed on the host cores (rank 0 only), one bounded sample of the
+    workload per step (ms_per_step is the sample's measured time; value extrapolates the sample to
+    the whole step, the fraction is stated).  The workload is the GPU arm's: C3 at one GPU, the C5
+    keyframe batch under torchrun (64 views: per view projection + forward of every pixel + the
+    backward of the top-40 % pixels over every Gaussian)."""
+    if rank != 0:
+        return
+    from synth import CONFIGS
+    eff = args.config or ("C5" if world > 1 else "C3")
+    cfg_name = "C3" if eff == "C5" else eff
+    cfg = CONFIGS[cfg_name]
+    HW = cfg.width * cfg.height
+    n_active = int(round(0.4 * HW)) if eff == "C5" else _oracle_active_count(cfg_name)
+    rows = []
+    for s in range(args.warmup + args.steps):
+        r = oracle_sample(cfg_name, args.ref_pixels, args.ref_pixels, seed=s)
+        if s >= args.warmup:
+            rows.append(r)
+    t_sample = statistics.mean(r["t_sample"] for r in rows)
+    t_unit = statistics.mean(oracle_step_seconds(r, cfg, n_active) for r in rows)
+    if eff == "C5":   # value in views / s: the batch step is 64 such views
+        v, t_step = 1.0 / t_unit, N_C5_VIEWS * t_unit
+        config = batch_config(cfg, world)
+        what = (f"one C5 view (projection + forward of all {HW} pixels + backward of the top-40 % = {n_active} "
+                f"pixels), x {N_C5_VIEWS} views per step")
+    else:
+        v, t_step = 1.0 / t_unit, t_unit
+        config = mapping_config(cfg, True, "CUDA graph of the whole step (2 streams)", world)
+        what = None
+    cpu = {"value": v, "unit": "iters/s", "cores": rows[0]["threads"], "kind": "oracle", "extrapolated": True,
+           "sample_fraction": t_sample / t_step,
+           "sample": ORACLE_SAMPLE.format(n=cfg.n, kf=rows[0]["k_fwd"], kb=rows[0]["k_bwd"], th=rows[0]["threads"],
+                                          ts=t_sample, wh=HW, p=n_active) + (f"; {what}" if what else "")}
+    line = {"metric": METRIC, "value": v, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * t_sample, "higher_is_better": True,
+            "scaling": "strong" if eff == "C5" else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config, "impl": "reference", "cpu_baseline": cpu,
+            "e2e": {"value": v, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def batch_config(cfg, world):
+    return {"workload": (f"C5 keyframe batch: {N_C5_VIEWS} views of the C3 Replica-shaped "
+                         f"{cfg.width}x{cfg.height} 1M-Gaussian scene (+-0.3 m / 15 deg around the "
+                         f"primary view); iteration = one view's FULL render + top-40 % colour-error "
+                         f"pixels + masked backward over ALL Gaussians; step = {N_C5_VIEWS} views + "
+                         f"in-place NCCL reduce-scatter + Adam on each rank's row block (position lr "
+                         f"0, others x 0.1) + in-place NCCL all-gathers (P:284)"),
+            "l2": "flushed between timed steps (256 MB write)", "launch": "eager (NCCL in the step)",
+            "parallelism": f"{world} ranks x {N_C5_VIEWS // world} views, sharded optimiser"}
+
+
+def mapping_config(cfg, cached, launch, world):
+    return {"workload": workload_name(cfg, cached),
+            "l2": "flushed between timed steps (256 MB write); Gaussian SoA 237 MB > L2",
+            "launch": launch, "parallelism": "single GPU" if world == 1 else f"{world} replicas"}
+
+
+SHAPES = {"C1": "small synthetic", "C2": "TUM-shaped", "C3": "Replica-shaped", "C4": "ScanNet++-shaped"}
 
 
 def workload_name(cfg, cached=True):
-    head = (f"{cfg.name} Replica-shaped {cfg.width}x{cfg.height}, {cfg.n} Gaussians (10% transparent), "
+    head = (f"{cfg.name} {SHAPES.get(cfg.name, 'synthetic')} {cfg.width}x{cfg.height}, {cfg.n} Gaussians "
+            f"({int(round(cfg.frac_transparent * 100))}% transparent), "
             f"{int(cfg.frac_unstable * 100)}% unstable slab, SH deg {cfg.sh_degree}; ")
     if cached:
         return head + ("step = frame ingest (A1,A2,A3/A4 FULL,A7, f3 stable cache) + one masked mapping "
                        "iteration (A1 on the unstable slots,A0,A2 merged with the cache,A3/A4,A5,A6)")
     return head + "step = frame ingest (A1,A2,A3/A4 FULL,A7) + one masked mapping iteration (A1,A0,A2,A3/A4,A5,A6)"
-
-
-def reference_arm(args, rank, world):
-    """--impl reference: the oracle timed on the host cores (rank 0 only), bounded sample per step."""
-    if rank != 0:
-        return
-    from synth import CONFIGS
-    cfg = CONFIGS[args.config]
-    # |P| of the C3 step as the GPU arm measures it (bench line `active.active_px`), else 12 % of the image
-    n_active = args.active_pixels or (83249 if args.config == "C3" else int(0.12 * cfg.width * cfg.height))
-    times = []
-    for s in range(args.warmup + args.steps):
-        r = cpu_baseline(args.config, n_pixels=args.ref_pixels, seed=s)
-        t_iter = oracle_step_seconds(r, cfg, n_active)
-        if s >= args.warmup:
-            times.append(t_iter)
-    t = statistics.mean(times)
-    v = 1.0 / t
-    line = {"metric": METRIC, "value": v, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1e3 * t, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload_name(cfg), "l2": "n/a (CPU)"},
-            "impl": "reference",
-            "cpu_baseline": {"value": v, "unit": "iters/s", "cores": r["threads"], "kind": "oracle",
-                             "sample": ORACLE_SAMPLE.format(n=cfg.n, k=args.ref_pixels, wh=cfg.width * cfg.height,
-                                                            p=n_active)},
-            "e2e": {"value": v, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
 
 
 def main():
@@ -188,10 +287,9 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C3")
+    ap.add_argument("--config", default=None, help="C2 | C3 | C4 | C5 (default: C3, or C5 under torchrun)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--ref-pixels", type=int, default=24)
-    ap.add_argument("--active-pixels", type=int, default=0)
+    ap.add_argument("--ref-pixels", type=int, default=64, help="oracle sample: forward and backward pixels")
     ap.add_argument("--phases", action="store_true", help="print per-call timings to stderr")
     ap.add_argument("--no-graph", action="store_true", help="launch every step eagerly (no CUDA graph)")
     ap.add_argument("--no-cache", action="store_true", help="iteration without the f3 stable-projection cache")
@@ -207,21 +305,162 @@ def main():
     if args.impl == "reference":
         reference_arm(args, rank, world)
         return
+    if args.config is None:   # the keyframe batch is the workload that shards (north star)
+        args.config = "C5" if world > 1 else "C3"
 
     import torch
     import torch.distributed as dist
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-
     import paper_2404_19706_b200 as P
     from paper_2404_19706_b200 import build as B
-    from paper_2404_19706_b200.dist import allreduce_grads
-    from synth import CONFIGS, make_frame, make_pose, make_scene, trajectory_pose
     if rank == 0:
         B.build()
     if world > 1:
         dist.barrier()
+    if args.config == "C5":
+        run_batch(args, rank, world, local)
+    elif args.config == "C4":
+        run_render_only(args, rank, world, local)
+    else:
+        if world > 1:
+            raise SystemExit("a single frame stays on one GPU (north star): multi-GPU runs use --config C5")
+        run_mapping(args, rank, world, local)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def measure_ablation(P, eng, gm, cam, pose, col, dep, restore, flush, reps=10):
+    """Table stable_gaussian_ablation on the bench's frame: time per optimisation iteration
+    (device, median of `reps`, map restored and L2 flushed between iterations, outside the events) for
+    (a) all Gaussians optimised over the whole image, (b) only the unstable Gaussians over the whole
+    image, (c) only the unstable Gaussians over the pixels they cover (P = Eq.12 + the 50 % tiles, the
+    production iteration, uncached and f3-cached).  (a) and (b): A1 + A2 + a FULL render + every pixel
+    active + the backward over the Gaussians of the row + Adam over them."""
+    import torch
+    from paper_2404_19706_b200 import mapping as M
+    stream = torch.cuda.current_stream()
+    restore()
+    eng.ingest(col, dep, pose)   # eager: the f3 cache (and its ready event) outside any graph capture
+    eng._global_state(1)
+    rb = eng.g_rb
+
+    def full_all_pixels():
+        P.project_and_bin(gm, pose, cam, eng.proj, eng.bins, eng.ws_bin)
+        P.render_color_depth(gm, eng.proj, eng.bins, pose, cam, P.RTGS_RENDER_FULL, rb)
+        P.topk_error_mask(rb, col, cam, 1.0, rb, eng.g_ws_topk)   # ratio 1: every pixel, every tile
+
+    def it_all():
+        full_all_pixels()
+        M.render_backward_masked(gm, eng.proj, eng.bins, pose, cam, rb, col, dep, eng.weights, eng.g_slot,
+                                 eng.g_gid, eng.g_grad, eng.g_loss, eng.g_ws_bwd)
+        eng.global_adam_block(0, eng.g_rows, lr_scale=1.0)
+
+    def it_unstable_all_px():
+        full_all_pixels()
+        M.render_backward_masked(gm, eng.proj, eng.bins, pose, cam, rb, col, dep, eng.weights, eng.slot_of_gid,
+                                 eng.gid_of_slot, eng.grad, eng.loss, eng.ws_bwd)
+        eng.optimizer_step()
+
+    def it_masked(cached):
+        def f():
+            eng.use_cache = cached
+            eng.forward_masked(pose)
+            eng.backward_adam(col, dep, pose)
+        return f
+
+    out = {}
+    use_cache0 = eng.use_cache
+    for name, fn in (("S_all_pixels", it_all), ("S_unstable_all_pixels", it_unstable_all_px),
+                     ("S_unstable_P_uncached", it_masked(False)), ("S_unstable_P", it_masked(True))):
+        ts = []
+        for _ in range(reps + 2):
+            restore()
+            flush.zero_()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        out[name + "_ms"] = round(statistics.median(ts[2:]), 4)
+    eng.use_cache = use_cache0
+    restore()
+    out["trend_holds"] = bool(out["S_all_pixels_ms"] > out["S_unstable_all_pixels_ms"] > out["S_unstable_P_ms"])
+    out["paper_ms"] = {"Storeroom": [9.8, 7.4, 5.2], "Hotel room": [8.4, 6.5, 4.7], "Home": [8.9, 6.4, 4.3],
+                       "note": "P:753-755, RTX 4090, order S / S_unstable all px / S_unstable unstable px; context"}
+    return out
+
+
+def c5_views(P, cfg, idx):
+    """The C5 keyframe views `idx` of the C3 scene (synth.make_pose view v: +-0.3 m / 15 deg around the
+    primary view), as device (colour, depth, pose) triples."""
+    import torch
+    from synth import make_frame, make_pose
+    out = []
+    for v in idx:
+        R, t = make_pose(cfg, view=v)
+        c, d = make_frame(cfg, (R, t))
+        out.append((torch.as_tensor(c, device="cuda"), torch.as_tensor(d, device="cuda"), P.make_pose(R, t)))
+    return out
+
+
+N_C5_VIEWS = 64
+
+
+def measure_c5_one_gpu(P, eng, cfg, restore, flush, reps=3):
+    """One C5 global step (64 views, every Gaussian, one Adam step) on this GPU: the T_1 of the
+    multi-GPU keyframe-batch runs (dist.global_step_sharded with one rank)."""
+    import torch
+    from paper_2404_19706_b200.dist import global_step_sharded
+    stream = torch.cuda.current_stream()
+    views = c5_views(P, cfg, range(N_C5_VIEWS))
+    global_step_sharded(eng, views)  # warm: allocates the all-Gaussian state
+    ts = []
+    for _ in range(reps):
+        restore()
+        flush.zero_()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        global_step_sharded(eng, views)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    t = statistics.median(ts)
+    del views
+    return {"views": N_C5_VIEWS, "ms_per_global_step": round(t, 3), "views_per_s": round(N_C5_VIEWS * 1e3 / t, 1),
+            "note": "BASELINE configs[4] at N = 1: per view FULL render + top-40 % pixels + masked backward over "
+                    "all 1M Gaussians; one Adam step (position lr 0, others x 0.1); eager"}
+
+
+def cpu_leg(args, cfg):
+    """`cpu_baseline` of the GPU line: the oracle as it stands on the host cores, a bounded sample of
+    the same step extrapolated (stated), plus the MEASURED whole C1 step (all threads / one)."""
+    try:
+        n_active = _oracle_active_count(cfg.name)
+        k = 4 * args.ref_pixels   # ~10-30 s of oracle work at C3 (16 host threads)
+        r = oracle_sample(cfg.name, k, k)
+        t_step = oracle_step_seconds(r, cfg, n_active)
+        out = {"value": 1.0 / t_step, "unit": "iters/s", "cores": r["threads"], "kind": "oracle",
+               "extrapolated": True, "sample_fraction": r["t_sample"] / t_step,
+               "sample": ORACLE_SAMPLE.format(n=cfg.n, kf=r["k_fwd"], kb=r["k_bwd"], th=r["threads"],
+                                              ts=r["t_sample"], wh=cfg.width * cfg.height, p=n_active)}
+        out["c1_measured"] = oracle_c1_measured()
+        return out
+    except Exception as e:  # report, never fake
+        return {"value": None, "error": repr(e)[:200]}
+
+
+def run_mapping(args, rank, world, local):
+    """C3 / C2: the mapping step (ingest + one masked iteration), CUDA graph, single GPU."""
+    import torch
+    import torch.distributed as dist
+    import paper_2404_19706_b200 as P
+    from synth import CONFIGS, make_frame, make_pose, make_scene, trajectory_pose
     cfg = CONFIGS[args.config]
     scene = make_scene(cfg)
     # each rank optimises the shared map from its own keyframe view (rank 0 = the primary view)
@@ -260,7 +499,7 @@ def main():
 
     def step(c, d, frame_idx):
         # ingest (side stream) || masked iteration (current stream); Adam waits for the ingest projection
-        eng.step(c, d, pose, seed=1234, frame_idx=frame_idx, reduce_grads=allreduce_grads if world > 1 else None)
+        eng.step(c, d, pose, seed=1234, frame_idx=frame_idx)
 
     for i in range(args.warmup):
         step(col, dep, i)
@@ -543,6 +782,16 @@ def main():
                          "Gaussians each, one Adam step (position lr 0, other rates x 0.1)"}
         restore()
 
+    # ---- Table stable_gaussian_ablation trend, supplementary ---------------------------
+    ablation = None
+    if rank == 0 and world == 1 and not args.no_window:
+        ablation = measure_ablation(P, eng, gm, cam, pose, col, dep, restore, flush)
+    # ---- the C5 keyframe batch on this one GPU (the multi-GPU runs' T_1), supplementary -----------
+    c5_one = None
+    if rank == 0 and world == 1 and not args.no_window and args.config == "C3":
+        c5_one = measure_c5_one_gpu(P, eng, cfg, restore, flush)
+        restore()
+
     # ---- the paper's mapping window, once (supplementary; mutates the map, so it runs last) -------
     # 6 frames (Replica window): ingest + insertion each, a new slot set, 50 iterations on
     # randomly sampled window frames through the per-frame f3 caches, fusion + state management.
@@ -602,10 +851,8 @@ def main():
             "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": workload_name(cfg, eng.use_cache),
-                       "l2": "flushed between timed steps (256 MB write); Gaussian SoA 237 MB > L2",
-                       "launch": "CUDA graph of the whole step (2 streams)" if graph is not None else "eager",
-                       "parallelism": f"dp{world} over keyframe views" if world > 1 else "single GPU"},
+            "config": mapping_config(cfg, eng.use_cache,
+                                     "CUDA graph of the whole step (2 streams)" if graph is not None else "eager", world),
             "roofline": {"kernel": "k_render_fwd<FULL> (A3/A4, dominant kernel of the step)", "bound": "alu",
                          "achieved": alu_achieved, "peak": alu_peak, "unit": "TFLOP/s", "frac": alu_achieved / alu_peak,
                          "traffic": traffic.get("k_render_fwd<FULL>"), "peak_kind": "derived: 148 SM x 128 FP32 lanes x sampled SM clock",
@@ -645,19 +892,304 @@ def main():
             "active": {"kept_tiles": counts[0], "active_px": counts[1], "instances_full": n_inst,
                        "instances_iter": ninst_iter},
         }
+        line["ablation"] = ablation
+        line["c5_one_gpu"] = c5_one
         if world == 1 and not args.no_cpu_baseline:
-            try:
-                r = cpu_baseline(args.config, n_pixels=args.ref_pixels)
-                t_cpu = oracle_step_seconds(r, cfg, max(counts[1], 1))
-                line["cpu_baseline"] = {"value": 1.0 / t_cpu, "unit": "iters/s", "cores": r["threads"], "kind": "oracle",
-                                        "sample": ORACLE_SAMPLE.format(n=cfg.n, k=r["n_pixels"], wh=cfg.width * cfg.height,
-                                                                       p=counts[1])}
-            except Exception as e:  # report, never fake
-                line["cpu_baseline"] = {"value": None, "error": repr(e)[:200]}
+            line["cpu_baseline"] = cpu_leg(args, cfg)
         print(json.dumps(line), flush=True)
+
+
+def _timed(run_step, between, steps, world, local, stream):
+    """W-excluded timed region: barrier + synchronize on both sides, CUDA events on `stream` around
+    each step, `between()` (map restore, L2 flush) outside the events; mean step ms, max over ranks;
+    nvidia-smi clocks sampled during the region."""
+    import torch
+    import torch.distributed as dist
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
     if world > 1:
         dist.barrier()
-        dist.destroy_process_group()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        t_spin = time.perf_counter()
+        while time.perf_counter() - t_spin < 0.25:  # keep the GPU busy while nvidia-smi starts sampling
+            run_step(0)
+        torch.cuda.synchronize()
+        for i in range(steps):
+            between()
+            starts[i].record(stream)
+            run_step(i)
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+    t = statistics.mean(s.elapsed_time(e) for s, e in zip(starts, ends))
+    if world > 1:
+        tt = torch.tensor([t], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt.item())
+        dist.barrier()
+    return t, clk.summary()
+
+
+def _alu_roofline(blends, t_ms, clocks, what):
+    sm_mhz = clocks.get("sm_mhz") or _peaks()[1]
+    peak = 148 * 128 * sm_mhz * 1e-3 * 1e9 / 1e12
+    ach = 16 * blends / (t_ms * 1e-3) / 1e12
+    return {"kernel": what, "bound": "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+            "traffic": None, "peak_kind": "derived: 148 SM x 128 FP32 lanes x sampled SM clock",
+            "algorithmic": f"16 FP32 instr x {blends} blends per launch", "time_ms": t_ms}
+
+
+def run_render_only(args, rank, world, local):
+    """C4 (BASELINE configs[3]): render-only novel views of the ScanNet++-shaped 4M-Gaussian map: per
+    step A1 project + A2 bin + A3/A4 FULL render (colour, T, depth, index, normals) at the next of 8
+    novel poses, one CUDA graph per pose.  value = frames/s (per GPU; replicas under torchrun)."""
+    import torch
+    import paper_2404_19706_b200 as P
+    from paper_2404_19706_b200 import mapping as M
+    from synth import CONFIGS, make_pose, make_scene
+    cfg = CONFIGS["C4"]
+    scene = make_scene(cfg)
+    gm = P.GaussianMap.from_arrays(scene)
+    cam = P.camera_of(cfg)
+    poses = [P.make_pose(*make_pose(cfg, view=v)) for v in range(8)]
+    n, cap = gm.n, 3 * cfg.n
+    proj, bins = M.ProjectedBuffers(n), M.BinBuffers(cam, cap)
+    ws = torch.empty(M.bin_workspace_size(n, cam, cap), dtype=torch.uint8, device="cuda")
+    rb = M.RenderBuffers(cam, count_blends=False)
+    rb.track_last = False
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+
+    def frame(k):
+        P.project_and_bin(gm, poses[k % len(poses)], cam, proj, bins, ws)
+        P.render_color_depth(gm, proj, bins, poses[k % len(poses)], cam, P.RTGS_RENDER_FULL, rb)
+
+    for k in range(max(args.warmup, len(poses))):
+        frame(k)
+    torch.cuda.synchronize()
+    worst = int(bins.n_instances.item())
+    if worst > cap:
+        raise RuntimeError(f"instance capacity {cap} < {worst}")
+    l0 = P.launch_count()
+    frame(0)
+    torch.cuda.synchronize()
+    per_frame = P.launch_count() - l0
+    graphs = []
+    for k in range(len(poses)):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            frame(k)
+        graphs.append(g)
+    torch.cuda.synchronize()
+    t_step, clocks = _timed(lambda i: graphs[i % len(graphs)].replay(), lambda: flush.zero_(), args.steps, world,
+                            local, stream)
+    # the FULL render alone + its blend count (counting variant, one extra launch), on pose 0
+    frame(0)
+    rt = []
+    for _ in range(10):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        P.render_color_depth(gm, proj, bins, poses[0], cam, P.RTGS_RENDER_FULL, rb)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        rt.append(e0.elapsed_time(e1))
+    t_render = statistics.mean(rt)
+    rb.count_blends = True
+    P.render_color_depth(gm, proj, bins, poses[0], cam, P.RTGS_RENDER_FULL, rb)
+    torch.cuda.synchronize()
+    blends = int(rb.counts[3].item())
+    rb.count_blends = False
+    # e2e through the public API: pose in (host struct, by value), colour + depth image read back to
+    # pinned host memory every frame
+    col_h = torch.empty((3, cam.height, cam.width), dtype=torch.float32).pin_memory()
+    dep_h = torch.empty((cam.height, cam.width), dtype=torch.float32).pin_memory()
+    n_e2e = max(10, args.steps // 2)
+    flush.zero_()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for i in range(n_e2e):
+        frame(i)
+        col_h.copy_(rb.color, non_blocking=True)
+        dep_h.copy_(rb.depth, non_blocking=True)
+    b.record(stream)
+    torch.cuda.synchronize()
+    t_e2e = a.elapsed_time(b) / n_e2e
+    if rank == 0:
+        line = {"metric": METRIC, "value": world * 1e3 / t_step, "unit": "frames/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": (f"C4 ScanNet++-shaped {cfg.width}x{cfg.height}, {cfg.n} Gaussians (10% "
+                                        f"transparent), SH deg {cfg.sh_degree}; step = render-only novel view: A1 "
+                                        f"project + A2 bin + A3/A4 FULL render (C, T, D, I, N) at one of 8 novel poses"),
+                           "l2": "flushed between timed steps (256 MB write); Gaussian SoA 948 MB > L2",
+                           "launch": "CUDA graph per pose", "parallelism": "single GPU" if world == 1 else
+                           f"{world} replicas"},
+                "roofline": _alu_roofline(blends, t_render, clocks, "k_render_fwd<FULL> (A3/A4, dominant kernel)"),
+                "blends": {"full_per_frame": blends, "full_blends_per_s": blends / (t_render * 1e-3)},
+                "clocks": clocks, "gpu_launches": int(per_frame * args.steps),
+                "e2e": {"value": world * 1e3 / t_e2e, "unit": "frames/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": int(col_h.nbytes + dep_h.nbytes),
+                        "note": "the pose enters by value in the call (host struct, 96 B); the rendered colour + "
+                                "depth image is read back to pinned host memory every frame"},
+                "instances": worst}
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                r = oracle_sample("C4", args.ref_pixels, 1)
+                t_cpu = r["t_proj"] + r["t_fwd"] * cfg.width * cfg.height / r["k_fwd"]
+                line["cpu_baseline"] = {"value": 1.0 / t_cpu, "unit": "frames/s", "cores": r["threads"],
+                                        "kind": "oracle", "extrapolated": True,
+                                        "sample": f"projection of all {cfg.n} Gaussians + forward render of "
+                                                  f"{r['k_fwd']} pixels (float64 torch CPU), extrapolated to the "
+                                                  f"{cfg.width * cfg.height} pixels of a frame"}
+            except Exception as e:
+                line["cpu_baseline"] = {"value": None, "error": repr(e)[:200]}
+        print(json.dumps(line), flush=True)
+
+
+def run_batch(args, rank, world, local):
+    """C5 (BASELINE configs[4]): the keyframe batch of 64 C3 views over `world` ranks
+    (dist.global_step_sharded).  value = views/s of the whole job (64 / step time, max over ranks);
+    T_1 / (N T_N) from the same step on rank 0 alone, measured in this run."""
+    import torch
+    import torch.distributed as dist
+    import paper_2404_19706_b200 as P
+    from paper_2404_19706_b200.dist import global_step_sharded, view_partition
+    from synth import CONFIGS, make_frame, make_pose, make_scene
+    cfg = CONFIGS["C3"]
+    scene = make_scene(cfg)
+    gm = P.GaussianMap.from_arrays(scene)
+    cam = P.camera_of(cfg)
+    eng = P.MappingEngine(gm, cam, capacity=4 * cfg.n)
+    mine = view_partition(N_C5_VIEWS, world, rank)
+    views = [None] * N_C5_VIEWS
+    for v, tr in zip(mine, c5_views(P, cfg, mine)):
+        views[v] = tr
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+
+    def step(_i=0):
+        global_step_sharded(eng, views)
+
+    step()   # allocates the all-Gaussian optimiser state (padded for `world` blocks)
+    torch.cuda.synchronize()
+    keys = ("pos", "log_scale", "rot", "sh")
+    snap = {k: gm.store[k].clone() for k in keys}
+    snap_eta = eng._state_store["eta"].clone()
+
+    def restore():
+        for k in keys:
+            gm.store[k].copy_(snap[k])
+        eng._state_store["eta"].copy_(snap_eta)
+
+    def between():
+        restore()
+        flush.zero_()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    l0 = P.launch_count()
+    step()
+    torch.cuda.synchronize()
+    launches = (P.launch_count() - l0) * args.steps
+    t_step, clocks = _timed(step, between, args.steps, world, local, stream)
+    # e2e: this rank's views arrive from pinned host memory every step, sensor-native (8-bit RGB +
+    # 16-bit depth at 5000 / m), decoded on the device into the views' buffers; loss read back
+    DEPTH_SCALE = 5000.0
+    host = []
+    for v in mine:
+        R, t = make_pose(cfg, view=v)
+        c, d = make_frame(cfg, (R, t))
+        host.append((torch.as_tensor(np.clip(np.rint(np.moveaxis(c, 0, -1) * 255), 0, 255).astype(np.uint8)).pin_memory(),
+                     torch.as_tensor(np.clip(np.rint(d * DEPTH_SCALE), 0, 65535).astype(np.uint16).view(np.int16)).pin_memory()))
+    st_c = torch.empty_like(host[0][0], device="cuda")
+    st_d = torch.empty_like(host[0][1], device="cuda")
+    loss_h = torch.empty(4, dtype=torch.float32).pin_memory()
+    n_e2e = max(3, args.steps // 4)
+    restore()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(n_e2e):
+        for (hc, hd), v in zip(host, mine):
+            st_c.copy_(hc, non_blocking=True)
+            st_d.copy_(hd, non_blocking=True)
+            P.decode_rgbd(st_c, st_d, DEPTH_SCALE, views[v][0], views[v][1])
+        step()
+        loss_h.copy_(eng.g_loss, non_blocking=True)
+    b.record(stream)
+    torch.cuda.synchronize()
+    t_e2e = a.elapsed_time(b) / n_e2e
+    if world > 1:
+        tt = torch.tensor([t_e2e], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_e2e = float(tt.item())
+    # T_1: rank 0 runs the whole 64-view batch alone (the others wait at the barrier)
+    t1 = None
+    per_view = {}
+    blends = None
+    if rank == 0:
+        restore()
+        allv = [views[v] if views[v] is not None else None for v in range(N_C5_VIEWS)]
+        missing = [v for v in range(N_C5_VIEWS) if allv[v] is None]
+        for v, tr in zip(missing, c5_views(P, cfg, missing)):
+            allv[v] = tr
+        global_step_sharded(eng, allv, world=1, rank=0)   # allocates the one-rank layout
+        torch.cuda.synchronize()
+        t1, _ = _timed(lambda i: global_step_sharded(eng, allv, world=1, rank=0), between, max(2, args.steps // 4),
+                       1, local, stream)
+        # per-view phases (view 0) and the dominant kernel's blend count
+        from paper_2404_19706_b200 import mapping as M
+        c0, d0, p0 = allv[0]
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+        restore()
+        flush.zero_()
+        torch.cuda.synchronize()
+        ev[0].record(stream)
+        P.project_and_bin(gm, p0, cam, eng.proj, eng.bins, eng.ws_bin)
+        ev[1].record(stream)
+        P.render_color_depth(gm, eng.proj, eng.bins, p0, cam, P.RTGS_RENDER_FULL, eng.g_rb)
+        ev[2].record(stream)
+        P.topk_error_mask(eng.g_rb, c0, cam, 0.4, eng.g_rb, eng.g_ws_topk)
+        ev[3].record(stream)
+        w = tuple(x / N_C5_VIEWS for x in eng.weights[:2]) + (eng.weights[2],)
+        M.render_backward_masked(gm, eng.proj, eng.bins, p0, cam, eng.g_rb, c0, d0, w, eng.g_slot, eng.g_gid,
+                                 eng.g_grad, eng.g_loss, eng.g_ws_bwd)
+        ev[4].record(stream)
+        torch.cuda.synchronize()
+        for k, name in enumerate(("project_bin", "render_full", "topk", "backward_all_gaussians")):
+            per_view[name] = round(ev[k].elapsed_time(ev[k + 1]), 4)
+        eng.g_grad.zero_()
+        eng.g_rb.count_blends = True
+        P.render_color_depth(gm, eng.proj, eng.bins, p0, cam, P.RTGS_RENDER_FULL, eng.g_rb)
+        torch.cuda.synchronize()
+        blends = int(eng.g_rb.counts[3].item())
+        eng.g_rb.count_blends = False
+        restore()
+    if world > 1:
+        dist.barrier()
+    if rank == 0:
+        views_s = N_C5_VIEWS * 1e3 / t_step
+        line = {"metric": METRIC, "value": views_s, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": t_step, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": batch_config(cfg, world),
+                "global_steps_per_s": 1e3 / t_step,
+                "scaling_measured": {"t1_ms": t1, "tN_ms": t_step, "efficiency": (t1 / (world * t_step)) if t1 else None,
+                                     "note": "T_1 = the same 64-view step on rank 0 alone, this run"},
+                "per_view_ms": per_view,
+                "roofline": _alu_roofline(blends, per_view.get("render_full", float("nan")), clocks,
+                                          "k_render_fwd<FULL> (A3/A4 of a view)") if blends else None,
+                "clocks": clocks, "gpu_launches": int(launches),
+                "e2e": {"value": N_C5_VIEWS * 1e3 / t_e2e, "unit": "iters/s",
+                        "h2d_bytes_per_step": int(sum(h[0].nbytes + h[1].nbytes for h in host)),
+                        "d2h_bytes_per_step": 16,
+                        "input": "per rank: its views' uint8 RGB + uint16 depth, decoded on the device"}}
+        print(json.dumps(line), flush=True)
 
 
 if __name__ == "__main__":

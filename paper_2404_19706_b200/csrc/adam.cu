@@ -46,7 +46,7 @@ __global__ void __launch_bounds__(kAdamThreads) k_adam(const AdamArgs a) {
   if (live) {
     gid = (size_t)a.gid_of_slot[slot];
     if (t == 0) eta0 = a.eta[gid];  // issued with the row gathers, not after the update
-    const bool transparent = a.flags[gid] & 1u;
+    const bool transparent = (a.flags[gid] & 5u) == 1u;  // transparent and not removed (R18, R29)
     const size_t row = (size_t)slot * D;
     const float th0v = (t < 10 && a.init_geom) ? a.init_geom[(size_t)slot * 10 + t] : 0.f;  // independent of gid
     float* shrow = a.sh + (size_t)(3 * K) * gid - 10;

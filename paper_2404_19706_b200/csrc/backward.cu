@@ -609,7 +609,7 @@ __global__ void __launch_bounds__(kPBS, RTGS_BWD_F64 ? 12 : 22) k_project_bwd(co
   }
   if (ns <= 0) return;
   if (tid < ns) sm.gid[tid] = a.gid_of_slot[s0 + tid];
-  if (ADAM && tid < ns) sm.transparent[tid] = a.flags[sm.gid[tid]] & 1u;
+  if (ADAM && tid < ns) sm.transparent[tid] = (a.flags[sm.gid[tid]] & 5u) == 1u;  // not removed (R18, R29)
   __syncthreads();
   // (loads batched 8 deep before their stores so that many are in flight per thread)
   constexpr int U = 8;

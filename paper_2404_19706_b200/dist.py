@@ -1,13 +1,14 @@
 """Multi-GPU plumbing for the keyframe-batch step (P:284 global optimisation).
 
 A single frame never leaves its GPU.  A batch of views is split across ranks (one process per GPU);
-each rank renders its views and accumulates the gradient of the shared slot parameters.  Then
-either ONE all-reduce sums the gradient buffers before the identical Adam step runs on every rank
-(global_step_distributed), or (global_step_sharded) a reduce-scatter hands every rank
-the summed gradient of its block of slots, each rank runs Adam on its block only, and an
-all-gather of the updated rows brings every rank's map copy back in sync: the same result with
-1/N of the optimiser work per rank.  NCCL over NVLink on the GPU box; gloo in the CPU tests (gloo
-has no reduce-scatter, so it is emulated by an all-reduce and a slice there).
+each rank renders its views and accumulates the gradient of every Gaussian (global slot == map
+row).  Then either ONE all-reduce sums the gradient buffers before the identical Adam step runs on
+every rank (global_step_distributed), or (global_step_sharded) an in-place
+reduce-scatter hands every rank the summed gradient of its block of rows, each rank runs Adam on
+its block only, and in-place all-gathers of the map arrays bring every rank's copy back in sync:
+the same result with 1/N of the optimiser work per rank, no packing, no scatter, no allocation.
+NCCL over NVLink on the GPU box; gloo in the CPU tests (gloo has no reduce-scatter, so it is
+emulated by an all-reduce there).
 """
 from __future__ import annotations
 
@@ -52,46 +53,65 @@ def shard_rows(n_rows: int, world: int) -> tuple[int, int]:
     return per, per * world
 
 
-def reduce_scatter_rows(full: torch.Tensor, world: int, rank: int, group=None) -> torch.Tensor:
-    """Sum `full` [world * per, ...] over ranks and return this rank's block of rows [per, ...]."""
+def _nccl(group) -> bool:
+    return dist.get_backend(group) == "nccl"
+
+
+def reduce_scatter_rows_(full: torch.Tensor, world: int, rank: int, group=None) -> torch.Tensor:
+    """IN PLACE: sum `full` [world * per, ...] over ranks into this rank's block of rows of `full`
+    (NCCL in-place reduce-scatter: the output is the input at offset rank * per) and return it."""
     per = full.shape[0] // world
-    if world == 1 or not (dist.is_available() and dist.is_initialized()):
-        return full[rank * per:(rank + 1) * per]
-    if dist.get_backend(group) == "nccl":
-        out = torch.empty((per,) + tuple(full.shape[1:]), dtype=full.dtype, device=full.device)
-        dist.reduce_scatter_tensor(out, full, op=dist.ReduceOp.SUM, group=group)
-        return out
-    dist.all_reduce(full, op=dist.ReduceOp.SUM, group=group)
-    return full[rank * per:(rank + 1) * per]
-
-
-def all_gather_rows(block: torch.Tensor, world: int, group=None) -> torch.Tensor:
-    """Concatenate every rank's block of rows in rank order."""
+    block = full[rank * per:(rank + 1) * per]
     if world == 1 or not (dist.is_available() and dist.is_initialized()):
         return block
-    if dist.get_backend(group) == "nccl":
-        out = torch.empty((world * block.shape[0],) + tuple(block.shape[1:]), dtype=block.dtype, device=block.device)
-        dist.all_gather_into_tensor(out, block.contiguous(), group=group)
-        return out
-    parts = [torch.empty_like(block) for _ in range(world)]
-    dist.all_gather(parts, block.contiguous(), group=group)
-    return torch.cat(parts, 0)
+    if _nccl(group):
+        dist.reduce_scatter_tensor(block, full, op=dist.ReduceOp.SUM, group=group)
+    else:  # gloo has no reduce-scatter: all-reduce, the block is then in place
+        dist.all_reduce(full, op=dist.ReduceOp.SUM, group=group)
+    return block
 
 
-def global_step_sharded(eng, views, group=None, ratio=0.4, lr_scale=0.1):
+def all_gather_rows_(full: torch.Tensor, world: int, rank: int, group=None) -> torch.Tensor:
+    """IN PLACE: every rank's block of rows of `full` [world * per, ...] (its own rows already there)
+    is copied to every other rank (NCCL in-place all-gather)."""
+    per = full.shape[0] // world
+    if world == 1 or not (dist.is_available() and dist.is_initialized()):
+        return full
+    block = full[rank * per:(rank + 1) * per]
+    if _nccl(group):
+        dist.all_gather_into_tensor(full, block, group=group)
+    else:  # gloo (CPU or CUDA tensors): an all-reduce of the blocks, each rank contributing its own
+        tmp = torch.zeros_like(full)
+        tmp[rank * per:(rank + 1) * per] = block
+        dist.all_reduce(tmp, op=dist.ReduceOp.SUM, group=group)
+        full.copy_(tmp)
+    return full
+
+
+def global_step_sharded(eng, views, group=None, ratio=0.4, lr_scale=0.1, world=None, rank=None):
     """(e) the keyframe batch over ranks with a sharded optimiser: this rank's views ->
-    gradient of every slot -> reduce-scatter (each rank: the summed rows of its slot block) -> Adam
-    on the block -> all-gather of the updated rows -> every map copy identical."""
-    rank = dist.get_rank(group) if dist.is_available() and dist.is_initialized() else 0
-    world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+    gradient of every Gaussian (slot == row) -> in-place reduce-scatter (each rank: the summed rows of
+    its block) -> Adam on the block -> in-place all-gathers of the block's rows of the map arrays and
+    of eta -> every map copy identical.  No host synchronisation and no allocation per step: the
+    gradient buffer and the map storage already have `world` equal blocks of rows
+    (MappingEngine._global_state).  `views` has one entry per view of the batch (entries of other
+    ranks' views are not read); world = rank = None take the process group's, world=1 runs the whole
+    batch here without collectives."""
+    on = dist.is_available() and dist.is_initialized()
+    if world is None:
+        world = dist.get_world_size(group) if on else 1
+    if rank is None:
+        rank = dist.get_rank(group) if (on and world > 1) else 0
     mine = [views[v] for v in view_partition(len(views), world, rank)]
-    eng.global_backward(mine, ratio=ratio, n_total=len(views))
-    S, D = int(eng.g_gid.numel()), eng.g_grad.shape[1]
-    per, padded = shard_rows(S, world)
-    full = torch.zeros((padded, D), dtype=eng.g_grad.dtype, device=eng.g_grad.device)
-    full[:S] = eng.g_grad[:S]
-    eng.g_grad.zero_()  # consumed
-    block = reduce_scatter_rows(full, world, rank, group)
-    packed = eng.global_adam_shard(block, rank * per, (rank + 1) * per, lr_scale=lr_scale)
-    eng.global_apply_rows(all_gather_rows(packed, world, group))
+    eng.global_backward(mine, ratio=ratio, n_total=len(views), world=world)
+    per, rows = eng.g_per, eng.g_rows
+    reduce_scatter_rows_(eng.g_grad[:rows], world, rank, group)
+    if world > 1:  # the other blocks held this rank's partial sums: consumed
+        eng.g_grad[: rank * per].zero_()
+        eng.g_grad[(rank + 1) * per: rows].zero_()
+    eng.global_adam_block(rank * per, (rank + 1) * per, lr_scale=lr_scale)
+    gm = eng.gm
+    for k in ("pos", "log_scale", "rot", "sh"):
+        all_gather_rows_(gm.store[k][:rows], world, rank, group)
+    all_gather_rows_(eng._state_store["eta"][:rows], world, rank, group)
     return eng.g_loss

@@ -28,6 +28,7 @@ from ._abi import RTGS_RENDER_COUNT, RTGS_RENDER_DENSE, RTGS_RENDER_COVERAGE, RT
 
 FLAG_TRANSPARENT = 1
 FLAG_STABLE = 2
+FLAG_REMOVED = 4  # NEXT f1: removed Gaussians (absorbing, culled by A1)
 
 
 def _p(t: torch.Tensor | None):
@@ -566,6 +567,12 @@ class MappingEngine:
         # per-Gaussian state (storage of capacity rows; the attributes are views of the live rows)
         self._state_store = {k: torch.zeros(n, dtype=torch.int32, device=device)
                              for k in ("eta", "err_count", "t_created")}
+        # L_reg anchors ("remaining the same as their initial values", R18): each Gaussian's
+        # geometry (pos 3, log-scale 3, rot 4) when it entered the map, per gid; the map handed to the
+        # engine counts as inserted now, f2 rows are recorded at insertion
+        self._anchor = torch.zeros((n, 10), dtype=torch.float32, device=device)
+        self._record_anchor(0, gm.n)
+        self._map_version = 0  # bumped whenever n or the flags change (global-step bookkeeping)
         self._view_state()
         self.state_counts = torch.zeros(4, dtype=torch.int32, device=device)
         self.ws_state = torch.empty(state_workspace_size(n), dtype=torch.uint8, device=device)
@@ -582,6 +589,13 @@ class MappingEngine:
         self.use_cache = True
         self.fused_adam = True
         self.reset_window()
+
+    def _record_anchor(self, r0: int, r1: int, stream=None):
+        if r1 > r0:
+            with torch.cuda.stream(torch.cuda.current_stream() if stream is None else stream):
+                self._anchor[r0:r1, 0:3] = self.gm.pos[r0:r1]
+                self._anchor[r0:r1, 3:6] = self.gm.log_scale[r0:r1]
+                self._anchor[r0:r1, 6:10] = self.gm.rot[r0:r1]
 
     def _view_state(self):
         n = self.gm.n
@@ -601,6 +615,10 @@ class MappingEngine:
             t = torch.zeros(capacity, dtype=v.dtype, device=self.device)
             t[: v.numel()].copy_(v)
             self._state_store[k] = t
+        a = torch.zeros((capacity, 10), dtype=torch.float32, device=self.device)
+        a[: self._anchor.shape[0]].copy_(self._anchor)
+        self._anchor = a
+        self._map_version += 1
         self._view_state()
         n, cam = capacity, self.cam
         self.proj = ProjectedBuffers(n, self.device)
@@ -650,9 +668,11 @@ class MappingEngine:
                       self.cam, insert_params(frame_idx), self.insert_result, self.ws_insert, stream)
         if sync:
             (torch.cuda.current_stream() if stream is None else stream).synchronize()
-            n_new = int(self.insert_result[4].item())
+            n_old, n_new = self.gm.n, int(self.insert_result[4].item())
             self.gm.resize(n_new)
             self._view_state()
+            self._record_anchor(n_old, n_new, stream)  # L_reg anchors of the new Gaussians
+            self._map_version += 1
         # (the f3 cache stays valid: new Gaussians are unstable, the stable lists are unchanged)
         return self.insert_result
 
@@ -698,7 +718,9 @@ class MappingEngine:
         gid_t = torch.nonzero((flags & FLAG_STABLE) == 0).flatten()  # (the host learns the count here)
         n_slots = int(gid_t.numel())
         cap = self.gm.capacity  # slot-indexed buffers hold the whole storage: no window reallocates them
-        self.n_transparent = int(((flags[gid_t] & FLAG_TRANSPARENT) != 0).sum()) if n_slots else 0
+        # N_t of R18: transparent slots that are not removed (removed Gaussians are culled, no L_reg)
+        self.n_transparent = int(((flags[gid_t] & (FLAG_TRANSPARENT | FLAG_REMOVED)) == FLAG_TRANSPARENT).sum()) \
+            if n_slots else 0
         self.gid_of_slot = self._buf("gid_of_slot", n_slots, (), torch.int32, cap_rows=cap)
         self.gid_of_slot.copy_(gid_t)
         self.slot_of_gid = self._buf("slot_of_gid", n, (), torch.int32, cap_rows=cap)
@@ -726,8 +748,12 @@ class MappingEngine:
         else:
             self.before.zero_()
             self.eta_before.zero_()
+        # L_reg anchors of the slots: each Gaussian's geometry at insertion, gathered by gid
         self.init_geom = self._buf("init_geom", rows, (10,), cap_rows=cap)
-        self.init_geom.copy_(self.before[:, :10])
+        if n_slots:
+            torch.index_select(self._anchor[:n], 0, gid_t, out=self.init_geom)
+        else:
+            self.init_geom.zero_()
         self.ws_bwd = self._buf("ws_bwd", backward_workspace_size(n_slots), (), torch.uint8,
                                 cap_rows=backward_workspace_size(cap))
         self.step_count = 0
@@ -879,6 +905,7 @@ class MappingEngine:
         manage_states(self.full, frame_color, frame_depth, self.cam, self.gm.flags, self.err_count, self.eta,
                       self.t_created, sp, self.state_counts, self.ws_state, stream)
         self._drop_cache()  # the stable set changed: every f3 cache is stale
+        self._map_version += 1
         self.reset_window()
 
     def map_window(self, frames, iterations=50, seed=0, first_frame_idx=0, insert=True):
@@ -919,34 +946,43 @@ class MappingEngine:
                                f"capacity >= {worst}")
 
     # --- (e) keyframe global optimisation -------------------------------------------------------
-    def _global_state(self):
-        """Slots = every non-removed Gaussian (rebuilt when the map changed); Adam state per call."""
+    def _global_state(self, world: int = 1):
+        """(e) slots = EVERY row of the map, slot == gid (R37: every non-removed Gaussian is optimised;
+        removed rows are culled by A1, get no gradient and no L_reg term, so their Adam step is an
+        exact no-op).  The gradient buffer has `world` equal blocks of rows (the reduce-scatter
+        shards), the map storage is grown to the padded row count (the in-place all-gathers).  Rebuilt
+        only when the map changed (n or flags, `_map_version`) or the world size did: no host
+        synchronisation per step."""
         n = self.gm.n
-        if getattr(self, "_g_n", None) != n or getattr(self, "_g_flags_sum", None) != int(self.gm.flags.sum()):
-            flags = self.gm.flags.cpu().numpy()
-            gid = np.nonzero((flags & 4) == 0)[0].astype(np.int32)
-            slot = np.full(n, -1, np.int32)
-            slot[gid] = np.arange(len(gid), dtype=np.int32)
-            self.g_gid = torch.zeros(max(len(gid), 1), dtype=torch.int32, device=self.device)[: len(gid)]
-            self.g_gid.copy_(torch.as_tensor(gid))
-            self.g_slot = torch.as_tensor(slot, device=self.device)
-            D = 10 + 3 * (self.gm.sh_degree + 1) ** 2
-            self.g_grad = torch.zeros((max(len(gid), 1), D), dtype=torch.float32, device=self.device)
-            self.g_m = torch.zeros_like(self.g_grad)
-            self.g_v = torch.zeros_like(self.g_grad)
-            self.g_ws_bwd = torch.empty(backward_workspace_size(len(gid)), dtype=torch.uint8, device=self.device)
-            self.g_ntr = int(((flags[gid] & FLAG_TRANSPARENT) != 0).sum())
-            self.g_rb = RenderBuffers(self.cam, self.device, count_blends=False)
-            self.g_ws_topk = torch.empty(topk_workspace_size(self.cam), dtype=torch.uint8, device=self.device)
-            self.g_loss = torch.zeros(4, dtype=torch.float32, device=self.device)
-            self._g_n, self._g_flags_sum = n, int(self.gm.flags.sum())
+        key = (n, self._map_version, world)
+        if getattr(self, "_g_key", None) == key:
+            return
+        per = max(1, -(-n // world))
+        padded = per * world
+        if padded > self.gm.capacity:
+            self.reserve(padded)
+            key = (n, self._map_version, world)
+        D = 10 + 3 * (self.gm.sh_degree + 1) ** 2
+        self.g_per, self.g_rows = per, padded
+        self.g_gid = torch.arange(n, dtype=torch.int32, device=self.device)
+        self.g_slot = self.g_gid
+        self.g_grad = torch.zeros((padded, D), dtype=torch.float32, device=self.device)
+        self.g_m = torch.zeros_like(self.g_grad)
+        self.g_v = torch.zeros_like(self.g_grad)
+        self.g_ws_bwd = torch.empty(backward_workspace_size(padded), dtype=torch.uint8, device=self.device)
+        flags = self.gm.flags
+        self.g_ntr = int(((flags & (FLAG_TRANSPARENT | FLAG_REMOVED)) == FLAG_TRANSPARENT).sum())  # (one sync)
+        self.g_rb = RenderBuffers(self.cam, self.device, count_blends=False)
+        self.g_ws_topk = torch.empty(topk_workspace_size(self.cam), dtype=torch.uint8, device=self.device)
+        self.g_loss = torch.zeros(4, dtype=torch.float32, device=self.device)
+        self._g_key = key
 
-    def global_backward(self, views, ratio=0.4, stream=None, n_total=None):
+    def global_backward(self, views, ratio=0.4, stream=None, n_total=None, world: int = 1):
         """(e) P:284, per keyframe view (colour, depth, pose): FULL render (A1, A2, A3/A4), its top
         `ratio` colour-error pixels (K9), the masked backward over ALL non-removed Gaussians with the
         loss weights divided by the number of views (the batch loss is the mean over the views),
         accumulated into g_grad.  Multi-GPU: every rank calls this on its share of the views."""
-        self._global_state()
+        self._global_state(world)
         nv = n_total if n_total is not None else len(views)   # multi-GPU: the views of ALL ranks
         w = tuple(x / max(1, nv) for x in self.weights[:2]) + (self.weights[2],)
         for (c, d, pose) in views:
@@ -961,61 +997,33 @@ class MappingEngine:
         return _abi.HParams(0.0, hp.lr_sh0 * lr_scale, hp.lr_shrest * lr_scale, hp.lr_scale * lr_scale,
                             hp.lr_rot * lr_scale, hp.beta1, hp.beta2, hp.eps)
 
-    def global_adam_shard(self, grad_rows: torch.Tensor, r0: int, r1: int, lr_scale=0.1, stream=None):
-        """(e) sharded over ranks: the Adam step of the global slots [r0, r1) (clipped to the slot
-        count) with their summed gradient rows `grad_rows` [>= r1 - r0, D] (consumed); writes those
-        Gaussians' parameters and eta on this map and returns them packed as rows [r1 - r0, D + 1]
-        (pos, log_scale, rot, sh, then eta's int32 bits as float32) for the all-gather."""
-        S = int(self.g_gid.numel())
-        D = self.g_grad.shape[1]
-        a, b = min(r0, S), min(r1, S)
-        packed = torch.zeros((r1 - r0, D + 1), dtype=torch.float32, device=self.device)
-        if b > a:
-            gid = self.g_gid[a:b]
-            g = gid.long()
-            m = torch.zeros((b - a, D), dtype=torch.float32, device=self.device)
-            v = torch.zeros_like(m)
-            # (L_reg has a zero gradient in a single step from the anchor: see global_step)
-            adam_step_unstable(self.gm, gid, grad_rows[: b - a], m, v, None, 0, self.weights[2],
-                               self._global_hparams(lr_scale), 1, self.eta, stream)
-            packed[: b - a, :10] = torch.cat([self.gm.pos[g], self.gm.log_scale[g], self.gm.rot[g]], 1)
-            packed[: b - a, 10:D] = self.gm.sh[g].reshape(b - a, D - 10)
-            packed[: b - a, D] = self.eta[g].view(torch.float32)
-        return packed
-
-    def global_apply_rows(self, packed: torch.Tensor):
-        """Write all-gathered packed rows (global slots [0, S); padding rows past S ignored) into the
-        map: parameters and eta of every optimised Gaussian (bit-exact copies of the owners' results)."""
-        S = int(self.g_gid.numel())
-        if S == 0:
+    def global_adam_block(self, r0: int, r1: int, lr_scale=0.1, stream=None):
+        """(e) the Adam step of the global slots (= rows) [r0, r1) clipped to n, from their summed
+        gradient rows g_grad[r0:r1] (consumed) with fresh moments (R37), position lr 0, the other
+        rates x lr_scale, and L_reg against the insertion anchors (R18); writes those rows of the map
+        and of eta in place."""
+        n = self.gm.n
+        a, b = min(r0, n), min(r1, n)
+        if b <= a:
             return
-        D = self.g_grad.shape[1]
-        rows = packed[:S]
-        g = self.g_gid.long()
-        self.gm.pos[g] = rows[:, 0:3]
-        self.gm.log_scale[g] = rows[:, 3:6]
-        self.gm.rot[g] = rows[:, 6:10]
-        self.gm.sh[g] = rows[:, 10:D].reshape(S, -1, 3)
-        self.eta[g] = rows[:, D].contiguous().view(torch.int32)
+        s = torch.cuda.current_stream() if stream is None else stream
+        with torch.cuda.stream(s):
+            self.g_m[a:b].zero_()
+            self.g_v[a:b].zero_()
+        adam_step_unstable(self.gm, self.g_gid[a:b], self.g_grad[a:b], self.g_m[a:b], self.g_v[a:b],
+                           self._anchor[a:b], self.g_ntr, self.weights[2], self._global_hparams(lr_scale), 1,
+                           self.eta, stream)
 
     def global_step(self, views, ratio=0.4, lr_scale=0.1, reduce_grads=None, stream=None, n_total=None):
         """(e) one global optimisation step: global_backward over `views`, the gradient sum
-        over ranks (`reduce_grads(g_grad)`, multi-GPU), then one Adam step of every non-removed
-        Gaussian with the position learning rate 0 and the others x lr_scale (reading R37: fresh
-        moments per global step; L_reg anchors the transparent geometry at its pre-step values)."""
+        over ranks (`reduce_grads(g_grad)`, multi-GPU: every rank then runs the identical update),
+        then one Adam step of every Gaussian with the position learning rate 0 and the others
+        x lr_scale (reading R37: fresh moments per global step; L_reg against the insertion anchors,
+        R18).  The sharded form is dist.global_step_sharded."""
         self.global_backward(views, ratio, stream, n_total)
         if reduce_grads is not None:
             reduce_grads(self.g_grad)
-        ghp = self._global_hparams(lr_scale)
-        s = torch.cuda.current_stream() if stream is None else stream
-        with torch.cuda.stream(s):
-            self.g_m.zero_()
-            self.g_v.zero_()
-        # L_reg (R18) anchors the transparent geometry at its values before this step, and the step
-        # is a single Adam update evaluated there: theta == theta_0, so dL_reg/dtheta is exactly 0 and
-        # no anchor copy is made (n_transparent 0 switches the term off; bit-identical result)
-        adam_step_unstable(self.gm, self.g_gid, self.g_grad, self.g_m, self.g_v, None, 0, self.weights[2], ghp,
-                           1, self.eta, stream)
+        self.global_adam_block(0, self.g_rows, lr_scale, stream)
         return self.g_loss
 
     def step(self, frame_color, frame_depth, pose: _abi.Pose, ingest_pose=None, seed=0, frame_idx=0,

@@ -51,7 +51,7 @@ def test_gloo_allreduce_equals_sum_over_all_views():
 
 
 def _shard_worker(rank, world, port, q):
-    from paper_2404_19706_b200.dist import all_gather_rows, reduce_scatter_rows, shard_rows
+    from paper_2404_19706_b200.dist import all_gather_rows_, reduce_scatter_rows_, shard_rows
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -61,16 +61,18 @@ def _shard_worker(rank, world, port, q):
     per, padded = shard_rows(S, world)
     full = torch.zeros((padded, D))
     full[:S] = torch.as_tensor(mine)
-    block = reduce_scatter_rows(full, world, rank)
-    upd = block * 2.0 + rank                                 # stand-in for the per-block optimiser
-    gathered = all_gather_rows(upd, world)
-    q.put((rank, per, block.numpy().copy(), gathered.numpy().copy()))
+    block = reduce_scatter_rows_(full, world, rank)          # in place: this rank's rows of `full`
+    summed = block.numpy().copy()
+    block.mul_(2.0).add_(rank)                               # stand-in for the per-block optimiser
+    all_gather_rows_(full, world, rank)                      # in place: every rank's block everywhere
+    q.put((rank, per, summed, full.numpy().copy()))
     dist.destroy_process_group()
 
 
 def test_gloo_sharded_rows_round_trip():
-    """reduce-scatter (emulated on gloo) hands each rank the summed rows of its block; the
-    all-gather returns every rank's updated block in rank order (padding rows included)."""
+    """The in-place reduce-scatter (emulated on gloo) leaves each rank the summed rows of its block in
+    place; the in-place all-gather puts every rank's updated block into every rank's buffer in rank
+    order (padding rows included)."""
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()

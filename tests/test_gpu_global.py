@@ -153,26 +153,43 @@ def test_global_step_runs_and_keeps_positions(api):
     assert torch.equal(gm.pos, pos0) and not torch.equal(gm.sh, sh0)
 
 
-def test_global_slots_exclude_removed(api):
+def test_global_step_removed_rows_untouched(api):
+    """Global slots are all rows (slot == gid, R37): removed rows (flags bit 2) are culled by A1, get
+    no gradient and no L_reg term, so one global step leaves them bit-identical; the other rows move."""
     cfg = CONFIGS["C1"]
     scene = make_scene(cfg)
     scene["flags"] = scene["flags"].copy()
     scene["flags"][::41] |= 4
     gm = device_map(scene)
     eng = api.MappingEngine(gm, api.camera_of(cfg))
-    eng._global_state()
-    gid = eng.g_gid.cpu().numpy()
-    np.testing.assert_array_equal(gid, np.nonzero((scene["flags"] & 4) == 0)[0])
-    slot = eng.g_slot.cpu().numpy()
-    assert (slot[::41] == -1).all() and (slot[gid] == np.arange(len(gid))).all()
+    views = []
+    for v in (None, 1):
+        R, t = make_pose(cfg, view=v)
+        c, d = make_frame(cfg, (R, t))
+        views.append((torch.as_tensor(c, device="cuda"), torch.as_tensor(d, device="cuda"), api.make_pose(R, t)))
+    keys = ("pos", "log_scale", "rot", "sh")
+    before = {k: getattr(gm, k).clone() for k in keys}
+    eta0 = eng.eta.clone()
+    # a drifted transparent removed row would move under L_reg if removed rows were not excluded
+    gm.log_scale[::41] += 0.01
+    before["log_scale"] = gm.log_scale.clone()
+    eng.global_step(views)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(eng.g_gid.cpu().numpy(), np.arange(gm.n))
+    rem = torch.zeros(gm.n, dtype=torch.bool, device="cuda")
+    rem[::41] = True
+    for k in keys:
+        assert torch.equal(getattr(gm, k)[rem], before[k][rem]), k
+    assert torch.equal(eng.eta[rem], eta0[rem])
+    assert not torch.equal(gm.sh[~rem], before["sh"][~rem])
 
 
 @pytest.mark.parametrize("world", [2, 3])
 def test_sharded_optimizer_equals_replicated(api, world):
-    """The sharded (e) step (reduce-scatter -> Adam on each rank's slot block -> all-gather) gives
-    every rank the map the replicated step computes, bit for bit: `world` ranks emulated in one
-    process on the same summed gradient (the collectives are covered by test_dist_cpu.py)."""
-    from paper_2404_19706_b200.dist import shard_rows
+    """The sharded (e) step (each rank: Adam on its block of rows, then the blocks copied between the
+    ranks' maps as the in-place all-gathers do) gives every rank the map the replicated step computes,
+    bit for bit: `world` ranks emulated in one process on the same summed gradient (the collectives
+    themselves run in test_dist_cpu.py and test_sharded_step_two_processes)."""
     cfg = CONFIGS["T2"]
     scene = make_scene(cfg)
     views = []
@@ -182,26 +199,95 @@ def test_sharded_optimizer_equals_replicated(api, world):
         views.append((torch.as_tensor(c, device="cuda"), torch.as_tensor(d, device="cuda"), api.make_pose(R, t)))
     engs = [api.MappingEngine(device_map(scene), api.camera_of(cfg)) for _ in range(world + 1)]
     engs[0].global_backward(views)
-    G = engs[0].g_grad.clone()              # the summed gradient (computed once: atomics order aside)
-    S, D = G.shape
-    for e in engs[1:]:
-        e._global_state()
-    # replicated reference: one block covering every slot
+    n = engs[0].gm.n
+    G = engs[0].g_grad[:n].clone()          # the summed gradient (computed once: atomics order aside)
     ref = engs[0]
-    ref.g_grad.zero_()
-    ref.global_apply_rows(ref.global_adam_shard(G.clone(), 0, S))
-    # sharded: rank r optimises rows [r per, (r+1) per), then every rank applies the gathered rows
-    per, padded = shard_rows(S, world)
-    full = torch.zeros((padded, D), device="cuda")
-    full[:S] = G
-    packed = [engs[1 + r].global_adam_shard(full[r * per:(r + 1) * per].clone(), r * per, (r + 1) * per)
-              for r in range(world)]
-    gathered = torch.cat(packed, 0)
+    ref.global_adam_block(0, ref.g_rows)
     for e in engs[1:]:
-        e.global_apply_rows(gathered)
+        e._global_state(world)
+        e.g_grad[:n] = G
+    per = engs[1].g_per
+    for r, e in enumerate(engs[1:]):
+        e.global_adam_block(r * per, (r + 1) * per)
     torch.cuda.synchronize()
-    for e in engs[1:]:
-        for k in ("pos", "log_scale", "rot", "sh", "opacity"):
+    for k in ("pos", "log_scale", "rot", "sh"):
+        for dst in engs[1:]:                 # the all-gather: every rank's block into every map
+            for r, src in enumerate(engs[1:]):
+                a, b = min(r * per, n), min((r + 1) * per, n)
+                getattr(dst.gm, k)[a:b] = getattr(src.gm, k)[a:b]
+        for e in engs[1:]:
             assert torch.equal(getattr(e.gm, k), getattr(ref.gm, k)), k
-        assert torch.equal(e.eta, ref.eta)
-    assert not torch.equal(ref.gm.sh, torch.as_tensor(scene["sh"], device="cuda"))
+    for dst in engs[1:]:
+        for r, src in enumerate(engs[1:]):
+            a, b = min(r * per, n), min((r + 1) * per, n)
+            dst.eta[a:b] = src.eta[a:b]
+        assert torch.equal(dst.eta, ref.eta)
+
+
+def _two_proc_worker(rank, world, port, q):
+    import os
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2404_19706_b200 as P
+    from paper_2404_19706_b200.dist import global_step_sharded
+    cfg = CONFIGS["T2"]
+    scene = make_scene(cfg)
+    gm = P.GaussianMap.from_arrays(scene)
+    eng = P.MappingEngine(gm, P.camera_of(cfg))
+    views = []
+    for v in (None, 1, 2):
+        R, t = make_pose(cfg, view=v)
+        c, d = make_frame(cfg, (R, t))
+        views.append((torch.as_tensor(c, device="cuda"), torch.as_tensor(d, device="cuda"), P.make_pose(R, t)))
+    global_step_sharded(eng, views)
+    torch.cuda.synchronize()
+    q.put((rank, {k: getattr(gm, k).cpu().numpy() for k in ("pos", "log_scale", "rot", "sh")},
+           eng.eta.cpu().numpy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sharded_step_two_processes(api):
+    """dist.global_step_sharded end to end in 2 processes (gloo over the CUDA tensors of one GPU:
+    host-mediated collectives, no kernel waits on another process): both ranks end with identical
+    maps, equal to the single-process global step on all views (gradients to float32 atomic order,
+    so Adam's sign-sensitive first step is compared where |g| is clearly non-zero)."""
+    import os
+    import torch.multiprocessing as mp
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 31500 + (os.getpid() % 1000)
+    ps = [ctx.Process(target=_two_proc_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in range(world)], key=lambda r: r[0])
+    for p in ps:
+        p.join(timeout=120)
+    for k in res[0][1]:
+        np.testing.assert_array_equal(res[0][1][k], res[1][1][k])
+    np.testing.assert_array_equal(res[0][2], res[1][2])
+    cfg = CONFIGS["T2"]
+    scene = make_scene(cfg)
+    gm = device_map(scene)
+    eng = api.MappingEngine(gm, api.camera_of(cfg))
+    views = []
+    for v in (None, 1, 2):
+        R, t = make_pose(cfg, view=v)
+        c, d = make_frame(cfg, (R, t))
+        views.append((torch.as_tensor(c, device="cuda"), torch.as_tensor(d, device="cuda"), api.make_pose(R, t)))
+    eng.global_backward(views)
+    g = eng.g_grad[: gm.n].cpu().numpy()
+    eng.global_adam_block(0, eng.g_rows)
+    torch.cuda.synchronize()
+    sh0 = scene["sh"].reshape(gm.n, -1)
+    dsh = res[0][1]["sh"].reshape(gm.n, -1)
+    ssh = gm.sh.cpu().numpy().reshape(gm.n, -1)
+    sel = np.abs(g[:, 10:]) > 1e-3 * np.abs(g[:, 10:]).max()
+    assert sel.sum() > 100
+    np.testing.assert_allclose(dsh[sel], ssh[sel], rtol=0, atol=1e-7)
+    assert not np.array_equal(dsh, sh0)
+    np.testing.assert_array_equal(res[0][1]["pos"], scene["pos"])      # position lr 0 (P:284)
