@@ -310,9 +310,17 @@ def main():
 
     import torch
     import torch.distributed as dist
+    # harness check only (RTGS_BENCH_ONE_GPU=1): every rank on cuda:0 with gloo, to exercise the N > 1
+    # code path on a one-GPU box; a real multi-GPU run is one process per GPU over NCCL
+    one_gpu = os.environ.get("RTGS_BENCH_ONE_GPU", "") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2404_19706_b200 as P
     from paper_2404_19706_b200 import build as B
     if rank == 0:
@@ -911,9 +919,15 @@ def _timed(run_step, between, steps, world, local, stream):
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
-        t_spin = time.perf_counter()
-        while time.perf_counter() - t_spin < 0.25:  # keep the GPU busy while nvidia-smi starts sampling
-            run_step(0)
+        # keep the GPU busy while nvidia-smi starts sampling; with collectives in the step every rank
+        # must run the same number of steps, so a fixed count there
+        if world > 1:
+            for _ in range(5):
+                run_step(0)
+        else:
+            t_spin = time.perf_counter()
+            while time.perf_counter() - t_spin < 0.25:
+                run_step(0)
         torch.cuda.synchronize()
         for i in range(steps):
             between()
