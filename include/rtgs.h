@@ -430,7 +430,8 @@ typedef struct {
  * the block mean; f/2, (c - 0.5)/2 per level), float64 vertex / normal maps per level (R31), then
  * coarse -> fine Gauss-Newton on E(xi) = sum ((T v - m) . n_m)^2: every valid current pixel is
  * transformed by the running estimate T (pose_io), projected with the level-0 intrinsics into the
- * model maps at model_pose (u^ = floor(x + 0.5)), paired when D^(u^) > 0, |T v - m| <= dist_gate and
+ * model maps at model_pose (u^ = the nearest pixel; within 1e-9 px of x.5 the lower one), paired when
+ * D^(u^) > 0, |T v - m| <= dist_gate and
  * (R n) . n_m >= cos_gate, m = model_pose (D^ K^-1 (u^, 1)), n_m = N^(u^) (R34); delta =
  * -(J^T J + lambda I)^-1 J^T r with lambda = 1e-6 max diag(J^T J), J = (n_m, p x n_m),
  * T <- Exp(delta) T (R35).

@@ -10,14 +10,19 @@ Readings: R33 pyramid: level l+1 keeps, per 2x2 block, the valid
 block's mean of valid depths (float32: sum in row-major order / count; strict '<', first wins; no
 valid pixel -> invalid), intrinsics f_{l+1} = f_l / 2, c_{l+1} = (c_l - 0.5) / 2 (pixel centres, R1),
 size floor(W_l / 2); vertex / normal maps per level as in f2 (R31).  R34 association: the current
-vertex p = T v is projected with the level-0 intrinsics into the full-resolution model maps at the
-model pose, u^ = round-half-up of the projection; pairs need a valid model depth (D^* > 0),
-||p - m|| <= 0.1 m and n_cur . n_model >= cos 30 deg (both world frame); residual r = (p - m) . n_m,
-Jacobian of the left increment T <- Exp(xi) T, xi = (rho, phi): J = (n_m, p x n_m).  R35 solver:
-Gauss-Newton with a relative damping, delta = -(J^T J + lambda I)^-1 J^T r, lambda = 1e-6 max diag(J^T J)
-(a single visible plane makes J^T J singular; the damping leaves its null space unmoved), on each level (iterations 10, 5, 4 coarse -> fine),
-a level stops when |delta| < 1e-6 or fewer than 6 pairs; T <- Exp(delta) T with the closed-form
-SE(3) exponential.
+vertex p = T v (every level) is projected with the level-0 intrinsics into the full-resolution model
+maps at the model pose; u^ = the nearest pixel, where a projection within 1e-9 px of a pixel
+boundary (x.5) goes to the LOWER pixel: a tolerance tie rule, so the integer decision does not
+depend on how the projection was rounded (at the model pose the coarse pixel centres project exactly
+onto x.5; the ties are counted); pairs need a valid model depth (D^* > 0), ||p - m|| <= 0.1 m
+(m = D^* back-projected at u^) and n_cur . n_model >= cos 30 deg (both world frame); residual
+r = (p - m) . n_m, Jacobian of the left increment T <- Exp(xi) T,
+xi = (rho, phi): J = (n_m, p x n_m).  R35 solver: Gauss-Newton with a relative damping,
+delta = -(J^T J + lambda I)^-1 J^T r, lambda = 1e-6 max diag(J^T J): a single visible plane leaves
+three directions unobservable (J^T J singular); J^T r has no component along them, so the damped
+solve moves them by exactly 0 (pinned in tests/test_oracle_icp.py); on each level (iterations 10, 5,
+4 coarse -> fine), a level stops when |delta| < 1e-6 or fewer than 6 pairs; T <- Exp(delta) T with
+the closed-form SE(3) exponential.
 
 Everything float64 except the float32 pyramid / normal-guard decisions named above.
 """
@@ -27,6 +32,7 @@ import numpy as np
 
 COS30 = math.cos(math.radians(30.0))
 DAMPING = 1e-6  # R35: relative Tikhonov damping, keeps unobservable directions (one plane) at 0
+TIE_EPS = 1e-9  # R34: projections this close to a pixel boundary are not associated
 
 
 def level_camera(cam, l):
@@ -37,14 +43,17 @@ def level_camera(cam, l):
     return c
 
 
-def downsample(depth):
-    """One pyramid step of a float32 depth image (R33)."""
+def downsample(depth, with_index=False):
+    """One pyramid step of a float32 depth image (R33).  with_index: also the selected child of every
+    coarse pixel as (dy, dx) of the 2x2 block, or (-1, -1) when the block has no valid depth."""
     d = np.asarray(depth, np.float32)
     H, W = d.shape[0] // 2, d.shape[1] // 2
     out = np.zeros((H, W), np.float32)
+    sel = np.full((H, W, 2), -1, np.int64)
+    offs = [(0, 0), (0, 1), (1, 0), (1, 1)]   # row-major within the block
     for y in range(H):
         for x in range(W):
-            vals = [d[2 * y, 2 * x], d[2 * y, 2 * x + 1], d[2 * y + 1, 2 * x], d[2 * y + 1, 2 * x + 1]]
+            vals = [d[2 * y + oy, 2 * x + ox] for oy, ox in offs]
             ok = [np.isfinite(v) and v > 0 for v in vals]
             if not any(ok):
                 continue
@@ -55,14 +64,15 @@ def downsample(depth):
                     s = np.float32(s + v)
                     n += 1
             avg = np.float32(s / np.float32(n))
-            best, bd = None, None
-            for v, o in zip(vals, ok):
+            best, bd, bk = None, None, None
+            for k, (v, o) in enumerate(zip(vals, ok)):
                 if o:
                     e = np.float32(abs(np.float32(v - avg)))
                     if bd is None or e < bd:
-                        best, bd = v, e
+                        best, bd, bk = v, e, k
             out[y, x] = best
-    return out
+            sel[y, x] = offs[bk]
+    return (out, sel) if with_index else out
 
 
 def pyramid(depth, levels):
@@ -120,7 +130,8 @@ def se3_exp(xi):
 
 
 def model_maps(depth_hat, normal_hat, cam, Rm, tm):
-    """Global model vertices from the rendered depth (D^ = -1: no hit) and the world normal map."""
+    """Global model vertices from the rendered depth (D^ <= 0: no hit) back-projected at the pixel
+    centres, and the world normal map."""
     d = np.asarray(depth_hat, np.float64)
     H, W = d.shape
     ys, xs = np.mgrid[0:H, 0:W].astype(np.float64)
@@ -130,34 +141,37 @@ def model_maps(depth_hat, normal_hat, cam, Rm, tm):
     return Vg, Ng, d > 0
 
 
+def nearest_pixel(x):
+    """R34: the nearest pixel index of coordinate x; within TIE_EPS of a boundary (x.5) the lower one.
+    Returns (index, tie)."""
+    fr = x - np.floor(x)
+    tie = np.abs(fr - 0.5) < TIE_EPS
+    return np.where(tie, np.floor(x), np.rint(x)), tie
+
+
 def linearize(V, N, valid, R, t, model, cam0, Rm, tm, dist_gate=0.1, cos_gate=COS30):
-    """Sum over the current level's valid pixels of the associated pairs (R34): returns
-    (A 6x6, b 6, E = sum r^2, count)."""
+    """Sum over the current level's valid pixels of the associated pairs (R34) in the full-resolution
+    model maps (`cam0` = level-0 intrinsics): returns (A 6x6, b 6, E = sum r^2, count, ties)."""
     Vg, Ng, mvalid = model
-    H0, W0 = mvalid.shape
+    Hl, Wl = mvalid.shape
+    cam = cam0
     idx = np.nonzero(valid.ravel())[0]
     v = V.reshape(-1, 3)[idx]
     n = N.reshape(-1, 3)[idx]
-    # The association decides integers (u^ = floor(x + 0.5); coarse-level pixel centres project
-    # exactly onto x.5 at the model pose), so p, q and x are formed with this exact sequence of
-    # correctly rounded float64 operations (elementwise, no BLAS / FMA), as the kernel does.
-    R = np.asarray(R, np.float64)
-    Rm = np.asarray(Rm, np.float64)
-    p = np.stack([((R[r, 0] * v[:, 0] + R[r, 1] * v[:, 1]) + R[r, 2] * v[:, 2]) + t[r] for r in range(3)], 1)
+    R, Rm = np.asarray(R, np.float64), np.asarray(Rm, np.float64)
+    p = v @ R.T + np.asarray(t, np.float64)          # current vertex in the world (T v)
     nw = n @ R.T
-    dd = p - np.asarray(tm, np.float64)
-    q = np.stack([(Rm[0, c] * dd[:, 0] + Rm[1, c] * dd[:, 1]) + Rm[2, c] * dd[:, 2] for c in range(3)], 1)
-    A = np.zeros((6, 6))
-    b = np.zeros(6)
-    E = 0.0
-    cnt = 0
+    q = (p - np.asarray(tm, np.float64)) @ Rm         # model camera frame: Rm^T (p - tm)
     with np.errstate(invalid="ignore", divide="ignore"):
-        ux = (cam0["fx"] * q[:, 0]) / q[:, 2] + cam0["cx"]
-        uy = (cam0["fy"] * q[:, 1]) / q[:, 2] + cam0["cy"]
+        ux = cam["fx"] * q[:, 0] / q[:, 2] + cam["cx"]
+        uy = cam["fy"] * q[:, 1] / q[:, 2] + cam["cy"]
     front = q[:, 2] > 0
-    ix = np.floor(np.where(front, ux, -1.0) + 0.5)
-    iy = np.floor(np.where(front, uy, -1.0) + 0.5)
-    inside = front & (ix >= 0) & (ix < W0) & (iy >= 0) & (iy < H0)
+    ux = np.where(front, ux, -1.0)
+    uy = np.where(front, uy, -1.0)
+    ix, tx = nearest_pixel(ux)
+    iy, ty = nearest_pixel(uy)
+    tie = front & (tx | ty)
+    inside = front & (ix >= 0) & (ix < Wl) & (iy >= 0) & (iy < Hl)
     ix = np.where(inside, ix, 0).astype(np.int64)
     iy = np.where(inside, iy, 0).astype(np.int64)
     m = Vg[iy, ix]
@@ -166,36 +180,41 @@ def linearize(V, N, valid, R, t, model, cam0, Rm, tm, dist_gate=0.1, cos_gate=CO
     diff = p - m
     ok &= np.linalg.norm(diff, axis=1) <= dist_gate
     ok &= np.sum(nw * nm, axis=1) >= cos_gate
-    for k in np.nonzero(ok)[0]:
-        J = np.concatenate([nm[k], np.cross(p[k], nm[k])])
-        r = float(np.dot(diff[k], nm[k]))
-        A += np.outer(J, J)
-        b += J * r
-        E += r * r
-        cnt += 1
-    return A, b, E, cnt
+    J = np.concatenate([nm[ok], np.cross(p[ok], nm[ok])], 1)
+    r = np.sum(diff[ok] * nm[ok], axis=1)
+    A = J.T @ J
+    b = J.T @ r
+    return A, b, float(r @ r), int(ok.sum()), int(tie.sum())
 
 
-def icp(depth_cur, cam, model, Rm, tm, R0, t0, levels=3, iters=(4, 5, 10), guard=0.1, eps=1e-6, min_pairs=6):
-    """Multi-level ICP (coarse -> fine).  iters[l] = Gauss-Newton iterations at level l (level 0 =
-    full resolution).  Returns (R, t, diagnostics list of (level, E, count, |delta|))."""
+def gn_step(A, b, damping=DAMPING):
+    """R35: delta = -(A + lambda I)^-1 b, lambda = damping * max diag(A)."""
+    lam = damping * float(np.max(np.diag(A)))
+    return -np.linalg.solve(A + lam * np.eye(6), b)
+
+
+def icp(depth_cur, cam, depth_hat, normal_hat, Rm, tm, R0, t0, levels=3, iters=(4, 5, 10), guard=0.1, eps=1e-6,
+        min_pairs=6):
+    """Multi-level ICP (coarse -> fine) of the current depth against the model render (D^*, world
+    N^* [3, H, W]) at the model pose.  iters[l] = Gauss-Newton iterations at level l (level 0 = full
+    resolution).  Returns (R, t, diagnostics list of (level, E, count, |delta|, ties))."""
     R, t = np.asarray(R0, np.float64).copy(), np.asarray(t0, np.float64).copy()
     pyr = pyramid(depth_cur, levels)
+    model = model_maps(depth_hat, normal_hat, cam, Rm, tm)
     diag = []
     for l in range(levels - 1, -1, -1):
         cl = level_camera(cam, l)
         V, N, valid = vertex_normal_map(pyr[l], cl, guard)
         for _ in range(iters[l]):
-            A, b, E, cnt = linearize(V, N, valid, R, t, model, cam, Rm, tm)
+            A, b, E, cnt, ties = linearize(V, N, valid, R, t, model, cam, Rm, tm)
             if cnt < min_pairs:
-                diag.append((l, E, cnt, 0.0))
+                diag.append((l, E, cnt, 0.0, ties))
                 break
-            lam = DAMPING * float(np.max(np.diag(A)))
-            delta = -np.linalg.solve(A + lam * np.eye(6), b)
+            delta = gn_step(A, b)
             dR, dt = se3_exp(delta)
             R, t = dR @ R, dR @ t + dt
             nd = float(np.linalg.norm(delta))
-            diag.append((l, E, cnt, nd))
+            diag.append((l, E, cnt, nd, ties))
             if nd < eps:
                 break
     return R, t, diag

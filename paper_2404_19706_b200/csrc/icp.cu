@@ -7,7 +7,8 @@
 //  k_vn_map       one thread per pixel of a level: float64 vertex and central-difference normal
 //                 (R31), stored as double4 (w = validity)
 //  k_icp_lin      one thread per current pixel: transform by the pose estimate (device memory),
-//                 projective association into the model maps, gates, J = (n_m, p x n_m), r; the 29
+//                 projective association into the model maps (nearest pixel, the R34 tolerance
+//                 tie rule at x.5), gates, J = (n_m, p x n_m), r; the 29
 //                 sums (upper-triangular J^T J, J^T r, r^2, count) reduced over the warp with
 //                 shuffles, over the CTA in shared memory, then one float64 atomic per value
 //  k_icp_solve    one thread: 6x6 Cholesky of A + 1e-6 max(diag A) I, delta = -(..)^-1 b, T <- Exp(delta) T, convergence flag,
@@ -128,6 +129,11 @@ struct LinArgs {
   IcpState* st;
 };
 
+__device__ __forceinline__ double nearest_px(double x) {
+  const double f = floor(x);
+  return fabs((x - f) - 0.5) < 1e-9 ? f : rint(x);
+}
+
 __device__ __forceinline__ double warp_sum_d(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -146,25 +152,22 @@ __global__ void __launch_bounds__(256) k_icp_lin(const LinArgs a) {
     if (v.w != 0.0) {
       const double4 nc = a.N[i];
       const double* T = a.pose;
-      // the association decides integers: p, q and the projection use this exact sequence of
-      // correctly rounded operations (no FMA contraction), as the oracle does
-      auto rowdot = [](double r0, double r1, double r2, double x, double y, double z) {
-        return __dadd_rn(__dadd_rn(__dmul_rn(r0, x), __dmul_rn(r1, y)), __dmul_rn(r2, z));
-      };
-      const double px = __dadd_rn(rowdot(T[0], T[1], T[2], v.x, v.y, v.z), T[9]);
-      const double py = __dadd_rn(rowdot(T[3], T[4], T[5], v.x, v.y, v.z), T[10]);
-      const double pz = __dadd_rn(rowdot(T[6], T[7], T[8], v.x, v.y, v.z), T[11]);
+      const double px = T[0] * v.x + T[1] * v.y + T[2] * v.z + T[9];
+      const double py = T[3] * v.x + T[4] * v.y + T[5] * v.z + T[10];
+      const double pz = T[6] * v.x + T[7] * v.y + T[8] * v.z + T[11];
       const double nwx = T[0] * nc.x + T[1] * nc.y + T[2] * nc.z;
       const double nwy = T[3] * nc.x + T[4] * nc.y + T[5] * nc.z;
       const double nwz = T[6] * nc.x + T[7] * nc.y + T[8] * nc.z;
       // model camera frame: q = Rm^T (p - tm)
-      const double dx = __dsub_rn(px, a.tm[0]), dy = __dsub_rn(py, a.tm[1]), dz = __dsub_rn(pz, a.tm[2]);
-      const double qx = rowdot(a.Rm[0], a.Rm[3], a.Rm[6], dx, dy, dz);
-      const double qy = rowdot(a.Rm[1], a.Rm[4], a.Rm[7], dx, dy, dz);
-      const double qz = rowdot(a.Rm[2], a.Rm[5], a.Rm[8], dx, dy, dz);
+      const double dx = px - a.tm[0], dy = py - a.tm[1], dz = pz - a.tm[2];
+      const double qx = a.Rm[0] * dx + a.Rm[3] * dy + a.Rm[6] * dz;
+      const double qy = a.Rm[1] * dx + a.Rm[4] * dy + a.Rm[7] * dz;
+      const double qz = a.Rm[2] * dx + a.Rm[5] * dy + a.Rm[8] * dz;
       if (qz > 0.0) {
-        const double ux = floor(__dadd_rn(__dadd_rn(__ddiv_rn(__dmul_rn(a.fx, qx), qz), a.cx), 0.5));
-        const double uy = floor(__dadd_rn(__dadd_rn(__ddiv_rn(__dmul_rn(a.fy, qy), qz), a.cy), 0.5));
+        // R34: nearest pixel, a projection within 1e-9 px of a boundary (x.5) to the lower one, so
+        // the integer does not depend on the projection's rounding (coarse pixel centres project
+        // exactly onto x.5 at the model pose)
+        const double ux = nearest_px(a.fx * qx / qz + a.cx), uy = nearest_px(a.fy * qy / qz + a.cy);
         if (ux >= 0.0 && ux < (double)a.W0 && uy >= 0.0 && uy < (double)a.H0) {
           const int mi = (int)uy * a.W0 + (int)ux;
           const float md = a.mdepth[mi];

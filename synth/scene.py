@@ -313,8 +313,10 @@ def make_scene(cfg: SceneConfig, n: int | None = None) -> dict:
     )
 
 
-def make_frame(cfg: SceneConfig, pose=None, seed_offset: int = 0):
-    """Target RGBD frame (color [3,H,W] in [0,1], depth [H,W] metres, 0 = invalid) at `pose`."""
+def make_frame(cfg: SceneConfig, pose=None, seed_offset: int = 0, normals: bool = False):
+    """Target RGBD frame (color [3,H,W] in [0,1], depth [H,W] metres, 0 = invalid) at `pose`; with
+    normals=True also the analytic world normal of the surface hit at every pixel [3,H,W] (camera
+    facing, zero where nothing is hit): scene data, e.g. stand-in model maps for tracking tests."""
     R, t = make_pose(cfg) if pose is None else pose
     Rw, tw = _world_transform(cfg)
     room = _room(cfg, np.random.default_rng(cfg.seed + 1))
@@ -325,7 +327,7 @@ def make_frame(cfg: SceneConfig, pose=None, seed_offset: int = 0):
     dc = np.stack([(px.ravel() - cfg.cx) / cfg.fx, (py.ravel() - cfg.cy) / cfg.fy,
                    np.ones(px.size)], axis=1)
     dr = dc @ Rc.T
-    tt, _, sid = _raycast(room, oc, dr)
+    tt, nrm, sid = _raycast(room, oc, dr)
     hit = np.isfinite(tt)
     depth = np.where(hit, tt, 0.0)  # camera-frame z since dc_z = 1
     P = oc[None, :] + dr * np.where(hit, tt, 0.0)[:, None]
@@ -340,4 +342,7 @@ def make_frame(cfg: SceneConfig, pose=None, seed_offset: int = 0):
         depth[rng.uniform(size=depth.shape) < cfg.hole_frac] = 0.0
     color = np.ascontiguousarray(color.T.reshape(3, cfg.height, cfg.width), dtype=np.float32)
     depth = np.ascontiguousarray(depth.reshape(cfg.height, cfg.width), dtype=np.float32)
+    if normals:
+        nw = np.where(hit[:, None], nrm @ Rw.T, 0.0)   # room frame -> world
+        return color, depth, np.ascontiguousarray(nw.T.reshape(3, cfg.height, cfg.width), dtype=np.float32)
     return color, depth

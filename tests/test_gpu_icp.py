@@ -1,9 +1,10 @@
 """GPU parity of the NEXT row f4 (frame-to-model point-to-plane ICP, Eq.10) vs oracle/icp.py.
 
-Same inputs on both sides (current depth, model depth / world normals, model pose, initial pose):
-per Gauss-Newton iteration the pair count is equal, the energy and the step norm agree to 1e-6 /
-1e-5 relative (float64 on both sides, different contraction and summation order), and the final
-pose agrees to 1e-8.  End to end, the tracker recovers a perturbed
+Same seeded inputs on both sides (current depth, model depth / world normals from synth, model pose,
+initial pose): per Gauss-Newton iteration the pair count is equal (the association's integer
+decisions are rounding-independent by the R34 tie rule: no shared op order), the energy and the step
+norm agree to 1e-6 / 1e-5 relative (float64 on both sides, different contraction and summation
+order), and the final pose agrees to 1e-8.  End to end, the tracker recovers a perturbed
 pose against a FULL render of the Gaussian map (the paper's use: model maps rendered from S*)."""
 import math
 
@@ -31,12 +32,12 @@ def _perturb(R, t, dt, ang_deg, axis):
     return dR @ R, t + np.asarray(dt, np.float64)
 
 
-def _analytic_model(cfg, cam, R, t):
-    _, d = make_frame(cfg, (R, t))
-    V, N, valid = OI.vertex_normal_map(d, cam)
-    Nw = np.moveaxis(np.where(valid[..., None], N @ np.asarray(R).T, 0.0), -1, 0)
+def _analytic_model(cfg, R, t):
+    """Stand-in model render (seeded scene data, synth): the analytic depth (no hit -> -1) and world
+    normals of the room at (R, t)."""
+    _, d, nw = make_frame(cfg, (R, t), normals=True)
     dh = np.where(d > 0, d, -1.0).astype(np.float32)
-    return dh, np.ascontiguousarray(Nw, dtype=np.float32)
+    return dh, nw
 
 
 @pytest.mark.parametrize("name,dt,ang", [("T1", [0.005, 0.0, 0.0], 0.0), ("T1", [0.012, -0.01, 0.011], 2.0),
@@ -45,12 +46,11 @@ def test_icp_parity(api, name, dt, ang):
     cfg = CONFIGS[name]
     cam = dict(fx=cfg.fx, fy=cfg.fy, cx=cfg.cx, cy=cfg.cy, width=cfg.width, height=cfg.height)
     R, t = make_pose(cfg)
-    dh, nw = _analytic_model(cfg, cam, R, t)
+    dh, nw = _analytic_model(cfg, R, t)
     R1, t1 = _perturb(R, t, dt, ang, [0.3, 1.0, -0.2])
     _, d1 = make_frame(cfg, (R1, t1))
-    # oracle (the float32 model arrays, as the GPU sees them)
-    model = OI.model_maps(dh.astype(np.float64), nw.astype(np.float64), cam, R, t)
-    Ro, to, diag_o = OI.icp(d1, cam, model, R, t, R, t)
+    # oracle on the same (float32) model arrays
+    Ro, to, diag_o = OI.icp(d1, cam, dh, nw, R, t, R, t)
     # GPU
     from paper_2404_19706_b200 import mapping as M
     c = api.camera_of(cfg)

@@ -75,12 +75,11 @@ def _room(cfg_name="T1", view=None):
 
 
 def _model(cfg, cam, R, t):
-    """Model maps from the analytic frame at (R, t): depth (0 -> -1) and world normals."""
-    _, d = make_frame(cfg, (R, t))
-    V, N, valid = OI.vertex_normal_map(d, cam)
-    Nw = np.moveaxis(np.where(valid[..., None], N @ np.asarray(R).T, 0.0), -1, 0)
+    """Model render from the analytic frame at (R, t): depth (0 -> -1) and the analytic world normals
+    of the surfaces (synth), as a FULL render would give them."""
+    _, d, nw = make_frame(cfg, (R, t), normals=True)
     dh = np.where(d > 0, d, -1.0)
-    return OI.model_maps(dh, Nw, cam, R, t), d
+    return (dh, nw), d
 
 
 def _perturb(R, t, dt, ang_deg, axis):
@@ -91,11 +90,13 @@ def _perturb(R, t, dt, ang_deg, axis):
 
 def test_jacobian_matches_finite_differences():
     cfg, cam, R, t = _room()
-    model, d = _model(cfg, cam, R, t)
+    (dh, nw), d = _model(cfg, cam, R, t)
+    model = OI.model_maps(dh, nw, cam, R, t)
     R1, t1 = _perturb(R, t, [0.004, -0.003, 0.002], 0.5, [1, 2, 3])
     _, d1 = make_frame(cfg, (R1, t1))
     V, N, valid = OI.vertex_normal_map(d1, cam)
-    A, b, E, cnt = OI.linearize(V, N, valid, R, t, model, cam, R, t)
+    A, b, E, cnt, ties = OI.linearize(V, N, valid, R, t, model, cam, R, t)
+    assert ties == 0
     assert cnt > 1000
     # with the association frozen, E(xi) = sum r_i(xi)^2 and grad = 2 b, Hessian ~ 2 A: check grad by FD
     Vg, Ng, mv = model
@@ -106,8 +107,8 @@ def test_jacobian_matches_finite_differences():
         Rx, tx = dR @ R, dR @ t + dt
         p = V.reshape(-1, 3)[idx] @ Rx.T + tx
         q = (p - t) @ R
-        ix = np.floor(cam["fx"] * q[:, 0] / q[:, 2] + cam["cx"] + 0.5).astype(int)
-        iy = np.floor(cam["fy"] * q[:, 1] / q[:, 2] + cam["cy"] + 0.5).astype(int)
+        ix = np.rint(cam["fx"] * q[:, 0] / q[:, 2] + cam["cx"]).astype(int)
+        iy = np.rint(cam["fy"] * q[:, 1] / q[:, 2] + cam["cy"]).astype(int)
         if keep is None:
             return ix, iy
         kk, jx, jy = keep
@@ -132,25 +133,66 @@ def test_jacobian_matches_finite_differences():
 
 def test_identity_frame_gives_zero_step():
     cfg, cam, R, t = _room()
-    model, d = _model(cfg, cam, R, t)
+    (dh, nw), d = _model(cfg, cam, R, t)
+    model = OI.model_maps(dh, nw, cam, R, t)
     # full resolution: the current vertices ARE the model vertices -> zero residuals, zero step
     V, N, valid = OI.vertex_normal_map(d, cam)
-    A, b, E, cnt = OI.linearize(V, N, valid, R, t, model, cam, R, t)
-    assert cnt > 10000 and E < 1e-24 and np.abs(b).max() < 1e-12
+    A, b, E, cnt, ties = OI.linearize(V, N, valid, R, t, model, cam, R, t)
+    assert cnt > 10000 and E < 1e-24 and np.abs(b).max() < 1e-12 and ties == 0
+    # level 1 at the model pose: every coarse pixel centre projects onto a boundary x.5 (R34 tie rule)
+    c1 = OI.level_camera(cam, 1)
+    V1, N1, valid1 = OI.vertex_normal_map(OI.pyramid(d, 2)[1], c1)
+    _, _, _, cnt1, ties1 = OI.linearize(V1, N1, valid1, R, t, model, cam, R, t)
+    assert ties1 == valid1.sum() and cnt1 > 1000
     # the coarse levels back-project a block's depth at the coarse pixel centre (slightly off the
     # surface), so they move the pose a little; the fine level brings it back
-    Rr, tr, diag = OI.icp(d, cam, model, R, t, R, t)
+    Rr, tr, diag = OI.icp(d, cam, dh, nw, R, t, R, t)
     assert np.linalg.norm(tr - t) < 1e-6 and abs((np.trace(Rr.T @ R) - 1) / 2 - 1) < 1e-12
+
+
+def test_nearest_pixel_tie_rule():
+    # R34: nearest pixel; within 1e-9 px of x.5 always the lower pixel, however x was rounded
+    x = np.array([3.2, 3.7, 4.5, 4.5 + 1e-12, 4.5 - 1e-12, 4.5 + 2e-9, -0.5, 0.49999999])
+    ix, tie = OI.nearest_pixel(x)
+    np.testing.assert_array_equal(ix, [3, 4, 4, 4, 4, 5, -1, 0])
+    np.testing.assert_array_equal(tie, [False, False, True, True, True, False, True, False])
+
+
+def test_damping_leaves_the_unobservable_directions_of_one_plane_at_zero():
+    """R35 on one fronto-parallel plane (z = 2 m, n = (0, 0, -1)) seen 1 cm farther: J = (n, p x n) =
+    (0, 0, -1, -p_y, p_x, 0), so t_x, t_y and the roll about z are unobservable (J^T J singular:
+    np.linalg.solve fails undamped).  With the pixel grid symmetric about the principal point,
+    sum p_x = sum p_y = 0, and the damped Gauss-Newton step is, by hand,
+        delta = (0, 0, -0.01 N / (N + lambda), 0, 0, 0),  lambda = 1e-6 max(N, sum p_y^2, sum p_x^2)
+    (r = (p - m) . n = -0.01 for every one of the N pairs: b_z = 0.01 N)."""
+    cam = dict(fx=50.0, fy=50.0, cx=15.5, cy=11.5, width=32, height=24)
+    model = OI.model_maps(np.full((24, 32), 2.0, np.float32), np.broadcast_to(np.array([0, 0, -1.0])[:, None, None],
+                                                                                (3, 24, 32)), cam, np.eye(3), np.zeros(3))
+    V, N, valid = OI.vertex_normal_map(np.full((24, 32), 2.01, np.float32), cam)
+    A, b, E, cnt, ties = OI.linearize(V, N, valid, np.eye(3), np.zeros(3), model, cam, np.eye(3), np.zeros(3))
+    assert cnt == valid.sum() == 30 * 22 and ties == 0
+    assert np.linalg.matrix_rank(A) == 3
+    p = V[valid].astype(np.float64)
+    lam = 1e-6 * max(cnt, float((p[:, 1] ** 2).sum()), float((p[:, 0] ** 2).sum()))
+    dz = float(np.float32(2.01)) - 2.0
+    delta = OI.gn_step(A, b)
+    np.testing.assert_allclose(delta[2], -dz * cnt / (cnt + lam), rtol=1e-9)
+    assert np.abs(delta[[0, 1, 5]]).max() < 1e-15 and np.abs(delta[[3, 4]]).max() < 1e-12
+    try:
+        undamped = np.linalg.solve(A, -b)
+        assert not np.isfinite(undamped).all() or np.abs(undamped).max() > 1e3
+    except np.linalg.LinAlgError:
+        pass
 
 
 def test_pose_recovery_on_the_synthetic_room():
     # S:457-459: 5 mm -> within 0.5 mm / 0.05 deg; 2 cm + 2 deg -> within 1 mm / 0.1 deg
     cfg, cam, R, t = _room()
-    model, _ = _model(cfg, cam, R, t)
+    (dh, nw), _ = _model(cfg, cam, R, t)
     for dt, ang, tol_t, tol_r in [([0.005, 0, 0], 0.0, 5e-4, 0.05), ([0.012, -0.01, 0.011], 2.0, 1e-3, 0.1)]:
         R1, t1 = _perturb(R, t, dt, ang, [0.3, 1.0, -0.2])
         _, d1 = make_frame(cfg, (R1, t1))
-        Rr, tr, diag = OI.icp(d1, cam, model, R, t, R, t)
+        Rr, tr, diag = OI.icp(d1, cam, dh, nw, R, t, R, t)
         err_t = np.linalg.norm(tr - t1)
         cosang = (np.trace(Rr.T @ R1) - 1) / 2
         err_r = math.degrees(math.acos(min(1.0, cosang)))
