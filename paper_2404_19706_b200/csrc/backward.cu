@@ -650,44 +650,79 @@ __global__ void __launch_bounds__(kPBS, RTGS_BWD_F64 ? 12 : 22) k_project_bwd(co
   __syncthreads();
   if (tid < ns) project_bwd_slot<K>(a, sm.sg + tid * kSG, sm.par + tid * 13, a.sh + (size_t)sm.gid[tid] * SHF, gout);
   __syncthreads();
+  // The epilogue walks the CTA's slot rows one after another, the warp's lanes over the row's D
+  // components (lane, lane + 32): m / v / grad / SH rows stream coalesced, and every per-component
+  // constant (learning-rate group, the SH (coefficient, channel) of the compact staging row) is a
+  // per-lane register instead of a division per element.  kPBS == 32: the CTA is one warp.
+  static_assert(kPBS == 32, "the epilogue maps the CTA's one warp onto the row components");
+  constexpr int NH = (D + 31) / 32;
+  const int lane = tid;
+  int jh[NH], gidx0[NH], gidx1[NH];  // component, and its compact-row operands (gidx1 < 0: geometry)
+#pragma unroll
+  for (int h = 0; h < NH; ++h) {
+    const int j = lane + 32 * h;
+    jh[h] = j;
+    if (j < 10) { gidx0[h] = j; gidx1[h] = -1; }
+    else {
+      const int kk = (j - 10) / 3, c = (j - 10) - 3 * kk;
+      gidx0[h] = 10 + kk; gidx1[h] = 10 + K + c;
+    }
+  }
+  auto grad_of = [&](int ls, int h) -> float {
+    const float* row = sm.out + ls * LD;
+    return gidx1[h] < 0 ? row[gidx0[h]] : row[gidx0[h]] * row[gidx1[h]];
+  };
   if constexpr (ADAM) {
     // A6 on the staged rows (the same update as k_adam, adam.cuh; SH updated in place in global
-    // memory, each element read and written by one thread): the slot gradient never leaves
-    // shared memory; m / v stream coalesced over the CTA's contiguous [ns x D] block, the new
-    // parameters go back into the staging and are written out below.
+    // memory): the slot gradient never leaves shared memory; the new geometry goes back into the
+    // staging and is written out below.
     const AdamBC bc = adam_bias(a.h);
-    float* M = a.m + (size_t)s0 * D;
-    float* Vm = a.v + (size_t)s0 * D;
-    for (int e0 = tid; e0 < ns * D; e0 += kPBS * U) {
-      float mo[U], vo[U];
+    float lrh[NH];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int e = e0 + u * kPBS;
-        mo[u] = e < ns * D ? M[e] : 0.f;
-        vo[u] = e < ns * D ? Vm[e] : 0.f;
+    for (int h = 0; h < NH; ++h) lrh[h] = adam_lr(a.h, min(jh[h], D - 1));
+    constexpr int SU = 4;  // slot rows in flight
+    for (int l0 = 0; l0 < ns; l0 += SU) {
+      float mo[SU][NH], vo[SU][NH], th[SU][NH];
+#pragma unroll
+      for (int u = 0; u < SU; ++u) {
+        const int ls = min(l0 + u, ns - 1);
+        const size_t gsh = (size_t)sm.gid[ls] * SHF;
+#pragma unroll
+        for (int h = 0; h < NH; ++h) {
+          const int j = jh[h];
+          const bool live = l0 + u < ns && j < D;
+          const size_t e = (size_t)(s0 + ls) * D + j;
+          mo[u][h] = live ? a.m[e] : 0.f;
+          vo[u][h] = live ? a.v[e] : 0.f;
+          th[u][h] = !live ? 0.f : (j < 10 ? sm.par[ls * 13 + j] : a.sh[gsh + (j - 10)]);
+        }
       }
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int e = e0 + u * kPBS;
-        if (e < ns * D) {
-          const int ls = e / D, j = e - ls * D;
-          float gg = sh_grad<K>(sm.out + ls * LD, j);
-          const size_t shi = (size_t)sm.gid[ls] * SHF + (j - 10);
-          const float th = j < 10 ? sm.par[ls * 13 + j] : a.sh[shi];
-          if (j < 10 && sm.transparent[ls]) {  // L_reg (R18)
+      for (int u = 0; u < SU; ++u) {
+        const int ls = l0 + u;
+        if (ls >= ns) break;
+        const size_t gsh = (size_t)sm.gid[ls] * SHF;
+        const bool tr = sm.transparent[ls];
+#pragma unroll
+        for (int h = 0; h < NH; ++h) {
+          const int j = jh[h];
+          if (j >= D) continue;
+          float gg = grad_of(ls, h);
+          if (j < 10 && tr) {  // L_reg (R18)
             const float th0 = a.init_geom ? a.init_geom[(size_t)(s0 + ls) * 10 + j] : 0.f;
-            gg += a.h.reg_coef * (th - th0);
+            gg += a.h.reg_coef * (th[u][h] - th0);
           }
-          float mm = mo[u], vv = vo[u];
-          const float nt = adam_one(a.h, bc, adam_lr(a.h, j), th, gg, mm, vv);
+          float mm = mo[u][h], vv = vo[u][h];
+          const float nt = adam_one(a.h, bc, lrh[h], th[u][h], gg, mm, vv);
           if (j < 10) sm.par[ls * 13 + j] = nt;
-          else a.wsh[shi] = nt;
-          M[e] = mm;
-          Vm[e] = vv;
+          else a.wsh[gsh + (j - 10)] = nt;
+          const size_t e = (size_t)(s0 + ls) * D + j;
+          a.m[e] = mm;
+          a.v[e] = vv;
         }
       }
     }
-    __syncthreads();
+    __syncwarp();
     for (int e = tid; e < ns * 10; e += kPBS) {
       const int ls = e / 10, c = e - ls * 10;
       const size_t g = (size_t)sm.gid[ls];
@@ -701,22 +736,21 @@ __global__ void __launch_bounds__(kPBS, RTGS_BWD_F64 ? 12 : 22) k_project_bwd(co
       if (nz) a.eta[sm.gid[tid]] += 1u;
     }
   } else {
-    float* G = a.grad + (size_t)s0 * D;
-    for (int e0 = tid; e0 < ns * D; e0 += kPBS * U) {  // coalesced read-modify-write, 8 loads in flight
-      float g[U];
+    constexpr int SU = 8;  // slot rows in flight
+    for (int l0 = 0; l0 < ns; l0 += SU) {
+      float g[SU][NH];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int e = e0 + u * kPBS;
-        g[u] = e < ns * D ? G[e] : 0.f;
-      }
+      for (int u = 0; u < SU; ++u)
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int e = e0 + u * kPBS;
-        if (e < ns * D) {
-          const int ls = e / D, j = e - ls * D;
-          G[e] = g[u] + sh_grad<K>(sm.out + ls * LD, j);
+        for (int h = 0; h < NH; ++h) {
+          const bool live = l0 + u < ns && jh[h] < D;
+          g[u][h] = live ? a.grad[(size_t)(s0 + l0 + u) * D + jh[h]] : 0.f;
         }
-      }
+#pragma unroll
+      for (int u = 0; u < SU; ++u)
+#pragma unroll
+        for (int h = 0; h < NH; ++h)
+          if (l0 + u < ns && jh[h] < D) a.grad[(size_t)(s0 + l0 + u) * D + jh[h]] = g[u][h] + grad_of(l0 + u, h);
     }
   }
 }
