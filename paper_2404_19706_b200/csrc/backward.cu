@@ -16,6 +16,12 @@
 #include "internal.h"
 #include "tilepipe.cuh"
 
+// RTGS_BWD_DENSE=1 builds the dense walk of K5 (every lane evaluates every bbox survivor) for
+// comparison with the default span-mask walk
+#ifndef RTGS_BWD_DENSE
+#define RTGS_BWD_DENSE 0
+#endif
+
 namespace rtgs {
 
 constexpr int kSG = 16;  // screen-space gradient floats per slot
@@ -79,6 +85,7 @@ static_assert(kBwdParts == 2 || kBwdParts == 4, "the backward splits a tile in 2
 struct BwdSmem {
   PipeRing ring;
   int32_t slot[kPipeStages][kPipeBatch];
+  uint8_t survq[kBwdWarps][kPipeBatch];  // span path: the stage's bbox survivors, in list order
   float red[3][kBwdWarps];
   uint32_t last_max;
 };
@@ -202,6 +209,91 @@ __global__ void __launch_bounds__(32 * (kBwdWarps + 1)) k_render_bwd(const BwdAr
   float B = 0.f;                         // colour cotangent behind the current entry
   const uint32_t mylast = want ? last : 0u;
   const uint32_t wlast = __reduce_max_sync(0xffffffffu, mylast);  // this warp's entries: [start, wlast)
+#if !RTGS_BWD_DENSE
+  // Span path (as the forward's): per stage the warp's bbox survivors are queued; rounds of <= 32
+  // survivors, BACK TO FRONT, get exact support span masks (a superset of the pairs that pass
+  // eval_pair), one transpose, and each lane walks its own pixel's bits from the highest (the
+  // nearest-to-the-back entry first).  Lanes hold different entries at a time, so each contributing
+  // lane adds its 8 screen-space values with two vector reductions (no warp reduce).
+  const uint32_t q0 = pin(smem_u32(&sm.survq[w][0]));
+  (void)plane;
+  for (int b = 0; b < nb; ++b) {
+    const int st = b % kPipeStages;
+    mbar_wait_sleep(&r.full[st], (uint32_t)(b / kPipeStages) & 1u);
+    const int lo = pipe_batch_lo(true, start, end, b);
+    if ((uint32_t)lo < wlast) {  // warp-uniform: the batch holds entries of this warp's pixels
+      const uint32_t srec = rec0 + (uint32_t)(st * sizeof(r.rec[0]));  // shared addresses of this stage
+      const uint32_t sslot = slot0 + (uint32_t)(st * sizeof(sm.slot[0]));
+      const uint32_t sgid = gid0 + (uint32_t)(st * sizeof(r.gid[0]));
+      const int cnt = pipe_batch_cnt(true, start, end, b);
+      int nq = 0;
+      for (int g0 = 0; g0 < cnt; g0 += 32) {
+        const int j = g0 + lane;
+        bool ov = false;
+        if (j < cnt && (uint32_t)(lo + j) < wlast) {
+          const float4 r0 = lds128(srec + 48u * j);
+          const float2 ext = unpack_ext(__uint_as_float(lds32(srec + 48u * j + 44u)));
+          ov = (r0.x + ext.x >= bx0) && (r0.x - ext.x <= bx1) && (r0.y + ext.y >= by0) && (r0.y - ext.y <= by1);
+        }
+        const uint32_t bal = __ballot_sync(0xffffffffu, ov);
+        if (ov) sts8(q0 + (uint32_t)(nq + __popc(bal & ((1u << lane) - 1u))), (uint32_t)j);
+        nq += __popc(bal);
+      }
+      __syncwarp();
+      for (int q = ((nq - 1) / 32) * 32; q >= 0 && nq > 0; q -= 32) {
+        uint32_t pm = 0u;
+        if (q + lane < nq) {
+          const uint32_t ra = srec + 48u * lds8(q0 + (uint32_t)(q + lane));
+          pm = support_mask(lds128(ra), lds128(ra + 16u), bx0, by0);
+        }
+        uint32_t lm = warp_transpose32(pm, (uint32_t)lane);
+        if (!want) lm = 0u;
+        const int trips = __reduce_max_sync(0xffffffffu, (uint32_t)__popc(lm));
+        for (int it = 0; it < trips; ++it) {
+          const bool has = lm != 0u;
+          const int jj = has ? 31 - __clz(lm) : 0;  // back to front
+          lm &= has ? ~(1u << jj) : 0xFFFFFFFFu;
+          const uint32_t idx = lds8(q0 + (uint32_t)(q + jj));
+          const uint32_t ra = srec + 48u * idx;
+          const float4 r0 = lds128(ra), r1 = lds128(ra + 16u), r2 = lds128(ra + 32u);
+          PairEval e;
+          // blended in the forward <=> passes the support test and lies before the pixel's `last`
+          const bool ok = eval_pair(r0, r1, fpx, fpy, e) && has && ((uint32_t)lo + idx < mylast);
+          const float inv1mf = __frcp_rn(__fsub_rn(1.f, e.f));  // IEEE reciprocal; 1 - f >= 0.01
+          const float Ti = ok ? __fmul_rn(T, inv1mf) : T;        // T before entry i
+          const float wgt = ok ? __fmul_rn(e.f, Ti) : 0.f;
+          const float G = __fmaf_rn(gCb, r2.z, __fmaf_rn(gCg, r2.y, gCr * r2.x));
+          if (ok) {
+            const uint32_t ent = lds32(sgid + 4u * idx);
+            const int slot = (ent & kSubBit) ? (int)(ent & ~kSubBit) : (int)lds32(sslot + 4u * idx);
+            if (slot >= 0) {
+              const float dLdf = __fmul_rn(Ti, __fsub_rn(G, B));
+              // f = alpha e^power; the 0.99 cap passes no gradient when active (R17)
+              const float dLdp = (e.f < kFMax) ? dLdf * e.f : 0.f;
+              // power = p2 / log2(e): d power / d dx = (2 A' dx + B' dy) / log2(e) = -(A dx + B dy)
+              const float sc = dLdp * (1.f / kLog2e);
+              float* sg = a.sgrad + (size_t)slot * kSG;
+              atomicAdd(reinterpret_cast<float4*>(sg),
+                        make_float4(sc * (2.f * r1.x * e.dx + r1.y * e.dy),   // d/d mu_x
+                                    sc * (2.f * r1.z * e.dy + r1.y * e.dx),   // d/d mu_y
+                                    -0.5f * dLdp * e.dx * e.dx,               // d/d A
+                                    -dLdp * e.dx * e.dy));                    // d/d B
+              atomicAdd(reinterpret_cast<float4*>(sg + 4),
+                        make_float4(-0.5f * dLdp * e.dy * e.dy,               // d/d C
+                                    gCr * wgt, gCg * wgt, gCb * wgt));        // d/d rgb
+            }
+          }
+          B = ok ? __fmaf_rn(e.f, __fsub_rn(G, B), B) : B;  // f G + (1 - f) B
+          T = Ti;
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&r.empty[st]);
+  }
+}
+
+#else  // RTGS_BWD_DENSE: the dense walk (every lane evaluates every bbox survivor), for comparison
   for (int b = 0; b < nb; ++b) {
     const int st = b % kPipeStages;
     mbar_wait(&r.full[st], (uint32_t)(b / kPipeStages) & 1u);
@@ -276,6 +368,7 @@ __global__ void __launch_bounds__(32 * (kBwdWarps + 1)) k_render_bwd(const BwdAr
     if (lane == 0) mbar_arrive(&r.empty[st]);
   }
 }
+#endif
 
 // ------------------------------------------------------------------------------------------------
 // K5b: chain rule through the projection (float32, recomputing the forward quantities)

@@ -200,77 +200,8 @@ cudaError_t launch_tile_coverage(const uint2* srange, const unsigned long long* 
 //      per-lane count, not the survivor count), with the unchanged eval_pair / blend arithmetic, so
 //      every decision and every value are bitwise those of the dense path (RTGS_RENDER_DENSE checks).
 
-// 32x32 bit-matrix transpose across the warp: in, lane i holds row i (bit c = M[i][c]); out, lane p
-// holds column p (bit j = M[j][p]).  Recursive block swaps, 5 shuffles.
-__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, uint32_t lane) {
-  const uint32_t M[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
-#pragma unroll
-  for (int i = 0; i < 5; ++i) {
-    const uint32_t s = 16u >> i, m = M[i];
-    const uint32_t y = __shfl_xor_sync(0xffffffffu, x, (int)s);
-    x = (lane & s) ? ((x & ~m) | ((y & ~m) >> s)) : ((x & m) | ((y & m) << s));
-  }
-  return x;
-}
+// (warp_transpose32 and support_mask: tilepipe.cuh, shared with the backward)
 
-// Pixels of the 8x4 block (bx0, by0) (bit 8*row + col) that MAY pass eval_pair for record (a, c)
-// (a = mu hi/lo, c = (A', B', C', log2 alpha), p2 = A' dx^2 + B' dx dy + C' dy^2, dx = mu_x - u_x).
-// For pixel row y (dy = mu_y - y) the support p2 >= pm is the dx interval centred at B' dy / (2A')
-// (x = mu_x - dx) of half-width sqrt(disc) / (2|A'|), disc = 4 A' pm - dy^2 (4 A'C' - B'^2).  The
-// threshold is lowered by 1 % + 0.01 (a 0.5 %-larger ellipse) and the interval widened by 0.02 px, far
-// beyond the float32 rounding of this computation and of eval_pair, so the mask is a superset.
-__device__ __forceinline__ uint32_t support_mask(const float4 a, const float4 c, float bx0, float by0) {
-  const float mx = a.x + a.z, my = a.y + a.w;
-  const float pmin = fmaxf(kP2Min, kLog2FMin - c.w);
-  const float pm = __fmaf_rn(pmin, 1.01f, -0.01f);
-  const float D0 = 4.f * c.x * pm;                       // > 0 (A' < 0, pm < 0)
-  const float D2 = __fmaf_rn(4.f * c.x, c.z, -c.y * c.y); // 4 A'C' - B'^2 > 0
-  const float inv2a = -0.5f / c.x;                       // 1 / (2 |A'|)
-  const float xs = -c.y * inv2a;                         // x centre = mu_x + xs dy
-  uint32_t m = 0u;
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const float dy = my - (by0 + (float)k);
-    const float disc = __fmaf_rn(-D2, dy * dy, D0);
-    if (disc >= 0.f) {
-      float sq;
-      asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(sq) : "f"(disc));  // ~2 ulp: inside the 0.02 px margin
-      const float h = __fmaf_rn(sq, inv2a, 0.02f);
-      const float xc = __fmaf_rn(xs, dy, mx) - bx0;
-      const int lo = (int)ceilf(fmaxf(xc - h, -1.f));
-      const int hi = (int)floorf(fminf(xc + h, 8.f));
-      const int l0 = max(lo, 0), h0 = min(hi, 7);
-      if (l0 <= h0) m |= ((0xFFu >> (7 - (h0 - l0))) << l0) << (8 * k);
-    }
-  }
-  return m;
-}
-
-struct FwdArgs {
-  const float4* rec;
-  const uint32_t* zkey;
-  const float4* sub_rec;  // NEXT f3 subset rows (entries with kSubBit), else NULL
-  const uint32_t* sub_zkey;
-  const int32_t* sub_gid;
-  const uint32_t* sorted_gid;
-  const uint2* range;
-  const uint32_t* tile_list;
-  const uint32_t* counts;
-  const uint32_t* active;
-  CamK cam;
-  float R[9];
-  float* color;
-  float* trans;
-  float* depth;
-  float* normal;
-  int32_t* index;
-  uint32_t* n_contrib;
-};
-
-// COUNT: accumulate the blended-pair statistic counts[3] (RTGS_RENDER_COUNT; the production renders of
-// the mapping step do not, saving 3 instructions per survivor)
-// LAST: track n_contrib (the sorted-list position past the last blended entry, which the backward
-// needs); a FULL render for the add masks / tracking only passes n_contrib = NULL and skips it
 // SPAN: the span-mask consumer (default); false = the dense consumer (RTGS_RENDER_DENSE, verification)
 #ifndef RTGS_SPAN_MINB
 #define RTGS_SPAN_MINB 5
