@@ -592,7 +592,7 @@ __device__ __forceinline__ void project_bwd_slot(const PBArgs& a, const float* s
   const float gc1 = par[11] > 0.f ? drgb[1] : 0.f;
   const float gc2 = par[12] > 0.f ? drgb[2] : 0.f;
   float shc[3 * K];
-  if constexpr ((3 * K) % 4 == 0) {  // 16-byte aligned row: vector reads (conflict-free with the padded pitch)
+  if constexpr ((3 * K) % 4 == 0) {  // 16-byte aligned row (K = 4, 16): LDG.128 straight from global memory
 #pragma unroll
     for (int q = 0; q < 3 * K / 4; ++q) {
       const float4 t4 = reinterpret_cast<const float4*>(shrow)[q];
@@ -680,10 +680,16 @@ __device__ __forceinline__ float sh_grad(const float* row, int j) {
   return row[10 + kk] * row[10 + K + c];
 }
 
-// 22 resident 32-slot CTAs per SM (<= 88 registers, ~8 KB shared): 148 x 22 x 32 = 104k slots in
-// one wave, so the C3 iteration's 100k unstable slots do not pay a second wave of CTA latency
+// Resident 32-slot CTAs per SM: 22 for SH degrees 2-3 (<= 88 registers, ~8 KB shared: 148 x 22 x 32 =
+// 104k slots in one wave, so the C3 iteration's 100k unstable slots do not pay a second wave of CTA
+// latency; -Xptxas -v: 12-28 B of spills at K = 9 / 16), 16 for degrees 0-1 (the 80-register cap
+// spilled ~100 B there; with 128 registers none).  RTGS_BWD_F64: 12.
+template <int K>
+struct PBMinBlocks {
+  static constexpr int value = RTGS_BWD_F64 ? 12 : (K >= 9 ? 22 : 16);
+};
 template <int K, bool ADAM>
-__global__ void __launch_bounds__(kPBS, RTGS_BWD_F64 ? 12 : 22) k_project_bwd(const PBArgs a) {
+__global__ void __launch_bounds__(kPBS, PBMinBlocks<K>::value) k_project_bwd(const PBArgs a) {
   using SM = PBSmem<K>;
   constexpr int D = SM::D, LD = SM::LD, SHF = SM::SHF;
   extern __shared__ __align__(16) unsigned char smem_raw[];
