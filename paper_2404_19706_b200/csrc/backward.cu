@@ -723,6 +723,17 @@ __global__ void __launch_bounds__(kPBS, PBMinBlocks<K>::value) k_project_bwd(con
     for (int u = 0; u < U; ++u)
       if (e0 + u * kPBS < ns * kSG) sm.sg[e0 + u * kPBS] = v[u];
   }
+  __syncwarp();
+  // slots that received any screen-space gradient this call; the accumulate form (no Adam: the
+  // keyframe batch, where most of the map is out of a view's top-40 % pixels) skips the others
+  // entirely -- their row gets + 0 -- instead of a read-modify-write of every row
+  bool touched = false;
+  if (tid < ns) {
+#pragma unroll
+    for (int k = 0; k < 13; ++k) touched |= sm.sg[tid * kSG + k] != 0.f;
+  }
+  const uint32_t tmask = __ballot_sync(0xffffffffu, touched);
+  if (!ADAM && tmask == 0u) return;
   for (int e0 = tid; e0 < ns * 13; e0 += kPBS * U) {
     float v[U];
 #pragma unroll
@@ -835,21 +846,28 @@ __global__ void __launch_bounds__(kPBS, PBMinBlocks<K>::value) k_project_bwd(con
       if (nz) a.eta[sm.gid[tid]] += 1u;
     }
   } else {
-    constexpr int SU = 8;  // slot rows in flight
-    for (int l0 = 0; l0 < ns; l0 += SU) {
+    constexpr int SU = 8;  // touched slot rows in flight
+    uint32_t rem = tmask;
+    while (rem) {
+      int ls[SU];
+#pragma unroll
+      for (int u = 0; u < SU; ++u) {
+        ls[u] = rem ? __ffs(rem) - 1 : -1;
+        rem &= rem ? rem - 1u : 0u;
+      }
       float g[SU][NH];
 #pragma unroll
       for (int u = 0; u < SU; ++u)
 #pragma unroll
         for (int h = 0; h < NH; ++h) {
-          const bool live = l0 + u < ns && jh[h] < D;
-          g[u][h] = live ? a.grad[(size_t)(s0 + l0 + u) * D + jh[h]] : 0.f;
+          const bool live = ls[u] >= 0 && jh[h] < D;
+          g[u][h] = live ? a.grad[(size_t)(s0 + ls[u]) * D + jh[h]] : 0.f;
         }
 #pragma unroll
       for (int u = 0; u < SU; ++u)
 #pragma unroll
         for (int h = 0; h < NH; ++h)
-          if (l0 + u < ns && jh[h] < D) a.grad[(size_t)(s0 + l0 + u) * D + jh[h]] = g[u][h] + grad_of(l0 + u, h);
+          if (ls[u] >= 0 && jh[h] < D) a.grad[(size_t)(s0 + ls[u]) * D + jh[h]] = g[u][h] + grad_of(ls[u], h);
     }
   }
 }
