@@ -1,0 +1,17 @@
+# Round-2 measurement pass (one gpurun call): GPU suite, the bench lines (C3 default with the CPU
+# oracle leg, C2, C4, C5 at N = 1), the reference arm, the ncu launch list of the C3 step and one
+# `ncu --set full` capture of the dominant kernels.  Outputs in gpurun_out/r2m_*.
+set -u
+python -m pytest tests -m gpu -q > gpurun_out/r2m_tests.log 2>&1; echo "tests: $(tail -1 gpurun_out/r2m_tests.log)"
+python bench.py --steps 20 --warmup 5 > gpurun_out/r2m_c3.log 2>&1; echo "c3 rc=$?"
+for c in C2 C4 C5; do
+  python bench.py --config $c --steps 20 --warmup 5 > gpurun_out/r2m_$c.log 2>&1; echo "$c rc=$?"
+done
+timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/r2m_ref.log 2>&1; echo "ref rc=$?"
+if timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/r2m_launches.csv \
+     python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-window > gpurun_out/r2m_ncu_launch.log 2>&1; then
+  timeout 1200 ncu -f --set full --clock-control none --import-source on \
+     -k regex:"k_render_fwd|k_render_bwd|k_project_bwd|k_project|k_tile_sort|k_emit" -s 40 -c 12 \
+     -o gpurun_out/r2m_prof python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-window > gpurun_out/r2m_ncu_full.log 2>&1
+  echo "ncu full rc=$?"
+fi
