@@ -457,6 +457,25 @@ rtgs_status rtgs_icp_track(const float* depth, const float* model_depth, const f
 rtgs_status rtgs_decode_rgbd(const uint8_t* rgb, const uint16_t* depth_raw, int32_t width, int32_t height,
                              float depth_scale, float* color, float* depth, void* stream);
 
+/* =============================================================================================
+ * Map layout (a framework step, not a step of the method): spatial order of the Gaussians.
+ * The paper's maps grow frame by frame from row-major pixel samples, so nearby Gaussians
+ * sit at nearby indices; these calls restore that coherence for a map in arbitrary order, which the
+ * binning's per-tile counters, the renderer's record gathers and the backward's gradient rows use.
+ *
+ * rtgs_morton_order: perm[r] = the gid at rank r when the live Gaussians (flags bit 2 clear; flags
+ *   NULLABLE = all live) are sorted by the 30-bit Morton code of their position quantised in the live
+ *   bounding box (per axis q = min(1023, (int)((p - lo) * (1024 / (hi - lo)))), float32 ops in that
+ *   order; a zero extent gives q = 0), ties by gid; removed Gaussians last, in gid order.  pos [n][3];
+ *   perm [n] device (uint32).  Workspace: rtgs_morton_workspace_size(n).
+ * rtgs_gather_rows: dst row r = src row perm[r] (rows of row_bytes bytes; n rows; src and dst must
+ *   not overlap) - applies a permutation to any per-Gaussian array. */
+size_t rtgs_morton_workspace_size(int32_t n);
+rtgs_status rtgs_morton_order(const float* pos, const uint8_t* flags, int32_t n, uint32_t* perm, void* workspace,
+                              size_t workspace_bytes, void* stream);
+rtgs_status rtgs_gather_rows(const void* src, void* dst, const uint32_t* perm, int32_t n, int32_t row_bytes,
+                             void* stream);
+
 /* rtgs_coverage_and_bin_cached: the f3 iteration's A0 + A2 in one call.  The subset rows are binned
  * over ALL tiles; M_unstable (R16) is decided per tile from those lists (every pixel tests the tile's
  * unstable instances until its first hit — identical decisions to the COVERAGE mode), giving

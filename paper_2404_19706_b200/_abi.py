@@ -128,6 +128,9 @@ EXPORTS = {
     "rtgs_merge_cached": (C.c_int, [P(Projected), P(Bins), P(Projected), vp, C.c_int32, P(Camera), P(RenderOut),
                                     P(Bins), vp, C.c_size_t, vp]),
     "rtgs_topk_workspace_size": (C.c_size_t, [P(Camera)]),
+    "rtgs_morton_workspace_size": (C.c_size_t, [C.c_int32]),
+    "rtgs_morton_order": (C.c_int, [vp, vp, C.c_int32, vp, vp, C.c_size_t, vp]),
+    "rtgs_gather_rows": (C.c_int, [vp, vp, vp, C.c_int32, C.c_int32, vp]),
     "rtgs_topk_error_mask": (C.c_int, [vp, vp, P(Camera), C.c_double, P(RenderOut), vp, C.c_size_t, vp]),
     "rtgs_status_string": (C.c_char_p, [C.c_int]),
     "rtgs_last_cuda_error": (C.c_char_p, []),

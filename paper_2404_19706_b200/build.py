@@ -13,7 +13,7 @@ INCLUDE = os.path.join(ROOT, "include")
 BUILD = os.path.join(PKG, "build")
 LIB = os.path.join(PKG, "librtgs.so")
 SOURCES = ["abi.cu", "project.cu", "sort.cu", "render.cu", "backward.cu", "adam.cu", "classify.cu", "state.cu",
-           "insert.cu", "icp.cu", "decode.cu"]
+           "insert.cu", "icp.cu", "decode.cu", "order.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 DEBUG = os.environ.get("RTGS_DEBUG", "") == "1"  # device asserts on indices (debug builds only)
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-Xcompiler", "-fPIC",

@@ -350,6 +350,25 @@ rtgs_status rtgs_merge_cached(const rtgs_projected* proj, const rtgs_bins* cache
                                     S(stream)));
 }
 
+size_t rtgs_morton_workspace_size(int32_t n) { return n < 0 ? 0 : morton_workspace_size(n); }
+
+rtgs_status rtgs_morton_order(const float* pos, const uint8_t* flags, int32_t n, uint32_t* perm, void* workspace,
+                              size_t workspace_bytes, void* stream) {
+  if (n < 0 || (n > 0 && (!pos || !perm || !a4(pos)))) return RTGS_ERR_INVALID_ARG;
+  if (n > 0 && (!workspace || workspace_bytes < morton_workspace_size(n))) return RTGS_ERR_WORKSPACE;
+  return finish(launch_morton_order(pos, flags, n, perm, workspace, S(stream)));
+}
+
+rtgs_status rtgs_gather_rows(const void* src, void* dst, const uint32_t* perm, int32_t n, int32_t row_bytes,
+                             void* stream) {
+  if (n < 0 || row_bytes <= 0 || (n > 0 && (!src || !dst || !perm))) return RTGS_ERR_INVALID_ARG;
+  const char* a = static_cast<const char*>(src);
+  const char* b = static_cast<const char*>(dst);
+  const size_t bytes = (size_t)n * row_bytes;
+  if (n > 0 && a < b + bytes && b < a + bytes) return RTGS_ERR_INVALID_ARG;  // overlapping
+  return finish(launch_gather_rows(src, dst, perm, n, row_bytes, S(stream)));
+}
+
 size_t rtgs_topk_workspace_size(const rtgs_camera* cam) { return cam_ok(cam) ? topk_workspace_size(*cam) : 0; }
 
 rtgs_status rtgs_topk_error_mask(const float* color_hat, const float* frame_color, const rtgs_camera* cam, double ratio,

@@ -177,4 +177,19 @@ __device__ __forceinline__ float2 unpack_ext(float w) {
                      __half2float(__ushort_as_half((unsigned short)(u >> 16))));
 }
 
+// warp-aggregated per-tile counting: the lanes' rect tiles in a warp-uniform loop, one atomic per
+// distinct tile per warp (match_any groups; spatially coherent maps put a warp's Gaussians on few
+// tiles, rtgs_morton_order)
+__device__ __forceinline__ void tile_count_agg(uint32_t* cnt, int nt, int w, int tx0, int ty0, int TX,
+                                               const uint8_t* keep) {
+  const int lane = threadIdx.x & 31;
+  const int ntmax = __reduce_max_sync(0xffffffffu, (uint32_t)nt);
+  for (int q = 0; q < ntmax; ++q) {
+    int t = q < nt ? (ty0 + q / w) * TX + tx0 + q % w : -1;
+    if (t >= 0 && keep && !keep[t]) t = -1;
+    const uint32_t peers = __match_any_sync(0xffffffffu, (uint32_t)t);
+    if (t >= 0 && lane == __ffs(peers) - 1) atomicAdd(&cnt[t], (uint32_t)__popc(peers));
+  }
+}
+
 }  // namespace rtgs

@@ -121,6 +121,11 @@ cudaError_t launch_topk(const float* chat, const float* c, const rtgs_camera& ca
 
 // generic device-wide exclusive scan of uint32 (length known on the host; zeros past the live part)
 size_t scan_workspace_size(size_t len);
+size_t morton_workspace_size(int n);
+cudaError_t launch_morton_order(const float* pos, const uint8_t* flags, int n, uint32_t* perm, void* ws,
+                                cudaStream_t s);
+cudaError_t launch_gather_rows(const void* src, void* dst, const uint32_t* perm, int n, int row_bytes,
+                               cudaStream_t s);
 cudaError_t launch_scan(const uint32_t* in, uint32_t* out, size_t len, uint32_t* total, void* ws, cudaStream_t s);
 
 }  // namespace rtgs

@@ -230,13 +230,14 @@ __global__ void __launch_bounds__(kProjThreads, 12) k_project(const ProjArgs a) 
     a.zkey[i] = zbits;
     a.rect[i] = rect;
     a.touched[i] = touched;
-    if (!SUB && a.cnt && vis) {  // A2 count, as k_tile_count (same tiles, same replica of Gaussian i)
-      uint32_t* c = a.cnt + (size_t)((i >> 8) & (kRep - 1)) * a.T;
-      const int tx0 = (int)(rect.x & 0xFFFF) / kTile, ty0 = (int)(rect.x >> 16) / kTile;
-      const int tx1 = (int)(rect.y & 0xFFFF) / kTile, ty1 = (int)(rect.y >> 16) / kTile;
-      for (int ty = ty0; ty <= ty1; ++ty)
-        for (int tx = tx0; tx <= tx1; ++tx) atomicAdd(&c[ty * a.TX + tx], 1u);
-    }
+  }
+  if (!SUB && a.cnt) {  // A2 count, as k_tile_count (same tiles, same replica of Gaussian i; warp-uniform)
+    uint32_t* c = a.cnt + (size_t)((i >> 8) & (kRep - 1)) * a.T;
+    const int tx0 = (int)(rect.x & 0xFFFF) / kTile, ty0 = (int)(rect.x >> 16) / kTile;
+    const int tx1 = (int)(rect.y & 0xFFFF) / kTile, ty1 = (int)(rect.y >> 16) / kTile;
+    const bool cnt_me = live && vis;
+    const int w = tx1 - tx0 + 1, nt = cnt_me ? w * (ty1 - ty0 + 1) : 0;
+    tile_count_agg(c, nt, w, tx0, ty0, a.TX, nullptr);
   }
 }
 

@@ -152,16 +152,16 @@ __global__ void __launch_bounds__(256) k_tile_count(const uint32_t* __restrict__
                                                     uint32_t* __restrict__ cnt) {
   const int i = blockIdx.x * 256 + threadIdx.x;
   cnt += (size_t)(blockIdx.x & (REP - 1)) * T;
-  if (i >= n) return;
-  const uint32_t z = zkey[i];
-  const uint2 rc = rect[i];  // both loads in flight together
-  int tx0, ty0, tx1, ty1;
-  if (z == 0xFFFFFFFFu || !rect_tiles(rc, tx0, ty0, tx1, ty1)) return;
-  for (int ty = ty0; ty <= ty1; ++ty)
-    for (int tx = tx0; tx <= tx1; ++tx) {
-      const int t = ty * TX + tx;
-      if (!keep || keep[t]) atomicAdd(&cnt[t], 1u);
-    }
+  uint32_t z = 0xFFFFFFFFu;
+  uint2 rc = make_uint2(1u, 0u);
+  if (i < n) {
+    z = zkey[i];
+    rc = rect[i];  // both loads in flight together
+  }
+  int tx0 = 0, ty0 = 0, tx1 = -1, ty1 = -1;
+  const bool vis = i < n && z != 0xFFFFFFFFu && rect_tiles(rc, tx0, ty0, tx1, ty1);
+  const int w = tx1 - tx0 + 1, nt = vis ? w * (ty1 - ty0 + 1) : 0;
+  tile_count_agg(cnt, nt, w, tx0, ty0, TX, keep);
 }
 
 // one CTA: tile_range[t] = [start, start + count) (clamped to the capacity), n_instances, and the
@@ -244,34 +244,35 @@ __global__ void __launch_bounds__(256) k_emit(const uint32_t* __restrict__ zkey,
   const size_t rep = (size_t)(blockIdx.x & (REP - 1)) * T;  // same replica as k_tile_count
   start += rep;
   cursor += rep;
-  if (i >= n) return;
-  const uint32_t z = zkey[i];
-  const uint2 rc = rect[i];
-  int tx0, ty0, tx1, ty1;
-  if (z == 0xFFFFFFFFu || !rect_tiles(rc, tx0, ty0, tx1, ty1)) return;
-  const uint32_t low = STB ? (((uint32_t)i << 1) | ((flags[i] >> 1) & 1u)) : (uint32_t)i;
+  const int lane = threadIdx.x & 31;
+  const uint32_t lt = (1u << lane) - 1u;
+  uint32_t z = 0xFFFFFFFFu;
+  uint2 rc = make_uint2(1u, 0u);
+  if (i < n) {
+    z = zkey[i];
+    rc = rect[i];
+  }
+  int tx0 = 0, ty0 = 0, tx1 = -1, ty1 = -1;
+  const bool vis = i < n && z != 0xFFFFFFFFu && rect_tiles(rc, tx0, ty0, tx1, ty1);
+  const uint32_t low = vis ? (STB ? (((uint32_t)i << 1) | ((flags[i] >> 1) & 1u)) : (uint32_t)i) : 0u;
   const unsigned long long k = ((unsigned long long)z << 32) | low;
-  // tiles in groups of 4: the group's cursor atomics (and start loads) are all in flight before
-  // the first store, instead of one atomic round trip per tile
-  const int w = tx1 - tx0 + 1, nt = w * (ty1 - ty0 + 1);
-  for (int q0 = 0; q0 < nt; q0 += 4) {
-    int t[4];
-    uint32_t base[4], off[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int q = q0 + u;
-      t[u] = q < nt ? (ty0 + q / w) * TX + tx0 + q % w : -1;
-      if (t[u] >= 0 && keep && !keep[t[u]]) t[u] = -1;
+  const int w = tx1 - tx0 + 1, nt = vis ? w * (ty1 - ty0 + 1) : 0;
+  // warp-uniform loop over the tiles of the lanes' rects: lanes that land on the same tile (spatially
+  // coherent maps, rtgs_morton_order) share ONE cursor atomic (match_any groups, the group's leader
+  // adds the group size and broadcasts the base), instead of one atomic round trip per instance
+  const int ntmax = __reduce_max_sync(0xffffffffu, (uint32_t)nt);
+  for (int q = 0; q < ntmax; ++q) {
+    int t = q < nt ? (ty0 + q / w) * TX + tx0 + q % w : -1;
+    if (t >= 0 && keep && !keep[t]) t = -1;
+    const uint32_t peers = __match_any_sync(0xffffffffu, (uint32_t)t);
+    const int leader = __ffs(peers) - 1;
+    uint32_t off = 0u;
+    if (t >= 0 && lane == leader) off = atomicAdd(&cursor[t], (uint32_t)__popc(peers));
+    off = __shfl_sync(0xffffffffu, off, leader) + __popc(peers & lt);
+    if (t >= 0) {
+      const uint32_t slot = start[t] + off;
+      if (slot < cap) keys[slot] = k;
     }
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (t[u] >= 0) {
-        base[u] = start[t[u]];
-        off[u] = atomicAdd(&cursor[t[u]], 1u);
-      }
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (t[u] >= 0 && base[u] + off[u] < cap) keys[base[u] + off[u]] = k;
   }
 }
 

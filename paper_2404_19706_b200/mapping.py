@@ -117,6 +117,23 @@ class GaussianMap:
         self.store = store
         self.resize(n)
 
+    def permute(self, perm: torch.Tensor, stream=None):
+        """Reorder the live rows: row r becomes old row perm[r] (every field; storage reallocated)."""
+        n = self.n
+        for k in _MAP_FIELDS:
+            old = self.store[k] if self.store is not None else getattr(self, k)
+            new = torch.empty_like(old)
+            if n:
+                gather_rows(old[:n], new, perm, stream)
+            if old.shape[0] > n:
+                new[n:].copy_(old[n:])
+            if self.store is not None:
+                self.store[k] = new
+            else:
+                setattr(self, k, new)
+        if self.store is not None:
+            self.resize(n)
+
     def c_struct(self) -> _abi.Gaussians:
         return _abi.Gaussians(_p(self.pos), _p(self.log_scale), _p(self.rot), _p(self.opacity), _p(self.sh),
                               _p(self.flags), self.n, self.sh_degree)
@@ -456,6 +473,28 @@ def icp_track(depth: torch.Tensor, model: RenderBuffers, model_pose: _abi.Pose, 
                                workspace.numel() * workspace.element_size(), _stream(stream)), "rtgs_icp_track")
 
 
+def morton_workspace_size(n: int) -> int:
+    return int(lib().rtgs_morton_workspace_size(int(n)))
+
+
+def morton_order(gm: GaussianMap, stream=None) -> torch.Tensor:
+    """Map layout: the permutation (device int32 view of uint32, perm[r] = gid at rank r) that sorts
+    the live Gaussians by the Morton code of their position, removed ones last (rtgs_morton_order)."""
+    n = gm.n
+    perm = torch.empty(max(n, 1), dtype=torch.int32, device=gm.pos.device)[:n]
+    ws = torch.empty(max(morton_workspace_size(n), 1), dtype=torch.uint8, device=gm.pos.device)
+    check(lib().rtgs_morton_order(_p(gm.pos), _p(gm.flags), n, _p(perm), _p(ws), ws.numel(), _stream(stream)),
+          "rtgs_morton_order")
+    return perm
+
+
+def gather_rows(src: torch.Tensor, dst: torch.Tensor, perm: torch.Tensor, stream=None):
+    """dst[r] = src[perm[r]] for the first perm.numel() rows (rtgs_gather_rows)."""
+    n = int(perm.numel())
+    row_bytes = (src.numel() // max(src.shape[0], 1)) * src.element_size()
+    check(lib().rtgs_gather_rows(_p(src), _p(dst), _p(perm), n, int(row_bytes), _stream(stream)), "rtgs_gather_rows")
+
+
 def decode_rgbd(rgb: torch.Tensor, depth_raw: torch.Tensor, depth_scale: float, color: torch.Tensor,
                 depth: torch.Tensor, stream=None):
     """Sensor-native frame (uint8 [H,W,3] RGB, uint16 [H,W] depth in raw units) -> planar float32
@@ -589,6 +628,30 @@ class MappingEngine:
         self.use_cache = True
         self.fused_adam = True
         self.reset_window()
+
+    def reorder_spatially(self, stream=None) -> torch.Tensor:
+        """Map layout (not a step of the method): put the map in Morton order (rtgs_morton_order) and
+        carry every per-Gaussian array along (parameters, flags, eta, e, t, L_reg anchors); the f3
+        caches and the window slots are rebuilt.  Gids change: returns perm (new row r = old gid
+        perm[r]).  The paper's maps, grown from row-major pixel samples frame by frame, are
+        spatially coherent already; this restores that for a map handed over in arbitrary order."""
+        perm = morton_order(self.gm, stream)
+        self.gm.permute(perm, stream)
+        n = self.gm.n
+        for k, v in list(self._state_store.items()):
+            new = v.clone()
+            if n:
+                gather_rows(v[:n], new, perm, stream)
+            self._state_store[k] = new
+        a = self._anchor.clone()
+        if n:
+            gather_rows(self._anchor[:n], a, perm, stream)
+        self._anchor = a
+        self._view_state()
+        self._drop_cache()
+        self._map_version += 1
+        self.reset_window()
+        return perm
 
     def _record_anchor(self, r0: int, r1: int, stream=None):
         if r1 > r0:

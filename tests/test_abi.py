@@ -26,7 +26,7 @@ def _declared():
 
 def test_every_declared_symbol_is_exported(L):
     names = _declared()
-    assert len(names) == 32
+    assert len(names) == 35
     for n in names:
         assert hasattr(L, n), n
     from paper_2404_19706_b200 import _abi
@@ -148,3 +148,15 @@ def test_next_row_entry_points_validate_on_host(L):
                                None, 0, None) == 1
     assert mapping.insert_workspace_size(1000, 64) > 0 and mapping.icp_workspace_size(cam, 3) > 0
     assert mapping.topk_workspace_size(cam) > 0
+
+
+def test_layout_calls_reject_bad_arguments(L):
+    import ctypes as C
+    # rtgs_morton_order / rtgs_gather_rows validate on the host before any launch
+    assert L.rtgs_morton_order(None, None, 10, None, None, 0, None) == 1
+    assert L.rtgs_gather_rows(None, None, None, 5, 4, None) == 1
+    assert L.rtgs_gather_rows(None, None, None, 5, 0, None) == 1
+    buf = (C.c_uint8 * 64)()
+    p = C.cast(buf, C.c_void_p)
+    assert L.rtgs_gather_rows(p, p, p, 4, 4, None) == 1                           # overlapping src / dst
+    assert L.rtgs_morton_workspace_size(-1) == 0 and L.rtgs_morton_workspace_size(1000) > 0
