@@ -296,6 +296,8 @@ def main():
     ap.add_argument("--no-fuse-adam", action="store_true", help="separate A5 backward and A6 Adam calls")
     ap.add_argument("--no-restore", action="store_true", help="diagnostic: let the map drift between timed steps")
     ap.add_argument("--no-window", action="store_true", help="skip the supplementary mapping-window measurement")
+    ap.add_argument("--no-reorder", action="store_true",
+                    help="keep the generator's Gaussian order instead of the engine's Morton layout")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -478,6 +480,8 @@ def run_mapping(args, rank, world, local):
     cam = P.camera_of(cfg)
     pose = P.make_pose(R, t)
     eng = P.MappingEngine(gm, cam, capacity=4 * cfg.n)
+    if not args.no_reorder:
+        eng.reorder_spatially()   # the framework's map layout (rtgs_morton_order), before any timing
     eng.use_cache = not args.no_cache
     eng.fused_adam = not args.no_fuse_adam
     col = torch.as_tensor(col_h, device="cuda")
@@ -964,6 +968,8 @@ def run_render_only(args, rank, world, local):
     cfg = CONFIGS["C4"]
     scene = make_scene(cfg)
     gm = P.GaussianMap.from_arrays(scene)
+    if not args.no_reorder:
+        gm.permute(P.morton_order(gm))   # the framework's map layout, before any timing
     cam = P.camera_of(cfg)
     poses = [P.make_pose(*make_pose(cfg, view=v)) for v in range(8)]
     n, cap = gm.n, 3 * cfg.n
@@ -1076,6 +1082,8 @@ def run_batch(args, rank, world, local):
     gm = P.GaussianMap.from_arrays(scene)
     cam = P.camera_of(cfg)
     eng = P.MappingEngine(gm, cam, capacity=4 * cfg.n)
+    if not args.no_reorder:
+        eng.reorder_spatially()   # the framework's map layout, before any timing
     mine = view_partition(N_C5_VIEWS, world, rank)
     views = [None] * N_C5_VIEWS
     for v, tr in zip(mine, c5_views(P, cfg, mine)):
