@@ -46,6 +46,8 @@ __global__ void __launch_bounds__(256) k_bbox(const float* __restrict__ pos, con
       hi[k] = fmaxf(hi[k], v);
     }
   }
+  __shared__ float s_lo[3][8], s_hi[3][8];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
     float a = lo[k], b = hi[k];
@@ -54,7 +56,14 @@ __global__ void __launch_bounds__(256) k_bbox(const float* __restrict__ pos, con
       a = fminf(a, __shfl_xor_sync(0xffffffffu, a, o));
       b = fmaxf(b, __shfl_xor_sync(0xffffffffu, b, o));
     }
-    if ((threadIdx.x & 31) == 0 && a <= b) {
+    if (lane == 0) { s_lo[k][w] = a; s_hi[k][w] = b; }
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) {  // one atomic pair per block and axis (same-address atomics serialise)
+    const int k = threadIdx.x;
+    float a = s_lo[k][0], b = s_hi[k][0];
+    for (int ww = 1; ww < 8; ++ww) { a = fminf(a, s_lo[k][ww]); b = fmaxf(b, s_hi[k][ww]); }
+    if (a <= b) {
       atomicMin(&bb[k], f2ord(a));
       atomicMax(&bb[3 + k], f2ord(b));
     }
@@ -197,7 +206,7 @@ cudaError_t launch_morton_order(const float* pos, const uint8_t* flags, int n, u
   OrderWS w = carve_order(n, static_cast<char*>(ws));
   const int nb = (n + kOrdBlock - 1) / kOrdBlock;
   k_bbox_init<<<1, 32, 0, s>>>(w.bb);
-  k_bbox<<<min((n + 255) / 256, 148 * 8), 256, 0, s>>>(pos, flags, n, w.bb);
+  k_bbox<<<min((n + 255) / 256, 148 * 2), 256, 0, s>>>(pos, flags, n, w.bb);
   k_morton<<<(n + 255) / 256, 256, 0, s>>>(pos, flags, n, w.bb, w.k0, w.v0);
   note_launch(3);
   uint32_t* kb[2] = {w.k0, w.k1};
