@@ -28,7 +28,10 @@ namespace rtgs {
 constexpr int kScanThreads = 256;
 constexpr int kScanItems = 8;
 constexpr int kScanChunk = kScanThreads * kScanItems;  // 2048
-constexpr int kSortThreads = 256;
+#ifndef RTGS_SORT_THREADS
+#define RTGS_SORT_THREADS 256
+#endif
+constexpr int kSortThreads = RTGS_SORT_THREADS;  // 128 or 256 (swept)
 constexpr int kSortWarps = kSortThreads / 32;
 constexpr int kSortCap = 1024;  // tile lists up to this length are sorted in shared memory
 
@@ -303,17 +306,29 @@ __device__ __forceinline__ void cta_radix_sort(unsigned long long* A, unsigned l
       __syncwarp();
     }
     __syncthreads();
-    {  // per digit: prefix over warps, then exclusive scan over digits
-      const int d = tid;  // kSortThreads == 256 digits
-      uint32_t run_w = 0;
+    {  // per digit: prefix over warps, then exclusive scan over digits (kDPT consecutive per thread)
+      constexpr int kDPT = 256 / kSortThreads;
+      uint32_t tot_d[kDPT], tsum = 0;
 #pragma unroll
-      for (int ww = 0; ww < kSortWarps; ++ww) {
-        const uint32_t c = wcnt[ww][d];
-        wcnt[ww][d] = run_w;
-        run_w += c;
+      for (int j = 0; j < kDPT; ++j) {
+        const int d = tid * kDPT + j;
+        uint32_t run_w = 0;
+#pragma unroll
+        for (int ww = 0; ww < kSortWarps; ++ww) {
+          const uint32_t c = wcnt[ww][d];
+          wcnt[ww][d] = run_w;
+          run_w += c;
+        }
+        tot_d[j] = run_w;
+        tsum += run_w;
       }
       uint32_t tot;
-      dstart[d] = block_excl_scan(run_w, scan_sh, &tot);
+      uint32_t ex = block_excl_scan(tsum, scan_sh, &tot);
+#pragma unroll
+      for (int j = 0; j < kDPT; ++j) {
+        dstart[tid * kDPT + j] = ex;
+        ex += tot_d[j];
+      }
     }
     __syncthreads();  // dstart written after the scan's own barriers
     for (int i = r0 + lane; i < r1; i += 32) {
@@ -439,7 +454,7 @@ struct StableOut {  // NEXT f3 cache written by the FULL binning (flags NULL: no
   uint32_t* n_stable;
 };
 
-__global__ void __launch_bounds__(kSortThreads, 6) k_tile_sort(const uint2* __restrict__ range,
+__global__ void __launch_bounds__(kSortThreads, 1536 / kSortThreads) k_tile_sort(const uint2* __restrict__ range,
                                                             unsigned long long* __restrict__ keys,
                                                             unsigned long long* __restrict__ tmp,
                                                             uint32_t* __restrict__ grank, int gid_bits,
