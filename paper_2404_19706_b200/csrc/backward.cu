@@ -709,6 +709,7 @@ __global__ void __launch_bounds__(kPBS, PBMinBlocks<K>::value) k_project_bwd(con
   if (ns <= 0) return;
   if (tid < ns) sm.gid[tid] = a.gid_of_slot[s0 + tid];
   if (ADAM && tid < ns) sm.transparent[tid] = (a.flags[sm.gid[tid]] & 5u) == 1u;  // not removed (R18, R29)
+  const uint32_t eta_now = (ADAM && tid < ns) ? a.eta[sm.gid[tid]] : 0u;  // (read early: used at the end)
   __syncthreads();
   // (loads batched 8 deep before their stores so that many are in flight per thread)
   constexpr int U = 8;
@@ -792,7 +793,7 @@ __global__ void __launch_bounds__(kPBS, PBMinBlocks<K>::value) k_project_bwd(con
     for (int h = 0; h < NH; ++h) lrh[h] = adam_lr(a.h, min(jh[h], D - 1));
     constexpr int SU = 4;  // slot rows in flight
     for (int l0 = 0; l0 < ns; l0 += SU) {
-      float mo[SU][NH], vo[SU][NH], th[SU][NH];
+      float mo[SU][NH], vo[SU][NH], th[SU][NH], t0[SU];
 #pragma unroll
       for (int u = 0; u < SU; ++u) {
         const int ls = min(l0 + u, ns - 1);
@@ -806,6 +807,9 @@ __global__ void __launch_bounds__(kPBS, PBMinBlocks<K>::value) k_project_bwd(con
           vo[u][h] = live ? a.v[e] : 0.f;
           th[u][h] = !live ? 0.f : (j < 10 ? sm.par[ls * 13 + j] : a.sh[gsh + (j - 10)]);
         }
+        // the L_reg anchor (lane < 10: the geometry components of h = 0), with the other loads
+        t0[u] = (lane < 10 && l0 + u < ns && a.init_geom && sm.transparent[ls])
+                    ? a.init_geom[(size_t)(s0 + ls) * 10 + lane] : 0.f;
       }
 #pragma unroll
       for (int u = 0; u < SU; ++u) {
@@ -818,10 +822,7 @@ __global__ void __launch_bounds__(kPBS, PBMinBlocks<K>::value) k_project_bwd(con
           const int j = jh[h];
           if (j >= D) continue;
           float gg = grad_of(ls, h);
-          if (j < 10 && tr) {  // L_reg (R18)
-            const float th0 = a.init_geom ? a.init_geom[(size_t)(s0 + ls) * 10 + j] : 0.f;
-            gg += a.h.reg_coef * (th[u][h] - th0);
-          }
+          if (j < 10 && tr) gg += a.h.reg_coef * (th[u][h] - t0[u]);  // L_reg (R18)
           float mm = mo[u][h], vv = vo[u][h];
           const float nt = adam_one(a.h, bc, lrh[h], th[u][h], gg, mm, vv);
           if (j < 10) sm.par[ls * 13 + j] = nt;
@@ -843,7 +844,7 @@ __global__ void __launch_bounds__(kPBS, PBMinBlocks<K>::value) k_project_bwd(con
       bool nz = false;
 #pragma unroll 8
       for (int j = 0; j < SHF; ++j) nz |= sh_grad<K>(sm.out + tid * LD, 10 + j) != 0.f;
-      if (nz) a.eta[sm.gid[tid]] += 1u;
+      if (nz) a.eta[sm.gid[tid]] = eta_now + 1u;
     }
   } else {
     constexpr int SU = 8;  // touched slot rows in flight
