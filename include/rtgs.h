@@ -185,6 +185,12 @@ rtgs_status rtgs_project_gaussians(const rtgs_gaussians* g, const rtgs_pose* pos
  * (see rtgs_bins).
  * ------------------------------------------------------------------------------------------- */
 size_t rtgs_bin_workspace_size(int32_t n, const rtgs_camera* cam, uint32_t capacity);
+/* rtgs_check_device_flags: every binning call that overflows its capacity also sets a
+ * sticky device flag; this call synchronises `stream`, reads and clears the flag, and returns
+ * RTGS_ERR_CAPACITY if any binning since the last check overflowed (re-run with a larger capacity),
+ * else RTGS_OK (RTGS_ERR_CUDA on a CUDA error).  Lets a caller enqueue whole iterations (or CUDA
+ * graphs of them) without a host synchronisation and validate once. */
+rtgs_status rtgs_check_device_flags(void* stream);
 rtgs_status rtgs_bin_and_sort(const rtgs_projected* proj, int32_t n, const rtgs_camera* cam,
                               const uint8_t* tile_keep, rtgs_bins* out, void* workspace, size_t workspace_bytes,
                               void* stream);

@@ -11,7 +11,7 @@ from .mapping import (GaussianMap, MappingEngine, ProjectedBuffers, BinBuffers, 
                       project_subset, coverage_rows, stable_cache_build, bin_and_sort_cached,
                       coverage_and_bin_cached, coverage_subset, merge_cached,
                       add_gaussians, insert_params, icp_track, icp_params, pose_device, decode_rgbd,
-                      topk_error_mask, morton_order, gather_rows,
+                      topk_error_mask, morton_order, gather_rows, check_device_flags,
                       make_camera, make_pose, camera_of,
                       hparams, add_params, launch_count, RTGS_RENDER_FULL, RTGS_RENDER_MASKED,
                       RTGS_RENDER_COVERAGE, RTGS_RENDER_COUNT, RTGS_RENDER_DENSE)

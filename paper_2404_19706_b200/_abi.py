@@ -11,6 +11,7 @@ RTGS_RENDER_FULL, RTGS_RENDER_MASKED, RTGS_RENDER_COVERAGE = 0, 1, 2
 RTGS_RENDER_COUNT = 16  # OR-ed into FULL / MASKED: count blended pairs into counts[3]
 RTGS_RENDER_DENSE = 32  # OR-ed into FULL / MASKED: the dense consumer (verification of the span masks)
 STATUS = {0: "RTGS_OK", 1: "RTGS_ERR_INVALID_ARG", 2: "RTGS_ERR_CAPACITY", 3: "RTGS_ERR_CUDA", 4: "RTGS_ERR_WORKSPACE"}
+RTGS_OK, RTGS_ERR_CAPACITY = 0, 2
 
 vp = C.c_void_p
 
@@ -129,6 +130,7 @@ EXPORTS = {
                                     P(Bins), vp, C.c_size_t, vp]),
     "rtgs_topk_workspace_size": (C.c_size_t, [P(Camera)]),
     "rtgs_morton_workspace_size": (C.c_size_t, [C.c_int32]),
+    "rtgs_check_device_flags": (C.c_int, [vp]),
     "rtgs_morton_order": (C.c_int, [vp, vp, C.c_int32, vp, vp, C.c_size_t, vp]),
     "rtgs_gather_rows": (C.c_int, [vp, vp, vp, C.c_int32, C.c_int32, vp]),
     "rtgs_topk_error_mask": (C.c_int, [vp, vp, P(Camera), C.c_double, P(RenderOut), vp, C.c_size_t, vp]),

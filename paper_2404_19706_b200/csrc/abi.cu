@@ -380,6 +380,18 @@ rtgs_status rtgs_topk_error_mask(const float* color_hat, const float* frame_colo
   return finish(launch_topk(color_hat, frame_color, *cam, ratio, *out, workspace, S(stream)));
 }
 
+rtgs_status rtgs_check_device_flags(void* stream) {
+  // synchronises `stream`, then reads and clears the sticky CAPACITY flag
+  cudaStream_t st = S(stream);
+  uint32_t* f = capacity_flag_ptr();
+  if (!f) return RTGS_ERR_CUDA;
+  uint32_t h = 0;
+  if (cudaMemcpyAsync(&h, f, 4, cudaMemcpyDeviceToHost, st) != cudaSuccess) return finish(cudaGetLastError());
+  if (cudaMemsetAsync(f, 0, 4, st) != cudaSuccess) return finish(cudaGetLastError());
+  if (cudaStreamSynchronize(st) != cudaSuccess) return finish(cudaGetLastError());
+  return h ? RTGS_ERR_CAPACITY : RTGS_OK;
+}
+
 const char* rtgs_status_string(rtgs_status s) {
   switch (s) {
     case RTGS_OK: return "RTGS_OK";

@@ -121,6 +121,7 @@ cudaError_t launch_topk(const float* chat, const float* c, const rtgs_camera& ca
 
 // generic device-wide exclusive scan of uint32 (length known on the host; zeros past the live part)
 size_t scan_workspace_size(size_t len);
+uint32_t* capacity_flag_ptr();  // device address of the sticky CAPACITY flag (sort.cu)
 size_t morton_workspace_size(int n);
 cudaError_t launch_morton_order(const float* pos, const uint8_t* flags, int n, uint32_t* perm, void* ws,
                                 cudaStream_t s);

@@ -25,6 +25,17 @@
 
 namespace rtgs {
 
+// sticky CAPACITY flag: set on the device by any binning whose instance count exceeds
+// its capacity (the outputs were truncated: memory-safe but invalid); read and cleared by
+// rtgs_check_device_flags, so the iteration itself stays free of host synchronisation
+__device__ uint32_t g_capacity_flag = 0u;
+
+uint32_t* capacity_flag_ptr() {
+  void* p = nullptr;
+  cudaGetSymbolAddress(&p, g_capacity_flag);
+  return static_cast<uint32_t*>(p);
+}
+
 constexpr int kScanThreads = 256;
 constexpr int kScanItems = 8;
 constexpr int kScanChunk = kScanThreads * kScanItems;  // 2048
@@ -231,7 +242,10 @@ __global__ void __launch_bounds__(1024) k_tile_offsets(const uint32_t* __restric
     carry += tot;
     __syncthreads();  // s_ex reused by the next chunk
   }
-  if (threadIdx.x == 0) *n_inst = carry;
+  if (threadIdx.x == 0) {
+    *n_inst = carry;
+    if (carry > cap) atomicOr(&g_capacity_flag, 1u);
+  }
 }
 
 // STB (the FULL binning that also builds the f3 cache): the key's low word is (gid << 1) | stable,
@@ -590,7 +604,10 @@ __global__ void __launch_bounds__(1024) k_merge_offsets(const uint32_t* __restri
     carry2 += tot2;
     __syncthreads();
   }
-  if (threadIdx.x == 0) *n_inst = carry2;
+  if (threadIdx.x == 0) {
+    *n_inst = carry2;
+    if (carry2 > cap) atomicOr(&g_capacity_flag, 1u);
+  }
 }
 
 // number of elements of the sorted key list k[0..n) that are < key (keys are distinct)

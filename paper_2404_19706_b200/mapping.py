@@ -473,6 +473,12 @@ def icp_track(depth: torch.Tensor, model: RenderBuffers, model_pose: _abi.Pose, 
                                workspace.numel() * workspace.element_size(), _stream(stream)), "rtgs_icp_track")
 
 
+def check_device_flags(stream=None) -> int:
+    """rtgs_check_device_flags: synchronise `stream`, read and clear the sticky CAPACITY flag; returns
+    the status (RTGS_OK or RTGS_ERR_CAPACITY)."""
+    return int(lib().rtgs_check_device_flags(_stream(stream)))
+
+
 def morton_workspace_size(n: int) -> int:
     return int(lib().rtgs_morton_workspace_size(int(n)))
 
@@ -987,6 +993,7 @@ class MappingEngine:
                 truncated = need > self.capacity
                 self.reserve_instances(need * 3 // 2)
                 if truncated:                   # the FULL lists were cut short: redo the frame
+                    check_device_flags()        # (that overflow is handled: clear the sticky flag)
                     self.ingest(c, d, pose, seed=seed, frame_idx=first_frame_idx + i)
             if insert:
                 self.insert(c, d, pose, frame_idx=first_frame_idx + i)
@@ -1000,13 +1007,16 @@ class MappingEngine:
         self.end_window(c, d, pose, frame_idx=first_frame_idx + len(frames) - 1)
         return loss
 
-    def check_capacity(self):
-        """Raise if the last binnings overflowed the instance capacity (their outputs were truncated:
-        memory-safe but invalid).  One host synchronisation."""
-        worst = max(int(self.bins.n_instances.item()), int(self.bins_full.n_instances.item()))
-        if worst > self.capacity:
-            raise RuntimeError(f"instance capacity {self.capacity} < {worst}: construct the MappingEngine with "
-                               f"capacity >= {worst}")
+    def check_capacity(self, stream=None):
+        """Raise if any binning since the last check overflowed its instance capacity (the outputs were
+        truncated: memory-safe but invalid) — the sticky device flag of rtgs_check_device_flags.  One
+        host synchronisation."""
+        st = check_device_flags(stream)
+        if st == _abi.RTGS_ERR_CAPACITY:
+            worst = max(int(self.bins.n_instances.item()), int(self.bins_full.n_instances.item()))
+            raise RuntimeError(f"instance capacity {self.capacity} exceeded (last binnings: {worst}): construct "
+                               f"the MappingEngine with a larger capacity")
+        check(st, "rtgs_check_device_flags")
 
     # --- (e) keyframe global optimisation -------------------------------------------------------
     def _global_state(self, world: int = 1):

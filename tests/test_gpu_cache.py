@@ -195,3 +195,23 @@ def test_cached_all_stable_is_empty(api):
     assert eng.cached(pose) and int(eng.gid_of_slot.numel()) == 0
     c = eng.out.counts.cpu().numpy()
     assert c[0] == 0 and c[2] == 0 and int(eng.bins.n_instances.item()) == 0
+
+
+def test_sticky_capacity_flag(api):
+    """a binning past its capacity sets the sticky device flag; rtgs_check_device_flags
+    reports RTGS_ERR_CAPACITY once and clears it; a binning within capacity leaves it clear."""
+    from paper_2404_19706_b200 import mapping as M
+    cfg = CONFIGS["C1"]
+    scene = make_scene(cfg)
+    R, t = make_pose(cfg)
+    gm = device_map(scene)
+    cam, pose = api.camera_of(cfg), api.make_pose(R, t)
+    n = gm.n
+    assert api.check_device_flags() == 0
+    for cap, expect in ((16, 2), (8 * n, 0)):
+        proj, bins = M.ProjectedBuffers(n), M.BinBuffers(cam, cap)
+        ws = torch.empty(M.bin_workspace_size(n, cam, cap), dtype=torch.uint8, device="cuda")
+        api.project_gaussians(gm, pose, cam, proj)
+        api.bin_and_sort(proj, n, cam, None, bins, ws)
+        assert api.check_device_flags() == expect
+        assert api.check_device_flags() == 0                       # cleared by the read
