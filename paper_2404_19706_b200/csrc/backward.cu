@@ -186,7 +186,12 @@ __global__ void __launch_bounds__(32 * (kBwdWarps + 1)) k_render_bwd(const BwdAr
       if (!(g & kSubBit)) cp_async4(&sm.slot[st][j], slot_of_gid + g);
     };
     auto flush = [](int, int) {};
+#if !RTGS_BWD_DENSE
+    pipe_produce<true, kBwdWarps>(r, a.rec, a.sub_rec, a.sorted_gid, start, end, extra, flush, (float)(tx * kTile),
+                                  (float)(ty * kTile + half * (kBwdWarps / 2) * 4));
+#else
     pipe_produce<true>(r, a.rec, a.sub_rec, a.sorted_gid, start, end, extra, flush);
+#endif
     return;
   }
 
@@ -227,14 +232,11 @@ __global__ void __launch_bounds__(32 * (kBwdWarps + 1)) k_render_bwd(const BwdAr
       const uint32_t sgid = gid0 + (uint32_t)(st * sizeof(r.gid[0]));
       const int cnt = pipe_batch_cnt(true, start, end, b);
       int nq = 0;
+      const uint32_t sbox = pin(smem_u32(&r.boxmask[st][0]));
       for (int g0 = 0; g0 < cnt; g0 += 32) {
         const int j = g0 + lane;
-        bool ov = false;
-        if (j < cnt && (uint32_t)(lo + j) < wlast) {
-          const float4 r0 = lds128(srec + 48u * j);
-          const float2 ext = unpack_ext(__uint_as_float(lds32(srec + 48u * j + 44u)));
-          ov = (r0.x + ext.x >= bx0) && (r0.x - ext.x <= bx1) && (r0.y + ext.y >= by0) && (r0.y - ext.y <= by1);
-        }
+        // the producer's box test (boxmask) and this warp's stop
+        const bool ov = j < cnt && (uint32_t)(lo + j) < wlast && ((lds8(sbox + (uint32_t)j) >> w) & 1u);
         const uint32_t bal = __ballot_sync(0xffffffffu, ov);
         if (ov) sts8(q0 + (uint32_t)(nq + __popc(bal & ((1u << lane) - 1u))), (uint32_t)j);
         nq += __popc(bal);

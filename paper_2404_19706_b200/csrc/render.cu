@@ -225,8 +225,10 @@ __global__ void __launch_bounds__(32 * ((MASKED ? kHalfWarps : kTileWarps) + 1),
   const uint2 rg = a.range[tile];
   const int start = (int)rg.x, end = (int)rg.y;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (w == NW) {  // producer warp
-    pipe_produce(r, a.rec, a.sub_rec, a.sorted_gid, start, end, [](int, int, uint32_t) {}, [](int, int) {});
+  if (w == NW) {  // producer warp (the span path also gets the per-record warp-box masks)
+    const int txp = tile % a.cam.TX, typ = tile / a.cam.TX;
+    pipe_produce<false, SPAN ? NW : 0>(r, a.rec, a.sub_rec, a.sorted_gid, start, end, [](int, int, uint32_t) {},
+                                       [](int, int) {}, (float)(txp * kTile), (float)(typ * kTile + half * (NW / 2) * 4));
     return;
   }
   const int tx = tile % a.cam.TX, ty = tile / a.cam.TX;
@@ -260,14 +262,10 @@ __global__ void __launch_bounds__(32 * ((MASKED ? kHalfWarps : kTileWarps) + 1),
         const int cnt = min(kPipeBatch, n - b * kPipeBatch);
         // 1. bbox survivors of the stage, in list order
         int nq = 0;
+        const uint32_t sbox = pin(smem_u32(&r.boxmask[st][0]));
         for (int g0 = 0; g0 < cnt; g0 += 32) {
           const int j = g0 + lane;
-          bool ov = false;
-          if (j < cnt) {
-            const float4 r0 = lds128(srec + 48u * j);
-            const float2 ext = unpack_ext(__uint_as_float(lds32(srec + 48u * j + 44u)));
-            ov = (r0.x + ext.x >= bx0) && (r0.x - ext.x <= bx1) && (r0.y + ext.y >= by0) && (r0.y - ext.y <= by1);
-          }
+          const bool ov = j < cnt && ((lds8(sbox + (uint32_t)j) >> w) & 1u);  // the producer's box test
           const uint32_t bal = __ballot_sync(0xffffffffu, ov);
           if (ov) sts8(q0 + (uint32_t)(nq + __popc(bal & ((1u << lane) - 1u))), (uint32_t)j);
           nq += __popc(bal);

@@ -25,6 +25,7 @@ constexpr int kHalfWarps = 4;
 struct PipeRing {
   float4 rec[kPipeStages][kPipeBatch][3];  // first 48 B of each record: mu hi/lo, conic', log2 alpha, rgb, ext
   uint32_t gid[kPipeStages][kPipeBatch];
+  uint8_t boxmask[kPipeStages][kPipeBatch];  // bit w: the record's support box overlaps warp w's block
   uint64_t full[kPipeStages];
   uint64_t empty[kPipeStages];
   int alive;                                // consumer warps not yet terminated
@@ -90,11 +91,15 @@ __device__ __forceinline__ int pipe_batch_cnt(bool rev, int start, int end, int 
   return rev ? (end - b * kPipeBatch) - max(start, end - (b + 1) * kPipeBatch)
              : min(kPipeBatch, end - start - b * kPipeBatch);
 }
-template <bool REV = false, typename Extra, typename Flush>
+// NBOX > 0: once a stage's copies have landed, the producer also writes boxmask: for each record
+// the NBOX consumer warps' 8x4 blocks (warp w at (bx, by) + ((w & 1) * 8, (w >> 1) * 4)) its support
+// box overlaps -- the test every consumer warp made on its own per record before (the same float
+// comparisons, so the same decisions), now once per record instead of once per (record, warp)
+template <bool REV = false, int NBOX = 0, typename Extra, typename Flush>
 __device__ __forceinline__ void pipe_produce(PipeRing& r, const float4* __restrict__ rec,
                                              const float4* __restrict__ sub_rec,
                                              const uint32_t* __restrict__ sorted_gid, int start, int end,
-                                             Extra extra, Flush flush) {
+                                             Extra extra, Flush flush, float bx = 0.f, float by = 0.f) {
   const int lane = threadIdx.x & 31;
   const int n = end - start;
   const int nb = n > 0 ? (n + kPipeBatch - 1) / kPipeBatch : 0;
@@ -127,8 +132,31 @@ __device__ __forceinline__ void pipe_produce(PipeRing& r, const float4* __restri
           extra(st, j, g[q]);
         }
       }
+      if constexpr (NBOX > 0) {
+        asm volatile("cp.async.wait_all;\n" ::: "memory");  // this stage's records have landed
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+          const int j = lane + 32 * q;
+          if (j < cnt) {
+            const float4 r0 = r.rec[st][j][0];
+            const float2 ext = unpack_ext(r.rec[st][j][2].w);
+            uint32_t m = 0u;
+#pragma unroll
+            for (int w = 0; w < NBOX; ++w) {
+              const float bx0 = bx + (float)((w & 1) * 8), bx1 = bx0 + 7.f;
+              const float by0 = by + (float)((w >> 1) * 4), by1 = by0 + 3.f;
+              const bool ov = (r0.x + ext.x >= bx0) && (r0.x - ext.x <= bx1) && (r0.y + ext.y >= by0) &&
+                              (r0.y - ext.y <= by1);
+              m |= ov ? (1u << w) : 0u;
+            }
+            r.boxmask[st][j] = (uint8_t)m;
+          }
+        }
+      }
     }
-    cp_async_mbar_arrive(&r.full[st]);
+    if constexpr (NBOX > 0) mbar_arrive(&r.full[st]);  // (copies waited for: a plain arrival)
+    else cp_async_mbar_arrive(&r.full[st]);
   }
   // the last stages are flushed once every consumer warp has released them
   for (int b = max(0, nb - kPipeStages); b < nb; ++b) {
