@@ -14,8 +14,14 @@
 
 namespace rtgs {
 
-constexpr int kPipeStages = 4;
-constexpr int kPipeBatch = 128;
+#ifndef RTGS_PIPE_STAGES
+#define RTGS_PIPE_STAGES 3
+#endif
+#ifndef RTGS_PIPE_BATCH
+#define RTGS_PIPE_BATCH 256
+#endif
+constexpr int kPipeStages = RTGS_PIPE_STAGES;  // (swept in round 2: 4 x 128 vs 3 x 256: 3 x 256 kept)
+constexpr int kPipeBatch = RTGS_PIPE_BATCH;    // <= 256: stage indices are bytes
 // consumer warps per CTA: 8 = a whole 16x16 tile (FULL render: thousands of tiles), 4 = half a tile
 // (MASKED render and backward: only the kept tiles, so half-tile CTAs double the parallelism and
 // even out the per-SM load)
