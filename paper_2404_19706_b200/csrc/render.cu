@@ -204,7 +204,7 @@ cudaError_t launch_tile_coverage(const uint2* srange, const unsigned long long* 
 
 // SPAN: the span-mask consumer (default); false = the dense consumer (RTGS_RENDER_DENSE, verification)
 #ifndef RTGS_SPAN_MINB
-#define RTGS_SPAN_MINB 5
+#define RTGS_SPAN_MINB 4
 #endif
 template <bool MASKED, bool COUNT, bool LAST = true, bool SPAN = true>
 __global__ void __launch_bounds__(32 * ((MASKED ? kHalfWarps : kTileWarps) + 1),
@@ -271,23 +271,34 @@ __global__ void __launch_bounds__(32 * ((MASKED ? kHalfWarps : kTileWarps) + 1),
           nq += __popc(bal);
         }
         __syncwarp();
-        // 2. rounds of <= 32 survivors: support masks, transpose, per-lane walk of the own bits
-        for (int q = 0; q < nq; q += 32) {
-          uint32_t pm = 0u;
+        // 2. rounds of <= 64 survivors: support masks, two transposes, per-lane walk of the own bits
+        //    (bits of word 0 = survivors q..q+31 first, then word 1: list order)
+        for (int q = 0; q < nq; q += 64) {
+          uint32_t pm0 = 0u, pm1 = 0u;
           if (q + lane < nq) {
             const uint32_t ra = srec + 48u * lds8(q0 + (uint32_t)(q + lane));
-            pm = support_mask(lds128(ra), lds128(ra + 16u), bx0, by0);
+            pm0 = support_mask(lds128(ra), lds128(ra + 16u), bx0, by0);
           }
-          uint32_t lm = warp_transpose32(pm, (uint32_t)lane);
-          if (done) lm = 0u;
+          if (q + 32 + lane < nq) {
+            const uint32_t ra = srec + 48u * lds8(q0 + (uint32_t)(q + 32 + lane));
+            pm1 = support_mask(lds128(ra), lds128(ra + 16u), bx0, by0);
+          }
+          uint32_t lm0 = warp_transpose32(pm0, (uint32_t)lane);
+          uint32_t lm1 = q + 32 < nq ? warp_transpose32(pm1, (uint32_t)lane) : 0u;  // (nq warp-uniform)
+          if (done) lm0 = lm1 = 0u;
           // warp-uniform trip count (the largest per-lane bit count): the body is predicated, not
           // a divergent branch, so no reconvergence bookkeeping per iteration
-          const int trips = __reduce_max_sync(0xffffffffu, (uint32_t)__popc(lm));
+          const int trips = __reduce_max_sync(0xffffffffu, (uint32_t)(__popc(lm0) + __popc(lm1)));
           for (int it = 0; it < trips; ++it) {
-            const bool has = lm != 0u;
-            const int jj = __ffs(lm) - 1;  // -1 without bits: survivor q is read and discarded
-            lm &= lm - 1u;
-            const uint32_t idx = lds8(q0 + (uint32_t)(q + max(jj, 0)));
+            const bool w0 = lm0 != 0u;
+            const uint32_t cur = w0 ? lm0 : lm1;
+            const bool has = cur != 0u;
+            // without bits: survivor q (always a valid record: a stale slot may hold NaN colour)
+            const int jj = has ? (w0 ? 0 : 32) + __ffs(cur) - 1 : 0;
+            const uint32_t nxt = cur & (cur - 1u);
+            lm0 = w0 ? nxt : lm0;
+            lm1 = w0 ? lm1 : nxt;
+            const uint32_t idx = lds8(q0 + (uint32_t)(q + jj));
             const uint32_t ra = srec + 48u * idx;
             const float4 r0 = lds128(ra), r1 = lds128(ra + 16u), r2 = lds128(ra + 32u);
             PairEval e;
@@ -297,7 +308,8 @@ __global__ void __launch_bounds__(32 * ((MASKED ? kHalfWarps : kTileWarps) + 1),
             const float test = __fmul_rn(T, __fsub_rn(1.f, e.f));
             const bool term = ok && (test < kTMin);
             done = done || term;
-            lm = term ? 0u : lm;
+            lm0 = term ? 0u : lm0;
+            lm1 = term ? 0u : lm1;
             ok = ok && !term;
             const float wgt = ok ? __fmul_rn(e.f, T) : 0.f;
             cr = __fmaf_rn(r2.x, wgt, cr);
