@@ -203,6 +203,15 @@ cudaError_t launch_tile_coverage(const uint2* srange, const unsigned long long* 
 // (warp_transpose32 and support_mask: tilepipe.cuh, shared with the backward)
 
 // SPAN: the span-mask consumer (default); false = the dense consumer (RTGS_RENDER_DENSE, verification)
+#ifdef RTGS_RENDER_STATS
+// experiment builds only (scripts/build_variant.py -DRTGS_RENDER_STATS): work counters of the span walk
+// [0] warp-batches, [1] survivors, [2] rounds, [3] trips, [4] lane-pairs walked (has), [5] blends,
+// [6] records seen, [7] rounds' survivor slots used (sum of min(64, nq - q))
+__device__ unsigned long long g_rstats[8];
+#define RSTAT(i, v) do { if (lane == 0) atomicAdd(&g_rstats[i], (unsigned long long)(v)); } while (0)  // v: no warp ops
+#else
+#define RSTAT(i, v) do { } while (0)
+#endif
 #ifndef RTGS_SPAN_MINB
 #define RTGS_SPAN_MINB 4
 #endif
@@ -246,7 +255,10 @@ __global__ void __launch_bounds__(32 * ((MASKED ? kHalfWarps : kTileWarps) + 1),
 
   const uint32_t rec0 = pin(smem_u32(&r.rec[0][0][0]));
   float T = 1.f, cr = 0.f, cg = 0.f, cb = 0.f;
-  int hitpos = -1;  // sorted-list position of the depth hit (the entry is fetched after the loop)
+  // sorted-list position of the depth hit (the entry is fetched after the loop); positions grow along
+  // the walk, so "the first hit" is the minimum over hits (kNoHit: none)
+  constexpr uint32_t kNoHit = 0xFFFFFFFFu;
+  uint32_t hitpos = kNoHit;
   uint32_t last = (uint32_t)start;
   uint32_t nblend = 0;  // blended (pixel, Gaussian) pairs of this lane (-> counts[3])
   bool wdone = __all_sync(0xffffffffu, done);
@@ -271,54 +283,78 @@ __global__ void __launch_bounds__(32 * ((MASKED ? kHalfWarps : kTileWarps) + 1),
           nq += __popc(bal);
         }
         __syncwarp();
-        // 2. rounds of <= 64 survivors: support masks, two transposes, per-lane walk of the own bits
-        //    (bits of word 0 = survivors q..q+31 first, then word 1: list order)
+        RSTAT(0, 1);
+        RSTAT(1, nq);
+        RSTAT(6, cnt);
+        // 2. rounds of <= 64 survivors: support masks, two transposes, per-lane walk of the own bits.
+        //    Lane l computes the masks of survivors q + 31 - l and q + 63 - l, so after the transposes
+        //    survivor q + j sits at bit 31 - j of word 0 (q + 32 + j: of word 1): list order is
+        //    leading-zero order, and the next survivor of a lane is one FLO away (no bit reverse).
         for (int q = 0; q < nq; q += 64) {
           uint32_t pm0 = 0u, pm1 = 0u;
-          if (q + lane < nq) {
-            const uint32_t ra = srec + 48u * lds8(q0 + (uint32_t)(q + lane));
+          if (q + 31 - lane < nq) {
+            const uint32_t ra = srec + 48u * lds8(q0 + (uint32_t)(q + 31 - lane));
             pm0 = support_mask(lds128(ra), lds128(ra + 16u), bx0, by0);
           }
-          if (q + 32 + lane < nq) {
-            const uint32_t ra = srec + 48u * lds8(q0 + (uint32_t)(q + 32 + lane));
+          if (q + 63 - lane < nq) {
+            const uint32_t ra = srec + 48u * lds8(q0 + (uint32_t)(q + 63 - lane));
             pm1 = support_mask(lds128(ra), lds128(ra + 16u), bx0, by0);
           }
           uint32_t lm0 = warp_transpose32(pm0, (uint32_t)lane);
           uint32_t lm1 = q + 32 < nq ? warp_transpose32(pm1, (uint32_t)lane) : 0u;  // (nq warp-uniform)
           if (done) lm0 = lm1 = 0u;
           // warp-uniform trip count (the largest per-lane bit count): the body is predicated, not
-          // a divergent branch, so no reconvergence bookkeeping per iteration
+          // a divergent branch, so no reconvergence bookkeeping per iteration.  A lane that terminates
+          // keeps stepping through its bits with every blend predicated off (done).
           const int trips = __reduce_max_sync(0xffffffffu, (uint32_t)(__popc(lm0) + __popc(lm1)));
+#ifdef RTGS_RENDER_STATS
+          RSTAT(2, 1);
+          RSTAT(3, trips);
+          RSTAT(7, min(64, nq - q));
+          const uint32_t npairs = __reduce_add_sync(0xffffffffu, (uint32_t)(__popc(lm0) + __popc(lm1)));
+          RSTAT(4, npairs);
+          uint32_t nbl = 0;
+#endif
+          const uint32_t qa0 = q0 + (uint32_t)q + 31u, qa1 = qa0 + 32u;  // survivor at bit b: qa - b
           for (int it = 0; it < trips; ++it) {
-            const bool w0 = lm0 != 0u;
+            const bool w0 = lm0 != 0u || lm1 == 0u;  // (no bits left: word 0)
             const uint32_t cur = w0 ? lm0 : lm1;
             const bool has = cur != 0u;
-            // without bits: survivor q (always a valid record: a stale slot may hold NaN colour)
-            const int jj = has ? (w0 ? 0 : 32) + __ffs(cur) - 1 : 0;
-            const uint32_t nxt = cur & (cur - 1u);
+            // b = the highest set bit (0xFFFFFFFF without bits: (b & 31) = 31 reads survivor q, a valid
+            // record -- a stale slot may hold NaN colour -- and the pair is discarded)
+            uint32_t b, top;
+            asm("bfind.u32 %0, %1;" : "=r"(b) : "r"(cur));
+            asm("shl.b32 %0, %1, %2;" : "=r"(top) : "r"(1u), "r"(b));  // 0 for b = 0xFFFFFFFF (clamped)
+            const uint32_t nxt = cur & ~top;
             lm0 = w0 ? nxt : lm0;
             lm1 = w0 ? lm1 : nxt;
-            const uint32_t idx = lds8(q0 + (uint32_t)(q + jj));
+            const uint32_t idx = lds8((w0 ? qa0 : qa1) - (b & 31u));
             const uint32_t ra = srec + 48u * idx;
             const float4 r0 = lds128(ra), r1 = lds128(ra + 16u), r2 = lds128(ra + 32u);
             PairEval e;
-            bool ok = eval_pair(r0, r1, fpx, fpy, e) && has;
+            bool ok = eval_pair(r0, r1, fpx, fpy, e) && has && !done;
+            const uint32_t pos = pbase - 1u + idx;  // sorted-list position of the pair
             // R9: the first f > e^-0.5, tested before termination
-            hitpos = (ok && hitpos < 0 && e.f > kDeltaAlpha) ? (int)(pbase - 1u + idx) : hitpos;
+            hitpos = min(hitpos, (ok && e.f > kDeltaAlpha) ? pos : kNoHit);
             const float test = __fmul_rn(T, __fsub_rn(1.f, e.f));
             const bool term = ok && (test < kTMin);
             done = done || term;
-            lm0 = term ? 0u : lm0;
-            lm1 = term ? 0u : lm1;
             ok = ok && !term;
             const float wgt = ok ? __fmul_rn(e.f, T) : 0.f;
             cr = __fmaf_rn(r2.x, wgt, cr);
             cg = __fmaf_rn(r2.y, wgt, cg);
             cb = __fmaf_rn(r2.z, wgt, cb);
             T = ok ? test : T;
-            if (LAST) last = ok ? pbase + idx : last;
+            if (LAST) last = ok ? pos + 1u : last;
             if (COUNT) nblend += ok ? 1u : 0u;
+#ifdef RTGS_RENDER_STATS
+            nbl += ok ? 1u : 0u;
+#endif
           }
+#ifdef RTGS_RENDER_STATS
+          const uint32_t nbw = __reduce_add_sync(0xffffffffu, nbl);
+          RSTAT(5, nbw);
+#endif
           if (__all_sync(0xffffffffu, done)) {
             wdone = true;
             if (lane == 0) atomicSub(&r.alive, 1);
@@ -355,7 +391,7 @@ __global__ void __launch_bounds__(32 * ((MASKED ? kHalfWarps : kTileWarps) + 1),
             PairEval e;
             bool ok = eval_pair(r0, r1, fpx, fpy, e) && !done;
             // R9: the first f > e^-0.5, tested before termination (position only: no load in the loop)
-            hitpos = (ok && hitpos < 0 && e.f > kDeltaAlpha) ? (int)(pbase - 1u) + idx : hitpos;
+            hitpos = min(hitpos, (ok && e.f > kDeltaAlpha) ? pbase - 1u + (uint32_t)idx : kNoHit);
             const float test = __fmul_rn(T, __fsub_rn(1.f, e.f));
             const bool term = ok && (test < kTMin);
             done = done || term;
@@ -393,7 +429,7 @@ __global__ void __launch_bounds__(32 * ((MASKED ? kHalfWarps : kTileWarps) + 1),
   if (LAST) a.n_contrib[lin] = last;
   float D = -1.f, N0 = 0.f, N1 = 0.f, N2 = 0.f;
   int32_t gid = -1;
-  const uint32_t hit = hitpos >= 0 ? a.sorted_gid[hitpos] : 0xFFFFFFFFu;  // list entry of the hit
+  const uint32_t hit = hitpos != kNoHit ? a.sorted_gid[hitpos] : 0xFFFFFFFFu;  // list entry of the hit
   if (hit != 0xFFFFFFFFu) {
     const bool sub = hit & kSubBit;
     const uint32_t row = hit & ~kSubBit;
@@ -481,3 +517,15 @@ cudaError_t launch_render(const rtgs_projected& proj, const rtgs_bins& bins, con
 }
 
 }  // namespace rtgs
+
+#ifdef RTGS_RENDER_STATS
+extern "C" int rtgs_debug_render_stats(unsigned long long* out, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, rtgs::g_rstats, sizeof(rtgs::g_rstats));
+  if (reset) {
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(rtgs::g_rstats, z, sizeof(z));
+  }
+  return (int)cudaGetLastError();
+}
+#endif
