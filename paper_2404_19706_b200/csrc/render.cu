@@ -213,13 +213,13 @@ __device__ unsigned long long g_rstats[8];
 #define RSTAT(i, v) do { } while (0)
 #endif
 #ifndef RTGS_SPAN_MINB
-#define RTGS_SPAN_MINB 4
+#define RTGS_SPAN_MINB 5
 #endif
 template <bool MASKED, bool COUNT, bool LAST = true, bool SPAN = true>
 __global__ void __launch_bounds__(32 * ((MASKED ? kHalfWarps : kTileWarps) + 1),
                                   SPAN && !MASKED ? RTGS_SPAN_MINB : 1) k_render_fwd(const FwdArgs a) {
   constexpr int NW = MASKED ? kHalfWarps : kTileWarps;  // MASKED: one CTA per half of a kept tile
-  __shared__ PipeRing r;  // static: stage addresses fold into immediates
+  __shared__ PipeRingT<false> r;  // static: stage addresses fold into immediates
   __shared__ uint8_t survq[SPAN ? NW : 1][kPipeBatch];  // per warp: the stage's bbox survivors, in order
   int tile, half = 0;
   if (MASKED) {
@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(32 * ((MASKED ? kHalfWarps : kTileWarps) + 1),
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (w == NW) {  // producer warp (the span path also gets the per-record warp-box masks)
     const int txp = tile % a.cam.TX, typ = tile / a.cam.TX;
-    pipe_produce<false, SPAN ? NW : 0>(r, a.rec, a.sub_rec, a.sorted_gid, start, end, [](int, int, uint32_t) {},
+    pipe_produce<false, SPAN ? NW : 0, false>(r, a.rec, a.sub_rec, a.sorted_gid, start, end, [](int, int, uint32_t) {},
                                        [](int, int) {}, (float)(txp * kTile), (float)(typ * kTile + half * (NW / 2) * 4));
     return;
   }

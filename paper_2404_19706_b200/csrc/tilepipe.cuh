@@ -28,17 +28,21 @@ constexpr int kPipeBatch = RTGS_PIPE_BATCH;    // <= 256: stage indices are byte
 constexpr int kTileWarps = 8;
 constexpr int kHalfWarps = 4;
 
-struct PipeRing {
+// GID: the ring also holds each record's list entry (the backward's gradient targets); the forward
+// fetches only its hit's entry, after the walk
+template <bool GID>
+struct PipeRingT {
   float4 rec[kPipeStages][kPipeBatch][3];  // first 48 B of each record: mu hi/lo, conic', log2 alpha, rgb, ext
-  uint32_t gid[kPipeStages][kPipeBatch];
+  uint32_t gid[GID ? kPipeStages : 1][GID ? kPipeBatch : 1];
   uint8_t boxmask[kPipeStages][kPipeBatch];  // bit w: the record's support box overlaps warp w's block
   uint64_t full[kPipeStages];
   uint64_t empty[kPipeStages];
   int alive;                                // consumer warps not yet terminated
 };
+using PipeRing = PipeRingT<true>;
 
-template <int NW>
-__device__ __forceinline__ void pipe_init(PipeRing& r) {
+template <int NW, typename Ring>
+__device__ __forceinline__ void pipe_init(Ring& r) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < kPipeStages; ++s) {
       mbar_init(&r.full[s], 32);
@@ -101,8 +105,8 @@ __device__ __forceinline__ int pipe_batch_cnt(bool rev, int start, int end, int 
 // the NBOX consumer warps' 8x4 blocks (warp w at (bx, by) + ((w & 1) * 8, (w >> 1) * 4)) its support
 // box overlaps -- the test every consumer warp made on its own per record before (the same float
 // comparisons, so the same decisions), now once per record instead of once per (record, warp)
-template <bool REV = false, int NBOX = 0, typename Extra, typename Flush>
-__device__ __forceinline__ void pipe_produce(PipeRing& r, const float4* __restrict__ rec,
+template <bool REV = false, int NBOX = 0, bool GID = true, typename Extra, typename Flush>
+__device__ __forceinline__ void pipe_produce(PipeRingT<GID>& r, const float4* __restrict__ rec,
                                              const float4* __restrict__ sub_rec,
                                              const uint32_t* __restrict__ sorted_gid, int start, int end,
                                              Extra extra, Flush flush, float bx = 0.f, float by = 0.f) {
@@ -130,7 +134,7 @@ __device__ __forceinline__ void pipe_produce(PipeRing& r, const float4* __restri
       for (int q = 0; q < PER; ++q) {
         const int j = lane + 32 * q;
         if (j < cnt) {
-          cp_async4(&r.gid[st][j], sorted_gid + lo + j);
+          if constexpr (GID) cp_async4(&r.gid[st][j], sorted_gid + lo + j);
           const float4* src = entry_rec(rec, sub_rec, g[q]);
           cp_async16(&r.rec[st][j][0], src);
           cp_async16(&r.rec[st][j][1], src + 1);
