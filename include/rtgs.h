@@ -32,7 +32,7 @@ extern "C" {
 typedef enum {
   RTGS_OK = 0,
   RTGS_ERR_INVALID_ARG = 1, /* null / mis-sized / misaligned argument, bad mode, non-finite pose  */
-  RTGS_ERR_CAPACITY = 2,    /* reserved: instance overflow is reported through n_instances        */
+  RTGS_ERR_CAPACITY = 2,    /* a binning exceeded its capacity (sticky flag, rtgs_check_device_flags) */
   RTGS_ERR_CUDA = 3,        /* a kernel launch failed; see rtgs_last_cuda_error()                 */
   RTGS_ERR_WORKSPACE = 4    /* workspace pointer null or smaller than the *_workspace_size query  */
 } rtgs_status;

@@ -842,11 +842,10 @@ __global__ void __launch_bounds__(kPBS, PBMinBlocks<K>::value) k_project_bwd(con
       float* dst = c < 3 ? a.wpos + 3 * g + c : (c < 6 ? a.wlog_scale + 3 * g + (c - 3) : a.wrot + 4 * g + (c - 6));
       *dst = sm.par[ls * 13 + c];
     }
-    if (tid < ns) {  // eta += 1 once per slot with a non-zero SH gradient (R20)
-      bool nz = false;
-#pragma unroll 8
-      for (int j = 0; j < SHF; ++j) nz |= sh_grad<K>(sm.out + tid * LD, 10 + j) != 0.f;
-      if (nz) a.eta[sm.gid[tid]] = eta_now + 1u;
+    if (tid < ns) {  // eta += 1 once per slot with a non-zero SH gradient (R20): the gradients are
+      // Y_k gc_c with Y_0 = C0 != 0, so some is non-zero iff some gc_c is (as in real arithmetic)
+      const float* row = sm.out + tid * LD;
+      if (row[10 + K] != 0.f || row[10 + K + 1] != 0.f || row[10 + K + 2] != 0.f) a.eta[sm.gid[tid]] = eta_now + 1u;
     }
   } else {
     constexpr int SU = 8;  // touched slot rows in flight

@@ -359,6 +359,68 @@ __device__ __forceinline__ void cta_radix_sort(unsigned long long* A, unsigned l
   *out = A;
 }
 
+// MSD bucket sort of a tile list held in shared memory (the default for lists up to kSortCap).
+// The keys are (zkey << 32 | low) and their unique ascending order is the (zkey, gid) order.  One
+// pass distributes them over kBuckets buckets by the top bits of (zkey - zmin): each key takes its
+// rank inside its bucket from a shared-memory atomic (an arbitrary order -- MSD needs no stability),
+// and after a scan of the bucket counts lands at start[bucket] + rank.  Then every key moves to its
+// bucket's start + the number of smaller keys in its bucket (a tile of ~700 keys spreads ~0.35 keys
+// per bucket; crowded buckets are ranked by as many threads as they hold keys).  So the result is
+// the same unique order as the LSD path, for a fraction of its instructions.  Returns false (nothing
+// written) when some bucket holds more than kMaxBucket keys (depths piled up in one bucket range):
+// the caller then runs the LSD sort.
+constexpr int kBuckets = 2048;
+constexpr int kBPT = kBuckets / kSortThreads;  // buckets per thread
+constexpr int kMaxBucket = 96;
+static_assert(kBuckets * 4 <= kSortWarps * 256 * 4, "the bucket counters reuse wcnt");
+__device__ __forceinline__ bool msd_bucket_sort(unsigned long long* A, unsigned long long* B, uint32_t* rk, int n,
+                                                uint32_t z0, int zbits, uint32_t* cnt, uint32_t* scan_sh) {
+  const int tid = threadIdx.x;
+  const int sh = max(0, zbits - 11);  // top 11 bits of the depth range (kBuckets = 2^11)
+#pragma unroll
+  for (int j = 0; j < kBPT; ++j) cnt[tid * kBPT + j] = 0u;
+  __syncthreads();
+  for (int i = tid; i < n; i += kSortThreads) {
+    const uint32_t d = ((uint32_t)(A[i] >> 32) - z0) >> sh;
+    rk[i] = atomicAdd(&cnt[d], 1u);
+  }
+  __syncthreads();
+  uint32_t c[kBPT], tsum = 0, cmax = 0;
+#pragma unroll
+  for (int j = 0; j < kBPT; ++j) {
+    c[j] = cnt[tid * kBPT + j];
+    tsum += c[j];
+    cmax = max(cmax, c[j]);
+  }
+  if (__syncthreads_or(cmax > (uint32_t)kMaxBucket)) return false;
+  uint32_t tot;
+  uint32_t st = block_excl_scan(tsum, scan_sh, &tot);
+#pragma unroll
+  for (int j = 0; j < kBPT; ++j) {
+    cnt[tid * kBPT + j] = st;  // bucket start
+    st += c[j];
+  }
+  __syncthreads();
+  for (int i = tid; i < n; i += kSortThreads) {
+    const unsigned long long k = A[i];
+    const uint32_t d = ((uint32_t)(k >> 32) - z0) >> sh;
+    B[cnt[d] + rk[i]] = k;
+  }
+  __syncthreads();
+  // final place of each key: its bucket's start + the number of smaller keys in the bucket (keys are
+  // unique: the low word holds the gid), one thread per key so a crowded bucket is ranked in parallel
+  for (int i = tid; i < n; i += kSortThreads) {
+    const unsigned long long k = B[i];
+    const uint32_t d = ((uint32_t)(k >> 32) - z0) >> sh;
+    const int lo = (int)cnt[d], hi = d + 1 < (uint32_t)kBuckets ? (int)cnt[d + 1] : n;
+    int r = 0;
+    for (int p = lo; p < hi; ++p) r += B[p] < k ? 1 : 0;
+    A[lo + r] = k;
+  }
+  __syncthreads();
+  return true;
+}
+
 // one tile's list: load, compress, depth-radix-sort, tie fix-up, write gids
 __device__ __forceinline__ void sort_tile(const unsigned long long* __restrict__ seg, unsigned long long* A,
                                           unsigned long long* B, uint32_t* rk, int n, int gid_bits,
@@ -381,6 +443,10 @@ __device__ __forceinline__ void sort_tile(const unsigned long long* __restrict__
   const uint32_t z0 = s_zmm[0];
   const uint32_t zr = s_zmm[1] - z0;
   const int zbits = zr ? 32 - __clz(zr) : 0;
+  if (copy_in && msd_bucket_sort(A, B, rk, n, z0, zbits, &wcnt[0][0], scan_sh)) {
+    for (int i = tid; i < n; i += kSortThreads) out_gid[i] = (uint32_t)(A[i] & 0xFFFFFFFFull);
+    return;
+  }
   // compress: key' = ((z - zmin) << gid_bits) | gid  (order-preserving for (z, gid))
   for (int i = tid; i < n; i += kSortThreads) {
     const unsigned long long k = A[i];

@@ -68,9 +68,9 @@ def test_project_parity(api, name):
     np.testing.assert_array_equal(tt[~v], 0)
 
 
-def _synthetic_projected(api, n, tx, ty, seed):
+def _synthetic_projected(api, n, tx, ty, seed, levels=(0.5, 1.0, 1.25, 2.0, 3.5), jitter=3):
     rng = np.random.default_rng(seed)
-    z = rng.choice(np.float32([0.5, 1.0, 1.25, 2.0, 3.5]), size=n) + rng.integers(0, 3, n).astype(np.float32) * np.float32(1e-3)
+    z = rng.choice(np.float32(levels), size=n) + rng.integers(0, jitter, n).astype(np.float32) * np.float32(1e-3)
     x0 = rng.integers(0, tx * 16, n)
     y0 = rng.integers(0, ty * 16, n)
     w = rng.geometric(0.15, n)
@@ -112,6 +112,30 @@ def test_bin_and_sort_bitexact(api, n, w, h, keep_frac):
     np.testing.assert_array_equal(bins.tile_range.cpu().numpy(), rng)
 
 
+@pytest.mark.parametrize("n,w,h,levels,jitter", [
+    (3000, 64, 48, (1.0, 2.0), 1),         # ~400 keys per tile on 2 depths: buckets overflow -> LSD path
+    (6000, 64, 48, (1.0,), 1),             # all keys of a tile tied on depth: gid order only
+    (3000, 64, 48, tuple(np.linspace(0.5, 8.0, 400)), 50),  # ~400 keys per tile, spread: MSD path
+    (12000, 32, 32, (1.0, 1.5), 2)])       # > kSortCap keys per tile: global-memory path
+def test_bin_and_sort_bitexact_sort_paths(api, n, w, h, levels, jitter):
+    """The tile sort's three paths (shared-memory MSD buckets; the LSD radix sort when a bucket piles
+    up; global memory for long lists) against the oracle's (tile, depth, gid) order."""
+    cam = api.make_camera(100, 100, w / 2, h / 2, w, h)
+    tx, ty = (w + 15) // 16, (h + 15) // 16
+    proj, z, tile_rect = _synthetic_projected(api, n, tx, ty, 5 + n, levels, jitter)
+    cap = 1 << 20
+    bins = api.BinBuffers(cam, cap)
+    from paper_2404_19706_b200 import mapping as M
+    ws = torch.empty(M.bin_workspace_size(n, cam, cap), dtype=torch.uint8, device="cuda")
+    api.bin_and_sort(proj, n, cam, None, bins, ws)
+    torch.cuda.synchronize()
+    tid, gid, rng = OB.instances_fast(z, tile_rect, tx, ty)
+    I = int(bins.n_instances.item())
+    assert I == len(gid)
+    np.testing.assert_array_equal(bins.sorted_gid[:I].cpu().numpy(), gid)
+    np.testing.assert_array_equal(bins.tile_range.cpu().numpy(), rng)
+
+
 def test_bin_overflow_reports_count(api):
     w, h, n = 200, 136, 3000
     cam = api.make_camera(100, 100, w / 2, h / 2, w, h)
@@ -124,6 +148,7 @@ def test_bin_overflow_reports_count(api):
     torch.cuda.synchronize()
     _, gid, _ = OB.instances_fast(z, tile_rect, 13, 9)
     assert int(bins.n_instances.item()) == len(gid) > cap
+    assert api.check_device_flags() == 2  # RTGS_ERR_CAPACITY, and cleared
 
 
 @pytest.mark.parametrize("name", ["C1", "C1b", "T1", "T2"])
