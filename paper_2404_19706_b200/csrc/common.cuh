@@ -184,11 +184,14 @@ __device__ __forceinline__ void tile_count_agg(uint32_t* cnt, int nt, int w, int
                                                const uint8_t* keep) {
   const int lane = threadIdx.x & 31;
   const int ntmax = __reduce_max_sync(0xffffffffu, (uint32_t)nt);
+  int cx = 0, tt = ty0 * TX + tx0;  // the lane's q-th tile, stepped row-major (no division by w)
   for (int q = 0; q < ntmax; ++q) {
-    int t = q < nt ? (ty0 + q / w) * TX + tx0 + q % w : -1;
+    int t = q < nt ? tt : -1;
     if (t >= 0 && keep && !keep[t]) t = -1;
     const uint32_t peers = __match_any_sync(0xffffffffu, (uint32_t)t);
     if (t >= 0 && lane == __ffs(peers) - 1) atomicAdd(&cnt[t], (uint32_t)__popc(peers));
+    ++tt;
+    if (++cx == w) { cx = 0; tt += TX - w; }
   }
 }
 

@@ -6,7 +6,7 @@
 // shared memory:
 //   1. k_tile_count   per Gaussian, per kept tile of its rect: atomicAdd(tile_count[t])
 //   2. k_tile_offsets one CTA: exclusive scan of the counts -> tile_range, n_instances
-//   3. k_emit         per Gaussian, per kept tile: slot = start[t] + atomicAdd(cursor[t]) and store
+//   3. k_emit         per Gaussian, per kept tile: slot = atomicAdd(cursor[t]) (cursor = the tile start) and store
 //                     the 64-bit pair (zkey << 32 | gid)   (order inside a tile still arbitrary)
 //   4. k_tile_sort    one CTA per tile: key' = ((zkey - zmin) << gid_bits) | gid, stable LSD radix
 //                     sort with 8-bit digits (warp match_any ranking) on the depth bits that vary
@@ -150,7 +150,9 @@ __device__ __forceinline__ bool rect_tiles(uint2 r, int& tx0, int& ty0, int& tx1
   const int x0 = (int)(short)(r.x & 0xFFFF), y0 = (int)(short)(r.x >> 16);
   const int x1 = (int)(short)(r.y & 0xFFFF), y1 = (int)(short)(r.y >> 16);
   if (x0 > x1 || y0 > y1) return false;
-  tx0 = x0 / kTile; ty0 = y0 / kTile; tx1 = x1 / kTile; ty1 = y1 / kTile;
+  // (visible rects are clamped to the image: coordinates >= 0, so the division is a shift)
+  tx0 = (int)((uint32_t)x0 / kTile); ty0 = (int)((uint32_t)y0 / kTile);
+  tx1 = (int)((uint32_t)x1 / kTile); ty1 = (int)((uint32_t)y1 / kTile);
   return true;
 }
 
@@ -254,12 +256,13 @@ __global__ void __launch_bounds__(1024) k_tile_offsets(const uint32_t* __restric
 template <int REP, bool STB = false>
 __global__ void __launch_bounds__(256) k_emit(const uint32_t* __restrict__ zkey, const uint2* __restrict__ rect,
                                               const uint8_t* __restrict__ keep, int n, int TX, int T,
-                                              const uint32_t* __restrict__ start, uint32_t* __restrict__ cursor,
-                                              uint32_t cap, unsigned long long* __restrict__ keys,
+                                              uint32_t* __restrict__ cursor, uint32_t cap,
+                                              unsigned long long* __restrict__ keys,
                                               const uint8_t* __restrict__ flags = nullptr) {
+  // cursor[r][t] starts at the replica's first slot of tile t (k_tile_offsets / k_merge_offsets write
+  // it), so the atomic returns the absolute slot: no dependent load of a start array per instance
   const int i = blockIdx.x * 256 + threadIdx.x;
   const size_t rep = (size_t)(blockIdx.x & (REP - 1)) * T;  // same replica as k_tile_count
-  start += rep;
   cursor += rep;
   const int lane = threadIdx.x & 31;
   const uint32_t lt = (1u << lane) - 1u;
@@ -278,18 +281,18 @@ __global__ void __launch_bounds__(256) k_emit(const uint32_t* __restrict__ zkey,
   // coherent maps, rtgs_morton_order) share ONE cursor atomic (match_any groups, the group's leader
   // adds the group size and broadcasts the base), instead of one atomic round trip per instance
   const int ntmax = __reduce_max_sync(0xffffffffu, (uint32_t)nt);
+  int cx = 0, tt = ty0 * TX + tx0;  // the lane's q-th tile, stepped row-major (no division by w)
   for (int q = 0; q < ntmax; ++q) {
-    int t = q < nt ? (ty0 + q / w) * TX + tx0 + q % w : -1;
+    int t = q < nt ? tt : -1;
+    ++tt;
+    if (++cx == w) { cx = 0; tt += TX - w; }
     if (t >= 0 && keep && !keep[t]) t = -1;
     const uint32_t peers = __match_any_sync(0xffffffffu, (uint32_t)t);
     const int leader = __ffs(peers) - 1;
     uint32_t off = 0u;
     if (t >= 0 && lane == leader) off = atomicAdd(&cursor[t], (uint32_t)__popc(peers));
     off = __shfl_sync(0xffffffffu, off, leader) + __popc(peers & lt);
-    if (t >= 0) {
-      const uint32_t slot = start[t] + off;
-      if (slot < cap) keys[slot] = k;
-    }
+    if (t >= 0 && off < cap) keys[off] = k;
   }
 }
 
@@ -773,7 +776,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_merge(const uint8_t* __re
 
 // ------------------------------------------------------------------------------------------------
 struct BinWS {
-  uint32_t *cnt, *start, *cursor, *grank;
+  uint32_t *cnt, *cursor, *grank;
   unsigned long long *keys, *tmp;
 };
 
@@ -788,9 +791,8 @@ static size_t carve(int n, const rtgs_camera& cam, uint32_t cap, BinWS* w, char*
   const CamK k = make_cam(cam);
   const size_t T = (size_t)k.TX * k.TY;
   BinWS t;
-  t.cnt = (uint32_t*)take(kRep * T * 4);      // cnt and cursor adjacent: one memset clears both
-  t.cursor = (uint32_t*)take(kRep * T * 4);
-  t.start = (uint32_t*)take(kRep * T * 4);
+  t.cnt = (uint32_t*)take(kRep * T * 4);
+  t.cursor = (uint32_t*)take(kRep * T * 4);  // written by the offsets kernels: each replica's first slot
   t.keys = (unsigned long long*)take((size_t)cap * 8 + 8);
   t.tmp = (unsigned long long*)take((size_t)cap * 8 + 8);
   t.grank = (uint32_t*)take((size_t)cap * 4 + 4);
@@ -809,15 +811,15 @@ static cudaError_t bin_from_counts(const rtgs_projected& proj, int n, const CamK
   const int T = k.TX * k.TY;
   const uint2* rect = reinterpret_cast<const uint2*>(proj.rect);
   const int nblk = (n + 255) / 256;
-  k_tile_offsets<kRep><<<1, 1024, 0, s>>>(w.cnt, T, out.capacity, w.start, reinterpret_cast<uint2*>(out.tile_range),
+  k_tile_offsets<kRep><<<1, 1024, 0, s>>>(w.cnt, T, out.capacity, w.cursor, reinterpret_cast<uint2*>(out.tile_range),
                                     out.n_instances);
   note_launch();
   if (n > 0) {
     if (so.flags)
-      k_emit<kRep, true><<<nblk, 256, 0, s>>>(proj.zkey, rect, keep, n, k.TX, T, w.start, w.cursor, out.capacity,
+      k_emit<kRep, true><<<nblk, 256, 0, s>>>(proj.zkey, rect, keep, n, k.TX, T, w.cursor, out.capacity,
                                               w.keys, so.flags);
     else
-      k_emit<kRep><<<nblk, 256, 0, s>>>(proj.zkey, rect, keep, n, k.TX, T, w.start, w.cursor, out.capacity, w.keys);
+      k_emit<kRep><<<nblk, 256, 0, s>>>(proj.zkey, rect, keep, n, k.TX, T, w.cursor, out.capacity, w.keys);
     note_launch();
     int gid_bits = 1;
     while (gid_bits < 32 && (1u << gid_bits) < (uint32_t)n) ++gid_bits;
@@ -842,7 +844,7 @@ cudaError_t launch_bin(const rtgs_projected& proj, int n, const rtgs_camera& cam
   const int T = k.TX * k.TY;
   BinWS w;
   carve(n, cam, out.capacity, &w, static_cast<char*>(ws));
-  cudaMemsetAsync(w.cnt, 0, (size_t)((char*)w.start - (char*)w.cnt), s);
+  cudaMemsetAsync(w.cnt, 0, (size_t)((char*)w.cursor - (char*)w.cnt), s);  // (the offsets write cursor)
   const uint2* rect = reinterpret_cast<const uint2*>(proj.rect);
   const int nblk = (n + 255) / 256;
   if (n > 0) {
@@ -858,7 +860,7 @@ cudaError_t launch_project_bin(const rtgs_gaussians& g, const PoseF& pose, const
   const CamK k = make_cam(cam);
   BinWS w;
   carve(g.n, cam, out.capacity, &w, static_cast<char*>(ws));
-  cudaMemsetAsync(w.cnt, 0, (size_t)((char*)w.start - (char*)w.cnt), s);
+  cudaMemsetAsync(w.cnt, 0, (size_t)((char*)w.cursor - (char*)w.cnt), s);  // (the offsets write cursor)
   StableOut so{nullptr, nullptr, nullptr, nullptr};
   if (cache) {
     so = StableOut{g.flags, cache->sorted_gid, reinterpret_cast<uint2*>(cache->tile_range), cache->n_instances};
@@ -920,7 +922,7 @@ cudaError_t launch_bin_cached(const rtgs_projected& proj, const rtgs_bins& cache
   (void)sn;
   BinWS w;
   carve(n_sub, cam, out.capacity, &w, static_cast<char*>(bws));
-  cudaMemsetAsync(w.cnt, 0, (size_t)((char*)w.start - (char*)w.cnt), s);
+  cudaMemsetAsync(w.cnt, 0, (size_t)((char*)w.cursor - (char*)w.cnt), s);  // (the offsets write cursor)
   const uint2* rect = reinterpret_cast<const uint2*>(sub.rect);
   const int nblk = (n_sub + 255) / 256;
   if (n_sub > 0) {
@@ -928,10 +930,10 @@ cudaError_t launch_bin_cached(const rtgs_projected& proj, const rtgs_bins& cache
     note_launch();
   }
   k_merge_offsets<kSubRep><<<1, 1024, 0, s>>>(w.cnt, keep, reinterpret_cast<const uint2*>(cache.tile_range), T, out.capacity,
-                                     w.start, srange, reinterpret_cast<uint2*>(out.tile_range), out.n_instances);
+                                     w.cursor, srange, reinterpret_cast<uint2*>(out.tile_range), out.n_instances);
   note_launch();
   if (n_sub > 0) {
-    k_emit<kSubRep><<<nblk, 256, 0, s>>>(sub.zkey, rect, keep, n_sub, k.TX, T, w.start, w.cursor, out.capacity, w.keys);
+    k_emit<kSubRep><<<nblk, 256, 0, s>>>(sub.zkey, rect, keep, n_sub, k.TX, T, w.cursor, out.capacity, w.keys);
     note_launch();
   }
   int row_bits = 1;
@@ -965,7 +967,7 @@ cudaError_t launch_coverage_subset(const rtgs_projected& sub, int n_sub, const r
   carve_cached(n_sub, cam, capacity, static_cast<char*>(ws), &ssorted, &srange, &sn, &bws);
   BinWS w;
   carve(n_sub, cam, capacity, &w, static_cast<char*>(bws));
-  cudaMemsetAsync(w.cnt, 0, (size_t)((char*)w.start - (char*)w.cnt), s);
+  cudaMemsetAsync(w.cnt, 0, (size_t)((char*)w.cursor - (char*)w.cnt), s);  // (the offsets write cursor)
   cudaMemsetAsync(cov.active_bits, 0, ((size_t)k.W * k.H + 31) / 32 * 4, s);
   cudaMemsetAsync(cov.counts, 0, 16, s);
   const uint2* rect = reinterpret_cast<const uint2*>(sub.rect);
@@ -974,10 +976,10 @@ cudaError_t launch_coverage_subset(const rtgs_projected& sub, int n_sub, const r
     k_tile_count<kSubRep><<<nblk, 256, 0, s>>>(sub.zkey, rect, nullptr, n_sub, k.TX, T, w.cnt);
     note_launch();
   }
-  k_tile_offsets<kSubRep><<<1, 1024, 0, s>>>(w.cnt, T, capacity, w.start, srange, sn);
+  k_tile_offsets<kSubRep><<<1, 1024, 0, s>>>(w.cnt, T, capacity, w.cursor, srange, sn);
   note_launch();
   if (n_sub > 0) {
-    k_emit<kSubRep><<<nblk, 256, 0, s>>>(sub.zkey, rect, nullptr, n_sub, k.TX, T, w.start, w.cursor, capacity, w.keys);
+    k_emit<kSubRep><<<nblk, 256, 0, s>>>(sub.zkey, rect, nullptr, n_sub, k.TX, T, w.cursor, capacity, w.keys);
     note_launch();
   }
   return launch_tile_coverage(srange, w.keys, reinterpret_cast<const float4*>(sub.rec), cam, cov, s);
@@ -996,7 +998,7 @@ cudaError_t launch_merge_cached(const rtgs_projected& proj, const rtgs_bins& cac
   BinWS w;
   carve(n_sub, cam, out.capacity, &w, static_cast<char*>(bws));
   k_merge_offsets<kSubRep><<<1, 1024, 0, s>>>(w.cnt, keep, reinterpret_cast<const uint2*>(cache.tile_range), T, out.capacity,
-                                     w.start, srange, reinterpret_cast<uint2*>(out.tile_range), out.n_instances);
+                                     w.cursor, srange, reinterpret_cast<uint2*>(out.tile_range), out.n_instances);
   note_launch();
   int row_bits = 1;
   while (row_bits < 32 && (1u << row_bits) < (uint32_t)n_sub) ++row_bits;
