@@ -10,7 +10,10 @@
 
 namespace rtgs {
 
-constexpr int kRep = 8;  // replicated per-tile counters of the binning: spreads same-address atomics 8 ways
+#ifndef RTGS_REP
+#define RTGS_REP 2
+#endif
+constexpr int kRep = RTGS_REP;  // replicated per-tile counters of the binning: spreads same-address atomics (swept 1/2/4/8 on Morton-ordered C3/C4 maps: 2)
 
 // once per (kernel attribute, device): per-device bit in `mask` (one-time cudaFuncSetAttribute calls
 // must be repeated on every device the process launches on)
