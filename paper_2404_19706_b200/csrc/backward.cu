@@ -83,7 +83,7 @@ constexpr int kBwdParts = kTile / (2 * kBwdWarps);  // CTAs per kept tile (each 
 static_assert(kBwdParts == 2 || kBwdParts == 4, "the backward splits a tile in 2 or 4 row bands");
 
 struct BwdSmem {
-  PipeRing ring;
+  PipeRingT<false> ring;  // (no list entries: the producer resolves each record's slot)
   int32_t slot[kPipeStages][kPipeBatch];
   uint8_t survq[kBwdWarps][kPipeBatch];  // span path: the stage's bbox survivors, in list order
   float red[3][kBwdWarps];
@@ -92,7 +92,7 @@ struct BwdSmem {
 
 __global__ void __launch_bounds__(32 * (kBwdWarps + 1)) k_render_bwd(const BwdArgs a) {
   __shared__ BwdSmem sm;  // static: stage addresses fold into immediates
-  PipeRing& r = sm.ring;
+  PipeRingT<false>& r = sm.ring;
   if ((int)(blockIdx.x / kBwdParts) >= (int)a.counts[0]) return;
   const int tile = (int)a.tile_list[blockIdx.x / kBwdParts];
   const int half = blockIdx.x % kBwdParts;  // row band of the tile
@@ -182,15 +182,17 @@ __global__ void __launch_bounds__(32 * (kBwdWarps + 1)) k_render_bwd(const BwdAr
   if (!consumer) {
     const int32_t* slot_of_gid = a.slot_of_gid;
     // slot of a gid entry via slot_of_gid; a subset entry (f3) carries its slot in the entry itself
+    // (a subset entry's slot is the entry itself: stored here, so the consumers read one slot per record)
     auto extra = [&](int st, int j, uint32_t g) {
       if (!(g & kSubBit)) cp_async4(&sm.slot[st][j], slot_of_gid + g);
+      else sm.slot[st][j] = (int32_t)(g & ~kSubBit);
     };
     auto flush = [](int, int) {};
 #if !RTGS_BWD_DENSE
-    pipe_produce<true, kBwdWarps>(r, a.rec, a.sub_rec, a.sorted_gid, start, end, extra, flush, (float)(tx * kTile),
+    pipe_produce<true, kBwdWarps, false>(r, a.rec, a.sub_rec, a.sorted_gid, start, end, extra, flush, (float)(tx * kTile),
                                   (float)(ty * kTile + half * (kBwdWarps / 2) * 4));
 #else
-    pipe_produce<true>(r, a.rec, a.sub_rec, a.sorted_gid, start, end, extra, flush);
+    pipe_produce<true, 0, false>(r, a.rec, a.sub_rec, a.sorted_gid, start, end, extra, flush);
 #endif
     return;
   }
@@ -208,7 +210,6 @@ __global__ void __launch_bounds__(32 * (kBwdWarps + 1)) k_render_bwd(const BwdAr
   const float bx0 = (float)wx0, bx1 = (float)(wx0 + 7), by0 = (float)wy0, by1 = (float)(wy0 + 3);
   const int nb = n > 0 ? (n + kPipeBatch - 1) / kPipeBatch : 0;
   const uint32_t rec0 = pin(smem_u32(&r.rec[0][0][0])), slot0 = pin(smem_u32(&sm.slot[0][0]));
-  const uint32_t gid0 = pin(smem_u32(&r.gid[0][0]));
   const int plane = (int)pin((uint32_t)lane);
   float T = want ? a.trans[lin] : 1.f;  // T after the last blended entry = the forward's T^
   float B = 0.f;                         // colour cotangent behind the current entry
@@ -222,6 +223,9 @@ __global__ void __launch_bounds__(32 * (kBwdWarps + 1)) k_render_bwd(const BwdAr
   // lane adds its 8 screen-space values with two vector reductions (no warp reduce).
   const uint32_t q0 = pin(smem_u32(&sm.survq[w][0]));
   (void)plane;
+#ifdef RTGS_BWD_NOATOM
+  float sink = 0.f;
+#endif
   for (int b = 0; b < nb; ++b) {
     const int st = b % kPipeStages;
     mbar_wait_sleep(&r.full[st], (uint32_t)(b / kPipeStages) & 1u);
@@ -229,7 +233,6 @@ __global__ void __launch_bounds__(32 * (kBwdWarps + 1)) k_render_bwd(const BwdAr
     if ((uint32_t)lo < wlast) {  // warp-uniform: the batch holds entries of this warp's pixels
       const uint32_t srec = rec0 + (uint32_t)(st * sizeof(r.rec[0]));  // shared addresses of this stage
       const uint32_t sslot = slot0 + (uint32_t)(st * sizeof(sm.slot[0]));
-      const uint32_t sgid = gid0 + (uint32_t)(st * sizeof(r.gid[0]));
       const int cnt = pipe_batch_cnt(true, start, end, b);
       int nq = 0;
       const uint32_t sbox = pin(smem_u32(&r.boxmask[st][0]));
@@ -261,28 +264,37 @@ __global__ void __launch_bounds__(32 * (kBwdWarps + 1)) k_render_bwd(const BwdAr
           PairEval e;
           // blended in the forward <=> passes the support test and lies before the pixel's `last`
           const bool ok = eval_pair(r0, r1, fpx, fpy, e) && has && ((uint32_t)lo + idx < mylast);
-          const float inv1mf = __frcp_rn(__fsub_rn(1.f, e.f));  // IEEE reciprocal; 1 - f >= 0.01
-          const float Ti = ok ? __fmul_rn(T, inv1mf) : T;        // T before entry i
+          // T before entry i: 1 - f >= 0.01, and the ~1 ulp reciprocal only scales T (no decision
+          // of the walk reads T: `ok` is the forward's support test and position)
+          float inv1mf;
+          asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv1mf) : "f"(__fsub_rn(1.f, e.f)));
+          const float Ti = ok ? __fmul_rn(T, inv1mf) : T;
           const float wgt = ok ? __fmul_rn(e.f, Ti) : 0.f;
           const float G = __fmaf_rn(gCb, r2.z, __fmaf_rn(gCg, r2.y, gCr * r2.x));
-          if (ok) {
-            const uint32_t ent = lds32(sgid + 4u * idx);
-            const int slot = (ent & kSubBit) ? (int)(ent & ~kSubBit) : (int)lds32(sslot + 4u * idx);
-            if (slot >= 0) {
+          const int slot = (int)lds32(sslot + 4u * idx);  // < 0: a stable Gaussian (no gradient)
+          {
+            {
               const float dLdf = __fmul_rn(Ti, __fsub_rn(G, B));
               // f = alpha e^power; the 0.99 cap passes no gradient when active (R17)
               const float dLdp = (e.f < kFMax) ? dLdf * e.f : 0.f;
               // power = p2 / log2(e): d power / d dx = (2 A' dx + B' dy) / log2(e) = -(A dx + B dy)
               const float sc = dLdp * (1.f / kLog2e);
-              float* sg = a.sgrad + (size_t)slot * kSG;
-              atomicAdd(reinterpret_cast<float4*>(sg),
-                        make_float4(sc * (2.f * r1.x * e.dx + r1.y * e.dy),   // d/d mu_x
-                                    sc * (2.f * r1.z * e.dy + r1.y * e.dx),   // d/d mu_y
-                                    -0.5f * dLdp * e.dx * e.dx,               // d/d A
-                                    -dLdp * e.dx * e.dy));                    // d/d B
-              atomicAdd(reinterpret_cast<float4*>(sg + 4),
-                        make_float4(-0.5f * dLdp * e.dy * e.dy,               // d/d C
-                                    gCr * wgt, gCg * wgt, gCb * wgt));        // d/d rgb
+              float* sg = a.sgrad + (size_t)max(slot, 0) * kSG;
+#ifdef RTGS_BWD_NOATOM  // experiment builds only: the pair cost without its gradient reductions
+              sink += sc * (2.f * r1.x * e.dx + r1.y * e.dy) + sc * (2.f * r1.z * e.dy + r1.y * e.dx) +
+                      dLdp * e.dx * e.dy + gCr * wgt + gCg * wgt + gCb * wgt + (float)(size_t)sg;
+#else
+              const float4 v0 = make_float4(sc * (2.f * r1.x * e.dx + r1.y * e.dy),   // d/d mu_x
+                                            sc * (2.f * r1.z * e.dy + r1.y * e.dx),   // d/d mu_y
+                                            -0.5f * dLdp * e.dx * e.dx,               // d/d A
+                                            -dLdp * e.dx * e.dy);                     // d/d B
+              const float4 v1 = make_float4(-0.5f * dLdp * e.dy * e.dy,               // d/d C
+                                            gCr * wgt, gCg * wgt, gCb * wgt);         // d/d rgb
+              if (ok && slot >= 0) {  // (the values above are formed branch-free on every lane)
+                atomicAdd(reinterpret_cast<float4*>(sg), v0);
+                atomicAdd(reinterpret_cast<float4*>(sg + 4), v1);
+              }
+#endif
             }
           }
           B = ok ? __fmaf_rn(e.f, __fsub_rn(G, B), B) : B;  // f G + (1 - f) B
@@ -293,6 +305,9 @@ __global__ void __launch_bounds__(32 * (kBwdWarps + 1)) k_render_bwd(const BwdAr
     __syncwarp();
     if (lane == 0) mbar_arrive(&r.empty[st]);
   }
+#ifdef RTGS_BWD_NOATOM
+  if (sink == 1234.5f) a.acc[3] = sink;
+#endif
 }
 
 #else  // RTGS_BWD_DENSE: the dense walk (every lane evaluates every bbox survivor), for comparison
@@ -303,7 +318,6 @@ __global__ void __launch_bounds__(32 * (kBwdWarps + 1)) k_render_bwd(const BwdAr
     if ((uint32_t)lo < wlast) {  // warp-uniform: the batch holds entries of this warp's pixels
       const uint32_t srec = rec0 + (uint32_t)(st * sizeof(r.rec[0]));  // shared addresses of this stage
       const uint32_t sslot = slot0 + (uint32_t)(st * sizeof(sm.slot[0]));
-      const uint32_t sgid = gid0 + (uint32_t)(st * sizeof(r.gid[0]));
       const int cnt = pipe_batch_cnt(true, start, end, b);
       for (int g0 = (cnt - 1) & ~31; g0 >= 0; g0 -= 32) {
         const int j = g0 + lane;
@@ -318,8 +332,7 @@ __global__ void __launch_bounds__(32 * (kBwdWarps + 1)) k_render_bwd(const BwdAr
           const int bit = 31 - __clz(m);  // back to front
           m ^= 1u << bit;
           const int idx = g0 + bit;
-          const uint32_t ent = lds32(sgid + 4u * idx);  // warp-uniform
-          const int slot = (ent & kSubBit) ? (int)(ent & ~kSubBit) : (int)lds32(sslot + 4u * idx);
+          const int slot = (int)lds32(sslot + 4u * idx);  // warp-uniform
           const uint32_t ra = srec + 48u * idx;
           const float4 r0 = lds128(ra), r1 = lds128(ra + 16u), r2 = lds128(ra + 32u);
           PairEval e;

@@ -433,12 +433,24 @@ __device__ __forceinline__ void sort_tile(const unsigned long long* __restrict__
   if (tid == 0) { s_zmm[0] = 0xFFFFFFFFu; s_zmm[1] = 0u; }
   __syncthreads();
   uint32_t zmin = 0xFFFFFFFFu, zmax = 0u;
-  for (int i = tid; i < n; i += kSortThreads) {
-    const unsigned long long k = seg[i];
-    const uint32_t z = (uint32_t)(k >> 32);
-    zmin = min(zmin, z);
-    zmax = max(zmax, z);
-    if (copy_in) A[i] = k;
+  constexpr int LU = 4;  // list loads in flight per thread
+  for (int i0 = tid; i0 < n; i0 += LU * kSortThreads) {
+    unsigned long long k[LU];
+#pragma unroll
+    for (int u = 0; u < LU; ++u) {
+      const int i = i0 + u * kSortThreads;
+      k[u] = i < n ? seg[i] : 0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < LU; ++u) {
+      const int i = i0 + u * kSortThreads;
+      if (i < n) {
+        const uint32_t z = (uint32_t)(k[u] >> 32);
+        zmin = min(zmin, z);
+        zmax = max(zmax, z);
+        if (copy_in) A[i] = k[u];
+      }
+    }
   }
   atomicMin(&s_zmm[0], zmin);
   atomicMax(&s_zmm[1], zmax);
