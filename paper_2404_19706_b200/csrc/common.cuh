@@ -177,22 +177,64 @@ __device__ __forceinline__ float2 unpack_ext(float w) {
                      __half2float(__ushort_as_half((unsigned short)(u >> 16))));
 }
 
-// warp-aggregated per-tile counting: the lanes' rect tiles in a warp-uniform loop, one atomic per
-// distinct tile per warp (match_any groups; spatially coherent maps put a warp's Gaussians on few
+// Warp-cooperative expansion of the lanes' rect tiles (lane: nt = w x h tiles from (tx0, ty0)): the
+// warp's instances (sum of nt over the lanes) are dealt out 32 per round, lane by lane in order, so a
+// warp holding one large rect takes ceil(sum / 32) rounds instead of max(nt) (each with an atomic
+// round trip).  f(t, o) is called warp-uniformly once per round: this lane holds an instance of tile t
+// from lane o (t = -1: none this round).
+// Warps whose largest rect is small (the common case: sub-tile splats) keep the plain per-lane loop
+// over max(nt) rounds, which costs less per round than the expansion's search.
+template <typename F>
+__device__ __forceinline__ void warp_expand_tiles(int nt, int w, int tx0, int ty0, int TX, F f) {
+  const int lane = threadIdx.x & 31;
+  const int ntmax = (int)__reduce_max_sync(0xffffffffu, (uint32_t)nt);
+  if (ntmax <= 4) {
+    int cx = 0, tt = ty0 * TX + tx0;  // the lane's q-th tile, stepped row-major
+    for (int q = 0; q < ntmax; ++q) {
+      f(q < nt ? tt : -1, lane);
+      ++tt;
+      if (++cx == w) { cx = 0; tt += TX - w; }
+    }
+    return;
+  }
+  const uint32_t incl = warp_incl_scan((uint32_t)nt);
+  const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+  const uint32_t excl = incl - (uint32_t)nt;
+  const float rw = 1.f / (float)max(w, 1);
+  for (uint32_t base = 0; base < total; base += 32) {
+    const uint32_t k = base + (uint32_t)lane;
+    int o = 0;  // the owner: the smallest lane with incl > k (binary lifting over the 32 prefix sums)
+#pragma unroll
+    for (int step = 16; step >= 1; step >>= 1) {
+      const uint32_t v = __shfl_sync(0xffffffffu, incl, o + step - 1);
+      if (v <= k) o += step;
+    }
+    const uint32_t ex = __shfl_sync(0xffffffffu, excl, o);
+    const int ow = __shfl_sync(0xffffffffu, w, o), ox = __shfl_sync(0xffffffffu, tx0, o);
+    const int oy = __shfl_sync(0xffffffffu, ty0, o);
+    const float orw = __shfl_sync(0xffffffffu, rw, o);
+    int t = -1;
+    if (k < total) {
+      const int q = (int)(k - ex);  // the instance's index in its rect, row-major
+      int qy = (int)(((float)q + 0.5f) * orw), qx = q - qy * ow;  // q / w in float, then exact:
+      if (qx < 0) { --qy; qx += ow; } else if (qx >= ow) { ++qy; qx -= ow; }
+      t = (oy + qy) * TX + ox + qx;
+    }
+    f(t, o);
+  }
+}
+
+// warp-aggregated per-tile counting: the lanes' rect tiles expanded across the warp, one atomic per
+// distinct tile per round (match_any groups; spatially coherent maps put a warp's Gaussians on few
 // tiles, rtgs_morton_order)
 __device__ __forceinline__ void tile_count_agg(uint32_t* cnt, int nt, int w, int tx0, int ty0, int TX,
                                                const uint8_t* keep) {
   const int lane = threadIdx.x & 31;
-  const int ntmax = __reduce_max_sync(0xffffffffu, (uint32_t)nt);
-  int cx = 0, tt = ty0 * TX + tx0;  // the lane's q-th tile, stepped row-major (no division by w)
-  for (int q = 0; q < ntmax; ++q) {
-    int t = q < nt ? tt : -1;
+  warp_expand_tiles(nt, w, tx0, ty0, TX, [&](int t, int) {
     if (t >= 0 && keep && !keep[t]) t = -1;
     const uint32_t peers = __match_any_sync(0xffffffffu, (uint32_t)t);
     if (t >= 0 && lane == __ffs(peers) - 1) atomicAdd(&cnt[t], (uint32_t)__popc(peers));
-    ++tt;
-    if (++cx == w) { cx = 0; tt += TX - w; }
-  }
+  });
 }
 
 }  // namespace rtgs

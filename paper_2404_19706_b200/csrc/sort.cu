@@ -277,23 +277,22 @@ __global__ void __launch_bounds__(256) k_emit(const uint32_t* __restrict__ zkey,
   const uint32_t low = vis ? (STB ? (((uint32_t)i << 1) | ((flags[i] >> 1) & 1u)) : (uint32_t)i) : 0u;
   const unsigned long long k = ((unsigned long long)z << 32) | low;
   const int w = tx1 - tx0 + 1, nt = vis ? w * (ty1 - ty0 + 1) : 0;
-  // warp-uniform loop over the tiles of the lanes' rects: lanes that land on the same tile (spatially
-  // coherent maps, rtgs_morton_order) share ONE cursor atomic (match_any groups, the group's leader
-  // adds the group size and broadcasts the base), instead of one atomic round trip per instance
-  const int ntmax = __reduce_max_sync(0xffffffffu, (uint32_t)nt);
-  int cx = 0, tt = ty0 * TX + tx0;  // the lane's q-th tile, stepped row-major (no division by w)
-  for (int q = 0; q < ntmax; ++q) {
-    int t = q < nt ? tt : -1;
-    ++tt;
-    if (++cx == w) { cx = 0; tt += TX - w; }
+  // the lanes' rect tiles expanded across the warp (warp_expand_tiles); lanes that land on the same
+  // tile in a round (spatially coherent maps, rtgs_morton_order) share ONE cursor atomic (match_any
+  // groups, the group's leader adds the group size and broadcasts the slot), instead of one atomic
+  // round trip per instance
+  const uint32_t klo = (uint32_t)k, khi = (uint32_t)(k >> 32);
+  warp_expand_tiles(nt, w, tx0, ty0, TX, [&](int t, int o) {
+    const unsigned long long ko = ((unsigned long long)__shfl_sync(0xffffffffu, khi, o) << 32) |
+                                  __shfl_sync(0xffffffffu, klo, o);
     if (t >= 0 && keep && !keep[t]) t = -1;
     const uint32_t peers = __match_any_sync(0xffffffffu, (uint32_t)t);
     const int leader = __ffs(peers) - 1;
     uint32_t off = 0u;
     if (t >= 0 && lane == leader) off = atomicAdd(&cursor[t], (uint32_t)__popc(peers));
     off = __shfl_sync(0xffffffffu, off, leader) + __popc(peers & lt);
-    if (t >= 0 && off < cap) keys[off] = k;
-  }
+    if (t >= 0 && off < cap) keys[off] = ko;
+  });
 }
 
 // Stable LSD radix sort of n 64-bit keys by one CTA on key bits [lo, lo + nbits) (8-bit digits).
