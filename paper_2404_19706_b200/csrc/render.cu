@@ -128,20 +128,29 @@ __global__ void __launch_bounds__(256) k_tile_coverage(const uint2* __restrict__
     __syncthreads();
     bool wdone = __all_sync(0xffffffffu, !inside || cov);
     for (int g0 = 0; g0 < cnt && !wdone; g0 += 32) {
+      // span masks (as the render's span walk): lane l computes instance g0 + l's superset mask of
+      // the warp's 16 x 2 pixels, one transpose gives each pixel the instances that MAY cover it,
+      // and the pixel runs the exact test only on those, until its first hit
       const int j = g0 + lane;
-      bool ov = false;
+      uint32_t pm = 0u;
       if (j < cnt) {
         const float4 r0 = sa[j];
         const float2 ext = unpack_ext(se[j]);
-        ov = (r0.x + ext.x >= bx0) && (r0.x - ext.x <= bx1) && (r0.y + ext.y >= by0) && (r0.y - ext.y <= by1);
+        if ((r0.x + ext.x >= bx0) && (r0.x - ext.x <= bx1) && (r0.y + ext.y >= by0) && (r0.y - ext.y <= by1))
+          pm = support_mask_16x2(r0, sb[j], bx0, by0);
       }
-      uint32_t m = __ballot_sync(0xffffffffu, ov);
-      while (m) {
-        const int idx = g0 + __ffs(m) - 1;
-        m &= m - 1;
-        PairEval e;
-        const bool hit = eval_pair(sa[idx], sb[idx], (float)px, (float)py, e);
-        cov = cov || (inside && hit);
+      uint32_t lm = warp_transpose32(pm, (uint32_t)lane);
+      if (!inside || cov) lm = 0u;
+      while (__any_sync(0xffffffffu, lm != 0u)) {
+        if (lm) {
+          const int idx = g0 + __ffs(lm) - 1;
+          lm &= lm - 1u;
+          PairEval e;
+          if (eval_pair(sa[idx], sb[idx], (float)px, (float)py, e)) {
+            cov = true;
+            lm = 0u;
+          }
+        }
       }
       wdone = __all_sync(0xffffffffu, !inside || cov);
     }

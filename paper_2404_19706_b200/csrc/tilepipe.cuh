@@ -223,6 +223,35 @@ __device__ __forceinline__ uint32_t support_mask(const float4 a, const float4 c,
   return m;
 }
 
+// The same superset mask for a 16 x 2 pixel block (bit 16*row + col): the coverage kernel's warp
+// (two tile rows).  Identical interval arithmetic to support_mask.
+__device__ __forceinline__ uint32_t support_mask_16x2(const float4 a, const float4 c, float bx0, float by0) {
+  const float mx = a.x + a.z, my = a.y + a.w;
+  const float pmin = fmaxf(kP2Min, kLog2FMin - c.w);
+  const float pm = __fmaf_rn(pmin, 1.01f, -0.01f);
+  const float D0 = 4.f * c.x * pm;
+  const float D2 = __fmaf_rn(4.f * c.x, c.z, -c.y * c.y);
+  const float inv2a = -0.5f / c.x;
+  const float xs = -c.y * inv2a;
+  uint32_t m = 0u;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const float dy = my - (by0 + (float)k);
+    const float disc = __fmaf_rn(-D2, dy * dy, D0);
+    if (disc >= 0.f) {
+      float sq;
+      asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(sq) : "f"(disc));
+      const float h = __fmaf_rn(sq, inv2a, 0.02f);
+      const float xc = __fmaf_rn(xs, dy, mx) - bx0;
+      const int lo = (int)ceilf(fmaxf(xc - h, -1.f));
+      const int hi = (int)floorf(fminf(xc + h, 16.f));
+      const int l0 = max(lo, 0), h0 = min(hi, 15);
+      if (l0 <= h0) m |= ((0xFFFFu >> (15 - (h0 - l0))) << l0) << (16 * k);
+    }
+  }
+  return m;
+}
+
 struct FwdArgs {
   const float4* rec;
   const uint32_t* zkey;
