@@ -117,7 +117,7 @@ __device__ __forceinline__ void pipe_produce(PipeRingT<GID>& r, const float4* __
     const int st = b % kPipeStages;
     const uint32_t ph = (uint32_t)(b / kPipeStages) & 1u;
     if (b >= kPipeStages) {
-      mbar_wait(&r.empty[st], ph ^ 1u);
+      mbar_wait_sleep(&r.empty[st], ph ^ 1u);  // (suspended, not spinning: measured neutral on time)
       flush(st, b - kPipeStages);
     }
     if (*((volatile int*)&r.alive) > 0) {
@@ -171,7 +171,7 @@ __device__ __forceinline__ void pipe_produce(PipeRingT<GID>& r, const float4* __
   // the last stages are flushed once every consumer warp has released them
   for (int b = max(0, nb - kPipeStages); b < nb; ++b) {
     const int st = b % kPipeStages;
-    mbar_wait(&r.empty[st], (uint32_t)(b / kPipeStages) & 1u);
+    mbar_wait_sleep(&r.empty[st], (uint32_t)(b / kPipeStages) & 1u);
     flush(st, b);
   }
 }

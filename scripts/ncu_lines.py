@@ -7,7 +7,7 @@ import sys
 
 
 def main(path, kernel, top=40):
-    out = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--kernel-name", f"regex:{kernel}",
+    out = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--kernel-name", f"regex:{kernel}", "--launch-skip", sys.argv[4] if len(sys.argv) > 4 else "0",
                           "--launch-count", "1", "--print-source", "cuda,sass"], capture_output=True, text=True).stdout
     f = lambda v: float(v) if v.replace(".", "", 1).isdigit() else 0.0
     rows, fname = [], ""
