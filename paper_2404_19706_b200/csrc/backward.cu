@@ -90,7 +90,10 @@ struct BwdSmem {
   uint32_t last_max;
 };
 
-__global__ void __launch_bounds__(32 * (kBwdWarps + 1)) k_render_bwd(const BwdArgs a) {
+#ifndef RTGS_BWD_MINB
+#define RTGS_BWD_MINB 1
+#endif
+__global__ void __launch_bounds__(32 * (kBwdWarps + 1), RTGS_BWD_MINB) k_render_bwd(const BwdArgs a) {
   __shared__ BwdSmem sm;  // static: stage addresses fold into immediates
   PipeRingT<false>& r = sm.ring;
   if ((int)(blockIdx.x / kBwdParts) >= (int)a.counts[0]) return;

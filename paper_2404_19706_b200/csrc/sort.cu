@@ -719,8 +719,28 @@ __device__ __forceinline__ void merge_tile(const uint32_t* __restrict__ S, int n
     return ((unsigned long long)szkey[r] << 32) | (uint32_t)sgid[r];
   };
   if (nS + nU <= sk_cap) {
-    for (int i = threadIdx.x; i < nS; i += blockDim.x) sk[i] = keyS(i);
-    for (int j = threadIdx.x; j < nU; j += blockDim.x) sk[nS + j] = keyU(j);
+    // key gathers 4 deep per thread (each key is two dependent loads: the id, then its zkey)
+    constexpr int GU = 4;
+    for (int i0 = threadIdx.x; i0 < nS + nU; i0 += GU * (int)blockDim.x) {
+      uint32_t id[GU];
+#pragma unroll
+      for (int u = 0; u < GU; ++u) {
+        const int i = i0 + u * (int)blockDim.x;
+        id[u] = i < nS ? S[i] : (i < nS + nU ? U[i - nS] : 0u);
+      }
+      uint32_t z[GU], lo[GU];
+#pragma unroll
+      for (int u = 0; u < GU; ++u) {
+        const int i = i0 + u * (int)blockDim.x;
+        z[u] = i < nS ? zfull[id[u]] : (i < nS + nU ? szkey[id[u]] : 0u);
+        lo[u] = i < nS ? id[u] : (i < nS + nU ? (uint32_t)sgid[id[u]] : 0u);
+      }
+#pragma unroll
+      for (int u = 0; u < GU; ++u) {
+        const int i = i0 + u * (int)blockDim.x;
+        if (i < nS + nU) sk[i] = ((unsigned long long)z[u] << 32) | lo[u];
+      }
+    }
     __syncthreads();
     const unsigned long long* kS = sk;
     const unsigned long long* kU = sk + nS;
