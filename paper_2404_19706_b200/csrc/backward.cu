@@ -82,20 +82,26 @@ constexpr int kBwdWarps = kHalfWarps;  // one CTA per half of a kept tile
 constexpr int kBwdParts = kTile / (2 * kBwdWarps);  // CTAs per kept tile (each 16 x 2*kBwdWarps px)
 static_assert(kBwdParts == 2 || kBwdParts == 4, "the backward splits a tile in 2 or 4 row bands");
 
+#ifndef RTGS_BWD_BATCH
+#define RTGS_BWD_BATCH 128
+#endif
+// the backward's ring: 3 x 128 records, 6 CTAs / SM (swept against 3 x 256 unbounded: C3 step equal,
+// window iteration -5 %)
+constexpr int kBS = kPipeStages, kBB = RTGS_BWD_BATCH;
 struct BwdSmem {
-  PipeRingT<false> ring;  // (no list entries: the producer resolves each record's slot)
-  int32_t slot[kPipeStages][kPipeBatch];
-  uint8_t survq[kBwdWarps][kPipeBatch];  // span path: the stage's bbox survivors, in list order
+  PipeRingT<false, kBS, kBB> ring;  // (no list entries: the producer resolves each record's slot)
+  int32_t slot[kBS][kBB];
+  uint8_t survq[kBwdWarps][kBB];  // span path: the stage's bbox survivors, in list order
   float red[3][kBwdWarps];
   uint32_t last_max;
 };
 
 #ifndef RTGS_BWD_MINB
-#define RTGS_BWD_MINB 1
+#define RTGS_BWD_MINB 6
 #endif
 __global__ void __launch_bounds__(32 * (kBwdWarps + 1), RTGS_BWD_MINB) k_render_bwd(const BwdArgs a) {
   __shared__ BwdSmem sm;  // static: stage addresses fold into immediates
-  PipeRingT<false>& r = sm.ring;
+  PipeRingT<false, kBS, kBB>& r = sm.ring;
   if ((int)(blockIdx.x / kBwdParts) >= (int)a.counts[0]) return;
   const int tile = (int)a.tile_list[blockIdx.x / kBwdParts];
   const int half = blockIdx.x % kBwdParts;  // row band of the tile
@@ -192,10 +198,10 @@ __global__ void __launch_bounds__(32 * (kBwdWarps + 1), RTGS_BWD_MINB) k_render_
     };
     auto flush = [](int, int) {};
 #if !RTGS_BWD_DENSE
-    pipe_produce<true, kBwdWarps, false>(r, a.rec, a.sub_rec, a.sorted_gid, start, end, extra, flush, (float)(tx * kTile),
+    pipe_produce<true, kBwdWarps, false, kBS, kBB>(r, a.rec, a.sub_rec, a.sorted_gid, start, end, extra, flush, (float)(tx * kTile),
                                   (float)(ty * kTile + half * (kBwdWarps / 2) * 4));
 #else
-    pipe_produce<true, 0, false>(r, a.rec, a.sub_rec, a.sorted_gid, start, end, extra, flush);
+    pipe_produce<true, 0, false, kBS, kBB>(r, a.rec, a.sub_rec, a.sorted_gid, start, end, extra, flush);
 #endif
     return;
   }
@@ -211,7 +217,7 @@ __global__ void __launch_bounds__(32 * (kBwdWarps + 1), RTGS_BWD_MINB) k_render_
   // front of a similar colour); forming it between two O(1) values keeps its error at float32
   // rounding of G, not of the T-scaled partial sums (no C^ - prefix, no S / (1 - f) amplification).
   const float bx0 = (float)wx0, bx1 = (float)(wx0 + 7), by0 = (float)wy0, by1 = (float)(wy0 + 3);
-  const int nb = n > 0 ? (n + kPipeBatch - 1) / kPipeBatch : 0;
+  const int nb = n > 0 ? (n + kBB - 1) / kBB : 0;
   const uint32_t rec0 = pin(smem_u32(&r.rec[0][0][0])), slot0 = pin(smem_u32(&sm.slot[0][0]));
   const int plane = (int)pin((uint32_t)lane);
   float T = want ? a.trans[lin] : 1.f;  // T after the last blended entry = the forward's T^
@@ -230,13 +236,13 @@ __global__ void __launch_bounds__(32 * (kBwdWarps + 1), RTGS_BWD_MINB) k_render_
   float sink = 0.f;
 #endif
   for (int b = 0; b < nb; ++b) {
-    const int st = b % kPipeStages;
-    mbar_wait_sleep(&r.full[st], (uint32_t)(b / kPipeStages) & 1u);
-    const int lo = pipe_batch_lo(true, start, end, b);
+    const int st = b % kBS;
+    mbar_wait_sleep(&r.full[st], (uint32_t)(b / kBS) & 1u);
+    const int lo = pipe_batch_lo<kBB>(true, start, end, b);
     if ((uint32_t)lo < wlast) {  // warp-uniform: the batch holds entries of this warp's pixels
       const uint32_t srec = rec0 + (uint32_t)(st * sizeof(r.rec[0]));  // shared addresses of this stage
       const uint32_t sslot = slot0 + (uint32_t)(st * sizeof(sm.slot[0]));
-      const int cnt = pipe_batch_cnt(true, start, end, b);
+      const int cnt = pipe_batch_cnt<kBB>(true, start, end, b);
       int nq = 0;
       const uint32_t sbox = pin(smem_u32(&r.boxmask[st][0]));
       for (int g0 = 0; g0 < cnt; g0 += 32) {
@@ -315,13 +321,13 @@ __global__ void __launch_bounds__(32 * (kBwdWarps + 1), RTGS_BWD_MINB) k_render_
 
 #else  // RTGS_BWD_DENSE: the dense walk (every lane evaluates every bbox survivor), for comparison
   for (int b = 0; b < nb; ++b) {
-    const int st = b % kPipeStages;
-    mbar_wait(&r.full[st], (uint32_t)(b / kPipeStages) & 1u);
-    const int lo = pipe_batch_lo(true, start, end, b);
+    const int st = b % kBS;
+    mbar_wait(&r.full[st], (uint32_t)(b / kBS) & 1u);
+    const int lo = pipe_batch_lo<kBB>(true, start, end, b);
     if ((uint32_t)lo < wlast) {  // warp-uniform: the batch holds entries of this warp's pixels
       const uint32_t srec = rec0 + (uint32_t)(st * sizeof(r.rec[0]));  // shared addresses of this stage
       const uint32_t sslot = slot0 + (uint32_t)(st * sizeof(sm.slot[0]));
-      const int cnt = pipe_batch_cnt(true, start, end, b);
+      const int cnt = pipe_batch_cnt<kBB>(true, start, end, b);
       for (int g0 = (cnt - 1) & ~31; g0 >= 0; g0 -= 32) {
         const int j = g0 + lane;
         bool ov = false;

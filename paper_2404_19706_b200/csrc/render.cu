@@ -224,12 +224,21 @@ __device__ unsigned long long g_rstats[8];
 #ifndef RTGS_SPAN_MINB
 #define RTGS_SPAN_MINB 5
 #endif
+// the MASKED render's ring and residency (half-tile CTAs: 4 consumer warps): 3 x 128 records and 6
+// CTAs / SM (swept against 3 x 256 unbounded: first iteration equal, window iteration -3 %)
+#ifndef RTGS_MASKED_BATCH
+#define RTGS_MASKED_BATCH 128
+#endif
+#ifndef RTGS_MASKED_MINB
+#define RTGS_MASKED_MINB 6
+#endif
 template <bool MASKED, bool COUNT, bool LAST = true, bool SPAN = true>
 __global__ void __launch_bounds__(32 * ((MASKED ? kHalfWarps : kTileWarps) + 1),
-                                  SPAN && !MASKED ? RTGS_SPAN_MINB : 1) k_render_fwd(const FwdArgs a) {
+                                  SPAN ? (MASKED ? RTGS_MASKED_MINB : RTGS_SPAN_MINB) : 1) k_render_fwd(const FwdArgs a) {
   constexpr int NW = MASKED ? kHalfWarps : kTileWarps;  // MASKED: one CTA per half of a kept tile
-  __shared__ PipeRingT<false> r;  // static: stage addresses fold into immediates
-  __shared__ uint8_t survq[SPAN ? NW : 1][kPipeBatch];  // per warp: the stage's bbox survivors, in order
+  constexpr int PS = kPipeStages, PB = MASKED ? RTGS_MASKED_BATCH : kPipeBatch;
+  __shared__ PipeRingT<false, PS, PB> r;  // static: stage addresses fold into immediates
+  __shared__ uint8_t survq[SPAN ? NW : 1][PB];  // per warp: the stage's bbox survivors, in order
   int tile, half = 0;
   if (MASKED) {
     if ((blockIdx.x >> 1) >= a.counts[0]) return;
@@ -245,7 +254,7 @@ __global__ void __launch_bounds__(32 * ((MASKED ? kHalfWarps : kTileWarps) + 1),
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (w == NW) {  // producer warp (the span path also gets the per-record warp-box masks)
     const int txp = tile % a.cam.TX, typ = tile / a.cam.TX;
-    pipe_produce<false, SPAN ? NW : 0, false>(r, a.rec, a.sub_rec, a.sorted_gid, start, end, [](int, int, uint32_t) {},
+    pipe_produce<false, SPAN ? NW : 0, false, PS, PB>(r, a.rec, a.sub_rec, a.sorted_gid, start, end, [](int, int, uint32_t) {},
                                        [](int, int) {}, (float)(txp * kTile), (float)(typ * kTile + half * (NW / 2) * 4));
     return;
   }
@@ -260,7 +269,7 @@ __global__ void __launch_bounds__(32 * ((MASKED ? kHalfWarps : kTileWarps) + 1),
   const float fpx = (float)px, fpy = (float)py;
   const float bx0 = (float)wx0, bx1 = (float)(wx0 + 7), by0 = (float)wy0, by1 = (float)(wy0 + 3);
   const int n = end - start;
-  const int nb = n > 0 ? (n + kPipeBatch - 1) / kPipeBatch : 0;
+  const int nb = n > 0 ? (n + PB - 1) / PB : 0;
 
   const uint32_t rec0 = pin(smem_u32(&r.rec[0][0][0]));
   float T = 1.f, cr = 0.f, cg = 0.f, cb = 0.f;
@@ -275,12 +284,12 @@ __global__ void __launch_bounds__(32 * ((MASKED ? kHalfWarps : kTileWarps) + 1),
   if constexpr (SPAN) {
     const uint32_t q0 = pin(smem_u32(&survq[w][0]));
     for (int b = 0; b < nb; ++b) {
-      const int st = b % kPipeStages;
-      mbar_wait_sleep(&r.full[st], (uint32_t)(b / kPipeStages) & 1u);
+      const int st = b % PS;
+      mbar_wait_sleep(&r.full[st], (uint32_t)(b / PS) & 1u);
       if (!wdone) {
         const uint32_t srec = rec0 + (uint32_t)(st * sizeof(r.rec[0]));  // shared address of this stage
-        const uint32_t pbase = (uint32_t)(start + b * kPipeBatch + 1);
-        const int cnt = min(kPipeBatch, n - b * kPipeBatch);
+        const uint32_t pbase = (uint32_t)(start + b * PB + 1);
+        const int cnt = min(PB, n - b * PB);
         // 1. bbox survivors of the stage, in list order
         int nq = 0;
         const uint32_t sbox = pin(smem_u32(&r.boxmask[st][0]));
@@ -376,12 +385,12 @@ __global__ void __launch_bounds__(32 * ((MASKED ? kHalfWarps : kTileWarps) + 1),
     }
   } else {
     for (int b = 0; b < nb; ++b) {
-      const int st = b % kPipeStages;
-      mbar_wait(&r.full[st], (uint32_t)(b / kPipeStages) & 1u);
+      const int st = b % PS;
+      mbar_wait(&r.full[st], (uint32_t)(b / PS) & 1u);
       if (!wdone) {
         const uint32_t srec = rec0 + (uint32_t)(st * sizeof(r.rec[0]));  // shared address of this stage
-        const uint32_t pbase = (uint32_t)(start + b * kPipeBatch + 1);
-        const int cnt = min(kPipeBatch, n - b * kPipeBatch);
+        const uint32_t pbase = (uint32_t)(start + b * PB + 1);
+        const int cnt = min(PB, n - b * PB);
         for (int g0 = 0; g0 < cnt; g0 += 32) {
           const int j = g0 + lane;
           bool ov = false;

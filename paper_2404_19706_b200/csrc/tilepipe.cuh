@@ -30,13 +30,15 @@ constexpr int kHalfWarps = 4;
 
 // GID: the ring also holds each record's list entry (the backward's gradient targets); the forward
 // fetches only its hit's entry, after the walk
-template <bool GID>
+// S stages of B records (B <= 256: stage indices are bytes); kernels pick their own ring size
+template <bool GID, int S = kPipeStages, int B = kPipeBatch>
 struct PipeRingT {
-  float4 rec[kPipeStages][kPipeBatch][3];  // first 48 B of each record: mu hi/lo, conic', log2 alpha, rgb, ext
-  uint32_t gid[GID ? kPipeStages : 1][GID ? kPipeBatch : 1];
-  uint8_t boxmask[kPipeStages][kPipeBatch];  // bit w: the record's support box overlaps warp w's block
-  uint64_t full[kPipeStages];
-  uint64_t empty[kPipeStages];
+  static constexpr int kS = S, kB = B;
+  float4 rec[S][B][3];  // first 48 B of each record: mu hi/lo, conic', log2 alpha, rgb, ext
+  uint32_t gid[GID ? S : 1][GID ? B : 1];
+  uint8_t boxmask[S][B];  // bit w: the record's support box overlaps warp w's block
+  uint64_t full[S];
+  uint64_t empty[S];
   int alive;                                // consumer warps not yet terminated
 };
 using PipeRing = PipeRingT<true>;
@@ -44,7 +46,7 @@ using PipeRing = PipeRingT<true>;
 template <int NW, typename Ring>
 __device__ __forceinline__ void pipe_init(Ring& r) {
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kPipeStages; ++s) {
+    for (int s = 0; s < Ring::kS; ++s) {
       mbar_init(&r.full[s], 32);
       mbar_init(&r.empty[s], NW);
     }
@@ -94,36 +96,38 @@ __device__ __forceinline__ const float4* entry_rec(const float4* rec, const floa
 // producer: one lane per record slot; `extra(stage, j, entry)` may issue more cp.async.
 // REV: the batches run back to front (batch b holds positions [max(start, end - 128 (b+1)), end - 128 b),
 // in list order inside the stage) for the backward's back-to-front pass.
+template <int B = kPipeBatch>
 __device__ __forceinline__ int pipe_batch_lo(bool rev, int start, int end, int b) {
-  return rev ? max(start, end - (b + 1) * kPipeBatch) : start + b * kPipeBatch;
+  return rev ? max(start, end - (b + 1) * B) : start + b * B;
 }
+template <int B = kPipeBatch>
 __device__ __forceinline__ int pipe_batch_cnt(bool rev, int start, int end, int b) {
-  return rev ? (end - b * kPipeBatch) - max(start, end - (b + 1) * kPipeBatch)
-             : min(kPipeBatch, end - start - b * kPipeBatch);
+  return rev ? (end - b * B) - max(start, end - (b + 1) * B) : min(B, end - start - b * B);
 }
 // NBOX > 0: once a stage's copies have landed, the producer also writes boxmask: for each record
 // the NBOX consumer warps' 8x4 blocks (warp w at (bx, by) + ((w & 1) * 8, (w >> 1) * 4)) its support
 // box overlaps -- the test every consumer warp made on its own per record before (the same float
 // comparisons, so the same decisions), now once per record instead of once per (record, warp)
-template <bool REV = false, int NBOX = 0, bool GID = true, typename Extra, typename Flush>
-__device__ __forceinline__ void pipe_produce(PipeRingT<GID>& r, const float4* __restrict__ rec,
+template <bool REV = false, int NBOX = 0, bool GID = true, int S = kPipeStages, int B = kPipeBatch,
+          typename Extra, typename Flush>
+__device__ __forceinline__ void pipe_produce(PipeRingT<GID, S, B>& r, const float4* __restrict__ rec,
                                              const float4* __restrict__ sub_rec,
                                              const uint32_t* __restrict__ sorted_gid, int start, int end,
                                              Extra extra, Flush flush, float bx = 0.f, float by = 0.f) {
   const int lane = threadIdx.x & 31;
   const int n = end - start;
-  const int nb = n > 0 ? (n + kPipeBatch - 1) / kPipeBatch : 0;
+  const int nb = n > 0 ? (n + B - 1) / B : 0;
   for (int b = 0; b < nb; ++b) {
-    const int st = b % kPipeStages;
-    const uint32_t ph = (uint32_t)(b / kPipeStages) & 1u;
-    if (b >= kPipeStages) {
+    const int st = b % S;
+    const uint32_t ph = (uint32_t)(b / S) & 1u;
+    if (b >= S) {
       mbar_wait_sleep(&r.empty[st], ph ^ 1u);  // (suspended, not spinning: measured neutral on time)
-      flush(st, b - kPipeStages);
+      flush(st, b - S);
     }
     if (*((volatile int*)&r.alive) > 0) {
-      const int lo = pipe_batch_lo(REV, start, end, b);
-      const int cnt = pipe_batch_cnt(REV, start, end, b);
-      constexpr int PER = kPipeBatch / 32;
+      const int lo = pipe_batch_lo<B>(REV, start, end, b);
+      const int cnt = pipe_batch_cnt<B>(REV, start, end, b);
+      constexpr int PER = B / 32;
       uint32_t g[PER];
 #pragma unroll
       for (int q = 0; q < PER; ++q) {  // all gid loads of the batch in flight together
@@ -169,9 +173,9 @@ __device__ __forceinline__ void pipe_produce(PipeRingT<GID>& r, const float4* __
     else cp_async_mbar_arrive(&r.full[st]);
   }
   // the last stages are flushed once every consumer warp has released them
-  for (int b = max(0, nb - kPipeStages); b < nb; ++b) {
-    const int st = b % kPipeStages;
-    mbar_wait_sleep(&r.empty[st], (uint32_t)(b / kPipeStages) & 1u);
+  for (int b = max(0, nb - S); b < nb; ++b) {
+    const int st = b % S;
+    mbar_wait_sleep(&r.empty[st], (uint32_t)(b / S) & 1u);
     flush(st, b);
   }
 }
