@@ -1144,21 +1144,40 @@ def run_batch(args, rank, world, local):
         c, d = make_frame(cfg, (R, t))
         host.append((torch.as_tensor(np.clip(np.rint(np.moveaxis(c, 0, -1) * 255), 0, 255).astype(np.uint8)).pin_memory(),
                      torch.as_tensor(np.clip(np.rint(d * DEPTH_SCALE), 0, 65535).astype(np.uint16).view(np.int16)).pin_memory()))
-    st_c = torch.empty_like(host[0][0], device="cuda")
-    st_d = torch.empty_like(host[0][1], device="cuda")
+    # streamed: the H2D copies of step i+1's views (copy stream, double-buffered sensor-native staging)
+    # overlap step i; step i+1 decodes its staging into the views' buffers once step i is done with them
+    stage = [[(torch.empty_like(hc, device="cuda"), torch.empty_like(hd, device="cuda")) for hc, hd in host]
+             for _ in range(2)]
+    copy_stream = torch.cuda.Stream()
+    ev_copied = [torch.cuda.Event() for _ in range(2)]
+    ev_free = [torch.cuda.Event() for _ in range(2)]
     loss_h = torch.empty(4, dtype=torch.float32).pin_memory()
-    n_e2e = max(3, args.steps // 4)
+    n_e2e = max(3, args.steps // 4)  # (the first step's copies are not overlapped)
     restore()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record(stream)
-    for _ in range(n_e2e):
-        for (hc, hd), v in zip(host, mine):
-            st_c.copy_(hc, non_blocking=True)
-            st_d.copy_(hd, non_blocking=True)
-            P.decode_rgbd(st_c, st_d, DEPTH_SCALE, views[v][0], views[v][1])
+    copy_stream.wait_stream(stream)
+
+    def h2d(i):
+        with torch.cuda.stream(copy_stream):
+            if i >= 2:
+                copy_stream.wait_event(ev_free[i % 2])
+            for (hc, hd), (sc, sd) in zip(host, stage[i % 2]):
+                sc.copy_(hc, non_blocking=True)
+                sd.copy_(hd, non_blocking=True)
+            ev_copied[i % 2].record(copy_stream)
+
+    h2d(0)
+    for i in range(n_e2e):
+        if i + 1 < n_e2e:
+            h2d(i + 1)
+        stream.wait_event(ev_copied[i % 2])
+        for (sc, sd), v in zip(stage[i % 2], mine):
+            P.decode_rgbd(sc, sd, DEPTH_SCALE, views[v][0], views[v][1])
+        ev_free[i % 2].record(stream)
         step()
         loss_h.copy_(eng.g_loss, non_blocking=True)
     b.record(stream)
