@@ -15,3 +15,7 @@ if timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 
      -o gpurun_out/r2m_prof python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-window > gpurun_out/r2m_ncu_full.log 2>&1
   echo "ncu full rc=$?"
 fi
+# the realistic window iteration (after insertions: every tile kept), kernel list of 3 iterations
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv \
+   --log-file gpurun_out/r2m_window_launches.csv python scripts/diag_window_iter.py > gpurun_out/r2m_window.log 2>&1
+echo "window rc=$?"
