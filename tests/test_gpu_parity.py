@@ -136,6 +136,41 @@ def test_bin_and_sort_bitexact_sort_paths(api, n, w, h, levels, jitter):
     np.testing.assert_array_equal(bins.tile_range.cpu().numpy(), rng)
 
 
+@pytest.mark.parametrize("keep_frac", [None, 0.6])
+def test_bin_and_sort_bitexact_large_rects(api, keep_frac):
+    """Rects of up to 40 x 30 tiles mixed with small ones: warps whose largest rect covers more than 4
+    tiles deal their instances out 32 per round (warp_expand_tiles) in the count and the emission;
+    the order must still be the oracle's (tile, depth, gid) order."""
+    n, w, h = 4000, 640, 480
+    cam = api.make_camera(100, 100, w / 2, h / 2, w, h)
+    tx, ty = (w + 15) // 16, (h + 15) // 16
+    proj, z, tile_rect = _synthetic_projected(api, n, tx, ty, 21, tuple(np.linspace(0.5, 6.0, 97)), 7)
+    rng = np.random.default_rng(5)
+    big = rng.uniform(size=n) < 0.08
+    rect = proj.rect.cpu().numpy().astype(np.int64)
+    x0, y0 = rng.integers(0, w - 1, n), rng.integers(0, h - 1, n)
+    x1 = np.minimum(x0 + rng.integers(16, 640, n), w - 1)
+    y1 = np.minimum(y0 + rng.integers(16, 480, n), h - 1)
+    vis = rect[:, 0] <= rect[:, 2]
+    sel = big & vis
+    rect[sel] = np.stack([x0, y0, x1, y1], 1)[sel]
+    proj.rect.copy_(torch.as_tensor(rect.astype(np.int16)))
+    tile_rect = np.where(vis[:, None], rect // 16, np.array([1, 1, 0, 0]))
+    keep = (np.random.default_rng(3).uniform(size=tx * ty) < keep_frac) if keep_frac is not None else None
+    ktens = torch.as_tensor(keep.astype(np.uint8), device="cuda") if keep is not None else None
+    cap = 1 << 21
+    bins = api.BinBuffers(cam, cap)
+    from paper_2404_19706_b200 import mapping as M
+    ws = torch.empty(M.bin_workspace_size(n, cam, cap), dtype=torch.uint8, device="cuda")
+    api.bin_and_sort(proj, n, cam, ktens, bins, ws)
+    torch.cuda.synchronize()
+    tid, gid, rng_o = OB.instances_fast(z, tile_rect, tx, ty, keep)
+    I = int(bins.n_instances.item())
+    assert I == len(gid) and sel.sum() > 100
+    np.testing.assert_array_equal(bins.sorted_gid[:I].cpu().numpy(), gid)
+    np.testing.assert_array_equal(bins.tile_range.cpu().numpy(), rng_o)
+
+
 def test_bin_overflow_reports_count(api):
     w, h, n = 200, 136, 3000
     cam = api.make_camera(100, 100, w / 2, h / 2, w, h)
