@@ -10,7 +10,7 @@ import sys
 WANT = {  # bench key -> kernel name prefix in the report (first launch that matches)
     "C3": {"k_render_fwd<FULL>": "void k_render_fwd<0, 0, 0, 1>", "k_project": "void k_project<16, 0>",
            "k_render_bwd": "k_render_bwd", "k_project_bwd<ADAM>": "void k_project_bwd<16, 1>"},
-    "C4": {"k_render_fwd<FULL>": "void k_render_fwd<0, 0, 0, 1>", "k_project": "void k_project<16, 1>"},
+    "C4": {"k_render_fwd<FULL>": "void k_render_fwd<0, 0, 0, 1>", "k_project": "void k_project<16, 0>"},
 }
 
 
