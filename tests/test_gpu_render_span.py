@@ -141,3 +141,37 @@ def test_forward_and_binning_deterministic(api, name):
     assert ni == int(bb.n_instances.item())
     assert torch.equal(ba.tile_range, bb.tile_range)
     assert torch.equal(ba.sorted_gid[:ni], bb.sorted_gid[:ni])
+
+
+@pytest.mark.parametrize("seed,n", [(4, 6000), (5, 40000)])
+def test_tile_coverage_span_equals_splat_adversarial(api, seed, n):
+    """A0 two ways on the adversarial shapes: the tile-list coverage (k_tile_coverage: span masks over
+    16x2 pixels, exact tests only where a mask bit is set) against the splat coverage (k_coverage:
+    the exact test on every support pixel, no masks).  Active bits, tile keep, kept list and counts
+    bitwise -- so the 16x2 masks are supersets on needles, razor discs, blades and edge-on splats."""
+    from paper_2404_19706_b200 import mapping as M
+    W, H, f = 333, 219, 290.0
+    scene = _adversarial(seed, n, W, H, f)
+    rng = np.random.default_rng(seed)
+    unstable = rng.uniform(size=n) < 0.35
+    scene["flags"] = (scene["flags"] | np.where(unstable, 0, M.FLAG_STABLE)).astype(np.uint8)
+    cam = api.make_camera(f, f, (W - 1) / 2, (H - 1) / 2, W, H)
+    pose = api.make_pose(np.eye(3), np.zeros(3))
+    gm = api.GaussianMap.from_arrays(scene)
+    proj = M.ProjectedBuffers(n)
+    api.project_gaussians(gm, pose, cam, proj)
+    a = M.RenderBuffers(cam)
+    api.render_color_depth(gm, proj, None, pose, cam, api.RTGS_RENDER_COVERAGE, a)
+    gids = torch.as_tensor(np.nonzero(unstable)[0].astype(np.int32), device="cuda")
+    sub = M.ProjectedBuffers(int(gids.numel()))
+    M.project_subset(gm, gids, pose, cam, sub)
+    b = M.RenderBuffers(cam)
+    cap = 200 * n
+    ws = torch.empty(M.bin_cached_workspace_size(int(gids.numel()), cam, cap), dtype=torch.uint8, device="cuda")
+    M.coverage_subset(sub, int(gids.numel()), cam, b, cap, ws)
+    torch.cuda.synchronize()
+    assert torch.equal(a.active_bits, b.active_bits)
+    assert torch.equal(a.tile_keep, b.tile_keep)
+    assert torch.equal(a.counts[:3], b.counts[:3]) and int(a.counts[2].item()) > 0
+    k = int(a.counts[0].item())
+    assert torch.equal(torch.sort(a.tile_list[:k]).values, torch.sort(b.tile_list[:k]).values)
