@@ -366,19 +366,22 @@ __device__ __forceinline__ void cta_radix_sort(unsigned long long* A, unsigned l
 // pass distributes them over kBuckets buckets by the top bits of (zkey - zmin): each key takes its
 // rank inside its bucket from a shared-memory atomic (an arbitrary order -- MSD needs no stability),
 // and after a scan of the bucket counts lands at start[bucket] + rank.  Then every key moves to its
-// bucket's start + the number of smaller keys in its bucket (a tile of ~700 keys spreads ~0.35 keys
+// bucket's start + the number of smaller keys in its bucket (a tile of ~700 keys spreads ~0.7 keys
 // per bucket; crowded buckets are ranked by as many threads as they hold keys).  So the result is
 // the same unique order as the LSD path, for a fraction of its instructions.  Returns false (nothing
 // written) when some bucket holds more than kMaxBucket keys (depths piled up in one bucket range):
 // the caller then runs the LSD sort.
-constexpr int kBuckets = 2048;
+#ifndef RTGS_MSD_BITS
+#define RTGS_MSD_BITS 10  // (swept 9 / 10 / 11: 10)
+#endif
+constexpr int kBuckets = 1 << RTGS_MSD_BITS;
 constexpr int kBPT = kBuckets / kSortThreads;  // buckets per thread
 constexpr int kMaxBucket = 96;
 static_assert(kBuckets * 4 <= kSortWarps * 256 * 4, "the bucket counters reuse wcnt");
 __device__ __forceinline__ bool msd_bucket_sort(unsigned long long* A, unsigned long long* B, uint32_t* rk, int n,
                                                 uint32_t z0, int zbits, uint32_t* cnt, uint32_t* scan_sh) {
   const int tid = threadIdx.x;
-  const int sh = max(0, zbits - 11);  // top 11 bits of the depth range (kBuckets = 2^11)
+  const int sh = max(0, zbits - RTGS_MSD_BITS);  // the top bits of the depth range (kBuckets of them)
 #pragma unroll
   for (int j = 0; j < kBPT; ++j) cnt[tid * kBPT + j] = 0u;
   __syncthreads();
