@@ -1015,7 +1015,19 @@ def run_render_only(args, rank, world, local):
         torch.cuda.synchronize()
         rt.append(e0.elapsed_time(e1))
     t_render = statistics.mean(rt)
+    # A1 alone (the plain projection), for its HBM roofline
+    pt = []
+    for _ in range(10):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        P.project_gaussians(gm, poses[0], cam, proj)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        pt.append(e0.elapsed_time(e1))
+    t_proj = statistics.mean(pt)
     rb.count_blends = True
+    P.project_and_bin(gm, poses[0], cam, proj, bins, ws)
     P.render_color_depth(gm, proj, bins, poses[0], cam, P.RTGS_RENDER_FULL, rb)
     torch.cuda.synchronize()
     blends = int(rb.counts[3].item())
@@ -1054,6 +1066,15 @@ def run_render_only(args, rank, world, local):
     torch.cuda.synchronize()
     t_e2e = a.elapsed_time(b) / n_e2e
     if rank == 0:
+        hbm, _, peak_kind = _peaks()
+        K = (cfg.sh_degree + 1) ** 2
+        a1_bytes = 12 + 12 + 16 + 4 + 12 * K + 64 + 4 + 8 + 4  # as the C3 line
+        a1_gbs = a1_bytes * cfg.n / (t_proj * 1e-3) / 1e9
+        traffic = {}
+        tp = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tp):
+            with open(tp) as f:
+                traffic = json.load(f).get("C4", {})
         line = {"metric": METRIC, "value": world * 1e3 / t_step, "unit": "frames/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
@@ -1063,7 +1084,15 @@ def run_render_only(args, rank, world, local):
                            "l2": "flushed between timed steps (256 MB write); Gaussian SoA 948 MB > L2",
                            "launch": "CUDA graph per pose", "parallelism": "single GPU" if world == 1 else
                            f"{world} replicas"},
-                "roofline": _alu_roofline(blends, t_render, clocks, "k_render_fwd<FULL> (A3/A4, dominant kernel)"),
+                "roofline": dict(_alu_roofline(blends, t_render, clocks, "k_render_fwd<FULL> (A3/A4, dominant kernel)"),
+                                 traffic=traffic.get("k_render_fwd<FULL>")),
+                "roofline_secondary": [{"kernel": "k_project (A1)", "bound": "hbm", "achieved": a1_gbs, "peak": hbm,
+                                        "unit": "GB/s", "frac": a1_gbs / hbm, "peak_kind": peak_kind,
+                                        "traffic": traffic.get("k_project"), "bytes_per_gaussian": a1_bytes,
+                                        "time_ms": t_proj,
+                                        # 76 % reads: above the measured copy (half reads), so also against
+                                        # the nominal 7.7 TB/s (B200_PROFILING.md)
+                                        "peak_nominal": 7700.0, "frac_nominal": a1_gbs / 7700.0}],
                 "blends": {"full_per_frame": blends, "full_blends_per_s": blends / (t_render * 1e-3)},
                 "clocks": clocks, "gpu_launches": int(per_frame * args.steps),
                 "e2e": {"value": world * 1e3 / t_e2e, "unit": "frames/s", "h2d_bytes_per_step": 0,
