@@ -265,9 +265,13 @@ __global__ void __launch_bounds__(32 * (kBwdWarps + 1), RTGS_BWD_MINB) k_render_
         const int trips = __reduce_max_sync(0xffffffffu, (uint32_t)__popc(lm));
         for (int it = 0; it < trips; ++it) {
           const bool has = lm != 0u;
-          const int jj = has ? 31 - __clz(lm) : 0;  // back to front
-          lm &= has ? ~(1u << jj) : 0xFFFFFFFFu;
-          const uint32_t idx = lds8(q0 + (uint32_t)(q + jj));
+          // back to front: the highest set bit (bfind; 0xFFFFFFFF without bits: such a lane reads
+          // survivor q, a queued record of this stage, and the pair is discarded)
+          uint32_t b, top;
+          asm("bfind.u32 %0, %1;" : "=r"(b) : "r"(lm));
+          asm("shl.b32 %0, %1, %2;" : "=r"(top) : "r"(1u), "r"(b));  // 0 for b = 0xFFFFFFFF (clamped)
+          lm &= ~top;
+          const uint32_t idx = lds8(q0 + (uint32_t)q + (has ? b : 0u));
           const uint32_t ra = srec + 48u * idx;
           const float4 r0 = lds128(ra), r1 = lds128(ra + 16u), r2 = lds128(ra + 32u);
           PairEval e;
