@@ -198,7 +198,7 @@ cudaError_t launch_tile_coverage(const uint2* srange, const unsigned long long* 
 // ------------------------------------------------------------------------------------------------
 // Span-mask path (round 2).  Per 8x4 warp block the dense path evaluated every surviving (record, block)
 // pair on all 32 lanes although ~5 lanes blend (sub-pixel splats): 45 instructions x 32 lanes per
-// survivor.  Instead, per batch of bbox survivors:
+// survivor.  Instead, per batch of bbox survivors (rounds of up to 64; the steps below for one word):
 //   1. lane l takes survivor l and computes the exact 32-bit pixel mask of its support over the block
 //      (support_mask: per pixel row, the x interval where p2 >= max(p2_min, log2(1/255) - log2 alpha),
 //      a quadratic in dx, enlarged by a safety margin so it is a SUPERSET of the pixels that pass
