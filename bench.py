@@ -641,6 +641,18 @@ def run_mapping(args, rank, world, local):
             torch.cuda.synchronize()
             rt.append(e0.elapsed_time(e1))
         phases["render_full_alone_ms"] = statistics.mean(rt)
+        # A2 alone (count, offsets, emission, tile sort of the full map; same lists as the ingest's)
+        bt = []
+        for _ in range(reps):
+            flush.zero_()
+            hold(0.5)
+            e0.record(stream)
+            P.bin_and_sort(eng.proj_full, gm.n, cam, None, eng.bins_full, eng.ws_bin_full)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            bt.append(e0.elapsed_time(e1))
+        phases["bin_alone_ms"] = statistics.mean(bt)
+        phases["bin_instances"] = int(eng.bins_full.n_instances.item())
         # NEXT f1 (once per window, not part of the step): Eq.9 fusion and the state transitions
         from paper_2404_19706_b200 import mapping as M
         hold(0.5)
@@ -884,7 +896,9 @@ def run_mapping(args, rank, world, local):
                  "frac": traffic["k_render_fwd<FULL>_warp_inst"] / t_render_s / (4 * 148 * clk_ghz * 1e9),
                  "peak_kind": "derived: 4 issue slots / clock / SM x 148 SM x sampled SM clock",
                  "algorithmic": "warp instructions executed per launch (ncu smsp__inst_executed.sum, profiles/traffic.json)",
-                 "time_ms": phases["render_full_alone_ms"]}] if "k_render_fwd<FULL>_warp_inst" in traffic else []),
+                 "time_ms": phases["render_full_alone_ms"]}] if "k_render_fwd<FULL>_warp_inst" in traffic else [])
+            + ([_a2_roofline(cfg, phases["bin_instances"], phases["bin_alone_ms"], hbm, peak_kind)]
+               if "bin_alone_ms" in phases else []),
             "blends": {"full_per_frame": blends_full, "masked_per_iter": blends_masked,
                        "full_blends_per_s": blends_full / t_render_s},
             "clocks": clocks,
@@ -946,6 +960,19 @@ def _timed(run_step, between, steps, world, local, stream):
         t = float(tt.item())
         dist.barrier()
     return t, clk.summary()
+
+
+def _a2_roofline(cfg, instances, t_ms, hbm, peak_kind):
+    """A2 (count, offsets, emission, tile sort) against HBM with SURVEY 8(d.3)'s compulsory bytes:
+    16 B per Gaussian + 4 B per instance + 8 B per tile (all Gaussians counted as visible: an upper
+    bound on the compulsory bytes, so a lower bound on nothing)."""
+    T = ((cfg.width + 15) // 16) * ((cfg.height + 15) // 16)
+    byts = 16 * cfg.n + 4 * instances + 8 * T
+    ach = byts / (t_ms * 1e-3) / 1e9
+    return {"kernel": "A2 bin_and_sort (k_tile_count, k_tile_offsets, k_emit, k_tile_sort)", "bound": "hbm",
+            "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "peak_kind": peak_kind,
+            "algorithmic": f"16 B x {cfg.n} Gaussians + 4 B x {instances} instances + 8 B x {T} tiles",
+            "time_ms": t_ms, "keys_per_s": instances / (t_ms * 1e-3)}
 
 
 def _alu_roofline(blends, t_ms, clocks, what):
@@ -1026,6 +1053,18 @@ def run_render_only(args, rank, world, local):
         torch.cuda.synchronize()
         pt.append(e0.elapsed_time(e1))
     t_proj = statistics.mean(pt)
+    P.project_gaussians(gm, poses[0], cam, proj)
+    bt = []
+    for _ in range(10):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        P.bin_and_sort(proj, n, cam, None, bins, ws)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        bt.append(e0.elapsed_time(e1))
+    t_bin = statistics.mean(bt)
+    bin_inst = int(bins.n_instances.item())
     rb.count_blends = True
     P.project_and_bin(gm, poses[0], cam, proj, bins, ws)
     P.render_color_depth(gm, proj, bins, poses[0], cam, P.RTGS_RENDER_FULL, rb)
@@ -1092,7 +1131,8 @@ def run_render_only(args, rank, world, local):
                                         "time_ms": t_proj,
                                         # 76 % reads: above the measured copy (half reads), so also against
                                         # the nominal 7.7 TB/s (B200_PROFILING.md)
-                                        "peak_nominal": 7700.0, "frac_nominal": a1_gbs / 7700.0}],
+                                        "peak_nominal": 7700.0, "frac_nominal": a1_gbs / 7700.0},
+                                       _a2_roofline(cfg, bin_inst, t_bin, hbm, peak_kind)],
                 "blends": {"full_per_frame": blends, "full_blends_per_s": blends / (t_render * 1e-3)},
                 "clocks": clocks, "gpu_launches": int(per_frame * args.steps),
                 "e2e": {"value": world * 1e3 / t_e2e, "unit": "frames/s", "h2d_bytes_per_step": 0,
