@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(32 * ((MASKED ? kHalfWarps : kTileWarps) + 1),
   if (w == NW) {  // producer warp (the span path also gets the per-record warp-box masks)
     const int txp = tile % a.cam.TX, typ = tile / a.cam.TX;
     pipe_produce<false, SPAN ? NW : 0, false, PS, PB>(r, a.rec, a.sub_rec, a.sorted_gid, start, end, [](int, int, uint32_t) {},
-                                       [](int, int) {}, (float)(txp * kTile), (float)(typ * kTile + half * (NW / 2) * 4));
+                                       NoFlush{}, (float)(txp * kTile), (float)(typ * kTile + half * (NW / 2) * 4));
     return;
   }
   const int tx = tile % a.cam.TX, ty = tile / a.cam.TX;

@@ -11,6 +11,7 @@
 // producer stops copying and only signals, and the CTA drains.
 #pragma once
 #include "common.cuh"
+#include <type_traits>
 
 namespace rtgs {
 
@@ -93,6 +94,11 @@ __device__ __forceinline__ const float4* entry_rec(const float4* rec, const floa
   return (e & kSubBit) ? sub_rec + (size_t)4 * (e & ~kSubBit) : rec + (size_t)4 * e;
 }
 
+// the flush of a producer whose stages need no per-stage epilogue (the forward render)
+struct NoFlush {
+  __device__ void operator()(int, int) const {}
+};
+
 // producer: one lane per record slot; `extra(stage, j, entry)` may issue more cp.async.
 // REV: the batches run back to front (batch b holds positions [max(start, end - 128 (b+1)), end - 128 b),
 // in list order inside the stage) for the backward's back-to-front pass.
@@ -172,7 +178,9 @@ __device__ __forceinline__ void pipe_produce(PipeRingT<GID, S, B>& r, const floa
     if constexpr (NBOX > 0) mbar_arrive(&r.full[st]);  // (copies waited for: a plain arrival)
     else cp_async_mbar_arrive(&r.full[st]);
   }
-  // the last stages are flushed once every consumer warp has released them
+  // the last stages are flushed once every consumer warp has released them (a producer without a
+  // flush has nothing left to do: it exits, and the ring lives on with the CTA)
+  if constexpr (std::is_same_v<Flush, NoFlush>) return;
   for (int b = max(0, nb - S); b < nb; ++b) {
     const int st = b % S;
     mbar_wait_sleep(&r.empty[st], (uint32_t)(b / S) & 1u);
