@@ -25,7 +25,7 @@
 namespace rtgs {
 
 constexpr int kSG = 16;  // screen-space gradient floats per slot
-constexpr int kDirectLanes = 4;  // <= this many contributing lanes: per-lane vector atomics
+[[maybe_unused]] constexpr int kDirectLanes = 4;  // (dense walk) <= this many contributing lanes: per-lane vector atomics
 
 // Transpose-reduce of 8 values over a warp in 9 shuffles (instead of 8 x 5): after the call, lane l
 // holds the warp sum of value j = 4*bit4(l) + 2*bit3(l) + bit2(l), identical on the 4 lanes l^{0..3}.
@@ -216,7 +216,8 @@ __global__ void __launch_bounds__(32 * (kBwdWarps + 1), RTGS_BWD_MINB) k_render_
   // since S_i = T_{i+1} B_i.  The difference G_i - B_i is the pixel's own cancellation (a Gaussian in
   // front of a similar colour); forming it between two O(1) values keeps its error at float32
   // rounding of G, not of the T-scaled partial sums (no C^ - prefix, no S / (1 - f) amplification).
-  const float bx0 = (float)wx0, bx1 = (float)(wx0 + 7), by0 = (float)wy0, by1 = (float)(wy0 + 3);
+  const float bx0 = (float)wx0, by0 = (float)wy0;
+  [[maybe_unused]] const float bx1 = (float)(wx0 + 7), by1 = (float)(wy0 + 3);  // (dense walk's box test)
   const int nb = n > 0 ? (n + kBB - 1) / kBB : 0;
   const uint32_t rec0 = pin(smem_u32(&r.rec[0][0][0])), slot0 = pin(smem_u32(&sm.slot[0][0]));
   const int plane = (int)pin((uint32_t)lane);

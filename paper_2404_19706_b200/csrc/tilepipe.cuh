@@ -180,11 +180,12 @@ __device__ __forceinline__ void pipe_produce(PipeRingT<GID, S, B>& r, const floa
   }
   // the last stages are flushed once every consumer warp has released them (a producer without a
   // flush has nothing left to do: it exits, and the ring lives on with the CTA)
-  if constexpr (std::is_same_v<Flush, NoFlush>) return;
-  for (int b = max(0, nb - S); b < nb; ++b) {
-    const int st = b % S;
-    mbar_wait_sleep(&r.empty[st], (uint32_t)(b / S) & 1u);
-    flush(st, b);
+  if constexpr (!std::is_same_v<Flush, NoFlush>) {
+    for (int b = max(0, nb - S); b < nb; ++b) {
+      const int st = b % S;
+      mbar_wait_sleep(&r.empty[st], (uint32_t)(b / S) & 1u);
+      flush(st, b);
+    }
   }
 }
 
