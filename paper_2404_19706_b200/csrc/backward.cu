@@ -713,9 +713,12 @@ __device__ __forceinline__ float sh_grad(const float* row, int j) {
 // 104k slots in one wave, so the C3 iteration's 100k unstable slots do not pay a second wave of CTA
 // latency; -Xptxas -v: 12-28 B of spills at K = 9 / 16), 16 for degrees 0-1 (the 80-register cap
 // spilled ~100 B there; with 128 registers none).  RTGS_BWD_F64: 12.
+#ifndef RTGS_PB_MINB
+#define RTGS_PB_MINB 22  // (swept round 2 at C3: 18 / 20 -> 62 us: a second wave; 25 -> 50 us: spills; 22 -> 48 us)
+#endif
 template <int K>
 struct PBMinBlocks {
-  static constexpr int value = RTGS_BWD_F64 ? 12 : (K >= 9 ? 22 : 16);
+  static constexpr int value = RTGS_BWD_F64 ? 12 : (K >= 9 ? RTGS_PB_MINB : 16);
 };
 template <int K, bool ADAM>
 __global__ void __launch_bounds__(kPBS, PBMinBlocks<K>::value) k_project_bwd(const PBArgs a) {
